@@ -1,0 +1,142 @@
+/*
+ * tpde_b200.h -- C ABI of the B200 (sm_100a) rank-truncation hot path.
+ *
+ * Drop-in boundary for the reference package `tensorpde` (pure Python,
+ * /root/reference/pkg/src/tensorpde).  The reference has no FFI; its boundary
+ * is the Python API.  Each entry point below replaces the
+ * compute behind one reference function; the Python package
+ * `paper_1803_10270_b200` binds them through ctypes with the same names,
+ * argument meaning and exceptions as the reference.
+ *
+ * Conventions
+ *  - All tensors are real fp64 in DEVICE memory, caller-owned.
+ *  - A d-mode CP tensor of rank R is ONE buffer: mode k is the row-major
+ *    (Q_k x R) block at element offset R * sum_{k'<k} Q_k'.  Slice k is
+ *    exactly the reference's `factors[k]` array (cp.py:43-59).
+ *  - `q` arguments are HOST arrays of d mode sizes.
+ *  - `stream` is a cudaStream_t passed as void* (no CUDA types in the ABI).
+ *  - Scratch comes from a caller-provided device workspace; query its size
+ *    with the matching *_ws_bytes function.  The library never allocates.
+ *  - Every call returns a status (TP_OK == 0).  Calls are stream-ordered and
+ *    re-entrant per stream; results are bitwise deterministic for a fixed
+ *    launch configuration.
+ */
+#ifndef TPDE_B200_H
+#define TPDE_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum tp_status {
+  TP_OK = 0,
+  TP_EINVAL = 1,        /* -> ValueError */
+  TP_ENONFINITE = 2,    /* -> ConditioningError / StepFailure (cp.py:178-179, implicit.py:162-163) */
+  TP_ENOTPD = 3,        /* Cholesky pivot <= 0 -> ConditioningError */
+  TP_ECUDA = 4,         /* -> RuntimeError */
+  TP_EWORKSPACE = 5,    /* workspace too small -> RuntimeError */
+  TP_EUNSUPPORTED = 6   /* size outside the compiled kernel limits -> ValueError */
+};
+
+const char* tp_version(void);
+const char* tp_status_string(int status);
+/* last CUDA error string seen by the library on this thread (for TP_ECUDA) */
+const char* tp_last_error(void);
+/* number of SMs of the current device, 0 if none */
+int tp_device_sms(void);
+
+/* ---------------------------------------------------------------------------
+ * Inner product of two CP tensors.
+ * Replaces cp.inner_product / cp.norm (cp.py:111-126) and the target
+ * self-norm of _CPTarget (cp.py:186-188):
+ *     out = sum_{l<ra, m<rb} prod_k (A_k^T B_k)[l, m]
+ * `same` != 0 declares A == B (same buffer): only upper tiles are computed.
+ * `out` is a device scalar.
+ * ------------------------------------------------------------------------- */
+size_t tp_cp_inner_ws_bytes(int d, const int* q, int ra, int rb);
+int tp_cp_inner_f64(int d, const int* q, int ra, const double* A, int rb, const double* B,
+                    int same, double* out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Fixed-target Gauss-Seidel CP-ALS (cp.cp_approx_als, cp.py:266-334, with
+ * _CPTarget cp.py:183-209 and _solve_gram cp.py:169-180).
+ *   V      : target, rank R (device, CP layout)
+ *   U      : rank-r guess: initial guess on entry, fit on exit (device, CP layout)
+ *   reg    : lambda.  reg_mode 0: fixed lambda = reg.
+ *            reg_mode 1: reference rule lambda = reg * max(tr(H),0)/r (cp.py:172)
+ *   tol, stall : reference stopping rules (cp.py:329-332); stall = -inf and
+ *            tol = 0 run exactly `sweeps` sweeps.
+ *   trace  : device array of >= sweeps doubles receiving the residual after
+ *            each sweep (cp.py:321-328), or NULL.
+ *   info   : device int[2]: {status, sweeps_done}.
+ *   grid   : CTAs of the persistent kernel (0 = library choice).
+ * The target norm ||V||^2 (needed only when trace != NULL or a stopping rule
+ * is active) is computed inside the call.
+ * ------------------------------------------------------------------------- */
+size_t tp_cp_als_ws_bytes(int d, const int* q, int R, int r, int grid);
+int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
+                  int sweeps, double reg, int reg_mode, double tol, double stall,
+                  double* trace, int* info, int grid, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Separable operator apply + concatenation (operators.apply,
+ * operators.py:48-62; cp.add/scale, cp.py:98-108).
+ * For each term t (0..n_terms-1) and mode k, writes
+ *     out_k[:, col_off + t*r_in : col_off + (t+1)*r_in] =
+ *         (k == 0 ? scale * weights[t] : 1) * E_{t,k} @ F_k
+ * where E_{t,k} is the identity when mat_idx[t*d + k] < 0, else the dense
+ * row-major (Q_k x Q_k) matrix at element offset mat_off[mat_idx[t*d+k]] of
+ * `mats` (device).  F has rank r_in, out has rank R_out.  Host arrays:
+ * q, weights, mat_idx, mat_off.  Terms are written term-major like the
+ * reference.
+ * ------------------------------------------------------------------------- */
+int tp_cp_apply_f64(int d, const int* q, int r_in, const double* F, int n_terms,
+                    const double* weights, double scale, const int* mat_idx,
+                    const double* mats, const long long* mat_off, int n_mats,
+                    double* out, int R_out, int col_off, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Batched hierarchical-Tucker truncation by hSVD (ht.truncate, ht.py:313-372,
+ * with ht.orthogonalize ht.py:294-310) on a balanced binary dimension tree
+ * (ht.balanced_tree, ht.py:79-98) with uniform leaf size Q and uniform input
+ * rank k at every non-root node.  Batch of `nb` independent tensors.
+ *   frames    : device, nb x n_leaves x (Q x k) row-major, leaves in tree preorder
+ *   transfers : device, nb x n_interior x (k x k x k) (root: k x k x 1 stored in a
+ *               k*k*k slot, only the first k*k entries used), interior nodes in
+ *               tree preorder, B[a][b][i] row-major.
+ *   Outputs (same layouts with rank r_out = min(r_max, k)):
+ *   out_frames nb x n_leaves x (Q x r_out), out_transfers nb x n_interior x
+ *   (r_out^3), out_ranks nb x n_nodes ints (kept rank per node),
+ *   est nb doubles (sqrt of discarded eigenvalue mass, ht.py:371-372),
+ *   norms nb doubles (||h||, ht.py:279-282).
+ * eps is the relative tolerance; budget (eps*||h||)^2/(2d-3) per node.
+ * ------------------------------------------------------------------------- */
+size_t tp_ht_truncate_ws_bytes(int d, int Q, int k, int nb);
+int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const double* transfers,
+                       int r_max, double eps, double* out_frames, double* out_transfers,
+                       int* out_ranks, double* est, double* norms,
+                       void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Fixed-rank implicit ALS step (implicit.step, implicit.py:222-301) for a
+ * pair A = sum_e eta_e (x)_k A_{e,k}, B = sum_z zeta_z (x)_k A_{z,k} with
+ * shared dense factors; Gauss-Seidel schedule, direct regularised solve
+ * (M_q + lam I) x = gamma_q by blocked Cholesky.
+ *   pairs : device, d x ra x ra x (Q x Q): pairs[k][e][z] = A_{e,k}^T A_{z,k}
+ *   f_old : device CP (rank r), f_new: device CP in/out (initial iterate = f_old)
+ *   orientation: 0 = corrected normal equations, 1 = reference build_gamma
+ *                (implicit.py:137-139)
+ * ------------------------------------------------------------------------- */
+size_t tp_implicit_ws_bytes(int d, int Q, int r, int ra);
+int tp_implicit_step_f64(int d, int Q, int r, int ra, const double* pairs, const double* eta,
+                         const double* zeta, const double* f_old, double* f_new,
+                         int sweeps, double delta_beta, double lam, int orientation,
+                         double* eps_conv, int* info, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TPDE_B200_H */

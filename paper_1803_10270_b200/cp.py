@@ -1,0 +1,328 @@
+"""Canonical (CP) tensors on the device and alternating least squares.
+
+Drop-in mirror of the reference ``tensorpde/cp.py``.  A rank-``R`` tensor over
+``d`` specs is ONE contiguous fp64 device buffer; mode ``k`` is the row-major
+``(Q_k, R)`` block at element offset ``R * sum_{k'<k} Q_k'`` -- exactly the
+reference's ``factors[k]`` array (cp.py:43-59), stacked mode-major.  Scalars
+live in mode 0 (cp.py:1-12).  Arithmetic is real fp64 (the BASELINE configs
+are real; the reference's complex128 agrees to ~1e-15 on real data, SURVEY
+8(c) S9).  All compute runs through the sm_100a C-ABI library; there is no
+CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ConditioningError
+from .basis import BasisSpec
+
+__all__ = [
+    "CPTensor", "ALSApproxConfig", "ConditioningError", "add", "scale", "inner_product", "norm",
+    "random_cp", "pad_rank", "cp_approx_als", "rank_reduce_als", "from_numpy_factors",
+]
+
+
+def _as_real_array(f, k):
+    if isinstance(f, torch.Tensor):
+        if f.is_complex():
+            if torch.any(f.imag != 0):
+                raise ValueError(f"dimension {k}: complex coefficients are not supported on the real-fp64 B200 path")
+            f = f.real
+        return f.detach().to(torch.float64)
+    a = np.asarray(f)
+    if np.iscomplexobj(a):
+        if np.any(a.imag != 0):
+            raise ValueError(f"dimension {k}: complex coefficients are not supported on the real-fp64 B200 path")
+        a = a.real
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64))
+
+
+class CPTensor:
+    """``CPTensor(specs, factors)`` validates like cp.py:47-59 and copies the
+    factors into one device buffer (value semantics, like the reference's
+    ``np.ascontiguousarray`` copy)."""
+
+    __slots__ = ("specs", "data", "_rank")
+
+    def __init__(self, specs, factors=None, *, data: torch.Tensor | None = None, rank: int | None = None):
+        self.specs = tuple(specs)
+        if data is not None:
+            self.data = data
+            self._rank = int(rank)
+            return
+        if factors is None or len(factors) != len(self.specs):
+            raise ValueError("one factor matrix per dimension required")
+        mats = [_as_real_array(f, k) for k, f in enumerate(factors)]
+        ranks = {int(m.shape[1]) if m.dim() == 2 else -1 for m in mats}
+        if len(ranks) != 1:
+            raise ValueError(f"inconsistent ranks across dimensions: {ranks}")
+        for k, (m, spec) in enumerate(zip(mats, self.specs)):
+            if m.dim() != 2 or m.shape[0] != spec.Q:
+                raise ValueError(f"dimension {k}: {m.shape[0]} rows != Q={spec.Q}")
+        r = mats[0].shape[1]
+        if r < 1:
+            raise ValueError("rank must be at least 1")
+        dev = _lib.device()
+        self.data = torch.cat([m.reshape(-1) for m in mats]).to(dev)
+        self._rank = int(r)
+
+    # -- shape
+    @property
+    def ndim(self) -> int:
+        return len(self.specs)
+
+    @property
+    def rank(self) -> int:
+        return self._rank
+
+    @property
+    def qs(self) -> tuple[int, ...]:
+        return tuple(s.Q for s in self.specs)
+
+    @property
+    def factors(self) -> list[torch.Tensor]:
+        """Per-mode ``(Q_k, R)`` views into the device buffer."""
+        out, off = [], 0
+        for q in self.qs:
+            n = q * self._rank
+            out.append(self.data[off:off + n].view(q, self._rank))
+            off += n
+        return out
+
+    def copy(self) -> "CPTensor":
+        return CPTensor(self.specs, data=self.data.clone(), rank=self._rank)
+
+    def norm(self) -> float:
+        return norm(self)
+
+    def to_numpy(self) -> list[np.ndarray]:
+        return [f.cpu().numpy().copy() for f in self.factors]
+
+    def __repr__(self):
+        return f"CPTensor(ndim={self.ndim}, Q={self.qs}, rank={self.rank}, device={self.data.device})"
+
+
+def from_numpy_factors(specs, factors) -> CPTensor:
+    return CPTensor(specs, factors)
+
+
+def empty_cp(specs, rank: int, dev=None) -> CPTensor:
+    n = sum(s.Q for s in specs) * rank
+    return CPTensor(specs, data=torch.empty(n, dtype=torch.float64, device=dev or _lib.device()), rank=rank)
+
+
+def _check_same_specs(f: CPTensor, g: CPTensor) -> None:
+    if f.specs != g.specs:
+        raise ValueError("operands live on different bases")
+
+
+def concat(specs, parts) -> CPTensor:
+    """Column concatenation of several (tensor, scale) parts in one device pass
+    (cp.add / cp.scale, cp.py:98-108).  Scale goes into mode 0."""
+    parts = [(t, float(c)) for t, c in parts]
+    R = sum(t.rank for t, _ in parts)
+    out = empty_cp(specs, R, parts[0][0].data.device)
+    col = 0
+    for t, c in parts:
+        _apply_raw(t, [[None] * t.ndim], [1.0], c, None, out, col)
+        col += t.rank
+    return out
+
+
+def add(f: CPTensor, g: CPTensor) -> CPTensor:
+    """Exact sum; ranks add, g's terms follow f's (cp.py:98-101)."""
+    _check_same_specs(f, g)
+    return concat(f.specs, [(f, 1.0), (g, 1.0)])
+
+
+def scale(f: CPTensor, c) -> CPTensor:
+    """Scalar multiple folded into mode 0 (cp.py:104-108)."""
+    if isinstance(c, complex):
+        if c.imag != 0:
+            raise ValueError("complex scalars are not supported on the real-fp64 B200 path")
+        c = c.real
+    return concat(f.specs, [(f, float(c))])
+
+
+def _inner_device(f: CPTensor, g: CPTensor, out: torch.Tensor) -> None:
+    L = _lib.lib()
+    qs = _lib.int_array(f.qs)
+    same = 1 if (f.data.data_ptr() == g.data.data_ptr() and f.rank == g.rank) else 0
+    nbytes = L.tp_cp_inner_ws_bytes(f.ndim, qs, f.rank, g.rank)
+    ws = _lib.WORKSPACE.get(nbytes, f.data.device)
+    st = L.tp_cp_inner_f64(f.ndim, qs, f.rank, f.data.data_ptr(), g.rank, g.data.data_ptr(), same,
+                           out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(f.data.device))
+    _lib.check(st, "inner_product")
+
+
+def inner_product(f: CPTensor, g: CPTensor) -> float:
+    """``<f, g> = sum_{l,n} prod_k (F_k^T G_k)[l, n]`` (cp.py:111-121).  Real
+    path: the conjugation on f is the identity.  Returns a Python float."""
+    _check_same_specs(f, g)
+    out = torch.empty(1, dtype=torch.float64, device=f.data.device)
+    _inner_device(f, g, out)
+    return float(out.item())
+
+
+def norm(f: CPTensor) -> float:
+    """cp.py:124-126."""
+    return float(math.sqrt(max(inner_product(f, f), 0.0)))
+
+
+def random_cp(specs, r: int, rng: np.random.Generator) -> CPTensor:
+    """Unit-normalised random terms (cp.py:129-136), real variant."""
+    factors = []
+    for spec in specs:
+        m = rng.standard_normal((spec.Q, r))
+        m /= np.linalg.norm(m, axis=0, keepdims=True)
+        factors.append(m)
+    return CPTensor(tuple(specs), factors)
+
+
+def pad_rank(f: CPTensor, r: int, rng: np.random.Generator, rel_scale: float = 1e-8) -> CPTensor:
+    """cp.py:139-146."""
+    if r < f.rank:
+        raise ValueError(f"cannot pad rank {f.rank} down to {r}")
+    if r == f.rank:
+        return f.copy()
+    pad = scale(random_cp(f.specs, r - f.rank, rng), rel_scale * max(norm(f), 1.0))
+    return add(f, pad)
+
+
+@dataclass
+class ALSApproxConfig:
+    """cp.py:150-163, plus:
+
+    ``reg``   -- ``None``: the reference rule lambda = 1e-12 tr(H)/r (cp.py:166-173);
+                 a float: fixed Tikhonov lambda (BASELINE: 1e-10).
+    ``grid``  -- CTAs of the persistent ALS kernel (0 = library heuristic).
+    ``max_sweeps/tol/stall/seed`` keep the reference meaning; ``stall=-inf``
+    and ``tol=0`` run exactly ``max_sweeps`` sweeps.
+    """
+
+    max_sweeps: int = 200
+    tol: float = 0.0
+    stall: float = 1e-13
+    seed: int = 0
+    quad_points: int = 0
+    reg: float | None = None
+    grid: int = 0
+
+
+_REG = 1e-12
+
+
+def _als_device(target: CPTensor, U: torch.Tensor, r: int, cfg: ALSApproxConfig,
+                trace_buf: torch.Tensor | None, info: torch.Tensor) -> None:
+    """Launch the fused ALS on the current stream; U is overwritten in place."""
+    L = _lib.lib()
+    qs = _lib.int_array(target.qs)
+    d = target.ndim
+    nbytes = L.tp_cp_als_ws_bytes(d, qs, target.rank, r, cfg.grid)
+    if nbytes == 0:
+        raise ValueError(f"unsupported ALS size: d={d}, R={target.rank}, r={r} (r <= 32, d <= 8)")
+    ws = _lib.WORKSPACE.get(nbytes, target.data.device)
+    reg, mode = (_REG, 1) if cfg.reg is None else (float(cfg.reg), 0)
+    st = L.tp_cp_als_f64(d, qs, target.rank, target.data.data_ptr(), r, U.data_ptr(), int(cfg.max_sweeps),
+                         reg, mode, float(cfg.tol), float(cfg.stall),
+                         trace_buf.data_ptr() if trace_buf is not None else None,
+                         info.data_ptr(), int(cfg.grid), ws.data_ptr(), ws.numel(),
+                         _lib.stream_ptr(target.data.device))
+    _lib.check(st, "cp_approx_als")
+
+
+def _check_info(info: torch.Tensor) -> int:
+    status, done = (int(v) for v in info.tolist())
+    if status & 2:
+        raise ConditioningError("normal equations produced non-finite coefficients")
+    if status & 1:
+        raise ConditioningError("regularised normal equations are not positive definite")
+    return done
+
+
+def cp_approx_als(target, r: int, config: ALSApproxConfig | None = None, *, specs=None,
+                  init: CPTensor | None = None, trace: list | None = None) -> CPTensor:
+    """Fit a rank-``r`` CP tensor to ``target`` by Gauss-Seidel ALS (cp.py:266-334).
+
+    One call = one launch of the persistent fused ALS kernel (all sweeps).
+    Callable targets (cp.py:212-263, quadrature projection) are out of the
+    hot-path scope and raise ``NotImplementedError``.
+    """
+    cfg = config or ALSApproxConfig()
+    if not isinstance(target, CPTensor):
+        if specs is None:
+            raise ValueError("callable targets require specs")
+        raise NotImplementedError("callable (quadrature) targets are outside the B200 hot path")
+    specs = target.specs
+    rng = np.random.default_rng(cfg.seed)
+    guess = init.copy() if init is not None else random_cp(specs, r, rng)
+    if guess.rank != r or guess.specs != tuple(specs):
+        raise ValueError("init shape does not match the requested fit")
+    dev = target.data.device
+    info = torch.zeros(2, dtype=torch.int32, device=dev)
+    tb = torch.zeros(max(cfg.max_sweeps, 1), dtype=torch.float64, device=dev) if trace is not None else None
+    _als_device(target, guess.data, r, cfg, tb, info)
+    done = _check_info(info)
+    if trace is not None:
+        trace.extend(tb[:done].tolist())
+    return guess
+
+
+def _relative_error(f: CPTensor, g: CPTensor, nf: float) -> float:
+    """Gram-identity error as in cp.py:369-375 (what the reference's adaptive loop uses)."""
+    d = inner_product(f, f) - 2.0 * inner_product(g, f) + inner_product(g, g)
+    return float(math.sqrt(max(d, 0.0)) / nf)
+
+
+def rank_reduce_als(f: CPTensor, r_target: int, eps: float, config: ALSApproxConfig | None = None) -> CPTensor:
+    """Adaptive rank 1..r_target, warm start + one fresh random term (cp.py:337-366).
+    Random terms are real (the reference draws complex ones)."""
+    if r_target < 1:
+        raise ValueError("target rank must be at least 1")
+    cfg = config or ALSApproxConfig()
+    nf = norm(f)
+    zero = CPTensor(f.specs, [np.zeros((s.Q, 1)) for s in f.specs])
+    if nf == 0.0:
+        return zero
+    rng = np.random.default_rng(cfg.seed)
+    best, best_err = zero, 1.0
+    guess = None
+    for r in range(1, r_target + 1):
+        init = random_cp(f.specs, 1, rng) if guess is None else add(guess, random_cp(f.specs, 1, rng))
+        guess = cp_approx_als(f, r, cfg, init=init)
+        err = _relative_error(f, guess, nf)
+        if err < best_err:
+            best, best_err = guess, err
+        if err <= eps:
+            return guess
+    return best
+
+
+# ---- operator apply into a preallocated target (shared with operators.py) ----
+
+def _apply_raw(f: CPTensor, mat_rows, weights, scale_, mats_dev, out: CPTensor, col_off: int,
+               mat_off=None) -> None:
+    """Launch tp_cp_apply_f64: mat_rows[t][k] is an int matrix index or None."""
+    L = _lib.lib()
+    d = f.ndim
+    n_terms = len(weights)
+    idx = []
+    for row in mat_rows:
+        idx.extend(-1 if m is None else int(m) for m in row)
+    n_mats = 0 if mat_off is None else len(mat_off)
+    st = L.tp_cp_apply_f64(d, _lib.int_array(f.qs), f.rank, f.data.data_ptr(), n_terms,
+                           _lib.double_array(weights), float(scale_), _lib.int_array(idx),
+                           None if mats_dev is None else mats_dev.data_ptr(),
+                           None if mat_off is None else _lib.ll_array(mat_off), n_mats,
+                           out.data.data_ptr(), out.rank, int(col_off), _lib.stream_ptr(f.data.device))
+    _lib.check(st, "apply")
+
+
+_ = ctypes  # keep import for type users

@@ -1,0 +1,656 @@
+// Fused, persistent CP-ALS (cp.cp_approx_als, cp.py:266-334) for sm_100a.
+//
+// One cooperative launch runs every sweep of a truncation.  CTA p owns a
+// contiguous slab of the R target terms and keeps, in shared memory, the
+// target factors of that slab for every mode (V_k[:, slab], transposed) and
+// the cross matrices C_k[:, slab] = U_k^T V_k[:, slab] (cp.py:190-195).
+// A mode update j (cp.py:311-320) is two phases separated by grid barriers:
+//
+//  A: finish the previous mode jp: stage U_jp (bulk async copies), C_jp[:, slab]
+//     by DMMA, this CTA's share of the Gram entries G_jp = U_jp^T U_jp;
+//     had = prod_{k!=j} C_k[:, slab] (cp.py:197-201); partial right-hand side
+//     Y_p = V_j[:, slab] had^T by DMMA (cp.py:203), written to a per-CTA slot.
+//  B: one bulk-async transaction pulls G_jp and this CTA's column slices of the
+//     P partial right-hand sides; the CTA sums the slices in fixed order,
+//     forms A = prod_{k!=j} G_k + lambda I (cp.py:312-315, 171-173) and inverts
+//     it with a register-resident symmetric sweep (256 threads, one barrier per
+//     pivot), then U_j[cols, :] = (A^-1 rhs)^T (cp.py:317).
+//
+// After each sweep (only if a trace or stopping rule needs it) the residual
+// ||V||^2 - 2 Re sum prod C + sum prod G (cp.py:321-332) is formed identically
+// in every CTA, so the stopping decision is uniform without host round trips.
+// All cross-CTA reductions use a fixed order: results are bitwise
+// reproducible for a fixed grid size.
+#include "tp_common.cuh"
+#include <cooperative_groups.h>
+#include <cstring>
+
+namespace cg = cooperative_groups;
+
+namespace tp {
+
+int inner_tiles(int ra, int rb, int same);
+int launch_inner(int d, const int* q, int ra, const double* A, int rb, const double* B, int same,
+                 double* out, double* partial, cudaStream_t st);
+
+constexpr int ALS_NT = 256;
+constexpr int ALS_NW = ALS_NT / 32;
+constexpr int ALS_PART = 1024;   // doubles of scratch for split-K partial tiles / reductions
+
+// padded shared-memory row stride: >= n and == 4 (mod 16) doubles, so DMMA
+// fragment loads (4 rows x 8 columns per half-warp) hit distinct banks
+__host__ __device__ inline int pad4(int n) { return n + (((4 - n % 16) + 16) % 16); }
+
+struct AlsArgs {
+  int d, R, r, sweeps, qmax, wmax, ncolmax, P;
+  int q[TP_MAXD];
+  long long offV[TP_MAXD], offU[TP_MAXD];
+  int qs[TP_MAXD];     // padded stride of V_k[:, slab]^T rows in shared memory
+  int qoff[TP_MAXD];   // shared-memory offset (doubles) of V_k[:, slab]^T
+  int sumqs;
+  const double* V;
+  double* U;
+  double* G;           // d * r * r
+  double* Y;           // P (consumer) x P (producer) x ncolmax x r
+  double* ovl;         // P
+  const double* norm_sq;
+  double* trace;
+  int* info;           // {status bits, sweeps done}
+  double reg;
+  int reg_mode;
+  double tol, stall;
+  int need_resid;
+  long long* prof;     // optional per-phase clock64 totals (CTA 0), debug hook
+};
+
+struct Smem {
+  uint64_t* bar;
+  double *Us, *Vs, *Cs, *Gs, *hadT, *Ai, *pub, *rb, *part, *scal;
+};
+
+__host__ __device__ inline size_t stage_doubles(int qmax, int r, int ncolmax, int P) {
+  // staging area shared by U_k (phase A, padded rows) and the P right-hand-side
+  // slices + one Gram (phase B)
+  size_t a = (size_t)qmax * r, b = (size_t)P * ncolmax * r + (size_t)r * r;   // raw Gram + P blocks
+  return a > b ? a : b;
+}
+
+__host__ __device__ inline size_t als_smem_doubles(int d, int sumqs, int r, int wmax, int ncolmax, int qmax, int P) {
+  const size_t w4 = (size_t)((wmax + 3) / 4) * 4;
+  return 8 + stage_doubles(qmax, r, ncolmax, P) + (size_t)wmax * sumqs + (size_t)d * r * wmax +
+         (size_t)d * r * pad4(r) + w4 * pad4(r) + (size_t)r * (r + 1) + 72 + (size_t)ncolmax * r + ALS_PART + 8;
+}
+
+__device__ inline Smem carve(double* base, const AlsArgs& a) {
+  Smem s;
+  size_t o = 0;
+  s.bar = reinterpret_cast<uint64_t*>(base + o); o += 8;
+  s.Us = base + o; o += stage_doubles(a.qmax, a.r, a.ncolmax, a.P);
+  s.Vs = base + o; o += (size_t)a.wmax * a.sumqs;
+  s.Cs = base + o; o += (size_t)a.d * a.r * a.wmax;
+  s.Gs = base + o; o += (size_t)a.d * a.r * pad4(a.r);
+  s.hadT = base + o; o += (size_t)((a.wmax + 3) / 4) * 4 * pad4(a.r);
+  s.Ai = base + o; o += (size_t)a.r * (a.r + 1);
+  s.pub = base + o; o += 72;
+  s.rb = base + o; o += (size_t)a.ncolmax * a.r;
+  s.part = base + o; o += ALS_PART;
+  s.scal = base + o;
+  return s;
+}
+
+// fast reciprocal: MUFU seed + 2 Newton steps (<= 1 ulp, no slow path)
+__device__ __forceinline__ double rcp_nr(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+
+// Stage U_k (Q_k x r, written by other CTAs) into sm.Us (row stride r): one
+// bulk async copy of the contiguous block through the TMA engine (per-row
+// copies serialise in the SM's copy unit and were 6x slower).
+__device__ void stage_u(const AlsArgs& a, const Smem& sm, int k, uint32_t& phase) {
+  const int n = a.q[k] * a.r;
+  const double* Uk = a.U + a.offU[k];
+  __syncthreads();   // previous users of sm.Us are done
+  if (((a.offU[k] | n) & 1) == 0) {
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(sm.bar, (uint32_t)n * 8u);
+      bulk_g2s(sm.Us, Uk, (uint32_t)n * 8u, sm.bar);
+    }
+    mbar_wait(sm.bar, phase);
+    phase ^= 1u;
+  } else {
+    for (int e = threadIdx.x; e < n; e += ALS_NT) sm.Us[e] = __ldcg(Uk + e);
+    __syncthreads();
+  }
+}
+
+// Cs[k][l][c] = sum_s U_k[s][l] V_k[s][c0 + c] (cp.py:190-195) on the DMMA
+// tensor pipe: M = l, N = c, K = s; output tiles x split-K over the 8 warps.
+__device__ void cross_slab(const AlsArgs& a, const Smem& sm, int k, int w) {
+  const int r = a.r, Q = a.q[k], ru = r, qs = a.qs[k];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* vs = sm.Vs + a.qoff[k];
+  double* C = sm.Cs + (size_t)k * r * a.wmax;
+  const int mt = (r + 7) / 8, nt = (w + 7) / 8, tiles = mt * nt;
+  int ks = 1;
+  while (tiles * ks < ALS_NW && ks < 8) ks <<= 1;
+  while (tiles * ks * 64 > ALS_PART && ks > 1) ks >>= 1;
+  const int ksteps = (Q + 3) / 4, per = (ksteps + ks - 1) / ks;
+  const bool direct = (ks == 1);
+  for (int it = warp; it < tiles * ks; it += ALS_NW) {
+    const int tile = it / ks, kp = it % ks;
+    const int m0 = (tile / nt) * 8, n0 = (tile % nt) * 8;
+    const int l = m0 + (lane >> 2), c = n0 + (lane >> 2);
+    double acc0 = 0.0, acc1 = 0.0;
+    const int kb = kp * per, ke = min(ksteps, kb + per);
+    for (int kk = kb; kk < ke; ++kk) {
+      const int s = 4 * kk + (lane & 3);
+      const double fa = (s < Q && l < r) ? sm.Us[s * ru + l] : 0.0;
+      const double fb = (s < Q && c < w) ? vs[c * qs + s] : 0.0;
+      dmma_8x8x4(acc0, acc1, fa, fb);
+    }
+    const int orow = m0 + (lane >> 2), ocol = n0 + 2 * (lane & 3);
+    if (direct) {
+      if (orow < r) {
+        if (ocol < w) C[orow * a.wmax + ocol] = acc0;
+        if (ocol + 1 < w) C[orow * a.wmax + ocol + 1] = acc1;
+      }
+    } else {
+      double* pt = sm.part + (size_t)it * 64;
+      pt[2 * lane] = acc0;
+      pt[2 * lane + 1] = acc1;
+    }
+  }
+  __syncthreads();
+  if (!direct) {
+    for (int e = threadIdx.x; e < tiles * 64; e += ALS_NT) {
+      const int tile = e / 64, ln = (e % 64) / 2, h = e & 1;
+      const int orow = (tile / nt) * 8 + (ln >> 2), ocol = (tile % nt) * 8 + 2 * (ln & 3) + h;
+      double acc = 0.0;
+      for (int kp = 0; kp < ks; ++kp) acc += sm.part[(size_t)(tile * ks + kp) * 64 + 2 * ln + h];
+      if (orow < r && ocol < w) C[orow * a.wmax + ocol] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// this CTA's share of G_k = U_k^T U_k (cp.py:318): the upper 8x8 tiles are
+// dealt round-robin to CTAs; each tile is one DMMA chain split over the warps.
+__device__ void gram_share(const AlsArgs& a, const Smem& sm, int k) {
+  const int r = a.r, Q = a.q[k], ru = r, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mt = (r + 7) / 8, ntile = mt * (mt + 1) / 2;
+  double* Gk = a.G + (size_t)k * r * r;
+  const int ksteps = (Q + 3) / 4, per = (ksteps + ALS_NW - 1) / ALS_NW;
+  for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+    int ti = 0, rem = t;
+    while (rem >= mt - ti) { rem -= mt - ti; ++ti; }
+    const int tj = ti + rem, m0 = ti * 8, n0 = tj * 8;
+    const int l = m0 + (lane >> 2), m = n0 + (lane >> 2);
+    double acc0 = 0.0, acc1 = 0.0;
+    const int kb = warp * per, ke = min(ksteps, kb + per);
+    for (int kk = kb; kk < ke; ++kk) {
+      const int s = 4 * kk + (lane & 3);
+      const double fa = (s < Q && l < r) ? sm.Us[s * ru + l] : 0.0;
+      const double fb = (s < Q && m < r) ? sm.Us[s * ru + m] : 0.0;
+      dmma_8x8x4(acc0, acc1, fa, fb);
+    }
+    __syncthreads();
+    sm.part[warp * 64 + 2 * lane] = acc0;
+    sm.part[warp * 64 + 2 * lane + 1] = acc1;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      const int ln = threadIdx.x >> 1, h = threadIdx.x & 1;
+      double acc = 0.0;
+      for (int w = 0; w < ALS_NW; ++w) acc += sm.part[w * 64 + threadIdx.x];
+      const int orow = m0 + (ln >> 2), ocol = n0 + 2 * (ln & 3) + h;
+      if (orow < r && ocol < r) {
+        Gk[orow * r + ocol] = acc;
+        Gk[ocol * r + orow] = acc;
+      }
+    }
+  }
+}
+
+// deterministic block sum (all threads call; result valid in all threads)
+__device__ inline double block_sum(double v, double* red) {
+  const int tid = threadIdx.x;
+  red[tid] = v;
+  __syncthreads();
+  for (int w = ALS_NT / 2; w > 0; w >>= 1) {
+    if (tid < w) red[tid] += red[tid + w];
+    __syncthreads();
+  }
+  double out = red[0];
+  __syncthreads();
+  return out;
+}
+
+// A = prod_{k!=j} G_k + lambda I and A^-1 -> sm.Ai (row stride r+1).
+// Symmetric sweep operator (in-place Gauss-Jordan on an SPD matrix; after
+// sweeping every pivot the array holds -A^-1), element-parallel: thread t owns
+// row t/8 and columns (t%8) + 8u, u < RM/8, in registers.  Symmetry gives
+// column k == row k, so each pivot step publishes one row and costs one
+// barrier.  Returns 1 if a pivot is not positive / finite.
+template <int RM>
+__device__ int gram_inverse(const AlsArgs& a, const Smem& sm, int j) {
+  constexpr int EPT = RM / 8;
+  const int r = a.r, gs = pad4(r), gk = r * gs, rp = r + 1, t = threadIdx.x;
+  const int i = t >> 3, c0 = t & 7;
+  double v[EPT];
+#pragma unroll
+  for (int u = 0; u < EPT; ++u) {
+    const int c = c0 + 8 * u;
+    double x = 0.0;
+    if (i < r && c < r) {
+      x = 1.0;
+      for (int k = 0; k < a.d; ++k)
+        if (k != j) x *= sm.Gs[(size_t)k * gk + i * gs + c];
+    }
+    v[u] = x;
+  }
+  // regulariser (cp.py:171-173): fixed lambda, or reg * max(tr A, 0) / r
+  double lam = a.reg;
+  if (a.reg_mode) {
+#pragma unroll
+    for (int u = 0; u < EPT; ++u)
+      if (c0 + 8 * u == i && i < r) sm.part[i] = v[u];
+    __syncthreads();
+    double tr = 0.0;
+    for (int q = 0; q < r; ++q) tr += sm.part[q];
+    lam = a.reg * fmax(tr, 0.0) / (double)r;
+  }
+#pragma unroll
+  for (int u = 0; u < EPT; ++u)
+    if (c0 + 8 * u == i && i < r) v[u] += lam;
+  if (i == 0)
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) sm.pub[c0 + 8 * u] = v[u];
+  __syncthreads();
+  int bad = 0;
+  for (int k = 0; k < r; ++k) {
+    const double* rk = sm.pub + (k & 1) * 36;
+    double* rn = sm.pub + ((k + 1) & 1) * 36;
+    const double d = rk[k];
+    if (!(d > 0.0) || !isfinite(d)) bad = 1;
+    const double id = rcp_nr(d);
+    const double f = (i < r ? rk[i] : 0.0) * id;   // a_ik / d  (column k == row k)
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const int c = c0 + 8 * u;
+      const double akc = rk[c];
+      double nv = fma(-f, akc, v[u]);
+      nv = (c == k) ? f : nv;
+      nv = (i == k) ? ((c == k) ? -id : akc * id) : nv;
+      v[u] = nv;
+    }
+    if (i == k + 1)
+#pragma unroll
+      for (int u = 0; u < EPT; ++u) rn[c0 + 8 * u] = v[u];
+    __syncthreads();
+  }
+  if (i < r)
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const int c = c0 + 8 * u;
+      if (c < r) sm.Ai[i * rp + c] = -v[u];
+    }
+  return bad;
+}
+
+// debug phase timers: barrier-synchronised so the attribution is exact
+#define PROF(ph)                                                        \
+  do {                                                                  \
+    if (a.prof) {                                                       \
+      __syncthreads();                                                  \
+      /* BAR.SYNC defers blocking to the next dependent instruction:  */ \
+      /* force it with a shared load before sampling the clock        */ \
+      prof_sink += *(volatile double*)sm.scal;                          \
+      long long now = clock64();                                        \
+      prof_acc[ph] += now - prof_t;                                     \
+      prof_t = now;                                                     \
+    }                                                                   \
+  } while (0)
+
+template <int RM>
+__global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constant__ AlsArgs a) {
+  extern __shared__ double smem[];
+  long long prof_t = clock64();
+  long long prof_acc[12] = {};
+  double prof_sink = 0.0;
+  cg::grid_group grid = cg::this_grid();
+  const Smem sm = carve(smem, a);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int p = blockIdx.x, P = gridDim.x, r = a.r, R = a.R, rr = r * r, rp = r + 1, rh = pad4(r);
+  const int c0 = (int)((long long)R * p / P), c1 = (int)((long long)R * (p + 1) / P), w = c1 - c0;
+  const int w4 = (w + 3) / 4 * 4;
+  int status = 0;
+  uint32_t bphase = 0;
+  if (tid == 0) {
+    mbar_init(sm.bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // zero hadT padding rows (c in [w, w4)) once
+  for (int e = tid; e < (w4 - w) * rh; e += ALS_NT) sm.hadT[(size_t)w * rh + e] = 0.0;
+  __syncthreads();
+
+  // ---- setup: stage V slab (transposed, padded), crosses and Grams of the initial guess
+  for (int k = 0; k < a.d; ++k) {
+    const int Q = a.q[k], qs = a.qs[k];
+    const double* Vk = a.V + a.offV[k];
+    double* vs = sm.Vs + a.qoff[k];
+    for (int e = tid; e < Q * w; e += ALS_NT) {
+      const int s = e / w, c = e % w;
+      vs[c * qs + s] = Vk[(size_t)s * R + c0 + c];
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < a.d; ++k) {
+    stage_u(a, sm, k, bphase);
+    cross_slab(a, sm, k, w);
+    gram_share(a, sm, k);
+  }
+  grid.sync();
+  const int gs = pad4(r), gk = r * gs;
+  for (int e = tid; e < a.d * rr; e += ALS_NT) {
+    const int k = e / rr, f = e % rr;
+    sm.Gs[(size_t)k * gk + (f / r) * gs + f % r] = __ldcg(a.G + e);
+  }
+  __syncthreads();
+
+  const double norm_sq = a.need_resid ? fmax(*a.norm_sq, 0.0) : 0.0;
+  const double t_norm = sqrt(norm_sq);
+  double prev = INFINITY;
+  int pending = -1, done = 0;
+  const bool bulk = (r & 1) == 0;
+
+  for (int sweep = 0; sweep < a.sweeps; ++sweep) {
+    for (int j = 0; j < a.d; ++j) {
+      // ---------------- phase A
+      PROF(0);
+      if (pending >= 0) {
+        stage_u(a, sm, pending, bphase);
+        PROF(10);
+        cross_slab(a, sm, pending, w);
+        PROF(11);
+        gram_share(a, sm, pending);
+      }
+      PROF(1);
+      const int Qj = a.q[j], qsj = a.qs[j];
+      for (int e = tid; e < r * w; e += ALS_NT) {
+        const int c = e / r, l = e % r;
+        double v = 1.0;
+        for (int k = 0; k < a.d; ++k)
+          if (k != j) v *= sm.Cs[((size_t)k * r + l) * a.wmax + c];
+        sm.hadT[c * rh + l] = v;
+      }
+      __syncthreads();
+      {
+        // Y_p[s][l] = sum_c V_j[s][c0+c] had[l][c]: M = s, N = l, K = c (DMMA).
+        // Stored consumer-major: row s goes to the CTA pc that owns column s in
+        // phase B, at YT[pc][p][s - s0(pc)][:], so every consumer later pulls
+        // one contiguous block with a single bulk copy.
+        const double* vs = sm.Vs + a.qoff[j];
+        const int mt = (Qj + 7) / 8, nt = (r + 7) / 8, kst = w4 / 4;
+        for (int m = warp; m < mt; m += ALS_NW) {
+          const int m0 = m * 8, s = m0 + (lane >> 2);
+          const bool srow = s < Qj;
+          const int pc = srow ? (int)((((long long)s + 1) * P + Qj - 1) / Qj) - 1 : 0;
+          const int ii = s - (int)((long long)Qj * pc / P);
+          double* yrow = a.Y + (((size_t)pc * P + p) * a.ncolmax + ii) * r;
+          for (int n = 0; n < nt; ++n) {
+            const int n0 = n * 8, l = n0 + (lane >> 2);
+            double acc0 = 0.0, acc1 = 0.0;
+            for (int kk = 0; kk < kst; ++kk) {
+              const int c = 4 * kk + (lane & 3);
+              const double av = (srow && c < w) ? vs[c * qsj + s] : 0.0;
+              const double fb = (l < r) ? sm.hadT[c * rh + l] : 0.0;
+              dmma_8x8x4(acc0, acc1, av, fb);
+            }
+            const int ocol = n0 + 2 * (lane & 3);
+            if (srow) {
+              if (ocol + 1 < r && (r & 1) == 0) {
+                *reinterpret_cast<double2*>(yrow + ocol) = make_double2(acc0, acc1);
+              } else {
+                if (ocol < r) yrow[ocol] = acc0;
+                if (ocol + 1 < r) yrow[ocol + 1] = acc1;
+              }
+            }
+          }
+        }
+      }
+      PROF(2);
+      grid.sync();
+      PROF(3);
+      // ---------------- phase B
+      const int s0 = (int)((long long)Qj * p / P), s1 = (int)((long long)Qj * (p + 1) / P);
+      const int ncol = s1 - s0, E = ncol * r;
+      const int nb = a.ncolmax * r;     // one producer's block for this consumer
+      double* ystage = sm.Us + rr;      // [q][nb] after one staged raw Gram
+      if (bulk) {
+        if (tid == 0) {
+          const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
+          const uint32_t ybytes = E > 0 ? (uint32_t)(P * nb) * 8u : 0u;
+          fence_proxy_async();
+          mbar_arrive_expect_tx(sm.bar, gbytes + ybytes);
+          if (gbytes) bulk_g2s(sm.Us, a.G + (size_t)pending * rr, gbytes, sm.bar);
+          if (ybytes) bulk_g2s(ystage, a.Y + (size_t)p * P * nb, ybytes, sm.bar);
+        }
+        mbar_wait(sm.bar, bphase);
+        bphase ^= 1u;
+        if (pending >= 0)
+          for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * gk + (e / r) * gs + e % r] = sm.Us[e];
+        for (int o = tid; o < E; o += ALS_NT) {
+          double acc = 0.0;
+          for (int q = 0; q < P; ++q) acc += ystage[(size_t)q * nb + o];
+          sm.rb[o] = acc;
+        }
+      } else {
+        if (pending >= 0)
+          for (int e = tid; e < rr; e += ALS_NT)
+            sm.Gs[(size_t)pending * gk + (e / r) * gs + e % r] = __ldcg(a.G + (size_t)pending * rr + e);
+        for (int o = tid; o < E; o += ALS_NT) {
+          double acc = 0.0;
+          for (int q = 0; q < P; ++q) acc += __ldcg(a.Y + ((size_t)p * P + q) * nb + o);
+          sm.rb[o] = acc;
+        }
+      }
+      __syncthreads();
+      PROF(4);
+      status |= gram_inverse<RM>(a, sm, j);
+      PROF(5);
+      if (E > 0) {
+        // X = A^-1 rhs  (columns of rhs are rows of rb)      (cp.py:317)
+        double* Uj = a.U + a.offU[j];
+        int nf = 0;
+        for (int e = tid; e < E; e += ALS_NT) {
+          const int sc = e / r, i = e % r;
+          double acc = 0.0;
+          for (int k = 0; k < r; ++k) acc = fma(sm.Ai[i * rp + k], sm.rb[sc * r + k], acc);
+          if (!isfinite(acc)) nf = 1;
+          Uj[(size_t)(s0 + sc) * r + i] = acc;
+        }
+        if (nf) atomicOr(a.info, 2);
+      }
+      pending = j;
+      PROF(6);
+      grid.sync();
+      PROF(7);
+    }
+    done = sweep + 1;
+    if (a.need_resid) {
+      // finish the last mode, then residual by the Gram identity (cp.py:321-326)
+      stage_u(a, sm, pending, bphase);
+      cross_slab(a, sm, pending, w);
+      gram_share(a, sm, pending);
+      double ov = 0.0;
+      for (int e = tid; e < r * w; e += ALS_NT) {
+        const int l = e / w, c = e % w;
+        double v = 1.0;
+        for (int k = 0; k < a.d; ++k) v *= sm.Cs[((size_t)k * r + l) * a.wmax + c];
+        ov += v;
+      }
+      ov = block_sum(ov, sm.part);
+      if (tid == 0) a.ovl[p] = ov;
+      grid.sync();
+      for (int e = tid; e < rr; e += ALS_NT)
+        sm.Gs[(size_t)pending * gk + (e / r) * gs + e % r] = __ldcg(a.G + (size_t)pending * rr + e);
+      pending = -1;
+      __syncthreads();
+      double self = 0.0;
+      for (int e = tid; e < rr; e += ALS_NT) {
+        double v = 1.0;
+        for (int k = 0; k < a.d; ++k) v *= sm.Gs[(size_t)k * gk + (e / r) * gs + e % r];
+        self += v;
+      }
+      self = block_sum(self, sm.part);
+      double ovt = 0.0;
+      if (warp == 0) {
+        for (int q = lane; q < P; q += 32) ovt += __ldcg(a.ovl + q);
+        ovt = warp_sum(ovt);
+        if (lane == 0) sm.scal[0] = ovt;
+      }
+      __syncthreads();
+      ovt = sm.scal[0];
+      const double resid = sqrt(fmax(norm_sq - 2.0 * ovt + self, 0.0));
+      if (p == 0 && tid == 0 && a.trace) a.trace[sweep] = resid;
+      __syncthreads();
+      if (resid <= a.tol * t_norm) break;
+      if (prev - resid < a.stall * fmax(t_norm, 1.0)) break;
+      prev = resid;
+    }
+  }
+  if (status && tid == 0 && p == 0) atomicOr(a.info, 1);
+  if (p == 0 && tid == 0) a.info[1] = done;
+  if (a.prof && p == 0 && tid == 0) {
+    for (int q = 0; q < 12; ++q) a.prof[q] += prof_acc[q];
+    if (prof_sink == 12345.0) a.prof[11] += 1;
+  }
+}
+
+struct AlsPlan {
+  AlsArgs a;
+  int P, rm;
+  size_t smem, ws_inner, ws_total;
+};
+
+static int choose_rm(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : 0)); }
+
+static const void* kernel_ptr(int rm) {
+  switch (rm) {
+    case 8: return (const void*)als_persistent<8>;
+    case 16: return (const void*)als_persistent<16>;
+    default: return (const void*)als_persistent<32>;
+  }
+}
+
+static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
+  if (d < 1 || d > TP_MAXD || R < 1 || r < 1 || !q) return TP_EINVAL;
+  for (int k = 0; k < d; ++k) if (q[k] < 1) return TP_EINVAL;
+  pl.rm = choose_rm(r);
+  if (!pl.rm) return TP_EUNSUPPORTED;
+  int dev = 0, nsm = 148, smem_optin = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  } else {
+    cudaGetLastError();
+  }
+  if (smem_optin <= 0) smem_optin = 227 * 1024;
+  int sumqs = 0, qmax = 0;
+  for (int k = 0; k < d; ++k) { sumqs += pad4(q[k]); qmax = q[k] > qmax ? q[k] : qmax; }
+  int P = grid;
+  if (P <= 0) {
+    double work = 4.0 * qmax * (double)R * r;   // flops of one mode update
+    P = (int)(work / 2.0e5);
+    if (P < 1) P = 1;
+  }
+  if (P > nsm) P = nsm;
+  if (P > R) P = R;
+  size_t smem = 0;
+  for (;;) {
+    int wmax = (R + P - 1) / P, ncolmax = (qmax + P - 1) / P;
+    smem = als_smem_doubles(d, sumqs, r, wmax, ncolmax, qmax, P) * sizeof(double);
+    if (smem <= (size_t)smem_optin) break;
+    if (P >= nsm || P >= R) return TP_EUNSUPPORTED;
+    ++P;
+  }
+  memset(&pl.a, 0, sizeof(pl.a));
+  AlsArgs& a = pl.a;
+  a.d = d; a.R = R; a.r = r; a.qmax = qmax; a.sumqs = sumqs; a.P = P;
+  a.wmax = (R + P - 1) / P; a.ncolmax = (qmax + P - 1) / P;
+  long long ov = 0, ou = 0;
+  int qo = 0;
+  for (int k = 0; k < d; ++k) {
+    a.q[k] = q[k]; a.qs[k] = pad4(q[k]); a.offV[k] = ov; a.offU[k] = ou; a.qoff[k] = qo;
+    ov += (long long)q[k] * R; ou += (long long)q[k] * r; qo += a.qs[k] * a.wmax;
+  }
+  pl.P = P;
+  pl.smem = smem;
+  pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
+  pl.ws_total = align_up(sizeof(double) * (size_t)d * r * r) + align_up(sizeof(double) * (size_t)P * P * a.ncolmax * r) +
+                align_up(sizeof(double) * (size_t)P) + align_up(sizeof(double)) + pl.ws_inner;
+  return TP_OK;
+}
+
+}  // namespace tp
+
+using namespace tp;
+
+static long long* g_prof = nullptr;
+
+extern "C" {
+
+// debug hook (not part of the public header): per-phase clock64 totals of CTA 0
+void tp_debug_set_als_profile(long long* dev_ptr) { g_prof = dev_ptr; }
+
+size_t tp_cp_als_ws_bytes(int d, const int* q, int R, int r, int grid) {
+  AlsPlan pl;
+  if (plan_als(d, q, R, r, grid, pl) != TP_OK) return 0;
+  return pl.ws_total;
+}
+
+int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
+                  int sweeps, double reg, int reg_mode, double tol, double stall,
+                  double* trace, int* info, int grid, void* ws, size_t ws_bytes, void* stream) {
+  if (!V || !U || !info || sweeps < 0 || !(reg >= 0.0)) return TP_EINVAL;
+  AlsPlan pl;
+  int st = plan_als(d, q, R, r, grid, pl);
+  if (st != TP_OK) return st;
+  if (!ws || ws_bytes < pl.ws_total) return TP_EWORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  AlsArgs& a = pl.a;
+  Carver cv(ws, ws_bytes);
+  a.G = cv.take<double>((size_t)d * r * r);
+  a.Y = cv.take<double>((size_t)pl.P * pl.P * a.ncolmax * r);
+  a.ovl = cv.take<double>(pl.P);
+  double* nsq = cv.take<double>(1);
+  double* part = cv.take<double>(pl.ws_inner / sizeof(double));
+  a.V = V; a.U = U; a.trace = trace; a.info = info;
+  a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = tol; a.stall = stall;
+  a.need_resid = (trace != nullptr) || (tol > 0.0) || (stall > -INFINITY);
+  a.norm_sq = nsq;
+  a.prof = g_prof;
+  cudaError_t e = cudaMemsetAsync(info, 0, 2 * sizeof(int), s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (a.need_resid) {
+    st = launch_inner(d, q, R, V, R, V, 1, nsq, part, s);   // ||V||^2 (cp.py:186-188)
+    if (st != TP_OK) return st;
+  }
+  const void* fn = kernel_ptr(pl.rm);
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  if (e != cudaSuccess) return cuda_status(e);
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ALS_NT, pl.smem);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (per_sm < 1) return TP_EUNSUPPORTED;
+  void* args[] = {&a};
+  e = cudaLaunchCooperativeKernel(fn, dim3(pl.P), dim3(ALS_NT), args, pl.smem, s);
+  return cuda_status(e);
+}
+
+}  // extern "C"

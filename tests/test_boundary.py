@@ -1,0 +1,88 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads and exports
+every symbol include/tpde_b200.h declares (no compute calls), and host-side
+validation mirrors the reference's error behaviour."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_1803_10270_b200 import _lib, basis, cp, operators
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    names = _lib.header_symbols()
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(L, n), n
+    assert L.tp_version().decode().startswith("tpde_b200")
+    assert L.tp_status_string(0).decode() == "ok"
+
+
+def test_signatures_cover_header():
+    assert set(_lib.header_symbols()) == set(_lib._SIGNATURES)
+
+
+def test_invalid_arguments_rejected_without_gpu():
+    L = _lib.lib()
+    q = _lib.int_array([4, 4])
+    assert L.tp_cp_inner_f64(0, q, 1, None, 1, None, 0, None, None, 0, None) == _lib.TP_EINVAL
+    assert L.tp_cp_als_f64(2, q, 4, None, 2, None, 1, 1e-10, 0, 0.0, 0.0, None, None, 0, None, 0,
+                           None) == _lib.TP_EINVAL
+    assert L.tp_cp_als_ws_bytes(2, q, 4, 40, 0) == 0  # r > 32 unsupported
+
+
+def test_cptensor_validation_mirrors_reference():
+    S = (basis.BasisSpec(5, 1.5), basis.BasisSpec(7, 2.0), basis.BasisSpec(3, 0.8))
+    with pytest.raises(ValueError, match="one factor matrix per dimension"):
+        cp.CPTensor(S, [np.zeros((5, 1))] * 2)
+    with pytest.raises(ValueError, match="inconsistent ranks"):
+        cp.CPTensor(S, [np.zeros((5, 1)), np.zeros((7, 2)), np.zeros((3, 1))])
+    with pytest.raises(ValueError, match="rows != Q"):
+        cp.CPTensor(S, [np.zeros((4, 1)), np.zeros((7, 1)), np.zeros((3, 1))])
+    with pytest.raises(ValueError, match="complex"):
+        cp.CPTensor(S, [np.ones((5, 1)) * 1j, np.zeros((7, 1)), np.zeros((3, 1))])
+
+
+def test_basis_spec_rules():
+    with pytest.raises(ValueError, match="odd"):
+        basis.BasisSpec(4, 1.0)
+    basis.BasisSpec(4, 1.0, "collocation")
+    with pytest.raises(ValueError, match="b must be positive"):
+        basis.BasisSpec(5, 0.0)
+
+
+def test_fourier_diff_matrix_exact_on_trig():
+    for Q in (8, 9, 32):
+        x = 2 * np.pi * np.arange(Q) / Q
+        D = basis.fourier_diff_matrix(Q)
+        for kk in range(1, (Q - 1) // 2 + 1):
+            np.testing.assert_allclose(D @ np.sin(kk * x), kk * np.cos(kk * x), atol=1e-11)
+
+
+def test_operator_validation_and_pairs():
+    S = tuple(basis.BasisSpec(6, np.pi, "collocation") for _ in range(3))
+    with pytest.raises(ValueError, match="one weight per term"):
+        operators.SeparableOperator(S, (1.0,), ((None,) * 3, (None,) * 3))
+    with pytest.raises(ValueError, match="at least one term"):
+        operators.SeparableOperator(S, (), ())
+    with pytest.raises(ValueError, match="every dimension"):
+        operators.SeparableOperator(S, (1.0,), ((None,) * 2,))
+    L = operators.advection_operator((1.0, 0.5, -0.75), S)
+    pair = operators.implicit_euler_pair(L, 0.1)
+    assert pair.eta == pytest.approx((1.0, 0.1, 0.05, -0.075), abs=1e-15)
+    assert pair.zeta == (1.0, 0.0, 0.0, 0.0)
+    cn = operators.crank_nicolson_pair(L, 0.1)
+    assert cn.eta[1] == pytest.approx(0.05) and cn.zeta[1] == pytest.approx(-0.05)
+    with pytest.raises(ValueError, match="complex"):
+        operators.dense_factor(basis.BasisSpec(5, 1.0), basis.FactorKind.DERIVATIVE)
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        _lib.device()
+    _ = ctypes

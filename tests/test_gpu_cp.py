@@ -1,0 +1,179 @@
+"""GPU parity: CP inner products, operator apply and the fused ALS kernel vs the
+oracle (oracle/ is pinned to the reference by tests/golden).  Bar: the stable
+relative difference of represented tensors <= 1e-9 per truncation (BASELINE
+north star); inner products to 1e-12 relative."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden, unpack_cp
+from oracle import cp_als as ocp
+from oracle import metrics, operators as oops
+
+pytestmark = pytest.mark.gpu
+
+tp = pytest.importorskip("paper_1803_10270_b200")
+from paper_1803_10270_b200 import cp, operators, workloads  # noqa: E402
+from paper_1803_10270_b200.basis import BasisSpec  # noqa: E402
+
+TOL_TRUNC = 1e-9
+
+
+def specs_for(qs):
+    return tuple(BasisSpec(q, math.pi, "collocation", lo=0.0) for q in qs)
+
+
+def rand_factors(rng, qs, r, scale=1.0):
+    return [scale * rng.standard_normal((q, r)) for q in qs]
+
+
+@pytest.mark.parametrize("qs,ra,rb", [((5, 7, 3), 3, 4), ((16,) * 6, 40, 40), ((33, 17, 64, 8), 70, 5),
+                                       ((256,) * 6, 512, 512), ((1, 2, 3), 1, 1)])
+def test_inner_product_matches_oracle(qs, ra, rb):
+    rng = np.random.default_rng(ra * 1000 + rb)
+    f = rand_factors(rng, qs, ra, 1 / math.sqrt(max(qs)))
+    g = rand_factors(rng, qs, rb, 1 / math.sqrt(max(qs)))
+    S = specs_for(qs)
+    F, G = cp.CPTensor(S, f), cp.CPTensor(S, g)
+    ref = ocp.inner_product(f, g).real
+    got = cp.inner_product(F, G)
+    assert abs(got - ref) <= 1e-12 * max(abs(ref), 1e-300) + 1e-14 * math.sqrt(abs(ocp.inner_product(f, f).real * ocp.inner_product(g, g).real))
+    # symmetric path (same buffer, upper tiles only)
+    ref_ff = ocp.inner_product(f, f).real
+    assert abs(cp.inner_product(F, F) - ref_ff) <= 1e-12 * abs(ref_ff)
+    assert abs(cp.norm(F) - math.sqrt(ref_ff)) <= 1e-12 * math.sqrt(ref_ff)
+
+
+def test_apply_matches_oracle():
+    g = load_golden("operators")
+    fr = unpack_cp(g, "col_f")
+    D, a = g["col_D"], g["col_a"]
+    S = specs_for([D.shape[0]] * 3)
+    op = operators.SeparableOperator(S, tuple(-a), tuple(tuple(D if k == t else None for k in range(3))
+                                                       for t in range(3)))
+    out = operators.apply(op, cp.CPTensor(S, fr))
+    ref = unpack_cp(g, "col_out")
+    for x, y in zip(out.to_numpy(), ref):
+        np.testing.assert_allclose(x, y, rtol=0, atol=1e-13)
+
+
+def test_add_scale_concatenate():
+    rng = np.random.default_rng(3)
+    S = specs_for((6, 5, 4))
+    f, g = rand_factors(rng, (6, 5, 4), 2), rand_factors(rng, (6, 5, 4), 3)
+    s = cp.add(cp.CPTensor(S, f), cp.scale(cp.CPTensor(S, g), -2.5))
+    ref = ocp.add(f, ocp.scale(g, -2.5))
+    assert s.rank == 5
+    for x, y in zip(s.to_numpy(), ref):
+        np.testing.assert_array_equal(x, y)
+
+
+def _als_case(V, init, sweeps, lam, stall=-np.inf, grid=0):
+    qs = [v.shape[0] for v in V]
+    S = specs_for(qs)
+    T = cp.CPTensor(S, V)
+    I0 = cp.CPTensor(S, init)
+    trace = []
+    cfg = cp.ALSApproxConfig(max_sweeps=sweeps, tol=0.0, stall=stall, reg=lam, grid=grid)
+    out = cp.cp_approx_als(T, init[0].shape[1], cfg, init=I0, trace=trace)
+    otrace = []
+    ref = ocp.als(V, init, sweeps, lam=lam, stall=stall, trace=otrace)
+    return out, ref, trace, otrace
+
+
+def test_als_golden_cases():
+    g = load_golden("cp_als")
+    for name in g["names"]:
+        name = str(name)
+        V = unpack_cp(g, f"{name}_V")
+        init = unpack_cp(g, f"{name}_init")
+        sweeps, lam, stall, r = g[f"{name}_meta"]
+        out, ref, trace, otrace = _als_case(V, init, int(sweeps), None if lam < 0 else float(lam), stall)
+        gold = unpack_cp(g, f"{name}_out")
+        rel = metrics.cp_rel_diff(gold, out.to_numpy())
+        assert rel <= TOL_TRUNC, (name, rel)
+        assert len(trace) == len(g[f"{name}_trace"]), name
+        np.testing.assert_allclose(trace, g[f"{name}_trace"], rtol=1e-6, atol=1e-8)
+
+
+@pytest.mark.parametrize("grid", [0, 1, 3, 17])
+def test_als_grid_sizes(grid):
+    rng = np.random.default_rng(7)
+    qs, R, r = (20, 24, 16, 12, 9), 37, 5
+    V = rand_factors(rng, qs, R, 0.3)
+    init = [v[:, :r].copy() for v in V]
+    out, ref, trace, otrace = _als_case(V, init, 12, 1e-10, grid=grid)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+    np.testing.assert_allclose(trace, otrace, rtol=1e-7, atol=1e-10)
+
+
+@pytest.mark.parametrize("r", [1, 6, 12, 16, 31, 32])
+def test_als_ranks(r):
+    rng = np.random.default_rng(100 + r)
+    qs, R = (24,) * 4, 3 * r + 5
+    V = rand_factors(rng, qs, R, 0.2)
+    init = [v[:, :r].copy() for v in V]
+    out, ref, _, _ = _als_case(V, init, 8, 1e-10)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+
+
+def test_als_config1_full_size():
+    w = workloads.cfg1(seed=0)
+    out, ref, trace, otrace = _als_case(w["V"], w["init"], w["sweeps"], w["lam"])
+    rel = metrics.cp_rel_diff(ref, out.to_numpy())
+    assert rel <= TOL_TRUNC, rel
+    assert len(trace) == 20
+    np.testing.assert_allclose(trace, otrace, rtol=1e-9)
+
+
+def test_als_deterministic_bitwise():
+    w = workloads.cfg1(seed=1, Q=64, R=128, r=16)
+    S = specs_for([64] * 6)
+    T, I0 = cp.CPTensor(S, w["V"]), cp.CPTensor(S, w["init"])
+    cfg = cp.ALSApproxConfig(max_sweeps=5, stall=-np.inf, reg=1e-10)
+    a = cp.cp_approx_als(T, 16, cfg, init=I0)
+    b = cp.cp_approx_als(T, 16, cfg, init=I0)
+    assert torch.equal(a.data, b.data)
+
+
+def test_als_stall_stop_matches_reference_rule():
+    rng = np.random.default_rng(9)
+    qs, r = (9, 8, 7, 6), 3
+    V = rand_factors(rng, qs, 10)
+    init = [v[:, :r].copy() for v in V]
+    out, ref, trace, otrace = _als_case(V, init, 200, None, stall=1e-13)
+    assert len(trace) == len(otrace)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+
+
+def test_als_zero_sweeps_returns_init_copy():
+    rng = np.random.default_rng(5)
+    S = specs_for((5, 6))
+    V = cp.CPTensor(S, rand_factors(rng, (5, 6), 4))
+    I0 = cp.CPTensor(S, rand_factors(rng, (5, 6), 2))
+    out = cp.cp_approx_als(V, 2, cp.ALSApproxConfig(max_sweeps=0), init=I0)
+    assert torch.equal(out.data, I0.data) and out.data.data_ptr() != I0.data.data_ptr()
+
+
+def test_als_rejects_bad_init():
+    rng = np.random.default_rng(5)
+    S = specs_for((5, 6))
+    V = cp.CPTensor(S, rand_factors(rng, (5, 6), 4))
+    with pytest.raises(ValueError, match="init"):
+        cp.cp_approx_als(V, 2, init=cp.CPTensor(S, rand_factors(rng, (5, 6), 3)))
+    with pytest.raises(ValueError, match="specs"):
+        cp.cp_approx_als(lambda p: p, 2)
+
+
+def test_rank_reduce_strips_noise():
+    rng = np.random.default_rng(8)
+    S = specs_for((7, 6, 5))
+    clean = cp.CPTensor(S, rand_factors(rng, (7, 6, 5), 2))
+    noisy = cp.pad_rank(clean, 4, rng, rel_scale=1e-9)
+    red = cp.rank_reduce_als(noisy, 2, eps=1e-7)
+    assert red.rank <= 2
+    rel = metrics.cp_rel_diff(noisy.to_numpy(), red.to_numpy())
+    assert rel < 1e-7
