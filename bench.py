@@ -1,0 +1,286 @@
+"""Benchmark: BASELINE config 1 (standalone CP-ALS truncation) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--grid P]
+
+A "step" is one 20-sweep ALS truncation (d=6, Q=256, R=512 -> r=32, lambda=1e-10,
+init = first 32 input terms, BASELINE.json configs[1]) of seeded synthetic input.
+
+* ``value``  -- sweeps/s of the fused ALS kernel with inputs resident in HBM,
+  CUDA-event timed per step on the launching stream, L2 flushed (256 MiB
+  write) between timed steps; whole-job aggregate over ranks (max time).
+* ``e2e``    -- the same metric through the public API ``cp_approx_als`` with
+  pinned HOST buffers: each step copies V and the initial guess host->device,
+  runs the truncation (incl. its one-int status check) and copies the fit back.
+* ``roofline`` -- algorithmic fp64 flops of one launch / mean
+  launch time vs the measured fp64 DMMA peak (profiles/r01_microbench.txt;
+  MEASURED_PEAKS.json has no fp64 entry).
+* ``cpu_baseline`` -- the oracle restatement of the reference path (complex128,
+  like the shipped reference) timed on this host's cores on a bounded sample.
+
+N > 1 (torchrun): each rank runs an independent truncation (weak scaling,
+replicas); the input-rank-sharded path is not in this round.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+D, Q, R, RANK_R, SWEEPS, LAM = 6, 256, 512, 32, 20, 1e-10
+# algorithmic flops (FMA = 2, no symmetry savings), SURVEY 8(d):
+SWEEP_FLOPS = D * (4 * RANK_R * Q * R + 4 * Q * RANK_R ** 2 + RANK_R ** 3 / 3)      # 107.0 MFLOP
+SETUP_FLOPS = D * 2 * RANK_R * Q * R + D * 2 * Q * RANK_R ** 2                       # crosses + Grams
+# the target self-norm (805 MFLOP) only runs when a trace / stopping rule needs it; off here
+FLOPS_PER_STEP = SWEEPS * SWEEP_FLOPS + SETUP_FLOPS
+FP64_PEAK_TFLOPS = 37.08   # measured DMMA m8n8k4 f64 on this pool's B200 (profiles/r01_microbench.txt)
+WORKLOAD = "cfg1: standalone CP-ALS d=6 Q=256 R=512 r=32, 20 sweeps, lambda=1e-10, init=first 32 terms"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline_run(seconds: float = 12.0):
+    """Oracle restatement of the reference path (complex128 like the shipped reference,
+    fixed lambda + fixed sweeps shims), all host threads via OpenBLAS."""
+    from oracle import cp_als as ocp
+    from paper_1803_10270_b200 import workloads
+    w = workloads.cfg1(0)
+    V = [v.astype(np.complex128) for v in w["V"]]
+    init = [u.astype(np.complex128) for u in w["init"]]
+    ocp.als(V, init, 2, lam=LAM)   # warm-up
+    n, t0 = 0, time.perf_counter()
+    while True:
+        ocp.als(V, init, SWEEPS, lam=LAM)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 200:
+            break
+    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": n * SWEEPS / el, "unit": "sweeps/s", "cores": cores, "kind": "port",
+            "sample": f"{n} full cfg1 truncations ({n * SWEEPS} sweeps) of the oracle (numpy complex128, "
+                      f"reference arithmetic), {el:.1f} s wall"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        pass
+    from oracle import cp_als as ocp
+    from paper_1803_10270_b200 import workloads
+    w = workloads.cfg1(0)
+    V = [v.astype(np.complex128) for v in w["V"]]
+    init = [u.astype(np.complex128) for u in w["init"]]
+    for _ in range(max(args.warmup, 1)):
+        ocp.als(V, init, 2, lam=LAM)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ocp.als(V, init, SWEEPS, lam=LAM)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    val = args.steps * SWEEPS / tot
+    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    line = {"metric": "CP-ALS sweeps/s", "value": val, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, seed 0)",
+            "config": {"workload": WORKLOAD, "l2": "n/a (CPU)"}, "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "sweeps/s", "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} cfg1 truncations of the oracle port (numpy complex128)"},
+            "e2e": {"value": val, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1803_10270_b200 import cp, workloads
+    from paper_1803_10270_b200 import _lib
+    dev = torch.device("cuda", local)
+    w = workloads.cfg1(seed=rank)
+    specs = w["specs"]
+    T = cp.CPTensor(specs, w["V"])
+    I0 = cp.CPTensor(specs, w["init"])
+    cfg = cp.ALSApproxConfig(max_sweeps=SWEEPS, tol=0.0, stall=-np.inf, reg=LAM, grid=args.grid)
+    info = torch.zeros(2, dtype=torch.int32, device=dev)
+    U = I0.data.clone()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def one():
+        U.copy_(I0.data)
+        cp._als_device(T, U, RANK_R, cfg, None, info)
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        for e0, e1 in evs:
+            flush.fill_(1.0)               # L2 flush outside the timed interval
+            U.copy_(I0.data)
+            e0.record(stream)
+            cp._als_device(T, U, RANK_R, cfg, None, info)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    _ = cp._check_info(info)
+    per = [e0.elapsed_time(e1) for e0, e1 in evs]
+    tot_ms = sum(per)
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * args.steps * SWEEPS / (tot_ms / 1e3)
+    ms_per_step = tot_ms / args.steps
+    achieved_tf = FLOPS_PER_STEP / (ms_per_step / 1e3) / 1e12
+
+    # ---- e2e: public API with pinned host buffers, H2D + call + D2H every step
+    hV = torch.cat([torch.as_tensor(v).reshape(-1) for v in w["V"]]).pin_memory()
+    hI = torch.cat([torch.as_tensor(u).reshape(-1) for u in w["init"]]).pin_memory()
+    hOut = torch.empty_like(hI).pin_memory()
+    dV = torch.empty_like(hV, device=dev)
+    dI = torch.empty_like(hI, device=dev)
+
+    def e2e_step():
+        dV.copy_(hV, non_blocking=True)
+        dI.copy_(hI, non_blocking=True)
+        Tt = cp.CPTensor(specs, data=dV, rank=R)
+        It = cp.CPTensor(specs, data=dI, rank=RANK_R)
+        out = cp.cp_approx_als(Tt, RANK_R, cfg, init=It)
+        hOut.copy_(out.data, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = world * args.steps * SWEEPS / (e2e_ms / 1e3)
+    traffic = None
+    prof_json = ROOT / "profiles" / "r01_als_ncu.json"
+    if prof_json.exists():
+        try:
+            traffic = json.loads(prof_json.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": "CP-ALS sweeps/s", "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1)/sqrt(Q), seed = rank)",
+            "config": {"workload": WORKLOAD, "l2": "flushed (256 MiB write) between timed steps",
+                       "grid_ctas": args.grid or "auto", "target_norm": "not computed (no trace / stopping rule)",
+                       "multi_gpu": "independent replicas per rank" if world > 1 else "single GPU"},
+            "e2e": {"value": e2e_val, "unit": "sweeps/s", "h2d_bytes_per_step": int((hV.numel() + hI.numel()) * 8),
+                    "d2h_bytes_per_step": int(hOut.numel() * 8 + 8)},
+            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "kernel": "tp::als_persistent<32> (one launch per step)",
+                         "flops_per_launch": FLOPS_PER_STEP,
+                         "peak_source": "measured fp64 DMMA peak (profiles/r01_microbench.txt); no fp64 entry in "
+                                        "MEASURED_PEAKS.json"},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "wall_s_timed_region": t_wall,
+        }
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline_run(args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    _ = _lib
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

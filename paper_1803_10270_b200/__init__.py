@@ -12,6 +12,7 @@ from ._lib import ConditioningError, StepFailure
 from .basis import BasisSpec, FactorKind, factor_matrix, fourier_diff_matrix
 from .cp import (ALSApproxConfig, CPTensor, add, cp_approx_als, inner_product, norm, pad_rank,
                  random_cp, rank_reduce_als, scale)
+from .ht import DimensionTree, HTTensor, balanced_tree, from_cp, truncate, truncate_batch
 from .operators import (CrankNicolsonPair, SeparableOperator, advection_operator, apply,
                         crank_nicolson_pair, implicit_euler_pair)
 
@@ -23,5 +24,6 @@ __all__ = [
     "add", "scale", "random_cp", "pad_rank", "ConditioningError", "StepFailure",
     "SeparableOperator", "CrankNicolsonPair", "advection_operator", "apply", "crank_nicolson_pair",
     "implicit_euler_pair",
+    "HTTensor", "DimensionTree", "balanced_tree", "from_cp", "truncate", "truncate_batch",
     "__version__",
 ]

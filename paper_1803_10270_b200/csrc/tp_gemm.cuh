@@ -1,0 +1,110 @@
+// Batched, arbitrarily-strided fp64 GEMM on the DMMA tensor pipe (sm_100a):
+//   C_z(m, n) = alpha * sum_k A_z(m, k) B_z(k, n) + beta * C_z(m, n)
+// Element (m, k) of A_z sits at A + offA(z) + m*sAm + k*sAk (same for B, C), so
+// transposes, tensor-mode contractions and Kronecker-style batched products are
+// all strided views -- no data is ever transposed in memory.
+// Batch z = (z1, z2): z1 indexes an optional device table of base offsets
+// (3 per entry: A, B, C) or uniform strides; z2 is an inner uniform batch.
+#pragma once
+#include "tp_common.cuh"
+
+namespace tp {
+
+constexpr int GB_TM = 64, GB_TN = 64, GB_TK = 16, GB_LD = 68;   // 68 == 4 (mod 16): conflict-free fragments
+
+struct BGemm {
+  int M, N, K, nb1, nb2;
+  long long sAm, sAk, sBk, sBn, sCm, sCn;
+  long long sA1, sB1, sC1;   // outer batch strides (used when offs == nullptr)
+  long long sA2, sB2, sC2;   // inner batch strides
+  const long long* offs;     // [nb1][3] base offsets or nullptr
+  const double* A;
+  const double* B;
+  double* C;
+  double alpha, beta;
+};
+
+static __global__ void __launch_bounds__(128) bgemm_kernel(const __grid_constant__ BGemm g) {
+  __shared__ double As[GB_TK][GB_LD];
+  __shared__ double Bs[GB_TK][GB_LD];
+  const int z = blockIdx.z, z1 = z / g.nb2, z2 = z % g.nb2;
+  long long oA, oB, oC;
+  if (g.offs) {
+    oA = g.offs[3 * z1]; oB = g.offs[3 * z1 + 1]; oC = g.offs[3 * z1 + 2];
+  } else {
+    oA = z1 * g.sA1; oB = z1 * g.sB1; oC = z1 * g.sC1;
+  }
+  const double* A = g.A + oA + z2 * g.sA2;
+  const double* B = g.B + oB + z2 * g.sB2;
+  double* C = g.C + oC + z2 * g.sC2;
+  const int m0 = blockIdx.y * GB_TM, n0 = blockIdx.x * GB_TN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const bool a_m_fast = g.sAm == 1, b_n_fast = g.sBn == 1;
+  for (int k0 = 0; k0 < g.K; k0 += GB_TK) {
+    __syncthreads();
+    for (int e = tid; e < GB_TK * GB_TM; e += 128) {
+      int kk, mm;
+      if (a_m_fast) { kk = e / GB_TM; mm = e % GB_TM; } else { mm = e / GB_TK; kk = e % GB_TK; }
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < g.M && k < g.K) ? A[m * g.sAm + k * g.sAk] : 0.0;
+    }
+    for (int e = tid; e < GB_TK * GB_TN; e += 128) {
+      int kk, nn;
+      if (b_n_fast) { kk = e / GB_TN; nn = e % GB_TN; } else { nn = e / GB_TK; kk = e % GB_TK; }
+      const int n = n0 + nn, k = k0 + kk;
+      Bs[kk][nn] = (n < g.N && k < g.K) ? B[k * g.sBk + n * g.sBn] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < GB_TK; ks += 4) {
+      const int kr = ks + (lane & 3), cc = lane >> 2;
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = As[kr][wm + 8 * i + cc];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = Bs[kr][wn + 8 * j + cc];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m0 + wm + 8 * i + (lane >> 2), n = n0 + wn + 8 * j + 2 * (lane & 3) + h;
+        if (m < g.M && n < g.N) {
+          double* c = C + m * g.sCm + n * g.sCn;
+          const double v = g.alpha * acc[i][j][h];
+          *c = (g.beta == 0.0) ? v : fma(g.beta, *c, v);
+        }
+      }
+}
+
+static inline BGemm bgemm_desc(int M, int N, int K, const double* A, long long sAm, long long sAk, const double* B,
+                        long long sBk, long long sBn, double* C, long long sCm, long long sCn) {
+  BGemm g{};
+  g.M = M; g.N = N; g.K = K; g.nb1 = 1; g.nb2 = 1;
+  g.A = A; g.B = B; g.C = C;
+  g.sAm = sAm; g.sAk = sAk; g.sBk = sBk; g.sBn = sBn; g.sCm = sCm; g.sCn = sCn;
+  g.alpha = 1.0; g.beta = 0.0;
+  return g;
+}
+
+static inline cudaError_t bgemm_launch(const BGemm& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.nb1 * g.nb2 <= 0) return cudaSuccess;
+  dim3 grid((g.N + GB_TN - 1) / GB_TN, (g.M + GB_TM - 1) / GB_TM, g.nb1 * g.nb2);
+  bgemm_kernel<<<grid, 128, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
+}  // namespace tp

@@ -1,12 +1,559 @@
-// Batched hSVD truncation of hierarchical Tucker tensors (ht.truncate) -- kernels follow.
+// Batched hierarchical-Tucker truncation by hSVD (ht.truncate, ht.py:313-372)
+// for sm_100a.
+//
+// Same truncation as the reference, computed in the Gramian gauge instead of
+// an explicit QR orthogonalization (ht.py:294-310):
+//   1. frame Grams, leaves -> root:  M_leaf = U^T U,  M_t = B_t^T (M_l (x) M_r) B_t
+//      (the root's 1x1 frame Gram is ||h||^2, ht.py:279-282);
+//   2. environment Grams in the original gauge, root -> leaves:
+//      Gh_l = sum B Gh_t M_r B^T,  Gh_r = sum B Gh_t M_l B^T;
+//   3. per non-root node: M_t = V L V^T (Jacobi), node Gram in the orthonormal
+//      gauge G_t = L^1/2 V^T Gh_t V L^1/2 (== the reference's node Gram up to an
+//      orthogonal change of basis, so the spectrum and the keep rule
+//      ht.py:346-359 are identical), G_t = W S W^T (Jacobi, descending);
+//   4. S_t = V L^+1/2 W[:, :keep] maps the old frame to the kept orthonormal
+//      one; projection U' = U S (leaves), B' = (S_l^T M_l (x) S_r^T M_r) B_t S_t
+//      (interior, ht.py:361-370).
+// Every contraction is a batched strided DMMA GEMM (tp_gemm.cuh); the batch runs
+// over tensors x tree nodes of one level wave.
 #include "tp_common.cuh"
+#include "tp_gemm.cuh"
+#include <cstring>
+#include <vector>
+
+namespace tp {
+
+struct Tree {
+  int n = 0, nleaf = 0, nint = 0, H = 0;
+  int parent[32], left[32], right[32], slot[32], height[32], depth[32], dims[32];
+};
+
+static int build_tree(Tree& T, int lo, int hi, int par, int dep) {
+  const int idx = T.n++;
+  T.parent[idx] = par;
+  T.depth[idx] = dep;
+  T.dims[idx] = hi - lo;
+  if (hi - lo == 1) {
+    T.left[idx] = T.right[idx] = -1;
+    T.slot[idx] = T.nleaf++;
+    T.height[idx] = 0;
+  } else {
+    T.slot[idx] = T.nint++;
+    const int half = (hi - lo) / 2;                 // left child takes the floor (ht.py:91)
+    T.left[idx] = build_tree(T, lo, lo + half, idx, dep + 1);
+    T.right[idx] = build_tree(T, lo + half, hi, idx, dep + 1);
+    const int h = 1 + (T.height[T.left[idx]] > T.height[T.right[idx]] ? T.height[T.left[idx]] : T.height[T.right[idx]]);
+    T.height[idx] = h;
+  }
+  if (T.height[idx] > T.H) T.H = T.height[idx];
+  return idx;
+}
+
+// ---------------------------------------------------------------------------
+// Batched cyclic Jacobi eigensolver for symmetric k x k matrices (k <= 64).
+// Round-robin (circle-method) ordering: each round rotates k/2 disjoint pairs
+// in parallel; rows, then columns and eigenvectors, are updated by all 256
+// threads.  Output: eigenvalues descending, eigenvectors as columns.
+// Matrix z lives at base index (z / per) * nn + first + z % per.
+// ---------------------------------------------------------------------------
+constexpr int JAC_NT = 256;
+
+__global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int first, int per, const double* Ain,
+                                                             double* Vout, double* wout, int max_sweeps) {
+  extern __shared__ double js[];
+  const int kp = k + (k & 1), ld = kp + 1;
+  double* a = js;
+  double* v = a + (size_t)kp * ld;
+  double* cs = v + (size_t)kp * ld;          // [kp/2][2]
+  int* pq = reinterpret_cast<int*>(cs + kp);  // [kp/2][2]
+  double* red = cs + 2 * kp;                  // [JAC_NT]
+  const int z = blockIdx.x;
+  const size_t base = (size_t)(z / per) * nn + first + z % per;
+  const double* in = Ain + base * k * k;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kp * kp; e += JAC_NT) {
+    const int i = e / kp, j = e % kp;
+    double x = 0.0;
+    if (i < k && j < k) x = 0.5 * (in[i * k + j] + in[j * k + i]);   // eigh(0.5 (G + G^T)), ht.py:347
+    a[i * ld + j] = x;
+    v[i * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int half = kp / 2;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    double off = 0.0, dia = 0.0;
+    for (int e = tid; e < kp * kp; e += JAC_NT) {
+      const int i = e / kp, j = e % kp;
+      const double x = a[i * ld + j];
+      if (i == j) dia += x * x; else off += x * x;
+    }
+    red[tid] = off;
+    __syncthreads();
+    for (int w = JAC_NT / 2; w > 0; w >>= 1) {
+      if (tid < w) red[tid] += red[tid + w];
+      __syncthreads();
+    }
+    off = red[0];
+    __syncthreads();
+    red[tid] = dia;
+    __syncthreads();
+    for (int w = JAC_NT / 2; w > 0; w >>= 1) {
+      if (tid < w) red[tid] += red[tid + w];
+      __syncthreads();
+    }
+    dia = red[0];
+    __syncthreads();
+    if (off <= 1e-32 * (off + dia) || off == 0.0) break;
+    for (int round = 0; round < kp - 1; ++round) {
+      if (tid < half) {
+        int p, q;
+        if (tid == 0) { p = round; q = kp - 1; }
+        else { p = (round + tid) % (kp - 1); q = (round - tid + kp - 1) % (kp - 1); }
+        if (p > q) { const int t = p; p = q; q = t; }
+        const double apq = a[p * ld + q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const double tau = (a[q * ld + q] - a[p * ld + p]) / (2.0 * apq);
+          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+        }
+        cs[2 * tid] = c; cs[2 * tid + 1] = s;
+        pq[2 * tid] = p; pq[2 * tid + 1] = q;
+      }
+      __syncthreads();
+      for (int e = tid; e < half * kp; e += JAC_NT) {      // rows p, q
+        const int pr = e / kp, j = e % kp;
+        const int p = pq[2 * pr], q = pq[2 * pr + 1];
+        const double c = cs[2 * pr], s = cs[2 * pr + 1];
+        const double x = a[p * ld + j], y = a[q * ld + j];
+        a[p * ld + j] = c * x - s * y;
+        a[q * ld + j] = s * x + c * y;
+      }
+      __syncthreads();
+      for (int e = tid; e < half * kp; e += JAC_NT) {      // columns p, q and eigenvectors
+        const int pr = e / kp, i = e % kp;
+        const int p = pq[2 * pr], q = pq[2 * pr + 1];
+        const double c = cs[2 * pr], s = cs[2 * pr + 1];
+        const double x = a[i * ld + p], y = a[i * ld + q];
+        a[i * ld + p] = c * x - s * y;
+        a[i * ld + q] = s * x + c * y;
+        const double vx = v[i * ld + p], vy = v[i * ld + q];
+        v[i * ld + p] = c * vx - s * vy;
+        v[i * ld + q] = s * vx + c * vy;
+      }
+      __syncthreads();
+    }
+  }
+  // sort descending (ties by index), write eigenvalues and eigenvector columns
+  double* Vo = Vout + base * k * k;
+  double* wo = wout + base * k;
+  int* rank = pq;   // reuse (kp/2*2 >= k ints)
+  __syncthreads();
+  if (tid < k) {
+    const double wi = a[tid * ld + tid];
+    int rk = 0;
+    for (int j = 0; j < k; ++j) {
+      const double wj = a[j * ld + j];
+      if (wj > wi || (wj == wi && j < tid)) ++rk;
+    }
+    rank[tid] = rk;
+    wo[rk] = wi;
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += JAC_NT) {
+    const int i = e / k, m = e % k;
+    Vo[i * k + rank[m]] = v[i * ld + m];
+  }
+}
+
+// G_t = diag(sqrt(l)) V^T Gh V diag(sqrt(l)) for every non-root node (one CTA each)
+__global__ void __launch_bounds__(256) form_g_kernel(int k, int nn, const double* Vm, const double* lam,
+                                                     const double* Gh, double* G) {
+  extern __shared__ double fs[];
+  const int z = blockIdx.x, per = nn - 1;
+  const size_t base = (size_t)(z / per) * nn + 1 + z % per;
+  const int ld = k + 1;
+  double* V = fs;
+  double* H = V + (size_t)k * ld;
+  double* P = H + (size_t)k * ld;
+  for (int e = threadIdx.x; e < k * k; e += 256) {
+    const int i = e / k, j = e % k;
+    V[i * ld + j] = Vm[base * k * k + e];
+    H[i * ld + j] = Gh[base * k * k + e];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += 256) {   // P = V^T H
+    const int m = e / k, j = e % k;
+    double acc = 0.0;
+    for (int i = 0; i < k; ++i) acc = fma(V[i * ld + m], H[i * ld + j], acc);
+    P[m * ld + j] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += 256) {   // G = P V, scaled
+    const int m = e / k, n = e % k;
+    double acc = 0.0;
+    for (int j = 0; j < k; ++j) acc = fma(P[m * ld + j], V[j * ld + n], acc);
+    const double sm = sqrt(fmax(lam[base * k + m], 0.0)), sn = sqrt(fmax(lam[base * k + n], 0.0));
+    G[base * k * k + e] = acc * sm * sn;
+  }
+}
+
+// keep rule (ht.py:349-358) per (tensor, non-root node); discarded mass; ranks
+__global__ void keep_rule_kernel(int k, int nn, int nb, int ndim, double eps, int r_max, const double* sig,
+                                 const double* Mf, int* keep, double* disc) {
+  const int z = blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = nn - 1;
+  if (z >= nb * per) return;
+  const int b = z / per, t = 1 + z % per;
+  const double total = sqrt(fmax(Mf[(size_t)b * nn * k * k], 0.0));
+  const double budget = (eps * total) * (eps * total) / (double)(2 * ndim - 3 > 1 ? 2 * ndim - 3 : 1);
+  const double* s = sig + ((size_t)b * nn + t) * k;
+  int kp = k;
+  double tail = 0.0;
+  while (kp > 1) {
+    const double step = fmax(s[kp - 1], 0.0);
+    if (kp > r_max || tail + step <= budget) { tail += step; --kp; }
+    else break;
+  }
+  keep[b * nn + t] = kp;
+  disc[b * nn + t] = tail;
+}
+
+__global__ void finish_kernel(int k, int nn, int nb, const double* Mf, const int* keep, const double* disc,
+                              double* est, double* norms, int* out_ranks) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  double s = 0.0;
+  for (int t = 1; t < nn; ++t) s += disc[b * nn + t];
+  est[b] = sqrt(fmax(s, 0.0));
+  norms[b] = sqrt(fmax(Mf[(size_t)b * nn * k * k], 0.0));
+  out_ranks[b * nn] = 1;
+  for (int t = 1; t < nn; ++t) out_ranks[b * nn + t] = keep[b * nn + t];
+}
+
+// S_t = V diag(l^+1/2) W[:, :keep] (k x ro, zero columns beyond keep); T_t = S_t^T M_t (ro x k)
+__global__ void __launch_bounds__(256) form_st_kernel(int k, int ro, int nn, const double* Vm, const double* lam,
+                                                      const double* Wg, const int* keep, const double* Mf,
+                                                      double* S, double* T) {
+  extern __shared__ double ss[];
+  const int z = blockIdx.x, per = nn - 1;
+  const size_t base = (size_t)(z / per) * nn + 1 + z % per;
+  const int kp = keep[base];
+  double* mu = ss;               // [k]
+  double* Sl = mu + k;           // [k][ro]
+  const double lmax = fmax(lam[base * k], 0.0);
+  for (int m = threadIdx.x; m < k; m += 256) {
+    const double l = lam[base * k + m];
+    mu[m] = (l > lmax * 1e-14 && l > 0.0) ? 1.0 / sqrt(l) : 0.0;
+  }
+  __syncthreads();
+  const double* V = Vm + base * k * k;
+  const double* W = Wg + base * k * k;
+  for (int e = threadIdx.x; e < k * ro; e += 256) {
+    const int i = e / ro, c = e % ro;
+    double acc = 0.0;
+    if (c < kp)
+      for (int m = 0; m < k; ++m) acc = fma(V[i * k + m] * mu[m], W[m * k + c], acc);
+    Sl[e] = acc;
+    S[base * k * ro + e] = acc;
+  }
+  __syncthreads();
+  const double* M = Mf + base * k * k;
+  for (int e = threadIdx.x; e < ro * k; e += 256) {
+    const int c = e / k, a2 = e % k;
+    double acc = 0.0;
+    for (int i = 0; i < k; ++i) acc = fma(Sl[i * ro + c], M[i * k + a2], acc);
+    T[base * ro * k + e] = acc;
+  }
+}
+
+// Bp[e][a][j] = B[a][e][j]  (k x k x kt per batch entry, offsets table)
+__global__ void transpose12_kernel(int k, int kt, const long long* offs, const double* B, double* Bp, long long sBp) {
+  const int z = blockIdx.y;
+  const double* src = B + offs[3 * z];
+  double* dst = Bp + z * sBp;
+  const int n = k * k * kt;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int a = e / (k * kt), r = e % (k * kt), b = r / kt, j = r % kt;
+    dst[(size_t)b * k * kt + a * kt + j] = src[e];
+  }
+}
+
+__global__ void set_root_env(int k, int nn, int nb, double* Gh) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) Gh[(size_t)b * nn * k * k] = 1.0;
+}
+
+struct HtPlan {
+  Tree T;
+  int d, Q, k, nb, ro, maxw;
+  size_t big, off_n, total;
+};
+
+static void plan_ht(int d, int Q, int k, int nb, int r_max, HtPlan& P) {
+  memset(&P.T, 0, sizeof(P.T));
+  build_tree(P.T, 0, d, -1, 0);
+  P.d = d; P.Q = Q; P.k = k; P.nb = nb;
+  P.ro = r_max < k ? r_max : k;
+  int maxw = 1;
+  for (int h = 1; h <= P.T.H; ++h) {
+    int c = 0;
+    for (int t = 0; t < P.T.n; ++t) if (P.T.left[t] >= 0 && P.T.height[t] == h) ++c;
+    maxw = c > maxw ? c : maxw;
+  }
+  for (int dp = 0; dp <= P.T.H; ++dp) {
+    int c = 0;
+    for (int t = 0; t < P.T.n; ++t) if (P.T.left[t] >= 0 && P.T.depth[t] == dp) ++c;
+    maxw = c > maxw ? c : maxw;
+  }
+  P.maxw = maxw;
+  const size_t k3 = (size_t)k * k * k;
+  size_t big = (size_t)nb * maxw * k3;
+  const size_t proj = (size_t)nb * P.T.nint * (size_t)k * k * P.ro;
+  P.big = big > proj ? big : proj;
+  const size_t nn = P.T.n, kk = (size_t)k * k;
+  P.off_n = (size_t)nb * (P.T.nleaf + P.T.nint) * 3 * 8 * 8;   // generous offset-table space
+  P.total = align_up(8 * nb * nn * kk) * 5 + align_up(8 * nb * nn * k) * 2 + align_up(8 * nb * nn * (size_t)k * P.ro) * 2 +
+            align_up(4 * nb * nn) + align_up(8 * nb * nn) + 3 * align_up(8 * P.big) + align_up(8 * P.off_n) + 256;
+}
+
+}  // namespace tp
+
+using namespace tp;
 
 extern "C" {
 
-size_t tp_ht_truncate_ws_bytes(int, int, int, int) { return 0; }
-int tp_ht_truncate_f64(int, int, int, int, const double*, const double*, int, double, double*, double*,
-                       int*, double*, double*, void*, size_t, void*) {
-  return TP_EUNSUPPORTED;
+size_t tp_ht_truncate_ws_bytes(int d, int Q, int k, int nb) {
+  if (d < 2 || d > 16 || Q < 1 || k < 1 || k > 64 || nb < 1) return 0;
+  HtPlan P;
+  plan_ht(d, Q, k, nb, k, P);
+  return P.total;
+}
+
+int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const double* transfers,
+                       int r_max, double eps, double* out_frames, double* out_transfers,
+                       int* out_ranks, double* est, double* norms,
+                       void* ws, size_t ws_bytes, void* stream) {
+  if (d < 2 || d > 16 || Q < 1 || k < 1 || nb < 1 || r_max < 1 || !(eps >= 0.0)) return TP_EINVAL;
+  if (!frames || !transfers || !out_frames || !out_transfers || !out_ranks || !est || !norms) return TP_EINVAL;
+  if (k > 64) return TP_EUNSUPPORTED;
+  HtPlan P;
+  plan_ht(d, Q, k, nb, r_max, P);
+  HtPlan P0;
+  plan_ht(d, Q, k, nb, k, P0);
+  if (!ws || ws_bytes < P0.total) return TP_EWORKSPACE;
+  const Tree& T = P.T;
+  const int nn = T.n, ro = P.ro;
+  const long long kk = (long long)k * k, k3 = kk * k;
+  cudaStream_t st = (cudaStream_t)stream;
+  Carver cv(ws, ws_bytes);
+  double* Mf = cv.take<double>((size_t)nb * nn * kk);
+  double* Gh = cv.take<double>((size_t)nb * nn * kk);
+  double* Vm = cv.take<double>((size_t)nb * nn * kk);
+  double* Wg = cv.take<double>((size_t)nb * nn * kk);
+  double* Gt = cv.take<double>((size_t)nb * nn * kk);
+  double* lam = cv.take<double>((size_t)nb * nn * k);
+  double* sig = cv.take<double>((size_t)nb * nn * k);
+  double* S = cv.take<double>((size_t)nb * nn * k * ro);
+  double* Tm = cv.take<double>((size_t)nb * nn * ro * k);
+  int* keep = cv.take<int>((size_t)nb * nn);
+  double* disc = cv.take<double>((size_t)nb * nn);
+  double* big1 = cv.take<double>(P0.big);
+  double* big2 = cv.take<double>(P0.big);
+  double* big3 = cv.take<double>(P0.big);
+  long long* doffs = cv.take<long long>(P0.off_n);
+  double* one = reinterpret_cast<double*>(cv.take<double>(1));
+  if (!cv.ok()) return TP_EWORKSPACE;
+
+  // all offset tables are built on the host and uploaded once
+  std::vector<long long> hoffs;
+  auto table = [&](const std::vector<long long>& v) {
+    const size_t at = hoffs.size();
+    hoffs.insert(hoffs.end(), v.begin(), v.end());
+    return at;
+  };
+  auto MF = [&](int b, int t) { return ((long long)b * nn + t) * kk; };
+  auto BT = [&](int b, int t) { return ((long long)b * T.nint + T.slot[t]) * k3; };
+  auto UF = [&](int b, int t) { return ((long long)b * T.nleaf + T.slot[t]) * (long long)Q * k; };
+
+  struct Call { BGemm g; size_t tab; int use_tab; };
+  std::vector<Call> calls;
+  std::vector<int> kinds;   // 0 = gemm, 1 = transpose(kt, tab, nb1), 2 = marker for non-gemm stage
+  struct Tr { int kt; size_t tab; int n; };
+  std::vector<Tr> trs;
+  std::vector<int> order;   // sequence of (kind) entries referencing calls / trs / stages
+  // stage ids: -1 eigh(M), -2 set_root_env, -3 form_g, -4 eigh(G), -5 keep, -6 form_st, -7 finish
+  auto add_gemm = [&](BGemm g, const std::vector<long long>& offs) {
+    Call c{g, 0, 0};
+    if (!offs.empty()) { c.tab = table(offs); c.use_tab = 1; c.g.nb1 = (int)(offs.size() / 3); }
+    calls.push_back(c);
+    order.push_back((int)calls.size() - 1);
+  };
+  auto add_stage = [&](int id) { order.push_back(id); };
+
+  // ---- 1. frame Grams, leaves -> root
+  {
+    std::vector<long long> o;
+    for (int b = 0; b < nb; ++b)
+      for (int t = 0; t < nn; ++t)
+        if (T.left[t] < 0) { o.push_back(UF(b, t)); o.push_back(UF(b, t)); o.push_back(MF(b, t)); }
+    add_gemm(bgemm_desc(k, k, Q, frames, 1, k, frames, k, 1, Mf, k, 1), o);
+  }
+  for (int h = 1; h <= T.H; ++h) {
+    std::vector<int> W;
+    for (int t = 0; t < nn; ++t) if (T.left[t] >= 0 && T.height[t] == h) W.push_back(t);
+    if (W.empty()) continue;
+    for (int kt : {k, 1}) {
+      std::vector<int> Wk;
+      for (int t : W) if ((t == 0 ? 1 : k) == kt) Wk.push_back(t);
+      if (Wk.empty()) continue;
+      std::vector<long long> o1, o2, o3;
+      int zz = 0;
+      for (int b = 0; b < nb; ++b)
+        for (int t : Wk) {
+          const long long zb = (long long)zz++ * k3;
+          o1.insert(o1.end(), {MF(b, T.left[t]), BT(b, t), zb});                 // T1 = M_l B
+          o2.insert(o2.end(), {MF(b, T.right[t]), zb, zb});                      // T2[c] = M_r T1[c]
+          o3.insert(o3.end(), {BT(b, t), zb, MF(b, t)});                         // M_t = B^T T2
+        }
+      BGemm g1 = bgemm_desc(k, k * kt, k, Mf, k, 1, transfers, (long long)k * kt, 1, big1, (long long)k * kt, 1);
+      add_gemm(g1, o1);
+      BGemm g2 = bgemm_desc(k, kt, k, Mf, k, 1, big1, kt, 1, big2, kt, 1);
+      g2.nb2 = k; g2.sA2 = 0; g2.sB2 = (long long)k * kt; g2.sC2 = (long long)k * kt;
+      add_gemm(g2, o2);
+      BGemm g3 = bgemm_desc(kt, kt, k * k, transfers, 1, kt, big2, kt, 1, Mf, kt, 1);
+      add_gemm(g3, o3);
+    }
+  }
+  add_stage(-1);   // eigh of frame Grams (non-root)
+  add_stage(-2);   // Gh_root = 1
+  // ---- 2. environment Grams, root -> leaves
+  for (int dp = 0; dp < T.H; ++dp) {
+    for (int kt : {k, 1}) {
+      std::vector<int> Wk;
+      for (int t = 0; t < nn; ++t)
+        if (T.left[t] >= 0 && T.depth[t] == dp && (t == 0 ? 1 : k) == kt) Wk.push_back(t);
+      if (Wk.empty()) continue;
+      std::vector<long long> oX, oY, oGl, oZ, oTr, oGr;
+      int zz = 0;
+      for (int b = 0; b < nb; ++b)
+        for (int t : Wk) {
+          const long long zb = (long long)zz++ * k3;
+          oX.insert(oX.end(), {BT(b, t), MF(b, t), zb});                          // X = B Gh_t
+          oY.insert(oY.end(), {MF(b, T.right[t]), zb, zb});                       // Y[a] = M_r X[a]
+          oGl.insert(oGl.end(), {zb, BT(b, t), MF(b, T.left[t])});                // Gh_l = Y B^T
+          oZ.insert(oZ.end(), {MF(b, T.left[t]), zb, zb});                        // Z'[b'] = M_l X[:, b', :]
+          oTr.insert(oTr.end(), {BT(b, t), 0, 0});
+          oGr.insert(oGr.end(), {zb, zb, MF(b, T.right[t])});                     // Gh_r = Z' Bp^T
+        }
+      const long long kkt = (long long)k * kt;
+      BGemm gX = bgemm_desc(k * k, kt, kt, transfers, kt, 1, Gh, kt, 1, big1, kt, 1);
+      add_gemm(gX, oX);
+      BGemm gY = bgemm_desc(k, kt, k, Mf, k, 1, big1, kt, 1, big2, kt, 1);
+      gY.nb2 = k; gY.sA2 = 0; gY.sB2 = kkt; gY.sC2 = kkt;
+      add_gemm(gY, oY);
+      BGemm gGl = bgemm_desc(k, k, k * kt, big2, kkt, 1, transfers, 1, kkt, Gh, k, 1);
+      add_gemm(gGl, oGl);
+      BGemm gZ = bgemm_desc(k, kt, k, Mf, k, 1, big1, kkt, 1, big2, kt, 1);
+      gZ.nb2 = k; gZ.sA2 = 0; gZ.sB2 = kt; gZ.sC2 = kkt;
+      add_gemm(gZ, oZ);
+      trs.push_back({kt, table(oTr), (int)(oTr.size() / 3)});
+      order.push_back(-100 - (int)(trs.size() - 1));
+      BGemm gGr = bgemm_desc(k, k, k * kt, big2, kkt, 1, big3, 1, kkt, Gh, k, 1);
+      add_gemm(gGr, oGr);
+    }
+  }
+  add_stage(-3);   // G_t = L^1/2 V^T Gh V L^1/2
+  add_stage(-4);   // eigh(G_t)
+  add_stage(-5);   // keep rule
+  add_stage(-6);   // S_t, T_t
+  add_stage(-7);   // est, norms, ranks
+  // ---- 4. projection
+  {
+    std::vector<long long> o;
+    for (int b = 0; b < nb; ++b)
+      for (int t = 0; t < nn; ++t)
+        if (T.left[t] < 0)
+          o.insert(o.end(), {UF(b, t), ((long long)b * nn + t) * k * ro, ((long long)b * T.nleaf + T.slot[t]) * Q * ro});
+    add_gemm(bgemm_desc(Q, ro, k, frames, k, 1, S, ro, 1, out_frames, ro, 1), o);
+  }
+  for (int kt : {k, 1}) {
+    const int rt = (kt == 1) ? 1 : ro;
+    std::vector<long long> o1, o2, o3;
+    int zz = 0;
+    for (int b = 0; b < nb; ++b)
+      for (int t = 0; t < nn; ++t) {
+        if (T.left[t] < 0 || (t == 0 ? 1 : k) != kt) continue;
+        const long long zb = (long long)zz++ * k * k * ro;
+        const long long sOff = ((long long)b * nn + t) * k * ro;
+        o1.insert(o1.end(), {BT(b, t), kt == 1 ? 0 : sOff, zb});                                  // X1 = B S_t
+        o2.insert(o2.end(), {((long long)b * nn + T.left[t]) * ro * k, zb, zb});                 // X2 = T_l X1
+        o3.insert(o3.end(), {((long long)b * nn + T.right[t]) * ro * k, zb,
+                             ((long long)b * T.nint + T.slot[t]) * (long long)ro * ro * ro});    // B'[c] = T_r X2[c]
+      }
+    if (o1.empty()) continue;
+    BGemm g1 = (kt == 1) ? bgemm_desc(k * k, 1, 1, transfers, 1, 1, one, 0, 0, big1, 1, 1)
+                         : bgemm_desc(k * k, ro, k, transfers, k, 1, S, ro, 1, big1, ro, 1);
+    add_gemm(g1, o1);
+    BGemm g2 = bgemm_desc(ro, k * rt, k, Tm, k, 1, big1, (long long)k * rt, 1, big2, (long long)k * rt, 1);
+    add_gemm(g2, o2);
+    BGemm g3 = bgemm_desc(ro, rt, k, Tm, k, 1, big2, rt, 1, out_transfers, rt, 1);
+    g3.nb2 = ro; g3.sA2 = 0; g3.sB2 = (long long)k * rt; g3.sC2 = (long long)ro * rt;
+    add_gemm(g3, o3);
+  }
+
+  if (hoffs.size() > P0.off_n) return TP_EWORKSPACE;
+  cudaError_t e = cudaMemcpyAsync(doffs, hoffs.data(), hoffs.size() * sizeof(long long), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  const double onev = 1.0;
+  e = cudaMemcpyAsync(one, &onev, sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  e = cudaMemsetAsync(Gh, 0, sizeof(double) * (size_t)nb * nn * kk, st);
+  if (e != cudaSuccess) return cuda_status(e);
+
+  const int kp = k + (k & 1);
+  const size_t jsm = sizeof(double) * ((size_t)2 * kp * (kp + 1) + 2 * kp + JAC_NT) + sizeof(int) * kp;
+  cudaFuncSetAttribute(jacobi_eigh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm);
+  const size_t fsm = sizeof(double) * 3 * (size_t)k * (k + 1);
+  cudaFuncSetAttribute(form_g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+  const size_t ssm = sizeof(double) * ((size_t)k + (size_t)k * ro);
+  const int nonroot = nb * (nn - 1);
+  for (int id : order) {
+    if (id >= 0) {
+      BGemm g = calls[id].g;
+      if (calls[id].use_tab) g.offs = doffs + calls[id].tab;
+      e = bgemm_launch(g, st);
+    } else if (id <= -100) {
+      const Tr& tr = trs[-100 - id];
+      dim3 grid(64, tr.n);
+      transpose12_kernel<<<grid, 256, 0, st>>>(k, tr.kt, doffs + tr.tab, transfers, big3, k3);
+      e = cudaGetLastError();
+    } else if (id == -1) {
+      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Mf, Vm, lam, 30);
+      e = cudaGetLastError();
+    } else if (id == -2) {
+      set_root_env<<<(nb + 127) / 128, 128, 0, st>>>(k, nn, nb, Gh);
+      e = cudaGetLastError();
+    } else if (id == -3) {
+      form_g_kernel<<<nonroot, 256, fsm, st>>>(k, nn, Vm, lam, Gh, Gt);
+      e = cudaGetLastError();
+    } else if (id == -4) {
+      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Gt, Wg, sig, 30);
+      e = cudaGetLastError();
+    } else if (id == -5) {
+      keep_rule_kernel<<<(nonroot + 127) / 128, 128, 0, st>>>(k, nn, nb, d, eps, r_max, sig, Mf, keep, disc);
+      e = cudaGetLastError();
+    } else if (id == -6) {
+      form_st_kernel<<<nonroot, 256, ssm, st>>>(k, ro, nn, Vm, lam, Wg, keep, Mf, S, Tm);
+      e = cudaGetLastError();
+    } else if (id == -7) {
+      finish_kernel<<<(nb + 127) / 128, 128, 0, st>>>(k, nn, nb, Mf, keep, disc, est, norms, out_ranks);
+      e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  return TP_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,143 @@
+"""GPU parity for the batched hSVD truncation (ht.truncate, ht.py:313-372) and the
+HT format operations, against the oracle (pinned to the reference by
+tests/golden/ht.npz).  Represented tensors are compared with the stable
+orthogonalisation-based metric (eigenvector gauge differs); bar 1e-9."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, unpack_ht
+from oracle import cp_als as ocp
+from oracle import ht_hsvd as oht
+from oracle import metrics
+
+pytestmark = pytest.mark.gpu
+
+from paper_1803_10270_b200 import cp, ht, operators  # noqa: E402
+from paper_1803_10270_b200.basis import BasisSpec  # noqa: E402
+
+TOL = 1e-9
+
+
+def specs(d, q):
+    return tuple(BasisSpec(q, math.pi, "collocation", lo=0.0) for _ in range(d))
+
+
+def random_ht(rng, d, q, k, scale=1.0):
+    nodes = oht.balanced_tree(d)
+    frames = [None] * len(nodes)
+    transfers = [None] * len(nodes)
+    for i, nd in enumerate(nodes):
+        if oht.is_leaf(nd):
+            frames[i] = scale * rng.standard_normal((q, k))
+        else:
+            transfers[i] = rng.standard_normal((k, k, 1 if i == 0 else k))
+    return nodes, frames, transfers
+
+
+def to_dev(d, q, o):
+    nodes, frames, transfers = o
+    return ht.HTTensor(specs(d, q), ht.balanced_tree(d), frames, transfers)
+
+
+def test_truncate_golden_cases():
+    g = load_golden("ht")
+    for name in g["names"]:
+        name = str(name)
+        d, q, rin, rmax, eps, est = g[f"{name}_meta"]
+        d, q = int(d), int(q)
+        nodes = oht.balanced_tree(d)
+        fin, tin = unpack_ht(g, f"{name}_in", nodes)
+        fout, tout = unpack_ht(g, f"{name}_out", nodes)
+        h = to_dev(d, q, (nodes, fin, tin))
+        red, my_est = ht.truncate(h, int(rmax), float(eps))
+        scale = max(1.0, float(g[f"{name}_norm_in"]))
+        assert abs(my_est - est) <= 1e-8 * scale, (name, my_est, est)
+        rel = metrics.ht_rel_diff((nodes, fout, tout), red.to_oracle())
+        assert rel <= TOL, (name, rel)
+        assert red.max_rank <= int(rmax)
+
+
+@pytest.mark.parametrize("d,q,k,rmax,eps", [(2, 9, 5, 3, 0.0), (3, 7, 6, 4, 0.0), (4, 10, 8, 3, 0.0),
+                                            (5, 6, 7, 7, 1e-2), (6, 12, 9, 4, 0.0), (7, 8, 6, 2, 0.0),
+                                            (8, 16, 12, 5, 0.0), (8, 20, 16, 16, 1e-3)])
+def test_truncate_matches_oracle(d, q, k, rmax, eps):
+    rng = np.random.default_rng(d * 100 + k)
+    o = random_ht(rng, d, q, k)
+    red, est = ht.truncate(to_dev(d, q, o), rmax, eps)
+    ref, oest = oht.truncate(o, rmax, eps)
+    assert abs(est - oest) <= 1e-8 * max(1.0, oht.norm(o)), (est, oest)
+    assert metrics.ht_rel_diff(ref, red.to_oracle()) <= TOL
+    assert red.max_rank <= rmax
+
+
+def test_truncate_batch_equals_individual():
+    rng = np.random.default_rng(5)
+    d, q, k = 6, 10, 8
+    os_ = [random_ht(rng, d, q, k) for _ in range(5)]
+    outs, ests = ht.truncate_batch([to_dev(d, q, o) for o in os_], 3, 0.0)
+    for o, out, e in zip(os_, outs, ests):
+        ref, oest = oht.truncate(o, 3, 0.0)
+        assert abs(e - oest) <= 1e-8 * max(1.0, oht.norm(o))
+        assert metrics.ht_rel_diff(ref, out.to_oracle()) <= TOL
+
+
+def test_truncate_config4_shape():
+    """BASELINE config 4 sizes (d=8, Q=128, ranks 64 -> 16, eps=0) on two tensors."""
+    rng = np.random.default_rng(0)
+    d, q, k = 8, 128, 64
+    os_ = [random_ht(rng, d, q, k) for _ in range(2)]
+    outs, ests = ht.truncate_batch([to_dev(d, q, o) for o in os_], 16, 0.0)
+    for o, out, e in zip(os_, outs, ests):
+        ref, oest = oht.truncate(o, 16, 0.0)
+        assert abs(e - oest) <= 1e-9 * oht.norm(o)
+        rel = metrics.ht_rel_diff(ref, out.to_oracle())
+        assert rel <= TOL, rel
+        assert out.max_rank == 16
+
+
+def test_truncate_inflated_rank_is_exact():
+    """ht.add(h, h) doubles ranks without content (reference test_ht.py:153-163)."""
+    rng = np.random.default_rng(3)
+    d, q = 4, 9
+    f = [rng.standard_normal((q, 2)) for _ in range(d)]
+    h = ht.from_cp(cp.CPTensor(specs(d, q), f))
+    red, est = ht.truncate(ht.add(h, h), 2, 0.0)
+    assert red.max_rank <= 2
+    assert est < 1e-6
+    ref = oht.scale(oht.from_cp(f), 2.0)
+    assert metrics.ht_rel_diff(ref, red.to_oracle()) <= 1e-8
+
+
+def test_norm_and_inner_product():
+    rng = np.random.default_rng(11)
+    d, q = 5, 7
+    o1, o2 = random_ht(rng, d, q, 4), random_ht(rng, d, q, 3)
+    h1, h2 = to_dev(d, q, o1), to_dev(d, q, o2)
+    n1 = oht.norm(o1)
+    assert abs(ht.norm(h1) - n1) <= 1e-12 * n1
+    ip = oht.inner_product(o1, o2).real
+    assert abs(ht.inner_product(h1, h2) - ip) <= 1e-10 * oht.norm(o1) * oht.norm(o2)
+
+
+def test_from_cp_add_scale_apply():
+    rng = np.random.default_rng(12)
+    d, q = 3, 8
+    S = specs(d, q)
+    f = [rng.standard_normal((q, 3)) for _ in range(d)]
+    g = [rng.standard_normal((q, 2)) for _ in range(d)]
+    h = ht.add(ht.from_cp(cp.CPTensor(S, f)), ht.scale(ht.from_cp(cp.CPTensor(S, g)), -0.5))
+    ref = oht.add(oht.from_cp(f), oht.scale(oht.from_cp(g), -0.5))
+    assert metrics.ht_rel_diff(ref, h.to_oracle()) <= 1e-13
+    assert abs(ht.norm(h) - oht.norm(ref)) <= 1e-12 * oht.norm(ref)
+    L = operators.advection_operator((1.0, 0.5, -0.75), S)
+    out = ht.apply_operator(L, ht.from_cp(cp.CPTensor(S, f)))
+    from paper_1803_10270_b200.basis import FactorKind, factor_matrix
+    D = factor_matrix(S[0], FactorKind.DERIVATIVE)
+    mats = [[D if k == t else None for k in range(d)] for t in range(d)]
+    from oracle import operators as oops
+    ref_cp = oops.apply([-1.0, -0.5, 0.75], mats, f)
+    assert metrics.ht_rel_diff(oht.from_cp(ref_cp), out.to_oracle()) <= 1e-12
+    _ = ocp
