@@ -80,70 +80,63 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int 
   }
   __syncthreads();
   const int half = kp / 2;
+  // fixed per-thread work split: pair = tid % half, element lane j0 = tid / half
+  const int my_pair = tid % half, stride = JAC_NT / half, j0 = tid / half;
+  const bool active = j0 < stride && tid < half * stride;
+  int* flag = reinterpret_cast<int*>(red);
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    double off = 0.0, dia = 0.0;
-    for (int e = tid; e < kp * kp; e += JAC_NT) {
-      const int i = e / kp, j = e % kp;
-      const double x = a[i * ld + j];
-      if (i == j) dia += x * x; else off += x * x;
-    }
-    red[tid] = off;
+    if (tid == 0) flag[0] = 0;
     __syncthreads();
-    for (int w = JAC_NT / 2; w > 0; w >>= 1) {
-      if (tid < w) red[tid] += red[tid + w];
-      __syncthreads();
-    }
-    off = red[0];
-    __syncthreads();
-    red[tid] = dia;
-    __syncthreads();
-    for (int w = JAC_NT / 2; w > 0; w >>= 1) {
-      if (tid < w) red[tid] += red[tid + w];
-      __syncthreads();
-    }
-    dia = red[0];
-    __syncthreads();
-    if (off <= 1e-32 * (off + dia) || off == 0.0) break;
     for (int round = 0; round < kp - 1; ++round) {
       if (tid < half) {
         int p, q;
         if (tid == 0) { p = round; q = kp - 1; }
         else { p = (round + tid) % (kp - 1); q = (round - tid + kp - 1) % (kp - 1); }
         if (p > q) { const int t = p; p = q; q = t; }
-        const double apq = a[p * ld + q];
+        const double apq = a[p * ld + q], app = a[p * ld + p], aqq = a[q * ld + q];
         double c = 1.0, s = 0.0;
-        if (apq != 0.0) {
-          const double tau = (a[q * ld + q] - a[p * ld + p]) / (2.0 * apq);
+        // threshold Jacobi: rotate only if a_pq is not negligible against the
+        // diagonal (relative accuracy criterion) -- a sweep without rotations
+        // means convergence
+        if (fabs(apq) > 1e-300 && fabs(apq) > 1e-16 * sqrt(fabs(app) * fabs(aqq))) {
+          const double tau = (aqq - app) / (2.0 * apq);
           const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + t * t);
           s = t * c;
+          flag[0] = 1;
         }
         cs[2 * tid] = c; cs[2 * tid + 1] = s;
         pq[2 * tid] = p; pq[2 * tid + 1] = q;
       }
       __syncthreads();
-      for (int e = tid; e < half * kp; e += JAC_NT) {      // rows p, q
-        const int pr = e / kp, j = e % kp;
-        const int p = pq[2 * pr], q = pq[2 * pr + 1];
-        const double c = cs[2 * pr], s = cs[2 * pr + 1];
-        const double x = a[p * ld + j], y = a[q * ld + j];
-        a[p * ld + j] = c * x - s * y;
-        a[q * ld + j] = s * x + c * y;
+      if (active) {                                           // rows p, q
+        const int p = pq[2 * my_pair], q = pq[2 * my_pair + 1];
+        const double c = cs[2 * my_pair], s = cs[2 * my_pair + 1];
+        if (s != 0.0)
+          for (int j = j0; j < kp; j += stride) {
+            const double x = a[p * ld + j], y = a[q * ld + j];
+            a[p * ld + j] = c * x - s * y;
+            a[q * ld + j] = s * x + c * y;
+          }
       }
       __syncthreads();
-      for (int e = tid; e < half * kp; e += JAC_NT) {      // columns p, q and eigenvectors
-        const int pr = e / kp, i = e % kp;
-        const int p = pq[2 * pr], q = pq[2 * pr + 1];
-        const double c = cs[2 * pr], s = cs[2 * pr + 1];
-        const double x = a[i * ld + p], y = a[i * ld + q];
-        a[i * ld + p] = c * x - s * y;
-        a[i * ld + q] = s * x + c * y;
-        const double vx = v[i * ld + p], vy = v[i * ld + q];
-        v[i * ld + p] = c * vx - s * vy;
-        v[i * ld + q] = s * vx + c * vy;
+      if (active) {                                           // columns p, q and eigenvectors
+        const int p = pq[2 * my_pair], q = pq[2 * my_pair + 1];
+        const double c = cs[2 * my_pair], s = cs[2 * my_pair + 1];
+        if (s != 0.0)
+          for (int i = j0; i < kp; i += stride) {
+            const double x = a[i * ld + p], y = a[i * ld + q];
+            a[i * ld + p] = c * x - s * y;
+            a[i * ld + q] = s * x + c * y;
+            const double vx = v[i * ld + p], vy = v[i * ld + q];
+            v[i * ld + p] = c * vx - s * vy;
+            v[i * ld + q] = s * vx + c * vy;
+          }
       }
       __syncthreads();
     }
+    if (flag[0] == 0) break;
+    __syncthreads();
   }
   // sort descending (ties by index), write eigenvalues and eigenvector columns
   double* Vo = Vout + base * k * k;
