@@ -86,3 +86,31 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(RuntimeError, match="CUDA device"):
         _lib.device()
     _ = ctypes
+
+
+def test_explicit_config_validation():
+    from paper_1803_10270_b200 import explicit
+    with pytest.raises(ValueError, match="dt"):
+        explicit.ExplicitConfig(dt=0.0, r_max=2)
+    with pytest.raises(ValueError, match="rank cap"):
+        explicit.ExplicitConfig(dt=0.1, r_max=0)
+    with pytest.raises(ValueError, match="format"):
+        explicit.ExplicitConfig(dt=0.1, r_max=2, format="tucker")
+    with pytest.raises(ValueError, match="startup"):
+        explicit.ExplicitConfig(dt=0.1, r_max=2, startup="euler")
+    with pytest.raises(ValueError, match="recipe"):
+        explicit.ExplicitConfig(dt=0.1, r_max=2, recipe="magic")
+
+
+def test_bgk_projection_is_exact_on_grid():
+    from paper_1803_10270_b200 import workloads
+    W, M, v, w = workloads.bgk_operator_terms(8, 10)
+    assert len(W) == 24
+    Pv = None
+    for wt, row in zip(W[4:], M[4:]):
+        t = wt * np.kron(np.kron(row[3], row[4]), row[5])
+        Pv = t if Pv is None else Pv + t
+    assert np.abs(Pv @ Pv - Pv).max() < 1e-13
+    M1 = workloads.maxwellian_1d(v)
+    mv = np.kron(np.kron(M1, M1), M1)
+    assert np.abs(Pv @ mv - mv).max() < 1e-13

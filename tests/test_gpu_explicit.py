@@ -1,0 +1,145 @@
+"""GPU parity of the explicit integrator (explicit.py:85-103) with device truncation,
+against the oracle (pinned by tests/golden/explicit.npz).  Per-truncation bar
+1e-9 (teacher forcing: the GPU truncation gets the oracle's exact input and
+init), final-solution bar 1e-8 (BASELINE north star)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, unpack_cp
+from oracle import explicit as oex
+from oracle import metrics
+
+pytestmark = pytest.mark.gpu
+
+from paper_1803_10270_b200 import cp, explicit, ht, operators, workloads  # noqa: E402
+from paper_1803_10270_b200.basis import fourier_diff_matrix  # noqa: E402
+from paper_1803_10270_b200.basis import BasisSpec  # noqa: E402
+
+
+def col_specs(d, q):
+    return tuple(BasisSpec(q, math.pi, "collocation", lo=0.0) for _ in range(d))
+
+
+def adv_op(S, D, a):
+    d = len(S)
+    return operators.SeparableOperator(S, tuple(-np.asarray(a)), tuple(tuple(D if k == t else None for k in range(d))
+                                                                      for t in range(d)))
+
+
+def test_fused_trajectory_golden():
+    g = load_golden("explicit")
+    q, d, r, dt, steps, sweeps, lam = g["meta"]
+    q, d, r, steps, sweeps = int(q), int(d), int(r), int(steps), int(sweeps)
+    S = col_specs(d, q)
+    L = adv_op(S, g["D"], g["a"])
+    cfg = explicit.ExplicitConfig(dt=float(dt), r_max=r, recipe="fused",
+                                  als=cp.ALSApproxConfig(max_sweeps=sweeps, stall=-np.inf, reg=float(lam)))
+    f0 = cp.CPTensor(S, unpack_cp(g, "step0"))
+    got = {}
+    explicit.run(f0, L, cfg, steps, callback=lambda n, f: got.__setitem__(n, f.to_numpy()))
+    for n in range(1, steps + 1):
+        rel = metrics.cp_rel_diff(unpack_cp(g, f"step{n}"), got[n])
+        assert rel <= 1e-8, (n, rel)
+    # same through the per-step API
+    f1 = explicit.startup_step(f0, L, cfg)
+    assert metrics.cp_rel_diff(unpack_cp(g, "step1"), f1.to_numpy()) <= 1e-9
+    f2 = explicit.ab2_step(f0, f1, L, cfg)
+    assert metrics.cp_rel_diff(unpack_cp(g, "step2"), f2.to_numpy()) <= 1e-8
+
+
+def _cfg0_setup(steps):
+    w = workloads.cfg0(0)
+    S = w["specs"]
+    L = adv_op(S, w["D"], w["a"])
+    cfg = explicit.ExplicitConfig(dt=w["dt"], r_max=w["r"], recipe="fused",
+                                  als=cp.ALSApproxConfig(max_sweeps=w["sweeps"], stall=-np.inf, reg=w["lam"]))
+    mats = [[w["D"] if k == t else None for k in range(6)] for t in range(6)]
+    return w, S, L, cfg, mats
+
+
+def test_config0_teacher_forced_truncations():
+    w, S, L, cfg, mats = _cfg0_setup(8)
+    f0 = w["ic"]["factors"]
+    red = oex.warm_als_reducer(w["sweeps"], w["lam"])
+    prev, cur = f0, oex.startup_fused(f0, list(-np.asarray(w["a"])), mats, w["dt"], w["r"], red)
+    for n in range(2, 8):
+        target = oex.ab2_target(prev, cur, list(-np.asarray(w["a"])), mats, w["dt"])
+        ref = red(target, cur)
+        got = cp.cp_approx_als(cp.CPTensor(S, target), w["r"], cfg.als, init=cp.CPTensor(S, cur))
+        rel = metrics.cp_rel_diff(ref, got.to_numpy())
+        assert rel <= 1e-9, (n, rel)
+        # the device AB2 target matches the oracle's exactly (same column order)
+        tgt = explicit.ab2_target(cp.CPTensor(S, prev), cp.CPTensor(S, cur), L, w["dt"])
+        assert metrics.cp_rel_diff(target, tgt.to_numpy()) <= 1e-14
+        prev, cur = cur, ref
+
+
+def test_config0_full_trajectory():
+    """100 steps of BASELINE config 0; final solution vs oracle <= 1e-8 and vs the
+    exact shifted solution within the oracle's own truncation error (+10%)."""
+    w, S, L, cfg, mats = _cfg0_setup(100)
+    f0 = w["ic"]["factors"]
+    out = explicit.run(cp.CPTensor(S, f0), L, cfg, w["steps"])
+    ref = oex.run_fused(f0, list(-np.asarray(w["a"])), mats, w["dt"], w["r"], w["steps"], w["sweeps"], w["lam"])
+    rel = metrics.cp_rel_diff(ref, out.to_numpy())
+    assert rel <= 1e-8, rel
+    exact = workloads.advection_exact(w["ic"], w["steps"] * w["dt"])
+    e_ref = metrics.cp_rel_diff(exact, ref)
+    e_gpu = metrics.cp_rel_diff(exact, out.to_numpy())
+    assert e_gpu <= 1.1 * e_ref + 1e-12, (e_gpu, e_ref)
+    assert e_ref < 5e-3
+
+
+def test_config3_short_trajectory():
+    w = workloads.cfg3(0)
+    S = w["specs"]
+    L = operators.SeparableOperator(S, tuple(w["weights"]), tuple(tuple(m) for m in w["mats"]))
+    cfg = explicit.ExplicitConfig(dt=w["dt"], r_max=w["r"], recipe="fused",
+                                  als=cp.ALSApproxConfig(max_sweeps=w["sweeps"], stall=-np.inf, reg=w["lam"]))
+    steps = 6
+    out = explicit.run(cp.CPTensor(S, w["factors"]), L, cfg, steps)
+    ref = oex.run_fused(w["factors"], w["weights"], w["mats"], w["dt"], w["r"], steps, w["sweeps"], w["lam"])
+    rel = metrics.cp_rel_diff(ref, out.to_numpy())
+    assert rel <= 1e-8, rel
+
+
+def test_split_recipe_matches_dense_formula_when_untruncated():
+    """Rank cap above need: every reduction is a no-op (reference test_explicit.py:35-52)."""
+    rng = np.random.default_rng(2)
+    d, q = 3, 8
+    S = col_specs(d, q)
+    D = fourier_diff_matrix(q)
+    L = adv_op(S, D, (1.0, 0.5, -0.75))
+    f0 = [rng.standard_normal((q, 2)) for _ in range(d)]
+    f1 = [rng.standard_normal((q, 2)) for _ in range(d)]
+    cfg = explicit.ExplicitConfig(dt=1e-3, r_max=1000)
+    out = explicit.ab2_step(cp.CPTensor(S, f0), cp.CPTensor(S, f1), L, cfg)
+    mats = [[D if k == t else None for k in range(d)] for t in range(d)]
+    ref = oex.ab2_target(f0, f1, [-1.0, -0.5, 0.75], mats, 1e-3)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= 1e-13
+    # HT format through the same API
+    h0, h1 = ht.from_cp(cp.CPTensor(S, f0)), ht.from_cp(cp.CPTensor(S, f1))
+    cfg_ht = explicit.ExplicitConfig(dt=1e-3, r_max=1000, format="ht")
+    out_h = explicit.ab2_step(h0, h1, L, cfg_ht)
+    from oracle import ht_hsvd as oht
+    assert metrics.ht_rel_diff(oht.from_cp(ref), out_h.to_oracle()) <= 1e-12
+
+
+def test_reduction_log_and_validation():
+    rng = np.random.default_rng(4)
+    d, q = 3, 8
+    S = col_specs(d, q)
+    L = adv_op(S, fourier_diff_matrix(q), (1.0, 0.5, -0.75))
+    f0 = cp.CPTensor(S, [rng.standard_normal((q, 1)) for _ in range(d)])
+    f1 = cp.CPTensor(S, [rng.standard_normal((q, 1)) for _ in range(d)])
+    log = []
+    out = explicit.ab2_step(f0, f1, L, explicit.ExplicitConfig(dt=1e-3, r_max=2), log=log)
+    assert [r.stage for r in log] == ["difference", "operator", "update"]
+    assert explicit.tensor_rank(out) <= 2
+    assert log[0].rank_before == 2 and log[0].error == 0.0
+    assert log[1].rank_before == 6 and log[1].rank_after <= 2
+    with pytest.raises(TypeError, match="same tensor format"):
+        explicit.ab2_step(f0, ht.from_cp(f1), L, explicit.ExplicitConfig(dt=1e-3, r_max=4))
