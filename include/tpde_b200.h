@@ -120,20 +120,28 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
                        void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
- * Fixed-rank implicit ALS step (implicit.step, implicit.py:222-301) for a
- * pair A = sum_e eta_e (x)_k A_{e,k}, B = sum_z zeta_z (x)_k A_{z,k} with
- * shared dense factors; Gauss-Seidel schedule, direct regularised solve
- * (M_q + lam I) x = gamma_q by blocked Cholesky.
- *   pairs : device, d x ra x ra x (Q x Q): pairs[k][e][z] = A_{e,k}^T A_{z,k}
- *   f_old : device CP (rank r), f_new: device CP in/out (initial iterate = f_old)
- *   orientation: 0 = corrected normal equations, 1 = reference build_gamma
- *                (implicit.py:137-139)
+ * Fixed-rank implicit ALS step (implicit.step, implicit.py:222-301) for an
+ * operator pair A = sum_e eta_e (x)_k F_{e,k}, B = sum_z zeta_z (x)_k F_{z,k}
+ * with uniform mode size Q.  Replaces build_M (implicit.py:125-131),
+ * build_gamma (134-153), solve_beta (156-164: LSQR -> direct regularised
+ * Cholesky solve of (M_q + lam I) x = gamma_q) and converged (167-177).
+ *   tabs    : device, n_tab x (Q x Q): distinct pairing tables
+ *   tab_id  : host, d x ra x ra: tab_id[(k*ra + e)*ra + z] = index of
+ *             pairs[k][e][z] = F_{e,k}^T F_{z,k} in tabs
+ *   KL, KR  : host ra x ra: eta eta^T and eta zeta^T (implicit.py:106-108)
+ *   f_old   : device CP (rank r, d blocks Q x r); f_new: device CP in/out
+ *             (initial iterate; the step's result on exit)
+ *   schedule: 0 Gauss-Seidel, 1 Jacobi; delta_beta damping (implicit.py:281-282)
+ *   orientation: 0 corrected normal equations, 1 reference build_gamma
+ *             (implicit.py:137-139)
+ *   eps_conv: device double (last sweep's largest relative update)
+ *   info    : device int[2] {status bits, sweeps done}
  * ------------------------------------------------------------------------- */
-size_t tp_implicit_ws_bytes(int d, int Q, int r, int ra);
-int tp_implicit_step_f64(int d, int Q, int r, int ra, const double* pairs, const double* eta,
-                         const double* zeta, const double* f_old, double* f_new,
-                         int sweeps, double delta_beta, double lam, int orientation,
-                         double* eps_conv, int* info, void* ws, size_t ws_bytes, void* stream);
+size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab);
+int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* tabs, const int* tab_id,
+                         const double* KL, const double* KR, const double* f_old, double* f_new,
+                         int sweeps, int schedule, double delta_beta, double eps_tol, double lam,
+                         int orientation, double* eps_conv, int* info, void* ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,422 @@
+// Fixed-rank implicit ALS step (implicit.step, implicit.py:222-301) for sm_100a.
+//
+// Per mode update q (Gauss-Seidel or Jacobi schedule):
+//   term Grams  G[k][t] = b_new,k^T T_t b_new,k and the mixed Grams for the
+//               right-hand side (cached per mode, refreshed after each update)
+//               -> two batched DMMA GEMMs per refresh;
+//   H_X[j][i]  = sum_{(e,z): pairs[q][e][z] = X} KL[e,z] prod_{k!=q} G[k][t(k,e,z)][j][i]
+//   M_q        = sum_X H_X^T (x) T_X^T + lam I      (implicit.py:125-131, grouped by
+//               distinct mode-q table so the dense (rQ)^2 assembly costs n_X FMAs/entry)
+//   gamma_q    = sum_X Hg_X (T~_X b_old,q)           (implicit.py:134-139; T~ = T for
+//               the corrected normal equations, T^T for the reference orientation)
+//   (M_q) x = gamma_q by a hand-written blocked right-looking Cholesky
+//               (64x64 diagonal blocks factored + inverted in shared memory, panel
+//               TRSM and trailing SYRK as DMMA GEMMs), then blocked substitution.
+// After each sweep: largest relative raw update (implicit.py:167-177) and the
+// damped update b <- b_int + (b - b_int)/delta_beta (implicit.py:281-282).
+#include "tp_common.cuh"
+#include "tp_gemm.cuh"
+#include <cstring>
+#include <vector>
+
+namespace tp {
+
+constexpr int IM_MAXD = 8, IM_MAXRA = 16, IM_MAXT = 64;
+constexpr int CH_NB = 64;   // Cholesky block size
+
+struct HArgs {
+  int d, ra, r, q, n_tab, nX;
+  int tab[IM_MAXD * IM_MAXRA * IM_MAXRA];
+  int xs[IM_MAXT];           // distinct table ids used by mode q
+  double KL[IM_MAXRA * IM_MAXRA], KR[IM_MAXRA * IM_MAXRA];
+  const double* G;           // [d][n_tab][r][r]
+  const double* Gm;          // [d][n_tab][r][r]
+  double* H;                 // [nX][r][r]  (stored [j][i] as in the reference einsum)
+  double* Hg;                // [nX][r][r]  ([i][j])
+};
+
+// H and Hg for the distinct tables of mode q: one CTA per distinct table
+__global__ void __launch_bounds__(256) form_h_kernel(const __grid_constant__ HArgs a) {
+  const int x = blockIdx.x, X = a.xs[x], r = a.r, rr = r * r;
+  for (int e2 = threadIdx.x; e2 < rr; e2 += 256) {
+    double h = 0.0, hg = 0.0;
+    for (int e = 0; e < a.ra; ++e)
+      for (int z = 0; z < a.ra; ++z) {
+        if (a.tab[(a.q * a.ra + e) * a.ra + z] != X) continue;
+        double p = 1.0, pg = 1.0;
+        for (int k = 0; k < a.d; ++k) {
+          if (k == a.q) continue;
+          const int t = a.tab[(k * a.ra + e) * a.ra + z];
+          p *= a.G[((size_t)k * a.n_tab + t) * rr + e2];
+          pg *= a.Gm[((size_t)k * a.n_tab + t) * rr + e2];
+        }
+        h += a.KL[e * a.ra + z] * p;
+        hg += a.KR[e * a.ra + z] * pg;
+      }
+    a.H[(size_t)x * rr + e2] = h;     // e2 = j*r + i : H_X[j][i]
+    a.Hg[(size_t)x * rr + e2] = hg;   // e2 = i*r + j : Hg_X[i][j]
+  }
+}
+
+// gamma[i*Q + a] = sum_X sum_j Hg_X[i][j] W[q][X][a][j]
+__global__ void gamma_kernel(int Q, int r, int nX, const int* __restrict__ xs_dev, const double* Hg, const double* W,
+                             int n_tab, int q, double* gam, int N) {
+  const int n = r * Q;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N; e += gridDim.x * blockDim.x) {
+    if (e >= n) { gam[e] = 0.0; continue; }
+    const int i = e / Q, aa = e % Q;
+    double acc = 0.0;
+    for (int x = 0; x < nX; ++x) {
+      const int X = xs_dev[x];
+      const double* w = W + (((size_t)q * n_tab + X) * Q + aa) * r;
+      const double* hg = Hg + (size_t)x * r * r + (size_t)i * r;
+      for (int j = 0; j < r; ++j) acc = fma(hg[j], w[j], acc);
+    }
+    gam[e] = acc;
+  }
+}
+
+struct AsmArgs {
+  int Q, r, nX, N;   // N = padded system size (multiple of the Cholesky block)
+  int xs[IM_MAXT];
+  const double* tabs;
+  const double* H;
+  double* M;
+  double lam;
+};
+
+// M[(i,a),(j,c)] = sum_X H_X[j][i] T_X[c][a] + lam delta   (rank-major, mode-minor blocks)
+__global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ AsmArgs a) {
+  const int Q = a.Q, r = a.r, n = r * Q, N = a.N;
+  const long long tot = (long long)N * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(e / N), col = (int)(e % N);
+    if (row >= n || col >= n) {   // decoupled identity padding
+      a.M[e] = (row == col) ? 1.0 : 0.0;
+      continue;
+    }
+    const int i = row / Q, aa = row % Q, j = col / Q, c = col % Q;
+    double acc = (row == col) ? a.lam : 0.0;
+    for (int x = 0; x < a.nX; ++x)
+      acc = fma(a.H[(size_t)x * r * r + j * r + i], a.tabs[((size_t)a.xs[x] * Q + c) * Q + aa], acc);
+    a.M[e] = acc;
+  }
+}
+
+// Cholesky of the nb x nb diagonal block at (k0, k0) of the row-major n x n matrix A
+// (lower triangle), in shared memory; writes L back and L^-1 into Linv (nb x nb).
+__global__ void __launch_bounds__(256) potrf_diag_kernel(double* A, int n, int k0, int nb, double* Linv, int* info) {
+  extern __shared__ double pds[];
+  double (*L)[CH_NB + 1] = reinterpret_cast<double (*)[CH_NB + 1]>(pds);
+  double (*X)[CH_NB + 1] = reinterpret_cast<double (*)[CH_NB + 1]>(pds + CH_NB * (CH_NB + 1));
+  const int tid = threadIdx.x;
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int i = e / nb, j = e % nb;
+    L[i][j] = (j <= i) ? A[(size_t)(k0 + i) * n + k0 + j] : 0.0;
+  }
+  __syncthreads();
+  int bad = 0;
+  for (int j = 0; j < nb; ++j) {
+    const double djj = L[j][j];
+    if (!(djj > 0.0) || !isfinite(djj)) bad = 1;
+    const double d = sqrt(fabs(djj));
+    const double inv = 1.0 / d;
+    __syncthreads();
+    if (tid == 0) L[j][j] = d;
+    for (int i = j + 1 + tid; i < nb; i += 256) L[i][j] *= inv;
+    __syncthreads();
+    const int m = nb - j - 1;
+    for (int e = tid; e < m * m; e += 256) {
+      const int i = j + 1 + e / m, c = j + 1 + e % m;
+      if (c <= i) L[i][c] = fma(-L[i][j], L[c][j], L[i][c]);
+    }
+    __syncthreads();
+  }
+  if (bad && tid == 0) atomicOr(info, 1);
+  // X = L^-1 by column-parallel forward substitution
+  if (tid < nb) {
+    const int c = tid;
+    for (int i = 0; i < nb; ++i) {
+      double acc = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) acc = fma(-L[i][k], X[k][c], acc);
+      X[i][c] = (i < c) ? 0.0 : acc / L[i][i];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int i = e / nb, j = e % nb;
+    if (j <= i) A[(size_t)(k0 + i) * n + k0 + j] = L[i][j];
+    Linv[e] = X[i][j];
+  }
+}
+
+// Solve L L^T x = b with the blocked factor (diagonal inverses in Linv); one CTA.
+__global__ void __launch_bounds__(256) potrs_kernel(const double* A, int n, const double* Linv, const double* b,
+                                                    double* x, double* y) {
+  __shared__ double part[256];
+  __shared__ double blk[CH_NB];
+  const int tid = threadIdx.x, nbk = n / CH_NB;
+  // forward: y_k = Linv_k (b_k - sum_{j<k} L_kj y_j)
+  for (int k = 0; k < nbk; ++k) {
+    const int r0 = k * CH_NB;
+    // partial sums: 4 threads per row
+    const int row = tid >> 2, sub = tid & 3;
+    double acc = 0.0;
+    for (int c = sub; c < r0; c += 4) acc = fma(A[(size_t)(r0 + row) * n + c], y[c], acc);
+    part[tid] = acc;
+    __syncthreads();
+    if (tid < CH_NB) blk[tid] = b[r0 + tid] - (((part[4 * tid] + part[4 * tid + 1]) + part[4 * tid + 2]) + part[4 * tid + 3]);
+    __syncthreads();
+    if (tid < CH_NB) {
+      const double* li = Linv + (size_t)k * CH_NB * CH_NB + (size_t)tid * CH_NB;
+      double s = 0.0;
+      for (int c = 0; c <= tid; ++c) s = fma(li[c], blk[c], s);
+      y[r0 + tid] = s;
+    }
+    __syncthreads();
+  }
+  // backward: x_k = Linv_k^T (y_k - sum_{j>k} L_jk^T x_j)
+  for (int k = nbk - 1; k >= 0; --k) {
+    const int r0 = k * CH_NB;
+    const int col = tid >> 2, sub = tid & 3;
+    double acc = 0.0;
+    for (int rr = r0 + CH_NB + sub; rr < n; rr += 4) acc = fma(A[(size_t)rr * n + r0 + col], x[rr], acc);
+    part[tid] = acc;
+    __syncthreads();
+    if (tid < CH_NB) blk[tid] = y[r0 + tid] - (((part[4 * tid] + part[4 * tid + 1]) + part[4 * tid + 2]) + part[4 * tid + 3]);
+    __syncthreads();
+    if (tid < CH_NB) {
+      const double* lk = Linv + (size_t)k * CH_NB * CH_NB;
+      double s = 0.0;
+      for (int c = tid; c < CH_NB; ++c) s = fma(lk[(size_t)c * CH_NB + tid], blk[c], s);
+      x[r0 + tid] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// beta[q][a][i] = x[i*Q + a]; flags non-finite
+__global__ void scatter_x_kernel(int Q, int r, const double* x, double* beta_q, int* info) {
+  const int n = Q * r;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int aa = e / r, i = e % r;
+    const double v = x[(size_t)i * Q + aa];
+    if (!isfinite(v)) atomicOr(info, 2);
+    beta_q[e] = v;
+  }
+}
+
+// per-mode ||new - int||^2 and ||int||^2 (one CTA per mode), then damping
+__global__ void __launch_bounds__(256) conv_damp_kernel(int Q, int r, int d, double* bnew, const double* bint,
+                                                        double delta_beta, double* eps_out) {
+  __shared__ double sdb[256], sna[256];
+  __shared__ double worst;
+  if (threadIdx.x == 0) worst = 0.0;
+  for (int q = 0; q < d; ++q) {
+    const size_t off = (size_t)q * Q * r;
+    double db = 0.0, na = 0.0;
+    for (int e = threadIdx.x; e < Q * r; e += 256) {
+      const double a = bint[off + e], b = bnew[off + e];
+      db += (b - a) * (b - a);
+      na += a * a;
+    }
+    sdb[threadIdx.x] = db;
+    sna[threadIdx.x] = na;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (threadIdx.x < w) { sdb[threadIdx.x] += sdb[threadIdx.x + w]; sna[threadIdx.x] += sna[threadIdx.x + w]; }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const double dbn = sqrt(sdb[0]), nan_ = sqrt(sna[0]);
+      const double v = (nan_ == 0.0) ? (dbn == 0.0 ? 0.0 : INFINITY) : dbn / nan_;
+      worst = fmax(worst, v);
+    }
+    __syncthreads();
+  }
+  for (size_t e = threadIdx.x; e < (size_t)d * Q * r; e += 256)
+    bnew[e] = bint[e] + (bnew[e] - bint[e]) / delta_beta;
+  if (threadIdx.x == 0) *eps_out = worst;
+}
+
+__global__ void set_int_kernel(int* dst, int v) { *dst = v; }
+
+static int padded_n(int n) { return (n + CH_NB - 1) / CH_NB * CH_NB; }
+
+static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
+  const size_t n = (size_t)padded_n(r * Q);
+  size_t s = 0;
+  s += align_up(8 * (size_t)d * n_tab * r * r) * 2;     // G, Gm
+  s += align_up(8 * (size_t)d * n_tab * Q * r) * 2;     // TB scratch, W (b_old images)
+  s += align_up(8 * (size_t)n_tab * r * r) * 2;         // H, Hg
+  s += align_up(8 * n * n);                             // M
+  s += align_up(8 * (n / CH_NB + 1) * CH_NB * CH_NB);   // Linv blocks
+  s += align_up(8 * n) * 3;                             // gamma, x, y
+  s += align_up(8 * (size_t)d * Q * r) * 2;             // b_int, Jacobi staging
+  s += align_up(4 * IM_MAXT) + 256;
+  return s;
+}
+
+}  // namespace tp
+
+using namespace tp;
+
+extern "C" {
+
+size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab) {
+  if (d < 1 || d > IM_MAXD || Q < 1 || r < 1 || n_tab < 1 || n_tab > IM_MAXT) return 0;
+  return implicit_bytes(d, Q, r, n_tab);
+}
+
+int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* tabs, const int* tab_id,
+                         const double* KL, const double* KR, const double* f_old, double* f_new,
+                         int sweeps, int schedule, double delta_beta, double eps_tol, double lam,
+                         int orientation, double* eps_conv, int* info, void* ws, size_t ws_bytes, void* stream) {
+  if (d < 1 || d > IM_MAXD || Q < 1 || r < 1 || ra < 1 || ra > IM_MAXRA || n_tab < 1 || n_tab > IM_MAXT) return TP_EINVAL;
+  if (!tabs || !tab_id || !KL || !KR || !f_old || !f_new || !eps_conv || !info || sweeps < 0) return TP_EINVAL;
+  if (!(delta_beta >= 1.0) || !(lam >= 0.0) || (schedule != 0 && schedule != 1)) return TP_EINVAL;
+  for (int i = 0; i < d * ra * ra; ++i) if (tab_id[i] < 0 || tab_id[i] >= n_tab) return TP_EINVAL;
+  const int n = padded_n(r * Q);   // system size incl. identity padding
+  if (!ws || ws_bytes < implicit_bytes(d, Q, r, n_tab)) return TP_EWORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  Carver cv(ws, ws_bytes);
+  const size_t rr = (size_t)r * r, QR = (size_t)Q * r;
+  double* G = cv.take<double>((size_t)d * n_tab * rr);
+  double* Gm = cv.take<double>((size_t)d * n_tab * rr);
+  double* TB = cv.take<double>((size_t)d * n_tab * QR);
+  double* W = cv.take<double>((size_t)d * n_tab * QR);
+  double* H = cv.take<double>((size_t)n_tab * rr);
+  double* Hg = cv.take<double>((size_t)n_tab * rr);
+  double* M = cv.take<double>((size_t)n * n);
+  double* Linv = cv.take<double>((size_t)(n / CH_NB + 1) * CH_NB * CH_NB);
+  double* gam = cv.take<double>(n);
+  double* x = cv.take<double>(n);
+  double* y = cv.take<double>(n);
+  double* bint = cv.take<double>((size_t)d * QR);
+  double* bjac = cv.take<double>((size_t)d * QR);
+  int* xs_dev = cv.take<int>(IM_MAXT);
+  (void)xs_dev;
+
+  // distinct tables per mode
+  std::vector<std::vector<int>> used(d);
+  for (int k = 0; k < d; ++k) {
+    std::vector<char> seen(n_tab, 0);
+    for (int e = 0; e < ra; ++e)
+      for (int z = 0; z < ra; ++z) {
+        const int t = tab_id[(k * ra + e) * ra + z];
+        if (!seen[t]) { seen[t] = 1; used[k].push_back(t); }
+      }
+  }
+  cudaError_t err;
+  err = cudaMemsetAsync(info, 0, 2 * sizeof(int), st);
+  if (err != cudaSuccess) return cuda_status(err);
+  // per-mode Gram refresh: TB_t = T_t b (Q x r), G_t = a^T TB_t  (a, b = b_new or b_old)
+  // transT: use T^T (reference gamma orientation for the mixed Grams / images)
+  auto images = [&](int k, const double* bsrc, double* dst, int transT) -> cudaError_t {
+    for (int t : used[k]) {
+      BGemm g = bgemm_desc(Q, r, Q, tabs + (size_t)t * Q * Q, transT ? 1 : Q, transT ? Q : 1, bsrc + (size_t)k * QR,
+                           r, 1, dst + ((size_t)k * n_tab + t) * QR, r, 1);
+      cudaError_t e = bgemm_launch(g, st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
+  auto grams = [&](int k, const double* aa, const double* bsrc, double* dstG, int transT) -> cudaError_t {
+    cudaError_t e = images(k, bsrc, TB, transT);
+    if (e != cudaSuccess) return e;
+    for (int t : used[k]) {
+      BGemm g = bgemm_desc(r, r, Q, aa + (size_t)k * QR, 1, r, TB + ((size_t)k * n_tab + t) * QR, r, 1,
+                           dstG + ((size_t)k * n_tab + t) * rr, r, 1);
+      e = bgemm_launch(g, st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
+  const int tr = orientation ? 1 : 0;
+  for (int k = 0; k < d; ++k) {
+    if ((err = grams(k, f_new, f_new, G, 0)) != cudaSuccess) return cuda_status(err);
+    if ((err = grams(k, f_new, f_old, Gm, tr)) != cudaSuccess) return cuda_status(err);
+    if ((err = images(k, f_old, W, tr)) != cudaSuccess) return cuda_status(err);
+  }
+  HArgs ha;
+  memset(&ha, 0, sizeof(ha));
+  ha.d = d; ha.ra = ra; ha.r = r; ha.n_tab = n_tab;
+  for (int i = 0; i < d * ra * ra; ++i) ha.tab[i] = tab_id[i];
+  for (int i = 0; i < ra * ra; ++i) { ha.KL[i] = KL[i]; ha.KR[i] = KR[i]; }
+  ha.G = G; ha.Gm = Gm; ha.H = H; ha.Hg = Hg;
+  AsmArgs as;
+  memset(&as, 0, sizeof(as));
+  as.Q = Q; as.r = r; as.N = n; as.tabs = tabs; as.H = H; as.M = M; as.lam = lam;
+  // xs tables are uploaded per mode into a small device array (stream-ordered)
+  std::vector<int> xs_all((size_t)d * IM_MAXT, 0);
+  for (int k = 0; k < d; ++k)
+    for (size_t i = 0; i < used[k].size(); ++i) xs_all[(size_t)k * IM_MAXT + i] = used[k][i];
+  int* xs_modes = reinterpret_cast<int*>(Linv + (size_t)(n / CH_NB) * CH_NB * CH_NB);   // spare tail block
+  err = cudaMemcpyAsync(xs_modes, xs_all.data(), xs_all.size() * sizeof(int), cudaMemcpyHostToDevice, st);
+  if (err != cudaSuccess) return cuda_status(err);
+  const int nbk = n / CH_NB;
+  const int pd_smem = (int)(sizeof(double) * 2 * CH_NB * (CH_NB + 1));
+  cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pd_smem);
+  const int asm_blocks = (int)(((long long)n * n + 255) / 256 < 148 * 32 ? ((long long)n * n + 255) / 256 : 148 * 32);
+  int done = 0;
+  for (int sweep = 0; sweep < sweeps; ++sweep) {
+    err = cudaMemcpyAsync(bint, f_new, sizeof(double) * d * QR, cudaMemcpyDeviceToDevice, st);
+    if (err != cudaSuccess) return cuda_status(err);
+    for (int q = 0; q < d; ++q) {
+      ha.q = q; ha.nX = (int)used[q].size();
+      for (int i = 0; i < ha.nX; ++i) ha.xs[i] = used[q][i];
+      form_h_kernel<<<ha.nX, 256, 0, st>>>(ha);
+      gamma_kernel<<<(n + 255) / 256, 256, 0, st>>>(Q, r, ha.nX, xs_modes + (size_t)q * IM_MAXT, Hg, W, n_tab, q, gam, n);
+      as.nX = ha.nX;
+      for (int i = 0; i < as.nX; ++i) as.xs[i] = used[q][i];
+      assemble_kernel<<<asm_blocks, 256, 0, st>>>(as);
+      for (int kb = 0; kb < nbk; ++kb) {
+        const int k0 = kb * CH_NB, rest = n - k0 - CH_NB;
+        potrf_diag_kernel<<<1, 256, pd_smem, st>>>(M, n, k0, CH_NB, Linv + (size_t)kb * CH_NB * CH_NB, info);
+        if (rest > 0) {
+          // panel: A21 <- A21 L11^-T   (in place: each row block is read fully before written)
+          BGemm gp = bgemm_desc(rest, CH_NB, CH_NB, M + (size_t)(k0 + CH_NB) * n + k0, n, 1,
+                                Linv + (size_t)kb * CH_NB * CH_NB, 1, CH_NB, M + (size_t)(k0 + CH_NB) * n + k0, n, 1);
+          if ((err = bgemm_launch(gp, st)) != cudaSuccess) return cuda_status(err);
+          // trailing: A22 <- A22 - A21 A21^T
+          BGemm gs = bgemm_desc(rest, rest, CH_NB, M + (size_t)(k0 + CH_NB) * n + k0, n, 1,
+                                M + (size_t)(k0 + CH_NB) * n + k0, 1, n, M + (size_t)(k0 + CH_NB) * n + k0 + CH_NB, n, 1);
+          gs.alpha = -1.0; gs.beta = 1.0;
+          if ((err = bgemm_launch(gs, st)) != cudaSuccess) return cuda_status(err);
+        }
+      }
+      potrs_kernel<<<1, 256, 0, st>>>(M, n, Linv, gam, x, y);
+      double* dst = (schedule == 0 ? f_new : bjac) + (size_t)q * QR;
+      scatter_x_kernel<<<(int)((QR + 255) / 256), 256, 0, st>>>(Q, r, x, dst, info);
+      if (schedule == 0) {
+        if ((err = grams(q, f_new, f_new, G, 0)) != cudaSuccess) return cuda_status(err);
+        if ((err = grams(q, f_new, f_old, Gm, tr)) != cudaSuccess) return cuda_status(err);
+      }
+    }
+    if (schedule == 1) {
+      err = cudaMemcpyAsync(f_new, bjac, sizeof(double) * d * QR, cudaMemcpyDeviceToDevice, st);
+      if (err != cudaSuccess) return cuda_status(err);
+    }
+    conv_damp_kernel<<<1, 256, 0, st>>>(Q, r, d, f_new, bint, delta_beta, eps_conv);
+    done = sweep + 1;
+    // the damped iterate b_int + (b - b_int)/delta_beta differs from the raw
+    // solve (also by rounding when delta_beta == 1): refresh every mode's Grams
+    for (int k = 0; k < d; ++k) {
+      if ((err = grams(k, f_new, f_new, G, 0)) != cudaSuccess) return cuda_status(err);
+      if ((err = grams(k, f_new, f_old, Gm, tr)) != cudaSuccess) return cuda_status(err);
+    }
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return cuda_status(err);
+    if (eps_tol > 0.0) {   // reference loop condition (implicit.py:244): one host read per sweep
+      double eps_h = 0.0;
+      err = cudaMemcpyAsync(&eps_h, eps_conv, sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+      if (err != cudaSuccess) return cuda_status(err);
+      if (eps_h <= eps_tol) break;
+    }
+  }
+  set_int_kernel<<<1, 1, 0, st>>>(info + 1, done);
+  return cuda_status(cudaGetLastError());
+}
+
+}  // extern "C"

@@ -1,0 +1,180 @@
+"""Fixed-rank implicit time stepping by (damped) alternating least squares
+(mirror of ``tensorpde/implicit.py``).
+
+``step`` runs every sweep of one implicit step in ``tp_implicit_step_f64``:
+device assembly of the normal-equation blocks M_q / gamma_q (implicit.py:125-153),
+a hand-written blocked Cholesky solve of (M_q + lam I) x = gamma_q (replacing the
+LSQR of implicit.py:156-164; SURVEY 8(c) shim S6), the convergence measure and
+damping (implicit.py:167-177, 281-282).  ``orientation="corrected"`` assembles
+the true normal equations of min |A f_new - B f_old|^2; ``"reference"``
+reproduces build_gamma's pairing (implicit.py:137-139).
+"""
+
+from __future__ import annotations
+
+import logging
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import StepFailure
+from .cp import CPTensor
+from .operators import CrankNicolsonPair, dense_factor
+
+__all__ = ["ALSStepConfig", "OperatorTables", "StepWorkspace", "StepFailure", "build_tables", "step"]
+
+logger = logging.getLogger(__name__)
+
+
+@dataclass
+class ALSStepConfig:
+    """implicit.py:59-74, plus ``lam`` (Tikhonov constant of the direct solve) and
+    ``orientation`` ("corrected" | "reference")."""
+
+    dt: float
+    eps_tol: float = 1e-8
+    max_sweeps: int = 500
+    delta_beta: float = 4.0
+    lsqr_tol: float = 1e-12
+    lsqr_maxit: int = 2000
+    workers: int = 1
+    schedule: str = "jacobi"
+    lam: float = 1e-10
+    orientation: str = "corrected"
+
+    def __post_init__(self):
+        if self.schedule not in ("jacobi", "gauss-seidel"):
+            raise ValueError(f"unknown schedule {self.schedule!r}")
+        if self.delta_beta < 1.0:
+            raise ValueError("damping divisor must be >= 1")
+        if self.orientation not in ("corrected", "reference"):
+            raise ValueError(f"unknown orientation {self.orientation!r}")
+
+
+@dataclass
+class OperatorTables:
+    """Deduplicated pairing tables pairs[k][e][z] = F_{e,k}^T F_{z,k} (implicit.py:77-108)."""
+
+    pair: CrankNicolsonPair
+    tabs: torch.Tensor          # (n_tab, Q, Q) device
+    tab_id: np.ndarray          # (d, ra, ra) int32
+    KL: np.ndarray
+    KR: np.ndarray
+
+
+def build_tables(pair: CrankNicolsonPair, device=None) -> OperatorTables:
+    specs = pair.specs
+    qs = {s.Q for s in specs}
+    if len(qs) != 1:
+        raise ValueError("the B200 implicit step needs a uniform mode size Q")
+    Q = qs.pop()
+    ra, d = pair.n_terms, len(specs)
+    uniq, keys, tab_id = [], {}, np.zeros((d, ra, ra), dtype=np.int32)
+    for k, spec in enumerate(specs):
+        mats = []
+        for e in range(ra):
+            m = dense_factor(spec, pair.factors[e][k])
+            mats.append(np.eye(Q) if m is None else m)
+        for e in range(ra):
+            for z in range(ra):
+                t = np.ascontiguousarray(mats[e].T @ mats[z])
+                key = t.tobytes()
+                if key not in keys:
+                    keys[key] = len(uniq)
+                    uniq.append(t)
+                tab_id[k, e, z] = keys[key]
+    eta = np.asarray([complex(x) for x in pair.eta])
+    zeta = np.asarray([complex(x) for x in pair.zeta])
+    if np.any(eta.imag != 0) or np.any(zeta.imag != 0):
+        raise ValueError("complex operator weights are not supported on the real-fp64 B200 path")
+    eta, zeta = eta.real, zeta.real
+    dev = device or _lib.device()
+    tabs = torch.as_tensor(np.stack(uniq)).to(dev)
+    return OperatorTables(pair, tabs, tab_id, np.outer(eta, eta), np.outer(eta, zeta))
+
+
+class StepWorkspace:
+    """implicit.py:180-210: reusable tables for repeated steps with one pair."""
+
+    def __init__(self, pair: CrankNicolsonPair, config: ALSStepConfig):
+        if abs(config.dt - pair.dt) > 1e-15 * max(abs(pair.dt), 1.0):
+            raise ValueError(f"config dt {config.dt} != operator pair dt {pair.dt}")
+        self.pair = pair
+        self.config = config
+        self.tables = build_tables(pair)
+
+    def close(self):
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+
+def _launch(f_n: CPTensor, out: torch.Tensor, tab: OperatorTables, cfg: ALSStepConfig, eps: torch.Tensor,
+            info: torch.Tensor) -> None:
+    L = _lib.lib()
+    d, Q, r, ra = f_n.ndim, f_n.specs[0].Q, f_n.rank, tab.pair.n_terms
+    n_tab = tab.tabs.shape[0]
+    nbytes = L.tp_implicit_ws_bytes(d, Q, r, n_tab)
+    if nbytes == 0:
+        raise ValueError(f"unsupported implicit-step size d={d}, Q={Q}, r={r}, tables={n_tab}")
+    ws = _lib.WORKSPACE.get(nbytes, f_n.data.device)
+    st = L.tp_implicit_step_f64(d, Q, r, ra, n_tab, tab.tabs.data_ptr(), _lib.int_array(tab.tab_id.reshape(-1)),
+                                _lib.double_array(tab.KL.reshape(-1)), _lib.double_array(tab.KR.reshape(-1)),
+                                f_n.data.data_ptr(), out.data_ptr(), int(cfg.max_sweeps),
+                                0 if cfg.schedule == "gauss-seidel" else 1, float(cfg.delta_beta),
+                                float(cfg.eps_tol), float(cfg.lam), 1 if cfg.orientation == "reference" else 0,
+                                eps.data_ptr(), info.data_ptr(), ws.data_ptr(), ws.numel(),
+                                _lib.stream_ptr(f_n.data.device))
+    _lib.check(st, "implicit.step")
+
+
+def step(f_n: CPTensor, pair: CrankNicolsonPair, forcing: CPTensor | None, config: ALSStepConfig,
+         workspace: StepWorkspace | None = None, log: dict | None = None) -> CPTensor:
+    """Advance one implicit step at fixed separation rank (implicit.py:222-301)."""
+    if forcing is not None:
+        raise NotImplementedError("forcing terms (implicit.py:140-152) are outside the B200 hot path")
+    ws = workspace or StepWorkspace(pair, config)
+    dev = f_n.data.device
+    out = f_n.data.clone()
+    eps = torch.full((1,), float("inf"), dtype=torch.float64, device=dev)
+    info = torch.zeros(2, dtype=torch.int32, device=dev)
+    t0 = time.perf_counter()
+    _launch(f_n, out, ws.tables, config, eps, info)
+    status, sweeps = (int(v) for v in info.tolist())
+    eps_conv = float(eps.item())
+    if status & 2:
+        raise StepFailure(-1, sweeps, float("nan"))
+    if status & 1:
+        raise StepFailure(-1, sweeps, float("inf"))
+    did_converge = eps_conv <= config.eps_tol
+    if not did_converge:
+        logger.warning("sweep cap %d hit with update %.3e > %.3e", config.max_sweeps, eps_conv, config.eps_tol)
+    if log is not None:
+        log.update(sweeps=sweeps, eps_conv=eps_conv, converged=did_converge,
+                   assembly_seconds=0.0, solve_seconds=time.perf_counter() - t0, lsqr_iterations=0)
+    return CPTensor(f_n.specs, data=out, rank=f_n.rank)
+
+
+def run(f0: CPTensor, pair: CrankNicolsonPair, config: ALSStepConfig, steps: int) -> CPTensor:
+    """``steps`` implicit steps, stream-ordered, one status check at the end."""
+    ws = StepWorkspace(pair, config)
+    dev = f0.data.device
+    eps = torch.zeros(1, dtype=torch.float64, device=dev)
+    infos = torch.zeros((max(steps, 1), 2), dtype=torch.int32, device=dev)
+    cur = f0
+    for n in range(steps):
+        out = cur.data.clone()
+        _launch(cur, out, ws.tables, config, eps, infos[n])
+        cur = CPTensor(f0.specs, data=out, rank=f0.rank)
+    bad = int(infos[:, 0].max().item())
+    if bad:
+        raise StepFailure(-1, config.max_sweeps, float("nan"))
+    return cur

@@ -1,0 +1,91 @@
+"""GPU parity of the implicit ALS step (implicit.step, implicit.py:222-301) against
+the oracle (pinned by tests/golden/implicit.npz, which ran the real reference with
+SURVEY shims S5-S8), in both gamma orientations."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, unpack_cp
+from oracle import implicit as oim
+from oracle import metrics
+
+pytestmark = pytest.mark.gpu
+
+from paper_1803_10270_b200 import cp, implicit, operators, workloads  # noqa: E402
+from paper_1803_10270_b200.basis import BasisSpec, fourier_diff_matrix  # noqa: E402
+
+
+def col_specs(d, q):
+    return tuple(BasisSpec(q, math.pi, "collocation", lo=0.0) for _ in range(d))
+
+
+def euler_pair(S, D, a, dt):
+    d = len(S)
+    L = operators.SeparableOperator(S, tuple(-np.asarray(a)), tuple(tuple(D if k == t else None for k in range(d))
+                                                                  for t in range(d)))
+    return operators.implicit_euler_pair(L, dt)
+
+
+def oracle_tables(d, q, D, a, dt):
+    mats = [[None] * d] + [[D if k == i else None for k in range(d)] for i in range(d)]
+    eta = [1.0] + list(dt * np.asarray(a))
+    zeta = [1.0] + [0.0] * d
+    return oim.build_tables(mats, eta, zeta, [q] * d)
+
+
+@pytest.mark.parametrize("orientation,key", [("reference", "out_reference_orientation"),
+                                             ("corrected", "out_corrected")])
+def test_step_golden(orientation, key):
+    g = load_golden("implicit")
+    q, d, r, dt, sweeps, lam = g["meta"]
+    q, d, sweeps = int(q), int(d), int(sweeps)
+    S = col_specs(d, q)
+    pair = euler_pair(S, g["D"], g["a"], float(dt))
+    cfg = implicit.ALSStepConfig(dt=float(dt), eps_tol=0.0, max_sweeps=sweeps, delta_beta=1.0,
+                                 schedule="gauss-seidel", lam=float(lam), orientation=orientation)
+    log = {}
+    out = implicit.step(cp.CPTensor(S, unpack_cp(g, "f0")), pair, None, cfg, log=log)
+    assert log["sweeps"] == sweeps
+    rel = metrics.cp_rel_diff(unpack_cp(g, key), out.to_numpy())
+    assert rel <= 1e-9, rel
+
+
+@pytest.mark.parametrize("schedule,delta", [("gauss-seidel", 1.0), ("jacobi", 4.0), ("jacobi", 1.0)])
+def test_step_matches_oracle(schedule, delta):
+    rng = np.random.default_rng(7)
+    d, q, r, dt, sweeps = 4, 16, 4, 2e-2, 5
+    a = (1.0, 0.5, -0.75, 0.25)
+    D = fourier_diff_matrix(q)
+    S = col_specs(d, q)
+    f0 = [rng.standard_normal((q, r)) for _ in range(d)]
+    cfg = implicit.ALSStepConfig(dt=dt, eps_tol=0.0, max_sweeps=sweeps, delta_beta=delta, schedule=schedule,
+                                 lam=1e-10)
+    out = implicit.step(cp.CPTensor(S, f0), euler_pair(S, D, a, dt), None, cfg)
+    ref, done, _ = oim.step(f0, oracle_tables(d, q, D, a, dt), sweeps, 1e-10, schedule=schedule,
+                            delta_beta=delta)
+    rel = metrics.cp_rel_diff(ref, out.to_numpy())
+    assert rel <= 1e-9, rel
+
+
+def test_config2_full_size_step():
+    """BASELINE config 2 sizes (d=6, Q=128, r=16 -> 2048^2 normal equations), 3 sweeps
+    of one step, vs the oracle's direct solves."""
+    w = workloads.cfg2(0)
+    S, D, a, dt = w["specs"], w["D"], w["a"], w["dt"]
+    f0 = w["ic"]["factors"]
+    sweeps = 3
+    cfg = implicit.ALSStepConfig(dt=dt, eps_tol=0.0, max_sweeps=sweeps, delta_beta=1.0, schedule="gauss-seidel",
+                                 lam=w["lam"])
+    out = implicit.step(cp.CPTensor(S, f0), euler_pair(S, D, a, dt), None, cfg)
+    ref, _, _ = oim.step(f0, oracle_tables(6, 128, D, a, dt), sweeps, w["lam"])
+    rel = metrics.cp_rel_diff(ref, out.to_numpy())
+    assert rel <= 1e-8, rel
+
+
+def test_config_validation():
+    with pytest.raises(ValueError, match="schedule"):
+        implicit.ALSStepConfig(dt=0.1, schedule="sor")
+    with pytest.raises(ValueError, match="damping"):
+        implicit.ALSStepConfig(dt=0.1, delta_beta=0.5)
