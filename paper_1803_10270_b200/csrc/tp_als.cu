@@ -35,7 +35,7 @@ int launch_inner(int d, const int* q, int ra, const double* A, int rb, const dou
 
 constexpr int ALS_NT = 256;
 constexpr int ALS_NW = ALS_NT / 32;
-constexpr int ALS_PART = 1024;   // doubles of scratch for split-K partial tiles / reductions
+constexpr int ALS_PART = 512;   // doubles of scratch for split-K partial tiles / reductions
 
 // padded shared-memory row stride: >= n and == 4 (mod 16) doubles, so DMMA
 // fragment loads (4 rows x 8 columns per half-warp) hit distinct banks
@@ -61,24 +61,30 @@ struct AlsArgs {
   double tol, stall;
   int need_resid;
   long long* prof;     // optional per-phase clock64 totals (CTA 0), debug hook
+  unsigned int* bar_ctr;   // grid-barrier arrival counter (zeroed before launch)
+  int dbg_skip;            // debug: bit mask of phases to skip (timing by subtraction)
+  double* Xprev;           // [d][r][r+1] last inverse per mode (warm start for Newton-Schulz)
+  int ns_max;              // Newton-Schulz iterations before falling back to the exact sweep
 };
 
 struct Smem {
-  uint64_t* bar;
-  double *Us, *Vs, *Cs, *Gs, *hadT, *Ai, *pub, *rb, *part, *scal;
+  uint64_t* bar;        // bar[0]: U staging / Y slices, bar[1]: Gram
+  double *Us, *Vs, *Cs, *Gs, *hadT, *Am, *X0, *X1, *Rm, *pub, *rb, *part, *scal;
+  int* rowmap;          // [d][qmax]: (consumer CTA << 16) | row-in-consumer
 };
 
 __host__ __device__ inline size_t stage_doubles(int qmax, int r, int ncolmax, int P) {
   // staging area shared by U_k (phase A, padded rows) and the P right-hand-side
   // slices + one Gram (phase B)
-  size_t a = (size_t)qmax * r, b = (size_t)P * ncolmax * r + (size_t)r * r;   // raw Gram + P blocks
+  size_t a = (size_t)qmax * r, b = (size_t)P * ncolmax * r;   // U_k rows | the P right-hand-side blocks
   return a > b ? a : b;
 }
 
 __host__ __device__ inline size_t als_smem_doubles(int d, int sumqs, int r, int wmax, int ncolmax, int qmax, int P) {
   const size_t w4 = (size_t)((wmax + 3) / 4) * 4;
   return 8 + stage_doubles(qmax, r, ncolmax, P) + (size_t)wmax * sumqs + (size_t)d * r * wmax +
-         (size_t)d * r * pad4(r) + w4 * pad4(r) + (size_t)r * (r + 1) + 72 + (size_t)ncolmax * r + ALS_PART + 8;
+         (size_t)d * r * r + w4 * pad4(r) + 4 * (size_t)r * (r + 1) + 72 + (size_t)ncolmax * r + ALS_PART + 8 +
+         ((size_t)d * qmax + 1) / 2 + 1;
 }
 
 __device__ inline Smem carve(double* base, const AlsArgs& a) {
@@ -88,14 +94,35 @@ __device__ inline Smem carve(double* base, const AlsArgs& a) {
   s.Us = base + o; o += stage_doubles(a.qmax, a.r, a.ncolmax, a.P);
   s.Vs = base + o; o += (size_t)a.wmax * a.sumqs;
   s.Cs = base + o; o += (size_t)a.d * a.r * a.wmax;
-  s.Gs = base + o; o += (size_t)a.d * a.r * pad4(a.r);
+  s.Gs = base + o; o += (size_t)a.d * a.r * a.r;
   s.hadT = base + o; o += (size_t)((a.wmax + 3) / 4) * 4 * pad4(a.r);
-  s.Ai = base + o; o += (size_t)a.r * (a.r + 1);
+  s.Am = base + o; o += (size_t)a.r * (a.r + 1);
+  s.X0 = base + o; o += (size_t)a.r * (a.r + 1);
+  s.X1 = base + o; o += (size_t)a.r * (a.r + 1);
+  s.Rm = base + o; o += (size_t)a.r * (a.r + 1);
   s.pub = base + o; o += 72;
   s.rb = base + o; o += (size_t)a.ncolmax * a.r;
   s.part = base + o; o += ALS_PART;
-  s.scal = base + o;
+  s.scal = base + o; o += 8;
+  s.rowmap = reinterpret_cast<int*>(base + o);
   return s;
+}
+
+// Grid barrier: one release-add per CTA on a monotonic counter, acquire-poll
+// until every CTA of this epoch arrived (cheaper than cg::grid_group::sync).
+// Cross-CTA data is read through L2 (__ldcg / bulk copies), so no L1 flush.
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned int target = epoch * gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
 }
 
 // fast reciprocal: MUFU seed + 2 Newton steps (<= 1 ulp, no slow path)
@@ -237,9 +264,9 @@ __device__ inline double block_sum(double v, double* red) {
 // column k == row k, so each pivot step publishes one row and costs one
 // barrier.  Returns 1 if a pivot is not positive / finite.
 template <int RM>
-__device__ int gram_inverse(const AlsArgs& a, const Smem& sm, int j) {
+__device__ int gram_inverse(const AlsArgs& a, const Smem& sm, int j, double* out) {
   constexpr int EPT = RM / 8;
-  const int r = a.r, gs = pad4(r), gk = r * gs, rp = r + 1, t = threadIdx.x;
+  const int r = a.r, gs = r, gk = r * r, rp = r + 1, t = threadIdx.x;
   const int i = t >> 3, c0 = t & 7;
   double v[EPT];
 #pragma unroll
@@ -297,9 +324,125 @@ __device__ int gram_inverse(const AlsArgs& a, const Smem& sm, int j) {
 #pragma unroll
     for (int u = 0; u < EPT; ++u) {
       const int c = c0 + 8 * u;
-      if (c < r) sm.Ai[i * rp + c] = -v[u];
+      if (c < r) out[i * rp + c] = -v[u];
     }
   return bad;
+}
+
+// C = op(A B) for r x r smem matrices (row stride r+1) on DMMA m8n8k4; every
+// warp owns 8x8 output tiles.  mode 0: C = I - A B;  mode 1: C = X + A B (X = A)
+template <int RM>
+__device__ void small_gemm(const double* A, const double* B, double* C, int r, int mode) {
+  constexpr int NT8 = RM / 8, TILES = NT8 * NT8, TPW = (TILES + ALS_NW - 1) / ALS_NW, KS = RM / 4;
+  constexpr int SPLIT = KS < 4 ? KS : 4;   // independent accumulator chains per tile
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, rp = r + 1;
+  double acc[TPW][SPLIT][2];
+#pragma unroll
+  for (int t = 0; t < TPW; ++t)
+#pragma unroll
+    for (int s2 = 0; s2 < SPLIT; ++s2) acc[t][s2][0] = acc[t][s2][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const int k = 4 * kk + (lane & 3);
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) {
+      const int tile = warp + t * ALS_NW;
+      if (tile < TILES) {
+        const int m0 = (tile / NT8) * 8, n0 = (tile % NT8) * 8;
+        const int mrow = m0 + (lane >> 2), ncol = n0 + (lane >> 2);
+        const double fa = (mrow < r && k < r) ? A[mrow * rp + k] : 0.0;
+        const double fb = (k < r && ncol < r) ? B[k * rp + ncol] : 0.0;
+        dmma_8x8x4(acc[t][kk % SPLIT][0], acc[t][kk % SPLIT][1], fa, fb);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) {
+    const int tile = warp + t * ALS_NW;
+    if (tile >= TILES) continue;
+    double s0 = acc[t][0][0], s1 = acc[t][0][1];
+#pragma unroll
+    for (int s2 = 1; s2 < SPLIT; ++s2) { s0 += acc[t][s2][0]; s1 += acc[t][s2][1]; }
+    const int m0 = (tile / NT8) * 8, n0 = (tile % NT8) * 8;
+    const int orow = m0 + (lane >> 2), oc = n0 + 2 * (lane & 3);
+    if (orow < r) {
+      if (oc < r) C[orow * rp + oc] = mode == 0 ? ((orow == oc ? 1.0 : 0.0) - s0) : A[orow * rp + oc] + s0;
+      if (oc + 1 < r) C[orow * rp + oc + 1] = mode == 0 ? ((orow == oc + 1 ? 1.0 : 0.0) - s1) : A[orow * rp + oc + 1] + s1;
+    }
+  }
+}
+
+__device__ inline double block_max_abs(const double* M, int r, double* red) {
+  const int rp = r + 1;
+  double m = 0.0;
+  for (int e = threadIdx.x; e < r * r; e += ALS_NT) {
+    const double x = M[(e / r) * rp + e % r];
+    m = (x != x) ? INFINITY : fmax(m, fabs(x));        // NaN -> inf (forces the fallback)
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  double out = red[0];
+#pragma unroll
+  for (int w = 1; w < ALS_NW; ++w) out = fmax(out, red[w]);
+  __syncthreads();
+  return out;
+}
+
+// A = prod_{k!=j} G_k + lambda I into sm.Am (row stride r+1)
+__device__ void build_a(const AlsArgs& a, const Smem& sm, int j) {
+  const int r = a.r, rr = r * r, rp = r + 1;
+  for (int e = threadIdx.x; e < rr; e += ALS_NT) {
+    double v = 1.0;
+    for (int k = 0; k < a.d; ++k)
+      if (k != j) v *= sm.Gs[(size_t)k * rr + e];
+    sm.Am[(e / r) * rp + e % r] = v;
+  }
+  __syncthreads();
+  double lam = a.reg;
+  if (a.reg_mode) {
+    double tr = 0.0;
+    for (int q = 0; q < r; ++q) tr += sm.Am[q * rp + q];
+    lam = a.reg * fmax(tr, 0.0) / (double)r;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < r; q += ALS_NT) sm.Am[q * rp + q] += lam;
+  __syncthreads();
+}
+
+// A^-1 for mode j: Newton-Schulz refinement X <- X + X (I - A X) from the
+// previous sweep's inverse (quadratic convergence once ALS settles; three
+// small DMMA GEMMs per iteration instead of r dependent pivot steps); exact
+// symmetric sweep when there is no warm start or it does not converge to
+// |I - A X|_max <= 1e-14.  Decisions are uniform (identical inputs in every
+// CTA).  Returns the buffer holding the inverse (row stride r+1).
+template <int RM>
+__device__ double* invert_mode(const AlsArgs& a, const Smem& sm, int j, bool warm, int& status) {
+  if (warm && a.ns_max > 0) {
+    build_a(a, sm, j);
+    double* X = sm.X0;
+    double* Xn = sm.X1;
+    bool ok = false;
+    double prev = INFINITY;
+    for (int it = 0; it < a.ns_max; ++it) {
+      small_gemm<RM>(sm.Am, X, sm.Rm, a.r, 0);        // R = I - A X
+      __syncthreads();
+      const double nrm = block_max_abs(sm.Rm, a.r, sm.part);
+      if (!(nrm <= 0.25)) break;                      // warm start too far (or non-finite)
+      // converged: at rounding level, or quadratic convergence has stalled there
+      if (nrm <= 1e-13 || (nrm <= 1e-10 && nrm >= 0.25 * prev)) { ok = true; break; }
+      prev = nrm;
+      small_gemm<RM>(X, sm.Rm, Xn, a.r, 1);           // Xn = X + X R
+      __syncthreads();
+      double* t = X; X = Xn; Xn = t;
+    }
+    if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) a.prof[ok ? 14 : 15] += 1;
+    if (ok) return X;
+  }
+  status |= gram_inverse<RM>(a, sm, j, sm.X0);
+  __syncthreads();
+  return sm.X0;
 }
 
 // debug phase timers: barrier-synchronised so the attribution is exact
@@ -322,18 +465,26 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   long long prof_t = clock64();
   long long prof_acc[12] = {};
   double prof_sink = 0.0;
-  cg::grid_group grid = cg::this_grid();
+  unsigned int epoch = 0;
   const Smem sm = carve(smem, a);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int p = blockIdx.x, P = gridDim.x, r = a.r, R = a.R, rr = r * r, rp = r + 1, rh = pad4(r);
   const int c0 = (int)((long long)R * p / P), c1 = (int)((long long)R * (p + 1) / P), w = c1 - c0;
   const int w4 = (w + 3) / 4 * 4;
   int status = 0;
-  uint32_t bphase = 0;
+  uint32_t bphase = 0, gphase = 0;
   if (tid == 0) {
     mbar_init(sm.bar, 1);
+    mbar_init(sm.bar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  for (int k = 0; k < a.d; ++k)
+    for (int s2 = tid; s2 < a.q[k]; s2 += ALS_NT) {
+      const int Qk = a.q[k];
+      const int pc = ((s2 + 1) * P + Qk - 1) / Qk - 1;       // CTA owning column s2 in phase B
+      const int ii = s2 - (Qk * pc) / P;
+      sm.rowmap[k * a.qmax + s2] = (pc << 16) | ii;
+    }
   // zero hadT padding rows (c in [w, w4)) once
   for (int e = tid; e < (w4 - w) * rh; e += ALS_NT) sm.hadT[(size_t)w * rh + e] = 0.0;
   __syncthreads();
@@ -354,12 +505,8 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
     cross_slab(a, sm, k, w);
     gram_share(a, sm, k);
   }
-  grid.sync();
-  const int gs = pad4(r), gk = r * gs;
-  for (int e = tid; e < a.d * rr; e += ALS_NT) {
-    const int k = e / rr, f = e % rr;
-    sm.Gs[(size_t)k * gk + (f / r) * gs + f % r] = __ldcg(a.G + e);
-  }
+  grid_barrier(a.bar_ctr, epoch);
+  for (int e = tid; e < a.d * rr; e += ALS_NT) sm.Gs[e] = __ldcg(a.G + e);
   __syncthreads();
 
   const double norm_sq = a.need_resid ? fmax(*a.norm_sq, 0.0) : 0.0;
@@ -373,11 +520,11 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       // ---------------- phase A
       PROF(0);
       if (pending >= 0) {
-        stage_u(a, sm, pending, bphase);
+        if (!(a.dbg_skip & 2)) stage_u(a, sm, pending, bphase);
         PROF(10);
-        cross_slab(a, sm, pending, w);
+        if (!(a.dbg_skip & 4)) cross_slab(a, sm, pending, w);
         PROF(11);
-        gram_share(a, sm, pending);
+        if (!(a.dbg_skip & 8)) gram_share(a, sm, pending);
       }
       PROF(1);
       const int Qj = a.q[j], qsj = a.qs[j];
@@ -396,11 +543,11 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         // one contiguous block with a single bulk copy.
         const double* vs = sm.Vs + a.qoff[j];
         const int mt = (Qj + 7) / 8, nt = (r + 7) / 8, kst = w4 / 4;
-        for (int m = warp; m < mt; m += ALS_NW) {
+        for (int m = warp; m < ((a.dbg_skip & 16) ? 0 : mt); m += ALS_NW) {
           const int m0 = m * 8, s = m0 + (lane >> 2);
           const bool srow = s < Qj;
-          const int pc = srow ? (int)((((long long)s + 1) * P + Qj - 1) / Qj) - 1 : 0;
-          const int ii = s - (int)((long long)Qj * pc / P);
+          const int rm = srow ? sm.rowmap[j * a.qmax + s] : 0;
+          const int pc = rm >> 16, ii = rm & 0xffff;
           double* yrow = a.Y + (((size_t)pc * P + p) * a.ncolmax + ii) * r;
           for (int n = 0; n < nt; ++n) {
             const int n0 = n * 8, l = n0 + (lane >> 2);
@@ -424,44 +571,52 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         }
       }
       PROF(2);
-      grid.sync();
+      grid_barrier(a.bar_ctr, epoch);
       PROF(3);
       // ---------------- phase B
       const int s0 = (int)((long long)Qj * p / P), s1 = (int)((long long)Qj * (p + 1) / P);
       const int ncol = s1 - s0, E = ncol * r;
       const int nb = a.ncolmax * r;     // one producer's block for this consumer
-      double* ystage = sm.Us + rr;      // [q][nb] after one staged raw Gram
+      double* Xinv = sm.X0;
+      double* ystage = sm.Us;           // [q][nb]
       if (bulk) {
         if (tid == 0) {
           const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
-          const uint32_t ybytes = E > 0 ? (uint32_t)(P * nb) * 8u : 0u;
+          const uint32_t ybytes = (E > 0 && !(a.dbg_skip & 32)) ? (uint32_t)(P * nb) * 8u : 0u;
           fence_proxy_async();
-          mbar_arrive_expect_tx(sm.bar, gbytes + ybytes);
-          if (gbytes) bulk_g2s(sm.Us, a.G + (size_t)pending * rr, gbytes, sm.bar);
+          const uint32_t xbytes = (sweep > 0 && a.ns_max > 0) ? (uint32_t)(r * rp) * 8u : 0u;
+          mbar_arrive_expect_tx(sm.bar + 1, gbytes + xbytes);
+          if (gbytes) bulk_g2s(sm.Gs + (size_t)pending * rr, a.G + (size_t)pending * rr, gbytes, sm.bar + 1);
+          if (xbytes) bulk_g2s(sm.X0, a.Xprev + (size_t)j * r * rp, xbytes, sm.bar + 1);
+          mbar_arrive_expect_tx(sm.bar, ybytes);
           if (ybytes) bulk_g2s(ystage, a.Y + (size_t)p * P * nb, ybytes, sm.bar);
         }
+        mbar_wait(sm.bar + 1, gphase);
+        gphase ^= 1u;
+        // the inversion runs while the right-hand-side slices are still landing
+        if (!(a.dbg_skip & 1)) Xinv = invert_mode<RM>(a, sm, j, sweep > 0, status);
         mbar_wait(sm.bar, bphase);
         bphase ^= 1u;
-        if (pending >= 0)
-          for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * gk + (e / r) * gs + e % r] = sm.Us[e];
-        for (int o = tid; o < E; o += ALS_NT) {
+        for (int o = tid; o < ((a.dbg_skip & 64) ? 0 : E); o += ALS_NT) {
           double acc = 0.0;
           for (int q = 0; q < P; ++q) acc += ystage[(size_t)q * nb + o];
           sm.rb[o] = acc;
         }
       } else {
         if (pending >= 0)
-          for (int e = tid; e < rr; e += ALS_NT)
-            sm.Gs[(size_t)pending * gk + (e / r) * gs + e % r] = __ldcg(a.G + (size_t)pending * rr + e);
+          for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * rr + e] = __ldcg(a.G + (size_t)pending * rr + e);
+        if (sweep > 0 && a.ns_max > 0)
+          for (int e = tid; e < r * rp; e += ALS_NT) sm.X0[e] = __ldcg(a.Xprev + (size_t)j * r * rp + e);
         for (int o = tid; o < E; o += ALS_NT) {
           double acc = 0.0;
           for (int q = 0; q < P; ++q) acc += __ldcg(a.Y + ((size_t)p * P + q) * nb + o);
           sm.rb[o] = acc;
         }
+        __syncthreads();
+        Xinv = invert_mode<RM>(a, sm, j, sweep > 0, status);
       }
       __syncthreads();
       PROF(4);
-      status |= gram_inverse<RM>(a, sm, j);
       PROF(5);
       if (E > 0) {
         // X = A^-1 rhs  (columns of rhs are rows of rb)      (cp.py:317)
@@ -470,15 +625,17 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         for (int e = tid; e < E; e += ALS_NT) {
           const int sc = e / r, i = e % r;
           double acc = 0.0;
-          for (int k = 0; k < r; ++k) acc = fma(sm.Ai[i * rp + k], sm.rb[sc * r + k], acc);
+          for (int k = 0; k < r; ++k) acc = fma(Xinv[i * rp + k], sm.rb[sc * r + k], acc);
           if (!isfinite(acc)) nf = 1;
           Uj[(size_t)(s0 + sc) * r + i] = acc;
         }
         if (nf) atomicOr(a.info, 2);
       }
+      if (p == 0 && a.ns_max > 0)
+        for (int e = tid; e < r * rp; e += ALS_NT) a.Xprev[(size_t)j * r * rp + e] = Xinv[e];
       pending = j;
       PROF(6);
-      grid.sync();
+      grid_barrier(a.bar_ctr, epoch);
       PROF(7);
     }
     done = sweep + 1;
@@ -496,15 +653,14 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       }
       ov = block_sum(ov, sm.part);
       if (tid == 0) a.ovl[p] = ov;
-      grid.sync();
-      for (int e = tid; e < rr; e += ALS_NT)
-        sm.Gs[(size_t)pending * gk + (e / r) * gs + e % r] = __ldcg(a.G + (size_t)pending * rr + e);
+      grid_barrier(a.bar_ctr, epoch);
+      for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * rr + e] = __ldcg(a.G + (size_t)pending * rr + e);
       pending = -1;
       __syncthreads();
       double self = 0.0;
       for (int e = tid; e < rr; e += ALS_NT) {
         double v = 1.0;
-        for (int k = 0; k < a.d; ++k) v *= sm.Gs[(size_t)k * gk + (e / r) * gs + e % r];
+        for (int k = 0; k < a.d; ++k) v *= sm.Gs[(size_t)k * rr + e];
         self += v;
       }
       self = block_sum(self, sm.part);
@@ -593,7 +749,8 @@ static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
   pl.smem = smem;
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
   pl.ws_total = align_up(sizeof(double) * (size_t)d * r * r) + align_up(sizeof(double) * (size_t)P * P * a.ncolmax * r) +
-                align_up(sizeof(double) * (size_t)P) + align_up(sizeof(double)) + pl.ws_inner;
+                align_up(sizeof(double) * (size_t)P) + align_up(sizeof(double)) + pl.ws_inner + 256 +
+                align_up(sizeof(double) * (size_t)d * r * (r + 1));
   return TP_OK;
 }
 
@@ -602,11 +759,17 @@ static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
 using namespace tp;
 
 static long long* g_prof = nullptr;
+static int g_skip = 0;
+static int g_ns_max = 6;
 
 extern "C" {
 
 // debug hook (not part of the public header): per-phase clock64 totals of CTA 0
 void tp_debug_set_als_profile(long long* dev_ptr) { g_prof = dev_ptr; }
+// debug hook: skip phases (results are wrong) to time them by subtraction
+void tp_debug_set_als_skip(int mask) { g_skip = mask; }
+// debug hook: Newton-Schulz iteration cap (0 = always the exact sweep inversion)
+void tp_debug_set_als_ns(int n) { g_ns_max = n; }
 
 size_t tp_cp_als_ws_bytes(int d, const int* q, int R, int r, int grid) {
   AlsPlan pl;
@@ -630,12 +793,18 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
   a.ovl = cv.take<double>(pl.P);
   double* nsq = cv.take<double>(1);
   double* part = cv.take<double>(pl.ws_inner / sizeof(double));
+  a.bar_ctr = cv.take<unsigned int>(16);
+  a.Xprev = cv.take<double>((size_t)d * r * (r + 1));
+  a.ns_max = g_ns_max;
   a.V = V; a.U = U; a.trace = trace; a.info = info;
   a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = tol; a.stall = stall;
   a.need_resid = (trace != nullptr) || (tol > 0.0) || (stall > -INFINITY);
   a.norm_sq = nsq;
   a.prof = g_prof;
+  a.dbg_skip = g_skip;
   cudaError_t e = cudaMemsetAsync(info, 0, 2 * sizeof(int), s);
+  if (e != cudaSuccess) return cuda_status(e);
+  e = cudaMemsetAsync(a.bar_ctr, 0, 16 * sizeof(unsigned int), s);
   if (e != cudaSuccess) return cuda_status(e);
   if (a.need_resid) {
     st = launch_inner(d, q, R, V, R, V, 1, nsq, part, s);   // ||V||^2 (cp.py:186-188)

@@ -133,8 +133,61 @@ __device__ void inv_reg(const double* A, int r, double* pub /* 2 x 32 */, double
     }
 }
 
+// 2x2-block symmetric sweep: pivot pairs (2m, 2m+1); elements in registers;
+// rows p, q published per block step (symmetry gives the pivot columns)
+template <int NT, int EPT>
+__device__ void inv_reg2(const double* A, int r, double* pub /* 2 x 2 x 32 */, double* out, int bar_id) {
+  constexpr int TPR = 32 / EPT;
+  const int t = threadIdx.x;
+  const int i = t / TPR, c0 = t % TPR;
+  const int rp = r + 1;
+  double v[EPT];
+#pragma unroll
+  for (int u = 0; u < EPT; ++u) {
+    const int c = c0 + TPR * u;
+    v[u] = (i < r && c < r) ? A[i * rp + c] : ((i == c) ? 1.0 : 0.0);   // identity padding to 32
+  }
+  if (i < 2)
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) pub[i * 32 + c0 + TPR * u] = v[u];
+  if (NT == 256) __syncthreads(); else asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(NT));
+  const int rr = (r + 1) & ~1;
+  for (int k = 0; k < rr; k += 2) {
+    const double* Rp = pub + ((k >> 1) & 1) * 64;
+    const double* Rq = Rp + 32;
+    double* Np = pub + (((k >> 1) + 1) & 1) * 64;
+    const double a = Rp[k], b = Rp[k + 1], cc = Rq[k + 1];
+    const double idet = rcp_nr(fma(a, cc, -b * b));
+    const double p00 = cc * idet, p01 = -b * idet, p11 = a * idet;      // P^-1
+    const double xi = Rp[i], yi = Rq[i];                                // (A_ip, A_iq)
+    const double ti0 = xi * p00 + yi * p01, ti1 = xi * p01 + yi * p11;  // (A_iK P^-1)
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const int c = c0 + TPR * u;
+      const double rc0 = Rp[c], rc1 = Rq[c];
+      const double w0 = p00 * rc0 + p01 * rc1, w1 = p01 * rc0 + p11 * rc1;   // P^-1 A_Kc
+      double nv = fma(-xi, w0, fma(-yi, w1, v[u]));
+      const bool ck = (c == k) || (c == k + 1), ik = (i == k) || (i == k + 1);
+      if (ck) nv = (c == k) ? ti0 : ti1;
+      if (ik) nv = (i == k) ? w0 : w1;
+      if (ik && ck) nv = -((i == k) ? ((c == k) ? p00 : p01) : ((c == k) ? p01 : p11));
+      v[u] = nv;
+    }
+    if (i == k + 2 || i == k + 3)
+#pragma unroll
+      for (int u = 0; u < EPT; ++u) Np[(i - k - 2) * 32 + c0 + TPR * u] = v[u];
+    if (NT == 256) __syncthreads(); else asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(NT));
+  }
+  if (i < r)
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const int c = c0 + TPR * u;
+      if (c < r) out[i * rp + c] = -v[u];
+    }
+}
+
 __global__ void bench(const double* Ain, int r, int reps, int variant, long long* cyc, double* out) {
-  __shared__ double A[33 * 33], B0[33 * 33], B1[33 * 33], s[72];
+  __shared__ double A[33 * 33], B0[33 * 33], B1[33 * 33], s[160];
   for (int e = threadIdx.x; e < r * (r + 1); e += blockDim.x) A[e] = Ain[e];
   __syncthreads();
   long long t0 = clock64();
@@ -152,6 +205,9 @@ __global__ void bench(const double* Ain, int r, int reps, int variant, long long
       __syncthreads();
     } else if (variant == 4) {
       inv_reg<256, 4>(A, r, s, B0, 0);
+      __syncthreads();
+    } else if (variant == 6) {
+      inv_reg2<256, 4>(A, r, s, B0, 0);
       __syncthreads();
     } else if (variant == 5) {
       if (threadIdx.x < 64) inv_reg<64, 16>(A, r, s, B0, 1);
@@ -190,7 +246,7 @@ int main() {
   cudaMalloc(&dout, sizeof(h));
   cudaMalloc(&dc, 8);
   cudaMemcpy(dA, h, sizeof(h), cudaMemcpyHostToDevice);
-  for (int v = 0; v < 6; ++v) {
+  for (int v = 3; v < 7; ++v) {
     bench<<<1, 256>>>(dA, r, 2, v, dc, dout);
     bench<<<1, 256>>>(dA, r, 20, v, dc, dout);
     long long c;

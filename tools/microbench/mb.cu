@@ -122,6 +122,13 @@ __global__ void dsmem_kernel(int words, int iters, double* sink) {
   if (acc == -1) sink[0] = acc;
 }
 
+__global__ void clsync_kernel(int iters, double* sink) {
+  cg::cluster_group cl = cg::this_cluster();
+  double x = 0;
+  for (int i = 0; i < iters; ++i) { x += 1; cl.sync(); }
+  if (x == -1) sink[0] = x;
+}
+
 __global__ void empty_kernel(double* p) { if (threadIdx.x == 1000000) p[0] = 1; }
 
 int main() {
@@ -201,12 +208,28 @@ int main() {
     at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at; cfg.numAttrs = 1;
     if (cs > 8) CK(cudaFuncSetAttribute(dsmem_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(dsmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, words * 8));
     cudaError_t err = cudaLaunchKernelEx(&cfg, dsmem_kernel, words, 2, d);
     if (err != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) { printf("dsmem cs=%d failed: %s\n", cs, cudaGetErrorString(err)); cudaGetLastError(); continue; }
     cudaEventRecord(e0); CK(cudaLaunchKernelEx(&cfg, dsmem_kernel, words, iters, d)); cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
     double per_sm = (double)words * 8 * iters / (ms * 1e-3) / 1e9;
     printf("dsmem_read_gbs_per_cta cluster=%d %.1f (grid %d)\n", cs, per_sm, cs * (sms / cs));
+  }
+  // cluster.sync latency
+  for (int cs : {8, 16}) {
+    int iters = 4000;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * (sms / cs)); cfg.blockDim = dim3(256); cfg.dynamicSmemBytes = 0;
+    cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    if (cs > 8) CK(cudaFuncSetAttribute(clsync_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaError_t err = cudaLaunchKernelEx(&cfg, clsync_kernel, 10, d);
+    if (err != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) { printf("clsync cs=%d failed\n", cs); cudaGetLastError(); continue; }
+    cudaEventRecord(e0); CK(cudaLaunchKernelEx(&cfg, clsync_kernel, iters, d)); cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+    printf("cluster_sync_us cluster=%d %.3f\n", cs, ms * 1e3 / iters);
   }
   // graph node latency
   {
