@@ -17,8 +17,12 @@ init = first 32 input terms, BASELINE.json configs[1]) of seeded synthetic input
 * ``cpu_baseline`` -- the oracle restatement of the reference path (complex128,
   like the shipped reference) timed on this host's cores on a bounded sample.
 
-N > 1 (torchrun): each rank runs an independent truncation (weak scaling,
-replicas); the input-rank-sharded path is not in this round.
+N > 1 (torchrun): ``--mode sharded`` (default for N > 1) shards the R input terms
+of ONE config-1 truncation across ranks with an NCCL all-reduce of the r x Q
+right-hand side per mode update (strong scaling, BASELINE configs[1]);
+``--mode replicas`` runs an independent truncation per rank (weak scaling).
+``extra_configs`` reports device-resident throughput of configs 0, 2, 3 (rank 0,
+N = 1) and of config 4 (batch of 64 HT tensors sharded across ranks).
 """
 
 from __future__ import annotations
@@ -146,6 +150,129 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def extra_configs(world, rank, dev):
+    """Device-resident throughput of the other BASELINE configs through the public API."""
+    import torch
+    from paper_1803_10270_b200 import cp, explicit, ht, implicit, operators, workloads
+    out = {}
+
+    def timed(fn, reps=1):
+        fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # config 4: 64 HT tensors, batch-sharded across ranks (no communication)
+    w4 = workloads.cfg4(0)
+    lo, hi = (64 * rank) // world, (64 * (rank + 1)) // world
+    from paper_1803_10270_b200 import _lib
+    F = torch.as_tensor(w4["frames"][lo:hi]).to(dev)
+    B = torch.as_tensor(w4["transfers"][lo:hi]).to(dev)
+    nb, d, Q, k, ro = hi - lo, w4["d"], w4["Q"], w4["k"], 16
+    OF = torch.zeros((nb, d, Q, ro), dtype=torch.float64, device=dev)
+    OB = torch.zeros((nb, d - 1, ro, ro, ro), dtype=torch.float64, device=dev)
+    rk = torch.zeros((nb, 2 * d - 1), dtype=torch.int32, device=dev)
+    est = torch.zeros(nb, dtype=torch.float64, device=dev)
+    nrm = torch.zeros(nb, dtype=torch.float64, device=dev)
+    L = _lib.lib()
+    ws = torch.empty(L.tp_ht_truncate_ws_bytes(d, Q, k, nb), dtype=torch.uint8, device=dev)
+
+    def c4():
+        _lib.check(L.tp_ht_truncate_f64(d, Q, k, nb, F.data_ptr(), B.data_ptr(), ro, 0.0, OF.data_ptr(),
+                                        OB.data_ptr(), rk.data_ptr(), est.data_ptr(), nrm.data_ptr(), ws.data_ptr(),
+                                        ws.numel(), _lib.stream_ptr(dev)))
+    ms = timed(c4, 3)
+    out["cfg4_hsvd_batch64"] = {"value": 64 / ms * 1e3, "unit": "tensors/s", "ms_per_batch": ms,
+                                "flops_per_tensor": 1.52e9, "achieved_tflops": 64 * 1.52e9 / (ms * 1e-3) / 1e12,
+                                "sharding": f"batch {nb} per rank"}
+    del F, B, OF, OB, ws
+    if world > 1:
+        return out
+    w0 = workloads.cfg0(0)
+    L0 = operators.advection_operator(w0["a"], w0["specs"])
+    c0 = explicit.ExplicitConfig(dt=w0["dt"], r_max=w0["r"], recipe="fused",
+                                 als=cp.ALSApproxConfig(max_sweeps=w0["sweeps"], stall=-np.inf, reg=w0["lam"]))
+    f0 = cp.CPTensor(w0["specs"], w0["ic"]["factors"])
+    ms = timed(lambda: explicit.run(f0, L0, c0, w0["steps"]))
+    out["cfg0_advection_explicit"] = {"value": w0["steps"] / ms * 1e3, "unit": "time-steps/s",
+                                      "ms_per_run_100_steps": ms}
+    w3 = workloads.cfg3(0)
+    L3 = operators.SeparableOperator(w3["specs"], tuple(w3["weights"]), tuple(tuple(m) for m in w3["mats"]))
+    c3 = explicit.ExplicitConfig(dt=w3["dt"], r_max=w3["r"], recipe="fused",
+                                 als=cp.ALSApproxConfig(max_sweeps=w3["sweeps"], stall=-np.inf, reg=w3["lam"]))
+    f3 = cp.CPTensor(w3["specs"], w3["factors"])
+    ms = timed(lambda: explicit.run(f3, L3, c3, w3["steps"]))
+    out["cfg3_bgk_explicit"] = {"value": w3["steps"] / ms * 1e3, "unit": "time-steps/s",
+                                "ms_per_run_200_steps": ms}
+    w2 = workloads.cfg2(0)
+    pair = operators.implicit_euler_pair(operators.advection_operator(w2["a"], w2["specs"]), w2["dt"])
+    c2 = implicit.ALSStepConfig(dt=w2["dt"], eps_tol=0.0, max_sweeps=w2["sweeps"], delta_beta=1.0,
+                                schedule="gauss-seidel", lam=w2["lam"])
+    f2 = cp.CPTensor(w2["specs"], w2["ic"]["factors"])
+    steps2 = 2
+    ms = timed(lambda: implicit.run(f2, pair, c2, steps2))
+    out["cfg2_implicit_euler"] = {"value": steps2 / ms * 1e3, "unit": "time-steps/s",
+                                  "sample": f"{steps2} of 50 steps", "ms_per_step": ms / steps2}
+    _ = ht
+    return out
+
+
+def run_sharded(args, world, rank, local, dev):
+    """One config-1 truncation R-sharded across ranks (strong scaling)."""
+    import torch
+    from paper_1803_10270_b200 import cp, parallel, workloads
+    w = workloads.cfg1(seed=0)
+    lo, hi = parallel.shard_range(R, world, rank)
+    specs = w["specs"]
+    Vs = cp.CPTensor(specs, [v[:, lo:hi] for v in w["V"]])
+    I0 = cp.CPTensor(specs, w["init"])
+    cfg = cp.ALSApproxConfig(max_sweeps=SWEEPS, tol=0.0, stall=-np.inf, reg=LAM)
+    comm = parallel.TorchDistComm() if world > 1 else parallel.LocalComm()
+    ops = parallel.DeviceShardOps(Vs, RANK_R)
+    U = I0.data.clone()
+    drv = parallel.ShardedALS(ops, comm, cfg)
+    stream = torch.cuda.current_stream(dev)
+    U.copy_(I0.data)
+    drv.capture(U, D)      # whole truncation (2520 launches incl. 120 all-reduces) as one CUDA graph
+
+    def one():
+        U.copy_(I0.data)
+        drv.replay()
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            one()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ops.check()
+    tot_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    return tot_ms, clk.summary()
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -153,6 +280,30 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mode = args.mode or ("sharded" if world > 1 else "fused")
+    if mode == "sharded":
+        dev = torch.device("cuda", local)
+        tot_ms, clocks = run_sharded(args, world, rank, local, dev)
+        ms_per_step = tot_ms / args.steps
+        value = args.steps * SWEEPS / (tot_ms / 1e3)
+        extras = extra_configs(world, rank, dev) if not args.no_extra else {}
+        if rank == 0:
+            achieved_tf = FLOPS_PER_STEP / (ms_per_step / 1e3) / 1e12
+            line = {"metric": "CP-ALS sweeps/s", "value": value, "unit": "sweeps/s", "n_gpus": world,
+                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                    "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, seed 0)",
+                    "config": {"workload": WORKLOAD, "parallelism": f"R-sharded x{world} (NCCL all-reduce of the "
+                                                                   f"r x Q rhs per mode update)",
+                               "l2": "inputs L2-resident, not flushed (host-orchestrated mode steps)"},
+                    "roofline": {"bound": "tensor", "achieved": achieved_tf / world, "peak": FP64_PEAK_TFLOPS,
+                                 "unit": "TFLOP/s", "frac": achieved_tf / world / FP64_PEAK_TFLOPS, "traffic": None,
+                                 "kernel": "tp_als_shard_* mode steps (per GPU)"},
+                    "gpu_launches": args.steps * (SWEEPS * D * 6 + 2 * D), "clocks": clocks,
+                    "extra_configs": extras}
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
     from paper_1803_10270_b200 import cp, workloads
     from paper_1803_10270_b200 import _lib
     dev = torch.device("cuda", local)
@@ -243,7 +394,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1)/sqrt(Q), seed = rank)",
             "config": {"workload": WORKLOAD, "l2": "flushed (256 MiB write) between timed steps",
                        "grid_ctas": args.grid or "auto", "target_norm": "not computed (no trace / stopping rule)",
-                       "multi_gpu": "independent replicas per rank" if world > 1 else "single GPU"},
+                       "multi_gpu": "independent replicas per rank (weak)" if world > 1 else "single GPU"},
             "e2e": {"value": e2e_val, "unit": "sweeps/s", "h2d_bytes_per_step": int((hV.numel() + hI.numel()) * 8),
                     "d2h_bytes_per_step": int(hOut.numel() * 8 + 8)},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -258,6 +409,9 @@ def run_ours(args):
         }
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_run(args.cpu_seconds)
+    extras = extra_configs(world, rank, dev) if not args.no_extra else {}
+    if rank == 0:
+        line["extra_configs"] = extras
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -273,6 +427,8 @@ def main():
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--mode", choices=["fused", "sharded", "replicas"], default=None)
+    ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

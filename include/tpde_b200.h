@@ -81,6 +81,24 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
                   double* trace, int* info, int grid, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Input-rank-sharded CP-ALS mode steps (BASELINE cfg1 multi-GPU).
+ * A rank holds the target slab V (rank R_l = its share of the R input terms,
+ * CP layout), the replicated guess U (rank r), its cross slab C (d x r x R_l)
+ * and the replicated Grams G (d x r x r).  Per mode update j (cp.py:310-320):
+ *   tp_als_shard_rhs_f64    rhs (r x Q_j) = (prod_{k!=j} C_k) V_j^T over the slab
+ *   <allreduce rhs across ranks>
+ *   tp_als_shard_update_f64 U_j = (A_j^-1 rhs)^T, G_j, C_j[:, slab]
+ * ------------------------------------------------------------------------- */
+size_t tp_als_shard_ws_bytes(int d, const int* q, int Rl, int r);
+int tp_als_shard_init_f64(int d, const int* q, int Rl, const double* V, int r, const double* U, double* C,
+                          double* G, void* stream);
+int tp_als_shard_rhs_f64(int d, const int* q, int Rl, const double* V, int r, const double* C, int j,
+                         double* rhs, void* ws, size_t ws_bytes, void* stream);
+int tp_als_shard_update_f64(int d, const int* q, int Rl, const double* V, int r, double* U, double* C, double* G,
+                            int j, const double* rhs, double reg, int reg_mode, int* info, void* ws,
+                            size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Separable operator apply + concatenation (operators.apply,
  * operators.py:48-62; cp.add/scale, cp.py:98-108).
  * For each term t (0..n_terms-1) and mode k, writes

@@ -56,6 +56,11 @@ _SIGNATURES = {
     "tp_cp_als_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _i, _d, _i, _d, _d, _vp, _vp, _i, _vp, _sz, _vp]),
     "tp_cp_apply_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _c_double_p, _d, _c_int_p, _vp, _c_ll_p, _i,
                              _vp, _i, _i, _vp]),
+    "tp_als_shard_ws_bytes": (_sz, [_i, _c_int_p, _i, _i]),
+    "tp_als_shard_init_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _vp, _vp, _vp]),
+    "tp_als_shard_rhs_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _i, _vp, _vp, _sz, _vp]),
+    "tp_als_shard_update_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _vp, _vp, _i, _vp, _d, _i, _vp, _vp, _sz,
+                                     _vp]),
     "tp_ht_truncate_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "tp_ht_truncate_f64": (_i, [_i, _i, _i, _i, _vp, _vp, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "tp_implicit_ws_bytes": (_sz, [_i, _i, _i, _i]),

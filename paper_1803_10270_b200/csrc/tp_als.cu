@@ -823,3 +823,143 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Input-rank-sharded ALS mode steps: a rank holds V[:, :, slab]
+// (R_l columns) and the replicated guess U.  Per mode update j the host runs
+//   tp_als_shard_rhs   (local partial of the right-hand side, r x Q_j)
+//   allreduce           (NCCL over NVLink / gloo; sum over ranks)
+//   tp_als_shard_update (A_j^-1, U_j, G_j, C_j[:, slab])
+// which reproduces cp_approx_als (cp.py:310-320) up to summation order.
+// ===========================================================================
+#include "tp_gemm.cuh"
+
+namespace tp {
+
+struct ShardDims {
+  int d, Rl, r, qmax;
+  int q[TP_MAXD];
+  long long offV[TP_MAXD], offU[TP_MAXD];
+};
+
+static int shard_dims(int d, const int* q, int Rl, int r, ShardDims& s) {
+  if (d < 1 || d > TP_MAXD || Rl < 1 || r < 1 || r > 32 || !q) return TP_EINVAL;
+  memset(&s, 0, sizeof(s));
+  s.d = d; s.Rl = Rl; s.r = r;
+  long long ov = 0, ou = 0;
+  for (int k = 0; k < d; ++k) {
+    if (q[k] < 1) return TP_EINVAL;
+    s.q[k] = q[k]; s.offV[k] = ov; s.offU[k] = ou;
+    ov += (long long)q[k] * Rl; ou += (long long)q[k] * r;
+    s.qmax = q[k] > s.qmax ? q[k] : s.qmax;
+  }
+  return TP_OK;
+}
+
+// hadT[c][l] = prod_{k != j} C_k[l][c]
+__global__ void shard_had_kernel(int d, int r, int Rl, int j, const double* C, double* hadT) {
+  const int n = r * Rl;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int c = e / r, l = e % r;
+    double v = 1.0;
+    for (int k = 0; k < d; ++k)
+      if (k != j) v *= C[((size_t)k * r + l) * Rl + c];
+    hadT[e] = v;
+  }
+}
+
+// one CTA: A = prod_{k!=j} G_k + lambda I, inverse by the symmetric sweep
+template <int RM>
+__global__ void __launch_bounds__(ALS_NT) shard_inverse_kernel(int d, int r, int j, const double* G, double reg,
+                                                               int reg_mode, double* Ainv, int* info) {
+  extern __shared__ double ss[];
+  AlsArgs a;
+  memset(&a, 0, sizeof(a));
+  a.d = d; a.r = r; a.reg = reg; a.reg_mode = reg_mode;
+  Smem sm;
+  memset(&sm, 0, sizeof(sm));
+  sm.Gs = ss;
+  sm.pub = sm.Gs + (size_t)d * r * r;
+  sm.part = sm.pub + 72;
+  for (int e = threadIdx.x; e < d * r * r; e += ALS_NT) sm.Gs[e] = G[e];
+  __syncthreads();
+  const int bad = gram_inverse<RM>(a, sm, j, Ainv);
+  if (bad && threadIdx.x == 0) atomicOr(info, 1);
+}
+
+static cudaError_t gemm(int M, int N, int K, const double* A, long long sAm, long long sAk, const double* B,
+                        long long sBk, long long sBn, double* C, long long sCm, long long sCn, cudaStream_t st) {
+  return bgemm_launch(bgemm_desc(M, N, K, A, sAm, sAk, B, sBk, sBn, C, sCm, sCn), st);
+}
+
+}  // namespace tp
+
+extern "C" {
+
+size_t tp_als_shard_ws_bytes(int d, const int* q, int Rl, int r) {
+  ShardDims s;
+  if (shard_dims(d, q, Rl, r, s) != TP_OK) return 0;
+  return align_up(8 * (size_t)r * Rl) + align_up(8 * (size_t)r * (r + 1)) + 256;
+}
+
+int tp_als_shard_init_f64(int d, const int* q, int Rl, const double* V, int r, const double* U, double* C,
+                          double* G, void* stream) {
+  ShardDims s;
+  int st = shard_dims(d, q, Rl, r, s);
+  if (st != TP_OK) return st;
+  if (!V || !U || !C || !G) return TP_EINVAL;
+  cudaStream_t cs = (cudaStream_t)stream;
+  for (int k = 0; k < d; ++k) {
+    const double* Uk = U + s.offU[k];
+    cudaError_t e = gemm(r, Rl, s.q[k], Uk, 1, r, V + s.offV[k], Rl, 1, C + (size_t)k * r * Rl, Rl, 1, cs);
+    if (e == cudaSuccess) e = gemm(r, r, s.q[k], Uk, 1, r, Uk, r, 1, G + (size_t)k * r * r, r, 1, cs);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  return TP_OK;
+}
+
+int tp_als_shard_rhs_f64(int d, const int* q, int Rl, const double* V, int r, const double* C, int j,
+                         double* rhs, void* ws, size_t ws_bytes, void* stream) {
+  ShardDims s;
+  int st = shard_dims(d, q, Rl, r, s);
+  if (st != TP_OK) return st;
+  if (!V || !C || !rhs || j < 0 || j >= d) return TP_EINVAL;
+  if (!ws || ws_bytes < tp_als_shard_ws_bytes(d, q, Rl, r)) return TP_EWORKSPACE;
+  cudaStream_t cs = (cudaStream_t)stream;
+  double* hadT = static_cast<double*>(ws);
+  shard_had_kernel<<<(r * Rl + 255) / 256, 256, 0, cs>>>(d, r, Rl, j, C, hadT);
+  // rhs[l][s] = sum_c had[l][c] V_j[s][c]      (cp.py:197-203)
+  cudaError_t e = gemm(r, s.q[j], Rl, hadT, 1, r, V + s.offV[j], 1, Rl, rhs, s.q[j], 1, cs);
+  return cuda_status(e == cudaSuccess ? cudaGetLastError() : e);
+}
+
+int tp_als_shard_update_f64(int d, const int* q, int Rl, const double* V, int r, double* U, double* C, double* G,
+                            int j, const double* rhs, double reg, int reg_mode, int* info, void* ws,
+                            size_t ws_bytes, void* stream) {
+  ShardDims s;
+  int st = shard_dims(d, q, Rl, r, s);
+  if (st != TP_OK) return st;
+  if (!V || !U || !C || !G || !rhs || !info || j < 0 || j >= d || !(reg >= 0.0)) return TP_EINVAL;
+  if (!ws || ws_bytes < tp_als_shard_ws_bytes(d, q, Rl, r)) return TP_EWORKSPACE;
+  cudaStream_t cs = (cudaStream_t)stream;
+  double* Ainv = static_cast<double*>(ws) + align_up(8 * (size_t)r * Rl) / 8;
+  const int rm = r <= 8 ? 8 : (r <= 16 ? 16 : 32);
+  const size_t smem = sizeof(double) * ((size_t)d * r * r + 72 + ALS_PART);
+  const void* fn = rm == 8 ? (const void*)shard_inverse_kernel<8>
+                           : (rm == 16 ? (const void*)shard_inverse_kernel<16> : (const void*)shard_inverse_kernel<32>);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (rm == 8) shard_inverse_kernel<8><<<1, ALS_NT, smem, cs>>>(d, r, j, G, reg, reg_mode, Ainv, info);
+  else if (rm == 16) shard_inverse_kernel<16><<<1, ALS_NT, smem, cs>>>(d, r, j, G, reg, reg_mode, Ainv, info);
+  else shard_inverse_kernel<32><<<1, ALS_NT, smem, cs>>>(d, r, j, G, reg, reg_mode, Ainv, info);
+  cudaError_t e = cudaGetLastError();
+  double* Uj = U + s.offU[j];
+  const int Q = s.q[j], rp = r + 1;
+  // U_j[s][i] = sum_m Ainv[i][m] rhs[m][s]       (cp.py:317)
+  if (e == cudaSuccess) e = gemm(Q, r, r, rhs, 1, Q, Ainv, 1, rp, Uj, r, 1, cs);
+  // G_j = U_j^T U_j, C_j[:, slab] = U_j^T V_j[:, slab]   (cp.py:318-320)
+  if (e == cudaSuccess) e = gemm(r, r, Q, Uj, 1, r, Uj, r, 1, G + (size_t)j * r * r, r, 1, cs);
+  if (e == cudaSuccess) e = gemm(r, Rl, Q, Uj, 1, r, V + s.offV[j], Rl, 1, C + (size_t)j * r * Rl, Rl, 1, cs);
+  return cuda_status(e);
+}
+
+}  // extern "C"
