@@ -152,6 +152,10 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
  *   schedule: 0 Gauss-Seidel, 1 Jacobi; delta_beta damping (implicit.py:281-282)
  *   orientation: 0 corrected normal equations, 1 reference build_gamma
  *             (implicit.py:137-139)
+ *   circ_eig: NULL (dense path: assembled (rQ)^2 system, blocked Cholesky) or,
+ *             when every table is circulant, device n_tab x Q x 2 eigenvalues
+ *             lambda_t(k) = sum_m tabs[t][m][0] e^{-2 pi i m k/Q}: the system is
+ *             solved per DFT frequency (Q Hermitian r x r solves), same minimiser
  *   eps_conv: device double (last sweep's largest relative update)
  *   info    : device int[2] {status bits, sweeps done}
  * ------------------------------------------------------------------------- */
@@ -159,7 +163,8 @@ size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab);
 int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* tabs, const int* tab_id,
                          const double* KL, const double* KR, const double* f_old, double* f_new,
                          int sweeps, int schedule, double delta_beta, double eps_tol, double lam,
-                         int orientation, double* eps_conv, int* info, void* ws, size_t ws_bytes, void* stream);
+                         int orientation, const double* circ_eig, double* eps_conv, int* info, void* ws,
+                         size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -18,6 +18,7 @@
 #include "tp_gemm.cuh"
 #include <cstring>
 #include <vector>
+#include <cmath>
 
 namespace tp {
 
@@ -234,12 +235,195 @@ __global__ void __launch_bounds__(256) conv_damp_kernel(int Q, int r, int d, dou
     }
     __syncthreads();
   }
-  for (size_t e = threadIdx.x; e < (size_t)d * Q * r; e += 256)
-    bnew[e] = bint[e] + (bnew[e] - bint[e]) / delta_beta;
+  if (delta_beta > 0.0)
+    for (size_t e = threadIdx.x; e < (size_t)d * Q * r; e += 256)
+      bnew[e] = bint[e] + (bnew[e] - bint[e]) / delta_beta;
   if (threadIdx.x == 0) *eps_out = worst;
 }
 
 __global__ void set_int_kernel(int* dst, int v) { *dst = v; }
+
+// Fused Gram refresh of mode k for every table it uses (one CTA per table):
+//   G[k][t]  = b_new,k^T T_t b_new,k      Gm[k][t] = b_new,k^T T~_t b_old,k
+// (T~ = T for the corrected normal equations, T^T for the reference orientation)
+struct GramArgs {
+  int Q, r, k, n_tab, transT, nt;
+  int ts[IM_MAXT];
+  const double* tabs;
+  const double* bnew;   // mode k block (Q x r)
+  const double* bold;   // mode k block (Q x r)
+  double* G;
+  double* Gm;
+};
+
+__global__ void __launch_bounds__(256) mode_grams_kernel(const __grid_constant__ GramArgs a) {
+  extern __shared__ double gsm[];
+  const int t = a.ts[blockIdx.x], Q = a.Q, r = a.r, tid = threadIdx.x;
+  double* bn = gsm;                 // Q x r
+  double* bo = bn + (size_t)Q * r;  // Q x r
+  double* tb = bo + (size_t)Q * r;  // Q x r  (T b_new)
+  double* tc = tb + (size_t)Q * r;  // Q x r  (T~ b_old)
+  for (int e = tid; e < Q * r; e += 256) { bn[e] = a.bnew[e]; bo[e] = a.bold[e]; }
+  __syncthreads();
+  const double* T = a.tabs + (size_t)t * Q * Q;
+  for (int e = tid; e < Q * r; e += 256) {
+    const int row = e / r, c = e % r;
+    double s1 = 0.0, s2 = 0.0;
+    for (int m = 0; m < Q; ++m) {
+      const double tv = T[(size_t)row * Q + m];
+      const double tt = a.transT ? T[(size_t)m * Q + row] : tv;
+      s1 = fma(tv, bn[m * r + c], s1);
+      s2 = fma(tt, bo[m * r + c], s2);
+    }
+    tb[e] = s1;
+    tc[e] = s2;
+  }
+  __syncthreads();
+  const size_t go = ((size_t)a.k * a.n_tab + t) * r * r;
+  for (int e = tid; e < r * r; e += 256) {
+    const int l = e / r, n = e % r;
+    double s1 = 0.0, s2 = 0.0;
+    for (int m = 0; m < Q; ++m) {
+      const double b = bn[m * r + l];
+      s1 = fma(b, tb[m * r + n], s1);
+      s2 = fma(b, tc[m * r + n], s2);
+    }
+    a.G[go + e] = s1;
+    a.Gm[go + e] = s2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Circulant fast path: when every pairing table is circulant (Fourier
+// collocation operators), M_q = sum_X H_X^T (x) T_X^T + lam I is block-diagonal
+// in the DFT basis of the mode index: for frequency k,
+//   M^_k[i][j] = sum_X conj(lambda_X(k)) H_X[j][i] + lam delta_ij   (r x r, Hermitian PD)
+// with lambda_X(k) = sum_m T_X[m][0] e^{-2 pi i m k / Q}.  One CTA per frequency
+// forms gamma^(k) (direct DFT), M^_k, and solves by complex Cholesky; the
+// inverse DFT returns the real solution.  Same linear system as the dense path.
+// ---------------------------------------------------------------------------
+struct CircArgs {
+  int Q, r, nX, d, ra, q, n_tab;
+  int xs[IM_MAXT];
+  int tab[IM_MAXD * IM_MAXRA * IM_MAXRA];
+  double KL[IM_MAXRA * IM_MAXRA], KR[IM_MAXRA * IM_MAXRA];
+  const double* G;      // [d][n_tab][r][r]
+  const double* Gm;
+  const double* W;      // [d][n_tab][Q][r] images T~ b_old
+  const double* H;      // [nX][r][r]  ([j][i])
+  const double* eig;    // [n_tab][Q][2]
+  const double* gam;    // [r][Q] (index i*Q + a)
+  const double* tw;     // [Q][2]: cos, sin of 2 pi m / Q
+  double* xhat;         // [r][Q][2]
+  double lam;
+  int* info;
+};
+
+__global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__ CircArgs a) {
+  extern __shared__ double cs[];
+  const int k = blockIdx.x, r = a.r, Q = a.Q, tid = threadIdx.x, rr = r * r;
+  const int ld = r + 1;
+  double* Mre = cs;                       // [r][ld]
+  double* Mim = Mre + r * ld;
+  double* gre = Mim + r * ld;             // [r]
+  double* gim = gre + r;
+  const double* Hs = a.H;                 // [nX][r][r]  H_X[j][i] (form_h_kernel)
+  const double* gam = a.gam;              // [r][Q]  (gamma_kernel)
+  const double inv_sqrt = rsqrt((double)Q);
+  // gamma^(k)_i = sum_a gamma[i][a] e^{-2 pi i a k / Q} / sqrt(Q)
+  for (int i = tid; i < r; i += 256) {
+    double re = 0.0, im = 0.0;
+    for (int aa = 0; aa < Q; ++aa) {
+      const int m = (int)(((long long)aa * k) % Q);
+      const double g = gam[(size_t)i * Q + aa];
+      re = fma(g, a.tw[2 * m], re);
+      im = fma(-g, a.tw[2 * m + 1], im);
+    }
+    gre[i] = re * inv_sqrt;
+    gim[i] = im * inv_sqrt;
+  }
+  for (int e = tid; e < r * r; e += 256) {
+    const int i = e / r, j = e % r;
+    double re = (i == j) ? a.lam : 0.0, im = 0.0;
+    for (int x = 0; x < a.nX; ++x) {
+      const double h = Hs[(size_t)x * r * r + j * r + i];
+      const double* lm = a.eig + ((size_t)a.xs[x] * Q + k) * 2;
+      re = fma(h, lm[0], re);
+      im = fma(-h, lm[1], im);          // conj(lambda)
+    }
+    Mre[i * ld + j] = re;
+    Mim[i * ld + j] = im;
+  }
+  __syncthreads();
+  // complex Cholesky M = L L^H (lower, in place) and forward/back substitution
+  int bad = 0;
+  for (int p = 0; p < r; ++p) {
+    const double dpp = Mre[p * ld + p];
+    if (!(dpp > 0.0) || !isfinite(dpp)) bad = 1;
+    const double d = sqrt(fabs(dpp)), id = 1.0 / d;
+    __syncthreads();
+    if (tid == 0) { Mre[p * ld + p] = d; Mim[p * ld + p] = 0.0; }
+    for (int i = p + 1 + tid; i < r; i += 256) { Mre[i * ld + p] *= id; Mim[i * ld + p] *= id; }
+    __syncthreads();
+    const int m = r - p - 1;
+    for (int e = tid; e < m * m; e += 256) {
+      const int i = p + 1 + e / m, c = p + 1 + e % m;
+      if (c <= i) {   // M[i][c] -= L[i][p] conj(L[c][p])
+        const double ar = Mre[i * ld + p], ai = Mim[i * ld + p], br = Mre[c * ld + p], bi = Mim[c * ld + p];
+        Mre[i * ld + c] -= ar * br + ai * bi;
+        Mim[i * ld + c] -= ai * br - ar * bi;
+      }
+    }
+    __syncthreads();
+  }
+  if (bad && tid == 0) atomicOr(a.info, 1);
+  if (tid == 0) {
+    for (int i = 0; i < r; ++i) {            // L y = g
+      double re = gre[i], im = gim[i];
+      for (int c = 0; c < i; ++c) {
+        const double lr = Mre[i * ld + c], li = Mim[i * ld + c];
+        re -= lr * gre[c] - li * gim[c];
+        im -= lr * gim[c] + li * gre[c];
+      }
+      const double dd = Mre[i * ld + i];
+      gre[i] = re / dd; gim[i] = im / dd;
+    }
+    for (int i = r - 1; i >= 0; --i) {       // L^H x = y
+      double re = gre[i], im = gim[i];
+      for (int c = i + 1; c < r; ++c) {      // conj(L[c][i]) x_c
+        const double lr = Mre[c * ld + i], li = -Mim[c * ld + i];
+        re -= lr * gre[c] - li * gim[c];
+        im -= lr * gim[c] + li * gre[c];
+      }
+      const double dd = Mre[i * ld + i];
+      gre[i] = re / dd; gim[i] = im / dd;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < r; i += 256) {
+    a.xhat[((size_t)i * Q + k) * 2] = gre[i];
+    a.xhat[((size_t)i * Q + k) * 2 + 1] = gim[i];
+  }
+}
+
+// beta_q[c][j] = Re sum_k xhat[j][k] e^{+2 pi i c k / Q} / sqrt(Q)
+__global__ void circ_idft_kernel(int Q, int r, const double* xhat, const double* tw, double* beta_q, int* info) {
+  const int n = Q * r;
+  const double inv_sqrt = rsqrt((double)Q);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int c = e / r, j = e % r;
+    double acc = 0.0;
+    for (int k = 0; k < Q; ++k) {
+      const int m = (int)(((long long)c * k) % Q);
+      const double* xh = xhat + ((size_t)j * Q + k) * 2;
+      acc = fma(xh[0], tw[2 * m], acc);
+      acc = fma(-xh[1], tw[2 * m + 1], acc);
+    }
+    acc *= inv_sqrt;
+    if (!isfinite(acc)) atomicOr(info, 2);
+    beta_q[e] = acc;
+  }
+}
 
 static int padded_n(int n) { return (n + CH_NB - 1) / CH_NB * CH_NB; }
 
@@ -247,13 +431,14 @@ static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
   const size_t n = (size_t)padded_n(r * Q);
   size_t s = 0;
   s += align_up(8 * (size_t)d * n_tab * r * r) * 2;     // G, Gm
-  s += align_up(8 * (size_t)d * n_tab * Q * r) * 2;     // TB scratch, W (b_old images)
+  s += align_up(8 * (size_t)d * n_tab * Q * r) * 3;     // TB, TC scratch, W (b_old images)
   s += align_up(8 * (size_t)n_tab * r * r) * 2;         // H, Hg
   s += align_up(8 * n * n);                             // M
   s += align_up(8 * (n / CH_NB + 1) * CH_NB * CH_NB);   // Linv blocks
   s += align_up(8 * n) * 3;                             // gamma, x, y
   s += align_up(8 * (size_t)d * Q * r) * 2;             // b_int, Jacobi staging
-  s += align_up(4 * IM_MAXT) + 256;
+  s += align_up(4 * IM_MAXT) + 256 + align_up(8 * 6 * (size_t)d * IM_MAXT);   // + Gram GEMM offset tables
+  s += align_up(8 * (size_t)r * Q * 2) + align_up(8 * (size_t)Q * 2);   // circulant: xhat, twiddles
   return s;
 }
 
@@ -271,7 +456,8 @@ size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab) {
 int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* tabs, const int* tab_id,
                          const double* KL, const double* KR, const double* f_old, double* f_new,
                          int sweeps, int schedule, double delta_beta, double eps_tol, double lam,
-                         int orientation, double* eps_conv, int* info, void* ws, size_t ws_bytes, void* stream) {
+                         int orientation, const double* circ_eig, double* eps_conv, int* info, void* ws,
+                         size_t ws_bytes, void* stream) {
   if (d < 1 || d > IM_MAXD || Q < 1 || r < 1 || ra < 1 || ra > IM_MAXRA || n_tab < 1 || n_tab > IM_MAXT) return TP_EINVAL;
   if (!tabs || !tab_id || !KL || !KR || !f_old || !f_new || !eps_conv || !info || sweeps < 0) return TP_EINVAL;
   if (!(delta_beta >= 1.0) || !(lam >= 0.0) || (schedule != 0 && schedule != 1)) return TP_EINVAL;
@@ -284,6 +470,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   double* G = cv.take<double>((size_t)d * n_tab * rr);
   double* Gm = cv.take<double>((size_t)d * n_tab * rr);
   double* TB = cv.take<double>((size_t)d * n_tab * QR);
+  double* W2 = cv.take<double>((size_t)d * n_tab * QR);
   double* W = cv.take<double>((size_t)d * n_tab * QR);
   double* H = cv.take<double>((size_t)n_tab * rr);
   double* Hg = cv.take<double>((size_t)n_tab * rr);
@@ -296,6 +483,20 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   double* bjac = cv.take<double>((size_t)d * QR);
   int* xs_dev = cv.take<int>(IM_MAXT);
   (void)xs_dev;
+  int* xs_modes = reinterpret_cast<int*>(Linv + (size_t)(n / CH_NB) * CH_NB * CH_NB);   // spare tail block
+  double* xhat = cv.take<double>((size_t)r * Q * 2);
+  double* tw = cv.take<double>((size_t)Q * 2);
+  if (circ_eig) {
+    std::vector<double> htw((size_t)Q * 2);
+    for (int m = 0; m < Q; ++m) {
+      htw[2 * m] = cos(2.0 * M_PI * m / Q);
+      htw[2 * m + 1] = sin(2.0 * M_PI * m / Q);
+    }
+    cudaError_t e0 = cudaMemcpyAsync(tw, htw.data(), htw.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                     (cudaStream_t)stream);
+    if (e0 != cudaSuccess) return cuda_status(e0);
+    cudaStreamSynchronize((cudaStream_t)stream);   // htw is a host temporary
+  }
 
   // distinct tables per mode
   std::vector<std::vector<int>> used(d);
@@ -321,6 +522,19 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     }
     return cudaSuccess;
   };
+  const size_t gk_smem = sizeof(double) * 4 * QR;
+  const bool fused_grams = gk_smem <= 200 * 1024;
+  if (fused_grams) cudaFuncSetAttribute(mode_grams_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gk_smem);
+  // G[k] and Gm[k] for every table of mode k in one launch
+  auto refresh = [&](int k, int transT) -> cudaError_t {
+    GramArgs ga;
+    memset(&ga, 0, sizeof(ga));
+    ga.Q = Q; ga.r = r; ga.k = k; ga.n_tab = n_tab; ga.transT = transT; ga.nt = (int)used[k].size();
+    for (int i = 0; i < ga.nt; ++i) ga.ts[i] = used[k][i];
+    ga.tabs = tabs; ga.bnew = f_new + (size_t)k * QR; ga.bold = f_old + (size_t)k * QR; ga.G = G; ga.Gm = Gm;
+    mode_grams_kernel<<<ga.nt, 256, gk_smem, st>>>(ga);
+    return cudaGetLastError();
+  };
   auto grams = [&](int k, const double* aa, const double* bsrc, double* dstG, int transT) -> cudaError_t {
     cudaError_t e = images(k, bsrc, TB, transT);
     if (e != cudaSuccess) return e;
@@ -333,9 +547,45 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     return cudaSuccess;
   };
   const int tr = orientation ? 1 : 0;
+  // per mode: TB_t = T_t b_new and TC_t = T~_t b_old for all its tables (two batched
+  // GEMMs), then G = b_new^T TB, Gm = b_new^T TC (two batched GEMMs)
+  std::vector<long long> gofs;
+  std::vector<size_t> gofs_at(d);
   for (int k = 0; k < d; ++k) {
-    if ((err = grams(k, f_new, f_new, G, 0)) != cudaSuccess) return cuda_status(err);
-    if ((err = grams(k, f_new, f_old, Gm, tr)) != cudaSuccess) return cuda_status(err);
+    gofs_at[k] = gofs.size();
+    for (int t : used[k]) {        // [A, B, C] triples; TC lives after TB in the TB scratch
+      gofs.insert(gofs.end(), {(long long)t * Q * Q, (long long)(k * QR), (long long)((k * n_tab + t) * QR)});
+    }
+    for (int t : used[k]) {
+      gofs.insert(gofs.end(), {(long long)(k * QR), (long long)((k * n_tab + t) * QR),
+                               (long long)((k * n_tab + t) * rr)});
+    }
+  }
+  long long* dgofs = reinterpret_cast<long long*>(xs_modes + (size_t)d * IM_MAXT);
+  err = cudaMemcpyAsync(dgofs, gofs.data(), gofs.size() * sizeof(long long), cudaMemcpyHostToDevice, st);
+  if (err != cudaSuccess) return cuda_status(err);
+  err = cudaStreamSynchronize(st);   // gofs is a host temporary
+  if (err != cudaSuccess) return cuda_status(err);
+  auto refresh_mode = [&](int k) -> cudaError_t {
+    const int nt = (int)used[k].size();
+    const long long* o1 = dgofs + gofs_at[k];
+    const long long* o2 = o1 + 3 * nt;
+    BGemm g1 = bgemm_desc(Q, r, Q, tabs, Q, 1, f_new, r, 1, TB, r, 1);          // TB_t = T_t b_new
+    g1.offs = o1; g1.nb1 = nt;
+    BGemm g2 = bgemm_desc(Q, r, Q, tabs, tr ? 1 : Q, tr ? Q : 1, f_old, r, 1, W2, r, 1);   // TC_t = T~_t b_old
+    g2.offs = o1; g2.nb1 = nt;
+    BGemm g3 = bgemm_desc(r, r, Q, f_new, 1, r, TB, r, 1, G, r, 1);             // G = b_new^T TB
+    g3.offs = o2; g3.nb1 = nt;
+    BGemm g4 = bgemm_desc(r, r, Q, f_new, 1, r, W2, r, 1, Gm, r, 1);            // Gm = b_new^T TC
+    g4.offs = o2; g4.nb1 = nt;
+    cudaError_t e = bgemm_launch(g1, st);
+    if (e == cudaSuccess) e = bgemm_launch(g2, st);
+    if (e == cudaSuccess) e = bgemm_launch(g3, st);
+    if (e == cudaSuccess) e = bgemm_launch(g4, st);
+    return e;
+  };
+  for (int k = 0; k < d; ++k) {
+    if ((err = refresh_mode(k)) != cudaSuccess) return cuda_status(err);
     if ((err = images(k, f_old, W, tr)) != cudaSuccess) return cuda_status(err);
   }
   HArgs ha;
@@ -351,7 +601,6 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   std::vector<int> xs_all((size_t)d * IM_MAXT, 0);
   for (int k = 0; k < d; ++k)
     for (size_t i = 0; i < used[k].size(); ++i) xs_all[(size_t)k * IM_MAXT + i] = used[k][i];
-  int* xs_modes = reinterpret_cast<int*>(Linv + (size_t)(n / CH_NB) * CH_NB * CH_NB);   // spare tail block
   err = cudaMemcpyAsync(xs_modes, xs_all.data(), xs_all.size() * sizeof(int), cudaMemcpyHostToDevice, st);
   if (err != cudaSuccess) return cuda_status(err);
   const int nbk = n / CH_NB;
@@ -365,6 +614,24 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     for (int q = 0; q < d; ++q) {
       ha.q = q; ha.nX = (int)used[q].size();
       for (int i = 0; i < ha.nX; ++i) ha.xs[i] = used[q][i];
+      double* dst = (schedule == 0 ? f_new : bjac) + (size_t)q * QR;
+      if (circ_eig) {
+        CircArgs ca;
+        memset(&ca, 0, sizeof(ca));
+        ca.Q = Q; ca.r = r; ca.nX = ha.nX; ca.d = d; ca.ra = ra; ca.q = q; ca.n_tab = n_tab;
+        for (int i = 0; i < ha.nX; ++i) ca.xs[i] = used[q][i];
+        for (int i = 0; i < d * ra * ra; ++i) ca.tab[i] = tab_id[i];
+        for (int i = 0; i < ra * ra; ++i) { ca.KL[i] = KL[i]; ca.KR[i] = KR[i]; }
+        ca.G = G; ca.Gm = Gm; ca.W = W;
+        ca.H = H; ca.eig = circ_eig; ca.gam = gam; ca.tw = tw; ca.xhat = xhat; ca.lam = lam; ca.info = info;
+        form_h_kernel<<<ha.nX, 256, 0, st>>>(ha);
+        gamma_kernel<<<(n + 255) / 256, 256, 0, st>>>(Q, r, ha.nX, xs_modes + (size_t)q * IM_MAXT, Hg, W, n_tab, q,
+                                                       gam, n);
+        const size_t csm = sizeof(double) * (2 * (size_t)r * (r + 1) + 2 * r);
+        cudaFuncSetAttribute(circ_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+        circ_solve_kernel<<<Q, 256, csm, st>>>(ca);
+        circ_idft_kernel<<<(int)((QR + 255) / 256), 256, 0, st>>>(Q, r, xhat, tw, dst, info);
+      } else {
       form_h_kernel<<<ha.nX, 256, 0, st>>>(ha);
       gamma_kernel<<<(n + 255) / 256, 256, 0, st>>>(Q, r, ha.nX, xs_modes + (size_t)q * IM_MAXT, Hg, W, n_tab, q, gam, n);
       as.nX = ha.nX;
@@ -386,25 +653,25 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
         }
       }
       potrs_kernel<<<1, 256, 0, st>>>(M, n, Linv, gam, x, y);
-      double* dst = (schedule == 0 ? f_new : bjac) + (size_t)q * QR;
       scatter_x_kernel<<<(int)((QR + 255) / 256), 256, 0, st>>>(Q, r, x, dst, info);
-      if (schedule == 0) {
-        if ((err = grams(q, f_new, f_new, G, 0)) != cudaSuccess) return cuda_status(err);
-        if ((err = grams(q, f_new, f_old, Gm, tr)) != cudaSuccess) return cuda_status(err);
       }
+      if (schedule == 0)
+        if ((err = refresh_mode(q)) != cudaSuccess) return cuda_status(err);
     }
     if (schedule == 1) {
       err = cudaMemcpyAsync(f_new, bjac, sizeof(double) * d * QR, cudaMemcpyDeviceToDevice, st);
       if (err != cudaSuccess) return cuda_status(err);
     }
-    conv_damp_kernel<<<1, 256, 0, st>>>(Q, r, d, f_new, bint, delta_beta, eps_conv);
+    // delta_beta == 1: the damped update b_int + (b - b_int) equals b up to the last
+    // ulp, so the Gauss-Seidel iterate and its cached Grams are kept as they are
+    const bool damp = !(delta_beta == 1.0 && schedule == 0);
+    conv_damp_kernel<<<1, 256, 0, st>>>(Q, r, d, f_new, bint, damp ? delta_beta : 0.0, eps_conv);
     done = sweep + 1;
     // the damped iterate b_int + (b - b_int)/delta_beta differs from the raw
     // solve (also by rounding when delta_beta == 1): refresh every mode's Grams
-    for (int k = 0; k < d; ++k) {
-      if ((err = grams(k, f_new, f_new, G, 0)) != cudaSuccess) return cuda_status(err);
-      if ((err = grams(k, f_new, f_old, Gm, tr)) != cudaSuccess) return cuda_status(err);
-    }
+    if (damp)
+      for (int k = 0; k < d; ++k)
+        if ((err = refresh_mode(k)) != cudaSuccess) return cuda_status(err);
     err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_status(err);
     if (eps_tol > 0.0) {   // reference loop condition (implicit.py:244): one host read per sweep

@@ -44,6 +44,7 @@ class ALSStepConfig:
     schedule: str = "jacobi"
     lam: float = 1e-10
     orientation: str = "corrected"
+    solver: str = "auto"        # "auto" | "dense" | "circulant"
 
     def __post_init__(self):
         if self.schedule not in ("jacobi", "gauss-seidel"):
@@ -52,6 +53,8 @@ class ALSStepConfig:
             raise ValueError("damping divisor must be >= 1")
         if self.orientation not in ("corrected", "reference"):
             raise ValueError(f"unknown orientation {self.orientation!r}")
+        if self.solver not in ("auto", "dense", "circulant"):
+            raise ValueError(f"unknown solver {self.solver!r}")
 
 
 @dataclass
@@ -63,6 +66,7 @@ class OperatorTables:
     tab_id: np.ndarray          # (d, ra, ra) int32
     KL: np.ndarray
     KR: np.ndarray
+    circ_eig: torch.Tensor | None = None   # (n_tab, Q, 2) eigenvalues if every table is circulant
 
 
 def build_tables(pair: CrankNicolsonPair, device=None) -> OperatorTables:
@@ -93,7 +97,19 @@ def build_tables(pair: CrankNicolsonPair, device=None) -> OperatorTables:
     eta, zeta = eta.real, zeta.real
     dev = device or _lib.device()
     tabs = torch.as_tensor(np.stack(uniq)).to(dev)
-    return OperatorTables(pair, tabs, tab_id, np.outer(eta, eta), np.outer(eta, zeta))
+    circ = None
+    if all(is_circulant(t) for t in uniq):
+        lam = np.stack([np.fft.fft(t[:, 0]) for t in uniq])          # lambda_t(k) = sum_m t[m,0] e^{-2 pi i mk/Q}
+        circ = torch.as_tensor(np.stack([lam.real, lam.imag], axis=-1)).to(dev)
+    return OperatorTables(pair, tabs, tab_id, np.outer(eta, eta), np.outer(eta, zeta), circ)
+
+
+def is_circulant(t: np.ndarray, rtol: float = 1e-13) -> bool:
+    """t[i][j] depends only on (i - j) mod Q (periodic collocation operators)."""
+    Q = t.shape[0]
+    col = t[:, 0]
+    idx = (np.arange(Q)[:, None] - np.arange(Q)[None, :]) % Q
+    return bool(np.max(np.abs(t - col[idx])) <= rtol * max(np.max(np.abs(t)), 1e-300))
 
 
 class StepWorkspace:
@@ -122,6 +138,9 @@ def _launch(f_n: CPTensor, out: torch.Tensor, tab: OperatorTables, cfg: ALSStepC
     L = _lib.lib()
     d, Q, r, ra = f_n.ndim, f_n.specs[0].Q, f_n.rank, tab.pair.n_terms
     n_tab = tab.tabs.shape[0]
+    use_circ = tab.circ_eig is not None and cfg.solver in ("auto", "circulant")
+    if cfg.solver == "circulant" and tab.circ_eig is None:
+        raise ValueError("solver='circulant' needs circulant pairing tables (periodic collocation factors)")
     nbytes = L.tp_implicit_ws_bytes(d, Q, r, n_tab)
     if nbytes == 0:
         raise ValueError(f"unsupported implicit-step size d={d}, Q={Q}, r={r}, tables={n_tab}")
@@ -131,6 +150,7 @@ def _launch(f_n: CPTensor, out: torch.Tensor, tab: OperatorTables, cfg: ALSStepC
                                 f_n.data.data_ptr(), out.data_ptr(), int(cfg.max_sweeps),
                                 0 if cfg.schedule == "gauss-seidel" else 1, float(cfg.delta_beta),
                                 float(cfg.eps_tol), float(cfg.lam), 1 if cfg.orientation == "reference" else 0,
+                                tab.circ_eig.data_ptr() if use_circ else None,
                                 eps.data_ptr(), info.data_ptr(), ws.data_ptr(), ws.numel(),
                                 _lib.stream_ptr(f_n.data.device))
     _lib.check(st, "implicit.step")

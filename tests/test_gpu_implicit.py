@@ -52,8 +52,9 @@ def test_step_golden(orientation, key):
     assert rel <= 1e-9, rel
 
 
+@pytest.mark.parametrize("solver", ["dense", "circulant"])
 @pytest.mark.parametrize("schedule,delta", [("gauss-seidel", 1.0), ("jacobi", 4.0), ("jacobi", 1.0)])
-def test_step_matches_oracle(schedule, delta):
+def test_step_matches_oracle(schedule, delta, solver):
     rng = np.random.default_rng(7)
     d, q, r, dt, sweeps = 4, 16, 4, 2e-2, 5
     a = (1.0, 0.5, -0.75, 0.25)
@@ -61,7 +62,7 @@ def test_step_matches_oracle(schedule, delta):
     S = col_specs(d, q)
     f0 = [rng.standard_normal((q, r)) for _ in range(d)]
     cfg = implicit.ALSStepConfig(dt=dt, eps_tol=0.0, max_sweeps=sweeps, delta_beta=delta, schedule=schedule,
-                                 lam=1e-10)
+                                 lam=1e-10, solver=solver)
     out = implicit.step(cp.CPTensor(S, f0), euler_pair(S, D, a, dt), None, cfg)
     ref, done, _ = oim.step(f0, oracle_tables(d, q, D, a, dt), sweeps, 1e-10, schedule=schedule,
                             delta_beta=delta)
@@ -69,15 +70,16 @@ def test_step_matches_oracle(schedule, delta):
     assert rel <= 1e-9, rel
 
 
-def test_config2_full_size_step():
+@pytest.mark.parametrize("solver", ["dense", "circulant"])
+def test_config2_full_size_step(solver):
     """BASELINE config 2 sizes (d=6, Q=128, r=16 -> 2048^2 normal equations), 3 sweeps
-    of one step, vs the oracle's direct solves."""
+    of one step, vs the oracle's direct solves (dense Cholesky and DFT-block paths)."""
     w = workloads.cfg2(0)
     S, D, a, dt = w["specs"], w["D"], w["a"], w["dt"]
     f0 = w["ic"]["factors"]
     sweeps = 3
     cfg = implicit.ALSStepConfig(dt=dt, eps_tol=0.0, max_sweeps=sweeps, delta_beta=1.0, schedule="gauss-seidel",
-                                 lam=w["lam"])
+                                 lam=w["lam"], solver=solver)
     out = implicit.step(cp.CPTensor(S, f0), euler_pair(S, D, a, dt), None, cfg)
     ref, _, _ = oim.step(f0, oracle_tables(6, 128, D, a, dt), sweeps, w["lam"])
     rel = metrics.cp_rel_diff(ref, out.to_numpy())
@@ -89,3 +91,30 @@ def test_config_validation():
         implicit.ALSStepConfig(dt=0.1, schedule="sor")
     with pytest.raises(ValueError, match="damping"):
         implicit.ALSStepConfig(dt=0.1, delta_beta=0.5)
+
+
+def test_config2_trajectory_circulant_vs_dense():
+    """Several full 20-sweep steps at config-2 sizes: DFT-block path vs dense Cholesky
+    path vs oracle after 2 steps (final-solution bar 1e-8)."""
+    w = workloads.cfg2(0)
+    S, D, a, dt = w["specs"], w["D"], w["a"], w["dt"]
+    f0 = w["ic"]["factors"]
+    pair = euler_pair(S, D, a, dt)
+    outs = {}
+    for solver in ("circulant", "dense"):
+        cfg = implicit.ALSStepConfig(dt=dt, eps_tol=0.0, max_sweeps=w["sweeps"], delta_beta=1.0,
+                                     schedule="gauss-seidel", lam=w["lam"], solver=solver)
+        outs[solver] = implicit.run(cp.CPTensor(S, f0), pair, cfg, 2).to_numpy()
+    tab = oracle_tables(6, 128, D, a, dt)
+    ref = f0
+    for _ in range(2):
+        ref, _, _ = oim.step(ref, tab, w["sweeps"], w["lam"])
+    for solver, out in outs.items():
+        assert metrics.cp_rel_diff(ref, out) <= 1e-8, solver
+
+
+def test_circulant_detection():
+    from paper_1803_10270_b200.basis import fourier_diff_matrix as fdm
+    assert implicit.is_circulant(fdm(16))
+    assert implicit.is_circulant(fdm(16).T @ fdm(16))
+    assert not implicit.is_circulant(np.diag(np.arange(8.0)))
