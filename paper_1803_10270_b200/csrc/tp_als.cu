@@ -63,27 +63,29 @@ struct AlsArgs {
   long long* prof;     // optional per-phase clock64 totals (CTA 0), debug hook
   unsigned int* bar_ctr;   // grid-barrier arrival counter (zeroed before launch)
   int dbg_skip;            // debug: bit mask of phases to skip (timing by subtraction)
-  double* Xprev;           // [d][r][r+1] last inverse per mode (warm start for Newton-Schulz)
+  double* Xprev;           // [d][r][pad4(r)] last inverse per mode (warm start for Newton-Schulz)
+  double* Upad;            // U_k with rows padded to pad4(r) (bulk-staged into conflict-free smem)
+  long long offUp[TP_MAXD];
   int ns_max;              // Newton-Schulz iterations before falling back to the exact sweep
 };
 
 struct Smem {
   uint64_t* bar;        // bar[0]: U staging / Y slices, bar[1]: Gram
-  double *Us, *Vs, *Cs, *Gs, *hadT, *Am, *X0, *X1, *Rm, *pub, *rb, *part, *scal;
+  double *Us, *Vs, *Cs, *Gs, *hadT, *Am, *X0, *X1, *Rm, *pub, *rb, *vb, *part, *scal;
   int* rowmap;          // [d][qmax]: (consumer CTA << 16) | row-in-consumer
 };
 
 __host__ __device__ inline size_t stage_doubles(int qmax, int r, int ncolmax, int P) {
   // staging area shared by U_k (phase A, padded rows) and the P right-hand-side
   // slices + one Gram (phase B)
-  size_t a = (size_t)qmax * r, b = (size_t)P * ncolmax * r;   // U_k rows | the P right-hand-side blocks
+  size_t a = (size_t)qmax * pad4(r), b = (size_t)P * ncolmax * r;   // U_k padded rows | the P rhs blocks
   return a > b ? a : b;
 }
 
 __host__ __device__ inline size_t als_smem_doubles(int d, int sumqs, int r, int wmax, int ncolmax, int qmax, int P) {
   const size_t w4 = (size_t)((wmax + 3) / 4) * 4;
   return 8 + stage_doubles(qmax, r, ncolmax, P) + (size_t)wmax * sumqs + (size_t)d * r * wmax +
-         (size_t)d * r * r + w4 * pad4(r) + 4 * (size_t)r * (r + 1) + 72 + (size_t)ncolmax * r + ALS_PART + 8 +
+         (size_t)d * r * r + w4 * pad4(r) + 4 * (size_t)r * pad4(r) + 72 + 4 * (size_t)ncolmax * r + ALS_PART + 8 +
          ((size_t)d * qmax + 1) / 2 + 1;
 }
 
@@ -96,12 +98,13 @@ __device__ inline Smem carve(double* base, const AlsArgs& a) {
   s.Cs = base + o; o += (size_t)a.d * a.r * a.wmax;
   s.Gs = base + o; o += (size_t)a.d * a.r * a.r;
   s.hadT = base + o; o += (size_t)((a.wmax + 3) / 4) * 4 * pad4(a.r);
-  s.Am = base + o; o += (size_t)a.r * (a.r + 1);
-  s.X0 = base + o; o += (size_t)a.r * (a.r + 1);
-  s.X1 = base + o; o += (size_t)a.r * (a.r + 1);
-  s.Rm = base + o; o += (size_t)a.r * (a.r + 1);
+  s.Am = base + o; o += (size_t)a.r * pad4(a.r);
+  s.X0 = base + o; o += (size_t)a.r * pad4(a.r);
+  s.X1 = base + o; o += (size_t)a.r * pad4(a.r);
+  s.Rm = base + o; o += (size_t)a.r * pad4(a.r);
   s.pub = base + o; o += 72;
   s.rb = base + o; o += (size_t)a.ncolmax * a.r;
+  s.vb = base + o; o += 3 * (size_t)a.ncolmax * a.r;
   s.part = base + o; o += ALS_PART;
   s.scal = base + o; o += 8;
   s.rowmap = reinterpret_cast<int*>(base + o);
@@ -135,71 +138,92 @@ __device__ __forceinline__ double rcp_nr(double d) {
   return fma(y, e, y);
 }
 
-// Stage U_k (Q_k x r, written by other CTAs) into sm.Us (row stride r): one
-// bulk async copy of the contiguous block through the TMA engine (per-row
-// copies serialise in the SM's copy unit and were 6x slower).
-__device__ void stage_u(const AlsArgs& a, const Smem& sm, int k, uint32_t& phase) {
-  const int n = a.q[k] * a.r;
-  const double* Uk = a.U + a.offU[k];
+// Stage U_k (Q_k x r, written by other CTAs) into sm.Us with rows padded to
+// pad4(r) (conflict-free DMMA fragments): one bulk async copy of the padded
+// copy Upad that phase B maintains (per-row copies serialise in the SM's copy
+// unit and were 6x slower).  from_user: initial guess, plain loads from U.
+__device__ void stage_u(const AlsArgs& a, const Smem& sm, int k, uint32_t& phase, bool from_user = false) {
+  const int r = a.r, rh = pad4(r), Q = a.q[k];
   __syncthreads();   // previous users of sm.Us are done
-  if (((a.offU[k] | n) & 1) == 0) {
+  if (!from_user) {
     if (threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)(Q * rh) * 8u;
       fence_proxy_async();
-      mbar_arrive_expect_tx(sm.bar, (uint32_t)n * 8u);
-      bulk_g2s(sm.Us, Uk, (uint32_t)n * 8u, sm.bar);
+      mbar_arrive_expect_tx(sm.bar, bytes);
+      bulk_g2s(sm.Us, a.Upad + a.offUp[k], bytes, sm.bar);
     }
     mbar_wait(sm.bar, phase);
     phase ^= 1u;
   } else {
-    for (int e = threadIdx.x; e < n; e += ALS_NT) sm.Us[e] = __ldcg(Uk + e);
+    const double* Uk = a.U + a.offU[k];
+    for (int e = threadIdx.x; e < Q * r; e += ALS_NT) sm.Us[(e / r) * rh + e % r] = __ldcg(Uk + e);
     __syncthreads();
   }
 }
 
 // Cs[k][l][c] = sum_s U_k[s][l] V_k[s][c0 + c] (cp.py:190-195) on the DMMA
-// tensor pipe: M = l, N = c, K = s; output tiles x split-K over the 8 warps.
+// tensor pipe: M = l, N = c, K = s.  A work item is (N tile, K range); its warp
+// runs all RM/8 M tiles as independent accumulator chains; the K-range partials
+// are summed in fixed order through scratch (sm.X1.., free in phase A).
+template <int RM>
 __device__ void cross_slab(const AlsArgs& a, const Smem& sm, int k, int w) {
-  const int r = a.r, Q = a.q[k], ru = r, qs = a.qs[k];
+  constexpr int MT = RM / 8;
+  const int r = a.r, Q = a.q[k], ru = pad4(r), qs = a.qs[k];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* vs = sm.Vs + a.qoff[k];
   double* C = sm.Cs + (size_t)k * r * a.wmax;
-  const int mt = (r + 7) / 8, nt = (w + 7) / 8, tiles = mt * nt;
-  int ks = 1;
-  while (tiles * ks < ALS_NW && ks < 8) ks <<= 1;
-  while (tiles * ks * 64 > ALS_PART && ks > 1) ks >>= 1;
-  const int ksteps = (Q + 3) / 4, per = (ksteps + ks - 1) / ks;
-  const bool direct = (ks == 1);
-  for (int it = warp; it < tiles * ks; it += ALS_NW) {
-    const int tile = it / ks, kp = it % ks;
-    const int m0 = (tile / nt) * 8, n0 = (tile % nt) * 8;
-    const int l = m0 + (lane >> 2), c = n0 + (lane >> 2);
-    double acc0 = 0.0, acc1 = 0.0;
-    const int kb = kp * per, ke = min(ksteps, kb + per);
+  double* part = sm.X1;                                   // 2 r pad4(r) doubles
+  const int nt = (w + 7) / 8, ksteps = (Q + 3) / 4, cap = 2 * r * ru;
+  int kp = ALS_NW / nt;
+  if (kp < 1) kp = 1;
+  while (kp > 1 && nt * kp * MT * 64 > cap) --kp;
+  const int per = (ksteps + kp - 1) / kp;
+  for (int it = warp; it < nt * kp; it += ALS_NW) {
+    const int n = it / kp, q = it - n * kp;
+    const int c = n * 8 + (lane >> 2);
+    double acc[MT][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+    const int kb = q * per, ke = min(ksteps, kb + per);
+#pragma unroll 2
     for (int kk = kb; kk < ke; ++kk) {
       const int s = 4 * kk + (lane & 3);
-      const double fa = (s < Q && l < r) ? sm.Us[s * ru + l] : 0.0;
-      const double fb = (s < Q && c < w) ? vs[c * qs + s] : 0.0;
-      dmma_8x8x4(acc0, acc1, fa, fb);
+      const bool sv = s < Q;
+      const double fb = (sv && c < w) ? vs[c * qs + s] : 0.0;
+      double fa[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int l = m * 8 + (lane >> 2);
+        fa[m] = (sv && l < r) ? sm.Us[s * ru + l] : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < MT; ++m) dmma_8x8x4(acc[m][0], acc[m][1], fa[m], fb);
     }
-    const int orow = m0 + (lane >> 2), ocol = n0 + 2 * (lane & 3);
-    if (direct) {
-      if (orow < r) {
-        if (ocol < w) C[orow * a.wmax + ocol] = acc0;
-        if (ocol + 1 < w) C[orow * a.wmax + ocol + 1] = acc1;
+    if (kp == 1) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int orow = m * 8 + (lane >> 2), ocol = n * 8 + 2 * (lane & 3);
+        if (orow < r) {
+          if (ocol < w) C[orow * a.wmax + ocol] = acc[m][0];
+          if (ocol + 1 < w) C[orow * a.wmax + ocol + 1] = acc[m][1];
+        }
       }
     } else {
-      double* pt = sm.part + (size_t)it * 64;
-      pt[2 * lane] = acc0;
-      pt[2 * lane + 1] = acc1;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        double* pt = part + ((size_t)it * MT + m) * 64;
+        pt[2 * lane] = acc[m][0];
+        pt[2 * lane + 1] = acc[m][1];
+      }
     }
   }
   __syncthreads();
-  if (!direct) {
-    for (int e = threadIdx.x; e < tiles * 64; e += ALS_NT) {
-      const int tile = e / 64, ln = (e % 64) / 2, h = e & 1;
-      const int orow = (tile / nt) * 8 + (ln >> 2), ocol = (tile % nt) * 8 + 2 * (ln & 3) + h;
+  if (kp > 1) {
+    for (int e = threadIdx.x; e < nt * MT * 64; e += ALS_NT) {
+      const int n = e / (MT * 64), rem = e - n * MT * 64, m = rem >> 6, ln = (rem & 63) >> 1, h = rem & 1;
+      const int orow = m * 8 + (ln >> 2), ocol = n * 8 + 2 * (ln & 3) + h;
       double acc = 0.0;
-      for (int kp = 0; kp < ks; ++kp) acc += sm.part[(size_t)(tile * ks + kp) * 64 + 2 * ln + h];
+      for (int q = 0; q < kp; ++q) acc += part[((size_t)(n * kp + q) * MT + m) * 64 + 2 * ln + h];
       if (orow < r && ocol < w) C[orow * a.wmax + ocol] = acc;
     }
     __syncthreads();
@@ -209,7 +233,7 @@ __device__ void cross_slab(const AlsArgs& a, const Smem& sm, int k, int w) {
 // this CTA's share of G_k = U_k^T U_k (cp.py:318): the upper 8x8 tiles are
 // dealt round-robin to CTAs; each tile is one DMMA chain split over the warps.
 __device__ void gram_share(const AlsArgs& a, const Smem& sm, int k) {
-  const int r = a.r, Q = a.q[k], ru = r, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = a.r, Q = a.q[k], ru = pad4(r), lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int mt = (r + 7) / 8, ntile = mt * (mt + 1) / 2;
   double* Gk = a.G + (size_t)k * r * r;
   const int ksteps = (Q + 3) / 4, per = (ksteps + ALS_NW - 1) / ALS_NW;
@@ -264,9 +288,9 @@ __device__ inline double block_sum(double v, double* red) {
 // column k == row k, so each pivot step publishes one row and costs one
 // barrier.  Returns 1 if a pivot is not positive / finite.
 template <int RM>
-__device__ int gram_inverse(const AlsArgs& a, const Smem& sm, int j, double* out) {
+__device__ int gram_inverse(const AlsArgs& a, const Smem& sm, int j, double* out, int os) {
   constexpr int EPT = RM / 8;
-  const int r = a.r, gs = r, gk = r * r, rp = r + 1, t = threadIdx.x;
+  const int r = a.r, gs = r, gk = r * r, t = threadIdx.x;
   const int i = t >> 3, c0 = t & 7;
   double v[EPT];
 #pragma unroll
@@ -324,125 +348,177 @@ __device__ int gram_inverse(const AlsArgs& a, const Smem& sm, int j, double* out
 #pragma unroll
     for (int u = 0; u < EPT; ++u) {
       const int c = c0 + 8 * u;
-      if (c < r) out[i * rp + c] = -v[u];
+      if (c < r) out[i * os + c] = -v[u];
     }
   return bad;
 }
 
-// C = op(A B) for r x r smem matrices (row stride r+1) on DMMA m8n8k4; every
-// warp owns 8x8 output tiles.  mode 0: C = I - A B;  mode 1: C = X + A B (X = A)
+// A = prod_{k!=j} G_k + lambda I into sm.Am (row stride pad4(r)); returns this
+// thread's partial max |A_ij|.  Thread t owns row t/8, columns t%8 + 8u.
 template <int RM>
-__device__ void small_gemm(const double* A, const double* B, double* C, int r, int mode) {
-  constexpr int NT8 = RM / 8, TILES = NT8 * NT8, TPW = (TILES + ALS_NW - 1) / ALS_NW, KS = RM / 4;
-  constexpr int SPLIT = KS < 4 ? KS : 4;   // independent accumulator chains per tile
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, rp = r + 1;
-  double acc[TPW][SPLIT][2];
+__device__ double build_a(const AlsArgs& a, const Smem& sm, int j) {
+  constexpr int EPT = RM / 8;
+  const int r = a.r, rr = r * r, rp = pad4(r), i = threadIdx.x >> 3, c0 = threadIdx.x & 7;
+  double lam = a.reg;
+  if (a.reg_mode) {   // reg * max(tr A, 0) / r  (cp.py:171-173)
+    double dg = 0.0;
+    if (threadIdx.x < r) {
+      dg = 1.0;
+      for (int k = 0; k < a.d; ++k)
+        if (k != j) dg *= sm.Gs[(size_t)k * rr + threadIdx.x * r + threadIdx.x];
+    }
+    const double tr = block_sum(dg, sm.part);
+    lam = a.reg * fmax(tr, 0.0) / (double)r;
+  }
+  double mx = 0.0;
+  if (i < r) {
 #pragma unroll
-  for (int t = 0; t < TPW; ++t)
+    for (int u = 0; u < EPT; ++u) {
+      const int c = c0 + 8 * u;
+      if (c < r) {
+        double f[TP_MAXD];
 #pragma unroll
-    for (int s2 = 0; s2 < SPLIT; ++s2) acc[t][s2][0] = acc[t][s2][1] = 0.0;
+        for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < a.d && k != j) ? sm.Gs[(size_t)k * rr + i * r + c] : 1.0;
+        double v = 1.0;
 #pragma unroll
-  for (int kk = 0; kk < KS; ++kk) {
-    const int k = 4 * kk + (lane & 3);
-#pragma unroll
-    for (int t = 0; t < TPW; ++t) {
-      const int tile = warp + t * ALS_NW;
-      if (tile < TILES) {
-        const int m0 = (tile / NT8) * 8, n0 = (tile % NT8) * 8;
-        const int mrow = m0 + (lane >> 2), ncol = n0 + (lane >> 2);
-        const double fa = (mrow < r && k < r) ? A[mrow * rp + k] : 0.0;
-        const double fb = (k < r && ncol < r) ? B[k * rp + ncol] : 0.0;
-        dmma_8x8x4(acc[t][kk % SPLIT][0], acc[t][kk % SPLIT][1], fa, fb);
+        for (int k = 0; k < TP_MAXD; ++k) v *= f[k];
+        if (c == i) v += lam;
+        sm.Am[i * rp + c] = v;
+        mx = fmax(mx, fabs(v));
       }
     }
   }
-#pragma unroll
-  for (int t = 0; t < TPW; ++t) {
-    const int tile = warp + t * ALS_NW;
-    if (tile >= TILES) continue;
-    double s0 = acc[t][0][0], s1 = acc[t][0][1];
-#pragma unroll
-    for (int s2 = 1; s2 < SPLIT; ++s2) { s0 += acc[t][s2][0]; s1 += acc[t][s2][1]; }
-    const int m0 = (tile / NT8) * 8, n0 = (tile % NT8) * 8;
-    const int orow = m0 + (lane >> 2), oc = n0 + 2 * (lane & 3);
-    if (orow < r) {
-      if (oc < r) C[orow * rp + oc] = mode == 0 ? ((orow == oc ? 1.0 : 0.0) - s0) : A[orow * rp + oc] + s0;
-      if (oc + 1 < r) C[orow * rp + oc + 1] = mode == 0 ? ((orow == oc + 1 ? 1.0 : 0.0) - s1) : A[orow * rp + oc + 1] + s1;
-    }
-  }
+  __syncthreads();
+  return mx;
 }
 
-__device__ inline double block_max_abs(const double* M, int r, double* red) {
-  const int rp = r + 1;
-  double m = 0.0;
-  for (int e = threadIdx.x; e < r * r; e += ALS_NT) {
-    const double x = M[(e / r) * rp + e % r];
-    m = (x != x) ? INFINITY : fmax(m, fabs(x));        // NaN -> inf (forces the fallback)
+// One stage of the vector solve: for o < E (o = sc * r + i)
+//   out[o] = base[o] + sgn * sum_k M[k][i] in[sc * r + k]
+// (column access: lanes read consecutive i, conflict-free).  Threads E..E+r-1
+// optionally run the same form for one extra vector (xin -> xout).
+__device__ inline double mv_dot(const double* M, int ld, const double* v, int i, int r) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = 0;
+  for (; k + 4 <= r; k += 4) {
+    s0 = fma(M[k * ld + i], v[k], s0);
+    s1 = fma(M[(k + 1) * ld + i], v[k + 1], s1);
+    s2 = fma(M[(k + 2) * ld + i], v[k + 2], s2);
+    s3 = fma(M[(k + 3) * ld + i], v[k + 3], s3);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  double out = red[0];
-#pragma unroll
-  for (int w = 1; w < ALS_NW; ++w) out = fmax(out, red[w]);
-  __syncthreads();
-  return out;
+  for (; k < r; ++k) s0 = fma(M[k * ld + i], v[k], s0);
+  return (s0 + s1) + (s2 + s3);
 }
 
-// A = prod_{k!=j} G_k + lambda I into sm.Am (row stride r+1)
-__device__ void build_a(const AlsArgs& a, const Smem& sm, int j) {
-  const int r = a.r, rr = r * r, rp = r + 1;
-  for (int e = threadIdx.x; e < rr; e += ALS_NT) {
-    double v = 1.0;
-    for (int k = 0; k < a.d; ++k)
-      if (k != j) v *= sm.Gs[(size_t)k * rr + e];
-    sm.Am[(e / r) * rp + e % r] = v;
-  }
-  __syncthreads();
-  double lam = a.reg;
-  if (a.reg_mode) {
-    double tr = 0.0;
-    for (int q = 0; q < r; ++q) tr += sm.Am[q * rp + q];
-    lam = a.reg * fmax(tr, 0.0) / (double)r;
-  }
-  __syncthreads();
-  for (int q = threadIdx.x; q < r; q += ALS_NT) sm.Am[q * rp + q] += lam;
-  __syncthreads();
-}
-
-// A^-1 for mode j: Newton-Schulz refinement X <- X + X (I - A X) from the
-// previous sweep's inverse (quadratic convergence once ALS settles; three
-// small DMMA GEMMs per iteration instead of r dependent pivot steps); exact
-// symmetric sweep when there is no warm start or it does not converge to
-// |I - A X|_max <= 1e-14.  Decisions are uniform (identical inputs in every
-// CTA).  Returns the buffer holding the inverse (row stride r+1).
+// Solve A_j u = b for this CTA's right-hand sides b = rows of sm.rb (cp.py:317);
+// A_j is already in sm.Am (build_a, max |A_ij| partial in ma) on the warm path
+// -> sm.vb + 2 * ncolmax * r.  Warm path (sweep > 0): one Newton-Schulz step of
+// the previous sweep's inverse X0 applied to the vectors (A is symmetric, X0 is
+// used through its transpose), u = X0' (2b - A X0' b), accepted when the backward
+// error is at rounding level, |b - A u|_max <= 1e-13 r |A|_max |u|_max (one step
+// squares |I - A X|).  Rows i == p (mod P) of X1 = 2 X0 - X0 A X0 become the
+// next sweep's warm start.  Otherwise (first sweep, or the check fails in this
+// CTA) the exact symmetric-sweep inverse.
 template <int RM>
-__device__ double* invert_mode(const AlsArgs& a, const Smem& sm, int j, bool warm, int& status) {
-  if (warm && a.ns_max > 0) {
-    build_a(a, sm, j);
-    double* X = sm.X0;
-    double* Xn = sm.X1;
-    bool ok = false;
-    double prev = INFINITY;
-    for (int it = 0; it < a.ns_max; ++it) {
-      small_gemm<RM>(sm.Am, X, sm.Rm, a.r, 0);        // R = I - A X
-      __syncthreads();
-      const double nrm = block_max_abs(sm.Rm, a.r, sm.part);
-      if (!(nrm <= 0.25)) break;                      // warm start too far (or non-finite)
-      // converged: at rounding level, or quadratic convergence has stalled there
-      if (nrm <= 1e-13 || (nrm <= 1e-10 && nrm >= 0.25 * prev)) { ok = true; break; }
-      prev = nrm;
-      small_gemm<RM>(X, sm.Rm, Xn, a.r, 1);           // Xn = X + X R
-      __syncthreads();
-      double* t = X; X = Xn; Xn = t;
-    }
-    if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) a.prof[ok ? 14 : 15] += 1;
-    if (ok) return X;
+__device__ void solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, int E, double ma, int& status) {
+  const int r = a.r, rh = pad4(r), P = gridDim.x, p = blockIdx.x, tid = threadIdx.x;
+  const int nv = a.ncolmax * r;
+  double* zb = sm.vb;
+  double* yb = sm.vb + nv;
+  double* ub = sm.vb + 2 * nv;
+  double* xr = sm.Rm;            // row of X0 A
+  // warm starts are double-buffered by sweep parity: this sweep reads buffer
+  // (sweep & 1) and writes the other, so results do not depend on CTA timing
+  double* Xn = a.Xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;
+  bool ok = false;
+#define NSPROF(slot)                                                                   \
+  if (a.prof && blockIdx.x == 0) {                                                     \
+    __syncthreads();                                                                   \
+    ns_sink += *(volatile double*)sm.scal;                                             \
+    const long long now = clock64();                                                   \
+    if (threadIdx.x == 0) a.prof[16 + (slot)] += now - ns_t;                           \
+    ns_t = now;                                                                        \
   }
-  status |= gram_inverse<RM>(a, sm, j, sm.X0);
+  long long ns_t = clock64();
+  double ns_sink = 0.0;
+  if (sweep > 0 && a.ns_max > 0) {
+    NSPROF(0);
+    const int nr = p < r ? r : 0;       // first owned warm-start row i = p
+    // stage 1: z = X0' b ; xr = (X0 A)[p, :]
+    for (int o = tid; o < E + nr; o += ALS_NT) {
+      if (o < E) {
+        const int sc = o / r, i = o - sc * r;
+        zb[o] = mv_dot(sm.X0, rh, sm.rb + sc * r, i, r);
+      } else {
+        xr[o - E] = mv_dot(sm.Am, rh, sm.X0 + p * rh, o - E, r);
+      }
+    }
+    __syncthreads();
+    NSPROF(1);
+    // stage 2: y = 2b - A z ; X1[p, :] = 2 X0[p, :] - xr X0
+    for (int o = tid; o < E + nr; o += ALS_NT) {
+      if (o < E) {
+        const int sc = o / r, i = o - sc * r;
+        yb[o] = 2.0 * sm.rb[o] - mv_dot(sm.Am, rh, zb + sc * r, i, r);
+      } else {
+        const int c = o - E;
+        Xn[(size_t)p * rh + c] = 2.0 * sm.X0[p * rh + c] - mv_dot(sm.X0, rh, xr, c, r);
+      }
+    }
+    __syncthreads();
+    NSPROF(2);
+    for (int i0 = p + P; i0 < r; i0 += P) {   // further owned rows (grids smaller than r)
+      for (int c = tid; c < r; c += ALS_NT) xr[c] = mv_dot(sm.Am, rh, sm.X0 + i0 * rh, c, r);
+      __syncthreads();
+      for (int c = tid; c < r; c += ALS_NT) Xn[(size_t)i0 * rh + c] = 2.0 * sm.X0[i0 * rh + c] - mv_dot(sm.X0, rh, xr, c, r);
+      __syncthreads();
+    }
+    // stage 3: u = X0' y
+    double mu = 0.0;
+    for (int o = tid; o < E; o += ALS_NT) {
+      const int sc = o / r, i = o - sc * r;
+      const double u = mv_dot(sm.X0, rh, yb + sc * r, i, r);
+      ub[o] = u;
+      mu = fmax(mu, fabs(u));
+    }
+    __syncthreads();
+    NSPROF(3);
+    // stage 4: backward-error check |b - A u|_max <= 1e-13 r |A|_max |u|_max
+    double mres = 0.0;
+    for (int o = tid; o < E; o += ALS_NT) {
+      const int sc = o / r, i = o - sc * r;
+      const double res = sm.rb[o] - mv_dot(sm.Am, rh, ub + sc * r, i, r);
+      mres = fmax(mres, fabs(res));
+    }
+    mres = (mres != mres) ? INFINITY : mres;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mres = fmax(mres, __shfl_xor_sync(0xffffffffu, mres, o));
+      mu = fmax(mu, __shfl_xor_sync(0xffffffffu, mu, o));
+      ma = fmax(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+    }
+    double* red = sm.part;
+    if ((tid & 31) == 0) { red[tid >> 5] = mres; red[8 + (tid >> 5)] = mu; red[16 + (tid >> 5)] = ma; }
+    __syncthreads();
+    mres = red[0]; mu = red[8]; ma = red[16];
+#pragma unroll
+    for (int w = 1; w < ALS_NW; ++w) { mres = fmax(mres, red[w]); mu = fmax(mu, red[8 + w]); ma = fmax(ma, red[16 + w]); }
+    ok = mres <= 1e-13 * (double)r * ma * mu;
+    if (a.prof && p == 0 && tid == 0) a.prof[ok ? 14 : 15] += 1;
+    __syncthreads();
+    NSPROF(4);
+  }
+  if (ns_sink == 12345.0) a.prof[24] += 1;
+  if (ok) return;
+  status |= gram_inverse<RM>(a, sm, j, sm.X0, rh);
   __syncthreads();
-  return sm.X0;
+  for (int o = tid; o < E; o += ALS_NT) {
+    const int sc = o / r, i = o - sc * r;
+    ub[o] = mv_dot(sm.X0, rh, sm.rb + sc * r, i, r);
+  }
+  if (a.ns_max > 0)
+    for (int i0 = p; i0 < r; i0 += P)
+      for (int c = tid; c < r; c += ALS_NT) Xn[(size_t)i0 * rh + c] = sm.X0[i0 * rh + c];
+  __syncthreads();
 }
 
 // debug phase timers: barrier-synchronised so the attribution is exact
@@ -468,7 +544,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   unsigned int epoch = 0;
   const Smem sm = carve(smem, a);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int p = blockIdx.x, P = gridDim.x, r = a.r, R = a.R, rr = r * r, rp = r + 1, rh = pad4(r);
+  const int p = blockIdx.x, P = gridDim.x, r = a.r, R = a.R, rr = r * r, rh = pad4(r);
   const int c0 = (int)((long long)R * p / P), c1 = (int)((long long)R * (p + 1) / P), w = c1 - c0;
   const int w4 = (w + 3) / 4 * 4;
   int status = 0;
@@ -501,8 +577,8 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   }
   __syncthreads();
   for (int k = 0; k < a.d; ++k) {
-    stage_u(a, sm, k, bphase);
-    cross_slab(a, sm, k, w);
+    stage_u(a, sm, k, bphase, true);
+    cross_slab<RM>(a, sm, k, w);
     gram_share(a, sm, k);
   }
   grid_barrier(a.bar_ctr, epoch);
@@ -522,49 +598,62 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       if (pending >= 0) {
         if (!(a.dbg_skip & 2)) stage_u(a, sm, pending, bphase);
         PROF(10);
-        if (!(a.dbg_skip & 4)) cross_slab(a, sm, pending, w);
+        if (!(a.dbg_skip & 4)) cross_slab<RM>(a, sm, pending, w);
         PROF(11);
         if (!(a.dbg_skip & 8)) gram_share(a, sm, pending);
       }
       PROF(1);
       const int Qj = a.q[j], qsj = a.qs[j];
       for (int e = tid; e < r * w; e += ALS_NT) {
-        const int c = e / r, l = e % r;
+        const int c = e / r, l = e - c * r;
+        double f[TP_MAXD];
+#pragma unroll
+        for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < a.d && k != j) ? sm.Cs[((size_t)k * r + l) * a.wmax + c] : 1.0;
         double v = 1.0;
-        for (int k = 0; k < a.d; ++k)
-          if (k != j) v *= sm.Cs[((size_t)k * r + l) * a.wmax + c];
+#pragma unroll
+        for (int k = 0; k < TP_MAXD; ++k) v *= f[k];
         sm.hadT[c * rh + l] = v;
       }
       __syncthreads();
-      {
-        // Y_p[s][l] = sum_c V_j[s][c0+c] had[l][c]: M = s, N = l, K = c (DMMA).
-        // Stored consumer-major: row s goes to the CTA pc that owns column s in
-        // phase B, at YT[pc][p][s - s0(pc)][:], so every consumer later pulls
-        // one contiguous block with a single bulk copy.
+      if (!(a.dbg_skip & 16)) {
+        // Y_p[s][l] = sum_c V_j[s][c0+c] had[l][c]: M = s, N = l, K = c (DMMA),
+        // all RM/8 N tiles of an M tile as independent chains.  Stored
+        // consumer-major: row s goes to the CTA pc that owns column s in phase
+        // B, at YT[pc][p][s - s0(pc)][:], so every consumer later pulls one
+        // contiguous block with a single bulk copy.
+        constexpr int NT = RM / 8;
         const double* vs = sm.Vs + a.qoff[j];
-        const int mt = (Qj + 7) / 8, nt = (r + 7) / 8, kst = w4 / 4;
-        for (int m = warp; m < ((a.dbg_skip & 16) ? 0 : mt); m += ALS_NW) {
-          const int m0 = m * 8, s = m0 + (lane >> 2);
+        const int mt = (Qj + 7) / 8, kst = w4 / 4;
+        for (int m = warp; m < mt; m += ALS_NW) {
+          const int s = m * 8 + (lane >> 2);
           const bool srow = s < Qj;
           const int rm = srow ? sm.rowmap[j * a.qmax + s] : 0;
           const int pc = rm >> 16, ii = rm & 0xffff;
           double* yrow = a.Y + (((size_t)pc * P + p) * a.ncolmax + ii) * r;
-          for (int n = 0; n < nt; ++n) {
-            const int n0 = n * 8, l = n0 + (lane >> 2);
-            double acc0 = 0.0, acc1 = 0.0;
-            for (int kk = 0; kk < kst; ++kk) {
-              const int c = 4 * kk + (lane & 3);
-              const double av = (srow && c < w) ? vs[c * qsj + s] : 0.0;
-              const double fb = (l < r) ? sm.hadT[c * rh + l] : 0.0;
-              dmma_8x8x4(acc0, acc1, av, fb);
+          double acc[NT][2];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+          for (int kk = 0; kk < kst; ++kk) {
+            const int c = 4 * kk + (lane & 3);
+            const double av = (srow && c < w) ? vs[c * qsj + s] : 0.0;
+            double fb[NT];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              const int l = n * 8 + (lane >> 2);
+              fb[n] = (l < r) ? sm.hadT[c * rh + l] : 0.0;
             }
-            const int ocol = n0 + 2 * (lane & 3);
-            if (srow) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n) dmma_8x8x4(acc[n][0], acc[n][1], av, fb[n]);
+          }
+          if (srow) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              const int ocol = n * 8 + 2 * (lane & 3);
               if (ocol + 1 < r && (r & 1) == 0) {
-                *reinterpret_cast<double2*>(yrow + ocol) = make_double2(acc0, acc1);
+                *reinterpret_cast<double2*>(yrow + ocol) = make_double2(acc[n][0], acc[n][1]);
               } else {
-                if (ocol < r) yrow[ocol] = acc0;
-                if (ocol + 1 < r) yrow[ocol + 1] = acc1;
+                if (ocol < r) yrow[ocol] = acc[n][0];
+                if (ocol + 1 < r) yrow[ocol + 1] = acc[n][1];
               }
             }
           }
@@ -577,62 +666,72 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       const int s0 = (int)((long long)Qj * p / P), s1 = (int)((long long)Qj * (p + 1) / P);
       const int ncol = s1 - s0, E = ncol * r;
       const int nb = a.ncolmax * r;     // one producer's block for this consumer
-      double* Xinv = sm.X0;
       double* ystage = sm.Us;           // [q][nb]
+      const bool warm_ns = sweep > 0 && a.ns_max > 0;
+      double ma = 0.0;
       if (bulk) {
         if (tid == 0) {
           const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
           const uint32_t ybytes = (E > 0 && !(a.dbg_skip & 32)) ? (uint32_t)(P * nb) * 8u : 0u;
           fence_proxy_async();
-          const uint32_t xbytes = (sweep > 0 && a.ns_max > 0) ? (uint32_t)(r * rp) * 8u : 0u;
+          const uint32_t xbytes = (sweep > 0 && a.ns_max > 0) ? (uint32_t)(r * rh) * 8u : 0u;
           mbar_arrive_expect_tx(sm.bar + 1, gbytes + xbytes);
           if (gbytes) bulk_g2s(sm.Gs + (size_t)pending * rr, a.G + (size_t)pending * rr, gbytes, sm.bar + 1);
-          if (xbytes) bulk_g2s(sm.X0, a.Xprev + (size_t)j * r * rp, xbytes, sm.bar + 1);
+          if (xbytes) bulk_g2s(sm.X0, a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh, xbytes, sm.bar + 1);
           mbar_arrive_expect_tx(sm.bar, ybytes);
           if (ybytes) bulk_g2s(ystage, a.Y + (size_t)p * P * nb, ybytes, sm.bar);
         }
         mbar_wait(sm.bar + 1, gphase);
         gphase ^= 1u;
-        // the inversion runs while the right-hand-side slices are still landing
-        if (!(a.dbg_skip & 1)) Xinv = invert_mode<RM>(a, sm, j, sweep > 0, status);
+        if (warm_ns) ma = build_a<RM>(a, sm, j);   // overlaps the slice fetch
+        PROF(8);
         mbar_wait(sm.bar, bphase);
         bphase ^= 1u;
+        PROF(5);
         for (int o = tid; o < ((a.dbg_skip & 64) ? 0 : E); o += ALS_NT) {
-          double acc = 0.0;
-          for (int q = 0; q < P; ++q) acc += ystage[(size_t)q * nb + o];
-          sm.rb[o] = acc;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          int q = 0;
+          for (; q + 4 <= P; q += 4) {
+            s0 += ystage[(size_t)q * nb + o];
+            s1 += ystage[(size_t)(q + 1) * nb + o];
+            s2 += ystage[(size_t)(q + 2) * nb + o];
+            s3 += ystage[(size_t)(q + 3) * nb + o];
+          }
+          for (; q < P; ++q) s0 += ystage[(size_t)q * nb + o];
+          sm.rb[o] = (s0 + s1) + (s2 + s3);
         }
       } else {
         if (pending >= 0)
           for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * rr + e] = __ldcg(a.G + (size_t)pending * rr + e);
         if (sweep > 0 && a.ns_max > 0)
-          for (int e = tid; e < r * rp; e += ALS_NT) sm.X0[e] = __ldcg(a.Xprev + (size_t)j * r * rp + e);
+          for (int e = tid; e < r * rh; e += ALS_NT)
+            sm.X0[e] = __ldcg(a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh + e);
         for (int o = tid; o < E; o += ALS_NT) {
           double acc = 0.0;
           for (int q = 0; q < P; ++q) acc += __ldcg(a.Y + ((size_t)p * P + q) * nb + o);
           sm.rb[o] = acc;
         }
         __syncthreads();
-        Xinv = invert_mode<RM>(a, sm, j, sweep > 0, status);
+        if (warm_ns) ma = build_a<RM>(a, sm, j);
       }
       __syncthreads();
       PROF(4);
-      PROF(5);
+      if (!(a.dbg_skip & 1)) solve_mode<RM>(a, sm, j, sweep, E, ma, status);
+      PROF(9);
       if (E > 0) {
-        // X = A^-1 rhs  (columns of rhs are rows of rb)      (cp.py:317)
+        const double* ub = sm.vb + 2 * a.ncolmax * r;
         double* Uj = a.U + a.offU[j];
+        double* Up = a.Upad + a.offUp[j];
         int nf = 0;
         for (int e = tid; e < E; e += ALS_NT) {
-          const int sc = e / r, i = e % r;
-          double acc = 0.0;
-          for (int k = 0; k < r; ++k) acc = fma(Xinv[i * rp + k], sm.rb[sc * r + k], acc);
-          if (!isfinite(acc)) nf = 1;
-          Uj[(size_t)(s0 + sc) * r + i] = acc;
+          const int sc = e / r, i = e - sc * r;
+          const double v = ub[e];
+          if (!isfinite(v)) nf = 1;
+          Uj[(size_t)(s0 + sc) * r + i] = v;
+          Up[(size_t)(s0 + sc) * rh + i] = v;
         }
         if (nf) atomicOr(a.info, 2);
       }
-      if (p == 0 && a.ns_max > 0)
-        for (int e = tid; e < r * rp; e += ALS_NT) a.Xprev[(size_t)j * r * rp + e] = Xinv[e];
       pending = j;
       PROF(6);
       grid_barrier(a.bar_ctr, epoch);
@@ -642,7 +741,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
     if (a.need_resid) {
       // finish the last mode, then residual by the Gram identity (cp.py:321-326)
       stage_u(a, sm, pending, bphase);
-      cross_slab(a, sm, pending, w);
+      cross_slab<RM>(a, sm, pending, w);
       gram_share(a, sm, pending);
       double ov = 0.0;
       for (int e = tid; e < r * w; e += ALS_NT) {
@@ -739,18 +838,19 @@ static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
   AlsArgs& a = pl.a;
   a.d = d; a.R = R; a.r = r; a.qmax = qmax; a.sumqs = sumqs; a.P = P;
   a.wmax = (R + P - 1) / P; a.ncolmax = (qmax + P - 1) / P;
-  long long ov = 0, ou = 0;
+  long long ov = 0, ou = 0, oup = 0;
   int qo = 0;
   for (int k = 0; k < d; ++k) {
     a.q[k] = q[k]; a.qs[k] = pad4(q[k]); a.offV[k] = ov; a.offU[k] = ou; a.qoff[k] = qo;
-    ov += (long long)q[k] * R; ou += (long long)q[k] * r; qo += a.qs[k] * a.wmax;
+    a.offUp[k] = oup;
+    ov += (long long)q[k] * R; ou += (long long)q[k] * r; qo += a.qs[k] * a.wmax; oup += (long long)q[k] * pad4(r);
   }
   pl.P = P;
   pl.smem = smem;
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
   pl.ws_total = align_up(sizeof(double) * (size_t)d * r * r) + align_up(sizeof(double) * (size_t)P * P * a.ncolmax * r) +
                 align_up(sizeof(double) * (size_t)P) + align_up(sizeof(double)) + pl.ws_inner + 256 +
-                align_up(sizeof(double) * (size_t)d * r * (r + 1));
+                align_up(sizeof(double) * 2 * (size_t)d * r * pad4(r)) + align_up(sizeof(double) * (size_t)oup);
   return TP_OK;
 }
 
@@ -794,7 +894,12 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
   double* nsq = cv.take<double>(1);
   double* part = cv.take<double>(pl.ws_inner / sizeof(double));
   a.bar_ctr = cv.take<unsigned int>(16);
-  a.Xprev = cv.take<double>((size_t)d * r * (r + 1));
+  a.Xprev = cv.take<double>(2 * (size_t)d * r * pad4(r));
+  {
+    long long nup = 0;
+    for (int k = 0; k < d; ++k) nup += (long long)q[k] * pad4(r);
+    a.Upad = cv.take<double>((size_t)nup);
+  }
   a.ns_max = g_ns_max;
   a.V = V; a.U = U; a.trace = trace; a.info = info;
   a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = tol; a.stall = stall;
@@ -883,7 +988,7 @@ __global__ void __launch_bounds__(ALS_NT) shard_inverse_kernel(int d, int r, int
   sm.part = sm.pub + 72;
   for (int e = threadIdx.x; e < d * r * r; e += ALS_NT) sm.Gs[e] = G[e];
   __syncthreads();
-  const int bad = gram_inverse<RM>(a, sm, j, Ainv);
+  const int bad = gram_inverse<RM>(a, sm, j, Ainv, r + 1);
   if (bad && threadIdx.x == 0) atomicOr(info, 1);
 }
 

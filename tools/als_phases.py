@@ -8,8 +8,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_1803_10270_b200 import _lib, cp, workloads  # noqa: E402
 
-NAMES = ["A:gram (after cross)", "A:had+Y", "sync1", "B:loadG", "B:chol||reduce", "B:solve+write", "sync2",
-         "(unused)", "warp0 invert", "warp1 reduce", "A:stage_u", "A:cross"]
+NAMES = ["(loop head)", "A:gram_share", "A:had+Y", "barrier1", "B:reduce", "B:wait Y slices", "B:write U",
+         "barrier2", "B:wait G/X", "B:solve (NS/exact)", "A:stage_u", "A:cross"]
 
 
 def run(grid, Q=256, R=512, r=32):
@@ -17,7 +17,7 @@ def run(grid, Q=256, R=512, r=32):
     T = cp.CPTensor(w["specs"], w["V"])
     I0 = cp.CPTensor(w["specs"], w["init"])
     dev = T.data.device
-    prof = torch.zeros(16, dtype=torch.int64, device=dev)
+    prof = torch.zeros(32, dtype=torch.int64, device=dev)
     L = _lib.lib()
     L.tp_debug_set_als_profile.argtypes = [ctypes.c_void_p]
     info = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -30,13 +30,20 @@ def run(grid, Q=256, R=512, r=32):
     torch.cuda.synchronize()
     L.tp_debug_set_als_profile(None)
     p = prof.cpu().numpy() / 120.0
-    tot = p[[0, 1, 2, 3, 4, 5, 6, 10, 11]].sum()
+    tot = p[:12].sum()
     print(f"grid={grid} Q={Q} R={R} r={r}: cycles per mode update (CTA 0): total {tot:.0f}")
-    for i in [10, 11, 0, 1, 2, 3, 4, 5, 6]:
+    for i in [0, 10, 11, 1, 2, 3, 8, 5, 4, 9, 6, 7]:
         print(f"   {NAMES[i]:22s} {p[i]:9.0f}  ({100*p[i]/tot:4.1f}%)")
     raw = prof.cpu().numpy()
-    print(f"   Newton-Schulz accepted {raw[14]}, fell back {raw[15]}")
+    print("   NS sub-phases (cycles per mode): build_a %.0f  st1 %.0f  st2 %.0f  st3 %.0f  check %.0f" % tuple(raw[16:21] / 120.0))
+    print(f"   Newton-Schulz accepted {raw[14]}, fell back {raw[15]}, residual checks {raw[13]}, one-step accepts {raw[12]}")
 
 
 if __name__ == "__main__":
-    run(0)
+    Lb = _lib.lib()
+    Lb.tp_debug_set_als_ns.argtypes = [ctypes.c_int]
+    for ns in (6, 0):
+        print(f"--- Newton-Schulz cap {ns}")
+        Lb.tp_debug_set_als_ns(ns)
+        for g in [int(x) for x in sys.argv[1:]] or [0]:
+            run(g)
