@@ -392,34 +392,58 @@ __device__ double build_a(const AlsArgs& a, const Smem& sm, int j) {
   return mx;
 }
 
-// One stage of the vector solve: for o < E (o = sc * r + i)
-//   out[o] = base[o] + sgn * sum_k M[k][i] in[sc * r + k]
-// (column access: lanes read consecutive i, conflict-free).  Threads E..E+r-1
-// optionally run the same form for one extra vector (xin -> xout).
-__device__ inline double mv_dot(const double* M, int ld, const double* v, int i, int r) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int k = 0;
-  for (; k + 4 <= r; k += 4) {
-    s0 = fma(M[k * ld + i], v[k], s0);
-    s1 = fma(M[(k + 1) * ld + i], v[k + 1], s1);
-    s2 = fma(M[(k + 2) * ld + i], v[k + 2], s2);
-    s3 = fma(M[(k + 3) * ld + i], v[k + 3], s3);
+// Vector solve stages: out = sum_k M[k][i] v[k] with TPO = RM/8 threads per
+// output (k interleaved over the group, shuffle reduction; column access keeps
+// the half-warp conflict-free).  All lanes must call (uniform loop bounds).
+template <int RM>
+__device__ __forceinline__ double mv_dot(const double* M, int ld, const double* v, int i, int r, int part) {
+  constexpr int TPO = RM / 8, KP = 8;
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int t = 0; t < KP; t += 2) {
+    const int k0 = part + TPO * t, k1 = k0 + TPO;
+    if (k0 < r) s0 = fma(M[k0 * ld + i], v[k0], s0);
+    if (k1 < r) s1 = fma(M[k1 * ld + i], v[k1], s1);
   }
-  for (; k < r; ++k) s0 = fma(M[k * ld + i], v[k], s0);
-  return (s0 + s1) + (s2 + s3);
+  double acc = s0 + s1;
+#pragma unroll
+  for (int o = TPO / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// (sum_k M[k][i] v[k], sum_k |M[k][i] v[k]|) -- for the componentwise check
+template <int RM>
+__device__ __forceinline__ double2 mv_dot_abs(const double* M, int ld, const double* v, int i, int r, int part) {
+  constexpr int TPO = RM / 8, KP = 8;
+  double s0 = 0.0, s1 = 0.0, a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int t = 0; t < KP; t += 2) {
+    const int k0 = part + TPO * t, k1 = k0 + TPO;
+    if (k0 < r) { const double x = M[k0 * ld + i] * v[k0]; s0 += x; a0 += fabs(x); }
+    if (k1 < r) { const double x = M[k1 * ld + i] * v[k1]; s1 += x; a1 += fabs(x); }
+  }
+  double acc = s0 + s1, ab = a0 + a1;
+#pragma unroll
+  for (int o = TPO / 2; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    ab += __shfl_xor_sync(0xffffffffu, ab, o);
+  }
+  return make_double2(acc, ab);
 }
 
 // Solve A_j u = b for this CTA's right-hand sides b = rows of sm.rb (cp.py:317);
-// A_j is already in sm.Am (build_a, max |A_ij| partial in ma) on the warm path
+// A_j is already in sm.Am (build_a) on the warm path
 // -> sm.vb + 2 * ncolmax * r.  Warm path (sweep > 0): one Newton-Schulz step of
 // the previous sweep's inverse X0 applied to the vectors (A is symmetric, X0 is
 // used through its transpose), u = X0' (2b - A X0' b), accepted when the backward
-// error is at rounding level, |b - A u|_max <= 1e-13 r |A|_max |u|_max (one step
-// squares |I - A X|).  Rows i == p (mod P) of X1 = 2 X0 - X0 A X0 become the
-// next sweep's warm start.  Otherwise (first sweep, or the check fails in this
-// CTA) the exact symmetric-sweep inverse.
+// error is at rounding level componentwise, |b - A u|_i <= 1e-13 r (|A||u|)_i (one step
+// squares |I - A X|).  Returns true then; the owned rows of X1 = 2 X0 - X0 A X0
+// (next sweep's warm start) are formed in the next phase A (ns_rows).
+// Otherwise (first sweep, or the check fails in this CTA) the exact
+// symmetric-sweep inverse, whose owned rows are stored directly.
 template <int RM>
-__device__ void solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, int E, double ma, int& status) {
+__device__ bool solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, int E, int& status) {
+  constexpr int TPO = RM / 8;
   const int r = a.r, rh = pad4(r), P = gridDim.x, p = blockIdx.x, tid = threadIdx.x;
   const int nv = a.ncolmax * r;
   double* zb = sm.vb;
@@ -430,95 +454,85 @@ __device__ void solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, i
   // (sweep & 1) and writes the other, so results do not depend on CTA timing
   double* Xn = a.Xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;
   bool ok = false;
-#define NSPROF(slot)                                                                   \
-  if (a.prof && blockIdx.x == 0) {                                                     \
-    __syncthreads();                                                                   \
-    ns_sink += *(volatile double*)sm.scal;                                             \
-    const long long now = clock64();                                                   \
-    if (threadIdx.x == 0) a.prof[16 + (slot)] += now - ns_t;                           \
-    ns_t = now;                                                                        \
-  }
-  long long ns_t = clock64();
-  double ns_sink = 0.0;
   if (sweep > 0 && a.ns_max > 0) {
-    NSPROF(0);
-    const int nr = p < r ? r : 0;       // first owned warm-start row i = p
-    // stage 1: z = X0' b ; xr = (X0 A)[p, :]
-    for (int o = tid; o < E + nr; o += ALS_NT) {
-      if (o < E) {
-        const int sc = o / r, i = o - sc * r;
-        zb[o] = mv_dot(sm.X0, rh, sm.rb + sc * r, i, r);
-      } else {
-        xr[o - E] = mv_dot(sm.Am, rh, sm.X0 + p * rh, o - E, r);
-      }
+    // stage 1: z = X0' b
+    for (int base = 0; base < E * TPO; base += ALS_NT) {
+      const int t = base + tid, o = t / TPO, part = t - o * TPO;
+      const bool act = o < E;
+      const int sc = act ? o / r : 0, i = act ? o - sc * r : 0;
+      const double acc = mv_dot<RM>(sm.X0, rh, sm.rb + sc * r, i, r, part);
+      if (act && part == 0) zb[o] = acc;
     }
     __syncthreads();
-    NSPROF(1);
-    // stage 2: y = 2b - A z ; X1[p, :] = 2 X0[p, :] - xr X0
-    for (int o = tid; o < E + nr; o += ALS_NT) {
-      if (o < E) {
-        const int sc = o / r, i = o - sc * r;
-        yb[o] = 2.0 * sm.rb[o] - mv_dot(sm.Am, rh, zb + sc * r, i, r);
-      } else {
-        const int c = o - E;
-        Xn[(size_t)p * rh + c] = 2.0 * sm.X0[p * rh + c] - mv_dot(sm.X0, rh, xr, c, r);
-      }
+    // stage 2: y = 2b - A z
+    for (int base = 0; base < E * TPO; base += ALS_NT) {
+      const int t = base + tid, o = t / TPO, part = t - o * TPO;
+      const bool act = o < E;
+      const int sc = act ? o / r : 0, i = act ? o - sc * r : 0;
+      const double acc = mv_dot<RM>(sm.Am, rh, zb + sc * r, i, r, part);
+      if (act && part == 0) yb[o] = 2.0 * sm.rb[o] - acc;
     }
     __syncthreads();
-    NSPROF(2);
-    for (int i0 = p + P; i0 < r; i0 += P) {   // further owned rows (grids smaller than r)
-      for (int c = tid; c < r; c += ALS_NT) xr[c] = mv_dot(sm.Am, rh, sm.X0 + i0 * rh, c, r);
-      __syncthreads();
-      for (int c = tid; c < r; c += ALS_NT) Xn[(size_t)i0 * rh + c] = 2.0 * sm.X0[i0 * rh + c] - mv_dot(sm.X0, rh, xr, c, r);
-      __syncthreads();
-    }
     // stage 3: u = X0' y
-    double mu = 0.0;
-    for (int o = tid; o < E; o += ALS_NT) {
-      const int sc = o / r, i = o - sc * r;
-      const double u = mv_dot(sm.X0, rh, yb + sc * r, i, r);
-      ub[o] = u;
-      mu = fmax(mu, fabs(u));
+    for (int base = 0; base < E * TPO; base += ALS_NT) {
+      const int t = base + tid, o = t / TPO, part = t - o * TPO;
+      const bool act = o < E;
+      const int sc = act ? o / r : 0, i = act ? o - sc * r : 0;
+      const double u = mv_dot<RM>(sm.X0, rh, yb + sc * r, i, r, part);
+      if (act && part == 0) ub[o] = u;
     }
     __syncthreads();
-    NSPROF(3);
-    // stage 4: backward-error check |b - A u|_max <= 1e-13 r |A|_max |u|_max
-    double mres = 0.0;
-    for (int o = tid; o < E; o += ALS_NT) {
-      const int sc = o / r, i = o - sc * r;
-      const double res = sm.rb[o] - mv_dot(sm.Am, rh, ub + sc * r, i, r);
-      mres = fmax(mres, fabs(res));
+    // stage 4: componentwise backward error |b - A u|_i <= 1e-13 r (|A| |u|)_i
+    int bad = 0;
+    for (int base = 0; base < E * TPO; base += ALS_NT) {
+      const int t = base + tid, o = t / TPO, part = t - o * TPO;
+      const bool act = o < E;
+      const int sc = act ? o / r : 0, i = act ? o - sc * r : 0;
+      const double2 au = mv_dot_abs<RM>(sm.Am, rh, ub + sc * r, i, r, part);
+      if (act && part == 0 && !(fabs(sm.rb[o] - au.x) <= 1e-13 * (double)r * au.y)) bad = 1;
     }
-    mres = (mres != mres) ? INFINITY : mres;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mres = fmax(mres, __shfl_xor_sync(0xffffffffu, mres, o));
-      mu = fmax(mu, __shfl_xor_sync(0xffffffffu, mu, o));
-      ma = fmax(ma, __shfl_xor_sync(0xffffffffu, ma, o));
-    }
-    double* red = sm.part;
-    if ((tid & 31) == 0) { red[tid >> 5] = mres; red[8 + (tid >> 5)] = mu; red[16 + (tid >> 5)] = ma; }
-    __syncthreads();
-    mres = red[0]; mu = red[8]; ma = red[16];
-#pragma unroll
-    for (int w = 1; w < ALS_NW; ++w) { mres = fmax(mres, red[w]); mu = fmax(mu, red[8 + w]); ma = fmax(ma, red[16 + w]); }
-    ok = mres <= 1e-13 * (double)r * ma * mu;
-    if (a.prof && p == 0 && tid == 0) a.prof[ok ? 14 : 15] += 1;
-    __syncthreads();
-    NSPROF(4);
+    ok = !__syncthreads_or(bad);
   }
-  if (ns_sink == 12345.0) a.prof[24] += 1;
-  if (ok) return;
+  if (ok) return true;
   status |= gram_inverse<RM>(a, sm, j, sm.X0, rh);
   __syncthreads();
-  for (int o = tid; o < E; o += ALS_NT) {
-    const int sc = o / r, i = o - sc * r;
-    ub[o] = mv_dot(sm.X0, rh, sm.rb + sc * r, i, r);
+  for (int base = 0; base < E * TPO; base += ALS_NT) {
+    const int t = base + tid, o = t / TPO, part = t - o * TPO;
+    const bool act = o < E;
+    const int sc = act ? o / r : 0, i = act ? o - sc * r : 0;
+    const double u = mv_dot<RM>(sm.X0, rh, sm.rb + sc * r, i, r, part);
+    if (act && part == 0) ub[o] = u;
   }
   if (a.ns_max > 0)
-    for (int i0 = p; i0 < r; i0 += P)
+    for (int i0 = P - 1 - p; i0 < r; i0 += P)
       for (int c = tid; c < r; c += ALS_NT) Xn[(size_t)i0 * rh + c] = sm.X0[i0 * rh + c];
   __syncthreads();
+  return false;
+}
+
+// Owned rows i == P-1-p (mod P) of the next warm start X1 = 2 X0 - X0 A X0 for
+// the mode solved last (A and X0 still in shared memory), phase A of the next
+// mode update (off the solve's critical path; the top CTAs own no Gram tiles).
+template <int RM>
+__device__ void ns_rows(const AlsArgs& a, const Smem& sm, int j, int sweep) {
+  constexpr int TPO = RM / 8;
+  const int r = a.r, rh = pad4(r), P = gridDim.x, p = blockIdx.x, tid = threadIdx.x;
+  double* Xn = a.Xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;
+  double* xr = sm.Rm;
+  for (int i0 = P - 1 - p; i0 < r; i0 += P) {
+    for (int base = 0; base < r * TPO; base += ALS_NT) {
+      const int t = base + tid, c = t / TPO, part = t - c * TPO;
+      const double acc = mv_dot<RM>(sm.Am, rh, sm.X0 + i0 * rh, c < r ? c : 0, r, part);
+      if (c < r && part == 0) xr[c] = acc;
+    }
+    __syncthreads();
+    for (int base = 0; base < r * TPO; base += ALS_NT) {
+      const int t = base + tid, c = t / TPO, part = t - c * TPO;
+      const double acc = mv_dot<RM>(sm.X0, rh, xr, c < r ? c : 0, r, part);
+      if (c < r && part == 0) Xn[(size_t)i0 * rh + c] = 2.0 * sm.X0[i0 * rh + c] - acc;
+    }
+    __syncthreads();
+  }
 }
 
 // debug phase timers: barrier-synchronised so the attribution is exact
@@ -588,7 +602,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   const double norm_sq = a.need_resid ? fmax(*a.norm_sq, 0.0) : 0.0;
   const double t_norm = sqrt(norm_sq);
   double prev = INFINITY;
-  int pending = -1, done = 0;
+  int pending = -1, done = 0, rows_mode = -1, rows_sweep = 0;
   const bool bulk = (r & 1) == 0;
 
   for (int sweep = 0; sweep < a.sweeps; ++sweep) {
@@ -601,6 +615,10 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         if (!(a.dbg_skip & 4)) cross_slab<RM>(a, sm, pending, w);
         PROF(11);
         if (!(a.dbg_skip & 8)) gram_share(a, sm, pending);
+      }
+      if (rows_mode >= 0) {   // warm-start rows of the previous NS solve
+        ns_rows<RM>(a, sm, rows_mode, rows_sweep);
+        rows_mode = -1;
       }
       PROF(1);
       const int Qj = a.q[j], qsj = a.qs[j];
@@ -668,7 +686,6 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       const int nb = a.ncolmax * r;     // one producer's block for this consumer
       double* ystage = sm.Us;           // [q][nb]
       const bool warm_ns = sweep > 0 && a.ns_max > 0;
-      double ma = 0.0;
       if (bulk) {
         if (tid == 0) {
           const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
@@ -683,7 +700,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         }
         mbar_wait(sm.bar + 1, gphase);
         gphase ^= 1u;
-        if (warm_ns) ma = build_a<RM>(a, sm, j);   // overlaps the slice fetch
+        if (warm_ns) build_a<RM>(a, sm, j);   // overlaps the slice fetch
         PROF(8);
         mbar_wait(sm.bar, bphase);
         bphase ^= 1u;
@@ -712,11 +729,11 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
           sm.rb[o] = acc;
         }
         __syncthreads();
-        if (warm_ns) ma = build_a<RM>(a, sm, j);
+        if (warm_ns) build_a<RM>(a, sm, j);
       }
       __syncthreads();
       PROF(4);
-      if (!(a.dbg_skip & 1)) solve_mode<RM>(a, sm, j, sweep, E, ma, status);
+      if (!(a.dbg_skip & 1) && solve_mode<RM>(a, sm, j, sweep, E, status)) { rows_mode = j; rows_sweep = sweep; }
       PROF(9);
       if (E > 0) {
         const double* ub = sm.vb + 2 * a.ncolmax * r;

@@ -35,8 +35,6 @@ def run(grid, Q=256, R=512, r=32):
     for i in [0, 10, 11, 1, 2, 3, 8, 5, 4, 9, 6, 7]:
         print(f"   {NAMES[i]:22s} {p[i]:9.0f}  ({100*p[i]/tot:4.1f}%)")
     raw = prof.cpu().numpy()
-    print("   NS sub-phases (cycles per mode): build_a %.0f  st1 %.0f  st2 %.0f  st3 %.0f  check %.0f" % tuple(raw[16:21] / 120.0))
-    print(f"   Newton-Schulz accepted {raw[14]}, fell back {raw[15]}, residual checks {raw[13]}, one-step accepts {raw[12]}")
 
 
 if __name__ == "__main__":
