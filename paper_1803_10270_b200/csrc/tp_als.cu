@@ -66,6 +66,10 @@ struct AlsArgs {
   double* Xprev;           // [d][r][pad4(r)] last inverse per mode (warm start for Newton-Schulz)
   double* Upad;            // U_k with rows padded to pad4(r) (bulk-staged into conflict-free smem)
   long long offUp[TP_MAXD];
+  // cluster variant (als_cluster): Pq CTAs per cluster share an R-slab, CTA b of a
+  // cluster owns row block b of every mode
+  int Pq, ldw, chunk, nbmax;
+  int qoffc[TP_MAXD];      // shared-memory offset of V_k[block rows, slab] ([s][c], stride ldw)
   int ns_max;              // Newton-Schulz iterations before falling back to the exact sweep
 };
 
@@ -73,6 +77,7 @@ struct Smem {
   uint64_t* bar;        // bar[0]: U staging / Y slices, bar[1]: Gram
   double *Us, *Vs, *Cs, *Gs, *hadT, *Am, *X0, *X1, *Rm, *pub, *rb, *vb, *part, *scal;
   int* rowmap;          // [d][qmax]: (consumer CTA << 16) | row-in-consumer
+  double *inbox, *mine;  // cluster variant: reduce-scatter inbox, this CTA's partial vector
 };
 
 __host__ __device__ inline size_t stage_doubles(int qmax, int r, int ncolmax, int P) {
@@ -622,8 +627,8 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       }
       PROF(1);
       const int Qj = a.q[j], qsj = a.qs[j];
-      for (int e = tid; e < r * w; e += ALS_NT) {
-        const int c = e / r, l = e - c * r;
+      for (int e = tid; e < r * w; e += ALS_NT) {   // lanes along c: conflict-free Cs rows
+        const int l = e / w, c = e - l * w;
         double f[TP_MAXD];
 #pragma unroll
         for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < a.d && k != j) ? sm.Cs[((size_t)k * r + l) * a.wmax + c] : 1.0;
@@ -804,20 +809,570 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   }
 }
 
+// ===========================================================================
+// Cluster variant.  The grid is Pr clusters x Pq CTAs; cluster a owns R-slab a,
+// CTA b of the cluster owns row block b of every mode.  A mode update keeps the
+// two grid barriers of als_persistent but moves ~5x less data per CTA: the
+// cross C_k[:, slab] = U_k^T V_k[:, slab] is summed over the Pq row blocks
+// inside the cluster (TMA bulk copies between the CTAs' shared memories, fixed
+// order), so each CTA stages only its block of U_k and writes only its block's
+// rows of the partial right-hand side.  The upper 8x8 Gram tiles are dealt to
+// clusters and reach every CTA through global memory after the next barrier.
+// ===========================================================================
+
+__host__ __device__ inline size_t cl_stage_doubles(int nbmax, int r, int ncolmax, int Pr) {
+  size_t x = (size_t)(((nbmax + 3) & ~3) + 1) * pad4(r), y = (size_t)Pr * ncolmax * r;
+  return x > y ? x : y;
+}
+
+__host__ __device__ inline size_t cl_smem_doubles(int d, int r, int wmax, int ldw, int sumnb, int nbmax, int ncolmax,
+                                                  int Pr, int Pq, int chunk, int qmax) {
+  const size_t w4 = (size_t)((wmax + 3) / 4) * 4, rh = pad4(r);
+  return 8 + cl_stage_doubles(nbmax, r, ncolmax, Pr) + (size_t)sumnb * ldw + (size_t)d * r * wmax + (size_t)d * r * r +
+         w4 * rh + (size_t)Pq * chunk + (size_t)Pq * chunk + 3 * (size_t)r * rh + 72 + 4 * (size_t)ncolmax * r +
+         ALS_PART + 8 + ((size_t)d * qmax + 1) / 2 + 1;
+}
+
+__device__ inline Smem carve_cl(double* base, const AlsArgs& a, int Pr) {
+  Smem s;
+  size_t o = 0;
+  s.bar = reinterpret_cast<uint64_t*>(base + o); o += 8;
+  s.Us = base + o; o += cl_stage_doubles(a.nbmax, a.r, a.ncolmax, Pr);
+  s.Vs = base + o; o += (size_t)a.sumqs * a.ldw;        // sumqs holds the padded sum of block rows here
+  s.Cs = base + o; o += (size_t)a.d * a.r * a.wmax;     // Cs[k]: r x w, row stride w
+  s.Gs = base + o; o += (size_t)a.d * a.r * a.r;
+  s.hadT = base + o; o += (size_t)((a.wmax + 3) / 4) * 4 * pad4(a.r);
+  s.inbox = base + o; o += (size_t)a.Pq * a.chunk;
+  s.mine = base + o; o += (size_t)a.Pq * a.chunk;
+  s.Am = base + o; o += (size_t)a.r * pad4(a.r);
+  s.X0 = base + o; o += (size_t)a.r * pad4(a.r);
+  s.X1 = nullptr;
+  s.Rm = base + o; o += (size_t)a.r * pad4(a.r);
+  s.pub = base + o; o += 72;
+  s.rb = base + o; o += (size_t)a.ncolmax * a.r;
+  s.vb = base + o; o += 3 * (size_t)a.ncolmax * a.r;
+  s.part = base + o; o += ALS_PART;
+  s.scal = base + o; o += 8;
+  s.rowmap = reinterpret_cast<int*>(base + o);
+  return s;
+}
+
+// U_k rows [qb0, qb0 + nb) -> sm.Us (row stride pad4(r)): bulk copy of the padded
+// copy, or plain loads from the user's U for the initial guess.  Rows
+// [nb, ceil4(nb)) are zeroed (K padding of the unpredicated DMMA loads).
+__device__ void cl_stage_u(const AlsArgs& a, const Smem& sm, int k, int qb0, int nb, uint32_t& phase, bool from_user) {
+  const int r = a.r, rh = pad4(r);
+  __syncthreads();
+  if (nb > 0) {
+    if (!from_user) {
+      if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)(nb * rh) * 8u;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(sm.bar, bytes);
+        bulk_g2s(sm.Us, a.Upad + a.offUp[k] + (size_t)qb0 * rh, bytes, sm.bar);
+      }
+      mbar_wait(sm.bar, phase);
+      phase ^= 1u;
+    } else {
+      const double* Uk = a.U + a.offU[k] + (size_t)qb0 * r;
+      for (int e = threadIdx.x; e < nb * r; e += ALS_NT) sm.Us[(e / r) * rh + e % r] = __ldcg(Uk + e);
+    }
+  }
+  const int nb4 = (nb + 3) & ~3;
+  for (int e = threadIdx.x; e < (nb4 - nb) * rh; e += ALS_NT) sm.Us[(size_t)nb * rh + e] = 0.0;
+  __syncthreads();
+}
+
+// NS independent 8x8 DMMA chains over K = 4 ksteps rows: acc[u] += A^T B_u with
+// A rows at a0 + s*arow (lane column fixed), B_u rows at b[u] + s*bst[u].  Rows
+// past the block are zero and out-of-range lanes read in-bounds padding that only
+// feeds discarded outputs, so the loads carry no predicates.
+template <int NS>
+__device__ __forceinline__ void cl_chains(uint32_t a0, uint32_t arow, const uint32_t* b, const uint32_t* bst, int ksteps,
+                                          double (&acc)[NS][2]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < NS; ++u) acc[u][0] = acc[u][1] = 0.0;
+#pragma unroll 2
+  for (int kk = 0; kk < ksteps; ++kk) {
+    const uint32_t s = 4u * (uint32_t)kk + (uint32_t)(lane & 3);
+    const double fa = lds64(a0 + s * arow);
+    double fb[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) fb[u] = lds64(b[u] + s * bst[u]);
+#pragma unroll
+    for (int u = 0; u < NS; ++u) dmma_8x8x4(acc[u][0], acc[u][1], fa, fb[u]);
+  }
+}
+
+// C items: m tile x group of NS n tiles of C[:, :w] = U_blk^T V_blk
+template <int NS>
+__device__ __forceinline__ void cl_c_item(const AlsArgs& a, const Smem& sm, const double* vs, int w, int nb, int m, int n0) {
+  const int r = a.r, rh = pad4(r), lane = threadIdx.x & 31, ntc = (w + 7) / 8;
+  const uint32_t us32 = smem_u32(sm.Us), vs32 = smem_u32(vs);
+  uint32_t b[NS], bst[NS];
+#pragma unroll
+  for (int u = 0; u < NS; ++u) {
+    const int n = min(n0 + u, ntc - 1);
+    b[u] = vs32 + 8u * (uint32_t)(n * 8 + (lane >> 2));
+    bst[u] = 8u * (uint32_t)a.ldw;
+  }
+  double acc[NS][2];
+  cl_chains<NS>(us32 + 8u * (uint32_t)(m * 8 + (lane >> 2)), 8u * (uint32_t)rh, b, bst, (nb + 3) / 4, acc);
+  const int orow = m * 8 + (lane >> 2);
+  if (orow >= r) return;
+#pragma unroll
+  for (int u = 0; u < NS; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ocol = (n0 + u) * 8 + 2 * (lane & 3) + h;
+      if (n0 + u < ntc && ocol < w) sm.mine[orow * w + ocol] = acc[u][h];
+    }
+}
+
+// this CTA's partials over its nb block rows of mode k into sm.mine:
+// [0, r w): C[l][c] = sum_s U[s][l] V[s][c];  then for each upper Gram tile t
+// owned by this cluster (t == cid mod Pr): 64 entries of sum_s U[s][l] U[s][m]
+template <int RM>
+__device__ void cl_partials(const AlsArgs& a, const Smem& sm, int k, int w, int nb, int cid, int Pr) {
+  const int r = a.r, rh = pad4(r), warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mtr = (r + 7) / 8, ntc = (w + 7) / 8, nG = mtr * (mtr + 1) / 2;
+  const double* vs = sm.Vs + a.qoffc[k];
+  int ngroups = (ALS_NW + mtr - 1) / mtr;
+  if (ngroups > ntc) ngroups = ntc;
+  int ns = (ntc + ngroups - 1) / ngroups;
+  if (ns > 4) { ns = 4; ngroups = (ntc + 3) / 4; }
+  const int nCi = mtr * ngroups, nGi = cid < nG ? (nG - 1 - cid) / Pr + 1 : 0;
+  for (int it = warp; it < nCi + nGi; it += ALS_NW) {
+    if (it < nCi) {
+      const int m = it / ngroups, n0 = (it - m * ngroups) * ns;
+      if (ns == 4) cl_c_item<4>(a, sm, vs, w, nb, m, n0);
+      else if (ns == 3) cl_c_item<3>(a, sm, vs, w, nb, m, n0);
+      else if (ns == 2) cl_c_item<2>(a, sm, vs, w, nb, m, n0);
+      else cl_c_item<1>(a, sm, vs, w, nb, m, n0);
+    } else {
+      const int gi = it - nCi;
+      int g = cid + gi * Pr, ti = 0;
+      while (g >= mtr - ti) { g -= mtr - ti; ++ti; }
+      const int tj = ti + g;
+      const uint32_t us32 = smem_u32(sm.Us);
+      const uint32_t b[1] = {us32 + 8u * (uint32_t)(tj * 8 + (lane >> 2))}, bst[1] = {8u * (uint32_t)rh};
+      double acc[1][2];
+      cl_chains<1>(us32 + 8u * (uint32_t)(ti * 8 + (lane >> 2)), 8u * (uint32_t)rh, b, bst, (nb + 3) / 4, acc);
+      double* t = sm.mine + (size_t)r * w + (size_t)gi * 64;
+      t[2 * lane] = acc[0][0];
+      t[2 * lane + 1] = acc[0][1];
+    }
+  }
+  __syncthreads();
+}
+
+// Cluster all-reduce of sm.mine (C slab partial [l][c] stride w, then this
+// cluster's Gram tiles), all by TMA bulk copies between the CTAs' shared
+// memories: every CTA pushes chunk q of its partial into CTA q's inbox, CTA q
+// sums its chunk in fixed rank order, keeps the C part in its own Cs[k] (r x w,
+// stride w) and pushes it into every peer's Cs[k]; reduced Gram tiles go to
+// global G (consumed after the next grid barrier).  Completion is tracked by
+// mbarriers sm.bar[2] (inbox) and sm.bar[3] (Cs); buffers are reused only after
+// grid barriers, so no cluster barrier is needed.
+__device__ void cl_exchange(const AlsArgs& a, const Smem& sm, cg::cluster_group& cl, int k, int w, int cid, int Pr,
+                            uint32_t& ph) {
+  const int r = a.r, rr = r * r, Pq = a.Pq, chunk = a.chunk, b = (int)cl.block_rank(), tid = threadIdx.x;
+  const int mtr = (r + 7) / 8, nG = mtr * (mtr + 1) / 2, nGi = cid < nG ? (nG - 1 - cid) / Pr + 1 : 0;
+  const int rw = r * w, L = rw + nGi * 64;
+  double* Ck = sm.Cs + (size_t)k * r * a.wmax;
+  const uint32_t bar_in = smem_u32(sm.bar + 2), bar_cs = smem_u32(sm.bar + 3);
+  auto clen = [&](int q) { const int lo = q * chunk, hi = min((q + 1) * chunk, rw); return hi > lo ? hi - lo : 0; };
+  __syncthreads();   // sm.mine complete
+  if (tid == 0) {
+    uint32_t cs_bytes = 0;
+    for (int q = 0; q < Pq; ++q) if (q != b) cs_bytes += 8u * (uint32_t)clen(q);
+    mbar_arrive_expect_tx(sm.bar + 2, 8u * (uint32_t)((Pq - 1) * chunk));
+    mbar_arrive_expect_tx(sm.bar + 3, cs_bytes);
+    fence_proxy_async();
+    const uint32_t inbox = smem_u32(sm.inbox) + 8u * (uint32_t)(b * chunk);
+    for (int q = 0; q < Pq; ++q)
+      if (q != b) bulk_s2cluster(mapa_u32(inbox, q), sm.mine + (size_t)q * chunk, 8u * (uint32_t)chunk, mapa_u32(bar_in, q));
+  }
+  mbar_wait(sm.bar + 2, ph);
+  double* Gk = a.G + (size_t)k * rr;
+  for (int e = tid; e < chunk; e += ALS_NT) {
+    const int idx = b * chunk + e;
+    if (idx < L) {
+      double v = 0.0;
+      for (int src = 0; src < Pq; ++src) v += (src == b) ? sm.mine[idx] : sm.inbox[(size_t)src * chunk + e];
+      if (idx < rw) {
+        Ck[idx] = v;
+      } else {
+        const int gi = (idx - rw) >> 6, ln = ((idx - rw) & 63) >> 1, h = (idx - rw) & 1;
+        int g = cid + gi * Pr, ti = 0;
+        while (g >= mtr - ti) { g -= mtr - ti; ++ti; }
+        const int tj = ti + g;
+        const int orow = ti * 8 + (ln >> 2), ocol = tj * 8 + 2 * (ln & 3) + h;
+        if (orow < r && ocol < r) { Gk[orow * r + ocol] = v; Gk[ocol * r + orow] = v; }
+      }
+    }
+  }
+  __syncthreads();
+  const int my = clen(b);
+  if (tid == 0 && my > 0) {
+    fence_proxy_async();
+    const uint32_t dst = smem_u32(Ck + (size_t)b * chunk);
+    for (int q = 0; q < Pq; ++q)
+      if (q != b) bulk_s2cluster(mapa_u32(dst, q), Ck + (size_t)b * chunk, 8u * (uint32_t)my, mapa_u32(bar_cs, q));
+  }
+  mbar_wait(sm.bar + 3, ph);
+  ph ^= 1u;
+}
+
+// had = prod_{k != j} C_k[:, slab] -> hadT[c][l], then the rows of block b of the
+// partial right-hand side Y[s][l] = sum_c V_j[s][c] had[l][c] (M = s, N = l,
+// K = c; DMMA, RM/8 independent chains per row tile), stored consumer-major
+// YT[pc][cluster][row-in-pc][:] for phase B.  Shared loads use 32-bit
+// addresses and no predicates (zero padding rows/columns, discarded lanes).
+template <int RM>
+__device__ void cl_had_y(const AlsArgs& a, const Smem& sm, int j, int w, int b, int cid, int Pr) {
+  constexpr int NT = RM / 8;
+  const int r = a.r, rh = pad4(r), ldw = a.ldw, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t cs32 = smem_u32(sm.Cs), ks = 8u * (uint32_t)(r * a.wmax);   // Cs[k]: r x w, stride w
+  for (int e = tid; e < r * w; e += ALS_NT) {   // lanes along c: conflict-free Cs rows
+    const int l = e / w, c = e - l * w;
+    const uint32_t base = cs32 + 8u * (uint32_t)(l * w + c);
+    double f[TP_MAXD];
+#pragma unroll
+    for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < a.d && k != j) ? lds64(base + (uint32_t)k * ks) : 1.0;
+    double v = 1.0;
+#pragma unroll
+    for (int k = 0; k < TP_MAXD; ++k) v *= f[k];
+    sm.hadT[c * rh + l] = v;
+  }
+  __syncthreads();
+  const int Qj = a.q[j], Pq = a.Pq, qb0 = Qj * b / Pq, nb = Qj * (b + 1) / Pq - qb0;
+  const int mt = (nb + 7) / 8, kst = (w + 3) / 4;
+  const uint32_t vs32 = smem_u32(sm.Vs + a.qoffc[j]), hd32 = smem_u32(sm.hadT);
+  for (int m = warp; m < mt; m += ALS_NW) {
+    const int s = m * 8 + (lane >> 2);
+    const uint32_t arow = vs32 + 8u * (uint32_t)(s * ldw + (lane & 3));
+    const uint32_t brow = hd32 + 8u * (uint32_t)((lane & 3) * rh + (lane >> 2));
+    double acc[NT][2];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+#pragma unroll 2
+    for (int kk = 0; kk < kst; ++kk) {
+      const double av = lds64(arow + 32u * (uint32_t)kk);
+      double fb[NT];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) fb[n] = lds64(brow + 8u * (uint32_t)(4 * kk * rh + 8 * n));
+#pragma unroll
+      for (int n = 0; n < NT; ++n) dmma_8x8x4(acc[n][0], acc[n][1], av, fb[n]);
+    }
+    if (s < nb) {
+      const int rm = sm.rowmap[j * a.qmax + qb0 + s];
+      const int pc = rm >> 16, ii = rm & 0xffff;
+      double* yrow = a.Y + (((size_t)pc * Pr + cid) * a.ncolmax + ii) * r;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int ocol = n * 8 + 2 * (lane & 3);
+        if (ocol + 1 < r && (r & 1) == 0) {
+          *reinterpret_cast<double2*>(yrow + ocol) = make_double2(acc[n][0], acc[n][1]);
+        } else {
+          if (ocol < r) yrow[ocol] = acc[n][0];
+          if (ocol + 1 < r) yrow[ocol + 1] = acc[n][1];
+        }
+      }
+    }
+  }
+}
+
+template <int RM>
+__global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__ AlsArgs a) {
+  extern __shared__ double smem[];
+  cg::cluster_group cl = cg::this_cluster();
+  long long prof_t = clock64();
+  long long prof_acc[16] = {};
+  double prof_sink = 0.0;
+  unsigned int epoch = 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Pq = a.Pq, b = (int)cl.block_rank(), p = blockIdx.x, P = gridDim.x, cid = p / Pq, Pr = P / Pq;
+  const Smem sm = carve_cl(smem, a, Pr);
+  const int r = a.r, R = a.R, rr = r * r, rh = pad4(r), ldw = a.ldw;
+  const int c0 = (int)((long long)R * cid / Pr), c1 = (int)((long long)R * (cid + 1) / Pr), w = c1 - c0;
+  const int w4 = (w + 3) / 4 * 4;
+  int status = 0;
+  uint32_t bphase = 0, gphase = 0, xphase = 0;
+  if (tid == 0) {
+    for (int q = 0; q < 4; ++q) mbar_init(sm.bar + q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int k = 0; k < a.d; ++k)
+    for (int s2 = tid; s2 < a.q[k]; s2 += ALS_NT) {
+      const int Qk = a.q[k];
+      const int pc = ((s2 + 1) * P + Qk - 1) / Qk - 1;       // CTA owning row s2 in phase B
+      const int ii = s2 - (Qk * pc) / P;
+      sm.rowmap[k * a.qmax + s2] = (pc << 16) | ii;
+    }
+  for (int e = tid; e < (w4 - w) * rh; e += ALS_NT) sm.hadT[(size_t)w * rh + e] = 0.0;
+  // ---- setup: V block rows x slab columns for every mode ([s][c], stride ldw);
+  // padding rows/columns stay zero
+  for (int e = tid; e < a.sumqs * ldw; e += ALS_NT) sm.Vs[e] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < a.d; ++k) {
+    const int Qk = a.q[k], qb0 = Qk * b / Pq, nb = Qk * (b + 1) / Pq - qb0;
+    const double* Vk = a.V + a.offV[k] + (size_t)qb0 * R + c0;
+    double* vs = sm.Vs + a.qoffc[k];
+    for (int e = tid; e < nb * w; e += ALS_NT) {
+      const int s2 = e / w, c = e - s2 * w;
+      vs[s2 * ldw + c] = Vk[(size_t)s2 * R + c];
+    }
+  }
+  cl.sync();   // peers' mbarriers initialised before any DSMEM copy
+  for (int k = 0; k < a.d; ++k) {
+    const int Qk = a.q[k], qb0 = Qk * b / Pq, nb = Qk * (b + 1) / Pq - qb0;
+    cl_stage_u(a, sm, k, qb0, nb, bphase, true);
+    cl_partials<RM>(a, sm, k, w, nb, cid, Pr);
+    cl_exchange(a, sm, cl, k, w, cid, Pr, xphase);
+  }
+  grid_barrier(a.bar_ctr, epoch);
+  for (int e = tid; e < a.d * rr; e += ALS_NT) sm.Gs[e] = __ldcg(a.G + e);
+  __syncthreads();
+
+  const double norm_sq = a.need_resid ? fmax(*a.norm_sq, 0.0) : 0.0;
+  const double t_norm = sqrt(norm_sq);
+  double prev = INFINITY;
+  int pending = -1, done = 0, rows_mode = -1, rows_sweep = 0;
+  const bool bulk = (r & 1) == 0;
+
+  for (int sweep = 0; sweep < a.sweeps; ++sweep) {
+    for (int j = 0; j < a.d; ++j) {
+      // ---------------- phase A
+      PROF(0);
+      if (pending >= 0) {
+        const int Qk = a.q[pending], qb0 = Qk * b / Pq, nb = Qk * (b + 1) / Pq - qb0;
+        cl_stage_u(a, sm, pending, qb0, nb, bphase, false);
+        PROF(10);
+        cl_partials<RM>(a, sm, pending, w, nb, cid, Pr);
+        PROF(11);
+        cl_exchange(a, sm, cl, pending, w, cid, Pr, xphase);
+        PROF(12);
+      }
+      if (rows_mode >= 0) {
+        ns_rows<RM>(a, sm, rows_mode, rows_sweep);
+        rows_mode = -1;
+      }
+      PROF(1);
+      const int Qj = a.q[j];
+      cl_had_y<RM>(a, sm, j, w, b, cid, Pr);
+      PROF(2);
+      grid_barrier(a.bar_ctr, epoch);
+      PROF(3);
+      // ---------------- phase B (rows [s0, s1) of mode j)
+      const int s0 = (int)((long long)Qj * p / P), s1 = (int)((long long)Qj * (p + 1) / P);
+      const int ncol = s1 - s0, E = ncol * r;
+      const int nbk = a.ncolmax * r;
+      double* ystage = sm.Us;
+      const bool warm_ns = sweep > 0 && a.ns_max > 0;
+      if (bulk) {
+        if (tid == 0) {
+          const uint32_t ybytes = E > 0 ? (uint32_t)(Pr * nbk) * 8u : 0u;
+          const uint32_t xbytes = warm_ns ? (uint32_t)(r * rh) * 8u : 0u;
+          const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
+          fence_proxy_async();
+          mbar_arrive_expect_tx(sm.bar + 1, xbytes + gbytes);
+          if (gbytes) bulk_g2s(sm.Gs + (size_t)pending * rr, a.G + (size_t)pending * rr, gbytes, sm.bar + 1);
+          if (xbytes) bulk_g2s(sm.X0, a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh, xbytes, sm.bar + 1);
+          mbar_arrive_expect_tx(sm.bar, ybytes);
+          if (ybytes) bulk_g2s(ystage, a.Y + (size_t)p * Pr * nbk, ybytes, sm.bar);
+        }
+        mbar_wait(sm.bar + 1, gphase);
+        gphase ^= 1u;
+        if (warm_ns) build_a<RM>(a, sm, j);   // overlaps the slice fetch
+        PROF(8);
+        mbar_wait(sm.bar, bphase);
+        bphase ^= 1u;
+        PROF(5);
+        for (int o = tid; o < E; o += ALS_NT) {
+          double s0a = 0.0, s1a = 0.0;
+          int q = 0;
+          for (; q + 2 <= Pr; q += 2) {
+            s0a += ystage[(size_t)q * nbk + o];
+            s1a += ystage[(size_t)(q + 1) * nbk + o];
+          }
+          for (; q < Pr; ++q) s0a += ystage[(size_t)q * nbk + o];
+          sm.rb[o] = s0a + s1a;
+        }
+      } else {
+        if (pending >= 0)
+          for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * rr + e] = __ldcg(a.G + (size_t)pending * rr + e);
+        if (warm_ns)
+          for (int e = tid; e < r * rh; e += ALS_NT)
+            sm.X0[e] = __ldcg(a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh + e);
+        for (int o = tid; o < E; o += ALS_NT) {
+          double s0a = 0.0, s1a = 0.0;
+          int q = 0;
+          for (; q + 2 <= Pr; q += 2) {
+            s0a += __ldcg(a.Y + ((size_t)p * Pr + q) * nbk + o);
+            s1a += __ldcg(a.Y + ((size_t)p * Pr + q + 1) * nbk + o);
+          }
+          for (; q < Pr; ++q) s0a += __ldcg(a.Y + ((size_t)p * Pr + q) * nbk + o);
+          sm.rb[o] = s0a + s1a;
+        }
+        __syncthreads();
+        if (warm_ns) build_a<RM>(a, sm, j);
+      }
+      __syncthreads();
+      PROF(4);
+      if (solve_mode<RM>(a, sm, j, sweep, E, status)) { rows_mode = j; rows_sweep = sweep; }
+      PROF(9);
+      if (E > 0) {
+        const double* ub = sm.vb + 2 * a.ncolmax * r;
+        double* Uj = a.U + a.offU[j];
+        double* Up = a.Upad + a.offUp[j];
+        int nf = 0;
+        for (int e = tid; e < E; e += ALS_NT) {
+          const int sc = e / r, i = e - sc * r;
+          const double v = ub[e];
+          if (!isfinite(v)) nf = 1;
+          Uj[(size_t)(s0 + sc) * r + i] = v;
+          Up[(size_t)(s0 + sc) * rh + i] = v;
+        }
+        if (nf) atomicOr(a.info, 2);
+      }
+      pending = j;
+      PROF(6);
+      grid_barrier(a.bar_ctr, epoch);
+      PROF(7);
+    }
+    done = sweep + 1;
+    if (a.need_resid) {
+      // finish the last mode, then residual by the Gram identity (cp.py:321-326)
+      const int Qk = a.q[pending], qb0 = Qk * b / Pq, nb = Qk * (b + 1) / Pq - qb0;
+      cl_stage_u(a, sm, pending, qb0, nb, bphase, false);
+      cl_partials<RM>(a, sm, pending, w, nb, cid, Pr);
+      cl_exchange(a, sm, cl, pending, w, cid, Pr, xphase);
+      double ov = 0.0;
+      if (b == 0)
+        for (int e = tid; e < r * w; e += ALS_NT) {
+          const int l = e / w, c = e % w;
+          double v = 1.0;
+          for (int k = 0; k < a.d; ++k) v *= sm.Cs[(size_t)k * r * a.wmax + l * w + c];
+          ov += v;
+        }
+      ov = block_sum(ov, sm.part);
+      if (tid == 0 && b == 0) a.ovl[cid] = ov;
+      grid_barrier(a.bar_ctr, epoch);
+      for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * rr + e] = __ldcg(a.G + (size_t)pending * rr + e);
+      pending = -1;
+      __syncthreads();
+      double self = 0.0;
+      for (int e = tid; e < rr; e += ALS_NT) {
+        double v = 1.0;
+        for (int k = 0; k < a.d; ++k) v *= sm.Gs[(size_t)k * rr + e];
+        self += v;
+      }
+      self = block_sum(self, sm.part);
+      double ovt = 0.0;
+      if (warp == 0) {
+        for (int q = lane; q < Pr; q += 32) ovt += __ldcg(a.ovl + q);
+        ovt = warp_sum(ovt);
+        if (lane == 0) sm.scal[0] = ovt;
+      }
+      __syncthreads();
+      ovt = sm.scal[0];
+      const double resid = sqrt(fmax(norm_sq - 2.0 * ovt + self, 0.0));
+      if (p == 0 && tid == 0 && a.trace) a.trace[sweep] = resid;
+      __syncthreads();
+      if (resid <= a.tol * t_norm) break;
+      if (prev - resid < a.stall * fmax(t_norm, 1.0)) break;
+      prev = resid;
+    }
+  }
+  if (status && tid == 0 && p == 0) atomicOr(a.info, 1);
+  if (p == 0 && tid == 0) a.info[1] = done;
+  if (a.prof && p == 0 && tid == 0) {
+    for (int q = 0; q < 16; ++q) a.prof[q] += prof_acc[q];
+    if (prof_sink == 12345.0) a.prof[11] += 1;
+  }
+  cl.sync();   // no CTA may exit while peers can still address its shared memory
+}
+
 struct AlsPlan {
   AlsArgs a;
-  int P, rm;
-  size_t smem, ws_inner, ws_total;
+  int P, rm, variant, Pr;   // variant 0: als_persistent, 1: als_cluster (P = Pr * a.Pq)
+  size_t smem, ws_inner, ws_total, ydoubles;
 };
+
+static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 force als_cluster
+static int g_cluster = 0;   // debug hook: cluster size (0 = auto)
 
 static int choose_rm(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : 0)); }
 
-static const void* kernel_ptr(int rm) {
+static const void* kernel_ptr(int rm, int variant) {
+  if (variant == 1) {
+    switch (rm) {
+      case 8: return (const void*)als_cluster<8>;
+      case 16: return (const void*)als_cluster<16>;
+      default: return (const void*)als_cluster<32>;
+    }
+  }
   switch (rm) {
     case 8: return (const void*)als_persistent<8>;
     case 16: return (const void*)als_persistent<16>;
     default: return (const void*)als_persistent<32>;
   }
+}
+
+static size_t ws_total_for(int d, const int* q, int r, int P, size_t ydoubles, size_t ws_inner) {
+  long long nup = 0;
+  for (int k = 0; k < d; ++k) nup += (long long)q[k] * pad4(r);
+  return align_up(sizeof(double) * (size_t)d * r * r) + align_up(sizeof(double) * ydoubles) +
+         align_up(sizeof(double) * (size_t)P) + align_up(sizeof(double)) + ws_inner + 256 +
+         align_up(sizeof(double) * 2 * (size_t)d * r * pad4(r)) + align_up(sizeof(double) * (size_t)nup);
+}
+
+// cluster variant: Pq CTAs per cluster, as many clusters (R-slabs) as can be co-resident
+static int plan_cluster(int d, const int* q, int R, int r, int Pq, int smem_optin, int nsm, AlsPlan& pl) {
+  int qmin = q[0], qmax = 0;
+  for (int k = 0; k < d; ++k) { qmin = q[k] < qmin ? q[k] : qmin; qmax = q[k] > qmax ? q[k] : qmax; }
+  if (Pq < 2 || Pq > qmin || (r & 1)) return TP_EUNSUPPORTED;
+  const void* fn = kernel_ptr(pl.rm, 1);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  if (Pq > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaGetLastError();
+  int Pr = nsm / Pq;
+  if (Pr > R) Pr = R;
+  for (; Pr >= 1; --Pr) {
+    const int P = Pr * Pq, wmax = (R + Pr - 1) / Pr, ldw = pad4(wmax), ncolmax = (qmax + P - 1) / P;
+    int sumnb = 0, nbmax = 0;
+    for (int k = 0; k < d; ++k) {
+      const int nb = (q[k] + Pq - 1) / Pq;
+      sumnb += (nb + 3) & ~3;
+      nbmax = nb > nbmax ? nb : nbmax;
+    }
+    sumnb += 8;   // slack rows: tile lanes past the last row stay in bounds
+    const int mtr = (r + 7) / 8, nG = mtr * (mtr + 1) / 2;
+    int chunk = (r * wmax + ((nG + Pr - 1) / Pr) * 64 + Pq - 1) / Pq;
+    chunk += chunk & 1;
+    const size_t smem = cl_smem_doubles(d, r, wmax, ldw, sumnb, nbmax, ncolmax, Pr, Pq, chunk, qmax) * sizeof(double);
+    if (smem > (size_t)smem_optin) continue;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = Pq; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(P); cfg.blockDim = dim3(ALS_NT); cfg.dynamicSmemBytes = smem; cfg.attrs = at; cfg.numAttrs = 1;
+    int nclu = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclu, fn, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
+    if (nclu < Pr) continue;
+    AlsArgs& a = pl.a;
+    a.Pq = Pq; a.ldw = ldw; a.chunk = chunk; a.nbmax = nbmax; a.sumqs = sumnb;
+    a.wmax = wmax; a.ncolmax = ncolmax; a.P = P;
+    int qo = 0;
+    for (int k = 0; k < d; ++k) { a.qoffc[k] = qo; qo += (((q[k] + Pq - 1) / Pq + 3) & ~3) * ldw; }
+    pl.P = P; pl.Pr = Pr; pl.smem = smem; pl.variant = 1;
+    pl.ydoubles = (size_t)P * Pr * ncolmax * r;
+    pl.ws_total = ws_total_for(d, q, r, P, pl.ydoubles, pl.ws_inner);
+    return TP_OK;
+  }
+  return TP_EUNSUPPORTED;
 }
 
 static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
@@ -865,9 +1420,23 @@ static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
   pl.P = P;
   pl.smem = smem;
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
-  pl.ws_total = align_up(sizeof(double) * (size_t)d * r * r) + align_up(sizeof(double) * (size_t)P * P * a.ncolmax * r) +
-                align_up(sizeof(double) * (size_t)P) + align_up(sizeof(double)) + pl.ws_inner + 256 +
-                align_up(sizeof(double) * 2 * (size_t)d * r * pad4(r)) + align_up(sizeof(double) * (size_t)oup);
+  pl.Pr = P;
+  pl.variant = 0;
+  pl.ydoubles = (size_t)P * P * a.ncolmax * r;
+  pl.ws_total = ws_total_for(d, q, r, P, pl.ydoubles, pl.ws_inner);
+  (void)oup;
+  // large truncations: the cluster variant (fewer bytes per CTA per mode update)
+  const bool want = g_variant == 2 || (g_variant == 0 && grid <= 0 && P >= 32 && g_cluster >= 0);
+  if (want) {
+    AlsPlan cp = pl;
+    const int sizes[3] = {8, 4, 2};
+    for (int t = 0; t < 3; ++t) {
+      const int Pq = g_cluster > 0 ? g_cluster : sizes[t];
+      if (plan_cluster(d, q, R, r, Pq, smem_optin, nsm, cp) == TP_OK) { pl = cp; return TP_OK; }
+      if (g_cluster > 0) break;
+    }
+    if (g_variant == 2) return TP_EUNSUPPORTED;
+  }
   return TP_OK;
 }
 
@@ -887,6 +1456,8 @@ void tp_debug_set_als_profile(long long* dev_ptr) { g_prof = dev_ptr; }
 void tp_debug_set_als_skip(int mask) { g_skip = mask; }
 // debug hook: Newton-Schulz iteration cap (0 = always the exact sweep inversion)
 void tp_debug_set_als_ns(int n) { g_ns_max = n; }
+// debug hook: kernel variant (0 auto, 1 als_persistent, 2 als_cluster) and cluster size (0 auto, -1 never)
+void tp_debug_set_als_variant(int variant, int cluster) { g_variant = variant; g_cluster = cluster; }
 
 size_t tp_cp_als_ws_bytes(int d, const int* q, int R, int r, int grid) {
   AlsPlan pl;
@@ -906,7 +1477,7 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
   AlsArgs& a = pl.a;
   Carver cv(ws, ws_bytes);
   a.G = cv.take<double>((size_t)d * r * r);
-  a.Y = cv.take<double>((size_t)pl.P * pl.P * a.ncolmax * r);
+  a.Y = cv.take<double>(pl.ydoubles);
   a.ovl = cv.take<double>(pl.P);
   double* nsq = cv.take<double>(1);
   double* part = cv.take<double>(pl.ws_inner / sizeof(double));
@@ -932,9 +1503,22 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
     st = launch_inner(d, q, R, V, R, V, 1, nsq, part, s);   // ||V||^2 (cp.py:186-188)
     if (st != TP_OK) return st;
   }
-  const void* fn = kernel_ptr(pl.rm);
+  const void* fn = kernel_ptr(pl.rm, pl.variant);
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return cuda_status(e);
+  if (pl.variant == 1) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = a.Pq; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.gridDim = dim3(pl.P); cfg.blockDim = dim3(ALS_NT); cfg.dynamicSmemBytes = pl.smem; cfg.stream = s;
+    cfg.attrs = at; cfg.numAttrs = 2;
+    void* args[] = {&a};
+    e = cudaLaunchKernelExC(&cfg, fn, args);
+    return cuda_status(e);
+  }
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ALS_NT, pl.smem);
   if (e != cudaSuccess) return cuda_status(e);

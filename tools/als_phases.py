@@ -9,7 +9,7 @@ sys.path.insert(0, ".")
 from paper_1803_10270_b200 import _lib, cp, workloads  # noqa: E402
 
 NAMES = ["(loop head)", "A:gram_share", "A:had+Y", "barrier1", "B:reduce", "B:wait Y slices", "B:write U",
-         "barrier2", "B:wait G/X", "B:solve (NS/exact)", "A:stage_u", "A:cross"]
+         "barrier2", "B:wait G/X", "B:solve (NS/exact)", "A:stage_u", "A:cross", "A:exchange", "-", "-", "-"]
 
 
 def run(grid, Q=256, R=512, r=32):
@@ -30,17 +30,21 @@ def run(grid, Q=256, R=512, r=32):
     torch.cuda.synchronize()
     L.tp_debug_set_als_profile(None)
     p = prof.cpu().numpy() / 120.0
-    tot = p[:12].sum()
+    tot = p[:16].sum()
     print(f"grid={grid} Q={Q} R={R} r={r}: cycles per mode update (CTA 0): total {tot:.0f}")
-    for i in [0, 10, 11, 1, 2, 3, 8, 5, 4, 9, 6, 7]:
+    for i in [0, 10, 11, 12, 1, 2, 3, 8, 5, 4, 9, 6, 7]:
         print(f"   {NAMES[i]:22s} {p[i]:9.0f}  ({100*p[i]/tot:4.1f}%)")
     raw = prof.cpu().numpy()
 
 
 if __name__ == "__main__":
+    import os
     Lb = _lib.lib()
     Lb.tp_debug_set_als_ns.argtypes = [ctypes.c_int]
-    for ns in (6, 0):
+    Lb.tp_debug_set_als_variant.argtypes = [ctypes.c_int, ctypes.c_int]
+    var = [int(x) for x in os.environ.get("ALS_VARIANT", "0,0").split(",")]
+    Lb.tp_debug_set_als_variant(var[0], var[1])
+    for ns in (6,):
         print(f"--- Newton-Schulz cap {ns}")
         Lb.tp_debug_set_als_ns(ns)
         for g in [int(x) for x in sys.argv[1:]] or [0]:
