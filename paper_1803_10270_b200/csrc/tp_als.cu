@@ -60,7 +60,8 @@ struct AlsArgs {
   int reg_mode;
   double tol, stall;
   int need_resid;
-  long long* prof;     // optional per-phase clock64 totals (CTA 0), debug hook
+  long long* prof;     // optional per-phase clock64 totals (CTA prof_cta), debug hook
+  int prof_cta;
   unsigned int* bar_ctr;   // grid-barrier arrival counter (zeroed before launch)
   int dbg_skip;            // debug: bit mask of phases to skip (timing by subtraction)
   double* Xprev;           // [d][r][pad4(r)] last inverse per mode (warm start for Newton-Schulz)
@@ -803,7 +804,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   }
   if (status && tid == 0 && p == 0) atomicOr(a.info, 1);
   if (p == 0 && tid == 0) a.info[1] = done;
-  if (a.prof && p == 0 && tid == 0) {
+  if (a.prof && p == a.prof_cta && tid == 0) {
     for (int q = 0; q < 12; ++q) a.prof[q] += prof_acc[q];
     if (prof_sink == 12345.0) a.prof[11] += 1;
   }
@@ -943,25 +944,32 @@ __device__ void cl_partials(const AlsArgs& a, const Smem& sm, int k, int w, int 
   int ns = (ntc + ngroups - 1) / ngroups;
   if (ns > 4) { ns = 4; ngroups = (ntc + 3) / 4; }
   const int nCi = mtr * ngroups, nGi = cid < nG ? (nG - 1 - cid) / Pr + 1 : 0;
-  for (int it = warp; it < nCi + nGi; it += ALS_NW) {
-    if (it < nCi) {
-      const int m = it / ngroups, n0 = (it - m * ngroups) * ns;
-      if (ns == 4) cl_c_item<4>(a, sm, vs, w, nb, m, n0);
-      else if (ns == 3) cl_c_item<3>(a, sm, vs, w, nb, m, n0);
-      else if (ns == 2) cl_c_item<2>(a, sm, vs, w, nb, m, n0);
-      else cl_c_item<1>(a, sm, vs, w, nb, m, n0);
-    } else {
-      const int gi = it - nCi;
-      int g = cid + gi * Pr, ti = 0;
-      while (g >= mtr - ti) { g -= mtr - ti; ++ti; }
-      const int tj = ti + g;
-      const uint32_t us32 = smem_u32(sm.Us);
-      const uint32_t b[1] = {us32 + 8u * (uint32_t)(tj * 8 + (lane >> 2))}, bst[1] = {8u * (uint32_t)rh};
-      double acc[1][2];
-      cl_chains<1>(us32 + 8u * (uint32_t)(ti * 8 + (lane >> 2)), 8u * (uint32_t)rh, b, bst, (nb + 3) / 4, acc);
-      double* t = sm.mine + (size_t)r * w + (size_t)gi * 64;
-      t[2 * lane] = acc[0][0];
-      t[2 * lane + 1] = acc[0][1];
+  for (int it = warp; it < nCi; it += ALS_NW) {
+    const int m = it / ngroups, n0 = (it - m * ngroups) * ns;
+    if (ns == 4) cl_c_item<4>(a, sm, vs, w, nb, m, n0);
+    else if (ns == 3) cl_c_item<3>(a, sm, vs, w, nb, m, n0);
+    else if (ns == 2) cl_c_item<2>(a, sm, vs, w, nb, m, n0);
+    else cl_c_item<1>(a, sm, vs, w, nb, m, n0);
+  }
+  // Gram tiles of this cluster: K split over the warps, partials summed in fixed order
+  const int ksteps = (nb + 3) / 4, kper = (ksteps + ALS_NW - 1) / ALS_NW;
+  const int kb = min(ksteps, warp * kper), ke = min(ksteps, kb + kper);
+  for (int gi = 0; gi < nGi; ++gi) {
+    int g = cid + gi * Pr, ti = 0;
+    while (g >= mtr - ti) { g -= mtr - ti; ++ti; }
+    const int tj = ti + g;
+    const uint32_t us32 = smem_u32(sm.Us) + 8u * (uint32_t)(4 * kb * rh);
+    const uint32_t bb[1] = {us32 + 8u * (uint32_t)(tj * 8 + (lane >> 2))}, bst[1] = {8u * (uint32_t)rh};
+    double acc[1][2];
+    cl_chains<1>(us32 + 8u * (uint32_t)(ti * 8 + (lane >> 2)), 8u * (uint32_t)rh, bb, bst, ke - kb, acc);
+    __syncthreads();
+    sm.part[warp * 64 + 2 * lane] = acc[0][0];
+    sm.part[warp * 64 + 2 * lane + 1] = acc[0][1];
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      double v = 0.0;
+      for (int q = 0; q < ALS_NW; ++q) v += sm.part[q * 64 + threadIdx.x];
+      sm.mine[(size_t)r * w + (size_t)gi * 64 + threadIdx.x] = v;
     }
   }
   __syncthreads();
@@ -975,8 +983,9 @@ __device__ void cl_partials(const AlsArgs& a, const Smem& sm, int k, int w, int 
 // global G (consumed after the next grid barrier).  Completion is tracked by
 // mbarriers sm.bar[2] (inbox) and sm.bar[3] (Cs); buffers are reused only after
 // grid barriers, so no cluster barrier is needed.
+template <int RM>
 __device__ void cl_exchange(const AlsArgs& a, const Smem& sm, cg::cluster_group& cl, int k, int w, int cid, int Pr,
-                            uint32_t& ph) {
+                            uint32_t& ph, int& rows_mode, int rows_sweep) {
   const int r = a.r, rr = r * r, Pq = a.Pq, chunk = a.chunk, b = (int)cl.block_rank(), tid = threadIdx.x;
   const int mtr = (r + 7) / 8, nG = mtr * (mtr + 1) / 2, nGi = cid < nG ? (nG - 1 - cid) / Pr + 1 : 0;
   const int rw = r * w, L = rw + nGi * 64;
@@ -989,10 +998,14 @@ __device__ void cl_exchange(const AlsArgs& a, const Smem& sm, cg::cluster_group&
     for (int q = 0; q < Pq; ++q) if (q != b) cs_bytes += 8u * (uint32_t)clen(q);
     mbar_arrive_expect_tx(sm.bar + 2, 8u * (uint32_t)((Pq - 1) * chunk));
     mbar_arrive_expect_tx(sm.bar + 3, cs_bytes);
-    fence_proxy_async();
+    fence_proxy_async_cluster();
     const uint32_t inbox = smem_u32(sm.inbox) + 8u * (uint32_t)(b * chunk);
     for (int q = 0; q < Pq; ++q)
       if (q != b) bulk_s2cluster(mapa_u32(inbox, q), sm.mine + (size_t)q * chunk, 8u * (uint32_t)chunk, mapa_u32(bar_in, q));
+  }
+  if (rows_mode >= 0) {   // warm-start rows of the previous solve, while the peers' chunks land
+    ns_rows<RM>(a, sm, rows_mode, rows_sweep);
+    rows_mode = -1;
   }
   mbar_wait(sm.bar + 2, ph);
   double* Gk = a.G + (size_t)k * rr;
@@ -1016,7 +1029,7 @@ __device__ void cl_exchange(const AlsArgs& a, const Smem& sm, cg::cluster_group&
   __syncthreads();
   const int my = clen(b);
   if (tid == 0 && my > 0) {
-    fence_proxy_async();
+    fence_proxy_async_cluster();
     const uint32_t dst = smem_u32(Ck + (size_t)b * chunk);
     for (int q = 0; q < Pq; ++q)
       if (q != b) bulk_s2cluster(mapa_u32(dst, q), Ck + (size_t)b * chunk, 8u * (uint32_t)my, mapa_u32(bar_cs, q));
@@ -1099,9 +1112,9 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
   const int c0 = (int)((long long)R * cid / Pr), c1 = (int)((long long)R * (cid + 1) / Pr), w = c1 - c0;
   const int w4 = (w + 3) / 4 * 4;
   int status = 0;
-  uint32_t bphase = 0, gphase = 0, xphase = 0;
+  uint32_t bphase = 0, gphase = 0, xphase = 0, xpf = 0;
   if (tid == 0) {
-    for (int q = 0; q < 4; ++q) mbar_init(sm.bar + q, 1);
+    for (int q = 0; q < 5; ++q) mbar_init(sm.bar + q, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int k = 0; k < a.d; ++k)
@@ -1130,7 +1143,8 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
     const int Qk = a.q[k], qb0 = Qk * b / Pq, nb = Qk * (b + 1) / Pq - qb0;
     cl_stage_u(a, sm, k, qb0, nb, bphase, true);
     cl_partials<RM>(a, sm, k, w, nb, cid, Pr);
-    cl_exchange(a, sm, cl, k, w, cid, Pr, xphase);
+    int none = -1;
+    cl_exchange<RM>(a, sm, cl, k, w, cid, Pr, xphase, none, 0);
   }
   grid_barrier(a.bar_ctr, epoch);
   for (int e = tid; e < a.d * rr; e += ALS_NT) sm.Gs[e] = __ldcg(a.G + e);
@@ -1152,12 +1166,19 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
         PROF(10);
         cl_partials<RM>(a, sm, pending, w, nb, cid, Pr);
         PROF(11);
-        cl_exchange(a, sm, cl, pending, w, cid, Pr, xphase);
+        cl_exchange<RM>(a, sm, cl, pending, w, cid, Pr, xphase, rows_mode, rows_sweep);
         PROF(12);
       }
       if (rows_mode >= 0) {
         ns_rows<RM>(a, sm, rows_mode, rows_sweep);
         rows_mode = -1;
+      }
+      // prefetch this mode's warm start (X0 is free once the rows are formed)
+      const bool warm_ns = sweep > 0 && a.ns_max > 0;
+      if (warm_ns && tid == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(sm.bar + 4, (uint32_t)(r * rh) * 8u);
+        bulk_g2s(sm.X0, a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh, (uint32_t)(r * rh) * 8u, sm.bar + 4);
       }
       PROF(1);
       const int Qj = a.q[j];
@@ -1170,21 +1191,19 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
       const int ncol = s1 - s0, E = ncol * r;
       const int nbk = a.ncolmax * r;
       double* ystage = sm.Us;
-      const bool warm_ns = sweep > 0 && a.ns_max > 0;
       if (bulk) {
         if (tid == 0) {
           const uint32_t ybytes = E > 0 ? (uint32_t)(Pr * nbk) * 8u : 0u;
-          const uint32_t xbytes = warm_ns ? (uint32_t)(r * rh) * 8u : 0u;
           const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
           fence_proxy_async();
-          mbar_arrive_expect_tx(sm.bar + 1, xbytes + gbytes);
+          mbar_arrive_expect_tx(sm.bar + 1, gbytes);
           if (gbytes) bulk_g2s(sm.Gs + (size_t)pending * rr, a.G + (size_t)pending * rr, gbytes, sm.bar + 1);
-          if (xbytes) bulk_g2s(sm.X0, a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh, xbytes, sm.bar + 1);
           mbar_arrive_expect_tx(sm.bar, ybytes);
           if (ybytes) bulk_g2s(ystage, a.Y + (size_t)p * Pr * nbk, ybytes, sm.bar);
         }
         mbar_wait(sm.bar + 1, gphase);
         gphase ^= 1u;
+        if (warm_ns) { mbar_wait(sm.bar + 4, xpf); xpf ^= 1u; }
         if (warm_ns) build_a<RM>(a, sm, j);   // overlaps the slice fetch
         PROF(8);
         mbar_wait(sm.bar, bphase);
@@ -1203,9 +1222,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
       } else {
         if (pending >= 0)
           for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * rr + e] = __ldcg(a.G + (size_t)pending * rr + e);
-        if (warm_ns)
-          for (int e = tid; e < r * rh; e += ALS_NT)
-            sm.X0[e] = __ldcg(a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh + e);
+        if (warm_ns) { mbar_wait(sm.bar + 4, xpf); xpf ^= 1u; }
         for (int o = tid; o < E; o += ALS_NT) {
           double s0a = 0.0, s1a = 0.0;
           int q = 0;
@@ -1248,7 +1265,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
       const int Qk = a.q[pending], qb0 = Qk * b / Pq, nb = Qk * (b + 1) / Pq - qb0;
       cl_stage_u(a, sm, pending, qb0, nb, bphase, false);
       cl_partials<RM>(a, sm, pending, w, nb, cid, Pr);
-      cl_exchange(a, sm, cl, pending, w, cid, Pr, xphase);
+      cl_exchange<RM>(a, sm, cl, pending, w, cid, Pr, xphase, rows_mode, rows_sweep);
       double ov = 0.0;
       if (b == 0)
         for (int e = tid; e < r * w; e += ALS_NT) {
@@ -1288,7 +1305,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
   }
   if (status && tid == 0 && p == 0) atomicOr(a.info, 1);
   if (p == 0 && tid == 0) a.info[1] = done;
-  if (a.prof && p == 0 && tid == 0) {
+  if (a.prof && p == a.prof_cta && tid == 0) {
     for (int q = 0; q < 16; ++q) a.prof[q] += prof_acc[q];
     if (prof_sink == 12345.0) a.prof[11] += 1;
   }
@@ -1445,6 +1462,7 @@ static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
 using namespace tp;
 
 static long long* g_prof = nullptr;
+static int g_prof_cta = 0;
 static int g_skip = 0;
 static int g_ns_max = 6;
 
@@ -1452,6 +1470,7 @@ extern "C" {
 
 // debug hook (not part of the public header): per-phase clock64 totals of CTA 0
 void tp_debug_set_als_profile(long long* dev_ptr) { g_prof = dev_ptr; }
+void tp_debug_set_als_profile_cta(int cta) { g_prof_cta = cta; }
 // debug hook: skip phases (results are wrong) to time them by subtraction
 void tp_debug_set_als_skip(int mask) { g_skip = mask; }
 // debug hook: Newton-Schulz iteration cap (0 = always the exact sweep inversion)
@@ -1494,6 +1513,7 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
   a.need_resid = (trace != nullptr) || (tol > 0.0) || (stall > -INFINITY);
   a.norm_sq = nsq;
   a.prof = g_prof;
+  a.prof_cta = g_prof_cta < 0 ? pl.P + g_prof_cta : g_prof_cta;
   a.dbg_skip = g_skip;
   cudaError_t e = cudaMemsetAsync(info, 0, 2 * sizeof(int), s);
   if (e != cudaSuccess) return cuda_status(e);

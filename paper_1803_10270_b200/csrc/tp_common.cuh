@@ -105,6 +105,10 @@ __device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, ui
 }
 
 // order this thread's prior generic-proxy accesses with later async-proxy (bulk copy) ones
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// same, for copies that write peer CTAs' shared memory
+__device__ __forceinline__ void fence_proxy_async_cluster() {
+  asm volatile("fence.proxy.async.shared::cluster;\n" ::: "memory");
+}
 
 }  // namespace tp

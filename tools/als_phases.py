@@ -44,6 +44,8 @@ if __name__ == "__main__":
     Lb.tp_debug_set_als_variant.argtypes = [ctypes.c_int, ctypes.c_int]
     var = [int(x) for x in os.environ.get("ALS_VARIANT", "0,0").split(",")]
     Lb.tp_debug_set_als_variant(var[0], var[1])
+    Lb.tp_debug_set_als_profile_cta.argtypes = [ctypes.c_int]
+    Lb.tp_debug_set_als_profile_cta(int(os.environ.get("ALS_PROF_CTA", "0")))
     for ns in (6,):
         print(f"--- Newton-Schulz cap {ns}")
         Lb.tp_debug_set_als_ns(ns)
