@@ -59,7 +59,8 @@ static int build_tree(Tree& T, int lo, int hi, int par, int dep) {
 constexpr int JAC_NT = 256;
 
 __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int first, int per, const double* Ain,
-                                                             double* Vout, double* wout, int max_sweeps) {
+                                                             double* Vout, double* wout, int max_sweeps, double tol,
+                                                             int* sweeps_out) {
   extern __shared__ double js[];
   const int kp = k + (k & 1), ld = kp + 1;
   double* a = js;
@@ -84,7 +85,9 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int 
   const int my_pair = tid % half, stride = JAC_NT / half, j0 = tid / half;
   const bool active = j0 < stride && tid < half * stride;
   int* flag = reinterpret_cast<int*>(red);
+  int sw = 0;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    sw = sweep + 1;
     if (tid == 0) flag[0] = 0;
     __syncthreads();
     for (int round = 0; round < kp - 1; ++round) {
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int 
         // threshold Jacobi: rotate only if a_pq is not negligible against the
         // diagonal (relative accuracy criterion) -- a sweep without rotations
         // means convergence
-        if (fabs(apq) > 1e-300 && fabs(apq) > 1e-16 * sqrt(fabs(app) * fabs(aqq))) {
+        if (fabs(apq) > 1e-300 && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
           const double tau = (aqq - app) / (2.0 * apq);
           const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + t * t);
@@ -138,6 +141,7 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int 
     if (flag[0] == 0) break;
     __syncthreads();
   }
+  if (sweeps_out && tid == 0) atomicAdd(sweeps_out, sw);
   // sort descending (ties by index), write eigenvalues and eigenvector columns
   double* Vo = Vout + base * k * k;
   double* wo = wout + base * k;
@@ -315,7 +319,16 @@ static void plan_ht(int d, int Q, int k, int nb, int r_max, HtPlan& P) {
 
 using namespace tp;
 
+static int g_jac_sweeps = 30;
+static double g_jac_tol = 1e-16;
+static int* g_jac_count = nullptr;
+
 extern "C" {
+
+// debug hook: Jacobi sweep cap, rotation threshold, optional device counter of sweeps done
+void tp_debug_set_jacobi(int max_sweeps, double tol, int* count) {
+  g_jac_sweeps = max_sweeps; g_jac_tol = tol; g_jac_count = count;
+}
 
 size_t tp_ht_truncate_ws_bytes(int d, int Q, int k, int nb) {
   if (d < 2 || d > 16 || Q < 1 || k < 1 || k > 64 || nb < 1) return 0;
@@ -523,7 +536,7 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
       transpose12_kernel<<<grid, 256, 0, st>>>(k, tr.kt, doffs + tr.tab, transfers, big3, k3);
       e = cudaGetLastError();
     } else if (id == -1) {
-      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Mf, Vm, lam, 30);
+      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Mf, Vm, lam, g_jac_sweeps, g_jac_tol, g_jac_count);
       e = cudaGetLastError();
     } else if (id == -2) {
       set_root_env<<<(nb + 127) / 128, 128, 0, st>>>(k, nn, nb, Gh);
@@ -532,7 +545,7 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
       form_g_kernel<<<nonroot, 256, fsm, st>>>(k, nn, Vm, lam, Gh, Gt);
       e = cudaGetLastError();
     } else if (id == -4) {
-      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Gt, Wg, sig, 30);
+      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Gt, Wg, sig, g_jac_sweeps, g_jac_tol, g_jac_count);
       e = cudaGetLastError();
     } else if (id == -5) {
       keep_rule_kernel<<<(nonroot + 127) / 128, 128, 0, st>>>(k, nn, nb, d, eps, r_max, sig, Mf, keep, disc);
