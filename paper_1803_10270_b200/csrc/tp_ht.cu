@@ -60,7 +60,7 @@ constexpr int JAC_NT = 256;
 
 __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int first, int per, const double* Ain,
                                                              double* Vout, double* wout, int max_sweeps, double tol,
-                                                             int* sweeps_out) {
+                                                             int* sweeps_out, const int* skip) {
   extern __shared__ double js[];
   const int kp = k + (k & 1), ld = kp + 1;
   double* a = js;
@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int 
   double* red = cs + 2 * kp;                  // [JAC_NT]
   const int z = blockIdx.x;
   const size_t base = (size_t)(z / per) * nn + first + z % per;
+  if (skip && skip[base]) return;   // factor already available (Cholesky)
   const double* in = Ain + base * k * k;
   const int tid = threadIdx.x;
   for (int e = tid; e < kp * kp; e += JAC_NT) {
@@ -164,9 +165,63 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int 
   }
 }
 
-// G_t = diag(sqrt(l)) V^T Gh V diag(sqrt(l)) for every non-root node (one CTA each)
+// Frame-Gram square-root factor by Cholesky, M_t = L L^T (one CTA per non-root
+// node, right-looking, 64 dependent steps instead of ~8 Jacobi sweeps).  In the
+// Gramian gauge only a factor F with F F^T = M_t enters: with F = L instead of
+// V diag(sqrt(l)) (ht.py:347-349) G_t = L^T Gh L has the same eigenvalues and
+// S_t = L^-T W_keep is the same basis, so the truncation is unchanged.  Nodes whose
+// Gram is numerically singular (a pivot <= 1e-12 max diag) keep the eigh path of
+// the reference (pseudo-inverse square root): ok[node] = 0.
+__global__ void __launch_bounds__(256) chol_frame_kernel(int k, int nn, const double* Mf, double* Lout, int* ok) {
+  extern __shared__ double cs_[];
+  const int z = blockIdx.x, per = nn - 1, ld = k + 1, tid = threadIdx.x;
+  const size_t base = (size_t)(z / per) * nn + 1 + z % per;
+  double* A = cs_;
+  double* dmax = A + (size_t)k * ld;
+  const double* M = Mf + base * k * k;
+  for (int e = tid; e < k * k; e += 256) {
+    const int i = e / k, j = e - i * k;
+    A[i * ld + j] = 0.5 * (M[e] + M[j * k + i]);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int i = 0; i < k; ++i) m = fmax(m, A[i * ld + i]);
+    dmax[0] = m;
+    dmax[1] = 1.0;   // ok
+  }
+  __syncthreads();
+  const double tol = 1e-12 * dmax[0];
+  for (int j = 0; j < k; ++j) {
+    const double piv = A[j * ld + j];
+    if (!(piv > tol)) { if (tid == 0) dmax[1] = 0.0; break; }   // uniform: every thread reads the same piv
+    const double dj = sqrt(piv), inv = 1.0 / dj;
+    __syncthreads();
+    for (int i = j + 1 + tid; i < k; i += 256) A[i * ld + j] *= inv;
+    if (tid == 0) A[j * ld + j] = dj;
+    __syncthreads();
+    const int n = k - 1 - j;   // trailing lower triangle (i >= c > j)
+    for (int e = tid; e < n * n; e += 256) {
+      const int i = j + 1 + e / n, c = j + 1 + e % n;
+      if (c <= i) A[i * ld + c] = fma(-A[i * ld + j], A[c * ld + j], A[i * ld + c]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  const int good = dmax[1] != 0.0;
+  if (tid == 0) ok[base] = good;
+  if (!good) return;
+  double* L = Lout + base * k * k;
+  for (int e = tid; e < k * k; e += 256) {
+    const int i = e / k, c = e - i * k;
+    L[e] = (c <= i) ? A[i * ld + c] : 0.0;
+  }
+}
+
+// G_t = diag(sqrt(l)) V^T Gh V diag(sqrt(l)) for every non-root node (one CTA each);
+// nodes with a Cholesky factor (ok) use G_t = L^T Gh L
 __global__ void __launch_bounds__(256) form_g_kernel(int k, int nn, const double* Vm, const double* lam,
-                                                     const double* Gh, double* G) {
+                                                     const double* Gh, double* G, const int* ok) {
   extern __shared__ double fs[];
   const int z = blockIdx.x, per = nn - 1;
   const size_t base = (size_t)(z / per) * nn + 1 + z % per;
@@ -191,6 +246,7 @@ __global__ void __launch_bounds__(256) form_g_kernel(int k, int nn, const double
     const int m = e / k, n = e % k;
     double acc = 0.0;
     for (int j = 0; j < k; ++j) acc = fma(P[m * ld + j], V[j * ld + n], acc);
+    if (ok[base]) { G[base * k * k + e] = acc; continue; }
     const double sm = sqrt(fmax(lam[base * k + m], 0.0)), sn = sqrt(fmax(lam[base * k + n], 0.0));
     G[base * k * k + e] = acc * sm * sn;
   }
@@ -232,11 +288,37 @@ __global__ void finish_kernel(int k, int nn, int nb, const double* Mf, const int
 // S_t = V diag(l^+1/2) W[:, :keep] (k x ro, zero columns beyond keep); T_t = S_t^T M_t (ro x k)
 __global__ void __launch_bounds__(256) form_st_kernel(int k, int ro, int nn, const double* Vm, const double* lam,
                                                       const double* Wg, const int* keep, const double* Mf,
-                                                      double* S, double* T) {
+                                                      double* S, double* T, const int* ok) {
   extern __shared__ double ss[];
   const int z = blockIdx.x, per = nn - 1;
   const size_t base = (size_t)(z / per) * nn + 1 + z % per;
   const int kp = keep[base];
+  if (ok[base]) {
+    // Cholesky factor: S = L^-T W_keep (back substitution, 16 threads per column),
+    // T = S^T M = W_keep^T L^T
+    const double* L = Vm + base * k * k;
+    const double* W = Wg + base * k * k;
+    double* Sl = ss;   // [k][ro]
+    const int c = threadIdx.x >> 4, part = threadIdx.x & 15;
+    for (int i = k - 1; i >= 0; --i) {
+      double acc = 0.0;
+      if (c < ro)
+        for (int m = i + 1 + part; m < k; m += 16) acc = fma(L[m * k + i], Sl[m * ro + c], acc);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (c < ro && part == 0) Sl[i * ro + c] = (c < kp) ? (W[i * k + c] - acc) / L[i * k + i] : 0.0;
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < k * ro; e += 256) S[base * k * ro + e] = Sl[e];
+    for (int e = threadIdx.x; e < ro * k; e += 256) {
+      const int cc = e / k, a2 = e % k;
+      double acc = 0.0;
+      if (cc < kp)
+        for (int i = 0; i <= a2; ++i) acc = fma(W[i * k + cc], L[a2 * k + i], acc);
+      T[base * ro * k + e] = acc;
+    }
+    return;
+  }
   double* mu = ss;               // [k]
   double* Sl = mu + k;           // [k][ro]
   const double lmax = fmax(lam[base * k], 0.0);
@@ -312,7 +394,7 @@ static void plan_ht(int d, int Q, int k, int nb, int r_max, HtPlan& P) {
   const size_t nn = P.T.n, kk = (size_t)k * k;
   P.off_n = (size_t)nb * (P.T.nleaf + P.T.nint) * 3 * 8 * 8;   // generous offset-table space
   P.total = align_up(8 * nb * nn * kk) * 5 + align_up(8 * nb * nn * k) * 2 + align_up(8 * nb * nn * (size_t)k * P.ro) * 2 +
-            align_up(4 * nb * nn) + align_up(8 * nb * nn) + 3 * align_up(8 * P.big) + align_up(8 * P.off_n) + 256;
+            2 * align_up(4 * nb * nn) + align_up(8 * nb * nn) + 3 * align_up(8 * P.big) + align_up(8 * P.off_n) + 256;
 }
 
 }  // namespace tp
@@ -322,6 +404,7 @@ using namespace tp;
 static int g_jac_sweeps = 30;
 static double g_jac_tol = 1e-16;
 static int* g_jac_count = nullptr;
+static int g_chol = 1;   // debug hook: 0 = eigh of every frame Gram (reference path)
 
 extern "C" {
 
@@ -329,6 +412,8 @@ extern "C" {
 void tp_debug_set_jacobi(int max_sweeps, double tol, int* count) {
   g_jac_sweeps = max_sweeps; g_jac_tol = tol; g_jac_count = count;
 }
+// debug hook: frame-Gram factor by Cholesky (1, default) or eigh (0)
+void tp_debug_set_ht_chol(int on) { g_chol = on; }
 
 size_t tp_ht_truncate_ws_bytes(int d, int Q, int k, int nb) {
   if (d < 2 || d > 16 || Q < 1 || k < 1 || k > 64 || nb < 1) return 0;
@@ -364,6 +449,7 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
   double* S = cv.take<double>((size_t)nb * nn * k * ro);
   double* Tm = cv.take<double>((size_t)nb * nn * ro * k);
   int* keep = cv.take<int>((size_t)nb * nn);
+  int* cholok = cv.take<int>((size_t)nb * nn);
   double* disc = cv.take<double>((size_t)nb * nn);
   double* big1 = cv.take<double>(P0.big);
   double* big2 = cv.take<double>(P0.big);
@@ -524,6 +610,8 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
   const size_t fsm = sizeof(double) * 3 * (size_t)k * (k + 1);
   cudaFuncSetAttribute(form_g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
   const size_t ssm = sizeof(double) * ((size_t)k + (size_t)k * ro);
+  const size_t csm = sizeof(double) * ((size_t)k * (k + 1) + 2);
+  cudaFuncSetAttribute(chol_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   const int nonroot = nb * (nn - 1);
   for (int id : order) {
     if (id >= 0) {
@@ -536,22 +624,30 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
       transpose12_kernel<<<grid, 256, 0, st>>>(k, tr.kt, doffs + tr.tab, transfers, big3, k3);
       e = cudaGetLastError();
     } else if (id == -1) {
-      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Mf, Vm, lam, g_jac_sweeps, g_jac_tol, g_jac_count);
+      if (g_chol) {
+        chol_frame_kernel<<<nonroot, 256, csm, st>>>(k, nn, Mf, Vm, cholok);
+      } else {
+        e = cudaMemsetAsync(cholok, 0, sizeof(int) * (size_t)nb * nn, st);
+        if (e != cudaSuccess) return cuda_status(e);
+      }
+      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Mf, Vm, lam, g_jac_sweeps, g_jac_tol, g_jac_count,
+                                                        cholok);
       e = cudaGetLastError();
     } else if (id == -2) {
       set_root_env<<<(nb + 127) / 128, 128, 0, st>>>(k, nn, nb, Gh);
       e = cudaGetLastError();
     } else if (id == -3) {
-      form_g_kernel<<<nonroot, 256, fsm, st>>>(k, nn, Vm, lam, Gh, Gt);
+      form_g_kernel<<<nonroot, 256, fsm, st>>>(k, nn, Vm, lam, Gh, Gt, cholok);
       e = cudaGetLastError();
     } else if (id == -4) {
-      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Gt, Wg, sig, g_jac_sweeps, g_jac_tol, g_jac_count);
+      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Gt, Wg, sig, g_jac_sweeps, g_jac_tol, g_jac_count,
+                                                        nullptr);
       e = cudaGetLastError();
     } else if (id == -5) {
       keep_rule_kernel<<<(nonroot + 127) / 128, 128, 0, st>>>(k, nn, nb, d, eps, r_max, sig, Mf, keep, disc);
       e = cudaGetLastError();
     } else if (id == -6) {
-      form_st_kernel<<<nonroot, 256, ssm, st>>>(k, ro, nn, Vm, lam, Wg, keep, Mf, S, Tm);
+      form_st_kernel<<<nonroot, 256, ssm, st>>>(k, ro, nn, Vm, lam, Wg, keep, Mf, S, Tm, cholok);
       e = cudaGetLastError();
     } else if (id == -7) {
       finish_kernel<<<(nb + 127) / 128, 128, 0, st>>>(k, nn, nb, Mf, keep, disc, est, norms, out_ranks);

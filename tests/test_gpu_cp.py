@@ -177,3 +177,39 @@ def test_rank_reduce_strips_noise():
     assert red.rank <= 2
     rel = metrics.cp_rel_diff(noisy.to_numpy(), red.to_numpy())
     assert rel < 1e-7
+
+
+@pytest.fixture
+def als_variant():
+    """Force the ALS kernel variant through the library's debug hook, restore auto after."""
+    import ctypes
+    from paper_1803_10270_b200 import _lib
+    L = _lib.lib()
+    L.tp_debug_set_als_variant.argtypes = [ctypes.c_int, ctypes.c_int]
+
+    def set_(variant, cluster=0):
+        L.tp_debug_set_als_variant(variant, cluster)
+    yield set_
+    L.tp_debug_set_als_variant(0, 0)
+
+
+@pytest.mark.parametrize("variant,cluster", [(1, 0), (2, 2), (2, 4), (2, 0)])
+@pytest.mark.parametrize("qs,R,r", [((64, 48, 80, 64), 96, 16), ((40, 37, 50), 61, 12), ((32,) * 5, 64, 30)])
+def test_als_kernel_variants(als_variant, variant, cluster, qs, R, r):
+    """Both persistent kernels (R-slab per CTA; clusters of row blocks with the DSMEM
+    cross all-reduce) on ragged mode sizes / slab widths, with the residual trace."""
+    als_variant(variant, cluster)
+    rng = np.random.default_rng(R + r)
+    V = rand_factors(rng, qs, R, 0.25)
+    init = [v[:, :r].copy() for v in V]
+    out, ref, trace, otrace = _als_case(V, init, 9, 1e-10)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+    np.testing.assert_allclose(trace, otrace, rtol=1e-8, atol=1e-12)
+
+
+@pytest.mark.parametrize("variant,cluster", [(1, 0), (2, 4)])
+def test_als_config1_variants(als_variant, variant, cluster):
+    als_variant(variant, cluster)
+    w = workloads.cfg1(seed=2)
+    out, ref, _, _ = _als_case(w["V"], w["init"], w["sweeps"], w["lam"])
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC

@@ -141,3 +141,27 @@ def test_from_cp_add_scale_apply():
     ref_cp = oops.apply([-1.0, -0.5, 0.75], mats, f)
     assert metrics.ht_rel_diff(oht.from_cp(ref_cp), out.to_oracle()) <= 1e-12
     _ = ocp
+
+
+@pytest.mark.parametrize("chol", [0, 1])
+def test_frame_factor_paths(chol):
+    """Frame-Gram square-root factor by Cholesky (default) or eigh (reference path),
+    with one rank-deficient leaf so both paths run inside one truncation."""
+    import ctypes
+    from paper_1803_10270_b200 import _lib
+    L = _lib.lib()
+    L.tp_debug_set_ht_chol.argtypes = [ctypes.c_int]
+    L.tp_debug_set_ht_chol(chol)
+    try:
+        rng = np.random.default_rng(21)
+        d, q, k = 6, 14, 8
+        o = random_ht(rng, d, q, k)
+        nodes, frames, transfers = o
+        leaf = next(i for i, nd in enumerate(nodes) if oht.is_leaf(nd))
+        frames[leaf][:, -2:] = frames[leaf][:, :2]     # duplicated columns: singular frame Gram
+        red, est = ht.truncate(to_dev(d, q, o), 4, 0.0)
+        ref, oest = oht.truncate(o, 4, 0.0)
+        assert abs(est - oest) <= 1e-8 * max(1.0, oht.norm(o))
+        assert metrics.ht_rel_diff(ref, red.to_oracle()) <= TOL
+    finally:
+        L.tp_debug_set_ht_chol(1)
