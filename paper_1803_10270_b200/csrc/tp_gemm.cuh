@@ -22,12 +22,16 @@ struct BGemm {
   const double* B;
   double* C;
   double alpha, beta;
+  int ksplit;                // split-K factor (>1: partial tiles to `part`, then bgemm_reduce)
+  double* part;              // [nb1*nb2][ksplit][M][N] partials when ksplit > 1
 };
 
 static __global__ void __launch_bounds__(128) bgemm_kernel(const __grid_constant__ BGemm g) {
   __shared__ double As[GB_TK][GB_LD];
   __shared__ double Bs[GB_TK][GB_LD];
-  const int z = blockIdx.z, z1 = z / g.nb2, z2 = z % g.nb2;
+  const int ks = g.ksplit > 1 ? g.ksplit : 1;
+  const int zz = blockIdx.z / ks, sidx = blockIdx.z - zz * ks;
+  const int z1 = zz / g.nb2, z2 = zz % g.nb2;
   long long oA, oB, oC;
   if (g.offs) {
     oA = g.offs[3 * z1]; oB = g.offs[3 * z1 + 1]; oC = g.offs[3 * z1 + 2];
@@ -46,7 +50,10 @@ static __global__ void __launch_bounds__(128) bgemm_kernel(const __grid_constant
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const bool a_m_fast = g.sAm == 1, b_n_fast = g.sBn == 1;
-  for (int k0 = 0; k0 < g.K; k0 += GB_TK) {
+  // split-K range of this CTA (whole GB_TK tiles)
+  const int ktiles = (g.K + GB_TK - 1) / GB_TK, kt0 = (int)((long long)ktiles * sidx / ks),
+            kt1 = (int)((long long)ktiles * (sidx + 1) / ks);
+  for (int k0 = kt0 * GB_TK; k0 < kt1 * GB_TK; k0 += GB_TK) {
     __syncthreads();
     for (int e = tid; e < GB_TK * GB_TM; e += 128) {
       int kk, mm;
@@ -83,11 +90,32 @@ static __global__ void __launch_bounds__(128) bgemm_kernel(const __grid_constant
       for (int h = 0; h < 2; ++h) {
         const int m = m0 + wm + 8 * i + (lane >> 2), n = n0 + wn + 8 * j + 2 * (lane & 3) + h;
         if (m < g.M && n < g.N) {
-          double* c = C + m * g.sCm + n * g.sCn;
-          const double v = g.alpha * acc[i][j][h];
-          *c = (g.beta == 0.0) ? v : fma(g.beta, *c, v);
+          if (ks > 1) {
+            g.part[(((size_t)zz * ks + sidx) * g.M + m) * g.N + n] = acc[i][j][h];
+          } else {
+            double* c = C + m * g.sCm + n * g.sCn;
+            const double v = g.alpha * acc[i][j][h];
+            *c = (g.beta == 0.0) ? v : fma(g.beta, *c, v);
+          }
         }
       }
+}
+
+// split-K epilogue: C_z = alpha * sum_s part[z][s] + beta * C_z (fixed order)
+static __global__ void bgemm_reduce_kernel(const __grid_constant__ BGemm g) {
+  const int z = blockIdx.y, z1 = z / g.nb2, z2 = z % g.nb2;
+  long long oC = g.offs ? g.offs[3 * z1 + 2] : z1 * g.sC1;
+  double* C = g.C + oC + z2 * g.sC2;
+  const size_t mn = (size_t)g.M * g.N;
+  const double* p = g.part + (size_t)z * g.ksplit * mn;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < mn; e += (size_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < g.ksplit; ++s) acc += p[s * mn + e];
+    const int m = (int)(e / g.N), n = (int)(e % g.N);
+    double* c = C + m * g.sCm + n * g.sCn;
+    const double v = g.alpha * acc;
+    *c = (g.beta == 0.0) ? v : fma(g.beta, *c, v);
+  }
 }
 
 static inline BGemm bgemm_desc(int M, int N, int K, const double* A, long long sAm, long long sAk, const double* B,
@@ -97,13 +125,31 @@ static inline BGemm bgemm_desc(int M, int N, int K, const double* A, long long s
   g.A = A; g.B = B; g.C = C;
   g.sAm = sAm; g.sAk = sAk; g.sBk = sBk; g.sBn = sBn; g.sCm = sCm; g.sCn = sCn;
   g.alpha = 1.0; g.beta = 0.0;
+  g.ksplit = 1; g.part = nullptr;
   return g;
+}
+
+// split-K factor that fills the GPU (>= 2 CTAs per SM) for K-heavy batched GEMMs
+static inline int bgemm_pick_split(const BGemm& g, int nsm = 148) {
+  const long long tiles = (long long)((g.N + GB_TN - 1) / GB_TN) * ((g.M + GB_TM - 1) / GB_TM) * g.nb1 * g.nb2;
+  const int ktiles = (g.K + GB_TK - 1) / GB_TK;
+  int s = 1;
+  while (tiles * s < 2LL * nsm && ktiles / (2 * s) >= 8) s *= 2;
+  return s;
 }
 
 static inline cudaError_t bgemm_launch(const BGemm& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.nb1 * g.nb2 <= 0) return cudaSuccess;
-  dim3 grid((g.N + GB_TN - 1) / GB_TN, (g.M + GB_TM - 1) / GB_TM, g.nb1 * g.nb2);
-  bgemm_kernel<<<grid, 128, 0, st>>>(g);
+  const int ks = (g.ksplit > 1 && g.part) ? g.ksplit : 1;
+  BGemm h = g;
+  h.ksplit = ks;
+  dim3 grid((g.N + GB_TN - 1) / GB_TN, (g.M + GB_TM - 1) / GB_TM, g.nb1 * g.nb2 * ks);
+  bgemm_kernel<<<grid, 128, 0, st>>>(h);
+  if (ks > 1) {
+    const size_t mn = (size_t)g.M * g.N;
+    dim3 rg((unsigned)((mn + 255) / 256 < 64 ? (mn + 255) / 256 : 64), g.nb1 * g.nb2);
+    bgemm_reduce_kernel<<<rg, 256, 0, st>>>(h);
+  }
   return cudaGetLastError();
 }
 

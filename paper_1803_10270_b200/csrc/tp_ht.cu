@@ -364,6 +364,9 @@ __global__ void set_root_env(int k, int nn, int nb, double* Gh) {
   if (b < nb) Gh[(size_t)b * nn * k * k] = 1.0;
 }
 
+// split-K partial tiles: bgemm_pick_split only splits below 2 x 148 x 2 CTAs of 64 x 64
+constexpr size_t HT_PART = (size_t)GB_TM * GB_TN * 4 * 148;
+
 struct HtPlan {
   Tree T;
   int d, Q, k, nb, ro, maxw;
@@ -394,7 +397,8 @@ static void plan_ht(int d, int Q, int k, int nb, int r_max, HtPlan& P) {
   const size_t nn = P.T.n, kk = (size_t)k * k;
   P.off_n = (size_t)nb * (P.T.nleaf + P.T.nint) * 3 * 8 * 8;   // generous offset-table space
   P.total = align_up(8 * nb * nn * kk) * 5 + align_up(8 * nb * nn * k) * 2 + align_up(8 * nb * nn * (size_t)k * P.ro) * 2 +
-            2 * align_up(4 * nb * nn) + align_up(8 * nb * nn) + 3 * align_up(8 * P.big) + align_up(8 * P.off_n) + 256;
+            2 * align_up(4 * nb * nn) + align_up(8 * nb * nn) + 3 * align_up(8 * P.big) + align_up(8 * P.off_n) + 256 +
+            align_up(8 * HT_PART);
 }
 
 }  // namespace tp
@@ -455,6 +459,7 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
   double* big2 = cv.take<double>(P0.big);
   double* big3 = cv.take<double>(P0.big);
   long long* doffs = cv.take<long long>(P0.off_n);
+  double* kpart = cv.take<double>(HT_PART);
   double* one = reinterpret_cast<double*>(cv.take<double>(1));
   if (!cv.ok()) return TP_EWORKSPACE;
 
@@ -479,6 +484,8 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
   auto add_gemm = [&](BGemm g, const std::vector<long long>& offs) {
     Call c{g, 0, 0};
     if (!offs.empty()) { c.tab = table(offs); c.use_tab = 1; c.g.nb1 = (int)(offs.size() / 3); }
+    const int ks = bgemm_pick_split(c.g);
+    if (ks > 1 && (size_t)c.g.M * c.g.N * c.g.nb1 * c.g.nb2 * ks <= HT_PART) { c.g.ksplit = ks; c.g.part = kpart; }
     calls.push_back(c);
     order.push_back((int)calls.size() - 1);
   };
