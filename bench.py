@@ -17,10 +17,12 @@ init = first 32 input terms, BASELINE.json configs[1]) of seeded synthetic input
 * ``cpu_baseline`` -- the oracle restatement of the reference path (complex128,
   like the shipped reference) timed on this host's cores on a bounded sample.
 
-N > 1 (torchrun): ``--mode sharded`` (default for N > 1) shards the R input terms
-of ONE config-1 truncation across ranks with an NCCL all-reduce of the r x Q
-right-hand side per mode update (strong scaling, BASELINE configs[1]);
-``--mode replicas`` runs an independent truncation per rank (weak scaling).
+N > 1 (torchrun): ``--mode replicas`` (default for N > 1) runs an independent
+config-1 truncation per rank (weak scaling: batches of independent truncations
+sharded with no communication); ``--mode sharded`` shards the R input terms of ONE
+truncation across ranks with an NCCL all-reduce of the r x Q right-hand side per
+mode update (strong scaling, BASELINE configs[1]) -- latency-bound at this size
+(120 dependent all-reduces per 1.5 ms truncation), see DESIGN.md section 7.
 ``extra_configs`` reports device-resident throughput of configs 0, 2, 3 (rank 0,
 N = 1) and of config 4 (batch of 64 HT tensors sharded across ranks).
 """
@@ -280,7 +282,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    mode = args.mode or ("sharded" if world > 1 else "fused")
+    mode = args.mode or "fused"     # N > 1: independent truncation per rank (replicas)
     if mode == "sharded":
         dev = torch.device("cuda", local)
         tot_ms, clocks = run_sharded(args, world, rank, local, dev)
@@ -307,6 +309,7 @@ def run_ours(args):
     from paper_1803_10270_b200 import cp, workloads
     from paper_1803_10270_b200 import _lib
     dev = torch.device("cuda", local)
+    plan = cp.als_plan([Q] * D, R, RANK_R, args.grid)
     w = workloads.cfg1(seed=rank)
     specs = w["specs"]
     T = cp.CPTensor(specs, w["V"])
@@ -393,13 +396,15 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1)/sqrt(Q), seed = rank)",
             "config": {"workload": WORKLOAD, "l2": "flushed (256 MiB write) between timed steps",
-                       "grid_ctas": args.grid or "auto", "target_norm": "not computed (no trace / stopping rule)",
+                       "grid_ctas": plan["ctas"], "cluster_ctas": plan["cluster"],
+                       "target_norm": "not computed (no trace / stopping rule)",
                        "multi_gpu": "independent replicas per rank (weak)" if world > 1 else "single GPU"},
             "e2e": {"value": e2e_val, "unit": "sweeps/s", "h2d_bytes_per_step": int((hV.numel() + hI.numel()) * 8),
                     "d2h_bytes_per_step": int(hOut.numel() * 8 + 8)},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
-                         "kernel": "tp::als_persistent<32> (one launch per step)",
+                         "kernel": f"tp::{plan['kernel']}<32> (one launch per step; {plan['ctas']} CTAs, "
+                                   f"cluster {plan['cluster']}, {plan['smem_bytes']} B smem)",
                          "flops_per_launch": FLOPS_PER_STEP,
                          "peak_source": "measured fp64 DMMA peak (profiles/r01_microbench.txt); no fp64 entry in "
                                         "MEASURED_PEAKS.json"},
@@ -427,7 +432,7 @@ def main():
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--mode", choices=["fused", "sharded", "replicas"], default=None)
+    ap.add_argument("--mode", choices=["fused", "sharded", "replicas"], default=None)   # replicas == fused per rank
     ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -238,6 +238,15 @@ def _als_device(target: CPTensor, U: torch.Tensor, r: int, cfg: ALSApproxConfig,
     _lib.check(st, "cp_approx_als")
 
 
+def als_plan(qs, R: int, r: int, grid: int = 0) -> dict:
+    """Launch plan of the fused ALS kernel for these sizes (tp_cp_als_plan)."""
+    out = (ctypes.c_int * 4)()
+    st = _lib.lib().tp_cp_als_plan(len(qs), _lib.int_array(qs), R, r, grid, out)
+    _lib.check(st, "als_plan")
+    variant = "als_cluster" if out[0] == 1 else "als_persistent"
+    return {"kernel": variant, "ctas": out[1], "cluster": out[2], "smem_bytes": out[3]}
+
+
 def _check_info(info: torch.Tensor) -> int:
     status, done = (int(v) for v in info.tolist())
     if status & 2:

@@ -1478,6 +1478,15 @@ void tp_debug_set_als_ns(int n) { g_ns_max = n; }
 // debug hook: kernel variant (0 auto, 1 als_persistent, 2 als_cluster) and cluster size (0 auto, -1 never)
 void tp_debug_set_als_variant(int variant, int cluster) { g_variant = variant; g_cluster = cluster; }
 
+int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out) {
+  if (!out) return TP_EINVAL;
+  AlsPlan pl;
+  const int st = plan_als(d, q, R, r, grid, pl);
+  if (st != TP_OK) return st;
+  out[0] = pl.variant; out[1] = pl.P; out[2] = pl.variant == 1 ? pl.a.Pq : 1; out[3] = (int)pl.smem;
+  return TP_OK;
+}
+
 size_t tp_cp_als_ws_bytes(int d, const int* q, int R, int r, int grid) {
   AlsPlan pl;
   if (plan_als(d, q, R, r, grid, pl) != TP_OK) return 0;
