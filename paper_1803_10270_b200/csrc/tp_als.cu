@@ -24,6 +24,7 @@
 #include "tp_common.cuh"
 #include <cooperative_groups.h>
 #include <cstring>
+#include <cstdlib>
 
 namespace cg = cooperative_groups;
 
@@ -1544,6 +1545,11 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
     at[1].val.cooperative = 1;
     cfg.gridDim = dim3(pl.P); cfg.blockDim = dim3(ALS_NT); cfg.dynamicSmemBytes = pl.smem; cfg.stream = s;
     cfg.attrs = at; cfg.numAttrs = 2;
+    // profiling aid: Nsight Compute cannot launch cooperative cluster kernels;
+    // TP_ALS_NONCOOP=1 drops the cooperative attribute (co-residency then rests on
+    // the occupancy check of plan_cluster, fine on an otherwise idle GPU)
+    static const bool noncoop = getenv("TP_ALS_NONCOOP") && getenv("TP_ALS_NONCOOP")[0] == '1';
+    if (noncoop) cfg.numAttrs = 1;
     void* args[] = {&a};
     e = cudaLaunchKernelExC(&cfg, fn, args);
     return cuda_status(e);
