@@ -105,7 +105,12 @@ __device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, ui
 }
 
 // order this thread's prior generic-proxy accesses with later async-proxy (bulk copy) ones
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// (all state spaces: the bulk copies read global data that other CTAs wrote with
+// generic stores, and overwrite shared memory this CTA read with generic loads)
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 // same, for copies that write peer CTAs' shared memory
 __device__ __forceinline__ void fence_proxy_async_cluster() {
   asm volatile("fence.proxy.async.shared::cluster;\n" ::: "memory");
