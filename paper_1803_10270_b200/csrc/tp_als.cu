@@ -123,6 +123,7 @@ __device__ inline Smem carve(double* base, const AlsArgs& a) {
 // Cross-CTA data is read through L2 (__ldcg / bulk copies), so no L1 flush.
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& epoch) {
   __syncthreads();
+  if (gridDim.x == 1) return;   // one CTA: the block barrier orders everything
   if (threadIdx.x == 0) {
     ++epoch;
     const unsigned int target = epoch * gridDim.x;
@@ -525,18 +526,29 @@ __device__ void ns_rows(const AlsArgs& a, const Smem& sm, int j, int sweep) {
   constexpr int TPO = RM / 8;
   const int r = a.r, rh = pad4(r), P = gridDim.x, p = blockIdx.x, tid = threadIdx.x;
   double* Xn = a.Xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;
-  double* xr = sm.Rm;
-  for (int i0 = P - 1 - p; i0 < r; i0 += P) {
-    for (int base = 0; base < r * TPO; base += ALS_NT) {
-      const int t = base + tid, c = t / TPO, part = t - c * TPO;
-      const double acc = mv_dot<RM>(sm.Am, rh, sm.X0 + i0 * rh, c < r ? c : 0, r, part);
-      if (c < r && part == 0) xr[c] = acc;
+  const int i_first = P - 1 - p;
+  if (i_first >= r) return;
+  const int nrows = (r - 1 - i_first) / P + 1;     // rows i_first, i_first + P, ...
+  // all owned rows at once, chunked so the X0 A rows fit the scratch (sm.Rm: r x pad4(r))
+  for (int c0 = 0; c0 < nrows; c0 += r) {
+    const int nr = min(r, nrows - c0);
+    double* xr = sm.Rm;                          // [nr][rh]: rows of X0 A
+    for (int base = 0; base < nr * r * TPO; base += ALS_NT) {
+      const int t = base + tid, o = t / TPO, part = t - o * TPO;
+      const bool act = o < nr * r;
+      const int q = act ? o / r : 0, c = act ? o - q * r : 0;
+      const int i0 = i_first + (c0 + q) * P;
+      const double acc = mv_dot<RM>(sm.Am, rh, sm.X0 + (act ? i0 : i_first) * rh, c, r, part);
+      if (act && part == 0) xr[q * rh + c] = acc;
     }
     __syncthreads();
-    for (int base = 0; base < r * TPO; base += ALS_NT) {
-      const int t = base + tid, c = t / TPO, part = t - c * TPO;
-      const double acc = mv_dot<RM>(sm.X0, rh, xr, c < r ? c : 0, r, part);
-      if (c < r && part == 0) Xn[(size_t)i0 * rh + c] = 2.0 * sm.X0[i0 * rh + c] - acc;
+    for (int base = 0; base < nr * r * TPO; base += ALS_NT) {
+      const int t = base + tid, o = t / TPO, part = t - o * TPO;
+      const bool act = o < nr * r;
+      const int q = act ? o / r : 0, c = act ? o - q * r : 0;
+      const int i0 = i_first + (c0 + q) * P;
+      const double acc = mv_dot<RM>(sm.X0, rh, xr + q * rh, c, r, part);
+      if (act && part == 0) Xn[(size_t)i0 * rh + c] = 2.0 * sm.X0[i0 * rh + c] - acc;
     }
     __syncthreads();
   }

@@ -12,7 +12,7 @@ NAMES = ["(loop head)", "A:gram_share", "A:had+Y", "barrier1", "B:reduce", "B:wa
          "barrier2", "B:wait G/X", "B:solve (NS/exact)", "A:stage_u", "A:cross", "A:exchange", "-", "-", "-"]
 
 
-def run(grid, Q=256, R=512, r=32):
+def run(grid, Q=256, R=512, r=32, sweeps=20):
     w = workloads.cfg1(0, Q=Q, R=R, r=r)
     T = cp.CPTensor(w["specs"], w["V"])
     I0 = cp.CPTensor(w["specs"], w["init"])
@@ -21,7 +21,7 @@ def run(grid, Q=256, R=512, r=32):
     L = _lib.lib()
     L.tp_debug_set_als_profile.argtypes = [ctypes.c_void_p]
     info = torch.zeros(2, dtype=torch.int32, device=dev)
-    cfg = cp.ALSApproxConfig(max_sweeps=20, stall=-np.inf, reg=1e-10, grid=grid)
+    cfg = cp.ALSApproxConfig(max_sweeps=sweeps, stall=-np.inf, reg=1e-10, grid=grid)
     U = I0.data.clone()
     cp._als_device(T, U, r, cfg, None, info)
     L.tp_debug_set_als_profile(prof.data_ptr())
@@ -29,7 +29,7 @@ def run(grid, Q=256, R=512, r=32):
     cp._als_device(T, U, r, cfg, None, info)
     torch.cuda.synchronize()
     L.tp_debug_set_als_profile(None)
-    p = prof.cpu().numpy() / 120.0
+    p = prof.cpu().numpy() / (sweeps * 6.0)
     tot = p[:16].sum()
     print(f"grid={grid} Q={Q} R={R} r={r}: cycles per mode update (CTA 0): total {tot:.0f}")
     for i in [0, 10, 11, 12, 1, 2, 3, 8, 5, 4, 9, 6, 7]:
@@ -49,5 +49,6 @@ if __name__ == "__main__":
     for ns in (6,):
         print(f"--- Newton-Schulz cap {ns}")
         Lb.tp_debug_set_als_ns(ns)
+        size = [int(x) for x in os.environ.get("ALS_SIZE", "256,512,32,20").split(",")]
         for g in [int(x) for x in sys.argv[1:]] or [0]:
-            run(g)
+            run(g, *size)
