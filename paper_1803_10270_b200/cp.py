@@ -25,7 +25,7 @@ from .basis import BasisSpec
 
 __all__ = [
     "CPTensor", "ALSApproxConfig", "ConditioningError", "add", "scale", "inner_product", "norm",
-    "random_cp", "pad_rank", "cp_approx_als", "rank_reduce_als", "from_numpy_factors",
+    "random_cp", "pad_rank", "cp_approx_als", "check", "rank_reduce_als", "from_numpy_factors",
 ]
 
 
@@ -49,9 +49,10 @@ class CPTensor:
     factors into one device buffer (value semantics, like the reference's
     ``np.ascontiguousarray`` copy)."""
 
-    __slots__ = ("specs", "data", "_rank")
+    __slots__ = ("specs", "data", "_rank", "pending_info")
 
     def __init__(self, specs, factors=None, *, data: torch.Tensor | None = None, rank: int | None = None):
+        self.pending_info = None
         self.specs = tuple(specs)
         if data is not None:
             self.data = data
@@ -257,12 +258,17 @@ def _check_info(info: torch.Tensor) -> int:
 
 
 def cp_approx_als(target, r: int, config: ALSApproxConfig | None = None, *, specs=None,
-                  init: CPTensor | None = None, trace: list | None = None) -> CPTensor:
+                  init: CPTensor | None = None, trace: list | None = None, sync: bool = True) -> CPTensor:
     """Fit a rank-``r`` CP tensor to ``target`` by Gauss-Seidel ALS (cp.py:266-334).
 
     One call = one launch of the persistent fused ALS kernel (all sweeps).
     Callable targets (cp.py:212-263, quadrature projection) are out of the
     hot-path scope and raise ``NotImplementedError``.
+
+    ``sync=False`` (B200 extension, pipelined callers): the status word is not
+    read back; the result carries it and ``check(result)`` raises the reference's
+    ConditioningError later (no host round trip per call).  Incompatible with
+    ``trace``.
     """
     cfg = config or ALSApproxConfig()
     if not isinstance(target, CPTensor):
@@ -278,10 +284,24 @@ def cp_approx_als(target, r: int, config: ALSApproxConfig | None = None, *, spec
     info = torch.zeros(2, dtype=torch.int32, device=dev)
     tb = torch.zeros(max(cfg.max_sweeps, 1), dtype=torch.float64, device=dev) if trace is not None else None
     _als_device(target, guess.data, r, cfg, tb, info)
+    if not sync:
+        if trace is not None:
+            raise ValueError("trace needs sync=True")
+        guess.pending_info = info
+        return guess
     done = _check_info(info)
     if trace is not None:
         trace.extend(tb[:done].tolist())
     return guess
+
+
+def check(result: CPTensor) -> CPTensor:
+    """Raise the deferred status of a ``cp_approx_als(..., sync=False)`` result."""
+    info = result.pending_info
+    if info is not None:
+        _check_info(info)
+        result.pending_info = None
+    return result
 
 
 def _relative_error(f: CPTensor, g: CPTensor, nf: float) -> float:

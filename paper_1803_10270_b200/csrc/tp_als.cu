@@ -25,6 +25,9 @@
 #include <cooperative_groups.h>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 namespace cg = cooperative_groups;
 
@@ -1405,7 +1408,40 @@ static int plan_cluster(int d, const int* q, int R, int r, int Pq, int smem_opti
   return TP_EUNSUPPORTED;
 }
 
+static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPlan& pl);
+
+// plans are pure functions of (device, sizes, grid, debug variant): cache them, the
+// cluster occupancy queries cost tens of microseconds per call
+struct PlanKey {
+  int dev, d, R, r, grid, variant, cluster;
+  int q[TP_MAXD];
+  bool operator==(const PlanKey& o) const { return memcmp(this, &o, sizeof(PlanKey)) == 0; }
+};
+
 static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
+  if (d < 1 || d > TP_MAXD || R < 1 || r < 1 || !q) return TP_EINVAL;
+  static std::mutex mu;
+  static std::vector<std::pair<PlanKey, AlsPlan>> cache;
+  PlanKey key;
+  memset(&key, 0, sizeof(key));
+  if (cudaGetDevice(&key.dev) != cudaSuccess) { cudaGetLastError(); key.dev = -1; }
+  key.d = d; key.R = R; key.r = r; key.grid = grid; key.variant = g_variant; key.cluster = g_cluster;
+  for (int k = 0; k < d; ++k) key.q[k] = q[k];
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : cache)
+      if (e.first == key) { pl = e.second; return TP_OK; }
+  }
+  const int st = plan_als_uncached(d, q, R, r, grid, pl);
+  if (st == TP_OK) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() > 64) cache.clear();
+    cache.emplace_back(key, pl);
+  }
+  return st;
+}
+
+static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
   if (d < 1 || d > TP_MAXD || R < 1 || r < 1 || !q) return TP_EINVAL;
   for (int k = 0; k < d; ++k) if (q[k] < 1) return TP_EINVAL;
   pl.rm = choose_rm(r);

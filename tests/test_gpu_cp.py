@@ -213,3 +213,17 @@ def test_als_config1_variants(als_variant, variant, cluster):
     w = workloads.cfg1(seed=2)
     out, ref, _, _ = _als_case(w["V"], w["init"], w["sweeps"], w["lam"])
     assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+
+
+def test_als_deferred_check_matches_sync():
+    rng = np.random.default_rng(12)
+    qs, R, r = (12, 10, 14), 20, 4
+    S = specs_for(qs)
+    V = cp.CPTensor(S, rand_factors(rng, qs, R, 0.3))
+    I0 = cp.CPTensor(S, [f[:, :r].copy() for f in V.to_numpy()])
+    cfg = cp.ALSApproxConfig(max_sweeps=6, stall=-np.inf, reg=1e-10)
+    a = cp.cp_approx_als(V, r, cfg, init=I0)
+    b = cp.check(cp.cp_approx_als(V, r, cfg, init=I0, sync=False))
+    assert torch.equal(a.data, b.data) and b.pending_info is None
+    with pytest.raises(ValueError, match="trace"):
+        cp.cp_approx_als(V, r, cfg, init=I0, sync=False, trace=[])
