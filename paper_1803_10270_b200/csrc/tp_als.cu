@@ -460,7 +460,6 @@ __device__ bool solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, i
   double* zb = sm.vb;
   double* yb = sm.vb + nv;
   double* ub = sm.vb + 2 * nv;
-  double* xr = sm.Rm;            // row of X0 A
   // warm starts are double-buffered by sweep parity: this sweep reads buffer
   // (sweep & 1) and writes the other, so results do not depend on CTA timing
   double* Xn = a.Xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;

@@ -130,11 +130,11 @@ static inline BGemm bgemm_desc(int M, int N, int K, const double* A, long long s
 }
 
 // split-K factor that fills the GPU (>= 2 CTAs per SM) for K-heavy batched GEMMs
-static inline int bgemm_pick_split(const BGemm& g, int nsm = 148) {
+static inline int bgemm_pick_split(const BGemm& g, int nsm = 148, int min_ktiles = 8) {
   const long long tiles = (long long)((g.N + GB_TN - 1) / GB_TN) * ((g.M + GB_TM - 1) / GB_TM) * g.nb1 * g.nb2;
   const int ktiles = (g.K + GB_TK - 1) / GB_TK;
   int s = 1;
-  while (tiles * s < 2LL * nsm && ktiles / (2 * s) >= 8) s *= 2;
+  while (tiles * s < 2LL * nsm && ktiles / (2 * s) >= min_ktiles) s *= 2;
   return s;
 }
 

@@ -23,6 +23,7 @@
 namespace tp {
 
 constexpr int IM_MAXD = 8, IM_MAXRA = 16, IM_MAXT = 64;
+constexpr size_t IM_KPART = 8;   // split-K partial space, in units of n_tab * Q * r doubles
 constexpr int CH_NB = 64;   // Cholesky block size
 
 struct HArgs {
@@ -243,56 +244,6 @@ __global__ void __launch_bounds__(256) conv_damp_kernel(int Q, int r, int d, dou
 
 __global__ void set_int_kernel(int* dst, int v) { *dst = v; }
 
-// Fused Gram refresh of mode k for every table it uses (one CTA per table):
-//   G[k][t]  = b_new,k^T T_t b_new,k      Gm[k][t] = b_new,k^T T~_t b_old,k
-// (T~ = T for the corrected normal equations, T^T for the reference orientation)
-struct GramArgs {
-  int Q, r, k, n_tab, transT, nt;
-  int ts[IM_MAXT];
-  const double* tabs;
-  const double* bnew;   // mode k block (Q x r)
-  const double* bold;   // mode k block (Q x r)
-  double* G;
-  double* Gm;
-};
-
-__global__ void __launch_bounds__(256) mode_grams_kernel(const __grid_constant__ GramArgs a) {
-  extern __shared__ double gsm[];
-  const int t = a.ts[blockIdx.x], Q = a.Q, r = a.r, tid = threadIdx.x;
-  double* bn = gsm;                 // Q x r
-  double* bo = bn + (size_t)Q * r;  // Q x r
-  double* tb = bo + (size_t)Q * r;  // Q x r  (T b_new)
-  double* tc = tb + (size_t)Q * r;  // Q x r  (T~ b_old)
-  for (int e = tid; e < Q * r; e += 256) { bn[e] = a.bnew[e]; bo[e] = a.bold[e]; }
-  __syncthreads();
-  const double* T = a.tabs + (size_t)t * Q * Q;
-  for (int e = tid; e < Q * r; e += 256) {
-    const int row = e / r, c = e % r;
-    double s1 = 0.0, s2 = 0.0;
-    for (int m = 0; m < Q; ++m) {
-      const double tv = T[(size_t)row * Q + m];
-      const double tt = a.transT ? T[(size_t)m * Q + row] : tv;
-      s1 = fma(tv, bn[m * r + c], s1);
-      s2 = fma(tt, bo[m * r + c], s2);
-    }
-    tb[e] = s1;
-    tc[e] = s2;
-  }
-  __syncthreads();
-  const size_t go = ((size_t)a.k * a.n_tab + t) * r * r;
-  for (int e = tid; e < r * r; e += 256) {
-    const int l = e / r, n = e % r;
-    double s1 = 0.0, s2 = 0.0;
-    for (int m = 0; m < Q; ++m) {
-      const double b = bn[m * r + l];
-      s1 = fma(b, tb[m * r + n], s1);
-      s2 = fma(b, tc[m * r + n], s2);
-    }
-    a.G[go + e] = s1;
-    a.Gm[go + e] = s2;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Circulant fast path: when every pairing table is circulant (Fourier
 // collocation operators), M_q = sum_X H_X^T (x) T_X^T + lam I is block-diagonal
@@ -321,7 +272,7 @@ struct CircArgs {
 
 __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__ CircArgs a) {
   extern __shared__ double cs[];
-  const int k = blockIdx.x, r = a.r, Q = a.Q, tid = threadIdx.x, rr = r * r;
+  const int k = blockIdx.x, r = a.r, Q = a.Q, tid = threadIdx.x;
   const int ld = r + 1;
   double* Mre = cs;                       // [r][ld]
   double* Mim = Mre + r * ld;
@@ -432,6 +383,7 @@ static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
   size_t s = 0;
   s += align_up(8 * (size_t)d * n_tab * r * r) * 2;     // G, Gm
   s += align_up(8 * (size_t)d * n_tab * Q * r) * 3;     // TB, TC scratch, W (b_old images)
+  s += align_up(8 * IM_KPART * n_tab * Q * r);          // split-K partial tiles
   s += align_up(8 * (size_t)n_tab * r * r) * 2;         // H, Hg
   s += align_up(8 * n * n);                             // M
   s += align_up(8 * (n / CH_NB + 1) * CH_NB * CH_NB);   // Linv blocks
@@ -472,6 +424,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   double* TB = cv.take<double>((size_t)d * n_tab * QR);
   double* W2 = cv.take<double>((size_t)d * n_tab * QR);
   double* W = cv.take<double>((size_t)d * n_tab * QR);
+  double* kpart = cv.take<double>(IM_KPART * (size_t)n_tab * QR);
   double* H = cv.take<double>((size_t)n_tab * rr);
   double* Hg = cv.take<double>((size_t)n_tab * rr);
   double* M = cv.take<double>((size_t)n * n);
@@ -517,31 +470,9 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     for (int t : used[k]) {
       BGemm g = bgemm_desc(Q, r, Q, tabs + (size_t)t * Q * Q, transT ? 1 : Q, transT ? Q : 1, bsrc + (size_t)k * QR,
                            r, 1, dst + ((size_t)k * n_tab + t) * QR, r, 1);
+      const int ks = bgemm_pick_split(g, 148, 2);
+      if (ks > 1 && (size_t)g.M * g.N * ks <= IM_KPART * (size_t)n_tab * QR) { g.ksplit = ks; g.part = kpart; }
       cudaError_t e = bgemm_launch(g, st);
-      if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-  };
-  const size_t gk_smem = sizeof(double) * 4 * QR;
-  const bool fused_grams = gk_smem <= 200 * 1024;
-  if (fused_grams) cudaFuncSetAttribute(mode_grams_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gk_smem);
-  // G[k] and Gm[k] for every table of mode k in one launch
-  auto refresh = [&](int k, int transT) -> cudaError_t {
-    GramArgs ga;
-    memset(&ga, 0, sizeof(ga));
-    ga.Q = Q; ga.r = r; ga.k = k; ga.n_tab = n_tab; ga.transT = transT; ga.nt = (int)used[k].size();
-    for (int i = 0; i < ga.nt; ++i) ga.ts[i] = used[k][i];
-    ga.tabs = tabs; ga.bnew = f_new + (size_t)k * QR; ga.bold = f_old + (size_t)k * QR; ga.G = G; ga.Gm = Gm;
-    mode_grams_kernel<<<ga.nt, 256, gk_smem, st>>>(ga);
-    return cudaGetLastError();
-  };
-  auto grams = [&](int k, const double* aa, const double* bsrc, double* dstG, int transT) -> cudaError_t {
-    cudaError_t e = images(k, bsrc, TB, transT);
-    if (e != cudaSuccess) return e;
-    for (int t : used[k]) {
-      BGemm g = bgemm_desc(r, r, Q, aa + (size_t)k * QR, 1, r, TB + ((size_t)k * n_tab + t) * QR, r, 1,
-                           dstG + ((size_t)k * n_tab + t) * rr, r, 1);
-      e = bgemm_launch(g, st);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -578,6 +509,14 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     g3.offs = o2; g3.nb1 = nt;
     BGemm g4 = bgemm_desc(r, r, Q, f_new, 1, r, W2, r, 1, Gm, r, 1);            // Gm = b_new^T TC
     g4.offs = o2; g4.nb1 = nt;
+    // latency-bound small GEMMs (K = Q): split K so each CTA walks 2 tiles
+    for (BGemm* g : {&g1, &g2, &g3, &g4}) {
+      const int ks = bgemm_pick_split(*g, 148, 2);
+      if (ks > 1 && (size_t)g->M * g->N * g->nb1 * g->nb2 * ks <= IM_KPART * (size_t)n_tab * QR) {
+        g->ksplit = ks;
+        g->part = kpart;
+      }
+    }
     cudaError_t e = bgemm_launch(g1, st);
     if (e == cudaSuccess) e = bgemm_launch(g2, st);
     if (e == cudaSuccess) e = bgemm_launch(g3, st);

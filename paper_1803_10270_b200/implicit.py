@@ -183,9 +183,10 @@ def step(f_n: CPTensor, pair: CrankNicolsonPair, forcing: CPTensor | None, confi
     return CPTensor(f_n.specs, data=out, rank=f_n.rank)
 
 
-def run(f0: CPTensor, pair: CrankNicolsonPair, config: ALSStepConfig, steps: int) -> CPTensor:
+def run(f0: CPTensor, pair: CrankNicolsonPair, config: ALSStepConfig, steps: int,
+        workspace: StepWorkspace | None = None) -> CPTensor:
     """``steps`` implicit steps, stream-ordered, one status check at the end."""
-    ws = StepWorkspace(pair, config)
+    ws = workspace or StepWorkspace(pair, config)
     dev = f0.data.device
     eps = torch.zeros(1, dtype=torch.float64, device=dev)
     infos = torch.zeros((max(steps, 1), 2), dtype=torch.int32, device=dev)

@@ -55,7 +55,8 @@ def cfg2(steps):
     cfg = implicit.ALSStepConfig(dt=w["dt"], eps_tol=0.0, max_sweeps=w["sweeps"], delta_beta=1.0,
                                  schedule="gauss-seidel", lam=w["lam"])
     f0 = cp.CPTensor(S, w["ic"]["factors"])
-    ms, _ = time_it(lambda: implicit.run(f0, pair, cfg, steps))
+    ws = implicit.StepWorkspace(pair, cfg)
+    ms, _ = time_it(lambda: implicit.run(f0, pair, cfg, steps, workspace=ws))
     print(f"cfg2: {steps} steps in {ms:.1f} ms -> {steps / ms * 1e3:.2f} steps/s", flush=True)
 
 
@@ -66,4 +67,4 @@ if __name__ == "__main__":
     if "cfg3" in which:
         cfg3(50)
     if "cfg2" in which:
-        cfg2(1)
+        cfg2(3)
