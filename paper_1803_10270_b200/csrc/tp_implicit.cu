@@ -30,6 +30,8 @@ struct HArgs {
   int d, ra, r, q, n_tab, nX;
   int tab[IM_MAXD * IM_MAXRA * IM_MAXRA];
   int xs[IM_MAXT];           // distinct table ids used by mode q
+  short pbeg[IM_MAXT + 1];   // term pairs (e, z) of mode q grouped by table: pairs[pbeg[x] .. pbeg[x+1])
+  short pairs[IM_MAXRA * IM_MAXRA];   // e * ra + z
   double KL[IM_MAXRA * IM_MAXRA], KR[IM_MAXRA * IM_MAXRA];
   const double* G;           // [d][n_tab][r][r]
   const double* Gm;          // [d][n_tab][r][r]
@@ -39,22 +41,25 @@ struct HArgs {
 
 // H and Hg for the distinct tables of mode q: one CTA per distinct table
 __global__ void __launch_bounds__(256) form_h_kernel(const __grid_constant__ HArgs a) {
-  const int x = blockIdx.x, X = a.xs[x], r = a.r, rr = r * r;
+  const int x = blockIdx.x, r = a.r, rr = r * r;
   for (int e2 = threadIdx.x; e2 < rr; e2 += 256) {
     double h = 0.0, hg = 0.0;
-    for (int e = 0; e < a.ra; ++e)
-      for (int z = 0; z < a.ra; ++z) {
-        if (a.tab[(a.q * a.ra + e) * a.ra + z] != X) continue;
-        double p = 1.0, pg = 1.0;
-        for (int k = 0; k < a.d; ++k) {
-          if (k == a.q) continue;
-          const int t = a.tab[(k * a.ra + e) * a.ra + z];
-          p *= a.G[((size_t)k * a.n_tab + t) * rr + e2];
-          pg *= a.Gm[((size_t)k * a.n_tab + t) * rr + e2];
-        }
-        h += a.KL[e * a.ra + z] * p;
-        hg += a.KR[e * a.ra + z] * pg;
+    for (int pi = a.pbeg[x]; pi < a.pbeg[x + 1]; ++pi) {   // only the pairs that map to table x
+      const int ez = a.pairs[pi], e = ez / a.ra, z = ez - e * a.ra;
+      double g[IM_MAXD], gm[IM_MAXD];
+#pragma unroll
+      for (int k = 0; k < IM_MAXD; ++k) {
+        const bool use = k < a.d && k != a.q;
+        const int t = use ? a.tab[(k * a.ra + e) * a.ra + z] : 0;
+        g[k] = use ? __ldg(a.G + ((size_t)k * a.n_tab + t) * rr + e2) : 1.0;
+        gm[k] = use ? __ldg(a.Gm + ((size_t)k * a.n_tab + t) * rr + e2) : 1.0;
       }
+      double p = 1.0, pg = 1.0;
+#pragma unroll
+      for (int k = 0; k < IM_MAXD; ++k) { p *= g[k]; pg *= gm[k]; }
+      h += a.KL[e * a.ra + z] * p;
+      hg += a.KR[e * a.ra + z] * pg;
+    }
     a.H[(size_t)x * rr + e2] = h;     // e2 = j*r + i : H_X[j][i]
     a.Hg[(size_t)x * rr + e2] = hg;   // e2 = i*r + j : Hg_X[i][j]
   }
@@ -358,21 +363,36 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
 }
 
 // beta_q[c][j] = Re sum_k xhat[j][k] e^{+2 pi i c k / Q} / sqrt(Q)
+// 8 lanes per output (frequencies k = part + 8 t, index m = c k mod Q stepped
+// incrementally), fixed-order shuffle reduction
 __global__ void circ_idft_kernel(int Q, int r, const double* xhat, const double* tw, double* beta_q, int* info) {
   const int n = Q * r;
   const double inv_sqrt = rsqrt((double)Q);
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-    const int c = e / r, j = e % r;
-    double acc = 0.0;
-    for (int k = 0; k < Q; ++k) {
-      const int m = (int)(((long long)c * k) % Q);
-      const double* xh = xhat + ((size_t)j * Q + k) * 2;
-      acc = fma(xh[0], tw[2 * m], acc);
-      acc = fma(-xh[1], tw[2 * m + 1], acc);
+  const int lanes = gridDim.x * blockDim.x;
+  for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 - (threadIdx.x & 7) < 8 * n; t0 += lanes) {
+    const int e = t0 >> 3, part = t0 & 7;
+    const bool act = e < n;
+    const int c = act ? e / r : 0, j = act ? e - c * r : 0;
+    double a0 = 0.0, a1 = 0.0;
+    if (act) {
+      const int step = (8 * c) % Q;
+      int m = (c * part) % Q;
+      for (int k = part; k < Q; k += 8) {
+        const double* xh = xhat + ((size_t)j * Q + k) * 2;
+        a0 = fma(xh[0], tw[2 * m], a0);
+        a1 = fma(-xh[1], tw[2 * m + 1], a1);
+        m += step;
+        if (m >= Q) m -= Q;
+      }
     }
-    acc *= inv_sqrt;
-    if (!isfinite(acc)) atomicOr(info, 2);
-    beta_q[e] = acc;
+    double acc = a0 + a1;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (act && part == 0) {
+      acc *= inv_sqrt;
+      if (!isfinite(acc)) atomicOr(info, 2);
+      beta_q[e] = acc;
+    }
   }
 }
 
@@ -553,6 +573,15 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     for (int q = 0; q < d; ++q) {
       ha.q = q; ha.nX = (int)used[q].size();
       for (int i = 0; i < ha.nX; ++i) ha.xs[i] = used[q][i];
+      {
+        int np = 0;
+        for (int i = 0; i < ha.nX; ++i) {
+          ha.pbeg[i] = (short)np;
+          for (int ez = 0; ez < ra * ra; ++ez)
+            if (tab_id[q * ra * ra + ez] == used[q][i]) ha.pairs[np++] = (short)ez;
+        }
+        ha.pbeg[ha.nX] = (short)np;
+      }
       double* dst = (schedule == 0 ? f_new : bjac) + (size_t)q * QR;
       if (circ_eig) {
         CircArgs ca;
@@ -569,7 +598,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
         const size_t csm = sizeof(double) * (2 * (size_t)r * (r + 1) + 2 * r);
         cudaFuncSetAttribute(circ_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
         circ_solve_kernel<<<Q, 256, csm, st>>>(ca);
-        circ_idft_kernel<<<(int)((QR + 255) / 256), 256, 0, st>>>(Q, r, xhat, tw, dst, info);
+        circ_idft_kernel<<<(int)((8 * QR + 255) / 256), 256, 0, st>>>(Q, r, xhat, tw, dst, info);
       } else {
       form_h_kernel<<<ha.nX, 256, 0, st>>>(ha);
       gamma_kernel<<<(n + 255) / 256, 256, 0, st>>>(Q, r, ha.nX, xs_modes + (size_t)q * IM_MAXT, Hg, W, n_tab, q, gam, n);
