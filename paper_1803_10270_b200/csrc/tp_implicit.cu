@@ -286,17 +286,28 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
   const double* Hs = a.H;                 // [nX][r][r]  H_X[j][i] (form_h_kernel)
   const double* gam = a.gam;              // [r][Q]  (gamma_kernel)
   const double inv_sqrt = rsqrt((double)Q);
-  // gamma^(k)_i = sum_a gamma[i][a] e^{-2 pi i a k / Q} / sqrt(Q)
-  for (int i = tid; i < r; i += 256) {
+  // gamma^(k)_i = sum_a gamma[i][a] e^{-2 pi i a k / Q} / sqrt(Q): 16 lanes per i,
+  // a = part + 16 t with the twiddle index stepped incrementally, shuffle reduction
+  for (int base = 0; base < 16 * r; base += 256) {
+    const int t = base + tid, i = t >> 4, part = t & 15;
     double re = 0.0, im = 0.0;
-    for (int aa = 0; aa < Q; ++aa) {
-      const int m = (int)(((long long)aa * k) % Q);
-      const double g = gam[(size_t)i * Q + aa];
-      re = fma(g, a.tw[2 * m], re);
-      im = fma(-g, a.tw[2 * m + 1], im);
+    if (i < r) {
+      const int step = (16 * k) % Q;
+      int m = (part * k) % Q;
+      for (int aa = part; aa < Q; aa += 16) {
+        const double g = gam[(size_t)i * Q + aa];
+        re = fma(g, a.tw[2 * m], re);
+        im = fma(-g, a.tw[2 * m + 1], im);
+        m += step;
+        if (m >= Q) m -= Q;
+      }
     }
-    gre[i] = re * inv_sqrt;
-    gim[i] = im * inv_sqrt;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, o);
+      im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (i < r && part == 0) { gre[i] = re * inv_sqrt; gim[i] = im * inv_sqrt; }
   }
   for (int e = tid; e < r * r; e += 256) {
     const int i = e / r, j = e % r;
@@ -333,26 +344,39 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
     __syncthreads();
   }
   if (bad && tid == 0) atomicOr(a.info, 1);
-  if (tid == 0) {
+  if (tid < 32) {   // one warp: per row the dot product over the lanes, then the pivot divide
+    const int lane = tid;
     for (int i = 0; i < r; ++i) {            // L y = g
-      double re = gre[i], im = gim[i];
-      for (int c = 0; c < i; ++c) {
+      double re = 0.0, im = 0.0;
+      for (int c = lane; c < i; c += 32) {
         const double lr = Mre[i * ld + c], li = Mim[i * ld + c];
-        re -= lr * gre[c] - li * gim[c];
-        im -= lr * gim[c] + li * gre[c];
+        re += lr * gre[c] - li * gim[c];
+        im += lr * gim[c] + li * gre[c];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
       }
       const double dd = Mre[i * ld + i];
-      gre[i] = re / dd; gim[i] = im / dd;
+      if (lane == 0) { gre[i] = (gre[i] - re) / dd; gim[i] = (gim[i] - im) / dd; }
+      __syncwarp();
     }
     for (int i = r - 1; i >= 0; --i) {       // L^H x = y
-      double re = gre[i], im = gim[i];
-      for (int c = i + 1; c < r; ++c) {      // conj(L[c][i]) x_c
+      double re = 0.0, im = 0.0;
+      for (int c = i + 1 + lane; c < r; c += 32) {   // conj(L[c][i]) x_c
         const double lr = Mre[c * ld + i], li = -Mim[c * ld + i];
-        re -= lr * gre[c] - li * gim[c];
-        im -= lr * gim[c] + li * gre[c];
+        re += lr * gre[c] - li * gim[c];
+        im += lr * gim[c] + li * gre[c];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
       }
       const double dd = Mre[i * ld + i];
-      gre[i] = re / dd; gim[i] = im / dd;
+      if (lane == 0) { gre[i] = (gre[i] - re) / dd; gim[i] = (gim[i] - im) / dd; }
+      __syncwarp();
     }
   }
   __syncthreads();
