@@ -308,11 +308,29 @@ def gen_implicit():
     np.savez_compressed(OUT / "implicit.npz", **store)
 
 
+def gen_io():
+    """Reference-written tensor files (io.save_tensor, io.py:55-71) + their decoded arrays."""
+    from tensorpde import io as rio
+    rng = np.random.default_rng(17)
+    specs = (BasisSpec(5, 1.5), BasisSpec(7, 2.0), BasisSpec(3, 1.0))
+    f = real_cp(specs, 3, rng)
+    rio.save_tensor(OUT / "io_cp.tensor", f)
+    store = {}
+    pack_cp("cp", f, store)
+    specs4 = (BasisSpec(5, 1.5), BasisSpec(3, 2.0), BasisSpec(7, 1.0), BasisSpec(5, 2.5))
+    h = ht.from_cp(real_cp(specs4, 2, rng))
+    h, _ = ht.truncate(ht.add(h, h), r_max=3, eps=1e-14)     # node ranks vary (reference test_io.py:46-50)
+    rio.save_tensor(OUT / "io_ht.tensor", h)
+    pack_ht("ht", h, store)
+    np.savez_compressed(OUT / "io.npz", **store)
+
+
+GENERATORS = {"cp_als": lambda: gen_cp_als(), "ht": lambda: gen_ht(), "operators": lambda: gen_operators(),
+              "explicit": lambda: gen_explicit(), "implicit": lambda: gen_implicit(), "io": lambda: gen_io()}
+
+
 if __name__ == "__main__":
-    gen_cp_als()
-    gen_ht()
-    gen_operators()
-    gen_explicit()
-    gen_implicit()
+    for name in (sys.argv[1:] or list(GENERATORS)):
+        GENERATORS[name]()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
