@@ -1458,7 +1458,7 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
   int P = grid;
   if (P <= 0) {
     double work = 4.0 * qmax * (double)R * r;   // flops of one mode update
-    P = (int)(work / 2.0e5);
+    P = (int)(work / 5.0e4);   // measured: cfg3 (R=588, r=12) best at >= 32 CTAs, cfg0 at 1
     if (P < 1) P = 1;
   }
   if (P > nsm) P = nsm;
@@ -1491,7 +1491,7 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
   pl.ws_total = ws_total_for(d, q, r, P, pl.ydoubles, pl.ws_inner);
   (void)oup;
   // large truncations: the cluster variant (fewer bytes per CTA per mode update)
-  const bool want = g_variant == 2 || (g_variant == 0 && grid <= 0 && P >= 32 && g_cluster >= 0);
+  const bool want = g_variant == 2 || (g_variant == 0 && grid <= 0 && P >= 64 && g_cluster >= 0);
   if (want) {
     AlsPlan cp = pl;
     const int sizes[3] = {8, 4, 2};
