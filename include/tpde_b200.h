@@ -103,6 +103,17 @@ int tp_als_shard_update_f64(int d, const int* q, int Rl, const double* V, int r,
                             size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Weight contractions (SURVEY 8(f) f3 device diagnostics): for weight sets
+ * W[w] = (W[w][0] | ... | W[w][d-1]) of length sum_k Q_k,
+ *   out[w] = sum_l prod_k W[w][k] . F_k[:, l]
+ * cp.evaluate (cp.py:84-95: W = basis values at a point) and the moment
+ * contractions of diagnostics.moments (diagnostics.py:60-64: W = integration
+ * weights).  W and out are device arrays.
+ * ------------------------------------------------------------------------- */
+int tp_cp_contract_f64(int d, const int* q, int R, const double* F, int nw, const double* W, double* out,
+                       void* stream);
+
+/* ---------------------------------------------------------------------------
  * Separable operator apply + concatenation (operators.apply,
  * operators.py:48-62; cp.add/scale, cp.py:98-108).
  * For each term t (0..n_terms-1) and mode k, writes

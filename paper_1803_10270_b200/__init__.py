@@ -14,6 +14,7 @@ from .cp import (ALSApproxConfig, CPTensor, add, cp_approx_als, inner_product, n
                  random_cp, rank_reduce_als, scale)
 from .ht import DimensionTree, HTTensor, balanced_tree, from_cp, truncate, truncate_batch
 from .io import load_tensor, save_tensor
+from . import diagnostics
 from .operators import (CrankNicolsonPair, SeparableOperator, advection_operator, apply,
                         crank_nicolson_pair, implicit_euler_pair)
 
@@ -26,6 +27,6 @@ __all__ = [
     "SeparableOperator", "CrankNicolsonPair", "advection_operator", "apply", "crank_nicolson_pair",
     "implicit_euler_pair",
     "HTTensor", "DimensionTree", "balanced_tree", "from_cp", "truncate", "truncate_batch",
-    "save_tensor", "load_tensor",
+    "save_tensor", "load_tensor", "diagnostics",
     "__version__",
 ]

@@ -23,7 +23,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["BasisSpec", "FactorKind", "factor_matrix", "fourier_diff_matrix", "nodes"]
+__all__ = ["quadrature_weights", "interpolation_weights", "BasisSpec", "FactorKind", "factor_matrix", "fourier_diff_matrix", "nodes"]
 
 
 class FactorKind(enum.Enum):
@@ -119,3 +119,56 @@ def factor_matrix(spec: BasisSpec, kind: FactorKind) -> np.ndarray:
     if kind is FactorKind.COORD_MULTIPLY:
         return np.diag(x)
     return np.diag(x) @ D
+
+
+def quadrature_weights(spec: BasisSpec, p: int) -> np.ndarray:
+    """Nodal counterpart of ``integration_weights`` (basis.py:159-165): weights w with
+    w . f ~ Int z^p f(z) dz for nodal values f.  Periodic collocation grids use the
+    trapezoid rule (spectrally accurate for smooth periodic integrands), uniform
+    grids on [-b, b] the composite trapezoid rule with half end weights."""
+    if p not in (0, 1, 2):
+        raise ValueError("moment power must be 0, 1 or 2")
+    if spec.kind == "fourier":
+        raise ValueError("the complex Galerkin basis is outside the real-fp64 device path")
+    x = nodes(spec)
+    if spec.kind == "collocation":
+        w = np.full(spec.Q, 2.0 * spec.b / spec.Q)
+    else:
+        h = 2.0 * spec.b / (spec.Q - 1) if spec.Q > 1 else 2.0 * spec.b
+        w = np.full(spec.Q, h)
+        if spec.Q > 1:
+            w[0] = w[-1] = 0.5 * h
+    return w * x ** p
+
+
+def interpolation_weights(spec: BasisSpec, z) -> np.ndarray:
+    """Rows v(z) with v(z) . f = the grid function's interpolant at z (the nodal
+    counterpart of ``eval_basis``, basis.py:74-94): trigonometric interpolation on
+    periodic collocation grids (band-limited, Nyquist mode as a cosine), piecewise
+    linear on uniform grids."""
+    z = np.atleast_1d(np.asarray(z, dtype=float))
+    if spec.kind == "fourier":
+        raise ValueError("the complex Galerkin basis is outside the real-fp64 device path")
+    Q = spec.Q
+    x = nodes(spec)
+    if spec.kind == "uniform":
+        out = np.zeros((z.size, Q))
+        if Q == 1:
+            out[:, 0] = 1.0
+            return out
+        h = x[1] - x[0]
+        t = np.clip((z - x[0]) / h, 0.0, Q - 1.0)
+        i = np.minimum(np.floor(t).astype(int), Q - 2)
+        fr = t - i
+        out[np.arange(z.size), i] = 1.0 - fr
+        out[np.arange(z.size), i + 1] = fr
+        return out
+    L = 2.0 * spec.b
+    theta = 2.0 * np.pi * (z[:, None] - x[None, :]) / L          # (m, Q)
+    kmax = (Q - 1) // 2
+    acc = np.ones_like(theta)
+    for m in range(1, kmax + 1):
+        acc += 2.0 * np.cos(m * theta)
+    if Q % 2 == 0:
+        acc += np.cos((Q // 2) * theta)
+    return acc / Q

@@ -190,6 +190,46 @@ __global__ void __launch_bounds__(256) cp_apply_kernel(const __grid_constant__ A
 
 using namespace tp;
 
+// Weight contractions of a CP tensor (moments, point evaluation):
+//   out[w] = sum_l prod_k ( W[w][k] . F_k[:, l] )
+// (cp.py:84-95 evaluate with basis values as W; diagnostics.py:60-64 _contract with
+// integration weights).  One CTA per weight set, terms over the threads, W staged
+// in shared memory, fixed-order block reduction.
+constexpr int CT_NT = 256;
+
+struct QOff { int v[TP_MAXD + 1]; };
+
+__global__ void __launch_bounds__(CT_NT) cp_contract_kernel(int d, const __grid_constant__ QOff qo_, int sumq, int R,
+                                                            const double* __restrict__ F,
+                                                            const double* __restrict__ W, double* out) {
+  extern __shared__ double ws_[];
+  double* w = ws_;                 // [sumq]
+  double* red = ws_ + sumq;        // [CT_NT]
+  const int* qo = qo_.v;
+  const int wi = blockIdx.x, tid = threadIdx.x;
+  for (int e = tid; e < sumq; e += CT_NT) w[e] = W[(size_t)wi * sumq + e];
+  __syncthreads();
+  double acc = 0.0;
+  for (int l = tid; l < R; l += CT_NT) {
+    double prod = 1.0;
+    for (int k = 0; k < d; ++k) {
+      const int q0 = qo[k], Q = qo[k + 1] - q0;
+      const double* Fk = F + (size_t)q0 * R + l;   // mode k block is (Q_k, R) row-major at R * q0
+      double dot = 0.0;
+      for (int s = 0; s < Q; ++s) dot = fma(w[q0 + s], Fk[(size_t)s * R], dot);
+      prod *= dot;
+    }
+    acc += prod;
+  }
+  red[tid] = acc;
+  __syncthreads();
+  for (int h = CT_NT / 2; h > 0; h >>= 1) {
+    if (tid < h) red[tid] += red[tid + h];
+    __syncthreads();
+  }
+  if (tid == 0) out[wi] = red[0];
+}
+
 extern "C" {
 
 const char* tp_version(void) { return "tpde_b200 0.1.0 (sm_100a)"; }
@@ -266,4 +306,24 @@ int tp_cp_apply_f64(int d, const int* q, int r_in, const double* F, int n_terms,
   return cuda_status(cudaGetLastError());
 }
 
+
+int tp_cp_contract_f64(int d, const int* q, int R, const double* F, int nw, const double* W, double* out,
+                       void* stream) {
+  if (d < 1 || d > TP_MAXD || R < 1 || nw < 0 || !q || !F || !out || (nw > 0 && !W)) return TP_EINVAL;
+  QOff qo;
+  qo.v[0] = 0;
+  for (int k = 0; k < d; ++k) {
+    if (q[k] < 1) return TP_EINVAL;
+    qo.v[k + 1] = qo.v[k] + q[k];
+  }
+  if (nw == 0) return TP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = sizeof(double) * ((size_t)qo.v[d] + CT_NT);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(cp_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  cp_contract_kernel<<<nw, CT_NT, smem, st>>>(d, qo, qo.v[d], R, F, W, out);
+  return cuda_status(cudaGetLastError());
+}
 }  // extern "C"

@@ -325,8 +325,34 @@ def gen_io():
     np.savez_compressed(OUT / "io.npz", **store)
 
 
+def gen_diagnostics():
+    """Reference diagnostics on fixed inputs (diagnostics.py:31-143)."""
+    from tensorpde import diagnostics as rdiag
+    from tensorpde import models
+    from tensorpde.basis import integration_weights
+    store = {}
+    rng = np.random.default_rng(23)
+    x, y = rng.standard_normal(50), rng.standard_normal(50)
+    store["nmae_x"], store["nmae_y"], store["nmae"] = x, y, rdiag.nmae(x, y)
+    t = np.linspace(0.0, 4.0, 30)
+    series = 3.0 * np.exp(-1.7 * t) + 1e-6
+    store["fit_t"], store["fit_series"] = t, series
+    store["fit_rate"] = rdiag.fit_decay_rate(t, series)
+    store["fit_rate_floor"] = rdiag.fit_decay_rate(t, series, floor=1e-6)
+    spec = models.BGKSpec(Q=11)
+    f = models.maxwellian_cp(spec)
+    rep = rdiag.moments(f, spec)
+    pack_cp("mw", f, store)
+    for p in (0, 1, 2):
+        store[f"mw_w{p}"] = np.stack([integration_weights(s, p) for s in f.specs])
+    store["mw_R"] = spec.R
+    store["mw_out"] = np.concatenate([[rep.mean_density], rep.mean_velocity, [rep.mean_temperature]])
+    np.savez_compressed(OUT / "diagnostics.npz", **store)
+
+
 GENERATORS = {"cp_als": lambda: gen_cp_als(), "ht": lambda: gen_ht(), "operators": lambda: gen_operators(),
-              "explicit": lambda: gen_explicit(), "implicit": lambda: gen_implicit(), "io": lambda: gen_io()}
+              "explicit": lambda: gen_explicit(), "implicit": lambda: gen_implicit(), "io": lambda: gen_io(),
+              "diagnostics": lambda: gen_diagnostics()}
 
 
 if __name__ == "__main__":
