@@ -26,9 +26,18 @@ struct BGemm {
   double* part;              // [nb1*nb2][ksplit][M][N] partials when ksplit > 1
 };
 
+// 8-byte global -> shared async copy (LDGSTS); src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(valid ? src : nullptr), "r"(valid ? 8 : 0)
+               : "memory");
+}
+
 static __global__ void __launch_bounds__(128) bgemm_kernel(const __grid_constant__ BGemm g) {
-  __shared__ double As[GB_TK][GB_LD];
-  __shared__ double Bs[GB_TK][GB_LD];
+  // two-stage cp.async pipeline: K tile t+1 streams into the other buffer while
+  // tile t is multiplied on the DMMA pipe
+  __shared__ double As[2][GB_TK][GB_LD];
+  __shared__ double Bs[2][GB_TK][GB_LD];
   const int ks = g.ksplit > 1 ? g.ksplit : 1;
   const int zz = blockIdx.z / ks, sidx = blockIdx.z - zz * ks;
   const int z1 = zz / g.nb2, z2 = zz % g.nb2;
@@ -53,34 +62,50 @@ static __global__ void __launch_bounds__(128) bgemm_kernel(const __grid_constant
   // split-K range of this CTA (whole GB_TK tiles)
   const int ktiles = (g.K + GB_TK - 1) / GB_TK, kt0 = (int)((long long)ktiles * sidx / ks),
             kt1 = (int)((long long)ktiles * (sidx + 1) / ks);
-  for (int k0 = kt0 * GB_TK; k0 < kt1 * GB_TK; k0 += GB_TK) {
-    __syncthreads();
+  auto issue = [&](int kt, int buf) {
+    const int k0 = kt * GB_TK;
+#pragma unroll 2
     for (int e = tid; e < GB_TK * GB_TM; e += 128) {
       int kk, mm;
       if (a_m_fast) { kk = e / GB_TM; mm = e % GB_TM; } else { mm = e / GB_TK; kk = e % GB_TK; }
       const int m = m0 + mm, k = k0 + kk;
-      As[kk][mm] = (m < g.M && k < g.K) ? A[m * g.sAm + k * g.sAk] : 0.0;
+      const bool v = m < g.M && k < g.K;
+      cp_async8(&As[buf][kk][mm], A + (v ? m * g.sAm + k * g.sAk : 0), v);
     }
+#pragma unroll 2
     for (int e = tid; e < GB_TK * GB_TN; e += 128) {
       int kk, nn;
       if (b_n_fast) { kk = e / GB_TN; nn = e % GB_TN; } else { nn = e / GB_TK; kk = e % GB_TK; }
       const int n = n0 + nn, k = k0 + kk;
-      Bs[kk][nn] = (n < g.N && k < g.K) ? B[k * g.sBk + n * g.sBn] : 0.0;
+      const bool v = n < g.N && k < g.K;
+      cp_async8(&Bs[buf][kk][nn], B + (v ? k * g.sBk + n * g.sBn : 0), v);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if (kt0 < kt1) issue(kt0, 0);
+  for (int kt = kt0; kt < kt1; ++kt) {
+    const int buf = (kt - kt0) & 1;
+    if (kt + 1 < kt1) {
+      issue(kt + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
 #pragma unroll
-    for (int ks = 0; ks < GB_TK; ks += 4) {
-      const int kr = ks + (lane & 3), cc = lane >> 2;
+    for (int ksub = 0; ksub < GB_TK; ksub += 4) {
+      const int kr = ksub + (lane & 3), cc = lane >> 2;
       double fa[4], fb[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) fa[i] = As[kr][wm + 8 * i + cc];
+      for (int i = 0; i < 4; ++i) fa[i] = As[buf][kr][wm + 8 * i + cc];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) fb[j] = Bs[kr][wn + 8 * j + cc];
+      for (int j = 0; j < 4; ++j) fb[j] = Bs[buf][kr][wn + 8 * j + cc];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
     }
+    __syncthreads();   // buffer `buf` is refilled by the next iteration's issue
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
