@@ -273,6 +273,10 @@ __device__ void gram_share(const AlsArgs& a, const Smem& sm, int k) {
       if (orow < r && ocol < r) {
         Gk[orow * r + ocol] = acc;
         Gk[ocol * r + orow] = acc;
+        if (gridDim.x == 1) {   // single CTA: no global round trip for its own Gram
+          sm.Gs[(size_t)k * r * r + orow * r + ocol] = acc;
+          sm.Gs[(size_t)k * r * r + ocol * r + orow] = acc;
+        }
       }
     }
   }
@@ -625,13 +629,18 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   double prev = INFINITY;
   int pending = -1, done = 0, rows_mode = -1, rows_sweep = 0;
   const bool bulk = (r & 1) == 0;
+  // single-CTA grid: the right-hand side, the Gram and the new factor stay in
+  // shared memory (no Y / G / U round trips through global memory)
+  const bool local = P == 1;
+  bool staged = false;     // local: sm.Us already holds the pending factor (padded rows)
 
   for (int sweep = 0; sweep < a.sweeps; ++sweep) {
     for (int j = 0; j < a.d; ++j) {
       // ---------------- phase A
       PROF(0);
       if (pending >= 0) {
-        if (!(a.dbg_skip & 2)) stage_u(a, sm, pending, bphase);
+        if (!(a.dbg_skip & 2) && !staged) stage_u(a, sm, pending, bphase);
+        staged = false;
         PROF(10);
         if (!(a.dbg_skip & 4)) cross_slab<RM>(a, sm, pending, w);
         PROF(11);
@@ -640,6 +649,12 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       if (rows_mode >= 0) {   // warm-start rows of the previous NS solve
         ns_rows<RM>(a, sm, rows_mode, rows_sweep);
         rows_mode = -1;
+      }
+      const bool warm_ns = sweep > 0 && a.ns_max > 0;
+      if (local && warm_ns && bulk && tid == 0) {   // prefetch this mode's warm start under phase A
+        fence_proxy_async();
+        mbar_arrive_expect_tx(sm.bar + 1, (uint32_t)(r * rh) * 8u);
+        bulk_g2s(sm.X0, a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh, (uint32_t)(r * rh) * 8u, sm.bar + 1);
       }
       PROF(1);
       const int Qj = a.q[j], qsj = a.qs[j];
@@ -668,7 +683,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
           const bool srow = s < Qj;
           const int rm = srow ? sm.rowmap[j * a.qmax + s] : 0;
           const int pc = rm >> 16, ii = rm & 0xffff;
-          double* yrow = a.Y + (((size_t)pc * P + p) * a.ncolmax + ii) * r;
+          double* yrow = local ? sm.rb + (size_t)s * r : a.Y + (((size_t)pc * P + p) * a.ncolmax + ii) * r;
           double acc[NT][2];
 #pragma unroll
           for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
@@ -706,8 +721,14 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       const int ncol = s1 - s0, E = ncol * r;
       const int nb = a.ncolmax * r;     // one producer's block for this consumer
       double* ystage = sm.Us;           // [q][nb]
-      const bool warm_ns = sweep > 0 && a.ns_max > 0;
-      if (bulk) {
+      if (local) {
+        if (warm_ns && bulk) { mbar_wait(sm.bar + 1, gphase); gphase ^= 1u; }
+        if (warm_ns && !bulk)   // odd r: shared rows not 16-byte aligned for the bulk copy
+          for (int e = tid; e < r * rh; e += ALS_NT)
+            sm.X0[e] = __ldcg(a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh + e);
+        __syncthreads();                // sm.rb (right-hand side) and sm.Gs complete
+        if (warm_ns) build_a<RM>(a, sm, j);
+      } else if (bulk) {
         if (tid == 0) {
           const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
           const uint32_t ybytes = (E > 0 && !(a.dbg_skip & 32)) ? (uint32_t)(P * nb) * 8u : 0u;
@@ -767,8 +788,10 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
           if (!isfinite(v)) nf = 1;
           Uj[(size_t)(s0 + sc) * r + i] = v;
           Up[(size_t)(s0 + sc) * rh + i] = v;
+          if (local) sm.Us[(size_t)(s0 + sc) * rh + i] = v;   // next phase A reads it in place
         }
         if (nf) atomicOr(a.info, 2);
+        if (local) staged = true;   // (cross_slab / gram_share guard the K range: no padding rows)
       }
       pending = j;
       PROF(6);
