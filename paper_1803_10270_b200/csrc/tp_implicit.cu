@@ -270,6 +270,9 @@ struct CircArgs {
   const double* eig;    // [n_tab][Q][2]
   const double* gam;    // [r][Q] (index i*Q + a)
   const double* tw;     // [Q][2]: cos, sin of 2 pi m / Q
+  const double* Hg;     // [nX][r][r] Hg_X[i][j] (form_h_kernel)
+  const double* bho;    // [Q][r][2] DFT of b_old for mode q (unnormalised)
+  int conj_tilde;       // 1: T~ = T^T (eigenvalues conj(lambda)), 0: T~ = T
   double* xhat;         // [r][Q][2]
   double lam;
   int* info;
@@ -284,22 +287,26 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
   double* gre = Mim + r * ld;             // [r]
   double* gim = gre + r;
   const double* Hs = a.H;                 // [nX][r][r]  H_X[j][i] (form_h_kernel)
-  const double* gam = a.gam;              // [r][Q]  (gamma_kernel)
   const double inv_sqrt = rsqrt((double)Q);
-  // gamma^(k)_i = sum_a gamma[i][a] e^{-2 pi i a k / Q} / sqrt(Q): 16 lanes per i,
-  // a = part + 16 t with the twiddle index stepped incrementally, shuffle reduction
+  // gamma^(k)_i = DFT_k(gamma_i) / sqrt(Q) straight from the Fourier coefficients of
+  // b_old (gamma = sum_X Hg_X (T~_X b_old)^T, T~_X circulant -> lambda~_X(k)):
+  //   gamma^(k)_i = sum_X sum_j Hg_X[i][j] lambda~_X(k) bo^(k)_j / sqrt(Q); 16 lanes per i
   for (int base = 0; base < 16 * r; base += 256) {
     const int t = base + tid, i = t >> 4, part = t & 15;
     double re = 0.0, im = 0.0;
     if (i < r) {
-      const int step = (16 * k) % Q;
-      int m = (part * k) % Q;
-      for (int aa = part; aa < Q; aa += 16) {
-        const double g = gam[(size_t)i * Q + aa];
-        re = fma(g, a.tw[2 * m], re);
-        im = fma(-g, a.tw[2 * m + 1], im);
-        m += step;
-        if (m >= Q) m -= Q;
+      for (int x = 0; x < a.nX; ++x) {
+        const double* lm = a.eig + ((size_t)a.xs[x] * Q + k) * 2;
+        const double lr = lm[0], li = a.conj_tilde ? -lm[1] : lm[1];
+        double sr = 0.0, si = 0.0;
+        for (int j = part; j < r; j += 16) {
+          const double h = a.Hg[((size_t)x * r + i) * r + j];
+          const double br = a.bho[((size_t)k * r + j) * 2], bi = a.bho[((size_t)k * r + j) * 2 + 1];
+          sr = fma(h, br, sr);
+          si = fma(h, bi, si);
+        }
+        re += lr * sr - li * si;
+        im += lr * si + li * sr;
       }
     }
 #pragma unroll
@@ -386,6 +393,88 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
   }
 }
 
+// Unnormalised DFT of the columns of a real Q x r factor: out[k][l][2] =
+// sum_s b[s][l] e^{-2 pi i s k / Q}; 8 lanes per output (as circ_idft_kernel)
+__global__ void dft_cols_kernel(int Q, int r, const double* b, const double* tw, double* out) {
+  const int n = Q * r;
+  const int lanes = gridDim.x * blockDim.x;
+  for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 - (threadIdx.x & 7) < 8 * n; t0 += lanes) {
+    const int e = t0 >> 3, part = t0 & 7;
+    const bool act = e < n;
+    const int k = act ? e / r : 0, l = act ? e - k * r : 0;
+    double re = 0.0, im = 0.0;
+    if (act) {
+      const int step = (8 * k) % Q;
+      int m = (k * part) % Q;
+      for (int s2 = part; s2 < Q; s2 += 8) {
+        const double v = b[(size_t)s2 * r + l];
+        re = fma(v, tw[2 * m], re);
+        im = fma(-v, tw[2 * m + 1], im);
+        m += step;
+        if (m >= Q) m -= Q;
+      }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, o);
+      im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (act && part == 0) { out[(size_t)e * 2] = re; out[(size_t)e * 2 + 1] = im; }
+  }
+}
+
+// Grams of mode k for its circulant tables from Fourier coefficients (Parseval):
+//   G[k][t][l][m]  = (1/Q) Re sum_f conj(bn^(f)_l) lambda_t(f)  bn^(f)_m
+//   Gm[k][t][l][m] = (1/Q) Re sum_f conj(bn^(f)_l) lambda~_t(f) bo^(f)_m
+// grid (tables, 2): y = 0 -> G, y = 1 -> Gm.  Replaces T_t b and b^T (T b) GEMMs.
+struct FGramArgs {
+  int Q, r, k, n_tab, conj_tilde;
+  int ts[IM_MAXT];
+  const double* eig;   // [n_tab][Q][2]
+  const double* bn;    // [Q][r][2]
+  const double* bo;    // [Q][r][2]
+  double* G;
+  double* Gm;
+};
+
+__global__ void __launch_bounds__(256) fourier_grams_kernel(const __grid_constant__ FGramArgs a) {
+  extern __shared__ double fg[];
+  const int Q = a.Q, r = a.r, t = a.ts[blockIdx.x], mixed = blockIdx.y, tid = threadIdx.x;
+  double* x = fg;                       // [Q][r][2]  bn
+  double* y = x + (size_t)Q * r * 2;    // [Q][r][2]  bn or bo
+  double* lam = y + (size_t)Q * r * 2;  // [Q][2]
+  const double* ysrc = mixed ? a.bo : a.bn;
+  for (int e = tid; e < Q * r * 2; e += 256) { x[e] = a.bn[e]; y[e] = ysrc[e]; }
+  for (int f = tid; f < Q; f += 256) {
+    lam[2 * f] = a.eig[((size_t)t * Q + f) * 2];
+    const double li = a.eig[((size_t)t * Q + f) * 2 + 1];
+    lam[2 * f + 1] = (mixed && a.conj_tilde) ? -li : li;
+  }
+  __syncthreads();
+  const double invQ = 1.0 / (double)Q;
+  double* out = (mixed ? a.Gm : a.G) + ((size_t)a.k * a.n_tab + t) * r * r;
+  for (int e = tid; e < r * r; e += 256) {
+    const int l = e / r, m = e - l * r;
+    double s0 = 0.0, s1 = 0.0;
+    for (int f = 0; f < Q; f += 2) {
+      {
+        const double xr = x[((size_t)f * r + l) * 2], xi = x[((size_t)f * r + l) * 2 + 1];
+        const double yr = y[((size_t)f * r + m) * 2], yi = y[((size_t)f * r + m) * 2 + 1];
+        const double pr = lam[2 * f] * yr - lam[2 * f + 1] * yi, pi = lam[2 * f] * yi + lam[2 * f + 1] * yr;
+        s0 += xr * pr + xi * pi;   // Re(conj(x) p)
+      }
+      if (f + 1 < Q) {
+        const int g = f + 1;
+        const double xr = x[((size_t)g * r + l) * 2], xi = x[((size_t)g * r + l) * 2 + 1];
+        const double yr = y[((size_t)g * r + m) * 2], yi = y[((size_t)g * r + m) * 2 + 1];
+        const double pr = lam[2 * g] * yr - lam[2 * g + 1] * yi, pi = lam[2 * g] * yi + lam[2 * g + 1] * yr;
+        s1 += xr * pr + xi * pi;
+      }
+    }
+    out[e] = (s0 + s1) * invQ;
+  }
+}
+
 // beta_q[c][j] = Re sum_k xhat[j][k] e^{+2 pi i c k / Q} / sqrt(Q)
 // 8 lanes per output (frequencies k = part + 8 t, index m = c k mod Q stepped
 // incrementally), fixed-order shuffle reduction
@@ -435,6 +524,7 @@ static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
   s += align_up(8 * (size_t)d * Q * r) * 2;             // b_int, Jacobi staging
   s += align_up(4 * IM_MAXT) + 256 + align_up(8 * 6 * (size_t)d * IM_MAXT);   // + Gram GEMM offset tables
   s += align_up(8 * (size_t)r * Q * 2) + align_up(8 * (size_t)Q * 2);   // circulant: xhat, twiddles
+  s += align_up(8 * (size_t)d * Q * r * 2) + align_up(8 * (size_t)Q * r * 2);   // circulant: DFT(b_old), DFT(b_new)
   return s;
 }
 
@@ -483,6 +573,8 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   int* xs_modes = reinterpret_cast<int*>(Linv + (size_t)(n / CH_NB) * CH_NB * CH_NB);   // spare tail block
   double* xhat = cv.take<double>((size_t)r * Q * 2);
   double* tw = cv.take<double>((size_t)Q * 2);
+  double* bho = cv.take<double>((size_t)d * Q * r * 2);
+  double* bhn = cv.take<double>((size_t)Q * r * 2);
   if (circ_eig) {
     std::vector<double> htw((size_t)Q * 2);
     for (int m = 0; m < Q; ++m) {
@@ -567,9 +659,30 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     if (e == cudaSuccess) e = bgemm_launch(g4, st);
     return e;
   };
+  const size_t fg_smem = sizeof(double) * (4 * QR + 2 * (size_t)Q);
+  const int dft_blocks = (int)((8 * QR + 255) / 256);
+  if (circ_eig) {
+    cudaFuncSetAttribute(fourier_grams_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fg_smem);
+    // DFT of every mode of b_old once per step
+    for (int k = 0; k < d; ++k)
+      dft_cols_kernel<<<dft_blocks, 256, 0, st>>>(Q, r, f_old + (size_t)k * QR, tw, bho + (size_t)k * QR * 2);
+  }
+  // Circulant tables: the Grams of mode k from Fourier coefficients (one DFT of
+  // b_new[k], one launch for G and Gm of all its tables) instead of four GEMMs
+  auto refresh_fourier = [&](int k) -> cudaError_t {
+    dft_cols_kernel<<<dft_blocks, 256, 0, st>>>(Q, r, f_new + (size_t)k * QR, tw, bhn);
+    FGramArgs fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.Q = Q; fa.r = r; fa.k = k; fa.n_tab = n_tab; fa.conj_tilde = tr;
+    for (size_t i = 0; i < used[k].size(); ++i) fa.ts[i] = used[k][i];
+    fa.eig = circ_eig; fa.bn = bhn; fa.bo = bho + (size_t)k * QR * 2; fa.G = G; fa.Gm = Gm;
+    fourier_grams_kernel<<<dim3((unsigned)used[k].size(), 2), 256, fg_smem, st>>>(fa);
+    return cudaGetLastError();
+  };
+  auto refresh_any = [&](int k) -> cudaError_t { return circ_eig ? refresh_fourier(k) : refresh_mode(k); };
   for (int k = 0; k < d; ++k) {
-    if ((err = refresh_mode(k)) != cudaSuccess) return cuda_status(err);
-    if ((err = images(k, f_old, W, tr)) != cudaSuccess) return cuda_status(err);
+    if ((err = refresh_any(k)) != cudaSuccess) return cuda_status(err);
+    if (!circ_eig && (err = images(k, f_old, W, tr)) != cudaSuccess) return cuda_status(err);
   }
   HArgs ha;
   memset(&ha, 0, sizeof(ha));
@@ -616,9 +729,8 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
         for (int i = 0; i < ra * ra; ++i) { ca.KL[i] = KL[i]; ca.KR[i] = KR[i]; }
         ca.G = G; ca.Gm = Gm; ca.W = W;
         ca.H = H; ca.eig = circ_eig; ca.gam = gam; ca.tw = tw; ca.xhat = xhat; ca.lam = lam; ca.info = info;
+        ca.Hg = Hg; ca.bho = bho + (size_t)q * QR * 2; ca.conj_tilde = tr;
         form_h_kernel<<<ha.nX, 256, 0, st>>>(ha);
-        gamma_kernel<<<(n + 255) / 256, 256, 0, st>>>(Q, r, ha.nX, xs_modes + (size_t)q * IM_MAXT, Hg, W, n_tab, q,
-                                                       gam, n);
         const size_t csm = sizeof(double) * (2 * (size_t)r * (r + 1) + 2 * r);
         cudaFuncSetAttribute(circ_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
         circ_solve_kernel<<<Q, 256, csm, st>>>(ca);
@@ -648,7 +760,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
       scatter_x_kernel<<<(int)((QR + 255) / 256), 256, 0, st>>>(Q, r, x, dst, info);
       }
       if (schedule == 0)
-        if ((err = refresh_mode(q)) != cudaSuccess) return cuda_status(err);
+        if ((err = refresh_any(q)) != cudaSuccess) return cuda_status(err);
     }
     if (schedule == 1) {
       err = cudaMemcpyAsync(f_new, bjac, sizeof(double) * d * QR, cudaMemcpyDeviceToDevice, st);
@@ -663,7 +775,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     // solve (also by rounding when delta_beta == 1): refresh every mode's Grams
     if (damp)
       for (int k = 0; k < d; ++k)
-        if ((err = refresh_mode(k)) != cudaSuccess) return cuda_status(err);
+        if ((err = refresh_any(k)) != cudaSuccess) return cuda_status(err);
     err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_status(err);
     if (eps_tol > 0.0) {   // reference loop condition (implicit.py:244): one host read per sweep
