@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(256) form_h_kernel(const __grid_constant__ HAr
   const int x = blockIdx.x, r = a.r, rr = r * r;
   for (int e2 = threadIdx.x; e2 < rr; e2 += 256) {
     double h = 0.0, hg = 0.0;
+#pragma unroll 4
     for (int pi = a.pbeg[x]; pi < a.pbeg[x + 1]; ++pi) {   // only the pairs that map to table x
       const int ez = a.pairs[pi], e = ez / a.ra, z = ez - e * a.ra;
       double g[IM_MAXD], gm[IM_MAXD];
@@ -286,7 +287,19 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
   double* Mim = Mre + r * ld;
   double* gre = Mim + r * ld;             // [r]
   double* gim = gre + r;
-  const double* Hs = a.H;                 // [nX][r][r]  H_X[j][i] (form_h_kernel)
+  // stage H, Hg, this frequency's eigenvalues and b_old coefficients (one round trip)
+  double* Hs_s = gim + r;                 // [nX][r][r]  H_X[j][i] (form_h_kernel)
+  double* Hg_s = Hs_s + (size_t)a.nX * r * r;
+  double* lam_s = Hg_s + (size_t)a.nX * r * r;   // [nX][2]
+  double* bo_s = lam_s + 2 * a.nX;        // [r][2]
+  for (int e = tid; e < a.nX * r * r; e += 256) { Hs_s[e] = __ldg(a.H + e); Hg_s[e] = __ldg(a.Hg + e); }
+  for (int x = tid; x < a.nX; x += 256) {
+    lam_s[2 * x] = __ldg(a.eig + ((size_t)a.xs[x] * Q + k) * 2);
+    lam_s[2 * x + 1] = __ldg(a.eig + ((size_t)a.xs[x] * Q + k) * 2 + 1);
+  }
+  for (int e = tid; e < 2 * r; e += 256) bo_s[e] = __ldg(a.bho + (size_t)k * r * 2 + e);
+  __syncthreads();
+  const double* Hs = Hs_s;
   const double inv_sqrt = rsqrt((double)Q);
   // gamma^(k)_i = DFT_k(gamma_i) / sqrt(Q) straight from the Fourier coefficients of
   // b_old (gamma = sum_X Hg_X (T~_X b_old)^T, T~_X circulant -> lambda~_X(k)):
@@ -296,12 +309,12 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
     double re = 0.0, im = 0.0;
     if (i < r) {
       for (int x = 0; x < a.nX; ++x) {
-        const double* lm = a.eig + ((size_t)a.xs[x] * Q + k) * 2;
+        const double* lm = lam_s + 2 * x;
         const double lr = lm[0], li = a.conj_tilde ? -lm[1] : lm[1];
         double sr = 0.0, si = 0.0;
         for (int j = part; j < r; j += 16) {
-          const double h = a.Hg[((size_t)x * r + i) * r + j];
-          const double br = a.bho[((size_t)k * r + j) * 2], bi = a.bho[((size_t)k * r + j) * 2 + 1];
+          const double h = Hg_s[((size_t)x * r + i) * r + j];
+          const double br = bo_s[2 * j], bi = bo_s[2 * j + 1];
           sr = fma(h, br, sr);
           si = fma(h, bi, si);
         }
@@ -321,7 +334,7 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
     double re = (i == j) ? a.lam : 0.0, im = 0.0;
     for (int x = 0; x < a.nX; ++x) {
       const double h = Hs[(size_t)x * r * r + j * r + i];
-      const double* lm = a.eig + ((size_t)a.xs[x] * Q + k) * 2;
+      const double* lm = lam_s + 2 * x;
       re = fma(h, lm[0], re);
       im = fma(-h, lm[1], im);          // conj(lambda)
     }
@@ -336,7 +349,7 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
     if (!(dpp > 0.0) || !isfinite(dpp)) bad = 1;
     const double d = sqrt(fabs(dpp)), id = 1.0 / d;
     __syncthreads();
-    if (tid == 0) { Mre[p * ld + p] = d; Mim[p * ld + p] = 0.0; }
+    if (tid == 0) { Mre[p * ld + p] = d; Mim[p * ld + p] = id; }   // diagonal: d, and 1/d in the (zero) imaginary slot
     for (int i = p + 1 + tid; i < r; i += 256) { Mre[i * ld + p] *= id; Mim[i * ld + p] *= id; }
     __syncthreads();
     const int m = r - p - 1;
@@ -351,38 +364,30 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
     __syncthreads();
   }
   if (bad && tid == 0) atomicOr(a.info, 1);
-  if (tid < 32) {   // one warp: per row the dot product over the lanes, then the pivot divide
+  if (tid < 32) {   // one warp, column-oriented: solve row i, then update the remaining rows in parallel
     const int lane = tid;
     for (int i = 0; i < r; ++i) {            // L y = g
-      double re = 0.0, im = 0.0;
-      for (int c = lane; c < i; c += 32) {
-        const double lr = Mre[i * ld + c], li = Mim[i * ld + c];
-        re += lr * gre[c] - li * gim[c];
-        im += lr * gim[c] + li * gre[c];
+      const double idd = Mim[i * ld + i];
+      const double yr = gre[i] * idd, yi = gim[i] * idd;
+      __syncwarp();
+      if (lane == 0) { gre[i] = yr; gim[i] = yi; }
+      for (int c = i + 1 + lane; c < r; c += 32) {   // g_c -= L[c][i] y_i
+        const double lr = Mre[c * ld + i], li = Mim[c * ld + i];
+        gre[c] -= lr * yr - li * yi;
+        gim[c] -= lr * yi + li * yr;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        re += __shfl_xor_sync(0xffffffffu, re, o);
-        im += __shfl_xor_sync(0xffffffffu, im, o);
-      }
-      const double dd = Mre[i * ld + i];
-      if (lane == 0) { gre[i] = (gre[i] - re) / dd; gim[i] = (gim[i] - im) / dd; }
       __syncwarp();
     }
     for (int i = r - 1; i >= 0; --i) {       // L^H x = y
-      double re = 0.0, im = 0.0;
-      for (int c = i + 1 + lane; c < r; c += 32) {   // conj(L[c][i]) x_c
-        const double lr = Mre[c * ld + i], li = -Mim[c * ld + i];
-        re += lr * gre[c] - li * gim[c];
-        im += lr * gim[c] + li * gre[c];
+      const double idd = Mim[i * ld + i];
+      const double xr = gre[i] * idd, xi = gim[i] * idd;
+      __syncwarp();
+      if (lane == 0) { gre[i] = xr; gim[i] = xi; }
+      for (int c = lane; c < i; c += 32) {   // y_c -= conj(L[i][c]) x_i
+        const double lr = Mre[i * ld + c], li = -Mim[i * ld + c];
+        gre[c] -= lr * xr - li * xi;
+        gim[c] -= lr * xi + li * xr;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        re += __shfl_xor_sync(0xffffffffu, re, o);
-        im += __shfl_xor_sync(0xffffffffu, im, o);
-      }
-      const double dd = Mre[i * ld + i];
-      if (lane == 0) { gre[i] = (gre[i] - re) / dd; gim[i] = (gim[i] - im) / dd; }
       __syncwarp();
     }
   }
@@ -731,7 +736,8 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
         ca.H = H; ca.eig = circ_eig; ca.gam = gam; ca.tw = tw; ca.xhat = xhat; ca.lam = lam; ca.info = info;
         ca.Hg = Hg; ca.bho = bho + (size_t)q * QR * 2; ca.conj_tilde = tr;
         form_h_kernel<<<ha.nX, 256, 0, st>>>(ha);
-        const size_t csm = sizeof(double) * (2 * (size_t)r * (r + 1) + 2 * r);
+        const size_t csm = sizeof(double) * (2 * (size_t)r * (r + 1) + 4 * (size_t)r + 2 * (size_t)ha.nX * r * r +
+                                             2 * (size_t)ha.nX);
         cudaFuncSetAttribute(circ_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
         circ_solve_kernel<<<Q, 256, csm, st>>>(ca);
         circ_idft_kernel<<<(int)((8 * QR + 255) / 256), 256, 0, st>>>(Q, r, xhat, tw, dst, info);
