@@ -40,12 +40,17 @@ struct HArgs {
 };
 
 // H and Hg for the distinct tables of mode q: one CTA per distinct table
+// H and Hg for the distinct tables of mode q: grid (table, element chunk); FH_SPLIT
+// lanes per element share the term pairs (shuffle reduction, fixed order)
+constexpr int FH_SPLIT = 4;
 __global__ void __launch_bounds__(256) form_h_kernel(const __grid_constant__ HArgs a) {
-  const int x = blockIdx.x, r = a.r, rr = r * r;
-  for (int e2 = threadIdx.x; e2 < rr; e2 += 256) {
-    double h = 0.0, hg = 0.0;
-#pragma unroll 4
-    for (int pi = a.pbeg[x]; pi < a.pbeg[x + 1]; ++pi) {   // only the pairs that map to table x
+  const int x = blockIdx.x, r = a.r, rr = r * r, lane = threadIdx.x & (FH_SPLIT - 1);
+  const int per_cta = 256 / FH_SPLIT;
+  const int e2 = blockIdx.y * per_cta + threadIdx.x / FH_SPLIT;
+  const bool act = e2 < rr;
+  double h = 0.0, hg = 0.0;
+  if (act) {
+    for (int pi = a.pbeg[x] + lane; pi < a.pbeg[x + 1]; pi += FH_SPLIT) {   // pairs mapping to table x
       const int ez = a.pairs[pi], e = ez / a.ra, z = ez - e * a.ra;
       double g[IM_MAXD], gm[IM_MAXD];
 #pragma unroll
@@ -61,6 +66,13 @@ __global__ void __launch_bounds__(256) form_h_kernel(const __grid_constant__ HAr
       h += a.KL[e * a.ra + z] * p;
       hg += a.KR[e * a.ra + z] * pg;
     }
+  }
+#pragma unroll
+  for (int o = FH_SPLIT / 2; o > 0; o >>= 1) {
+    h += __shfl_xor_sync(0xffffffffu, h, o);
+    hg += __shfl_xor_sync(0xffffffffu, hg, o);
+  }
+  if (act && lane == 0) {
     a.H[(size_t)x * rr + e2] = h;     // e2 = j*r + i : H_X[j][i]
     a.Hg[(size_t)x * rr + e2] = hg;   // e2 = i*r + j : Hg_X[i][j]
   }
@@ -458,25 +470,23 @@ __global__ void __launch_bounds__(256) fourier_grams_kernel(const __grid_constan
   __syncthreads();
   const double invQ = 1.0 / (double)Q;
   double* out = (mixed ? a.Gm : a.G) + ((size_t)a.k * a.n_tab + t) * r * r;
-  for (int e = tid; e < r * r; e += 256) {
-    const int l = e / r, m = e - l * r;
-    double s0 = 0.0, s1 = 0.0;
-    for (int f = 0; f < Q; f += 2) {
-      {
+  // 4 lanes per output (frequencies f = part + 4 u), shuffle reduction; blockIdx.z
+  // selects a chunk of 64 outputs
+  for (int base = blockIdx.z * 256; base < min(4 * r * r, (int)(blockIdx.z + 1) * 256); base += 256) {
+    const int tt = base + tid, e = tt >> 2, part = tt & 3;
+    const bool act = e < r * r;
+    const int l = act ? e / r : 0, m = act ? e - l * r : 0;
+    double s0 = 0.0;
+    if (act)
+      for (int f = part; f < Q; f += 4) {
         const double xr = x[((size_t)f * r + l) * 2], xi = x[((size_t)f * r + l) * 2 + 1];
         const double yr = y[((size_t)f * r + m) * 2], yi = y[((size_t)f * r + m) * 2 + 1];
         const double pr = lam[2 * f] * yr - lam[2 * f + 1] * yi, pi = lam[2 * f] * yi + lam[2 * f + 1] * yr;
         s0 += xr * pr + xi * pi;   // Re(conj(x) p)
       }
-      if (f + 1 < Q) {
-        const int g = f + 1;
-        const double xr = x[((size_t)g * r + l) * 2], xi = x[((size_t)g * r + l) * 2 + 1];
-        const double yr = y[((size_t)g * r + m) * 2], yi = y[((size_t)g * r + m) * 2 + 1];
-        const double pr = lam[2 * g] * yr - lam[2 * g + 1] * yi, pi = lam[2 * g] * yi + lam[2 * g + 1] * yr;
-        s1 += xr * pr + xi * pi;
-      }
-    }
-    out[e] = (s0 + s1) * invQ;
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+    if (act && part == 0) out[e] = s0 * invQ;
   }
 }
 
@@ -681,7 +691,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     fa.Q = Q; fa.r = r; fa.k = k; fa.n_tab = n_tab; fa.conj_tilde = tr;
     for (size_t i = 0; i < used[k].size(); ++i) fa.ts[i] = used[k][i];
     fa.eig = circ_eig; fa.bn = bhn; fa.bo = bho + (size_t)k * QR * 2; fa.G = G; fa.Gm = Gm;
-    fourier_grams_kernel<<<dim3((unsigned)used[k].size(), 2), 256, fg_smem, st>>>(fa);
+    fourier_grams_kernel<<<dim3((unsigned)used[k].size(), 2, (unsigned)((4 * r * r + 255) / 256)), 256, fg_smem, st>>>(fa);
     return cudaGetLastError();
   };
   auto refresh_any = [&](int k) -> cudaError_t { return circ_eig ? refresh_fourier(k) : refresh_mode(k); };
@@ -735,14 +745,14 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
         ca.G = G; ca.Gm = Gm; ca.W = W;
         ca.H = H; ca.eig = circ_eig; ca.gam = gam; ca.tw = tw; ca.xhat = xhat; ca.lam = lam; ca.info = info;
         ca.Hg = Hg; ca.bho = bho + (size_t)q * QR * 2; ca.conj_tilde = tr;
-        form_h_kernel<<<ha.nX, 256, 0, st>>>(ha);
+        form_h_kernel<<<dim3(ha.nX, (r * r + 256 / FH_SPLIT - 1) / (256 / FH_SPLIT)), 256, 0, st>>>(ha);
         const size_t csm = sizeof(double) * (2 * (size_t)r * (r + 1) + 4 * (size_t)r + 2 * (size_t)ha.nX * r * r +
                                              2 * (size_t)ha.nX);
         cudaFuncSetAttribute(circ_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
         circ_solve_kernel<<<Q, 256, csm, st>>>(ca);
         circ_idft_kernel<<<(int)((8 * QR + 255) / 256), 256, 0, st>>>(Q, r, xhat, tw, dst, info);
       } else {
-      form_h_kernel<<<ha.nX, 256, 0, st>>>(ha);
+      form_h_kernel<<<dim3(ha.nX, (r * r + 256 / FH_SPLIT - 1) / (256 / FH_SPLIT)), 256, 0, st>>>(ha);
       gamma_kernel<<<(n + 255) / 256, 256, 0, st>>>(Q, r, ha.nX, xs_modes + (size_t)q * IM_MAXT, Hg, W, n_tab, q, gam, n);
       as.nX = ha.nX;
       for (int i = 0; i < as.nX; ++i) as.xs[i] = used[q][i];
