@@ -412,10 +412,17 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
 
 // Unnormalised DFT of the columns of a real Q x r factor: out[k][l][2] =
 // sum_s b[s][l] e^{-2 pi i s k / Q}; 8 lanes per output (as circ_idft_kernel)
-__global__ void dft_cols_kernel(int Q, int r, const double* b, const double* tw, double* out) {
+__global__ void __launch_bounds__(256) dft_cols_kernel(int Q, int r, const double* b, const double* tw, double* out) {
+  // one CTA per frequency block: the factor (Q x r) and the twiddles staged in
+  // shared memory, 8 lanes per (frequency, column), shuffle reduction
+  extern __shared__ double dsm[];
+  double* bs = dsm;                  // [Q][r]
+  double* ts = bs + (size_t)Q * r;   // [Q][2]
+  for (int e = threadIdx.x; e < Q * r; e += 256) bs[e] = __ldg(b + e);
+  for (int e = threadIdx.x; e < 2 * Q; e += 256) ts[e] = __ldg(tw + e);
+  __syncthreads();
   const int n = Q * r;
-  const int lanes = gridDim.x * blockDim.x;
-  for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 - (threadIdx.x & 7) < 8 * n; t0 += lanes) {
+  for (int t0 = blockIdx.x * 256 + threadIdx.x; t0 - (threadIdx.x & 7) < 8 * n; t0 += gridDim.x * 256) {
     const int e = t0 >> 3, part = t0 & 7;
     const bool act = e < n;
     const int k = act ? e / r : 0, l = act ? e - k * r : 0;
@@ -424,9 +431,9 @@ __global__ void dft_cols_kernel(int Q, int r, const double* b, const double* tw,
       const int step = (8 * k) % Q;
       int m = (k * part) % Q;
       for (int s2 = part; s2 < Q; s2 += 8) {
-        const double v = b[(size_t)s2 * r + l];
-        re = fma(v, tw[2 * m], re);
-        im = fma(-v, tw[2 * m + 1], im);
+        const double v = bs[s2 * r + l];
+        re = fma(v, ts[2 * m], re);
+        im = fma(-v, ts[2 * m + 1], im);
         m += step;
         if (m >= Q) m -= Q;
       }
@@ -493,11 +500,17 @@ __global__ void __launch_bounds__(256) fourier_grams_kernel(const __grid_constan
 // beta_q[c][j] = Re sum_k xhat[j][k] e^{+2 pi i c k / Q} / sqrt(Q)
 // 8 lanes per output (frequencies k = part + 8 t, index m = c k mod Q stepped
 // incrementally), fixed-order shuffle reduction
-__global__ void circ_idft_kernel(int Q, int r, const double* xhat, const double* tw, double* beta_q, int* info) {
+__global__ void __launch_bounds__(256) circ_idft_kernel(int Q, int r, const double* xhat, const double* tw,
+                                                        double* beta_q, int* info) {
+  extern __shared__ double ism[];
+  double* xs = ism;                    // [r][Q][2]
+  double* ts = xs + (size_t)r * Q * 2; // [Q][2]
+  for (int e = threadIdx.x; e < 2 * r * Q; e += 256) xs[e] = __ldg(xhat + e);
+  for (int e = threadIdx.x; e < 2 * Q; e += 256) ts[e] = __ldg(tw + e);
+  __syncthreads();
   const int n = Q * r;
   const double inv_sqrt = rsqrt((double)Q);
-  const int lanes = gridDim.x * blockDim.x;
-  for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 - (threadIdx.x & 7) < 8 * n; t0 += lanes) {
+  for (int t0 = blockIdx.x * 256 + threadIdx.x; t0 - (threadIdx.x & 7) < 8 * n; t0 += gridDim.x * 256) {
     const int e = t0 >> 3, part = t0 & 7;
     const bool act = e < n;
     const int c = act ? e / r : 0, j = act ? e - c * r : 0;
@@ -506,9 +519,9 @@ __global__ void circ_idft_kernel(int Q, int r, const double* xhat, const double*
       const int step = (8 * c) % Q;
       int m = (c * part) % Q;
       for (int k = part; k < Q; k += 8) {
-        const double* xh = xhat + ((size_t)j * Q + k) * 2;
-        a0 = fma(xh[0], tw[2 * m], a0);
-        a1 = fma(-xh[1], tw[2 * m + 1], a1);
+        const double* xh = xs + ((size_t)j * Q + k) * 2;
+        a0 = fma(xh[0], ts[2 * m], a0);
+        a1 = fma(-xh[1], ts[2 * m + 1], a1);
         m += step;
         if (m >= Q) m -= Q;
       }
@@ -676,16 +689,21 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   };
   const size_t fg_smem = sizeof(double) * (4 * QR + 2 * (size_t)Q);
   const int dft_blocks = (int)((8 * QR + 255) / 256);
+  const size_t dft_smem = sizeof(double) * (QR + 2 * (size_t)Q), idft_smem = sizeof(double) * (2 * QR + 2 * (size_t)Q);
+  if (circ_eig) {
+    cudaFuncSetAttribute(dft_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dft_smem);
+    cudaFuncSetAttribute(circ_idft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)idft_smem);
+  }
   if (circ_eig) {
     cudaFuncSetAttribute(fourier_grams_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fg_smem);
     // DFT of every mode of b_old once per step
     for (int k = 0; k < d; ++k)
-      dft_cols_kernel<<<dft_blocks, 256, 0, st>>>(Q, r, f_old + (size_t)k * QR, tw, bho + (size_t)k * QR * 2);
+      dft_cols_kernel<<<dft_blocks, 256, dft_smem, st>>>(Q, r, f_old + (size_t)k * QR, tw, bho + (size_t)k * QR * 2);
   }
   // Circulant tables: the Grams of mode k from Fourier coefficients (one DFT of
   // b_new[k], one launch for G and Gm of all its tables) instead of four GEMMs
   auto refresh_fourier = [&](int k) -> cudaError_t {
-    dft_cols_kernel<<<dft_blocks, 256, 0, st>>>(Q, r, f_new + (size_t)k * QR, tw, bhn);
+    dft_cols_kernel<<<dft_blocks, 256, dft_smem, st>>>(Q, r, f_new + (size_t)k * QR, tw, bhn);
     FGramArgs fa;
     memset(&fa, 0, sizeof(fa));
     fa.Q = Q; fa.r = r; fa.k = k; fa.n_tab = n_tab; fa.conj_tilde = tr;
@@ -750,7 +768,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
                                              2 * (size_t)ha.nX);
         cudaFuncSetAttribute(circ_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
         circ_solve_kernel<<<Q, 256, csm, st>>>(ca);
-        circ_idft_kernel<<<(int)((8 * QR + 255) / 256), 256, 0, st>>>(Q, r, xhat, tw, dst, info);
+        circ_idft_kernel<<<(int)((8 * QR + 255) / 256), 256, idft_smem, st>>>(Q, r, xhat, tw, dst, info);
       } else {
       form_h_kernel<<<dim3(ha.nX, (r * r + 256 / FH_SPLIT - 1) / (256 / FH_SPLIT)), 256, 0, st>>>(ha);
       gamma_kernel<<<(n + 255) / 256, 256, 0, st>>>(Q, r, ha.nX, xs_modes + (size_t)q * IM_MAXT, Hg, W, n_tab, q, gam, n);
