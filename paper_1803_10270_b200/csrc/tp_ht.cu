@@ -81,10 +81,9 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int 
     v[i * ld + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  const int half = kp / 2;
-  // fixed per-thread work split: pair = tid % half, element lane j0 = tid / half
-  const int my_pair = tid % half, stride = JAC_NT / half, j0 = tid / half;
-  const bool active = j0 < stride && tid < half * stride;
+  const int half = kp / 2, lane = tid & 31, warp = tid >> 5;
+  // work split: warp w owns pairs w, w + 8, ...; its lanes run along the
+  // contiguous row / the column (conflict-free shared accesses, warp-uniform skips)
   int* flag = reinterpret_cast<int*>(red);
   int sw = 0;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
@@ -113,29 +112,31 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int 
         pq[2 * tid] = p; pq[2 * tid + 1] = q;
       }
       __syncthreads();
-      if (active) {                                           // rows p, q
-        const int p = pq[2 * my_pair], q = pq[2 * my_pair + 1];
-        const double c = cs[2 * my_pair], s = cs[2 * my_pair + 1];
-        if (s != 0.0)
-          for (int j = j0; j < kp; j += stride) {
-            const double x = a[p * ld + j], y = a[q * ld + j];
-            a[p * ld + j] = c * x - s * y;
-            a[q * ld + j] = s * x + c * y;
-          }
+      for (int pr = warp; pr < half; pr += JAC_NT / 32) {     // rows p, q
+        const double s = cs[2 * pr + 1];
+        if (s == 0.0) continue;
+        const int p = pq[2 * pr], q = pq[2 * pr + 1];
+        const double c = cs[2 * pr];
+        for (int j = lane; j < kp; j += 32) {
+          const double x = a[p * ld + j], y = a[q * ld + j];
+          a[p * ld + j] = c * x - s * y;
+          a[q * ld + j] = s * x + c * y;
+        }
       }
       __syncthreads();
-      if (active) {                                           // columns p, q and eigenvectors
-        const int p = pq[2 * my_pair], q = pq[2 * my_pair + 1];
-        const double c = cs[2 * my_pair], s = cs[2 * my_pair + 1];
-        if (s != 0.0)
-          for (int i = j0; i < kp; i += stride) {
-            const double x = a[i * ld + p], y = a[i * ld + q];
-            a[i * ld + p] = c * x - s * y;
-            a[i * ld + q] = s * x + c * y;
-            const double vx = v[i * ld + p], vy = v[i * ld + q];
-            v[i * ld + p] = c * vx - s * vy;
-            v[i * ld + q] = s * vx + c * vy;
-          }
+      for (int pr = warp; pr < half; pr += JAC_NT / 32) {     // columns p, q and eigenvectors
+        const double s = cs[2 * pr + 1];
+        if (s == 0.0) continue;
+        const int p = pq[2 * pr], q = pq[2 * pr + 1];
+        const double c = cs[2 * pr];
+        for (int i = lane; i < kp; i += 32) {
+          const double x = a[i * ld + p], y = a[i * ld + q];
+          a[i * ld + p] = c * x - s * y;
+          a[i * ld + q] = s * x + c * y;
+          const double vx = v[i * ld + p], vy = v[i * ld + q];
+          v[i * ld + p] = c * vx - s * vy;
+          v[i * ld + q] = s * vx + c * vy;
+        }
       }
       __syncthreads();
     }
