@@ -81,7 +81,8 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
                   double* trace, int* info, int grid, void* ws, size_t ws_bytes, void* stream);
 /* Launch plan tp_cp_als_f64 would use (no reference counterpart; introspection
  * for benchmarks/tests): out[0] kernel variant (0 = R-slab per CTA, 1 = clusters
- * of row blocks), out[1] CTAs, out[2] CTAs per cluster, out[3] shared bytes/CTA. */
+ * of row blocks, 2 = one CTA with the problem resident in shared memory),
+ * out[1] CTAs, out[2] CTAs per cluster, out[3] shared bytes/CTA. */
 int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out);
 
 /* ---------------------------------------------------------------------------

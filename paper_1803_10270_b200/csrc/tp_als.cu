@@ -849,6 +849,158 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
 }
 
 // ===========================================================================
+// Small-problem variant (one CTA, everything resident in shared memory): the
+// target V, the iterate U, all crosses C_k and Grams G_k.  A mode update is five
+// CTA-synchronised passes of plain FFMA loops (the work is a few 10^4 MACs, far
+// too small for the DMMA pipe or for any cross-CTA exchange):
+//   1. had[c][l] = prod_{k!=j} C_k[l][c];  A_j = prod_{k!=j} G_k + lambda I
+//   2. rhs[s][l] = sum_c V_j[s][c] had[c][l]            (cp.py:197-203)
+//   3. A_j^-1 by the symmetric sweep (exact, cp.py:312-317)
+//   4. U_j[s][i] = sum_m A^-1[i][m] rhs[s][m]
+//   5. C_j[l][c] = sum_s U_j[s][l] V_j[s][c], G_j = U_j^T U_j (cp.py:318-320)
+// plus the residual / stopping rule per sweep (cp.py:321-332).  Used when the
+// planner's grid is one CTA and the problem fits (config 0).
+// ===========================================================================
+
+__host__ __device__ inline size_t sm_small_doubles(int d, int sumq, int qmax, int R, int r) {
+  const size_t rp = (size_t)r + 1;
+  return 8 + (size_t)sumq * R + (size_t)sumq * r + (size_t)d * r * R + (size_t)d * r * r + (size_t)R * r +
+         (size_t)qmax * r + 2 * r * rp + 72 + ALS_PART + 8;
+}
+
+template <int RM>
+__global__ void __launch_bounds__(ALS_NT, 1) als_small(const __grid_constant__ AlsArgs a) {
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x, d = a.d, r = a.r, R = a.R, rr = r * r, rp = r + 1;
+  int sumq = 0;
+  int qo[TP_MAXD + 1];
+  qo[0] = 0;
+  for (int k = 0; k < d; ++k) { qo[k + 1] = qo[k] + a.q[k]; }
+  sumq = qo[d];
+  double* Vs = smem + 8;                       // [sumq][R] (global layout)
+  double* Us = Vs + (size_t)sumq * R;          // [sumq][r]
+  double* Cs = Us + (size_t)sumq * r;          // [d][r][R]
+  double* Gsm = Cs + (size_t)d * r * R;        // [d][r][r]
+  double* had = Gsm + (size_t)d * rr;          // [R][r]
+  double* rhs = had + (size_t)R * r;           // [qmax][r]
+  double* Am = rhs + (size_t)a.qmax * r;       // [r][r+1]
+  double* Ai = Am + (size_t)r * rp;            // [r][r+1]
+  Smem sm;
+  memset(&sm, 0, sizeof(sm));
+  sm.Gs = Gsm;
+  sm.pub = Ai + (size_t)r * rp;
+  sm.part = sm.pub + 72;
+  sm.scal = sm.part + ALS_PART;
+  for (int e = tid; e < sumq * R; e += ALS_NT) Vs[e] = a.V[e];
+  for (int e = tid; e < sumq * r; e += ALS_NT) Us[e] = a.U[e];
+  __syncthreads();
+  // crosses and Grams of mode k from Us / Vs
+  auto refresh = [&](int k) {
+    const double* Uk = Us + (size_t)qo[k] * r;
+    const double* Vk = Vs + (size_t)qo[k] * R;
+    const int Q = a.q[k], n1 = r * R, n2 = n1 + rr;
+    for (int o = tid; o < n2; o += ALS_NT) {
+      double s0 = 0.0, s1 = 0.0;
+      if (o < n1) {          // C_k[l][c], lanes along c
+        const int l = o / R, c = o - l * R;
+        int s = 0;
+        for (; s + 2 <= Q; s += 2) {
+          s0 = fma(Uk[s * r + l], Vk[(size_t)s * R + c], s0);
+          s1 = fma(Uk[(s + 1) * r + l], Vk[(size_t)(s + 1) * R + c], s1);
+        }
+        if (s < Q) s0 = fma(Uk[s * r + l], Vk[(size_t)s * R + c], s0);
+        Cs[(size_t)k * n1 + o] = s0 + s1;
+      } else {               // G_k[l][m]
+        const int g = o - n1, l = g / r, m = g - l * r;
+        int s = 0;
+        for (; s + 2 <= Q; s += 2) {
+          s0 = fma(Uk[s * r + l], Uk[s * r + m], s0);
+          s1 = fma(Uk[(s + 1) * r + l], Uk[(s + 1) * r + m], s1);
+        }
+        if (s < Q) s0 = fma(Uk[s * r + l], Uk[s * r + m], s0);
+        Gsm[(size_t)k * rr + g] = s0 + s1;
+      }
+    }
+  };
+  for (int k = 0; k < d; ++k) refresh(k);
+  __syncthreads();
+  const double norm_sq = a.need_resid ? fmax(*a.norm_sq, 0.0) : 0.0;
+  const double t_norm = sqrt(norm_sq);
+  double prev = INFINITY;
+  int status = 0, done = 0;
+  for (int sweep = 0; sweep < a.sweeps; ++sweep) {
+    for (int j = 0; j < d; ++j) {
+      const int Qj = a.q[j];
+      // 1. Hadamards
+      for (int e = tid; e < r * R; e += ALS_NT) {   // lanes along c (contiguous Cs rows)
+        const int l = e / R, c = e - l * R;
+        double v = 1.0;
+        for (int k = 0; k < d; ++k)
+          if (k != j) v *= Cs[((size_t)k * r + l) * R + c];
+        had[c * r + l] = v;
+      }
+      __syncthreads();
+      // 2. right-hand side rows, and 3. the inverse (the sweep builds A itself)
+      for (int o = tid; o < Qj * r; o += ALS_NT) {
+        const int s = o / r, l = o - s * r;
+        const double* vrow = Vs + (size_t)(qo[j] + s) * R;
+        double s0 = 0.0, s1 = 0.0;
+        int c = 0;
+        for (; c + 2 <= R; c += 2) {
+          s0 = fma(vrow[c], had[c * r + l], s0);
+          s1 = fma(vrow[c + 1], had[(c + 1) * r + l], s1);
+        }
+        if (c < R) s0 = fma(vrow[c], had[c * r + l], s0);
+        rhs[o] = s0 + s1;
+      }
+      __syncthreads();
+      status |= gram_inverse<RM>(a, sm, j, Ai, rp);
+      __syncthreads();
+      // 4. U_j[s][i] = sum_m A^-1[i][m] rhs[s][m]
+      double* Uj = Us + (size_t)qo[j] * r;
+      int nf = 0;
+      for (int o = tid; o < Qj * r; o += ALS_NT) {
+        const int s = o / r, i = o - s * r;
+        double acc = 0.0;
+        for (int m = 0; m < r; ++m) acc = fma(Ai[i * rp + m], rhs[s * r + m], acc);
+        if (!isfinite(acc)) nf = 1;
+        Uj[o] = acc;
+      }
+      if (nf) atomicOr(a.info, 2);
+      __syncthreads();
+      // 5. refresh C_j, G_j
+      refresh(j);
+      __syncthreads();
+    }
+    done = sweep + 1;
+    if (a.need_resid) {   // residual by the Gram identity (cp.py:321-326), identical in every thread
+      double ov = 0.0, self = 0.0;
+      for (int e = tid; e < r * R; e += ALS_NT) {
+        const int l = e / R, c = e - l * R;
+        double v = 1.0;
+        for (int k = 0; k < d; ++k) v *= Cs[((size_t)k * r + l) * R + c];
+        ov += v;
+      }
+      for (int e = tid; e < rr; e += ALS_NT) {
+        double v = 1.0;
+        for (int k = 0; k < d; ++k) v *= Gsm[(size_t)k * rr + e];
+        self += v;
+      }
+      ov = block_sum(ov, sm.part);
+      self = block_sum(self, sm.part);
+      const double resid = sqrt(fmax(norm_sq - 2.0 * ov + self, 0.0));
+      if (tid == 0 && a.trace) a.trace[sweep] = resid;
+      if (resid <= a.tol * t_norm) break;
+      if (prev - resid < a.stall * fmax(t_norm, 1.0)) break;
+      prev = resid;
+    }
+  }
+  for (int e = tid; e < sumq * r; e += ALS_NT) a.U[e] = Us[e];
+  if (status && tid == 0) atomicOr(a.info, 1);
+  if (tid == 0) a.info[1] = done;
+}
+
+// ===========================================================================
 // Cluster variant.  The grid is Pr clusters x Pq CTAs; cluster a owns R-slab a,
 // CTA b of the cluster owns row block b of every mode.  A mode update keeps the
 // two grid barriers of als_persistent but moves ~5x less data per CTA: the
@@ -1352,16 +1504,23 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
 
 struct AlsPlan {
   AlsArgs a;
-  int P, rm, variant, Pr;   // variant 0: als_persistent, 1: als_cluster (P = Pr * a.Pq)
+  int P, rm, variant, Pr;   // variant 0: als_persistent, 1: als_cluster (P = Pr * a.Pq), 2: als_small
   size_t smem, ws_inner, ws_total, ydoubles;
 };
 
-static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 force als_cluster
+static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 force als_cluster, 3 force als_small
 static int g_cluster = 0;   // debug hook: cluster size (0 = auto)
 
 static int choose_rm(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : 0)); }
 
 static const void* kernel_ptr(int rm, int variant) {
+  if (variant == 2) {
+    switch (rm) {
+      case 8: return (const void*)als_small<8>;
+      case 16: return (const void*)als_small<16>;
+      default: return (const void*)als_small<32>;
+    }
+  }
   if (variant == 1) {
     switch (rm) {
       case 8: return (const void*)als_cluster<8>;
@@ -1524,6 +1683,17 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
       if (g_cluster > 0) break;
     }
     if (g_variant == 2) return TP_EUNSUPPORTED;
+  }
+  // tiny problems: one CTA with everything in shared memory
+  if (g_variant == 3 || (g_variant == 0 && grid <= 0 && P == 1)) {
+    int sumq = 0;
+    for (int k = 0; k < d; ++k) sumq += q[k];
+    const size_t sm_small = sm_small_doubles(d, sumq, qmax, R, r) * sizeof(double);
+    if (sm_small <= (size_t)smem_optin) {
+      pl.variant = 2; pl.P = 1; pl.Pr = 1; pl.smem = sm_small;
+    } else if (g_variant == 3) {
+      return TP_EUNSUPPORTED;
+    }
   }
   return TP_OK;
 }

@@ -227,3 +227,17 @@ def test_als_deferred_check_matches_sync():
     assert torch.equal(a.data, b.data) and b.pending_info is None
     with pytest.raises(ValueError, match="trace"):
         cp.cp_approx_als(V, r, cfg, init=I0, sync=False, trace=[])
+
+
+@pytest.mark.parametrize("qs,R,r", [((32,) * 6, 78, 6), ((5, 7, 3), 6, 2), ((9, 8, 7, 6), 10, 3), ((20, 16, 24), 41, 12),
+                                    ((16, 12), 40, 9)])
+def test_als_small_variant(als_variant, qs, R, r):
+    """One CTA with the whole problem in shared memory (config 0 sizes and ragged
+    shapes), with the residual trace; forced through the debug hook."""
+    als_variant(3, 0)
+    rng = np.random.default_rng(R + 7 * r)
+    V = rand_factors(rng, qs, R, 0.3)
+    init = [v[:, :r].copy() for v in V]
+    out, ref, trace, otrace = _als_case(V, init, 10, 1e-10)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+    np.testing.assert_allclose(trace, otrace, rtol=1e-8, atol=1e-12)

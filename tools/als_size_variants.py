@@ -15,7 +15,7 @@ T = cp.CPTensor(w["specs"], w["V"])
 I0 = cp.CPTensor(w["specs"], w["init"])
 info = torch.zeros(2, dtype=torch.int32, device=T.data.device)
 U = I0.data.clone()
-for name, var, cs, grid in [("auto", 0, 0, 0), ("persistent g=1", 1, 0, 1), ("persistent g=4", 1, 0, 4),
+for name, var, cs, grid in [("auto", 0, 0, 0), ("small", 3, 0, 0), ("persistent g=1", 1, 0, 1), ("persistent g=4", 1, 0, 4),
                             ("persistent g=12", 1, 0, 12), ("persistent g=32", 1, 0, 32), ("persistent g=64", 1, 0, 64),
                             ("cluster2", 2, 2, 0), ("cluster4", 2, 4, 0), ("cluster8", 2, 8, 0)]:
     L.tp_debug_set_als_variant(var, cs)
