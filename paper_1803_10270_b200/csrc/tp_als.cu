@@ -1020,7 +1020,7 @@ __host__ __device__ inline size_t cl_smem_doubles(int d, int r, int wmax, int ld
                                                   int Pr, int Pq, int chunk, int qmax) {
   const size_t w4 = (size_t)((wmax + 3) / 4) * 4, rh = pad4(r);
   return 8 + cl_stage_doubles(nbmax, r, ncolmax, Pr) + (size_t)sumnb * ldw + (size_t)d * r * wmax + (size_t)d * r * r +
-         w4 * rh + (size_t)Pq * chunk + (size_t)Pq * chunk + 3 * (size_t)r * rh + 72 + 4 * (size_t)ncolmax * r +
+         w4 * rh + (size_t)(Pq - 1) * chunk + (size_t)chunk + 3 * (size_t)r * rh + 72 + 4 * (size_t)ncolmax * r +
          ALS_PART + 8 + ((size_t)d * qmax + 1) / 2 + 1;
 }
 
@@ -1033,8 +1033,8 @@ __device__ inline Smem carve_cl(double* base, const AlsArgs& a, int Pr) {
   s.Cs = base + o; o += (size_t)a.d * a.r * a.wmax;     // Cs[k]: r x w, row stride w
   s.Gs = base + o; o += (size_t)a.d * a.r * a.r;
   s.hadT = base + o; o += (size_t)((a.wmax + 3) / 4) * 4 * pad4(a.r);
-  s.inbox = base + o; o += (size_t)a.Pq * a.chunk;
-  s.mine = base + o; o += (size_t)a.Pq * a.chunk;
+  s.inbox = base + o; o += (size_t)(a.Pq - 1) * a.chunk;   // one slot per peer, a.chunk = max partial length
+  s.mine = base + o; o += (size_t)a.chunk;
   s.Am = base + o; o += (size_t)a.r * pad4(a.r);
   s.X0 = base + o; o += (size_t)a.r * pad4(a.r);
   s.X1 = nullptr;
@@ -1166,66 +1166,54 @@ __device__ void cl_partials(const AlsArgs& a, const Smem& sm, int k, int w, int 
 }
 
 // Cluster all-reduce of sm.mine (C slab partial [l][c] stride w, then this
-// cluster's Gram tiles), all by TMA bulk copies between the CTAs' shared
-// memories: every CTA pushes chunk q of its partial into CTA q's inbox, CTA q
-// sums its chunk in fixed rank order, keeps the C part in its own Cs[k] (r x w,
-// stride w) and pushes it into every peer's Cs[k]; reduced Gram tiles go to
-// global G (consumed after the next grid barrier).  Completion is tracked by
-// mbarriers sm.bar[2] (inbox) and sm.bar[3] (Cs); buffers are reused only after
-// grid barriers, so no cluster barrier is needed.
+// cluster's Gram tiles) in ONE round of TMA bulk copies between the CTAs' shared
+// memories: every CTA pushes its whole partial into each peer's inbox slot, then
+// every CTA sums the Pq partials in fixed rank order (bitwise identical results
+// in the whole cluster) into its Cs[k]; the reduced Gram tiles go to global G
+// from rank 0 (consumed after the next grid barrier).  Completion is tracked by
+// mbarrier sm.bar[2]; buffers are reused only after grid barriers, so no cluster
+// barrier is needed.
 template <int RM>
 __device__ void cl_exchange(const AlsArgs& a, const Smem& sm, cg::cluster_group& cl, int k, int w, int cid, int Pr,
                             uint32_t& ph, int& rows_mode, int rows_sweep) {
-  const int r = a.r, rr = r * r, Pq = a.Pq, chunk = a.chunk, b = (int)cl.block_rank(), tid = threadIdx.x;
+  const int r = a.r, rr = r * r, Pq = a.Pq, stride = a.chunk, b = (int)cl.block_rank(), tid = threadIdx.x;
   const int mtr = (r + 7) / 8, nG = mtr * (mtr + 1) / 2, nGi = cid < nG ? (nG - 1 - cid) / Pr + 1 : 0;
-  const int rw = r * w, L = rw + nGi * 64;
+  const int rw = r * w, L = rw + nGi * 64, L2 = (L + 1) & ~1;   // even: 16-byte bulk sizes
   double* Ck = sm.Cs + (size_t)k * r * a.wmax;
-  const uint32_t bar_in = smem_u32(sm.bar + 2), bar_cs = smem_u32(sm.bar + 3);
-  auto clen = [&](int q) { const int lo = q * chunk, hi = min((q + 1) * chunk, rw); return hi > lo ? hi - lo : 0; };
+  const uint32_t bar_in = smem_u32(sm.bar + 2);
   __syncthreads();   // sm.mine complete
   if (tid == 0) {
-    uint32_t cs_bytes = 0;
-    for (int q = 0; q < Pq; ++q) if (q != b) cs_bytes += 8u * (uint32_t)clen(q);
-    mbar_arrive_expect_tx(sm.bar + 2, 8u * (uint32_t)((Pq - 1) * chunk));
-    mbar_arrive_expect_tx(sm.bar + 3, cs_bytes);
+    mbar_arrive_expect_tx(sm.bar + 2, 8u * (uint32_t)((Pq - 1) * L2));
     fence_proxy_async_cluster();
-    const uint32_t inbox = smem_u32(sm.inbox) + 8u * (uint32_t)(b * chunk);
-    for (int q = 0; q < Pq; ++q)
-      if (q != b) bulk_s2cluster(mapa_u32(inbox, q), sm.mine + (size_t)q * chunk, 8u * (uint32_t)chunk, mapa_u32(bar_in, q));
+    for (int q = 0; q < Pq; ++q)   // my partial -> CTA q's inbox slot for source b
+      if (q != b) {
+        const uint32_t slot = smem_u32(sm.inbox) + 8u * (uint32_t)((b - (b > q)) * stride);
+        bulk_s2cluster(mapa_u32(slot, q), sm.mine, 8u * (uint32_t)L2, mapa_u32(bar_in, q));
+      }
   }
-  if (rows_mode >= 0) {   // warm-start rows of the previous solve, while the peers' chunks land
+  if (rows_mode >= 0) {   // warm-start rows of the previous solve, while the peers' partials land
     ns_rows<RM>(a, sm, rows_mode, rows_sweep);
     rows_mode = -1;
   }
   mbar_wait(sm.bar + 2, ph);
+  ph ^= 1u;
   double* Gk = a.G + (size_t)k * rr;
-  for (int e = tid; e < chunk; e += ALS_NT) {
-    const int idx = b * chunk + e;
-    if (idx < L) {
-      double v = 0.0;
-      for (int src = 0; src < Pq; ++src) v += (src == b) ? sm.mine[idx] : sm.inbox[(size_t)src * chunk + e];
-      if (idx < rw) {
-        Ck[idx] = v;
-      } else {
-        const int gi = (idx - rw) >> 6, ln = ((idx - rw) & 63) >> 1, h = (idx - rw) & 1;
-        int g = cid + gi * Pr, ti = 0;
-        while (g >= mtr - ti) { g -= mtr - ti; ++ti; }
-        const int tj = ti + g;
-        const int orow = ti * 8 + (ln >> 2), ocol = tj * 8 + 2 * (ln & 3) + h;
-        if (orow < r && ocol < r) { Gk[orow * r + ocol] = v; Gk[ocol * r + orow] = v; }
-      }
+  for (int idx = tid; idx < L; idx += ALS_NT) {
+    double v = 0.0;
+    for (int src = 0; src < Pq; ++src)
+      v += (src == b) ? sm.mine[idx] : sm.inbox[(size_t)(src - (src > b)) * stride + idx];
+    if (idx < rw) {
+      Ck[idx] = v;
+    } else if (b == 0) {
+      const int gi = (idx - rw) >> 6, ln = ((idx - rw) & 63) >> 1, h = (idx - rw) & 1;
+      int g = cid + gi * Pr, ti = 0;
+      while (g >= mtr - ti) { g -= mtr - ti; ++ti; }
+      const int tj = ti + g;
+      const int orow = ti * 8 + (ln >> 2), ocol = tj * 8 + 2 * (ln & 3) + h;
+      if (orow < r && ocol < r) { Gk[orow * r + ocol] = v; Gk[ocol * r + orow] = v; }
     }
   }
   __syncthreads();
-  const int my = clen(b);
-  if (tid == 0 && my > 0) {
-    fence_proxy_async_cluster();
-    const uint32_t dst = smem_u32(Ck + (size_t)b * chunk);
-    for (int q = 0; q < Pq; ++q)
-      if (q != b) bulk_s2cluster(mapa_u32(dst, q), Ck + (size_t)b * chunk, 8u * (uint32_t)my, mapa_u32(bar_cs, q));
-  }
-  mbar_wait(sm.bar + 3, ph);
-  ph ^= 1u;
 }
 
 // had = prod_{k != j} C_k[:, slab] -> hadT[c][l], then the rows of block b of the
@@ -1564,7 +1552,7 @@ static int plan_cluster(int d, const int* q, int R, int r, int Pq, int smem_opti
     }
     sumnb += 8;   // slack rows: tile lanes past the last row stay in bounds
     const int mtr = (r + 7) / 8, nG = mtr * (mtr + 1) / 2;
-    int chunk = (r * wmax + ((nG + Pr - 1) / Pr) * 64 + Pq - 1) / Pq;
+    int chunk = r * wmax + ((nG + Pr - 1) / Pr) * 64;   // longest partial (all-to-all exchange)
     chunk += chunk & 1;
     const size_t smem = cl_smem_doubles(d, r, wmax, ldw, sumnb, nbmax, ncolmax, Pr, Pq, chunk, qmax) * sizeof(double);
     if (smem > (size_t)smem_optin) continue;
