@@ -166,6 +166,118 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_eigh_kernel(int k, int nn, int 
   }
 }
 
+// Same cyclic Jacobi (identical pair ordering, rotation formula and threshold),
+// one barrier per round instead of three: every warp recomputes the k/2
+// rotations of the round (lane = pair, warp-uniform results, no shared
+// hand-off), and the two-sided update A <- J^T A J is done as independent 2x2
+// blocks (rows of pair P, columns of pair P'), read from one buffer and written
+// to the other (double-buffered A, so angle reads and block writes of a round
+// never race).  Eigenvector columns are rotated in place by their owner lane.
+// Warp w owns row pairs w, w + 8, w + 16, w + 24; lane l owns column pair l.
+__global__ void __launch_bounds__(JAC_NT) jacobi_db_kernel(int k, int nn, int first, int per, const double* Ain,
+                                                           double* Vout, double* wout, int max_sweeps, double tol,
+                                                           int* sweeps_out, const int* skip) {
+  extern __shared__ double js[];
+  const int kp = k + (k & 1), ld = kp + 1, half = kp / 2, m1 = kp - 1;
+  double* Ac = js;
+  double* An = Ac + (size_t)kp * ld;
+  double* v = An + (size_t)kp * ld;
+  const int z = blockIdx.x;
+  const size_t base = (size_t)(z / per) * nn + first + z % per;
+  if (skip && skip[base]) return;
+  const double* in = Ain + base * k * k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < kp * kp; e += JAC_NT) {
+    const int i = e / kp, j = e % kp;
+    double x = 0.0;
+    if (i < k && j < k) x = 0.5 * (in[i * k + j] + in[j * k + i]);   // eigh(0.5 (G + G^T)), ht.py:347
+    Ac[i * ld + j] = x;
+    v[i * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const bool live = lane < half;
+  int sw = 0;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    sw = sweep + 1;
+    bool any = false;
+    for (int round = 0; round < m1; ++round) {
+      int p = round, q = m1;
+      if (lane != 0) { p = (round + lane) % m1; q = (round - lane + m1) % m1; }
+      if (p > q) { const int t = p; p = q; q = t; }
+      double c = 1.0, s = 0.0, t = 0.0;
+      int rot = 0;
+      if (live) {
+        const double apq = Ac[p * ld + q], app = Ac[p * ld + p], aqq = Ac[q * ld + q];
+        if (fabs(apq) > 1e-300 && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
+          const double tau = (aqq - app) / (2.0 * apq);
+          t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+          rot = 1;
+        }
+      }
+      any |= __any_sync(0xffffffffu, rot) != 0;
+      // eigenvector columns p, q (rows warp, warp + 8, ...)
+      if (live && rot) {
+        for (int i = warp; i < kp; i += JAC_NT / 32) {
+          const double vx = v[i * ld + p], vy = v[i * ld + q];
+          v[i * ld + p] = c * vx - s * vy;
+          v[i * ld + q] = s * vx + c * vy;
+        }
+      }
+      double apq_d = 0.0;
+      if (live) apq_d = Ac[p * ld + q];
+      for (int P = warp; P < half; P += JAC_NT / 32) {
+        const int pP = __shfl_sync(0xffffffffu, p, P), qP = __shfl_sync(0xffffffffu, q, P);
+        const double cP = __shfl_sync(0xffffffffu, c, P), sP = __shfl_sync(0xffffffffu, s, P);
+        if (!live) continue;
+        double* r0 = An + pP * ld;
+        double* r1 = An + qP * ld;
+        if (P == lane) {        // diagonal block: the rotation annihilates a_pq exactly
+          if (rot) {
+            r0[pP] = Ac[pP * ld + pP] - t * apq_d;
+            r1[qP] = Ac[qP * ld + qP] + t * apq_d;
+            r0[qP] = 0.0;
+            r1[pP] = 0.0;
+          } else {
+            r0[pP] = Ac[pP * ld + pP]; r0[qP] = Ac[pP * ld + qP];
+            r1[pP] = Ac[qP * ld + pP]; r1[qP] = Ac[qP * ld + qP];
+          }
+          continue;
+        }
+        const double x00 = Ac[pP * ld + p], x01 = Ac[pP * ld + q];
+        const double x10 = Ac[qP * ld + p], x11 = Ac[qP * ld + q];
+        const double y00 = cP * x00 - sP * x10, y01 = cP * x01 - sP * x11;   // rows (pair P)
+        const double y10 = sP * x00 + cP * x10, y11 = sP * x01 + cP * x11;
+        r0[p] = c * y00 - s * y01; r0[q] = s * y00 + c * y01;                // columns (pair P')
+        r1[p] = c * y10 - s * y11; r1[q] = s * y10 + c * y11;
+      }
+      __syncthreads();
+      double* tmp = Ac; Ac = An; An = tmp;
+    }
+    if (!any) break;
+  }
+  if (sweeps_out && tid == 0) atomicAdd(sweeps_out, sw);
+  double* Vo = Vout + base * k * k;
+  double* wo = wout + base * k;
+  int* rank = reinterpret_cast<int*>(An);   // scratch (An is dead after the last barrier)
+  if (tid < k) {
+    const double wi = Ac[tid * ld + tid];
+    int rk = 0;
+    for (int j = 0; j < k; ++j) {
+      const double wj = Ac[j * ld + j];
+      if (wj > wi || (wj == wi && j < tid)) ++rk;
+    }
+    rank[tid] = rk;
+    wo[rk] = wi;
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += JAC_NT) {
+    const int i = e / k, m = e % k;
+    Vo[i * k + rank[m]] = v[i * ld + m];
+  }
+}
+
 // Frame-Gram square-root factor by Cholesky, M_t = L L^T (one CTA per non-root
 // node, right-looking, 64 dependent steps instead of ~8 Jacobi sweeps).  In the
 // Gramian gauge only a factor F with F F^T = M_t enters: with F = L instead of
@@ -410,6 +522,7 @@ static int g_jac_sweeps = 30;
 static double g_jac_tol = 1e-16;
 static int* g_jac_count = nullptr;
 static int g_chol = 1;   // debug hook: 0 = eigh of every frame Gram (reference path)
+static int g_jac_db = 1;  // debug hook: 1 = one-barrier double-buffered Jacobi, 0 = three-barrier
 
 extern "C" {
 
@@ -419,6 +532,8 @@ void tp_debug_set_jacobi(int max_sweeps, double tol, int* count) {
 }
 // debug hook: frame-Gram factor by Cholesky (1, default) or eigh (0)
 void tp_debug_set_ht_chol(int on) { g_chol = on; }
+// debug hook: Jacobi kernel (1 = double-buffered one-barrier rounds, default; 0 = three-barrier rounds)
+void tp_debug_set_jacobi_impl(int db) { g_jac_db = db; }
 
 size_t tp_ht_truncate_ws_bytes(int d, int Q, int k, int nb) {
   if (d < 2 || d > 16 || Q < 1 || k < 1 || k > 64 || nb < 1) return 0;
@@ -613,8 +728,10 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
   if (e != cudaSuccess) return cuda_status(e);
 
   const int kp = k + (k & 1);
-  const size_t jsm = sizeof(double) * ((size_t)2 * kp * (kp + 1) + 2 * kp + JAC_NT) + sizeof(int) * kp;
-  cudaFuncSetAttribute(jacobi_eigh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm);
+  const size_t jsm = g_jac_db ? sizeof(double) * (size_t)3 * kp * (kp + 1)
+                              : sizeof(double) * ((size_t)2 * kp * (kp + 1) + 2 * kp + JAC_NT) + sizeof(int) * kp;
+  auto jac = g_jac_db ? jacobi_db_kernel : jacobi_eigh_kernel;
+  cudaFuncSetAttribute(jac, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm);
   const size_t fsm = sizeof(double) * 3 * (size_t)k * (k + 1);
   cudaFuncSetAttribute(form_g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
   const size_t ssm = sizeof(double) * ((size_t)k + (size_t)k * ro);
@@ -638,7 +755,7 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
         e = cudaMemsetAsync(cholok, 0, sizeof(int) * (size_t)nb * nn, st);
         if (e != cudaSuccess) return cuda_status(e);
       }
-      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Mf, Vm, lam, g_jac_sweeps, g_jac_tol, g_jac_count,
+      jac<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Mf, Vm, lam, g_jac_sweeps, g_jac_tol, g_jac_count,
                                                         cholok);
       e = cudaGetLastError();
     } else if (id == -2) {
@@ -648,7 +765,7 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
       form_g_kernel<<<nonroot, 256, fsm, st>>>(k, nn, Vm, lam, Gh, Gt, cholok);
       e = cudaGetLastError();
     } else if (id == -4) {
-      jacobi_eigh_kernel<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Gt, Wg, sig, g_jac_sweeps, g_jac_tol, g_jac_count,
+      jac<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Gt, Wg, sig, g_jac_sweeps, g_jac_tol, g_jac_count,
                                                         nullptr);
       e = cudaGetLastError();
     } else if (id == -5) {

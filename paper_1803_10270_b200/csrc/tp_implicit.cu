@@ -19,6 +19,7 @@
 #include <cstring>
 #include <vector>
 #include <cmath>
+#include <algorithm>
 
 namespace tp {
 
@@ -537,6 +538,419 @@ __global__ void __launch_bounds__(256) circ_idft_kernel(int Q, int r, const doub
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused circulant Gauss-Seidel step: one cooperative launch runs every sweep.
+// The iterate lives in the Fourier domain as the half spectrum
+// X[q][k] = DFT_k(beta_q) / sqrt(Q), k = 0 .. Q/2 (beta real, so X(Q-k) = conj X(k)
+// and the other half is never stored or solved).  Per mode update q:
+//   (1) frequency phase, CTA per k: the r x r Hermitian system
+//       M^(k) = sum_X conj(lambda_X(k)) H_X^T + lam I,  gamma^(k) = sum_X lambda~_X(k) Hg_X bo^(k) / sqrt(Q)
+//       (same systems as circ_solve_kernel), complex Cholesky, X[q][k] <- x;
+//       this frequency's Parseval terms of the new Grams of mode q,
+//       w_k Re(conj x_l lambda_t x_m) and w_k Re(conj x_l lambda~_t bo_m) / sqrt(Q)
+//       (w_k = 2 for the frequencies standing for a conjugate pair), and of the
+//       relative update ||new - old||, ||old|| (implicit.py:167-177, Parseval);
+//   grid barrier;
+//   (2) entry phase, CTA per flat Gram entry e = l r + m: fixed-order sum of the
+//       frequency terms -> G[q][t][e], Gm[q][t][e]; then H_X[e], Hg_X[e] of the next
+//       mode (form_h_kernel's products: entry-local, so the owner of e has every
+//       G[k][t][e] it needs);
+//   grid barrier.
+// After the last sweep every CTA writes its share of beta = IDFT(X) (real).
+// Replaces form_h + circ_solve + circ_idft + dft_cols + fourier_grams (5 launches
+// and 3 dependent round trips per mode update).  Rounding differs from the
+// unfused path (spectrum kept instead of re-transforming the real iterate).
+// ---------------------------------------------------------------------------
+constexpr int CG_NT = 256, CG_MAXR = 32, CG_MAXX = 16;
+
+struct CircGsArgs {
+  int Q, r, d, ra, n_tab, nf, sweeps, conj_tilde, ne;
+  double lam, eps_tol;
+  unsigned char tslot[IM_MAXD * IM_MAXRA * IM_MAXRA];   // slot in used[k] of the table of (k, e, z)
+  int nused[IM_MAXD];
+  int used[IM_MAXD][CG_MAXX];
+  short pbeg[IM_MAXD][CG_MAXX + 1];          // pairs of (mode, table slot): pairs[q][pbeg[q][u] .. pbeg[q][u+1])
+  short pairs[IM_MAXD][IM_MAXRA * IM_MAXRA];
+  double KL[IM_MAXRA * IM_MAXRA], KR[IM_MAXRA * IM_MAXRA];
+  const double* eig;   // [n_tab][Q][2]
+  const double* tw;    // [Q][2] cos, sin of 2 pi m / Q
+  const double* f_old; // [d][Q][r]
+  double* f_new;       // [d][Q][r] in: initial iterate, out: solution
+  double* X;           // [d][nf][r][2]
+  double* Bo;          // [d][nf][r][2] unnormalised DFT of f_old
+  double* G;           // [d][n_tab][r*r]
+  double* Gm;
+  double* H;           // [CG_MAXX][r*r]  H_X[j][i] of the current mode (slot u of used[q])
+  double* Hg;          // [CG_MAXX][r*r]  Hg_X[i][j]
+  double* part;        // [d][nf][2][CG_MAXX][r*r] frequency terms of the Grams
+  double* convp;       // [d][nf][2]
+  double* eps_out;
+  int* info;           // [0] flags, [1] sweeps done
+  int* stop;
+  unsigned int* bar;
+};
+
+__device__ __forceinline__ void cg_grid_sync(unsigned int* ctr, unsigned int& epoch) {
+  __syncthreads();
+  if (gridDim.x == 1) return;
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned int target = epoch * gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+
+// Frequency terms of the Grams of mode q at frequency k (x, bo: r complex in smem;
+// lm: lambda_t(k) of the slots of used[q], smem)
+__device__ void cg_gram_terms(const CircGsArgs& a, int q, int k, const double* x, const double* bo,
+                              const double* lm, double wk) {
+  const int r = a.r, rr = r * r, nu = a.nused[q];
+  const double isq = rsqrt((double)a.Q);
+  double* out = a.part + ((size_t)q * a.nf + k) * 2 * CG_MAXX * rr;
+  for (int e = threadIdx.x; e < 2 * nu * rr; e += CG_NT) {
+    const int g = e / (nu * rr), rem = e - g * nu * rr, u = rem / rr, l2 = rem - u * rr, l = l2 / r, m = l2 - l * r;
+    const double lr = lm[2 * u];
+    double li = lm[2 * u + 1];
+    const double xr = x[2 * l], xi = x[2 * l + 1];
+    double yr, yi, s = wk;
+    if (g == 0) { yr = x[2 * m]; yi = x[2 * m + 1]; }
+    else { yr = bo[2 * m]; yi = bo[2 * m + 1]; if (a.conj_tilde) li = -li; s *= isq; }
+    const double pr = lr * yr - li * yi, pi = lr * yi + li * yr;
+    out[((size_t)g * CG_MAXX + u) * rr + l2] = s * (xr * pr + xi * pi);
+  }
+}
+
+// Entry phase.  CTA c owns the flat Gram entries e = c + i * grid (i < ne) for the
+// whole launch and caches G / Gm of every mode at those entries in shared memory
+// (gc[g][k][slot][i]).  Reduce the frequency terms of mode q (8 lanes per item,
+// fixed-order shuffle tree), then H_X, Hg_X of mode qn at the owned entries (8 lanes
+// per item over the term pairs).
+__device__ void cg_entries(const CircGsArgs& a, double* gc, int q, int qn) {
+  const int r = a.r, rr = r * r, nf = a.nf, ne = a.ne, tid = threadIdx.x, part = tid & 7;
+  int nown = 0;
+  for (int e = blockIdx.x; e < rr; e += gridDim.x) ++nown;
+  const int nu = a.nused[q];
+  const double* pbase = a.part + (size_t)q * nf * 2 * CG_MAXX * rr;
+  for (int it0 = 0; it0 < nown * 2 * nu; it0 += CG_NT / 8) {
+    const int it = it0 + (tid >> 3);
+    const bool act = it < nown * 2 * nu;
+    int i = 0, g = 0, u = 0;
+    double s = 0.0;
+    if (act) {
+      i = it / (2 * nu); const int rem = it - i * 2 * nu; g = rem / nu; u = rem - g * nu;
+      const int e = blockIdx.x + i * gridDim.x;
+      const double* p = pbase + ((size_t)g * CG_MAXX + u) * rr + e;
+      for (int k = part; k < nf; k += 8) s += __ldcg(p + (size_t)k * 2 * CG_MAXX * rr);
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (act && part == 0) {
+      const int e = blockIdx.x + i * gridDim.x;
+      (g == 0 ? a.G : a.Gm)[((size_t)q * a.n_tab + a.used[q][u]) * rr + e] = s;
+      gc[((size_t)(g * IM_MAXD + q) * CG_MAXX + u) * ne + i] = s;
+    }
+  }
+  if (qn < 0) return;
+  __syncthreads();
+  const int nx = a.nused[qn];
+  for (int it0 = 0; it0 < nown * 2 * nx; it0 += CG_NT / 8) {
+    const int it = it0 + (tid >> 3);
+    const bool act = it < nown * 2 * nx;
+    int i = 0, g = 0, u = 0;
+    double h = 0.0;
+    if (act) {
+      i = it / (2 * nx); const int rem = it - i * 2 * nx; g = rem / nx; u = rem - g * nx;
+      const double* gg = gc + (size_t)g * IM_MAXD * CG_MAXX * ne + i;
+      for (int pi = a.pbeg[qn][u] + part; pi < a.pbeg[qn][u + 1]; pi += 8) {
+        const int ez = a.pairs[qn][pi];
+        double p = 1.0;
+        for (int k = 0; k < a.d; ++k)
+          if (k != qn) p *= gg[((size_t)k * CG_MAXX + a.tslot[k * a.ra * a.ra + ez]) * ne];
+        h += (g == 0 ? a.KL[ez] : a.KR[ez]) * p;
+      }
+    }
+    h += __shfl_xor_sync(0xffffffffu, h, 4);
+    h += __shfl_xor_sync(0xffffffffu, h, 2);
+    h += __shfl_xor_sync(0xffffffffu, h, 1);
+    if (act && part == 0) (g == 0 ? a.H : a.Hg)[(size_t)u * rr + blockIdx.x + i * gridDim.x] = h;
+  }
+}
+
+__global__ void __launch_bounds__(CG_NT) circ_gs_kernel(const __grid_constant__ CircGsArgs a) {
+  extern __shared__ double cg[];
+  const int Q = a.Q, r = a.r, rr = r * r, nf = a.nf, tid = threadIdx.x, ld = r + 1;
+  const double isq = rsqrt((double)Q);
+  double* Mre = cg;                          // [r][ld]
+  double* Mim = Mre + r * ld;
+  double* gx = Mim + r * ld;                 // [r][2] right-hand side / solution
+  double* xo = gx + 2 * r;                   // [r][2] previous iterate
+  double* bo = xo + 2 * r;                   // [r][2]
+  double* lam = bo + 2 * r;                  // [CG_MAXX][2]
+  double* gc = lam + 2 * CG_MAXX;            // [2][IM_MAXD][CG_MAXX][ne] owned Gram entries
+  double* scr = gc + (size_t)2 * IM_MAXD * CG_MAXX * a.ne;   // scratch (a.scr doubles)
+  double* Hs = scr;                          // [CG_MAXX][rr]
+  double* Hgs = Hs + (size_t)CG_MAXX * rr;   // [CG_MAXX][rr]
+  unsigned int epoch = 0;
+  auto wgt = [&](int k) { return (k == 0 || 2 * k == Q) ? 1.0 : 2.0; };
+
+  // ---- (I0) half spectra of the iterate (X, scaled 1/sqrt Q) and of b_old (Bo):
+  // work item = (which, mode), the factor and the twiddles staged in shared memory
+  for (int w = blockIdx.x; w < 2 * a.d; w += gridDim.x) {
+    const int which = w / a.d, q = w - which * a.d;
+    const double* src = (which ? a.f_old : a.f_new) + (size_t)q * Q * r;
+    double* ts = scr + (size_t)Q * r;
+    __syncthreads();
+    for (int e = tid; e < Q * r; e += CG_NT) scr[e] = src[e];
+    for (int e = tid; e < 2 * Q; e += CG_NT) ts[e] = __ldg(a.tw + e);
+    __syncthreads();
+    for (int o = tid; o < nf * r; o += CG_NT) {
+      const int k = o / r, j = o - k * r;
+      double sr = 0.0, si = 0.0;
+      int m = 0;
+      for (int s = 0; s < Q; ++s) {
+        const double v = scr[s * r + j];
+        sr = fma(v, ts[2 * m], sr);
+        si = fma(-v, ts[2 * m + 1], si);
+        m += k;
+        if (m >= Q) m -= Q;
+      }
+      if (k == 0 || 2 * k == Q) si = 0.0;
+      const double sc = which ? 1.0 : isq;
+      double* dst = (which ? a.Bo : a.X) + (((size_t)q * nf + k) * r + j) * 2;
+      dst[0] = sr * sc;
+      dst[1] = si * sc;
+    }
+  }
+  cg_grid_sync(a.bar, epoch);
+  // ---- (I1) frequency terms of the Grams of every mode
+  for (int k = blockIdx.x; k < nf; k += gridDim.x) {
+    for (int q = 0; q < a.d; ++q) {
+      for (int e = tid; e < 2 * r; e += CG_NT) {
+        gx[e] = __ldcg(a.X + ((size_t)q * nf + k) * r * 2 + e);
+        bo[e] = __ldcg(a.Bo + ((size_t)q * nf + k) * r * 2 + e);
+      }
+      for (int u = tid; u < a.nused[q]; u += CG_NT) {
+        lam[2 * u] = __ldg(a.eig + ((size_t)a.used[q][u] * Q + k) * 2);
+        lam[2 * u + 1] = __ldg(a.eig + ((size_t)a.used[q][u] * Q + k) * 2 + 1);
+      }
+      __syncthreads();
+      cg_gram_terms(a, q, k, gx, bo, lam, wgt(k));
+      __syncthreads();
+    }
+  }
+  cg_grid_sync(a.bar, epoch);
+  // ---- (I2) Grams of every mode, H of mode 0
+  for (int q = 0; q < a.d; ++q) {
+    cg_entries(a, gc, q, q == a.d - 1 ? 0 : -1);
+    __syncthreads();
+  }
+  cg_grid_sync(a.bar, epoch);
+
+  int done = 0;
+  for (int sweep = 0; sweep < a.sweeps; ++sweep) {
+    for (int q = 0; q < a.d; ++q) {
+      const int nx = a.nused[q];
+      // ---- (1) frequency phase
+      for (int e = tid; e < nx * rr; e += CG_NT) { Hs[e] = __ldcg(a.H + e); Hgs[e] = __ldcg(a.Hg + e); }
+      for (int k = blockIdx.x; k < nf; k += gridDim.x) {
+        for (int x = tid; x < nx; x += CG_NT) {
+          lam[2 * x] = __ldg(a.eig + ((size_t)a.used[q][x] * Q + k) * 2);
+          lam[2 * x + 1] = __ldg(a.eig + ((size_t)a.used[q][x] * Q + k) * 2 + 1);
+        }
+        for (int e = tid; e < 2 * r; e += CG_NT) {
+          bo[e] = __ldcg(a.Bo + ((size_t)q * nf + k) * r * 2 + e);
+          xo[e] = __ldcg(a.X + ((size_t)q * nf + k) * r * 2 + e);
+        }
+        __syncthreads();
+        // gamma^(k)_i = sum_X lambda~_X(k) sum_j Hg_X[i][j] bo_j / sqrt(Q)   (8 lanes per i)
+        for (int base = 0; base < 8 * r; base += CG_NT) {
+          const int t = base + tid, i = t >> 3, part = t & 7;
+          double re = 0.0, im = 0.0;
+          if (i < r) {
+            for (int x = 0; x < nx; ++x) {
+              const double lr = lam[2 * x], li = a.conj_tilde ? -lam[2 * x + 1] : lam[2 * x + 1];
+              double sr = 0.0, si = 0.0;
+              for (int j = part; j < r; j += 8) {
+                const double h = Hgs[((size_t)x * r + i) * r + j];
+                sr = fma(h, bo[2 * j], sr);
+                si = fma(h, bo[2 * j + 1], si);
+              }
+              re += lr * sr - li * si;
+              im += lr * si + li * sr;
+            }
+          }
+#pragma unroll
+          for (int o = 4; o > 0; o >>= 1) {
+            re += __shfl_xor_sync(0xffffffffu, re, o);
+            im += __shfl_xor_sync(0xffffffffu, im, o);
+          }
+          if (i < r && part == 0) { gx[2 * i] = re * isq; gx[2 * i + 1] = im * isq; }
+        }
+        // M[i][j] = sum_X H_X[j][i] conj(lambda_X(k)) + lam delta_ij
+        for (int e = tid; e < rr; e += CG_NT) {
+          const int i = e / r, j = e - i * r;
+          double re = (i == j) ? a.lam : 0.0, im = 0.0;
+          for (int x = 0; x < nx; ++x) {
+            const double h = Hs[(size_t)x * rr + j * r + i];
+            re = fma(h, lam[2 * x], re);
+            im = fma(-h, lam[2 * x + 1], im);
+          }
+          Mre[i * ld + j] = re;
+          Mim[i * ld + j] = im;
+        }
+        __syncthreads();
+        // complex Cholesky M = L L^H (lower, in place)
+        int bad = 0;
+        for (int p = 0; p < r; ++p) {
+          const double dpp = Mre[p * ld + p];
+          if (!(dpp > 0.0) || !isfinite(dpp)) bad = 1;
+          const double dg = sqrt(fabs(dpp)), id = 1.0 / dg;
+          __syncthreads();
+          if (tid == 0) { Mre[p * ld + p] = dg; Mim[p * ld + p] = id; }
+          for (int i = p + 1 + tid; i < r; i += CG_NT) { Mre[i * ld + p] *= id; Mim[i * ld + p] *= id; }
+          __syncthreads();
+          const int m = r - p - 1;
+          for (int e = tid; e < m * m; e += CG_NT) {
+            const int i = p + 1 + e / m, c = p + 1 + e % m;
+            if (c <= i) {
+              const double ar = Mre[i * ld + p], ai = Mim[i * ld + p], br = Mre[c * ld + p], bi = Mim[c * ld + p];
+              Mre[i * ld + c] -= ar * br + ai * bi;
+              Mim[i * ld + c] -= ai * br - ar * bi;
+            }
+          }
+          __syncthreads();
+        }
+        if (bad && tid == 0) atomicOr(a.info, 1);
+        if (tid < 32) {
+          const int lane = tid;
+          for (int i = 0; i < r; ++i) {            // L y = g
+            const double idd = Mim[i * ld + i];
+            const double yr = gx[2 * i] * idd, yi = gx[2 * i + 1] * idd;
+            __syncwarp();
+            if (lane == 0) { gx[2 * i] = yr; gx[2 * i + 1] = yi; }
+            for (int c = i + 1 + lane; c < r; c += 32) {
+              const double lr = Mre[c * ld + i], li = Mim[c * ld + i];
+              gx[2 * c] -= lr * yr - li * yi;
+              gx[2 * c + 1] -= lr * yi + li * yr;
+            }
+            __syncwarp();
+          }
+          for (int i = r - 1; i >= 0; --i) {       // L^H x = y
+            const double idd = Mim[i * ld + i];
+            const double xr = gx[2 * i] * idd, xi = gx[2 * i + 1] * idd;
+            __syncwarp();
+            if (lane == 0) { gx[2 * i] = xr; gx[2 * i + 1] = xi; }
+            for (int c = lane; c < i; c += 32) {
+              const double lr = Mre[i * ld + c], li = -Mim[i * ld + c];
+              gx[2 * c] -= lr * xr - li * xi;
+              gx[2 * c + 1] -= lr * xi + li * xr;
+            }
+            __syncwarp();
+          }
+          if (k == 0 || 2 * k == Q)
+            for (int i = lane; i < r; i += 32) gx[2 * i + 1] = 0.0;   // self-conjugate frequency: real
+          __syncwarp();
+          // relative-update terms (Parseval, weight w_k)
+          double dd = 0.0, nn = 0.0;
+          for (int i = lane; i < r; i += 32) {
+            const double dr = gx[2 * i] - xo[2 * i], di = gx[2 * i + 1] - xo[2 * i + 1];
+            dd += dr * dr + di * di;
+            nn += xo[2 * i] * xo[2 * i] + xo[2 * i + 1] * xo[2 * i + 1];
+            if (!isfinite(gx[2 * i]) || !isfinite(gx[2 * i + 1])) atomicOr(a.info, 2);
+          }
+          dd = warp_sum(dd);
+          nn = warp_sum(nn);
+          if (lane == 0) {
+            a.convp[((size_t)q * nf + k) * 2] = wgt(k) * dd;
+            a.convp[((size_t)q * nf + k) * 2 + 1] = wgt(k) * nn;
+          }
+        }
+        __syncthreads();
+        for (int e = tid; e < 2 * r; e += CG_NT) a.X[((size_t)q * nf + k) * r * 2 + e] = gx[e];
+        cg_gram_terms(a, q, k, gx, bo, lam, wgt(k));
+        __syncthreads();
+      }
+      cg_grid_sync(a.bar, epoch);
+      // ---- (2) entry phase (+ the sweep's relative update after the last mode)
+      const bool last = q == a.d - 1;
+      cg_entries(a, gc, q, last ? (sweep + 1 < a.sweeps ? 0 : -1) : q + 1);
+      if (last && blockIdx.x == gridDim.x - 1) {
+        __syncthreads();
+        if (tid < 32) {
+          double worst = 0.0;
+          for (int qq = 0; qq < a.d; ++qq) {
+            double dd = 0.0, nn = 0.0;
+            for (int k = tid; k < nf; k += 32) {
+              dd += __ldcg(a.convp + ((size_t)qq * nf + k) * 2);
+              nn += __ldcg(a.convp + ((size_t)qq * nf + k) * 2 + 1);
+            }
+            dd = sqrt(warp_sum(dd));
+            nn = sqrt(warp_sum(nn));
+            const double v = (nn == 0.0) ? (dd == 0.0 ? 0.0 : INFINITY) : dd / nn;
+            worst = fmax(worst, v);
+          }
+          if (tid == 0) {
+            *a.eps_out = worst;
+            *a.stop = (a.eps_tol > 0.0 && worst <= a.eps_tol) ? 1 : 0;
+          }
+        }
+      }
+      cg_grid_sync(a.bar, epoch);
+    }
+    done = sweep + 1;
+    if (*(volatile int*)a.stop) break;   // reference loop condition (implicit.py:244)
+  }
+  // ---- real solution beta_q[c][j] = (1/sqrt Q) Re sum_k X(k) e^{+2 pi i c k / Q} (half spectrum),
+  // one mode per CTA, spectrum and twiddles staged in shared memory
+  for (int q = blockIdx.x; q < a.d; q += gridDim.x) {
+    double* xs = scr;
+    double* ts = scr + (size_t)nf * r * 2;
+    __syncthreads();
+    for (int e = tid; e < nf * r * 2; e += CG_NT) xs[e] = __ldcg(a.X + (size_t)q * nf * r * 2 + e);
+    for (int e = tid; e < 2 * Q; e += CG_NT) ts[e] = __ldg(a.tw + e);
+    __syncthreads();
+    for (int o = tid; o < Q * r; o += CG_NT) {
+      const int c = o / r, j = o - c * r;
+      double acc = 0.0;
+      int m = 0;
+      for (int k = 0; k < nf; ++k) {
+        acc += wgt(k) * (xs[(k * r + j) * 2] * ts[2 * m] - xs[(k * r + j) * 2 + 1] * ts[2 * m + 1]);
+        m += c;
+        if (m >= Q) m -= Q;
+      }
+      acc *= isq;
+      if (!isfinite(acc)) atomicOr(a.info, 2);
+      a.f_new[(size_t)q * Q * r + o] = acc;
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) a.info[1] = done;
+}
+
+static size_t circ_gs_scr(int Q, int r) {
+  const size_t nf = (size_t)Q / 2 + 1;
+  size_t s = 2 * (size_t)CG_MAXX * r * r;
+  s = std::max(s, (size_t)Q * r + 2 * (size_t)Q);
+  s = std::max(s, nf * r * 2 + 2 * (size_t)Q);
+  return s;
+}
+
+static size_t circ_gs_smem(int Q, int r, int ne) {
+  return sizeof(double) * (2 * (size_t)r * (r + 1) + 6 * (size_t)r + 2 * CG_MAXX +
+                           (size_t)2 * IM_MAXD * CG_MAXX * ne + circ_gs_scr(Q, r));
+}
+
+static size_t circ_gs_bytes(int d, int Q, int r) {
+  const size_t nf = (size_t)Q / 2 + 1;
+  return align_up(8 * (size_t)d * nf * r * 2) * 2 + align_up(8 * (size_t)CG_MAXX * r * r) * 2 +
+         align_up(8 * (size_t)d * nf * 2 * CG_MAXX * r * r) + align_up(8 * (size_t)d * nf * 2) + 256 + 256;
+}
+
 static int padded_n(int n) { return (n + CH_NB - 1) / CH_NB * CH_NB; }
 
 static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
@@ -553,6 +967,7 @@ static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
   s += align_up(4 * IM_MAXT) + 256 + align_up(8 * 6 * (size_t)d * IM_MAXT);   // + Gram GEMM offset tables
   s += align_up(8 * (size_t)r * Q * 2) + align_up(8 * (size_t)Q * 2);   // circulant: xhat, twiddles
   s += align_up(8 * (size_t)d * Q * r * 2) + align_up(8 * (size_t)Q * r * 2);   // circulant: DFT(b_old), DFT(b_new)
+  s += circ_gs_bytes(d, Q, r);                                                   // fused circulant Gauss-Seidel
   return s;
 }
 
@@ -560,7 +975,12 @@ static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
 
 using namespace tp;
 
+static int g_circ_fused = 1;   // debug hook: 0 = per-kernel circulant path
+
 extern "C" {
+
+// debug hook: fused circulant Gauss-Seidel kernel on (1, default) / off (0)
+void tp_debug_set_circ_fused(int on) { g_circ_fused = on; }
 
 size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab) {
   if (d < 1 || d > IM_MAXD || Q < 1 || r < 1 || n_tab < 1 || n_tab > IM_MAXT) return 0;
@@ -628,6 +1048,71 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   cudaError_t err;
   err = cudaMemsetAsync(info, 0, 2 * sizeof(int), st);
   if (err != cudaSuccess) return cuda_status(err);
+
+  // fused circulant Gauss-Seidel step (one cooperative launch) when it applies
+  bool fused = g_circ_fused && circ_eig && schedule == 0 && delta_beta == 1.0 && r <= CG_MAXR;
+  for (int k = 0; k < d && fused; ++k) fused = used[k].size() <= (size_t)CG_MAXX;
+  if (fused) {
+    const int nf = Q / 2 + 1;
+    CircGsArgs* ga = new CircGsArgs;
+    memset(ga, 0, sizeof(*ga));
+    ga->Q = Q; ga->r = r; ga->d = d; ga->ra = ra; ga->n_tab = n_tab; ga->nf = nf; ga->sweeps = sweeps;
+    ga->conj_tilde = orientation ? 1 : 0; ga->lam = lam; ga->eps_tol = eps_tol;
+    for (int k = 0; k < d; ++k)
+      for (int ez = 0; ez < ra * ra; ++ez) {
+        const int t = tab_id[k * ra * ra + ez];
+        for (size_t u = 0; u < used[k].size(); ++u)
+          if (used[k][u] == t) ga->tslot[k * ra * ra + ez] = (unsigned char)u;
+      }
+    for (int i = 0; i < ra * ra; ++i) { ga->KL[i] = KL[i]; ga->KR[i] = KR[i]; }
+    for (int k = 0; k < d; ++k) {
+      ga->nused[k] = (int)used[k].size();
+      int np = 0;
+      for (size_t u = 0; u < used[k].size(); ++u) {
+        ga->used[k][u] = used[k][u];
+        ga->pbeg[k][u] = (short)np;
+        for (int ez = 0; ez < ra * ra; ++ez)
+          if (tab_id[k * ra * ra + ez] == used[k][u]) ga->pairs[k][np++] = (short)ez;
+      }
+      ga->pbeg[k][used[k].size()] = (short)np;
+    }
+    ga->eig = circ_eig; ga->tw = tw; ga->f_old = f_old; ga->f_new = f_new;
+    ga->X = cv.take<double>((size_t)d * nf * r * 2);
+    ga->Bo = cv.take<double>((size_t)d * nf * r * 2);
+    ga->H = cv.take<double>((size_t)CG_MAXX * r * r);
+    ga->Hg = cv.take<double>((size_t)CG_MAXX * r * r);
+    ga->part = cv.take<double>((size_t)d * nf * 2 * CG_MAXX * r * r);
+    ga->convp = cv.take<double>((size_t)d * nf * 2);
+    ga->bar = cv.take<unsigned int>(32);
+    ga->stop = reinterpret_cast<int*>(ga->bar + 16);
+    ga->G = G; ga->Gm = Gm; ga->eps_out = eps_conv; ga->info = info;
+    int nsm = 0, dev = 0;
+    err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (err != cudaSuccess) { delete ga; return cuda_status(err); }
+    // grid: one CTA per half-spectrum frequency, fewer if they cannot all be resident
+    int grid = nf < nsm ? nf : nsm, per_sm = 0;
+    size_t smem = 0;
+    for (;;) {
+      ga->ne = (r * r + grid - 1) / grid;
+      smem = circ_gs_smem(Q, r, ga->ne);
+      if (smem > 227 * 1024) { per_sm = 0; break; }
+      err = cudaFuncSetAttribute(circ_gs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, circ_gs_kernel, CG_NT, smem);
+      if (err != cudaSuccess) { delete ga; return cuda_status(err); }
+      if (per_sm * nsm >= grid || grid <= 1) break;
+      grid = per_sm * nsm;
+    }
+    if (per_sm >= 1) {
+      err = cudaMemsetAsync(ga->bar, 0, 32 * sizeof(unsigned int), st);
+      void* args[] = {ga};
+      if (err == cudaSuccess)
+        err = cudaLaunchCooperativeKernel((const void*)circ_gs_kernel, dim3(grid), dim3(CG_NT), args, smem, st);
+      delete ga;   // kernel parameters are copied at launch
+      return cuda_status(err);
+    }
+    delete ga;   // does not fit: per-kernel path below
+  }
   // per-mode Gram refresh: TB_t = T_t b (Q x r), G_t = a^T TB_t  (a, b = b_new or b_old)
   // transT: use T^T (reference gamma orientation for the mixed Grams / images)
   auto images = [&](int k, const double* bsrc, double* dst, int transT) -> cudaError_t {

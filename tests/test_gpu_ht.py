@@ -165,3 +165,34 @@ def test_frame_factor_paths(chol):
         assert metrics.ht_rel_diff(ref, red.to_oracle()) <= TOL
     finally:
         L.tp_debug_set_ht_chol(1)
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("chol", [0, 1])
+@pytest.mark.parametrize("d,q,k,rmax,eps", [(4, 9, 7, 3, 0.0), (5, 20, 13, 6, 1e-3), (8, 70, 64, 16, 0.0)])
+def test_jacobi_kernels(impl, chol, d, q, k, rmax, eps):
+    """Both Jacobi eigensolvers (three-barrier and double-buffered one-barrier rounds),
+    with and without the Cholesky frame factor, odd and maximal k, against the oracle."""
+    import ctypes
+    from paper_1803_10270_b200 import _lib
+    L = _lib.lib()
+    L.tp_debug_set_ht_chol.argtypes = [ctypes.c_int]
+    L.tp_debug_set_jacobi_impl.argtypes = [ctypes.c_int]
+    L.tp_debug_set_ht_chol(chol)
+    L.tp_debug_set_jacobi_impl(impl)
+    try:
+        rng = np.random.default_rng(100 + k)
+        o = random_ht(rng, d, q, k)
+        red, est = ht.truncate(to_dev(d, q, o), rmax, eps)
+        ref, oest = oht.truncate(o, rmax, eps)
+        assert abs(est - oest) <= 1e-8 * max(1.0, oht.norm(o))
+        assert metrics.ht_rel_diff(ref, red.to_oracle()) <= TOL
+        assert red.ranks == tuple(int(x) for x in ref_ranks(ref))
+    finally:
+        L.tp_debug_set_ht_chol(1)
+        L.tp_debug_set_jacobi_impl(1)
+
+
+def ref_ranks(o):
+    nodes, frames, transfers = o
+    return [frames[i].shape[1] if oht.is_leaf(nd) else transfers[i].shape[2] for i, nd in enumerate(nodes)]

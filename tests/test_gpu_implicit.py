@@ -118,3 +118,56 @@ def test_circulant_detection():
     assert implicit.is_circulant(fdm(16))
     assert implicit.is_circulant(fdm(16).T @ fdm(16))
     assert not implicit.is_circulant(np.diag(np.arange(8.0)))
+
+
+@pytest.fixture
+def circ_fused():
+    import ctypes
+    from paper_1803_10270_b200 import _lib
+    L = _lib.lib()
+    L.tp_debug_set_circ_fused.argtypes = [ctypes.c_int]
+    yield L.tp_debug_set_circ_fused
+    L.tp_debug_set_circ_fused(1)
+
+
+@pytest.mark.parametrize("fused", [0, 1])
+@pytest.mark.parametrize("orientation", ["corrected", "reference"])
+@pytest.mark.parametrize("d,q,r,eps_tol", [(3, 15, 5, 1e-7), (4, 16, 4, 0.0), (2, 9, 3, 1e-4)])
+def test_circulant_gauss_seidel_fused(circ_fused, fused, orientation, d, q, r, eps_tol):
+    """Fused one-launch circulant Gauss-Seidel step (half spectrum kept on the device)
+    and the per-kernel path against the oracle: odd and even Q, early stop on eps_tol
+    (same sweep count as the reference loop, implicit.py:244), both gamma orientations."""
+    circ_fused(fused)
+    rng = np.random.default_rng(40 + q)
+    dt, sweeps = 2e-2, 30
+    a = tuple(rng.uniform(-1, 1, d))
+    D = fourier_diff_matrix(q)
+    S = col_specs(d, q)
+    f0 = [rng.standard_normal((q, r)) for _ in range(d)]
+    cfg = implicit.ALSStepConfig(dt=dt, eps_tol=eps_tol, max_sweeps=sweeps if eps_tol > 0 else 6, delta_beta=1.0,
+                                 schedule="gauss-seidel", lam=1e-10, solver="circulant", orientation=orientation)
+    log = {}
+    out = implicit.step(cp.CPTensor(S, f0), euler_pair(S, D, a, dt), None, cfg, log=log)
+    ref, done, eps = oim.step(f0, oracle_tables(d, q, D, a, dt), cfg.max_sweeps, 1e-10, eps_tol=eps_tol,
+                              orientation=orientation)
+    assert log["sweeps"] == done
+    assert abs(log["eps_conv"] - eps) <= 1e-8 * max(eps, 1e-300) + 1e-14
+    rel = metrics.cp_rel_diff(ref, out.to_numpy())
+    assert rel <= 1e-9, rel
+
+
+@pytest.mark.parametrize("fused", [0, 1])
+def test_config2_steps_fused_vs_unfused(circ_fused, fused):
+    """Config-2 sizes, 2 full steps of 20 sweeps, both circulant paths vs the oracle."""
+    circ_fused(fused)
+    w = workloads.cfg2(0)
+    S, D, a, dt = w["specs"], w["D"], w["a"], w["dt"]
+    f0 = w["ic"]["factors"]
+    cfg = implicit.ALSStepConfig(dt=dt, eps_tol=0.0, max_sweeps=w["sweeps"], delta_beta=1.0,
+                                 schedule="gauss-seidel", lam=w["lam"], solver="circulant")
+    out = implicit.run(cp.CPTensor(S, f0), euler_pair(S, D, a, dt), cfg, 2).to_numpy()
+    tab = oracle_tables(6, 128, D, a, dt)
+    ref = f0
+    for _ in range(2):
+        ref, _, _ = oim.step(ref, tab, w["sweeps"], w["lam"])
+    assert metrics.cp_rel_diff(ref, out) <= 1e-8
