@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(256) circ_idft_kernel(int Q, int r, const doub
 // and 3 dependent round trips per mode update).  Rounding differs from the
 // unfused path (spectrum kept instead of re-transforming the real iterate).
 // ---------------------------------------------------------------------------
-constexpr int CG_NT = 256, CG_MAXR = 32, CG_MAXX = 16;
+constexpr int CG_NT = 256, CG_MAXR = 32, CG_MAXX = 16, CG_WR = 16;
 
 struct CircGsArgs {
   int Q, r, d, ra, n_tab, nf, sweeps, conj_tilde, ne;
@@ -588,7 +588,15 @@ struct CircGsArgs {
   int* info;           // [0] flags, [1] sweeps done
   int* stop;
   unsigned int* bar;
+  long long* prof;     // debug: per-phase clock64 totals of CTA 0 (nullptr = off)
 };
+
+#define CG_PROF(i)                                                               \
+  if (a.prof && blockIdx.x == 0 && tid == 0) {                                   \
+    const long long now = clock64();                                             \
+    a.prof[i] += now - t_prev;                                                   \
+    t_prev = now;                                                                \
+  }
 
 __device__ __forceinline__ void cg_grid_sync(unsigned int* ctr, unsigned int& epoch) {
   __syncthreads();
@@ -612,16 +620,18 @@ __device__ void cg_gram_terms(const CircGsArgs& a, int q, int k, const double* x
   const int r = a.r, rr = r * r, nu = a.nused[q];
   const double isq = rsqrt((double)a.Q);
   double* out = a.part + ((size_t)q * a.nf + k) * 2 * CG_MAXX * rr;
-  for (int e = threadIdx.x; e < 2 * nu * rr; e += CG_NT) {
-    const int g = e / (nu * rr), rem = e - g * nu * rr, u = rem / rr, l2 = rem - u * rr, l = l2 / r, m = l2 - l * r;
-    const double lr = lm[2 * u];
-    double li = lm[2 * u + 1];
+  const double cs = a.conj_tilde ? -1.0 : 1.0;
+  for (int l2 = threadIdx.x; l2 < rr; l2 += CG_NT) {
+    const int l = l2 / r, m = l2 - l * r;
     const double xr = x[2 * l], xi = x[2 * l + 1];
-    double yr, yi, s = wk;
-    if (g == 0) { yr = x[2 * m]; yi = x[2 * m + 1]; }
-    else { yr = bo[2 * m]; yi = bo[2 * m + 1]; if (a.conj_tilde) li = -li; s *= isq; }
-    const double pr = lr * yr - li * yi, pi = lr * yi + li * yr;
-    out[((size_t)g * CG_MAXX + u) * rr + l2] = s * (xr * pr + xi * pi);
+    const double yr = x[2 * m], yi = x[2 * m + 1], br = bo[2 * m], bi = bo[2 * m + 1];
+    for (int u = 0; u < nu; ++u) {
+      const double lr = lm[2 * u], li = lm[2 * u + 1], lt = cs * li;
+      const double pr = lr * yr - li * yi, pi = lr * yi + li * yr;       // lambda_t x_m
+      const double qr = lr * br - lt * bi, qi = lr * bi + lt * br;       // lambda~_t bo_m
+      out[(size_t)u * rr + l2] = wk * (xr * pr + xi * pi);
+      out[((size_t)CG_MAXX + u) * rr + l2] = wk * isq * (xr * qr + xi * qi);
+    }
   }
 }
 
@@ -630,7 +640,14 @@ __device__ void cg_gram_terms(const CircGsArgs& a, int q, int k, const double* x
 // (gc[g][k][slot][i]).  Reduce the frequency terms of mode q (8 lanes per item,
 // fixed-order shuffle tree), then H_X, Hg_X of mode qn at the owned entries (8 lanes
 // per item over the term pairs).
-__device__ void cg_entries(const CircGsArgs& a, double* gc, int q, int qn) {
+struct CgTabs {
+  unsigned char tslot[IM_MAXD * IM_MAXRA * IM_MAXRA];
+  short pairs[IM_MAXD][IM_MAXRA * IM_MAXRA];
+  short pbeg[IM_MAXD][CG_MAXX + 1];
+  double KL[IM_MAXRA * IM_MAXRA], KR[IM_MAXRA * IM_MAXRA];
+};
+
+__device__ void cg_entries(const CircGsArgs& a, const CgTabs& tb, double* gc, int q, int qn, long long& t_prev) {
   const int r = a.r, rr = r * r, nf = a.nf, ne = a.ne, tid = threadIdx.x, part = tid & 7;
   int nown = 0;
   for (int e = blockIdx.x; e < rr; e += gridDim.x) ++nown;
@@ -645,7 +662,17 @@ __device__ void cg_entries(const CircGsArgs& a, double* gc, int q, int qn) {
       i = it / (2 * nu); const int rem = it - i * 2 * nu; g = rem / nu; u = rem - g * nu;
       const int e = blockIdx.x + i * gridDim.x;
       const double* p = pbase + ((size_t)g * CG_MAXX + u) * rr + e;
-      for (int k = part; k < nf; k += 8) s += __ldcg(p + (size_t)k * 2 * CG_MAXX * rr);
+      const size_t ks = (size_t)2 * CG_MAXX * rr;
+      for (int k0 = 0; k0 < nf; k0 += 64) {   // 8 independent loads in flight per lane
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = k0 + part + 8 * j;
+          v[j] = k < nf ? __ldcg(p + (size_t)k * ks) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += v[j];
+      }
     }
     s += __shfl_xor_sync(0xffffffffu, s, 4);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
@@ -658,6 +685,11 @@ __device__ void cg_entries(const CircGsArgs& a, double* gc, int q, int qn) {
   }
   if (qn < 0) return;
   __syncthreads();
+  if (a.prof && blockIdx.x == 0 && tid == 0) {
+    const long long now = clock64();
+    a.prof[9] += now - t_prev;
+    t_prev = now;
+  }
   const int nx = a.nused[qn];
   for (int it0 = 0; it0 < nown * 2 * nx; it0 += CG_NT / 8) {
     const int it = it0 + (tid >> 3);
@@ -667,12 +699,17 @@ __device__ void cg_entries(const CircGsArgs& a, double* gc, int q, int qn) {
     if (act) {
       i = it / (2 * nx); const int rem = it - i * 2 * nx; g = rem / nx; u = rem - g * nx;
       const double* gg = gc + (size_t)g * IM_MAXD * CG_MAXX * ne + i;
-      for (int pi = a.pbeg[qn][u] + part; pi < a.pbeg[qn][u + 1]; pi += 8) {
-        const int ez = a.pairs[qn][pi];
+      const int ra2 = a.ra * a.ra;
+      for (int pi = tb.pbeg[qn][u] + part; pi < tb.pbeg[qn][u + 1]; pi += 8) {
+        const int ez = tb.pairs[qn][pi];
+        double f[IM_MAXD];
+#pragma unroll
+        for (int k = 0; k < IM_MAXD; ++k)   // independent loads, then the product in mode order
+          f[k] = (k < a.d && k != qn) ? gg[((size_t)k * CG_MAXX + tb.tslot[k * ra2 + ez]) * ne] : 1.0;
         double p = 1.0;
-        for (int k = 0; k < a.d; ++k)
-          if (k != qn) p *= gg[((size_t)k * CG_MAXX + a.tslot[k * a.ra * a.ra + ez]) * ne];
-        h += (g == 0 ? a.KL[ez] : a.KR[ez]) * p;
+#pragma unroll
+        for (int k = 0; k < IM_MAXD; ++k) p *= f[k];
+        h += (g == 0 ? tb.KL[ez] : tb.KR[ez]) * p;
       }
     }
     h += __shfl_xor_sync(0xffffffffu, h, 4);
@@ -682,7 +719,135 @@ __device__ void cg_entries(const CircGsArgs& a, double* gc, int q, int qn) {
   }
 }
 
-__global__ void __launch_bounds__(CG_NT) circ_gs_kernel(const __grid_constant__ CircGsArgs a) {
+// x = M^-1 g for the Hermitian positive definite r x r system of one frequency.
+// Register-resident warp version (r <= R): lane i holds row i of M (padded to the
+// identity), right-looking complex Cholesky M = L L^H with the forward
+// substitution folded in (one shuffle broadcast per pivot and per trailing
+// column), L^H x = y from a transposed copy of L through shared memory.
+__device__ __forceinline__ double cg_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int it = 0; it < 3; ++it) y = y * fma(-0.5 * x * y, y, 1.5);
+  return y;
+}
+
+template <int R>
+__device__ __forceinline__ void cg_warp_solve(double* Mre, double* Mim, double* gx, int r, int ld, int* info) {
+  const int lane = threadIdx.x & 31;
+  const bool row = lane < r;
+  double mr[R], mi[R];
+#pragma unroll
+  for (int c = 0; c < R; ++c) {
+    const bool in = row && c < r;
+    mr[c] = in ? Mre[lane * ld + c] : (c == lane ? 1.0 : 0.0);
+    mi[c] = in ? Mim[lane * ld + c] : 0.0;
+  }
+  double gr = row ? gx[2 * lane] : 0.0, gi = row ? gx[2 * lane + 1] : 0.0;
+  double myid = 1.0;
+  int bad = 0;
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    const double dpp = __shfl_sync(0xffffffffu, mr[p], p);
+    if (p < r && (!(dpp > 0.0) || !isfinite(dpp))) bad = 1;
+    const double id = cg_rsqrt(fabs(dpp));
+    if (lane == p) myid = id;
+    const double ypr = __shfl_sync(0xffffffffu, gr * id, p), ypi = __shfl_sync(0xffffffffu, gi * id, p);
+    if (lane > p) {
+      mr[p] *= id; mi[p] *= id;                        // L[i][p]
+      gr -= mr[p] * ypr - mi[p] * ypi;                 // g_i -= L[i][p] y_p
+      gi -= mr[p] * ypi + mi[p] * ypr;
+    } else if (lane == p) {
+      gr = ypr; gi = ypi;
+    }
+#pragma unroll
+    for (int c = 0; c < R; ++c) {                      // M[i][c] -= L[i][p] conj(L[c][p]), i >= c > p
+      if (c <= p) continue;                            // (fixed trip count: keeps mr/mi in registers)
+      const double br = __shfl_sync(0xffffffffu, mr[p], c), bi = __shfl_sync(0xffffffffu, mi[p], c);
+      if (lane >= c) {
+        mr[c] -= mr[p] * br + mi[p] * bi;
+        mi[c] -= mi[p] * br - mr[p] * bi;
+      }
+    }
+  }
+  if (bad && lane == 0) atomicOr(info, 1);
+  // transpose L through shared memory: lane c needs L[i][c] for i > c
+  __syncwarp();
+  if (row)
+#pragma unroll
+    for (int c = 0; c < R; ++c)
+      if (c < lane) { Mre[lane * ld + c] = mr[c]; Mim[lane * ld + c] = mi[c]; }
+  __syncwarp();
+  double lr_[R], li_[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const bool in = row && i > lane && i < r;
+    lr_[i] = in ? Mre[i * ld + lane] : 0.0;
+    li_[i] = in ? Mim[i * ld + lane] : 0.0;
+  }
+#pragma unroll
+  for (int i = R - 1; i >= 0; --i) {                   // L^H x = y
+    const double xr = __shfl_sync(0xffffffffu, gr * myid, i), xi = __shfl_sync(0xffffffffu, gi * myid, i);
+    if (lane == i) { gr = xr; gi = xi; }
+    else if (lane < i) {                               // y_c -= conj(L[i][c]) x_i
+      gr -= lr_[i] * xr + li_[i] * xi;
+      gi -= lr_[i] * xi - li_[i] * xr;
+    }
+  }
+  if (row) { gx[2 * lane] = gr; gx[2 * lane + 1] = gi; }
+}
+
+// CTA version for 16 < r <= 32 (shared-memory right-looking Cholesky)
+__device__ void cg_cta_solve(double* Mre, double* Mim, double* gx, int r, int ld, int* info) {
+  const int tid = threadIdx.x;
+  int bad = 0;
+  for (int p = 0; p < r; ++p) {
+    const double dpp = Mre[p * ld + p];
+    const double gpr = gx[2 * p], gpi = gx[2 * p + 1];
+    if (!(dpp > 0.0) || !isfinite(dpp)) bad = 1;
+    const double id = cg_rsqrt(fabs(dpp));
+    const double ypr = gpr * id, ypi = gpi * id;
+    __syncthreads();
+    if (tid == 0) { Mim[p * ld + p] = id; gx[2 * p] = ypr; gx[2 * p + 1] = ypi; }
+    for (int i = p + 1 + tid; i < r; i += CG_NT) { Mre[i * ld + p] *= id; Mim[i * ld + p] *= id; }
+    __syncthreads();
+    const int m = r - p - 1;
+    for (int e = tid; e < m * m + m; e += CG_NT) {
+      if (e < m * m) {
+        const int i = p + 1 + e / m, c = p + 1 + e % m;
+        if (c <= i) {
+          const double ar = Mre[i * ld + p], ai = Mim[i * ld + p], br = Mre[c * ld + p], bi = Mim[c * ld + p];
+          Mre[i * ld + c] -= ar * br + ai * bi;
+          Mim[i * ld + c] -= ai * br - ar * bi;
+        }
+      } else {
+        const int i = p + 1 + (e - m * m);
+        const double lr = Mre[i * ld + p], li = Mim[i * ld + p];
+        gx[2 * i] -= lr * ypr - li * ypi;
+        gx[2 * i + 1] -= lr * ypi + li * ypr;
+      }
+    }
+    __syncthreads();
+  }
+  if (bad && tid == 0) atomicOr(info, 1);
+  if (__shfl_sync(0xffffffffu, tid >> 5, 0) == 0) {
+    const int lane = tid & 31;
+    double yr = lane < r ? gx[2 * lane] : 0.0, yi = lane < r ? gx[2 * lane + 1] : 0.0;
+    const double myid = lane < r ? Mim[lane * ld + lane] : 0.0;
+    for (int i = r - 1; i >= 0; --i) {
+      const double xr = __shfl_sync(0xffffffffu, yr * myid, i), xi = __shfl_sync(0xffffffffu, yi * myid, i);
+      if (lane == i) { yr = xr; yi = xi; }
+      else if (lane < i) {
+        const double lr = Mre[i * ld + lane], li = -Mim[i * ld + lane];
+        yr -= lr * xr - li * xi;
+        yi -= lr * xi + li * xr;
+      }
+    }
+    if (lane < r) { gx[2 * lane] = yr; gx[2 * lane + 1] = yi; }
+  }
+}
+
+__global__ void __launch_bounds__(CG_NT, 1) circ_gs_kernel(const __grid_constant__ CircGsArgs a) {
   extern __shared__ double cg[];
   const int Q = a.Q, r = a.r, rr = r * r, nf = a.nf, tid = threadIdx.x, ld = r + 1;
   const double isq = rsqrt((double)Q);
@@ -697,7 +862,19 @@ __global__ void __launch_bounds__(CG_NT) circ_gs_kernel(const __grid_constant__ 
   double* Hs = scr;                          // [CG_MAXX][rr]
   double* Hgs = Hs + (size_t)CG_MAXX * rr;   // [CG_MAXX][rr]
   unsigned int epoch = 0;
+  long long t_prev = clock64();
   auto wgt = [&](int k) { return (k == 0 || 2 * k == Q) ? 1.0 : 2.0; };
+  // per-lane indexed tables: shared memory, not the (serialising) parameter bank
+  __shared__ CgTabs tb;
+  {
+    const int ra2 = a.ra * a.ra;
+    for (int e = tid; e < a.d * ra2; e += CG_NT) tb.tslot[e] = a.tslot[e];
+    for (int e = tid; e < a.d * ra2; e += CG_NT) tb.pairs[e / ra2][e % ra2] = a.pairs[e / ra2][e % ra2];
+    for (int e = tid; e < a.d * (CG_MAXX + 1); e += CG_NT) tb.pbeg[e / (CG_MAXX + 1)][e % (CG_MAXX + 1)] =
+        a.pbeg[e / (CG_MAXX + 1)][e % (CG_MAXX + 1)];
+    for (int e = tid; e < ra2; e += CG_NT) { tb.KL[e] = a.KL[e]; tb.KR[e] = a.KR[e]; }
+    __syncthreads();
+  }
 
   // ---- (I0) half spectra of the iterate (X, scaled 1/sqrt Q) and of b_old (Bo):
   // work item = (which, mode), the factor and the twiddles staged in shared memory
@@ -747,15 +924,17 @@ __global__ void __launch_bounds__(CG_NT) circ_gs_kernel(const __grid_constant__ 
   cg_grid_sync(a.bar, epoch);
   // ---- (I2) Grams of every mode, H of mode 0
   for (int q = 0; q < a.d; ++q) {
-    cg_entries(a, gc, q, q == a.d - 1 ? 0 : -1);
+    cg_entries(a, tb, gc, q, q == a.d - 1 ? 0 : -1, t_prev);
     __syncthreads();
   }
   cg_grid_sync(a.bar, epoch);
 
   int done = 0;
+  t_prev = clock64();
   for (int sweep = 0; sweep < a.sweeps; ++sweep) {
     for (int q = 0; q < a.d; ++q) {
       const int nx = a.nused[q];
+      CG_PROF(0)
       // ---- (1) frequency phase
       for (int e = tid; e < nx * rr; e += CG_NT) { Hs[e] = __ldcg(a.H + e); Hgs[e] = __ldcg(a.Hg + e); }
       for (int k = blockIdx.x; k < nf; k += gridDim.x) {
@@ -768,6 +947,7 @@ __global__ void __launch_bounds__(CG_NT) circ_gs_kernel(const __grid_constant__ 
           xo[e] = __ldcg(a.X + ((size_t)q * nf + k) * r * 2 + e);
         }
         __syncthreads();
+        CG_PROF(1)
         // gamma^(k)_i = sum_X lambda~_X(k) sum_j Hg_X[i][j] bo_j / sqrt(Q)   (8 lanes per i)
         for (int base = 0; base < 8 * r; base += CG_NT) {
           const int t = base + tid, i = t >> 3, part = t & 7;
@@ -792,9 +972,10 @@ __global__ void __launch_bounds__(CG_NT) circ_gs_kernel(const __grid_constant__ 
           }
           if (i < r && part == 0) { gx[2 * i] = re * isq; gx[2 * i + 1] = im * isq; }
         }
-        // M[i][j] = sum_X H_X[j][i] conj(lambda_X(k)) + lam delta_ij
+        // M[i][j] = sum_X H_X[j][i] conj(lambda_X(k)) + lam delta_ij  (lanes along i:
+        // contiguous H reads, conflict-free padded M writes)
         for (int e = tid; e < rr; e += CG_NT) {
-          const int i = e / r, j = e - i * r;
+          const int j = e / r, i = e - j * r;
           double re = (i == j) ? a.lam : 0.0, im = 0.0;
           for (int x = 0; x < nx; ++x) {
             const double h = Hs[(size_t)x * rr + j * r + i];
@@ -805,54 +986,17 @@ __global__ void __launch_bounds__(CG_NT) circ_gs_kernel(const __grid_constant__ 
           Mim[i * ld + j] = im;
         }
         __syncthreads();
-        // complex Cholesky M = L L^H (lower, in place)
-        int bad = 0;
-        for (int p = 0; p < r; ++p) {
-          const double dpp = Mre[p * ld + p];
-          if (!(dpp > 0.0) || !isfinite(dpp)) bad = 1;
-          const double dg = sqrt(fabs(dpp)), id = 1.0 / dg;
-          __syncthreads();
-          if (tid == 0) { Mre[p * ld + p] = dg; Mim[p * ld + p] = id; }
-          for (int i = p + 1 + tid; i < r; i += CG_NT) { Mre[i * ld + p] *= id; Mim[i * ld + p] *= id; }
-          __syncthreads();
-          const int m = r - p - 1;
-          for (int e = tid; e < m * m; e += CG_NT) {
-            const int i = p + 1 + e / m, c = p + 1 + e % m;
-            if (c <= i) {
-              const double ar = Mre[i * ld + p], ai = Mim[i * ld + p], br = Mre[c * ld + p], bi = Mim[c * ld + p];
-              Mre[i * ld + c] -= ar * br + ai * bi;
-              Mim[i * ld + c] -= ai * br - ar * bi;
-            }
-          }
-          __syncthreads();
+        CG_PROF(2)
+        if (r <= CG_WR) {
+          // warp-uniform by construction (lets the compiler drop the divergent-shuffle wrappers)
+          if (__shfl_sync(0xffffffffu, tid >> 5, 0) == 0) cg_warp_solve<CG_WR>(Mre, Mim, gx, r, ld, a.info);
+        } else {
+          cg_cta_solve(Mre, Mim, gx, r, ld, a.info);
         }
-        if (bad && tid == 0) atomicOr(a.info, 1);
-        if (tid < 32) {
-          const int lane = tid;
-          for (int i = 0; i < r; ++i) {            // L y = g
-            const double idd = Mim[i * ld + i];
-            const double yr = gx[2 * i] * idd, yi = gx[2 * i + 1] * idd;
-            __syncwarp();
-            if (lane == 0) { gx[2 * i] = yr; gx[2 * i + 1] = yi; }
-            for (int c = i + 1 + lane; c < r; c += 32) {
-              const double lr = Mre[c * ld + i], li = Mim[c * ld + i];
-              gx[2 * c] -= lr * yr - li * yi;
-              gx[2 * c + 1] -= lr * yi + li * yr;
-            }
-            __syncwarp();
-          }
-          for (int i = r - 1; i >= 0; --i) {       // L^H x = y
-            const double idd = Mim[i * ld + i];
-            const double xr = gx[2 * i] * idd, xi = gx[2 * i + 1] * idd;
-            __syncwarp();
-            if (lane == 0) { gx[2 * i] = xr; gx[2 * i + 1] = xi; }
-            for (int c = lane; c < i; c += 32) {
-              const double lr = Mre[i * ld + c], li = -Mim[i * ld + c];
-              gx[2 * c] -= lr * xr - li * xi;
-              gx[2 * c + 1] -= lr * xi + li * xr;
-            }
-            __syncwarp();
-          }
+        __syncthreads();
+        CG_PROF(3)
+        if (__shfl_sync(0xffffffffu, tid >> 5, 0) == 0) {
+          const int lane = tid & 31;
           if (k == 0 || 2 * k == Q)
             for (int i = lane; i < r; i += 32) gx[2 * i + 1] = 0.0;   // self-conjugate frequency: real
           __syncwarp();
@@ -872,14 +1016,19 @@ __global__ void __launch_bounds__(CG_NT) circ_gs_kernel(const __grid_constant__ 
           }
         }
         __syncthreads();
+        CG_PROF(4)
         for (int e = tid; e < 2 * r; e += CG_NT) a.X[((size_t)q * nf + k) * r * 2 + e] = gx[e];
         cg_gram_terms(a, q, k, gx, bo, lam, wgt(k));
         __syncthreads();
+        CG_PROF(5)
       }
       cg_grid_sync(a.bar, epoch);
+      CG_PROF(6)
       // ---- (2) entry phase (+ the sweep's relative update after the last mode)
       const bool last = q == a.d - 1;
-      cg_entries(a, gc, q, last ? (sweep + 1 < a.sweeps ? 0 : -1) : q + 1);
+      cg_entries(a, tb, gc, q, last ? (sweep + 1 < a.sweeps ? 0 : -1) : q + 1, t_prev);
+      __syncthreads();
+      CG_PROF(7)
       if (last && blockIdx.x == gridDim.x - 1) {
         __syncthreads();
         if (tid < 32) {
@@ -902,6 +1051,7 @@ __global__ void __launch_bounds__(CG_NT) circ_gs_kernel(const __grid_constant__ 
         }
       }
       cg_grid_sync(a.bar, epoch);
+      CG_PROF(8)
     }
     done = sweep + 1;
     if (*(volatile int*)a.stop) break;   // reference loop condition (implicit.py:244)
@@ -976,11 +1126,14 @@ static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
 using namespace tp;
 
 static int g_circ_fused = 1;   // debug hook: 0 = per-kernel circulant path
+static long long* g_circ_prof = nullptr;
 
 extern "C" {
 
 // debug hook: fused circulant Gauss-Seidel kernel on (1, default) / off (0)
 void tp_debug_set_circ_fused(int on) { g_circ_fused = on; }
+// debug hook: device array of >= 16 int64 receiving per-phase clock64 totals of CTA 0
+void tp_debug_set_circ_prof(long long* p) { g_circ_prof = p; }
 
 size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab) {
   if (d < 1 || d > IM_MAXD || Q < 1 || r < 1 || n_tab < 1 || n_tab > IM_MAXT) return 0;
@@ -1085,7 +1238,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     ga->convp = cv.take<double>((size_t)d * nf * 2);
     ga->bar = cv.take<unsigned int>(32);
     ga->stop = reinterpret_cast<int*>(ga->bar + 16);
-    ga->G = G; ga->Gm = Gm; ga->eps_out = eps_conv; ga->info = info;
+    ga->G = G; ga->Gm = Gm; ga->eps_out = eps_conv; ga->info = info; ga->prof = g_circ_prof;
     int nsm = 0, dev = 0;
     err = cudaGetDevice(&dev);
     if (err == cudaSuccess) err = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
