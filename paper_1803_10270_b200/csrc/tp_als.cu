@@ -76,6 +76,8 @@ struct AlsArgs {
   int Pq, ldw, chunk, nbmax;
   int qoffc[TP_MAXD];      // shared-memory offset of V_k[block rows, slab] ([s][c], stride ldw)
   int ns_max;              // Newton-Schulz iterations before falling back to the exact sweep
+  int clustered;           // als_persistent launched as ONE cluster of P CTAs: cluster barriers
+  int local_gram;          // als_persistent: every CTA forms the whole Gram of the pending mode
 };
 
 struct Smem {
@@ -137,6 +139,23 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ep
     } while ((int)(v - target) < 0);
   }
   __syncthreads();
+}
+
+// All-CTA barrier of als_persistent: a hardware cluster barrier (release/acquire
+// at cluster scope, ~400 cycles) when the whole grid is one cluster, otherwise the
+// global-memory grid barrier (~3K cycles incl. skew).  Cross-CTA data is read
+// through L2 (__ldcg / bulk copies) in both cases.
+__device__ __forceinline__ void all_barrier(const AlsArgs& a, unsigned int& epoch) {
+  if (a.clustered) {
+    // the cluster-scope release alone did not order this CTA's global stores before
+    // the peers' L2 reads (stale G / ovl seen on a fresh workspace): gather the CTA's
+    // stores with bar.sync, then one gpu-scope fence (as the grid barrier's release)
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  } else {
+    grid_barrier(a.bar_ctr, epoch);
+  }
 }
 
 // fast reciprocal: MUFU seed + 2 Newton steps (<= 1 ulp, no slow path)
@@ -243,12 +262,15 @@ __device__ void cross_slab(const AlsArgs& a, const Smem& sm, int k, int w) {
 
 // this CTA's share of G_k = U_k^T U_k (cp.py:318): the upper 8x8 tiles are
 // dealt round-robin to CTAs; each tile is one DMMA chain split over the warps.
-__device__ void gram_share(const AlsArgs& a, const Smem& sm, int k) {
+// local: every CTA forms all tiles into its own sm.Gs (small r: cheaper than the
+// global round trip after the barrier).
+__device__ void gram_share(const AlsArgs& a, const Smem& sm, int k, bool local = false) {
   const int r = a.r, Q = a.q[k], ru = pad4(r), lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int mt = (r + 7) / 8, ntile = mt * (mt + 1) / 2;
   double* Gk = a.G + (size_t)k * r * r;
   const int ksteps = (Q + 3) / 4, per = (ksteps + ALS_NW - 1) / ALS_NW;
-  for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+  const int t0 = local ? 0 : blockIdx.x, tstep = local ? 1 : gridDim.x;
+  for (int t = t0; t < ntile; t += tstep) {
     int ti = 0, rem = t;
     while (rem >= mt - ti) { rem -= mt - ti; ++ti; }
     const int tj = ti + rem, m0 = ti * 8, n0 = tj * 8;
@@ -271,9 +293,11 @@ __device__ void gram_share(const AlsArgs& a, const Smem& sm, int k) {
       for (int w = 0; w < ALS_NW; ++w) acc += sm.part[w * 64 + threadIdx.x];
       const int orow = m0 + (ln >> 2), ocol = n0 + 2 * (ln & 3) + h;
       if (orow < r && ocol < r) {
-        Gk[orow * r + ocol] = acc;
-        Gk[ocol * r + orow] = acc;
-        if (gridDim.x == 1) {   // single CTA: no global round trip for its own Gram
+        if (!local || blockIdx.x == 0) {
+          Gk[orow * r + ocol] = acc;
+          Gk[ocol * r + orow] = acc;
+        }
+        if (gridDim.x == 1 || local) {   // no global round trip for this CTA's own Gram
           sm.Gs[(size_t)k * r * r + orow * r + ocol] = acc;
           sm.Gs[(size_t)k * r * r + ocol * r + orow] = acc;
         }
@@ -587,10 +611,11 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   const int c0 = (int)((long long)R * p / P), c1 = (int)((long long)R * (p + 1) / P), w = c1 - c0;
   const int w4 = (w + 3) / 4 * 4;
   int status = 0;
-  uint32_t bphase = 0, gphase = 0;
+  uint32_t bphase = 0, gphase = 0, xphase = 0;
   if (tid == 0) {
     mbar_init(sm.bar, 1);
     mbar_init(sm.bar + 1, 1);
+    mbar_init(sm.bar + 2, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int k = 0; k < a.d; ++k)
@@ -620,7 +645,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
     cross_slab<RM>(a, sm, k, w);
     gram_share(a, sm, k);
   }
-  grid_barrier(a.bar_ctr, epoch);
+  all_barrier(a, epoch);
   for (int e = tid; e < a.d * rr; e += ALS_NT) sm.Gs[e] = __ldcg(a.G + e);
   __syncthreads();
 
@@ -644,17 +669,17 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         PROF(10);
         if (!(a.dbg_skip & 4)) cross_slab<RM>(a, sm, pending, w);
         PROF(11);
-        if (!(a.dbg_skip & 8)) gram_share(a, sm, pending);
+        if (!(a.dbg_skip & 8)) gram_share(a, sm, pending, a.local_gram != 0);
       }
       if (rows_mode >= 0) {   // warm-start rows of the previous NS solve
         ns_rows<RM>(a, sm, rows_mode, rows_sweep);
         rows_mode = -1;
       }
       const bool warm_ns = sweep > 0 && a.ns_max > 0;
-      if (local && warm_ns && bulk && tid == 0) {   // prefetch this mode's warm start under phase A
+      if (warm_ns && bulk && tid == 0) {   // prefetch this mode's warm start under phase A
         fence_proxy_async();
-        mbar_arrive_expect_tx(sm.bar + 1, (uint32_t)(r * rh) * 8u);
-        bulk_g2s(sm.X0, a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh, (uint32_t)(r * rh) * 8u, sm.bar + 1);
+        mbar_arrive_expect_tx(sm.bar + 2, (uint32_t)(r * rh) * 8u);
+        bulk_g2s(sm.X0, a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh, (uint32_t)(r * rh) * 8u, sm.bar + 2);
       }
       PROF(1);
       const int Qj = a.q[j], qsj = a.qs[j];
@@ -714,7 +739,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         }
       }
       PROF(2);
-      grid_barrier(a.bar_ctr, epoch);
+      all_barrier(a, epoch);
       PROF(3);
       // ---------------- phase B
       const int s0 = (int)((long long)Qj * p / P), s1 = (int)((long long)Qj * (p + 1) / P);
@@ -722,7 +747,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       const int nb = a.ncolmax * r;     // one producer's block for this consumer
       double* ystage = sm.Us;           // [q][nb]
       if (local) {
-        if (warm_ns && bulk) { mbar_wait(sm.bar + 1, gphase); gphase ^= 1u; }
+        if (warm_ns && bulk) { mbar_wait(sm.bar + 2, xphase); xphase ^= 1u; }
         if (warm_ns && !bulk)   // odd r: shared rows not 16-byte aligned for the bulk copy
           for (int e = tid; e < r * rh; e += ALS_NT)
             sm.X0[e] = __ldcg(a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh + e);
@@ -730,18 +755,17 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         if (warm_ns) build_a<RM>(a, sm, j);
       } else if (bulk) {
         if (tid == 0) {
-          const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
+          const uint32_t gbytes = (pending >= 0 && !a.local_gram) ? (uint32_t)rr * 8u : 0u;
           const uint32_t ybytes = (E > 0 && !(a.dbg_skip & 32)) ? (uint32_t)(P * nb) * 8u : 0u;
           fence_proxy_async();
-          const uint32_t xbytes = (sweep > 0 && a.ns_max > 0) ? (uint32_t)(r * rh) * 8u : 0u;
-          mbar_arrive_expect_tx(sm.bar + 1, gbytes + xbytes);
+          mbar_arrive_expect_tx(sm.bar + 1, gbytes);
           if (gbytes) bulk_g2s(sm.Gs + (size_t)pending * rr, a.G + (size_t)pending * rr, gbytes, sm.bar + 1);
-          if (xbytes) bulk_g2s(sm.X0, a.Xprev + ((size_t)(sweep & 1) * a.d + j) * r * rh, xbytes, sm.bar + 1);
           mbar_arrive_expect_tx(sm.bar, ybytes);
           if (ybytes) bulk_g2s(ystage, a.Y + (size_t)p * P * nb, ybytes, sm.bar);
         }
         mbar_wait(sm.bar + 1, gphase);
         gphase ^= 1u;
+        if (warm_ns) { mbar_wait(sm.bar + 2, xphase); xphase ^= 1u; }
         if (warm_ns) build_a<RM>(a, sm, j);   // overlaps the slice fetch
         PROF(8);
         mbar_wait(sm.bar, bphase);
@@ -760,7 +784,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
           sm.rb[o] = (s0 + s1) + (s2 + s3);
         }
       } else {
-        if (pending >= 0)
+        if (pending >= 0 && !a.local_gram)
           for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * rr + e] = __ldcg(a.G + (size_t)pending * rr + e);
         if (sweep > 0 && a.ns_max > 0)
           for (int e = tid; e < r * rh; e += ALS_NT)
@@ -795,7 +819,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       }
       pending = j;
       PROF(6);
-      grid_barrier(a.bar_ctr, epoch);
+      all_barrier(a, epoch);
       PROF(7);
     }
     done = sweep + 1;
@@ -803,7 +827,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       // finish the last mode, then residual by the Gram identity (cp.py:321-326)
       stage_u(a, sm, pending, bphase);
       cross_slab<RM>(a, sm, pending, w);
-      gram_share(a, sm, pending);
+      gram_share(a, sm, pending, a.local_gram != 0);
       double ov = 0.0;
       for (int e = tid; e < r * w; e += ALS_NT) {
         const int l = e / w, c = e % w;
@@ -813,7 +837,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       }
       ov = block_sum(ov, sm.part);
       if (tid == 0) a.ovl[p] = ov;
-      grid_barrier(a.bar_ctr, epoch);
+      all_barrier(a, epoch);
       for (int e = tid; e < rr; e += ALS_NT) sm.Gs[(size_t)pending * rr + e] = __ldcg(a.G + (size_t)pending * rr + e);
       pending = -1;
       __syncthreads();
@@ -1492,16 +1516,19 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
 
 struct AlsPlan {
   AlsArgs a;
-  int P, rm, variant, Pr;   // variant 0: als_persistent, 1: als_cluster (P = Pr * a.Pq), 2: als_small
+  int P, rm, variant, Pr;   // variant 0: als_persistent, 1: als_cluster (P = Pr * a.Pq), 2: als_small,
+                            // 3: als_persistent as one cluster of P CTAs
   size_t smem, ws_inner, ws_total, ydoubles;
 };
 
-static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 force als_cluster, 3 force als_small
+static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 force als_cluster, 3 force als_small,
+                            // 4 force als_persistent as one cluster (grid = cluster size)
 static int g_cluster = 0;   // debug hook: cluster size (0 = auto)
 
 static int choose_rm(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : 0)); }
 
 static const void* kernel_ptr(int rm, int variant) {
+  if (variant == 3) variant = 0;   // als_persistent launched as one cluster
   if (variant == 2) {
     switch (rm) {
       case 8: return (const void*)als_small<8>;
@@ -1579,6 +1606,35 @@ static int plan_cluster(int d, const int* q, int R, int r, int Pq, int smem_opti
 
 static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPlan& pl);
 
+// als_persistent as one cluster of Pc <= 16 CTAs (pl already holds the persistent
+// plan's per-mode offsets; only the grid-dependent fields change)
+static int plan_persistent_cluster(int d, const int* q, int R, int r, int Pc, int smem_optin, AlsPlan& pl) {
+  if (Pc < 2 || Pc > 16 || Pc > R) return TP_EUNSUPPORTED;
+  AlsArgs& a = pl.a;
+  const int wmax = (R + Pc - 1) / Pc, ncolmax = (a.qmax + Pc - 1) / Pc;
+  const size_t smem = als_smem_doubles(d, a.sumqs, r, wmax, ncolmax, a.qmax, Pc) * sizeof(double);
+  if (smem > (size_t)smem_optin) return TP_EUNSUPPORTED;
+  const void* fn = kernel_ptr(pl.rm, 0);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  if (Pc > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = Pc; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(Pc); cfg.blockDim = dim3(ALS_NT); cfg.dynamicSmemBytes = smem; cfg.attrs = at; cfg.numAttrs = 1;
+  int nclu = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclu, fn, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
+  if (nclu < 1) return TP_EUNSUPPORTED;
+  int qo = 0;
+  for (int k = 0; k < d; ++k) { a.qoff[k] = qo; qo += a.qs[k] * wmax; }
+  a.wmax = wmax; a.ncolmax = ncolmax; a.P = Pc; a.Pq = Pc; a.clustered = 1;
+  pl.P = Pc; pl.Pr = Pc; pl.smem = smem; pl.variant = 3;
+  pl.ydoubles = (size_t)Pc * Pc * ncolmax * r;
+  pl.ws_total = ws_total_for(d, q, r, Pc, pl.ydoubles, pl.ws_inner);
+  return TP_OK;
+}
+
 // plans are pure functions of (device, sizes, grid, debug variant): cache them, the
 // cluster occupancy queries cost tens of microseconds per call
 struct PlanKey {
@@ -1652,6 +1708,7 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
     a.offUp[k] = oup;
     ov += (long long)q[k] * R; ou += (long long)q[k] * r; qo += a.qs[k] * a.wmax; oup += (long long)q[k] * pad4(r);
   }
+  a.local_gram = 0;   // (r <= 16 measured slower: 3 tiles recomputed cost more than the round trip)
   pl.P = P;
   pl.smem = smem;
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
@@ -1660,6 +1717,20 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
   pl.ydoubles = (size_t)P * P * a.ncolmax * r;
   pl.ws_total = ws_total_for(d, q, r, P, pl.ydoubles, pl.ws_inner);
   (void)oup;
+  // mid-size problems: the same kernel as ONE cluster of up to 16 CTAs (hardware
+  // cluster barriers instead of the global-memory grid barrier)
+  if (g_variant == 4) {
+    const int Pc = grid > 0 ? grid : (P < 16 ? P : 16);
+    if (plan_persistent_cluster(d, q, R, r, Pc, smem_optin, pl) == TP_OK) return TP_OK;
+    return TP_EUNSUPPORTED;
+  }
+  // measured (tools/als_cl_scan.py): config 3 (Q=64, R=588, r=12) 9.41 -> 8.75 us per
+  // mode update as one 16-CTA cluster instead of 36 CTAs with grid barriers; larger
+  // Q (128) loses, so only short modes take it
+  if (g_variant == 0 && grid <= 0 && P >= 12 && P <= 40 && qmax <= 64) {
+    AlsPlan cp = pl;
+    if (plan_persistent_cluster(d, q, R, r, 16, smem_optin, cp) == TP_OK) { pl = cp; return TP_OK; }
+  }
   // large truncations: the cluster variant (fewer bytes per CTA per mode update)
   const bool want = g_variant == 2 || (g_variant == 0 && grid <= 0 && P >= 64 && g_cluster >= 0);
   if (want) {
@@ -1712,7 +1783,7 @@ int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out) {
   AlsPlan pl;
   const int st = plan_als(d, q, R, r, grid, pl);
   if (st != TP_OK) return st;
-  out[0] = pl.variant; out[1] = pl.P; out[2] = pl.variant == 1 ? pl.a.Pq : 1; out[3] = (int)pl.smem;
+  out[0] = pl.variant; out[1] = pl.P; out[2] = (pl.variant == 1 || pl.variant == 3) ? pl.a.Pq : 1; out[3] = (int)pl.smem;
   return TP_OK;
 }
 
@@ -1764,7 +1835,11 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
   const void* fn = kernel_ptr(pl.rm, pl.variant);
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return cuda_status(e);
-  if (pl.variant == 1) {
+  if (pl.variant == 1 || pl.variant == 3) {
+    if (pl.variant == 3 && pl.P > 8) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return cuda_status(e);
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;

@@ -193,11 +193,12 @@ def als_variant():
     L.tp_debug_set_als_variant(0, 0)
 
 
-@pytest.mark.parametrize("variant,cluster", [(1, 0), (2, 2), (2, 4), (2, 0)])
+@pytest.mark.parametrize("variant,cluster", [(1, 0), (2, 2), (2, 4), (2, 0), (4, 0)])
 @pytest.mark.parametrize("qs,R,r", [((64, 48, 80, 64), 96, 16), ((40, 37, 50), 61, 12), ((32,) * 5, 64, 30)])
 def test_als_kernel_variants(als_variant, variant, cluster, qs, R, r):
     """Both persistent kernels (R-slab per CTA; clusters of row blocks with the DSMEM
-    cross all-reduce) on ragged mode sizes / slab widths, with the residual trace."""
+    cross all-reduce; variant 4 = the R-slab kernel as ONE cluster with hardware
+    cluster barriers) on ragged mode sizes / slab widths, with the residual trace."""
     als_variant(variant, cluster)
     rng = np.random.default_rng(R + r)
     V = rand_factors(rng, qs, R, 0.25)
