@@ -39,7 +39,8 @@ int launch_inner(int d, const int* q, int ra, const double* A, int rb, const dou
 
 constexpr int ALS_NT = 256;
 constexpr int ALS_NW = ALS_NT / 32;
-constexpr int ALS_PART = 512;   // doubles of scratch for split-K partial tiles / reductions
+constexpr int ALS_PART = 512;
+constexpr int ALS_SMALL_NT8 = 512;   // als_small block size for r <= 8 (no 256-thread inverse mapping)   // doubles of scratch for split-K partial tiles / reductions
 
 // padded shared-memory row stride: >= n and == 4 (mod 16) doubles, so DMMA
 // fragment loads (4 rows x 8 columns per half-warp) hit distinct banks
@@ -158,15 +159,6 @@ __device__ __forceinline__ void all_barrier(const AlsArgs& a, unsigned int& epoc
   }
 }
 
-// fast reciprocal: MUFU seed + 2 Newton steps (<= 1 ulp, no slow path)
-__device__ __forceinline__ double rcp_nr(double d) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-  double e = fma(-d, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-d, y, 1.0);
-  return fma(y, e, y);
-}
 
 // Stage U_k (Q_k x r, written by other CTAs) into sm.Us with rows padded to
 // pad4(r) (conflict-free DMMA fragments): one bulk async copy of the padded
@@ -307,11 +299,12 @@ __device__ void gram_share(const AlsArgs& a, const Smem& sm, int k, bool local =
 }
 
 // deterministic block sum (all threads call; result valid in all threads)
+template <int NT = ALS_NT>
 __device__ inline double block_sum(double v, double* red) {
   const int tid = threadIdx.x;
   red[tid] = v;
   __syncthreads();
-  for (int w = ALS_NT / 2; w > 0; w >>= 1) {
+  for (int w = NT / 2; w > 0; w >>= 1) {
     if (tid < w) red[tid] += red[tid + w];
     __syncthreads();
   }
@@ -886,14 +879,79 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
 // planner's grid is one CTA and the problem fits (config 0).
 // ===========================================================================
 
+// A_j = prod_{k != j} G_k + lambda I (r <= 8) inverted by ONE warp with the
+// symmetric sweep operator of gram_inverse (same pivot order and update formulas),
+// elements in registers: lane t owns row t/4, columns t%4 and t%4 + 4; the pivot
+// row is broadcast by shuffles instead of a shared-memory hand-off + block barrier.
+// Writes A^-1 to out (row stride os); returns 1 if a pivot is not positive/finite.
+__device__ int warp_sweep_inverse8(const AlsArgs& a, const double* Gs, int j, double* out, int os) {
+  const int r = a.r, rr = r * r, t = threadIdx.x & 31, i = t >> 2, cq = t & 3;
+  double v[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int c = cq + 4 * u;
+    double x = 0.0;
+    if (i < r && c < r) {
+      double f[TP_MAXD];
+#pragma unroll
+      for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < a.d && k != j) ? Gs[(size_t)k * rr + i * r + c] : 1.0;
+      x = 1.0;
+#pragma unroll
+      for (int k = 0; k < TP_MAXD; ++k) x *= f[k];
+    }
+    v[u] = x;
+  }
+  double lam = a.reg;
+  if (a.reg_mode) {   // reg * max(tr A, 0) / r  (cp.py:171-173)
+    double dg = 0.0;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) dg += (cq + 4 * u == i && i < r) ? v[u] : 0.0;
+    lam = a.reg * fmax(warp_sum(dg), 0.0) / (double)r;
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    if (cq + 4 * u == i && i < r) v[u] += lam;
+  int bad = 0;
+  for (int k = 0; k < r; ++k) {
+    const int srow = k << 2;
+    const double rk0 = __shfl_sync(0xffffffffu, v[0], srow | cq);     // a_k,cq
+    const double rk1 = __shfl_sync(0xffffffffu, v[1], srow | cq);     // a_k,cq+4
+    const double ri0 = __shfl_sync(0xffffffffu, v[0], srow | (i & 3));
+    const double ri1 = __shfl_sync(0xffffffffu, v[1], srow | (i & 3));
+    const double dk0 = __shfl_sync(0xffffffffu, v[0], srow | (k & 3));
+    const double dk1 = __shfl_sync(0xffffffffu, v[1], srow | (k & 3));
+    const double dd = (k >> 2) ? dk1 : dk0;                              // a_kk
+    if (!(dd > 0.0) || !isfinite(dd)) bad = 1;
+    const double id = rcp_nr(dd);
+    const double aik = (i < r) ? ((i >> 2) ? ri1 : ri0) : 0.0;          // a_ik == a_ki
+    const double f = aik * id;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = cq + 4 * u;
+      const double akc = u ? rk1 : rk0;
+      double nv = fma(-f, akc, v[u]);
+      nv = (c == k) ? f : nv;
+      nv = (i == k) ? ((c == k) ? -id : akc * id) : nv;
+      v[u] = nv;
+    }
+  }
+  if (i < r)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = cq + 4 * u;
+      if (c < r) out[i * os + c] = -v[u];
+    }
+  return bad;
+}
+
 __host__ __device__ inline size_t sm_small_doubles(int d, int sumq, int qmax, int R, int r) {
   const size_t rp = (size_t)r + 1;
   return 8 + (size_t)sumq * R + (size_t)sumq * r + (size_t)d * r * R + (size_t)d * r * r + (size_t)R * r +
          (size_t)qmax * r + 2 * r * rp + 72 + ALS_PART + 8;
 }
 
-template <int RM>
-__global__ void __launch_bounds__(ALS_NT, 1) als_small(const __grid_constant__ AlsArgs a) {
+template <int RM, int NT>
+__global__ void __launch_bounds__(NT, 1) als_small(const __grid_constant__ AlsArgs a) {
   extern __shared__ double smem[];
   const int tid = threadIdx.x, d = a.d, r = a.r, R = a.R, rr = r * r, rp = r + 1;
   int sumq = 0;
@@ -915,35 +973,32 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_small(const __grid_constant__ A
   sm.pub = Ai + (size_t)r * rp;
   sm.part = sm.pub + 72;
   sm.scal = sm.part + ALS_PART;
-  for (int e = tid; e < sumq * R; e += ALS_NT) Vs[e] = a.V[e];
-  for (int e = tid; e < sumq * r; e += ALS_NT) Us[e] = a.U[e];
+  for (int e = tid; e < sumq * R; e += NT) Vs[e] = a.V[e];
+  for (int e = tid; e < sumq * r; e += NT) Us[e] = a.U[e];
   __syncthreads();
   // crosses and Grams of mode k from Us / Vs
   auto refresh = [&](int k) {
     const double* Uk = Us + (size_t)qo[k] * r;
     const double* Vk = Vs + (size_t)qo[k] * R;
     const int Q = a.q[k], n1 = r * R, n2 = n1 + rr;
-    for (int o = tid; o < n2; o += ALS_NT) {
-      double s0 = 0.0, s1 = 0.0;
-      if (o < n1) {          // C_k[l][c], lanes along c
-        const int l = o / R, c = o - l * R;
-        int s = 0;
-        for (; s + 2 <= Q; s += 2) {
-          s0 = fma(Uk[s * r + l], Vk[(size_t)s * R + c], s0);
-          s1 = fma(Uk[(s + 1) * r + l], Vk[(size_t)(s + 1) * R + c], s1);
-        }
-        if (s < Q) s0 = fma(Uk[s * r + l], Vk[(size_t)s * R + c], s0);
-        Cs[(size_t)k * n1 + o] = s0 + s1;
-      } else {               // G_k[l][m]
-        const int g = o - n1, l = g / r, m = g - l * r;
-        int s = 0;
-        for (; s + 2 <= Q; s += 2) {
-          s0 = fma(Uk[s * r + l], Uk[s * r + m], s0);
-          s1 = fma(Uk[(s + 1) * r + l], Uk[(s + 1) * r + m], s1);
-        }
-        if (s < Q) s0 = fma(Uk[s * r + l], Uk[s * r + m], s0);
-        Gsm[(size_t)k * rr + g] = s0 + s1;
+    for (int o = tid; o < n2; o += NT) {
+      // C_k[l][c] (lanes along c) or G_k[l][m]: sum_s U[s][l] X[s][c], four
+      // independent accumulators so the shared loads of 4 rows are in flight together
+      const bool isc = o < n1;
+      const int g = isc ? o : o - n1, w = isc ? R : r, l = g / w, c = g - l * w;
+      const double* X = isc ? Vk : Uk;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int s = 0;
+      for (; s + 4 <= Q; s += 4) {
+        s0 = fma(Uk[s * r + l], X[(size_t)s * w + c], s0);
+        s1 = fma(Uk[(s + 1) * r + l], X[(size_t)(s + 1) * w + c], s1);
+        s2 = fma(Uk[(s + 2) * r + l], X[(size_t)(s + 2) * w + c], s2);
+        s3 = fma(Uk[(s + 3) * r + l], X[(size_t)(s + 3) * w + c], s3);
       }
+      for (; s < Q; ++s) s0 = fma(Uk[s * r + l], X[(size_t)s * w + c], s0);
+      const double v = (s0 + s1) + (s2 + s3);
+      if (isc) Cs[(size_t)k * n1 + o] = v;
+      else Gsm[(size_t)k * rr + g] = v;
     }
   };
   for (int k = 0; k < d; ++k) refresh(k);
@@ -952,66 +1007,101 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_small(const __grid_constant__ A
   const double t_norm = sqrt(norm_sq);
   double prev = INFINITY;
   int status = 0, done = 0;
+  long long prof_acc[6] = {}, prof_t = clock64();
+  double prof_sink = 0.0;
+  auto mark = [&](int ph) {   // debug phase timers (a.prof): clock64 after each block barrier
+    if (a.prof) {
+      prof_sink += *(volatile double*)sm.scal;
+      const long long now = clock64();
+      prof_acc[ph] += now - prof_t;
+      prof_t = now;
+    }
+  };
   for (int sweep = 0; sweep < a.sweeps; ++sweep) {
     for (int j = 0; j < d; ++j) {
       const int Qj = a.q[j];
-      // 1. Hadamards
-      for (int e = tid; e < r * R; e += ALS_NT) {   // lanes along c (contiguous Cs rows)
+      mark(5);
+      // 1. Hadamards (independent loads of the d-1 factors, then the product)
+      for (int e = tid; e < r * R; e += NT) {   // lanes along c (contiguous Cs rows)
         const int l = e / R, c = e - l * R;
+        double f[TP_MAXD];
+#pragma unroll
+        for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < d && k != j) ? Cs[((size_t)k * r + l) * R + c] : 1.0;
         double v = 1.0;
-        for (int k = 0; k < d; ++k)
-          if (k != j) v *= Cs[((size_t)k * r + l) * R + c];
+#pragma unroll
+        for (int k = 0; k < TP_MAXD; ++k) v *= f[k];
         had[c * r + l] = v;
       }
       __syncthreads();
-      // 2. right-hand side rows, and 3. the inverse (the sweep builds A itself)
-      for (int o = tid; o < Qj * r; o += ALS_NT) {
-        const int s = o / r, l = o - s * r;
-        const double* vrow = Vs + (size_t)(qo[j] + s) * R;
-        double s0 = 0.0, s1 = 0.0;
-        int c = 0;
-        for (; c + 2 <= R; c += 2) {
-          s0 = fma(vrow[c], had[c * r + l], s0);
-          s1 = fma(vrow[c + 1], had[(c + 1) * r + l], s1);
+      mark(0);
+      // 2. right-hand side rows; 3. the inverse.  r <= 8: warp 0 inverts A_j by the
+      // symmetric sweep with shuffles while the other warps form the right-hand side
+      const bool winv = RM == 8;
+      const int t0 = winv ? 32 : 0;
+      if (winv && tid < 32) {
+        status |= warp_sweep_inverse8(a, Gsm, j, Ai, rp);
+      } else {
+        for (int o = tid - t0; o < Qj * r; o += NT - t0) {
+          const int s = o / r, l = o - s * r;
+          const double* vrow = Vs + (size_t)(qo[j] + s) * R;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          int c = 0;
+          for (; c + 4 <= R; c += 4) {
+            s0 = fma(vrow[c], had[c * r + l], s0);
+            s1 = fma(vrow[c + 1], had[(c + 1) * r + l], s1);
+            s2 = fma(vrow[c + 2], had[(c + 2) * r + l], s2);
+            s3 = fma(vrow[c + 3], had[(c + 3) * r + l], s3);
+          }
+          for (; c < R; ++c) s0 = fma(vrow[c], had[c * r + l], s0);
+          rhs[o] = (s0 + s1) + (s2 + s3);
         }
-        if (c < R) s0 = fma(vrow[c], had[c * r + l], s0);
-        rhs[o] = s0 + s1;
       }
       __syncthreads();
-      status |= gram_inverse<RM>(a, sm, j, Ai, rp);
-      __syncthreads();
+      if (!winv) {
+        status |= gram_inverse<RM>(a, sm, j, Ai, rp);
+        __syncthreads();
+      }
+      mark(1);
       // 4. U_j[s][i] = sum_m A^-1[i][m] rhs[s][m]
       double* Uj = Us + (size_t)qo[j] * r;
       int nf = 0;
-      for (int o = tid; o < Qj * r; o += ALS_NT) {
+      for (int o = tid; o < Qj * r; o += NT) {
         const int s = o / r, i = o - s * r;
-        double acc = 0.0;
-        for (int m = 0; m < r; ++m) acc = fma(Ai[i * rp + m], rhs[s * r + m], acc);
+        double a0 = 0.0, a1 = 0.0;
+        int m = 0;
+        for (; m + 2 <= r; m += 2) {
+          a0 = fma(Ai[i * rp + m], rhs[s * r + m], a0);
+          a1 = fma(Ai[i * rp + m + 1], rhs[s * r + m + 1], a1);
+        }
+        if (m < r) a0 = fma(Ai[i * rp + m], rhs[s * r + m], a0);
+        const double acc = a0 + a1;
         if (!isfinite(acc)) nf = 1;
         Uj[o] = acc;
       }
       if (nf) atomicOr(a.info, 2);
       __syncthreads();
+      mark(2);
       // 5. refresh C_j, G_j
       refresh(j);
       __syncthreads();
+      mark(3);
     }
     done = sweep + 1;
     if (a.need_resid) {   // residual by the Gram identity (cp.py:321-326), identical in every thread
       double ov = 0.0, self = 0.0;
-      for (int e = tid; e < r * R; e += ALS_NT) {
+      for (int e = tid; e < r * R; e += NT) {
         const int l = e / R, c = e - l * R;
         double v = 1.0;
         for (int k = 0; k < d; ++k) v *= Cs[((size_t)k * r + l) * R + c];
         ov += v;
       }
-      for (int e = tid; e < rr; e += ALS_NT) {
+      for (int e = tid; e < rr; e += NT) {
         double v = 1.0;
         for (int k = 0; k < d; ++k) v *= Gsm[(size_t)k * rr + e];
         self += v;
       }
-      ov = block_sum(ov, sm.part);
-      self = block_sum(self, sm.part);
+      ov = block_sum<NT>(ov, sm.part);
+      self = block_sum<NT>(self, sm.part);
       const double resid = sqrt(fmax(norm_sq - 2.0 * ov + self, 0.0));
       if (tid == 0 && a.trace) a.trace[sweep] = resid;
       if (resid <= a.tol * t_norm) break;
@@ -1019,9 +1109,13 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_small(const __grid_constant__ A
       prev = resid;
     }
   }
-  for (int e = tid; e < sumq * r; e += ALS_NT) a.U[e] = Us[e];
+  for (int e = tid; e < sumq * r; e += NT) a.U[e] = Us[e];
   if (status && tid == 0) atomicOr(a.info, 1);
   if (tid == 0) a.info[1] = done;
+  if (a.prof && tid == 0) {
+    for (int q = 0; q < 6; ++q) a.prof[q] += prof_acc[q];
+    if (prof_sink == 12345.0) a.prof[11] += 1;
+  }
 }
 
 // ===========================================================================
@@ -1531,9 +1625,9 @@ static const void* kernel_ptr(int rm, int variant) {
   if (variant == 3) variant = 0;   // als_persistent launched as one cluster
   if (variant == 2) {
     switch (rm) {
-      case 8: return (const void*)als_small<8>;
-      case 16: return (const void*)als_small<16>;
-      default: return (const void*)als_small<32>;
+      case 8: return (const void*)als_small<8, ALS_SMALL_NT8>;
+      case 16: return (const void*)als_small<16, ALS_NT>;
+      default: return (const void*)als_small<32, ALS_NT>;
     }
   }
   if (variant == 1) {
@@ -1858,11 +1952,12 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
     return cuda_status(e);
   }
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ALS_NT, pl.smem);
+  const int nt = (pl.variant == 2 && pl.rm == 8) ? ALS_SMALL_NT8 : ALS_NT;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, pl.smem);
   if (e != cudaSuccess) return cuda_status(e);
   if (per_sm < 1) return TP_EUNSUPPORTED;
   void* args[] = {&a};
-  e = cudaLaunchCooperativeKernel(fn, dim3(pl.P), dim3(ALS_NT), args, pl.smem, s);
+  e = cudaLaunchCooperativeKernel(fn, dim3(pl.P), dim3(nt), args, pl.smem, s);
   return cuda_status(e);
 }
 
