@@ -244,7 +244,8 @@ def als_plan(qs, R: int, r: int, grid: int = 0) -> dict:
     out = (ctypes.c_int * 4)()
     st = _lib.lib().tp_cp_als_plan(len(qs), _lib.int_array(qs), R, r, grid, out)
     _lib.check(st, "als_plan")
-    variant = {0: "als_persistent", 1: "als_cluster", 2: "als_small", 3: "als_persistent_cluster"}[out[0]]
+    variant = {0: "als_persistent", 1: "als_cluster", 2: "als_small", 3: "als_persistent_cluster",
+               5: "als_tiny8"}[out[0]]
     return {"kernel": variant, "ctas": out[1], "cluster": out[2], "smem_bytes": out[3]}
 
 

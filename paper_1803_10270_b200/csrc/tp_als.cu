@@ -474,7 +474,8 @@ __device__ __forceinline__ double2 mv_dot_abs(const double* M, int ld, const dou
 // Otherwise (first sweep, or the check fails in this CTA) the exact
 // symmetric-sweep inverse, whose owned rows are stored directly.
 template <int RM>
-__device__ bool solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, int E, int& status) {
+__device__ bool solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, int E, int& status,
+                           unsigned int& ns_fail) {
   constexpr int TPO = RM / 8;
   const int r = a.r, rh = pad4(r), P = gridDim.x, p = blockIdx.x, tid = threadIdx.x;
   const int nv = a.ncolmax * r;
@@ -485,7 +486,13 @@ __device__ bool solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, i
   // (sweep & 1) and writes the other, so results do not depend on CTA timing
   double* Xn = a.Xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;
   bool ok = false;
-  if (sweep > 0 && a.ns_max > 0) {
+  // after a failed Newton-Schulz check (ill-conditioned normal equations) this CTA
+  // goes straight to the exact inverse for that mode in the next sweep, then
+  // retries (measured on config 3 data: a failed attempt costs ~2K cycles on top
+  // of the exact path)
+  const bool try_ns = !((ns_fail >> j) & 1u);
+  ns_fail &= ~(1u << j);
+  if (try_ns && sweep > 0 && a.ns_max > 0) {
     // stage 1: z = X0' b
     for (int base = 0; base < E * TPO; base += ALS_NT) {
       const int t = base + tid, o = t / TPO, part = t - o * TPO;
@@ -523,6 +530,7 @@ __device__ bool solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, i
       if (act && part == 0 && !(fabs(sm.rb[o] - au.x) <= 1e-13 * (double)r * au.y)) bad = 1;
     }
     ok = !__syncthreads_or(bad);
+    if (!ok) ns_fail |= 1u << j;
   }
   if (ok) return true;
   status |= gram_inverse<RM>(a, sm, j, sm.X0, rh);
@@ -646,6 +654,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   const double t_norm = sqrt(norm_sq);
   double prev = INFINITY;
   int pending = -1, done = 0, rows_mode = -1, rows_sweep = 0;
+  unsigned int ns_fail = 0;   // modes whose Newton-Schulz check failed in this CTA
   const bool bulk = (r & 1) == 0;
   // single-CTA grid: the right-hand side, the Gram and the new factor stay in
   // shared memory (no Y / G / U round trips through global memory)
@@ -792,7 +801,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       }
       __syncthreads();
       PROF(4);
-      if (!(a.dbg_skip & 1) && solve_mode<RM>(a, sm, j, sweep, E, status)) { rows_mode = j; rows_sweep = sweep; }
+      if (!(a.dbg_skip & 1) && solve_mode<RM>(a, sm, j, sweep, E, status, ns_fail)) { rows_mode = j; rows_sweep = sweep; }
       PROF(9);
       if (E > 0) {
         const double* ub = sm.vb + 2 * a.ncolmax * r;
@@ -1110,6 +1119,219 @@ __global__ void __launch_bounds__(NT, 1) als_small(const __grid_constant__ AlsAr
     }
   }
   for (int e = tid; e < sumq * r; e += NT) a.U[e] = Us[e];
+  if (status && tid == 0) atomicOr(a.info, 1);
+  if (tid == 0) a.info[1] = done;
+  if (a.prof && tid == 0) {
+    for (int q = 0; q < 6; ++q) a.prof[q] += prof_acc[q];
+    if (prof_sink == 12345.0) a.prof[11] += 1;
+  }
+}
+
+// ===========================================================================
+// Tiny-problem variant for r <= 8 (config 0): one CTA of 512 threads with the
+// whole problem in shared memory like als_small, but every contraction on the
+// DMMA pipe over zero-padded operands (modes padded to 8-row tiles, R to a
+// multiple of 8 with a conflict-free row stride, r to 8):
+//   1. had[c][l] = prod_{k!=j} C_k[l][c]
+//   2. rhs = V_j had (M = s, N = l, K = c split over warps 1..15)  |  warp 0:
+//      A_j^-1 by the shuffle sweep (warp_sweep_inverse8)
+//   3. U_j = rhs A_j^-1 (sums the K-split partials in its fragment loads)
+//   4. C_j = U_j^T V_j and G_j = U_j^T U_j (one warp per 8-column tile)
+// Four block barriers per mode update; same algorithm as cp.py:311-320.
+// ===========================================================================
+constexpr int TINY_NT = 512, TINY_NW = TINY_NT / 32, TINY_KSMAX = 4;
+constexpr int TINY_PLD = 12;   // row stride of the right-hand-side partials (2-way, not 4-way, bank use)
+
+struct TinyDims {
+  int R8, Rs, sumqp, qmaxp;
+  int qp[TP_MAXD], qo[TP_MAXD];
+};
+
+__host__ __device__ inline void tiny_dims(const int* q, int d, int R, TinyDims& t) {
+  t.R8 = (R + 7) & ~7;
+  t.Rs = pad4(t.R8);
+  t.sumqp = 0; t.qmaxp = 0;
+  for (int k = 0; k < d; ++k) {
+    t.qp[k] = (q[k] + 7) & ~7;
+    t.qo[k] = t.sumqp;
+    t.sumqp += t.qp[k];
+    t.qmaxp = t.qp[k] > t.qmaxp ? t.qp[k] : t.qmaxp;
+  }
+}
+
+__host__ __device__ inline size_t tiny_smem_doubles(int d, int r, const TinyDims& t) {
+  return 8 + (size_t)t.sumqp * t.Rs + (size_t)t.sumqp * 8 + (size_t)d * 8 * t.Rs + (size_t)d * r * r +
+         (size_t)t.R8 * 8 + (size_t)TINY_KSMAX * t.qmaxp * TINY_PLD + 64 + ALS_PART + 8;
+}
+
+__global__ void __launch_bounds__(TINY_NT, 1) als_tiny8(const __grid_constant__ AlsArgs a) {
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  const int d = a.d, r = a.r, R = a.R, rr = r * r;
+  TinyDims td;
+  tiny_dims(a.q, d, R, td);
+  const int Rs = td.Rs, R8 = td.R8;
+  double* scal = smem;                               // [8]
+  double* Vs = smem + 8;                             // [sumqp][Rs]
+  double* Us = Vs + (size_t)td.sumqp * Rs;           // [sumqp][8]
+  double* Cs = Us + (size_t)td.sumqp * 8;            // [d][8][Rs]
+  double* Gsm = Cs + (size_t)d * 8 * Rs;             // [d][r][r]
+  double* had = Gsm + (size_t)d * rr;                // [R8][8]
+  double* part = had + (size_t)R8 * 8;               // [KS][qmaxp][TINY_PLD]
+  double* Ai = part + (size_t)TINY_KSMAX * td.qmaxp * TINY_PLD;   // [8][8]
+  double* red = Ai + 64;                             // [ALS_PART]
+  const size_t total = tiny_smem_doubles(d, r, td);
+  for (size_t e = tid; e < total; e += TINY_NT) smem[e] = 0.0;   // all padding stays zero
+  __syncthreads();
+  for (int k = 0; k < d; ++k) {
+    const int Q = a.q[k];
+    const double* Vk = a.V + a.offV[k];
+    for (int e = tid; e < Q * R; e += TINY_NT) {
+      const int s = e / R, c = e - s * R;
+      Vs[(size_t)(td.qo[k] + s) * Rs + c] = Vk[e];
+    }
+    const double* Uk = a.U + a.offU[k];
+    for (int e = tid; e < Q * r; e += TINY_NT) {
+      const int s = e / r, l = e - s * r;
+      Us[(td.qo[k] + s) * 8 + l] = Uk[e];
+    }
+  }
+  __syncthreads();
+  // C_k = U_k^T V_k (8 x R8 tiles) and G_k = U_k^T U_k: item n < R8/8 is C tile n,
+  // item R8/8 the Gram tile; K = the padded rows of mode k
+  const int ntc = R8 / 8;
+  auto refresh_item = [&](int k, int n) {
+    const int ks = td.qp[k] / 4;
+    const double* ua = Us + (size_t)td.qo[k] * 8;
+    const double* vb = (n < ntc) ? Vs + (size_t)td.qo[k] * Rs + n * 8 : ua;
+    const int ldb = (n < ntc) ? Rs : 8;
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < ks; ++kk) {
+      const int srow = 4 * kk + t4;
+      dmma_8x8x4(c0, c1, ua[srow * 8 + g], vb[(size_t)srow * ldb + g]);
+    }
+    if (n < ntc) {
+      double* crow = Cs + ((size_t)k * 8 + g) * Rs + n * 8 + 2 * t4;
+      crow[0] = c0; crow[1] = c1;
+    } else if (g < r) {
+      if (2 * t4 < r) Gsm[(size_t)k * rr + g * r + 2 * t4] = c0;
+      if (2 * t4 + 1 < r) Gsm[(size_t)k * rr + g * r + 2 * t4 + 1] = c1;
+    }
+  };
+  for (int it = warp; it < d * (ntc + 1); it += TINY_NW) refresh_item(it / (ntc + 1), it % (ntc + 1));
+  __syncthreads();
+  const double norm_sq = a.need_resid ? fmax(*a.norm_sq, 0.0) : 0.0;
+  const double t_norm = sqrt(norm_sq);
+  double prev = INFINITY;
+  int status = 0, done = 0;
+  long long prof_acc[6] = {}, prof_t = clock64();
+  double prof_sink = 0.0;
+  auto mark = [&](int ph) {   // debug phase timers (a.prof): clock64 after each block barrier
+    if (a.prof) {
+      prof_sink += *(volatile double*)scal;
+      const long long now = clock64();
+      prof_acc[ph] += now - prof_t;
+      prof_t = now;
+    }
+  };
+  for (int sweep = 0; sweep < a.sweeps; ++sweep) {
+    for (int j = 0; j < d; ++j) {
+      const int Qj = a.q[j], mt = td.qp[j] / 8;
+      mark(5);
+      // 1.+2. warp 0 inverts A_j (its Grams are final since the previous refresh)
+      // while warps 1.. form had[c][l] = prod_{k != j} C_k[l][c] (rows l >= r and
+      // columns c >= R are zero), meet at a named barrier, then the K-split
+      // partial right-hand sides part[ks][s][l] = sum_c V_j[s][c] had[c][l]
+      int ksn = (TINY_NW - 1) / mt;
+      ksn = ksn < 1 ? 1 : (ksn > TINY_KSMAX ? TINY_KSMAX : ksn);
+      if (warp == 0) {
+        status |= warp_sweep_inverse8(a, Gsm, j, Ai, 8);
+        if (a.prof) prof_acc[4] += clock64() - prof_t;   // inverse alone (debug)
+      } else {
+        for (int e = tid - 32; e < R8 * 8; e += TINY_NT - 32) {
+          const int c = e >> 3, l = e & 7;
+          double f[TP_MAXD];
+#pragma unroll
+          for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < d && k != j) ? Cs[((size_t)k * 8 + l) * Rs + c] : 1.0;
+          double v = 1.0;
+#pragma unroll
+          for (int k = 0; k < TP_MAXD; ++k) v *= f[k];
+          had[e] = v;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(TINY_NT - 32) : "memory");
+        mark(0);
+        const int ksteps = R8 / 4;
+        const double* va = Vs + (size_t)td.qo[j] * Rs;
+        for (int it = warp - 1; it < mt * ksn; it += TINY_NW - 1) {
+          const int m = it / ksn, ks = it - m * ksn;
+          const int kb = ksteps * ks / ksn, ke = ksteps * (ks + 1) / ksn;
+          const double* arow = va + (size_t)(m * 8 + g) * Rs + t4;
+          const double* bcol = had + t4 * 8 + g;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll 4
+          for (int kk = kb; kk < ke; ++kk) dmma_8x8x4(c0, c1, arow[4 * kk], bcol[32 * kk]);
+          double* pr = part + ((size_t)ks * td.qmaxp + m * 8 + g) * TINY_PLD + 2 * t4;
+          pr[0] = c0; pr[1] = c1;
+        }
+      }
+      __syncthreads();
+      mark(1);
+      // 3. U_j[s][i] = sum_m rhs[s][m] A^-1[m][i]  (K = 8: two k-steps)
+      if (warp < mt) {
+        const int s = warp * 8 + g;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int m = 4 * kk + t4;
+          double av = 0.0;
+          for (int ks = 0; ks < ksn; ++ks) av += part[((size_t)ks * td.qmaxp + s) * TINY_PLD + m];
+          dmma_8x8x4(c0, c1, av, Ai[m * 8 + g]);
+        }
+        if (!isfinite(c0) || !isfinite(c1)) atomicOr(a.info, 2);
+        if (s < Qj) {
+          double* ur = Us + (size_t)(td.qo[j] + s) * 8 + 2 * t4;
+          ur[0] = c0; ur[1] = c1;
+        }
+      }
+      __syncthreads();
+      mark(2);
+      // 4. C_j, G_j
+      for (int it = warp; it <= ntc; it += TINY_NW) refresh_item(j, it);
+      __syncthreads();
+      mark(3);
+    }
+    done = sweep + 1;
+    if (a.need_resid) {   // residual by the Gram identity (cp.py:321-326), identical in every thread
+      double ov = 0.0, self = 0.0;
+      for (int e = tid; e < r * R; e += TINY_NT) {
+        const int l = e / R, c = e - l * R;
+        double v = 1.0;
+        for (int k = 0; k < d; ++k) v *= Cs[((size_t)k * 8 + l) * Rs + c];
+        ov += v;
+      }
+      for (int e = tid; e < rr; e += TINY_NT) {
+        double v = 1.0;
+        for (int k = 0; k < d; ++k) v *= Gsm[(size_t)k * rr + e];
+        self += v;
+      }
+      ov = block_sum<TINY_NT>(ov, red);
+      self = block_sum<TINY_NT>(self, red);
+      const double resid = sqrt(fmax(norm_sq - 2.0 * ov + self, 0.0));
+      if (tid == 0 && a.trace) a.trace[sweep] = resid;
+      if (resid <= a.tol * t_norm) break;
+      if (prev - resid < a.stall * fmax(t_norm, 1.0)) break;
+      prev = resid;
+    }
+  }
+  (void)scal;
+  for (int k = 0; k < d; ++k) {
+    double* Uk = a.U + a.offU[k];
+    for (int e = tid; e < a.q[k] * r; e += TINY_NT) {
+      const int s = e / r, l = e - s * r;
+      Uk[e] = Us[(td.qo[k] + s) * 8 + l];
+    }
+  }
   if (status && tid == 0) atomicOr(a.info, 1);
   if (tid == 0) a.info[1] = done;
   if (a.prof && tid == 0) {
@@ -1450,6 +1672,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
   const double t_norm = sqrt(norm_sq);
   double prev = INFINITY;
   int pending = -1, done = 0, rows_mode = -1, rows_sweep = 0;
+  unsigned int ns_fail = 0;   // modes whose Newton-Schulz check failed in this CTA
   const bool bulk = (r & 1) == 0;
 
   for (int sweep = 0; sweep < a.sweeps; ++sweep) {
@@ -1534,7 +1757,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
       }
       __syncthreads();
       PROF(4);
-      if (solve_mode<RM>(a, sm, j, sweep, E, status)) { rows_mode = j; rows_sweep = sweep; }
+      if (solve_mode<RM>(a, sm, j, sweep, E, status, ns_fail)) { rows_mode = j; rows_sweep = sweep; }
       PROF(9);
       if (E > 0) {
         const double* ub = sm.vb + 2 * a.ncolmax * r;
@@ -1611,17 +1834,18 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
 struct AlsPlan {
   AlsArgs a;
   int P, rm, variant, Pr;   // variant 0: als_persistent, 1: als_cluster (P = Pr * a.Pq), 2: als_small,
-                            // 3: als_persistent as one cluster of P CTAs
+                            // 3: als_persistent as one cluster of P CTAs, 5: als_tiny8 (r <= 8, one CTA)
   size_t smem, ws_inner, ws_total, ydoubles;
 };
 
 static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 force als_cluster, 3 force als_small,
-                            // 4 force als_persistent as one cluster (grid = cluster size)
+                            // 4 force als_persistent as one cluster (grid = cluster size), 5 force als_tiny8
 static int g_cluster = 0;   // debug hook: cluster size (0 = auto)
 
 static int choose_rm(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : 0)); }
 
 static const void* kernel_ptr(int rm, int variant) {
+  if (variant == 5) return (const void*)als_tiny8;
   if (variant == 3) variant = 0;   // als_persistent launched as one cluster
   if (variant == 2) {
     switch (rm) {
@@ -1837,7 +2061,17 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
     }
     if (g_variant == 2) return TP_EUNSUPPORTED;
   }
-  // tiny problems: one CTA with everything in shared memory
+  // tiny problems: one CTA with everything in shared memory; r <= 8 on the DMMA pipe
+  if (pl.rm == 8 && (g_variant == 5 || (g_variant == 0 && grid <= 0 && P == 1))) {
+    TinyDims td;
+    tiny_dims(q, d, R, td);
+    const size_t sm_tiny = tiny_smem_doubles(d, r, td) * sizeof(double);
+    if (sm_tiny <= (size_t)smem_optin) {
+      pl.variant = 5; pl.P = 1; pl.Pr = 1; pl.smem = sm_tiny;
+      return TP_OK;
+    }
+    if (g_variant == 5) return TP_EUNSUPPORTED;
+  }
   if (g_variant == 3 || (g_variant == 0 && grid <= 0 && P == 1)) {
     int sumq = 0;
     for (int k = 0; k < d; ++k) sumq += q[k];
@@ -1946,18 +2180,23 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
     // TP_ALS_NONCOOP=1 drops the cooperative attribute (co-residency then rests on
     // the occupancy check of plan_cluster, fine on an otherwise idle GPU)
     static const bool noncoop = getenv("TP_ALS_NONCOOP") && getenv("TP_ALS_NONCOOP")[0] == '1';
-    if (noncoop) cfg.numAttrs = 1;
+    // one cluster is co-scheduled by construction: no cooperative attribute (also
+    // keeps the launch capturable in CUDA graphs)
+    if (noncoop || pl.variant == 3) cfg.numAttrs = 1;
     void* args[] = {&a};
     e = cudaLaunchKernelExC(&cfg, fn, args);
     return cuda_status(e);
   }
   int per_sm = 0;
-  const int nt = (pl.variant == 2 && pl.rm == 8) ? ALS_SMALL_NT8 : ALS_NT;
+  const int nt = pl.variant == 5 ? TINY_NT : ((pl.variant == 2 && pl.rm == 8) ? ALS_SMALL_NT8 : ALS_NT);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, pl.smem);
   if (e != cudaSuccess) return cuda_status(e);
   if (per_sm < 1) return TP_EUNSUPPORTED;
   void* args[] = {&a};
-  e = cudaLaunchCooperativeKernel(fn, dim3(pl.P), dim3(nt), args, pl.smem, s);
+  if (pl.P == 1)   // one CTA: a plain launch (graph-capturable; the grid barrier is a no-op)
+    e = cudaLaunchKernel(fn, dim3(1), dim3(nt), args, pl.smem, s);
+  else
+    e = cudaLaunchCooperativeKernel(fn, dim3(pl.P), dim3(nt), args, pl.smem, s);
   return cuda_status(e);
 }
 

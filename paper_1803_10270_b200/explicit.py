@@ -139,10 +139,17 @@ def startup_step(f_0, L: SeparableOperator, config: ExplicitConfig, log: list | 
     return _reduce(add(f_0, scale(lh, config.dt)), config, "startup-update", log)
 
 
-def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, callback=None) -> CPTensor:
+def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, callback=None,
+        graph: bool = True) -> CPTensor:
     """Fused-recipe CP trajectory (RK2 startup + AB2), fully stream-ordered:
     one fused-ALS launch per update, status words gathered on the device and
-    checked once at the end (no per-step host synchronisation)."""
+    checked once at the end (no per-step host synchronisation).
+
+    ``graph``: after the startup and one eager AB2 step, one AB2 step (target
+    assembly, truncation, state rotation) is captured into a CUDA graph and
+    replayed for the remaining steps -- no per-step host launch overhead.  The
+    replayed kernels are the eager ones on the same data: results are bitwise
+    identical to ``graph=False``."""
     if config.recipe != "fused" or not isinstance(f0, CPTensor):
         prev, cur = f0, startup_step(f0, L, config)
         for n in range(2, steps + 1):
@@ -166,11 +173,33 @@ def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, 
     prev = f0
     if callback:
         callback(1, cur)
-    for n in range(2, steps + 1):
+    use_graph = graph and callback is None and dev.type == "cuda" and steps >= 4 and \
+        L.n_terms * 2 * r + r > r
+    n_eager = 2 if use_graph else steps
+    for n in range(2, n_eager + 1):
         nxt = trunc(ab2_target(prev, cur, L, config.dt), cur, n)
         prev, cur = cur, nxt
         if callback:
             callback(n, cur)
+    if use_graph:
+        # static state buffers; the captured step rotates them in place
+        pbuf, cbuf = prev.data.clone(), cur.data.clone()
+        slot = infos[n_eager + 1]
+        agg = torch.zeros(2, dtype=torch.int32, device=dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            P = CPTensor(cur.specs, data=pbuf, rank=r)
+            C = CPTensor(cur.specs, data=cbuf, rank=r)
+            tgt = ab2_target(P, C, L, config.dt)
+            nxt = cbuf.clone()
+            cp._als_device(tgt, nxt, r, config.als, None, slot)
+            agg.bitwise_or_(slot)
+            pbuf.copy_(cbuf)
+            cbuf.copy_(nxt)
+        for _ in range(n_eager + 1, steps + 1):
+            g.replay()
+        infos[n_eager + 1].copy_(agg)
+        cur = CPTensor(cur.specs, data=cbuf, rank=r)
     bad = int(infos[:, 0].max().item())
     if bad & 2:
         raise cp.ConditioningError("normal equations produced non-finite coefficients")

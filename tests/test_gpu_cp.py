@@ -242,3 +242,22 @@ def test_als_small_variant(als_variant, qs, R, r):
     out, ref, trace, otrace = _als_case(V, init, 10, 1e-10)
     assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
     np.testing.assert_allclose(trace, otrace, rtol=1e-8, atol=1e-12)
+
+
+@pytest.mark.parametrize("qs,R,r", [((32,) * 6, 78, 6), ((5, 7, 3), 6, 2), ((9, 8, 7, 6), 10, 3), ((20, 16, 24), 41, 8),
+                                    ((16, 12), 40, 1), ((33, 17, 40, 9, 12), 29, 7)])
+def test_als_tiny8_variant(als_variant, qs, R, r):
+    """r <= 8 in one CTA on the DMMA pipe (zero-padded tiles: ragged Q, R not a
+    multiple of 8), with the residual trace; forced through the debug hook."""
+    als_variant(5, 0)
+    rng = np.random.default_rng(R + 11 * r)
+    V = rand_factors(rng, qs, R, 0.3)
+    init = [v[:, :r].copy() for v in V]
+    out, ref, trace, otrace = _als_case(V, init, 10, 1e-10)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+    np.testing.assert_allclose(trace, otrace, rtol=1e-8, atol=1e-12)
+
+
+def test_als_auto_plan_config0_is_tiny8():
+    from paper_1803_10270_b200 import cp as _cp
+    assert _cp.als_plan((32,) * 6, 78, 6)["kernel"] == "als_tiny8"

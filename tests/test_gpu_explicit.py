@@ -143,3 +143,23 @@ def test_reduction_log_and_validation():
     assert log[1].rank_before == 6 and log[1].rank_after <= 2
     with pytest.raises(TypeError, match="same tensor format"):
         explicit.ab2_step(f0, ht.from_cp(f1), L, explicit.ExplicitConfig(dt=1e-3, r_max=4))
+
+
+@pytest.mark.parametrize("which,steps", [("cfg0", 12), ("cfg3", 6)])
+def test_graph_replay_matches_eager(which, steps):
+    """explicit.run captures one AB2 step in a CUDA graph and replays it: the
+    trajectory must be bitwise identical to the eager launches."""
+    import torch
+    if which == "cfg0":
+        w, S, L, cfg, _ = _cfg0_setup(steps)
+        f0 = cp.CPTensor(S, w["ic"]["factors"])
+    else:
+        w = workloads.cfg3(0)
+        S = w["specs"]
+        L = operators.SeparableOperator(S, tuple(w["weights"]), tuple(tuple(m) for m in w["mats"]))
+        cfg = explicit.ExplicitConfig(dt=w["dt"], r_max=w["r"], recipe="fused",
+                                      als=cp.ALSApproxConfig(max_sweeps=w["sweeps"], stall=-np.inf, reg=w["lam"]))
+        f0 = cp.CPTensor(S, w["factors"])
+    a = explicit.run(f0, L, cfg, steps, graph=False)
+    b = explicit.run(f0, L, cfg, steps, graph=True)
+    assert torch.equal(a.data, b.data)
