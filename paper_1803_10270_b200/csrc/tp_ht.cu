@@ -299,6 +299,159 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_db_kernel(int k, int nn, int fi
   }
 }
 
+// Same cyclic Jacobi (pair ordering, rotation formula, threshold) on the upper
+// triangle only, as independent 2x2 blocks: per round, warp 0 computes the k/2
+// rotations (and updates the diagonal blocks) while warps 1.. apply the PREVIOUS
+// round's rotations to the eigenvector columns; one barrier; then every thread
+// updates ~2 of the (k/2)(k/2-1)/2 off-diagonal upper blocks (rows of pair P,
+// columns of pair P' > P) in place; one barrier.  Half the shared traffic and ~1/4 of the instructions of the
+// row-then-column kernel.  Matrix z lives at base index (z / per) * nn + first + z % per.
+__global__ void __launch_bounds__(JAC_NT) jacobi_sym_kernel(int k, int nn, int first, int per, const double* Ain,
+                                                            double* Vout, double* wout, int max_sweeps, double tol,
+                                                            int* sweeps_out, const int* skip) {
+  extern __shared__ double js[];
+  const int kp = k + (k & 1), ld = kp + 1, half = kp / 2, m1 = kp - 1;
+#define PK(i, j) ((i) * kp - (((i) * ((i) + 1)) >> 1) + (j))   // packed upper index, i <= j
+  double* a = js;                              // packed upper triangle: (i <= j) at a[PK(i, j)]
+  double* v = a + (size_t)kp * (kp + 1) / 2;   // [kp][ld]
+  double* rot = v + (size_t)kp * ld;           // [2][32][3]: c, s, t (round parity)
+  int* rpq = reinterpret_cast<int*>(rot + 2 * 32 * 3);   // [2][32][2]: p, q
+  int* flagbuf = rpq + 2 * 32 * 2;             // [2] per sweep parity
+  unsigned short* blk = reinterpret_cast<unsigned short*>(flagbuf + 2);   // [nblk]: P | P' << 8
+  const int z = blockIdx.x;
+  const size_t base = (size_t)(z / per) * nn + first + z % per;
+  if (skip && skip[base]) return;
+  const double* in = Ain + base * k * k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < kp * kp; e += JAC_NT) {
+    const int i = e / kp, j = e % kp;
+    double x = 0.0;
+    if (i < k && j < k) x = 0.5 * (in[i * k + j] + in[j * k + i]);   // eigh(0.5 (G + G^T)), ht.py:347
+    if (i <= j) a[PK(i, j)] = x;
+    v[i * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  const int nblk = half * (half - 1) / 2;   // off-diagonal upper blocks (diagonal ones: warp 0)
+  for (int b = tid; b < nblk; b += JAC_NT) {
+    int P = 0, rem = b;
+    while (rem >= half - 1 - P) { rem -= half - 1 - P; ++P; }
+    blk[b] = (unsigned short)(P | ((P + 1 + rem) << 8));
+  }
+  __syncthreads();
+  const double tol2 = tol * tol;
+  bool any = false;    // warp 0: rotations in this sweep
+  int sw = 0, pending = -1, gr = 0;   // pending: round parity whose rotations still await the eigenvector update
+  // eigenvector columns p, q of each rotated pair: warp per pair (uniform skip and
+  // parameter loads), lanes along the rows
+  auto v_update = [&](int par, int w0, int nw) {
+    const double* R = rot + par * 96;
+    const int* PQ = rpq + par * 64;
+    for (int P = warp - w0; P < half; P += nw) {
+      const double s_ = R[3 * P + 1];
+      if (s_ == 0.0) continue;
+      const double c_ = R[3 * P];
+      const int p = PQ[2 * P], q = PQ[2 * P + 1];
+      for (int i = lane; i < kp; i += 32) {
+        const double vx = v[i * ld + p], vy = v[i * ld + q];
+        v[i * ld + p] = c_ * vx - s_ * vy;
+        v[i * ld + q] = s_ * vx + c_ * vy;
+      }
+    }
+  };
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    sw = sweep + 1;
+    any = false;
+    for (int round = 0; round < m1; ++round, ++gr) {
+      const int par = gr & 1;   // global round parity (m1 is odd: round parity would repeat across sweeps)
+      if (warp == 0) {
+        if (lane < half) {
+          int p = round, q = m1;
+          if (lane != 0) {
+            p = round + lane; p -= (p >= m1) ? m1 : 0;
+            q = round - lane; q += (q < 0) ? m1 : 0;
+          }
+          if (p > q) { const int t_ = p; p = q; q = t_; }
+          const double apq = a[PK(p, q)], app = a[PK(p, p)], aqq = a[PK(q, q)];
+          double c = 1.0, s_ = 0.0, t = 0.0;
+          if (fabs(apq) > 1e-300 && apq * apq > tol2 * fabs(app * aqq)) {
+            const double tau = (aqq - app) * rcp_nr(2.0 * apq), at = fabs(tau);
+            if (at < 1e100) {
+              const double h = fma(tau, tau, 1.0);
+              t = (tau >= 0.0 ? 1.0 : -1.0) * rcp_nr(at + h * rsqrt_nr(h));
+            } else {
+              t = (tau >= 0.0 ? 0.5 : -0.5) * rcp_nr(at);
+            }
+            c = rsqrt_nr(fma(t, t, 1.0));
+            s_ = t * c;
+            any = true;
+            // diagonal block of the pair (no other thread touches it this round)
+            a[PK(p, p)] = app - t * apq;
+            a[PK(q, q)] = aqq + t * apq;
+            a[PK(p, q)] = 0.0;
+          }
+          double* R = rot + par * 96 + 3 * lane;
+          R[0] = c; R[1] = s_; R[2] = t;
+          rpq[par * 64 + 2 * lane] = p; rpq[par * 64 + 2 * lane + 1] = q;
+        }
+        if (round == m1 - 1) {
+          const bool anyw = __any_sync(0xffffffffu, any);
+          if (lane == 0) flagbuf[sweep & 1] = anyw ? 1 : 0;
+        }
+      } else if (pending >= 0) {
+        v_update(pending, 1, JAC_NT / 32 - 1);
+      }
+      __syncthreads();
+      // off-diagonal upper 2x2 blocks (rows of pair P, columns of pair P2 > P), in place
+      const double* R = rot + par * 96;
+      const int* PQ = rpq + par * 64;
+      for (int b = tid; b < nblk; b += JAC_NT) {
+        const int P = blk[b] & 0xff, P2 = blk[b] >> 8;
+        const int p = PQ[2 * P], q = PQ[2 * P + 1];
+        const double cP = R[3 * P], sP = R[3 * P + 1];
+        const double c2 = R[3 * P2], s2 = R[3 * P2 + 1];
+        if (sP == 0.0 && s2 == 0.0) continue;
+        const int p2 = PQ[2 * P2], q2 = PQ[2 * P2 + 1];
+        // storage of (row, col) in the upper triangle
+        const int i00 = p < p2 ? PK(p, p2) : PK(p2, p);
+        const int i01 = p < q2 ? PK(p, q2) : PK(q2, p);
+        const int i10 = q < p2 ? PK(q, p2) : PK(p2, q);
+        const int i11 = q < q2 ? PK(q, q2) : PK(q2, q);
+        const double x00 = a[i00], x01 = a[i01], x10 = a[i10], x11 = a[i11];
+        const double y00 = cP * x00 - sP * x10, y01 = cP * x01 - sP * x11;   // rows (pair P)
+        const double y10 = sP * x00 + cP * x10, y11 = sP * x01 + cP * x11;
+        a[i00] = c2 * y00 - s2 * y01; a[i01] = s2 * y00 + c2 * y01;          // columns (pair P2)
+        a[i10] = c2 * y10 - s2 * y11; a[i11] = s2 * y10 + c2 * y11;
+      }
+      pending = par;
+      __syncthreads();
+    }
+    if (flagbuf[sweep & 1] == 0) break;
+  }
+  if (pending >= 0) {
+    v_update(pending, 0, JAC_NT / 32);
+    __syncthreads();
+  }
+  if (sweeps_out && tid == 0) atomicAdd(sweeps_out, sw);
+  double* Vo = Vout + base * k * k;
+  double* wo = wout + base * k;
+  int* rank = rpq;   // scratch
+  if (tid < k) {
+    const double wi = a[PK(tid, tid)];
+    int rk = 0;
+    for (int j = 0; j < k; ++j) {
+      const double wj = a[PK(j, j)];
+      if (wj > wi || (wj == wi && j < tid)) ++rk;
+    }
+    rank[tid] = rk;
+    wo[rk] = wi;
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += JAC_NT) {
+    const int i = e / k, m = e % k;
+    Vo[i * k + rank[m]] = v[i * ld + m];
+  }
+#undef PK
+}
+
 // Frame-Gram square-root factor by Cholesky, M_t = L L^T (one CTA per non-root
 // node, right-looking, 64 dependent steps instead of ~8 Jacobi sweeps).  In the
 // Gramian gauge only a factor F with F F^T = M_t enters: with F = L instead of
@@ -543,7 +696,7 @@ static int g_jac_sweeps = 30;
 static double g_jac_tol = 1e-16;
 static int* g_jac_count = nullptr;
 static int g_chol = 1;   // debug hook: 0 = eigh of every frame Gram (reference path)
-static int g_jac_db = 0;  // debug hook: 1 = one-barrier double-buffered Jacobi, 0 = three-barrier (default: faster, measured)
+static int g_jac_db = 2;  // debug hook: 0 = three-barrier rows/columns, 1 = double-buffered blocks, 2 = upper-triangle blocks (default)
 
 extern "C" {
 
@@ -553,7 +706,7 @@ void tp_debug_set_jacobi(int max_sweeps, double tol, int* count) {
 }
 // debug hook: frame-Gram factor by Cholesky (1, default) or eigh (0)
 void tp_debug_set_ht_chol(int on) { g_chol = on; }
-// debug hook: Jacobi kernel (1 = double-buffered one-barrier rounds, default; 0 = three-barrier rounds)
+// debug hook: Jacobi kernel (0 = three-barrier rounds, 1 = double-buffered blocks, 2 = upper-triangle blocks, default)
 void tp_debug_set_jacobi_impl(int db) { g_jac_db = db; }
 
 size_t tp_ht_truncate_ws_bytes(int d, int Q, int k, int nb) {
@@ -749,9 +902,12 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
   if (e != cudaSuccess) return cuda_status(e);
 
   const int kp = k + (k & 1);
-  const size_t jsm = g_jac_db ? sizeof(double) * (size_t)3 * kp * (kp + 1)
-                              : sizeof(double) * ((size_t)2 * kp * (kp + 1) + 2 * kp + JAC_NT) + sizeof(int) * kp;
-  auto jac = g_jac_db ? jacobi_db_kernel : jacobi_eigh_kernel;
+  const size_t jsm = g_jac_db == 1 ? sizeof(double) * (size_t)3 * kp * (kp + 1)
+                   : g_jac_db == 2 ? sizeof(double) * ((size_t)kp * (kp + 1) / 2 + (size_t)kp * (kp + 1) + 2 * 32 * 3) +
+                                         sizeof(int) * (2 * 32 * 2 + 2) +
+                                         sizeof(unsigned short) * 33 * 32 / 2 + 16
+                                   : sizeof(double) * ((size_t)2 * kp * (kp + 1) + 2 * kp + JAC_NT) + sizeof(int) * kp;
+  auto jac = g_jac_db == 1 ? jacobi_db_kernel : (g_jac_db == 2 ? jacobi_sym_kernel : jacobi_eigh_kernel);
   cudaFuncSetAttribute(jac, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm);
   const size_t fsm = sizeof(double) * 3 * (size_t)k * (k + 1);
   cudaFuncSetAttribute(form_g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);

@@ -9,7 +9,7 @@ L = _lib.lib()
 L.tp_debug_set_jacobi_impl.argtypes = [ctypes.c_int]
 L.tp_debug_set_jacobi.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_void_p]
 cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
-for impl in [0, 1, 0, 1]:
+for impl in [0, 2, 0, 2]:
     L.tp_debug_set_jacobi_impl(impl)
     L.tp_debug_set_jacobi(30, 1e-16, cnt.data_ptr())
     cnt.zero_()
