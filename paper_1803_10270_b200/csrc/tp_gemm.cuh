@@ -126,6 +126,125 @@ static __global__ void __launch_bounds__(128) bgemm_kernel(const __grid_constant
       }
 }
 
+// 16-byte global -> shared async copy (LDGSTS.128)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+// Same tiling and fragment schedule as bgemm_kernel (64 x 64 tile, 4 warps of
+// 32 x 32, m8n8k4 DMMA), with a STAGES-deep cp.async ring of TK-deep K tiles in
+// dynamic shared memory and 16-byte copies along a contiguous, 16-byte aligned
+// M (A) / N (B) dimension.
+template <int STAGES, int TK>
+static __global__ void __launch_bounds__(128) bgemm_pipe_kernel(const __grid_constant__ BGemm g) {
+  extern __shared__ double gsm[];
+  double* As = gsm;                                  // [STAGES][TK][GB_LD]
+  double* Bs = gsm + (size_t)STAGES * TK * GB_LD;    // [STAGES][TK][GB_LD]
+  const int ks = g.ksplit > 1 ? g.ksplit : 1;
+  const int zz = blockIdx.z / ks, sidx = blockIdx.z - zz * ks;
+  const int z1 = zz / g.nb2, z2 = zz % g.nb2;
+  long long oA, oB, oC;
+  if (g.offs) {
+    oA = g.offs[3 * z1]; oB = g.offs[3 * z1 + 1]; oC = g.offs[3 * z1 + 2];
+  } else {
+    oA = z1 * g.sA1; oB = z1 * g.sB1; oC = z1 * g.sC1;
+  }
+  const double* A = g.A + oA + z2 * g.sA2;
+  const double* B = g.B + oB + z2 * g.sB2;
+  double* C = g.C + oC + z2 * g.sC2;
+  const int m0 = blockIdx.y * GB_TM, n0 = blockIdx.x * GB_TN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const bool a_m_fast = g.sAm == 1, b_n_fast = g.sBn == 1;
+  const bool a_vec = a_m_fast && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (g.sAk % 2 == 0);
+  const bool b_vec = b_n_fast && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) && (g.sBk % 2 == 0);
+  const int ktiles = (g.K + TK - 1) / TK, kt0 = (int)((long long)ktiles * sidx / ks),
+            kt1 = (int)((long long)ktiles * (sidx + 1) / ks);
+  auto load_tile = [&](const double* X, long long sXi, long long sXk, int I, int i0, bool fast, bool vec, double* dst,
+                       int k0) {
+    if (vec) {
+#pragma unroll 2
+      for (int e = tid; e < TK * GB_TM / 2; e += 128) {
+        const int kk = e / (GB_TM / 2), ii = 2 * (e % (GB_TM / 2));
+        const int i = i0 + ii, k = k0 + kk;
+        double* d = dst + kk * GB_LD + ii;
+        if (k < g.K && i + 1 < I) {
+          cp_async16(d, X + i + k * sXk);
+        } else {
+          cp_async8(d, X + ((i < I && k < g.K) ? i + k * sXk : 0), i < I && k < g.K);
+          cp_async8(d + 1, X + ((i + 1 < I && k < g.K) ? i + 1 + k * sXk : 0), i + 1 < I && k < g.K);
+        }
+      }
+    } else {
+#pragma unroll 2
+      for (int e = tid; e < TK * GB_TM; e += 128) {
+        int kk, ii;
+        if (fast) { kk = e / GB_TM; ii = e % GB_TM; } else { ii = e / TK; kk = e % TK; }
+        const int i = i0 + ii, k = k0 + kk;
+        const bool v = i < I && k < g.K;
+        cp_async8(dst + kk * GB_LD + ii, X + (v ? i * sXi + k * sXk : 0), v);
+      }
+    }
+  };
+  auto issue = [&](int kt, int buf) {
+    const int k0 = kt * TK;
+    load_tile(A, g.sAm, g.sAk, g.M, m0, a_m_fast, a_vec, As + (size_t)buf * TK * GB_LD, k0);
+    load_tile(B, g.sBn, g.sBk, g.N, n0, b_n_fast, b_vec, Bs + (size_t)buf * TK * GB_LD, k0);
+  };
+  // prologue: STAGES - 1 tiles in flight (one commit group per stage, possibly empty)
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (kt0 + st < kt1) issue(kt0 + st, st);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  for (int kt = kt0; kt < kt1; ++kt) {
+    const int it = kt - kt0, buf = it % STAGES;
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 2) : "memory");
+    __syncthreads();   // tile `it` visible to all; the buffer refilled below is free
+    if (kt + STAGES - 1 < kt1) issue(kt + STAGES - 1, (it + STAGES - 1) % STAGES);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const double* Ab = As + (size_t)buf * TK * GB_LD;
+    const double* Bb = Bs + (size_t)buf * TK * GB_LD;
+#pragma unroll
+    for (int ksub = 0; ksub < TK; ksub += 4) {
+      const int kr = ksub + (lane & 3), cc = lane >> 2;
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = Ab[kr * GB_LD + wm + 8 * i + cc];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = Bb[kr * GB_LD + wn + 8 * j + cc];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m0 + wm + 8 * i + (lane >> 2), n = n0 + wn + 8 * j + 2 * (lane & 3) + h;
+        if (m < g.M && n < g.N) {
+          if (ks > 1) {
+            g.part[(((size_t)zz * ks + sidx) * g.M + m) * g.N + n] = acc[i][j][h];
+          } else {
+            double* c = C + m * g.sCm + n * g.sCn;
+            const double v = g.alpha * acc[i][j][h];
+            *c = (g.beta == 0.0) ? v : fma(g.beta, *c, v);
+          }
+        }
+      }
+}
+
 // split-K epilogue: C_z = alpha * sum_s part[z][s] + beta * C_z (fixed order)
 static __global__ void bgemm_reduce_kernel(const __grid_constant__ BGemm g) {
   const int z = blockIdx.y, z1 = z / g.nb2, z2 = z % g.nb2;
@@ -163,13 +282,34 @@ static inline int bgemm_pick_split(const BGemm& g, int nsm = 148, int min_ktiles
   return s;
 }
 
+// kernel variant (debug / tuning hook): 0 = two-stage static-smem kernel,
+// 1 = 3-stage TK 16, 2 = 2-stage TK 32, 3 = 3-stage TK 32, 4 = 4-stage TK 16
+static int g_bgemm_variant = 1;
+
+template <int STAGES, int TK>
+static inline void bgemm_pipe_launch(dim3 grid, const BGemm& h, cudaStream_t st) {
+  const size_t smem = sizeof(double) * 2 * STAGES * TK * GB_LD;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(bgemm_pipe_kernel<STAGES, TK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  bgemm_pipe_kernel<STAGES, TK><<<grid, 128, smem, st>>>(h);
+}
+
 static inline cudaError_t bgemm_launch(const BGemm& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.nb1 * g.nb2 <= 0) return cudaSuccess;
   const int ks = (g.ksplit > 1 && g.part) ? g.ksplit : 1;
   BGemm h = g;
   h.ksplit = ks;
   dim3 grid((g.N + GB_TN - 1) / GB_TN, (g.M + GB_TM - 1) / GB_TM, g.nb1 * g.nb2 * ks);
-  bgemm_kernel<<<grid, 128, 0, st>>>(h);
+  switch (g_bgemm_variant) {
+    case 1: bgemm_pipe_launch<3, 16>(grid, h, st); break;
+    case 2: bgemm_pipe_launch<2, 32>(grid, h, st); break;
+    case 3: bgemm_pipe_launch<3, 32>(grid, h, st); break;
+    case 4: bgemm_pipe_launch<4, 16>(grid, h, st); break;
+    default: bgemm_kernel<<<grid, 128, 0, st>>>(h);
+  }
   if (ks > 1) {
     const size_t mn = (size_t)g.M * g.N;
     dim3 rg((unsigned)((mn + 255) / 256 < 64 ? (mn + 255) / 256 : 64), g.nb1 * g.nb2);

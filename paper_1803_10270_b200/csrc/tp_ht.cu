@@ -704,6 +704,8 @@ extern "C" {
 void tp_debug_set_jacobi(int max_sweeps, double tol, int* count) {
   g_jac_sweeps = max_sweeps; g_jac_tol = tol; g_jac_count = count;
 }
+// debug hook: batched-GEMM kernel variant of the hSVD chain (tp_gemm.cuh g_bgemm_variant)
+void tp_debug_set_bgemm_variant(int v) { g_bgemm_variant = v; }
 // debug hook: frame-Gram factor by Cholesky (1, default) or eigh (0)
 void tp_debug_set_ht_chol(int on) { g_chol = on; }
 // debug hook: Jacobi kernel (0 = three-barrier rounds, 1 = double-buffered blocks, 2 = upper-triangle blocks, default)
