@@ -132,6 +132,32 @@ int tp_cp_apply_f64(int d, const int* q, int r_in, const double* F, int n_terms,
                     double* out, int R_out, int col_off, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Complex128 CP path (the reference's own arithmetic,
+ * cp.py:59, and its complex Fourier Galerkin factor matrices, basis.py:168-187).
+ * Complex arrays are interleaved (re, im) doubles (numpy/torch complex128
+ * layout); sizes count complex elements.
+ *   tp_cp_apply_c128 : operators.apply / cp.add / cp.scale (operators.py:48-62,
+ *                      cp.py:98-108) with complex weights (host, 2 doubles per
+ *                      term), complex scale and complex factor matrices.
+ *   tp_cp_inner_c128 : cp.inner_product (cp.py:111-121), conjugate on A;
+ *                      out = 2 device doubles (re, im).
+ *   tp_cp_als_c128   : cp.cp_approx_als (cp.py:266-334) with the reference's
+ *                      normal equations (gram X = had @ T_j^T, factor = X^T),
+ *                      one CTA, problem resident in shared memory
+ *                      (TP_EUNSUPPORTED when it does not fit).
+ * ------------------------------------------------------------------------- */
+int tp_cp_apply_c128(int d, const int* q, int r_in, const double* F, int n_terms, const double* weights,
+                     double scale_re, double scale_im, const int* mat_idx, const double* mats,
+                     const long long* mat_off, int n_mats, double* out, int R_out, int col_off, void* stream);
+size_t tp_cp_inner_c128_ws_bytes(int d, const int* q, int ra, int rb);
+int tp_cp_inner_c128(int d, const int* q, int ra, const double* A, int rb, const double* B, double* out,
+                     void* ws, size_t ws_bytes, void* stream);
+size_t tp_cp_als_c128_ws_bytes(int d, const int* q, int R, int r);
+int tp_cp_als_c128(int d, const int* q, int R, const double* V, int r, double* U, int sweeps, double reg,
+                   int reg_mode, double tol, double stall, double* trace, int* info, void* ws, size_t ws_bytes,
+                   void* stream);
+
+/* ---------------------------------------------------------------------------
  * Batched hierarchical-Tucker truncation by hSVD (ht.truncate, ht.py:313-372,
  * with ht.orthogonalize ht.py:294-310) on a balanced binary dimension tree
  * (ht.balanced_tree, ht.py:79-98) with uniform leaf size Q and uniform input

@@ -58,6 +58,12 @@ _SIGNATURES = {
     "tp_cp_contract_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _vp, _vp]),
     "tp_cp_apply_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _c_double_p, _d, _c_int_p, _vp, _c_ll_p, _i,
                              _vp, _i, _i, _vp]),
+    "tp_cp_apply_c128": (_i, [_i, _c_int_p, _i, _vp, _i, _c_double_p, _d, _d, _c_int_p, _vp, _c_ll_p, _i,
+                              _vp, _i, _i, _vp]),
+    "tp_cp_inner_c128_ws_bytes": (_sz, [_i, _c_int_p, _i, _i]),
+    "tp_cp_inner_c128": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _vp, _vp, _sz, _vp]),
+    "tp_cp_als_c128_ws_bytes": (_sz, [_i, _c_int_p, _i, _i]),
+    "tp_cp_als_c128": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _i, _d, _i, _d, _d, _vp, _vp, _vp, _sz, _vp]),
     "tp_als_shard_ws_bytes": (_sz, [_i, _c_int_p, _i, _i]),
     "tp_als_shard_init_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _vp, _vp, _vp]),
     "tp_als_shard_rhs_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _i, _vp, _vp, _sz, _vp]),

@@ -4,10 +4,12 @@ Drop-in mirror of the reference ``tensorpde/cp.py``.  A rank-``R`` tensor over
 ``d`` specs is ONE contiguous fp64 device buffer; mode ``k`` is the row-major
 ``(Q_k, R)`` block at element offset ``R * sum_{k'<k} Q_k'`` -- exactly the
 reference's ``factors[k]`` array (cp.py:43-59), stacked mode-major.  Scalars
-live in mode 0 (cp.py:1-12).  Arithmetic is real fp64 (the BASELINE configs
-are real; the reference's complex128 agrees to ~1e-15 on real data, SURVEY
-8(c) S9).  All compute runs through the sm_100a C-ABI library; there is no
-CPU fallback.
+live in mode 0 (cp.py:1-12).  Real-valued data runs in real fp64 (the
+BASELINE configs are real; the reference's complex128 agrees to ~1e-15 on real
+data).  Complex data (the reference's Fourier Galerkin basis,
+complex random initial terms) runs in complex128 through the ``*_c128``
+kernels, the reference's own arithmetic.  All compute
+runs through the sm_100a C-ABI library; there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -25,21 +27,24 @@ from .basis import BasisSpec
 
 __all__ = [
     "CPTensor", "ALSApproxConfig", "ConditioningError", "add", "scale", "inner_product", "norm",
-    "random_cp", "pad_rank", "cp_approx_als", "check", "rank_reduce_als", "from_numpy_factors",
+    "random_cp", "pad_rank", "cp_approx_als", "check", "rank_reduce_als", "from_numpy_factors", "as_complex",
 ]
 
 
-def _as_real_array(f, k):
+def _as_array(f, k):
+    """Factor k as a CPU tensor: float64 when the values are real (also a complex
+    array with zero imaginary part), complex128 otherwise."""
     if isinstance(f, torch.Tensor):
+        f = f.detach().cpu()
         if f.is_complex():
             if torch.any(f.imag != 0):
-                raise ValueError(f"dimension {k}: complex coefficients are not supported on the real-fp64 B200 path")
+                return f.to(torch.complex128)
             f = f.real
-        return f.detach().to(torch.float64)
+        return f.to(torch.float64)
     a = np.asarray(f)
     if np.iscomplexobj(a):
         if np.any(a.imag != 0):
-            raise ValueError(f"dimension {k}: complex coefficients are not supported on the real-fp64 B200 path")
+            return torch.as_tensor(np.ascontiguousarray(a, dtype=np.complex128))
         a = a.real
     return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64))
 
@@ -60,7 +65,9 @@ class CPTensor:
             return
         if factors is None or len(factors) != len(self.specs):
             raise ValueError("one factor matrix per dimension required")
-        mats = [_as_real_array(f, k) for k, f in enumerate(factors)]
+        mats = [_as_array(f, k) for k, f in enumerate(factors)]
+        if any(m.is_complex() for m in mats):   # one complex factor -> the whole tensor is complex128
+            mats = [m.to(torch.complex128) for m in mats]
         ranks = {int(m.shape[1]) if m.dim() == 2 else -1 for m in mats}
         if len(ranks) != 1:
             raise ValueError(f"inconsistent ranks across dimensions: {ranks}")
@@ -75,6 +82,10 @@ class CPTensor:
         self._rank = int(r)
 
     # -- shape
+    @property
+    def is_complex(self) -> bool:
+        return self.data.is_complex()
+
     @property
     def ndim(self) -> int:
         return len(self.specs)
@@ -114,9 +125,20 @@ def from_numpy_factors(specs, factors) -> CPTensor:
     return CPTensor(specs, factors)
 
 
-def empty_cp(specs, rank: int, dev=None) -> CPTensor:
+def empty_cp(specs, rank: int, dev=None, dtype=torch.float64) -> CPTensor:
     n = sum(s.Q for s in specs) * rank
-    return CPTensor(specs, data=torch.empty(n, dtype=torch.float64, device=dev or _lib.device()), rank=rank)
+    return CPTensor(specs, data=torch.empty(n, dtype=dtype, device=dev or _lib.device()), rank=rank)
+
+
+def as_complex(f: CPTensor) -> CPTensor:
+    """complex128 copy of a real tensor (the reference's coercion, cp.py:59); complex tensors pass through."""
+    if f.is_complex:
+        return f
+    return CPTensor(f.specs, data=f.data.to(torch.complex128), rank=f.rank)
+
+
+def _is_cplx_scalar(c) -> bool:
+    return isinstance(c, complex) and c.imag != 0
 
 
 def _check_same_specs(f: CPTensor, g: CPTensor) -> None:
@@ -126,10 +148,12 @@ def _check_same_specs(f: CPTensor, g: CPTensor) -> None:
 
 def concat(specs, parts) -> CPTensor:
     """Column concatenation of several (tensor, scale) parts in one device pass
-    (cp.add / cp.scale, cp.py:98-108).  Scale goes into mode 0."""
-    parts = [(t, float(c)) for t, c in parts]
+    (cp.add / cp.scale, cp.py:98-108).  Scale goes into mode 0.  Any complex
+    part or scale makes the result complex128."""
+    cplx = any(t.is_complex or _is_cplx_scalar(complex(c)) for t, c in parts)
+    parts = [(t, complex(c) if cplx else float(complex(c).real)) for t, c in parts]
     R = sum(t.rank for t, _ in parts)
-    out = empty_cp(specs, R, parts[0][0].data.device)
+    out = empty_cp(specs, R, parts[0][0].data.device, torch.complex128 if cplx else torch.float64)
     col = 0
     for t, c in parts:
         _apply_raw(t, [[None] * t.ndim], [1.0], c, None, out, col)
@@ -145,11 +169,7 @@ def add(f: CPTensor, g: CPTensor) -> CPTensor:
 
 def scale(f: CPTensor, c) -> CPTensor:
     """Scalar multiple folded into mode 0 (cp.py:104-108)."""
-    if isinstance(c, complex):
-        if c.imag != 0:
-            raise ValueError("complex scalars are not supported on the real-fp64 B200 path")
-        c = c.real
-    return concat(f.specs, [(f, float(c))])
+    return concat(f.specs, [(f, c)])
 
 
 def _inner_device(f: CPTensor, g: CPTensor, out: torch.Tensor) -> None:
@@ -163,10 +183,27 @@ def _inner_device(f: CPTensor, g: CPTensor, out: torch.Tensor) -> None:
     _lib.check(st, "inner_product")
 
 
-def inner_product(f: CPTensor, g: CPTensor) -> float:
-    """``<f, g> = sum_{l,n} prod_k (F_k^T G_k)[l, n]`` (cp.py:111-121).  Real
-    path: the conjugation on f is the identity.  Returns a Python float."""
+def _inner_device_c(f: CPTensor, g: CPTensor, out: torch.Tensor) -> None:
+    L = _lib.lib()
+    f, g = as_complex(f), as_complex(g)
+    qs = _lib.int_array(f.qs)
+    nbytes = L.tp_cp_inner_c128_ws_bytes(f.ndim, qs, f.rank, g.rank)
+    ws = _lib.WORKSPACE.get(nbytes, f.data.device)
+    st = L.tp_cp_inner_c128(f.ndim, qs, f.rank, f.data.data_ptr(), g.rank, g.data.data_ptr(), out.data_ptr(),
+                            ws.data_ptr(), ws.numel(), _lib.stream_ptr(f.data.device))
+    _lib.check(st, "inner_product")
+
+
+def inner_product(f: CPTensor, g: CPTensor):
+    """``<f, g> = sum_{l,n} prod_k (F_k^H G_k)[l, n]`` (cp.py:111-121), conjugate
+    on f.  Real tensors: a Python float (the conjugation is the identity);
+    complex tensors: a Python complex, like the reference."""
     _check_same_specs(f, g)
+    if f.is_complex or g.is_complex:
+        out = torch.empty(2, dtype=torch.float64, device=f.data.device)
+        _inner_device_c(f, g, out)
+        re, im = out.tolist()
+        return complex(re, im)
     out = torch.empty(1, dtype=torch.float64, device=f.data.device)
     _inner_device(f, g, out)
     return float(out.item())
@@ -174,26 +211,31 @@ def inner_product(f: CPTensor, g: CPTensor) -> float:
 
 def norm(f: CPTensor) -> float:
     """cp.py:124-126."""
-    return float(math.sqrt(max(inner_product(f, f), 0.0)))
+    return float(math.sqrt(max(complex(inner_product(f, f)).real, 0.0)))
 
 
-def random_cp(specs, r: int, rng: np.random.Generator) -> CPTensor:
-    """Unit-normalised random terms (cp.py:129-136), real variant."""
+def random_cp(specs, r: int, rng: np.random.Generator, complex_: bool = False) -> CPTensor:
+    """Unit-normalised random terms (cp.py:129-136).  ``complex_=True`` draws
+    exactly like the reference (real and imaginary N(0,1) parts from the same
+    generator); the default real variant is used for real targets."""
     factors = []
     for spec in specs:
-        m = rng.standard_normal((spec.Q, r))
+        if complex_:
+            m = rng.standard_normal((spec.Q, r)) + 1j * rng.standard_normal((spec.Q, r))
+        else:
+            m = rng.standard_normal((spec.Q, r))
         m /= np.linalg.norm(m, axis=0, keepdims=True)
         factors.append(m)
     return CPTensor(tuple(specs), factors)
 
 
 def pad_rank(f: CPTensor, r: int, rng: np.random.Generator, rel_scale: float = 1e-8) -> CPTensor:
-    """cp.py:139-146."""
+    """cp.py:139-146 (complex random terms for a complex tensor)."""
     if r < f.rank:
         raise ValueError(f"cannot pad rank {f.rank} down to {r}")
     if r == f.rank:
         return f.copy()
-    pad = scale(random_cp(f.specs, r - f.rank, rng), rel_scale * max(norm(f), 1.0))
+    pad = scale(random_cp(f.specs, r - f.rank, rng, f.is_complex), rel_scale * max(norm(f), 1.0))
     return add(f, pad)
 
 
@@ -222,10 +264,26 @@ _REG = 1e-12
 
 def _als_device(target: CPTensor, U: torch.Tensor, r: int, cfg: ALSApproxConfig,
                 trace_buf: torch.Tensor | None, info: torch.Tensor) -> None:
-    """Launch the fused ALS on the current stream; U is overwritten in place."""
+    """Launch the fused ALS on the current stream; U is overwritten in place
+    (complex128 target and U: the one-CTA complex kernel)."""
     L = _lib.lib()
     qs = _lib.int_array(target.qs)
     d = target.ndim
+    if target.is_complex:
+        if not U.is_complex():
+            raise ValueError("complex target needs a complex guess")
+        nbytes = L.tp_cp_als_c128_ws_bytes(d, qs, target.rank, r)
+        if nbytes == 0:
+            raise ValueError(f"unsupported complex ALS size: d={d}, R={target.rank}, r={r} "
+                             "(the complex path keeps the problem in one CTA's shared memory)")
+        ws = _lib.WORKSPACE.get(nbytes, target.data.device)
+        reg, mode = (_REG, 1) if cfg.reg is None else (float(cfg.reg), 0)
+        st = L.tp_cp_als_c128(d, qs, target.rank, target.data.data_ptr(), r, U.data_ptr(), int(cfg.max_sweeps),
+                              reg, mode, float(cfg.tol), float(cfg.stall),
+                              trace_buf.data_ptr() if trace_buf is not None else None,
+                              info.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(target.data.device))
+        _lib.check(st, "cp_approx_als")
+        return
     nbytes = L.tp_cp_als_ws_bytes(d, qs, target.rank, r, cfg.grid)
     if nbytes == 0:
         raise ValueError(f"unsupported ALS size: d={d}, R={target.rank}, r={r} (r <= 32, d <= 8)")
@@ -278,9 +336,11 @@ def cp_approx_als(target, r: int, config: ALSApproxConfig | None = None, *, spec
         raise NotImplementedError("callable (quadrature) targets are outside the B200 hot path")
     specs = target.specs
     rng = np.random.default_rng(cfg.seed)
-    guess = init.copy() if init is not None else random_cp(specs, r, rng)
+    guess = init.copy() if init is not None else random_cp(specs, r, rng, target.is_complex)
     if guess.rank != r or guess.specs != tuple(specs):
         raise ValueError("init shape does not match the requested fit")
+    if target.is_complex or guess.is_complex:   # the reference's complex128 arithmetic
+        target, guess = as_complex(target), as_complex(guess).copy()
     dev = target.data.device
     info = torch.zeros(2, dtype=torch.int32, device=dev)
     tb = torch.zeros(max(cfg.max_sweeps, 1), dtype=torch.float64, device=dev) if trace is not None else None
@@ -307,25 +367,30 @@ def check(result: CPTensor) -> CPTensor:
 
 def _relative_error(f: CPTensor, g: CPTensor, nf: float) -> float:
     """Gram-identity error as in cp.py:369-375 (what the reference's adaptive loop uses)."""
-    d = inner_product(f, f) - 2.0 * inner_product(g, f) + inner_product(g, g)
+    d = (complex(inner_product(f, f)).real - 2.0 * complex(inner_product(g, f)).real
+         + complex(inner_product(g, g)).real)
     return float(math.sqrt(max(d, 0.0)) / nf)
 
 
 def rank_reduce_als(f: CPTensor, r_target: int, eps: float, config: ALSApproxConfig | None = None) -> CPTensor:
     """Adaptive rank 1..r_target, warm start + one fresh random term (cp.py:337-366).
-    Random terms are real (the reference draws complex ones)."""
+    Complex targets draw the reference's complex random terms from the same
+    generator sequence; real targets draw real terms (real fp64 path)."""
     if r_target < 1:
         raise ValueError("target rank must be at least 1")
     cfg = config or ALSApproxConfig()
     nf = norm(f)
+    cz = f.is_complex
     zero = CPTensor(f.specs, [np.zeros((s.Q, 1)) for s in f.specs])
+    if cz:
+        zero = as_complex(zero)
     if nf == 0.0:
         return zero
     rng = np.random.default_rng(cfg.seed)
     best, best_err = zero, 1.0
     guess = None
     for r in range(1, r_target + 1):
-        init = random_cp(f.specs, 1, rng) if guess is None else add(guess, random_cp(f.specs, 1, rng))
+        init = random_cp(f.specs, 1, rng, cz) if guess is None else add(guess, random_cp(f.specs, 1, rng, cz))
         guess = cp_approx_als(f, r, cfg, init=init)
         err = _relative_error(f, guess, nf)
         if err < best_err:
@@ -339,7 +404,8 @@ def rank_reduce_als(f: CPTensor, r_target: int, eps: float, config: ALSApproxCon
 
 def _apply_raw(f: CPTensor, mat_rows, weights, scale_, mats_dev, out: CPTensor, col_off: int,
                mat_off=None) -> None:
-    """Launch tp_cp_apply_f64: mat_rows[t][k] is an int matrix index or None."""
+    """Launch tp_cp_apply_f64 (or tp_cp_apply_c128 when ``out`` is complex128):
+    mat_rows[t][k] is an int matrix index or None."""
     L = _lib.lib()
     d = f.ndim
     n_terms = len(weights)
@@ -347,6 +413,23 @@ def _apply_raw(f: CPTensor, mat_rows, weights, scale_, mats_dev, out: CPTensor, 
     for row in mat_rows:
         idx.extend(-1 if m is None else int(m) for m in row)
     n_mats = 0 if mat_off is None else len(mat_off)
+    if out.is_complex:
+        f = as_complex(f)
+        if mats_dev is not None and not mats_dev.is_complex():
+            mats_dev = mats_dev.to(torch.complex128)
+        w = []
+        for x in weights:
+            x = complex(x)
+            w += [x.real, x.imag]
+        sc = complex(scale_)
+        st = L.tp_cp_apply_c128(d, _lib.int_array(f.qs), f.rank, f.data.data_ptr(), n_terms, _lib.double_array(w),
+                                sc.real, sc.imag, _lib.int_array(idx),
+                                None if mats_dev is None else mats_dev.data_ptr(),
+                                None if mat_off is None else _lib.ll_array(mat_off), n_mats,
+                                out.data.data_ptr(), out.rank, int(col_off), _lib.stream_ptr(f.data.device))
+        _lib.check(st, "apply")
+        return
+    scale_ = complex(scale_).real
     st = L.tp_cp_apply_f64(d, _lib.int_array(f.qs), f.rank, f.data.data_ptr(), n_terms,
                            _lib.double_array(weights), float(scale_), _lib.int_array(idx),
                            None if mats_dev is None else mats_dev.data_ptr(),

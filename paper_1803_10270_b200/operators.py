@@ -1,11 +1,13 @@
 """Separable linear operators (mirror of ``tensorpde/operators.py``).
 
 An operator is ``sum_t w_t prod_k E^t_k``.  Beyond the reference's
-``FactorKind`` entries (operators.py:28-45), a factor may be a dense real
+``FactorKind`` entries (operators.py:28-45), a factor may be a dense
 ``(Q_k, Q_k)`` matrix or ``None`` (identity) -- the extension SURVEY 8(a) row
 A4 requires for the BASELINE collocation operators (Fourier D, diag(v),
 rank-1 moment projectors).  ``apply`` runs the sm_100a K1 kernel and writes
-the term-major result (operators.py:48-62) in one launch.
+the term-major result (operators.py:48-62) in one launch; complex factor
+matrices (the reference's Fourier Galerkin basis) or complex weights run the
+complex128 kernel and give a complex result.
 """
 
 from __future__ import annotations
@@ -54,12 +56,19 @@ def _is_identity(m) -> bool:
 def _real_weight(w) -> float:
     w = complex(w)
     if w.imag != 0:
-        raise ValueError("complex operator weights are not supported on the real-fp64 B200 path")
+        raise ValueError("complex operator weights are not supported by the real-fp64 implicit path")
     return w.real
 
 
+def _weight(w):
+    """Real weights stay float (real kernel); complex ones select the complex128 path."""
+    w = complex(w)
+    return w if w.imag != 0 else w.real
+
+
 def dense_factor(spec: BasisSpec, m) -> np.ndarray | None:
-    """Resolve a factor entry to a dense real matrix (None = identity)."""
+    """Resolve a factor entry to a dense matrix (None = identity): float64 when
+    real-valued, complex128 otherwise (Fourier Galerkin factors, basis.py:168-187)."""
     if _is_identity(m):
         return None
     if isinstance(m, FactorKind):
@@ -67,8 +76,9 @@ def dense_factor(spec: BasisSpec, m) -> np.ndarray | None:
     m = np.asarray(m)
     if np.iscomplexobj(m):
         if np.any(m.imag != 0):
-            raise ValueError("complex factor matrices (Fourier Galerkin basis) are not supported on the "
-                             "real-fp64 B200 path; use a collocation basis")
+            if m.shape != (spec.Q, spec.Q):
+                raise ValueError(f"factor matrix shape {m.shape} != ({spec.Q}, {spec.Q})")
+            return np.ascontiguousarray(m, dtype=np.complex128)
         m = m.real
     if m.shape != (spec.Q, spec.Q):
         raise ValueError(f"factor matrix shape {m.shape} != ({spec.Q}, {spec.Q})")
@@ -97,26 +107,39 @@ def device_tables(op: SeparableOperator, dev: torch.device):
                 off += dm.size
             idx_row.append(keys[key])
         rows.append(idx_row)
-    buf = torch.as_tensor(np.concatenate(mats) if mats else np.zeros(1), dtype=torch.float64).to(dev)
-    weights = [_real_weight(w) for w in op.weights]
+    weights = [_weight(w) for w in op.weights]
+    cplx = any(np.iscomplexobj(m) for m in mats) or any(isinstance(w, complex) for w in weights)
+    dt = np.complex128 if cplx else np.float64
+    buf = torch.as_tensor(np.concatenate([m.astype(dt) for m in mats]) if mats else np.zeros(1, dtype=dt)).to(dev)
     out = (buf, offs, rows, weights)
     _TABLES[op] = out
     return out
 
 
-def apply_into(op: SeparableOperator, f: CPTensor, out: CPTensor, col_off: int, scale: float = 1.0) -> None:
+def is_complex(op: SeparableOperator) -> bool:
+    """True when the operator needs the complex128 path (complex factors or weights)."""
+    buf = device_tables(op, _lib.device())[0]
+    return buf.is_complex()
+
+
+def apply_into(op: SeparableOperator, f: CPTensor, out: CPTensor, col_off: int, scale=1.0) -> None:
     """Write ``scale * op(f)`` into columns [col_off, col_off + n_terms*rank) of ``out``."""
     if op.specs != f.specs:
         raise ValueError("operator and tensor live on different bases")
     buf, offs, rows, weights = device_tables(op, f.data.device)
+    if (buf.is_complex() or f.is_complex) and not out.is_complex:
+        raise ValueError("complex operator or tensor needs a complex128 output")
     _apply_raw(f, rows, weights, scale, buf, out, col_off, offs)
 
 
 def apply(op: SeparableOperator, f: CPTensor) -> CPTensor:
-    """Apply exactly; result rank ``n_terms * f.rank``, term-major (operators.py:48-62)."""
+    """Apply exactly; result rank ``n_terms * f.rank``, term-major (operators.py:48-62).
+    Complex operator or tensor: complex128 result."""
     if op.specs != f.specs:
         raise ValueError("operator and tensor live on different bases")
-    out = empty_cp(f.specs, op.n_terms * f.rank, f.data.device)
+    buf = device_tables(op, f.data.device)[0]
+    cplx = buf.is_complex() or f.is_complex
+    out = empty_cp(f.specs, op.n_terms * f.rank, f.data.device, torch.complex128 if cplx else torch.float64)
     apply_into(op, f, out, 0)
     return out
 

@@ -350,9 +350,45 @@ def gen_diagnostics():
     np.savez_compressed(OUT / "diagnostics.npz", **store)
 
 
+def gen_complex():
+    """Complex128 path in the reference's native arithmetic, no shims:
+    rank_reduce_als with its complex random terms (cp.py:337-366) and the reference's
+    explicit split recipe (explicit.py:85-103) on the Fourier Galerkin basis with the
+    reference advection operator (operators.py:65-87)."""
+    from tensorpde import explicit
+    store = {}
+    rng = np.random.default_rng(41)
+    specs = (BasisSpec(5, 1.5), BasisSpec(7, 2.0), BasisSpec(3, 0.8))
+    # exactly rank 2: the adaptive loop (ranks 1, 2) stops at rank 2 with a converged
+    # fit (a non-converged or noise-fitting best rank would make the stall-terminated
+    # result sensitive at the 1e-8 level)
+    f = cp.random_cp(specs, 2, rng)
+    red = cp.rank_reduce_als(f, 3, 1e-9)
+    pack_cp("rr_f", f, store)
+    pack_cp("rr_out", red, store)
+    # explicit split recipe: 2-D sheared advection, Galerkin Q = 9
+    specs2 = (BasisSpec(9, 3.0), BasisSpec(9, 3.0))
+    op = operators.advection_operator(spiral_matrix(2, 2.0), specs2)
+    f0 = cp.scale(cp.random_cp(specs2, 2, rng), 0.5)
+    cfg = explicit.ExplicitConfig(dt=1e-2, r_max=3, eps_rank=1e-8)
+    traj = [f0, explicit.startup_step(f0, op, cfg)]
+    for _ in range(2):
+        traj.append(explicit.ab2_step(traj[-2], traj[-1], op, cfg))
+    for n, g in enumerate(traj):
+        pack_cp(f"ex_step{n}", g, store)
+    store["ex_weights"] = np.array(op.weights)
+    for t, row in enumerate(op.factors):
+        for k, kind in enumerate(row):
+            if kind is not FactorKind.IDENTITY:
+                store[f"ex_E{t}_{k}"] = factor_matrix(specs2[k], kind)
+    store["ex_nterms"] = np.array(op.n_terms)
+    store["ex_meta"] = np.array([9, 3.0, 1e-2, 3, 1e-8])
+    np.savez_compressed(OUT / "complex.npz", **store)
+
+
 GENERATORS = {"cp_als": lambda: gen_cp_als(), "ht": lambda: gen_ht(), "operators": lambda: gen_operators(),
               "explicit": lambda: gen_explicit(), "implicit": lambda: gen_implicit(), "io": lambda: gen_io(),
-              "diagnostics": lambda: gen_diagnostics()}
+              "diagnostics": lambda: gen_diagnostics(), "complex": lambda: gen_complex()}
 
 
 if __name__ == "__main__":

@@ -41,8 +41,11 @@ def test_cptensor_validation_mirrors_reference():
         cp.CPTensor(S, [np.zeros((5, 1)), np.zeros((7, 2)), np.zeros((3, 1))])
     with pytest.raises(ValueError, match="rows != Q"):
         cp.CPTensor(S, [np.zeros((4, 1)), np.zeros((7, 1)), np.zeros((3, 1))])
-    with pytest.raises(ValueError, match="complex"):
-        cp.CPTensor(S, [np.ones((5, 1)) * 1j, np.zeros((7, 1)), np.zeros((3, 1))])
+    # complex factors select the complex128 path; real-valued complex
+    # arrays stay on the real fp64 path (the reference's coercion is value-preserving)
+    import torch
+    assert cp._as_array(np.ones((5, 1)) * 1j, 0).dtype == torch.complex128
+    assert cp._as_array(np.ones((5, 1)) + 0j, 0).dtype == torch.float64
 
 
 def test_basis_spec_rules():
@@ -75,8 +78,12 @@ def test_operator_validation_and_pairs():
     assert pair.zeta == (1.0, 0.0, 0.0, 0.0)
     cn = operators.crank_nicolson_pair(L, 0.1)
     assert cn.eta[1] == pytest.approx(0.05) and cn.zeta[1] == pytest.approx(-0.05)
-    with pytest.raises(ValueError, match="complex"):
-        operators.dense_factor(basis.BasisSpec(5, 1.0), basis.FactorKind.DERIVATIVE)
+    D = operators.dense_factor(basis.BasisSpec(5, 1.0), basis.FactorKind.DERIVATIVE)
+    assert D.dtype == np.complex128
+    np.testing.assert_allclose(D, np.diag(1j * np.pi * np.arange(-2, 3) / 1.0))   # basis.py:168-187
+    with pytest.raises(ValueError, match="complex operator weights"):
+        operators.implicit_euler_pair(operators.SeparableOperator(S, (1j,), ((basis.FactorKind.DERIVATIVE, None, None),)),
+                                      0.1)
 
 
 def test_no_cpu_fallback_without_device():

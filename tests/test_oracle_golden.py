@@ -118,3 +118,27 @@ def test_implicit_step_golden():
         assert done == sweeps
         rel = metrics.cp_rel_diff(unpack_cp(g, key), out)
         assert rel < 1e-12, (orient, rel)
+
+
+def _complex_ex_setup():
+    g = load_golden("complex")
+    nt = int(g["ex_nterms"])
+    mats = [[g[f"ex_E{t}_{k}"] if f"ex_E{t}_{k}" in g else None for k in range(2)] for t in range(nt)]
+    return g, list(g["ex_weights"]), mats
+
+
+def test_complex_rank_reduce_and_split_recipe_golden():
+    """Oracle vs the reference run natively in complex128 (rank_reduce_als with its
+    complex random terms; the explicit split recipe on the Galerkin basis)."""
+    from oracle import cp_als as ocp
+    from oracle import explicit as oex
+    g, w, mats = _complex_ex_setup()
+    out = ocp.rank_reduce(unpack_cp(g, "rr_f"), 3, 1e-9)
+    assert metrics.cp_rel_diff(unpack_cp(g, "rr_out"), out) <= 1e-12
+    red = lambda t, init: ocp.rank_reduce(t, 3, 1e-8)  # noqa: E731
+    f0 = unpack_cp(g, "ex_step0")
+    traj = [f0, oex.startup_split(f0, w, mats, 1e-2, 3, red)]
+    for _ in range(2):
+        traj.append(oex.ab2_split(traj[-2], traj[-1], w, mats, 1e-2, 3, red))
+    for n, f in enumerate(traj):
+        assert metrics.cp_rel_diff(unpack_cp(g, f"ex_step{n}"), f) <= 1e-10, n
