@@ -1235,49 +1235,59 @@ __global__ void __launch_bounds__(TINY_NT, 1) als_tiny8(const __grid_constant__ 
       prof_t = now;
     }
   };
+  // K splits of the right-hand side of mode j (warps 1.. share M tiles x K ranges)
+  // worker warps 1..15 (measured: keeping warp 0's sub-partition free of workers
+  // shortens the inverse chain 2.97K -> 2.16K cycles but lengthens the workers' path
+  // more, 2.51 -> 2.62 us per mode update)
+  constexpr int NWK = TINY_NW - 1, NTK = NWK * 32;
+  const bool worker = warp != 0;
+  const int wk = warp - 1;
+  const int tk = tid - 32;
+  auto ksn_of = [&](int j) {
+    const int mt = td.qp[j] / 8;
+    int ksn = NWK / mt;
+    return ksn < 1 ? 1 : (ksn > TINY_KSMAX ? TINY_KSMAX : ksn);
+  };
+  // warps 1..: had[c][l] = prod_{k != j} C_k[l][c] (rows l >= r and columns c >= R
+  // are zero), a named barrier, then part[ks][s][l] = sum_c V_j[s][c] had[c][l]
+  auto hadamard_rhs = [&](int j) {
+    for (int e = tk; e < R8 * 8; e += NTK) {
+      const int c = e >> 3, l = e & 7;
+      double f[TP_MAXD];
+#pragma unroll
+      for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < d && k != j) ? Cs[((size_t)k * 8 + l) * Rs + c] : 1.0;
+      double v = 1.0;
+#pragma unroll
+      for (int k = 0; k < TP_MAXD; ++k) v *= f[k];
+      had[e] = v;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NTK) : "memory");
+    const int mt = td.qp[j] / 8, ksn = ksn_of(j), ksteps = R8 / 4;
+    const double* va = Vs + (size_t)td.qo[j] * Rs;
+    for (int it = wk; it < mt * ksn; it += NWK) {
+      const int m = it / ksn, ks = it - m * ksn;
+      const int kb = ksteps * ks / ksn, ke = ksteps * (ks + 1) / ksn;
+      const double* arow = va + (size_t)(m * 8 + g) * Rs + t4;
+      const double* bcol = had + t4 * 8 + g;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll 4
+      for (int kk = kb; kk < ke; ++kk) dmma_8x8x4(c0, c1, arow[4 * kk], bcol[32 * kk]);
+      double* pr = part + ((size_t)ks * td.qmaxp + m * 8 + g) * TINY_PLD + 2 * t4;
+      pr[0] = c0; pr[1] = c1;
+    }
+  };
+  // Software pipeline across mode updates: the Grams of A_{j+1} are final as soon as
+  // G_j is, so warp 0 forms G_j and inverts A_{j+1} while warps 1.. form C_j, the
+  // Hadamard and the right-hand side of mode j+1 (named barrier among themselves).
+  // Two block barriers per mode update; the inverse is off the critical path.
+  if (warp == 0) status |= warp_sweep_inverse8(a, Gsm, 0, Ai, 8);
+  else if (worker) hadamard_rhs(0);
+  __syncthreads();
   for (int sweep = 0; sweep < a.sweeps; ++sweep) {
     for (int j = 0; j < d; ++j) {
-      const int Qj = a.q[j], mt = td.qp[j] / 8;
+      const int Qj = a.q[j], mt = td.qp[j] / 8, ksn = ksn_of(j);
       mark(5);
-      // 1.+2. warp 0 inverts A_j (its Grams are final since the previous refresh)
-      // while warps 1.. form had[c][l] = prod_{k != j} C_k[l][c] (rows l >= r and
-      // columns c >= R are zero), meet at a named barrier, then the K-split
-      // partial right-hand sides part[ks][s][l] = sum_c V_j[s][c] had[c][l]
-      int ksn = (TINY_NW - 1) / mt;
-      ksn = ksn < 1 ? 1 : (ksn > TINY_KSMAX ? TINY_KSMAX : ksn);
-      if (warp == 0) {
-        status |= warp_sweep_inverse8(a, Gsm, j, Ai, 8);
-        if (a.prof) prof_acc[4] += clock64() - prof_t;   // inverse alone (debug)
-      } else {
-        for (int e = tid - 32; e < R8 * 8; e += TINY_NT - 32) {
-          const int c = e >> 3, l = e & 7;
-          double f[TP_MAXD];
-#pragma unroll
-          for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < d && k != j) ? Cs[((size_t)k * 8 + l) * Rs + c] : 1.0;
-          double v = 1.0;
-#pragma unroll
-          for (int k = 0; k < TP_MAXD; ++k) v *= f[k];
-          had[e] = v;
-        }
-        asm volatile("bar.sync 1, %0;" ::"r"(TINY_NT - 32) : "memory");
-        mark(0);
-        const int ksteps = R8 / 4;
-        const double* va = Vs + (size_t)td.qo[j] * Rs;
-        for (int it = warp - 1; it < mt * ksn; it += TINY_NW - 1) {
-          const int m = it / ksn, ks = it - m * ksn;
-          const int kb = ksteps * ks / ksn, ke = ksteps * (ks + 1) / ksn;
-          const double* arow = va + (size_t)(m * 8 + g) * Rs + t4;
-          const double* bcol = had + t4 * 8 + g;
-          double c0 = 0.0, c1 = 0.0;
-#pragma unroll 4
-          for (int kk = kb; kk < ke; ++kk) dmma_8x8x4(c0, c1, arow[4 * kk], bcol[32 * kk]);
-          double* pr = part + ((size_t)ks * td.qmaxp + m * 8 + g) * TINY_PLD + 2 * t4;
-          pr[0] = c0; pr[1] = c1;
-        }
-      }
-      __syncthreads();
-      mark(1);
-      // 3. U_j[s][i] = sum_m rhs[s][m] A^-1[m][i]  (K = 8: two k-steps)
+      // U_j[s][i] = sum_m rhs[s][m] A^-1[m][i]  (K = 8: two k-steps; sums the K splits)
       if (warp < mt) {
         const int s = warp * 8 + g;
         double c0 = 0.0, c1 = 0.0;
@@ -1296,8 +1306,18 @@ __global__ void __launch_bounds__(TINY_NT, 1) als_tiny8(const __grid_constant__ 
       }
       __syncthreads();
       mark(2);
-      // 4. C_j, G_j
-      for (int it = warp; it <= ntc; it += TINY_NW) refresh_item(j, it);
+      const bool more = !(sweep == a.sweeps - 1 && j == d - 1);
+      const int jn = (j + 1 == d) ? 0 : j + 1;
+      if (warp == 0) {
+        refresh_item(j, ntc);   // G_j
+        __syncwarp();
+        if (more) status |= warp_sweep_inverse8(a, Gsm, jn, Ai, 8);
+        if (a.prof) prof_acc[4] += clock64() - prof_t;   // warp-0 path (debug)
+      } else if (worker) {
+        for (int it = wk; it < ntc; it += NWK) refresh_item(j, it);   // C_j
+        asm volatile("bar.sync 1, %0;" ::"r"(NTK) : "memory");
+        if (more) hadamard_rhs(jn);
+      }
       __syncthreads();
       mark(3);
     }

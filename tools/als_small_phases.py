@@ -18,7 +18,7 @@ cp.cp_approx_als(T, r, cfg, init=I0)
 torch.cuda.synchronize()
 L.tp_debug_set_als_profile(None)
 p = prof.cpu().numpy()[:6] / (6.0 * sw)
-names = ["hadamard", "rhs+inverse", "U_j", "refresh C,G", "(inverse)", "loop head"]
+names = ["-", "-", "U_j", "refresh+next(had,rhs | G,inverse)", "(warp-0 path)", "loop head"]
 print(f"cycles per mode update: total {p.sum() - p[4]:.0f}")
 for n, v in zip(names, p):
     print(f"  {n:12s} {v:7.0f}")
