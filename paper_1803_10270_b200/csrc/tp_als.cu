@@ -79,6 +79,7 @@ struct AlsArgs {
   int ns_max;              // Newton-Schulz iterations before falling back to the exact sweep
   int clustered;           // als_persistent launched as ONE cluster of P CTAs: cluster barriers
   int local_gram;          // als_persistent: every CTA forms the whole Gram of the pending mode
+  int early_inv;           // als_persistent, r <= 16: exact A_j^-1 formed in phase A by warps 0-3
 };
 
 struct Smem {
@@ -187,20 +188,27 @@ __device__ void stage_u(const AlsArgs& a, const Smem& sm, int k, uint32_t& phase
 // tensor pipe: M = l, N = c, K = s.  A work item is (N tile, K range); its warp
 // runs all RM/8 M tiles as independent accumulator chains; the K-range partials
 // are summed in fixed order through scratch (sm.X1.., free in phase A).
+// wbase/nw/barid: run on warps [wbase, wbase + nw) synchronised by named barrier
+// barid (0 = the whole CTA, __syncthreads)
 template <int RM>
-__device__ void cross_slab(const AlsArgs& a, const Smem& sm, int k, int w) {
+__device__ void cross_slab(const AlsArgs& a, const Smem& sm, int k, int w, int wbase = 0, int nw = ALS_NW,
+                           int barid = 0) {
   constexpr int MT = RM / 8;
   const int r = a.r, Q = a.q[k], ru = pad4(r), qs = a.qs[k];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - wbase, nthr = nw * 32;
+  auto sync = [&]() {
+    if (barid == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(nthr) : "memory");
+  };
   const double* vs = sm.Vs + a.qoff[k];
   double* C = sm.Cs + (size_t)k * r * a.wmax;
   double* part = sm.X1;                                   // 2 r pad4(r) doubles
   const int nt = (w + 7) / 8, ksteps = (Q + 3) / 4, cap = 2 * r * ru;
-  int kp = ALS_NW / nt;
+  int kp = nw / nt;
   if (kp < 1) kp = 1;
   while (kp > 1 && nt * kp * MT * 64 > cap) --kp;
   const int per = (ksteps + kp - 1) / kp;
-  for (int it = warp; it < nt * kp; it += ALS_NW) {
+  for (int it = warp; it < nt * kp; it += nw) {
     const int n = it / kp, q = it - n * kp;
     const int c = n * 8 + (lane >> 2);
     double acc[MT][2];
@@ -239,16 +247,16 @@ __device__ void cross_slab(const AlsArgs& a, const Smem& sm, int k, int w) {
       }
     }
   }
-  __syncthreads();
+  sync();
   if (kp > 1) {
-    for (int e = threadIdx.x; e < nt * MT * 64; e += ALS_NT) {
+    for (int e = threadIdx.x - wbase * 32; e < nt * MT * 64; e += nthr) {
       const int n = e / (MT * 64), rem = e - n * MT * 64, m = rem >> 6, ln = (rem & 63) >> 1, h = rem & 1;
       const int orow = m * 8 + (ln >> 2), ocol = n * 8 + 2 * (ln & 3) + h;
       double acc = 0.0;
       for (int q = 0; q < kp; ++q) acc += part[((size_t)(n * kp + q) * MT + m) * 64 + 2 * ln + h];
       if (orow < r && ocol < w) C[orow * a.wmax + ocol] = acc;
     }
-    __syncthreads();
+    sync();
   }
 }
 
@@ -585,6 +593,107 @@ __device__ void ns_rows(const AlsArgs& a, const Smem& sm, int j, int sweep) {
   }
 }
 
+// Early-inverse path (als_persistent, r <= 16): warps 0-3 form the whole Gram of
+// mode k from the staged U (one 8x8 upper tile per warp, full K chain) into
+// sm.Gs[k]; named barrier 2 over those 128 threads.
+template <int RM>
+__device__ void gram_local_w4(const AlsArgs& a, const Smem& sm, int k) {
+  const int r = a.r, Q = a.q[k], ru = pad4(r), lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mt = (r + 7) / 8, ntile = mt * (mt + 1) / 2;
+  double* G = sm.Gs + (size_t)k * r * r;
+  for (int t = warp; t < ntile; t += 4) {
+    int ti = 0, rem = t;
+    while (rem >= mt - ti) { rem -= mt - ti; ++ti; }
+    const int tj = ti + rem, l = ti * 8 + (lane >> 2), m = tj * 8 + (lane >> 2);
+    double acc0 = 0.0, acc1 = 0.0;
+    const int ksteps = (Q + 3) / 4;
+#pragma unroll 4
+    for (int kk = 0; kk < ksteps; ++kk) {
+      const int s = 4 * kk + (lane & 3);
+      const double fa = (s < Q && l < r) ? sm.Us[s * ru + l] : 0.0;
+      const double fb = (s < Q && m < r) ? sm.Us[s * ru + m] : 0.0;
+      dmma_8x8x4(acc0, acc1, fa, fb);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int orow = ti * 8 + (lane >> 2), ocol = tj * 8 + 2 * (lane & 3) + h;
+      const double v = h ? acc1 : acc0;
+      if (orow < r && ocol < r) { G[orow * r + ocol] = v; G[ocol * r + orow] = v; }
+    }
+  }
+  asm volatile("bar.sync 2, 128;" ::: "memory");
+}
+
+// gram_inverse on the 128 threads of warps 0-3 (RM <= 16: thread t owns row t/8,
+// columns t%8 + 8u), named barrier 2 instead of the block barrier
+template <int RM>
+__device__ int gram_inverse_w4(const AlsArgs& a, const Smem& sm, int j, double* out, int os) {
+  constexpr int EPT = RM / 8;
+  const int r = a.r, gk = r * r, t = threadIdx.x;
+  const int i = t >> 3, c0 = t & 7;
+  double v[EPT];
+#pragma unroll
+  for (int u = 0; u < EPT; ++u) {
+    const int c = c0 + 8 * u;
+    double x = 0.0;
+    if (i < r && c < r) {
+      double f[TP_MAXD];
+#pragma unroll
+      for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < a.d && k != j) ? sm.Gs[(size_t)k * gk + i * r + c] : 1.0;
+      x = 1.0;
+#pragma unroll
+      for (int k = 0; k < TP_MAXD; ++k) x *= f[k];
+    }
+    v[u] = x;
+  }
+  double lam = a.reg;
+  if (a.reg_mode) {
+#pragma unroll
+    for (int u = 0; u < EPT; ++u)
+      if (c0 + 8 * u == i && i < r) sm.part[i] = v[u];
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    double tr = 0.0;
+    for (int q = 0; q < r; ++q) tr += sm.part[q];
+    lam = a.reg * fmax(tr, 0.0) / (double)r;
+  }
+#pragma unroll
+  for (int u = 0; u < EPT; ++u)
+    if (c0 + 8 * u == i && i < r) v[u] += lam;
+  if (i == 0)
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) sm.pub[c0 + 8 * u] = v[u];
+  asm volatile("bar.sync 2, 128;" ::: "memory");
+  int bad = 0;
+  for (int k = 0; k < r; ++k) {
+    const double* rk = sm.pub + (k & 1) * 36;
+    double* rn = sm.pub + ((k + 1) & 1) * 36;
+    const double d = rk[k];
+    if (!(d > 0.0) || !isfinite(d)) bad = 1;
+    const double id = rcp_nr(d);
+    const double f = (i < r ? rk[i] : 0.0) * id;
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const int c = c0 + 8 * u;
+      const double akc = rk[c];
+      double nv = fma(-f, akc, v[u]);
+      nv = (c == k) ? f : nv;
+      nv = (i == k) ? ((c == k) ? -id : akc * id) : nv;
+      v[u] = nv;
+    }
+    if (i == k + 1)
+#pragma unroll
+      for (int u = 0; u < EPT; ++u) rn[c0 + 8 * u] = v[u];
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+  }
+  if (i < r)
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const int c = c0 + 8 * u;
+      if (c < r) out[i * os + c] = -v[u];
+    }
+  return bad;
+}
+
 // debug phase timers: barrier-synchronised so the attribution is exact
 #define PROF(ph)                                                        \
   do {                                                                  \
@@ -661,8 +770,134 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   const bool local = P == 1;
   bool staged = false;     // local: sm.Us already holds the pending factor (padded rows)
 
+  // early-inverse mode (r <= 16, multi-CTA): no Newton-Schulz warm starts; phase A
+  // is warp-specialised -- warps 0-3 form the Gram of the previous mode and the
+  // exact inverse of A_j while warps 4-7 form the Hadamard and the partial
+  // right-hand side -- so phase B is one fixed-order reduction and one mat-vec
+  const bool ei = RM <= 16 && a.early_inv && !local;
   for (int sweep = 0; sweep < a.sweeps; ++sweep) {
     for (int j = 0; j < a.d; ++j) {
+      if (ei) {
+        PROF(0);
+        if (pending >= 0) {
+          stage_u(a, sm, pending, bphase);
+          PROF(10);
+          cross_slab<RM>(a, sm, pending, w);   // all warps (measured: the cross on warps 4-7 in
+          PROF(11);                            // parallel with the inverse is slower, 490 vs 458 us)
+        }
+        const int Qj = a.q[j], qsj = a.qs[j];
+        if (warp < 4) {
+          if (pending >= 0) gram_local_w4<RM>(a, sm, pending);
+          status |= gram_inverse_w4<RM>(a, sm, j, sm.X0, rh);
+        } else {
+          for (int e = tid - 128; e < r * w; e += ALS_NT - 128) {
+            const int l = e / w, c = e - l * w;
+            double f[TP_MAXD];
+#pragma unroll
+            for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < a.d && k != j) ? sm.Cs[((size_t)k * r + l) * a.wmax + c] : 1.0;
+            double v = 1.0;
+#pragma unroll
+            for (int k = 0; k < TP_MAXD; ++k) v *= f[k];
+            sm.hadT[c * rh + l] = v;
+          }
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+          constexpr int NT = RM / 8;
+          const double* vs = sm.Vs + a.qoff[j];
+          const int mt = (Qj + 7) / 8, kst = w4 / 4;
+          for (int m = warp - 4; m < mt; m += ALS_NW - 4) {
+            const int s = m * 8 + (lane >> 2);
+            const bool srow = s < Qj;
+            const int rm = srow ? sm.rowmap[j * a.qmax + s] : 0;
+            const int pc = rm >> 16, ii = rm & 0xffff;
+            double* yrow = a.Y + (((size_t)pc * P + p) * a.ncolmax + ii) * r;
+            double acc[NT][2];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+            for (int kk = 0; kk < kst; ++kk) {
+              const int c = 4 * kk + (lane & 3);
+              const double av = (srow && c < w) ? vs[c * qsj + s] : 0.0;
+              double fb[NT];
+#pragma unroll
+              for (int n = 0; n < NT; ++n) {
+                const int l = n * 8 + (lane >> 2);
+                fb[n] = (l < r) ? sm.hadT[c * rh + l] : 0.0;
+              }
+#pragma unroll
+              for (int n = 0; n < NT; ++n) dmma_8x8x4(acc[n][0], acc[n][1], av, fb[n]);
+            }
+            if (srow) {
+#pragma unroll
+              for (int n = 0; n < NT; ++n) {
+                const int ocol = n * 8 + 2 * (lane & 3);
+                if (ocol < r) yrow[ocol] = acc[n][0];
+                if (ocol + 1 < r) yrow[ocol + 1] = acc[n][1];
+              }
+            }
+          }
+        }
+        PROF(2);
+        all_barrier(a, epoch);
+        PROF(3);
+        const int s0 = (int)((long long)Qj * p / P), s1 = (int)((long long)Qj * (p + 1) / P);
+        const int ncol = s1 - s0, E = ncol * r, nb = a.ncolmax * r;
+        double* ystage = sm.Us;
+        if (bulk) {
+          if (tid == 0) {
+            const uint32_t ybytes = E > 0 ? (uint32_t)(P * nb) * 8u : 0u;
+            fence_proxy_async();
+            mbar_arrive_expect_tx(sm.bar, ybytes);
+            if (ybytes) bulk_g2s(ystage, a.Y + (size_t)p * P * nb, ybytes, sm.bar);
+          }
+          mbar_wait(sm.bar, bphase);
+          bphase ^= 1u;
+          for (int o = tid; o < E; o += ALS_NT) {
+            double q0 = 0.0, q1 = 0.0;
+            int q = 0;
+            for (; q + 2 <= P; q += 2) { q0 += ystage[(size_t)q * nb + o]; q1 += ystage[(size_t)(q + 1) * nb + o]; }
+            for (; q < P; ++q) q0 += ystage[(size_t)q * nb + o];
+            sm.rb[o] = q0 + q1;
+          }
+        } else {
+          for (int o = tid; o < E; o += ALS_NT) {
+            double acc = 0.0;
+            for (int q = 0; q < P; ++q) acc += __ldcg(a.Y + ((size_t)p * P + q) * nb + o);
+            sm.rb[o] = acc;
+          }
+        }
+        __syncthreads();
+        PROF(5);
+        {   // U_j rows = (A_j^-1 b)^T  (cp.py:317)
+          constexpr int TPO = RM / 8;
+          double* ub = sm.vb + 2 * a.ncolmax * r;
+          for (int base = 0; base < E * TPO; base += ALS_NT) {
+            const int t = base + tid, o = t / TPO, part = t - o * TPO;
+            const bool act = o < E;
+            const int sc = act ? o / r : 0, i = act ? o - sc * r : 0;
+            const double u = mv_dot<RM>(sm.X0, rh, sm.rb + sc * r, i, r, part);
+            if (act && part == 0) ub[o] = u;
+          }
+          __syncthreads();
+          PROF(9);
+          if (E > 0) {
+            double* Uj = a.U + a.offU[j];
+            double* Up = a.Upad + a.offUp[j];
+            int nf = 0;
+            for (int e = tid; e < E; e += ALS_NT) {
+              const int sc = e / r, i = e - sc * r;
+              const double v = ub[e];
+              if (!isfinite(v)) nf = 1;
+              Uj[(size_t)(s0 + sc) * r + i] = v;
+              Up[(size_t)(s0 + sc) * rh + i] = v;
+            }
+            if (nf) atomicOr(a.info, 2);
+          }
+        }
+        pending = j;
+        PROF(6);
+        all_barrier(a, epoch);
+        PROF(7);
+        continue;
+      }
       // ---------------- phase A
       PROF(0);
       if (pending >= 0) {
@@ -829,7 +1064,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       // finish the last mode, then residual by the Gram identity (cp.py:321-326)
       stage_u(a, sm, pending, bphase);
       cross_slab<RM>(a, sm, pending, w);
-      gram_share(a, sm, pending, a.local_gram != 0);
+      gram_share(a, sm, pending, a.local_gram != 0 || ei);
       double ov = 0.0;
       for (int e = tid; e < r * w; e += ALS_NT) {
         const int l = e / w, c = e % w;
@@ -1858,6 +2093,7 @@ struct AlsPlan {
   size_t smem, ws_inner, ws_total, ydoubles;
 };
 
+static int g_early_inv = 1;   // debug hook: early exact inverse in the clustered R-slab kernel (r <= 16)
 static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 force als_cluster, 3 force als_small,
                             // 4 force als_persistent as one cluster (grid = cluster size), 5 force als_tiny8
 static int g_cluster = 0;   // debug hook: cluster size (0 = auto)
@@ -1967,6 +2203,7 @@ static int plan_persistent_cluster(int d, const int* q, int R, int r, int Pc, in
   int qo = 0;
   for (int k = 0; k < d; ++k) { a.qoff[k] = qo; qo += a.qs[k] * wmax; }
   a.wmax = wmax; a.ncolmax = ncolmax; a.P = Pc; a.Pq = Pc; a.clustered = 1;
+  a.early_inv = (r <= 16 && g_early_inv) ? 1 : 0;
   pl.P = Pc; pl.Pr = Pc; pl.smem = smem; pl.variant = 3;
   pl.ydoubles = (size_t)Pc * Pc * ncolmax * r;
   pl.ws_total = ws_total_for(d, q, r, Pc, pl.ydoubles, pl.ws_inner);
@@ -1988,7 +2225,7 @@ static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
   PlanKey key;
   memset(&key, 0, sizeof(key));
   if (cudaGetDevice(&key.dev) != cudaSuccess) { cudaGetLastError(); key.dev = -1; }
-  key.d = d; key.R = R; key.r = r; key.grid = grid; key.variant = g_variant; key.cluster = g_cluster;
+  key.d = d; key.R = R; key.r = r; key.grid = grid; key.variant = g_variant * 2 + g_early_inv; key.cluster = g_cluster;
   for (int k = 0; k < d; ++k) key.q[k] = q[k];
   {
     std::lock_guard<std::mutex> lk(mu);
@@ -2047,6 +2284,7 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
     ov += (long long)q[k] * R; ou += (long long)q[k] * r; qo += a.qs[k] * a.wmax; oup += (long long)q[k] * pad4(r);
   }
   a.local_gram = 0;   // (r <= 16 measured slower: 3 tiles recomputed cost more than the round trip)
+  a.early_inv = (r <= 16 && P > 1 && g_early_inv) ? 1 : 0;   // exact inverse formed in phase A (warps 0-3)
   pl.P = P;
   pl.smem = smem;
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
@@ -2062,10 +2300,11 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
     if (plan_persistent_cluster(d, q, R, r, Pc, smem_optin, pl) == TP_OK) return TP_OK;
     return TP_EUNSUPPORTED;
   }
-  // measured (tools/als_cl_scan.py): config 3 (Q=64, R=588, r=12) 9.41 -> 8.75 us per
-  // mode update as one 16-CTA cluster instead of 36 CTAs with grid barriers; larger
-  // Q (128) loses, so only short modes take it
-  if (g_variant == 0 && grid <= 0 && P >= 12 && P <= 40 && qmax <= 64) {
+  // measured (tools/als_cl_scan.py, tools/ei_scan.sh; with the early inverse for r <= 16):
+  // one 16-CTA cluster beats the grid-barrier R-slab kernel at 12-49 CTAs -- config 3
+  // (Q=64, R=588, r=12) 8.37 -> 7.60 us per mode update, (96, 200, 8) 7.89 -> 6.77,
+  // (128, 300, 16) 9.26 -> 9.11
+  if (g_variant == 0 && grid <= 0 && P >= 8 && P <= 64) {
     AlsPlan cp = pl;
     if (plan_persistent_cluster(d, q, R, r, 16, smem_optin, cp) == TP_OK) { pl = cp; return TP_OK; }
   }
@@ -2125,6 +2364,7 @@ void tp_debug_set_als_skip(int mask) { g_skip = mask; }
 void tp_debug_set_als_ns(int n) { g_ns_max = n; }
 // debug hook: kernel variant (0 auto, 1 als_persistent, 2 als_cluster) and cluster size (0 auto, -1 never)
 void tp_debug_set_als_variant(int variant, int cluster) { g_variant = variant; g_cluster = cluster; }
+void tp_debug_set_als_early_inv(int on) { g_early_inv = on; }
 
 int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out) {
   if (!out) return TP_EINVAL;

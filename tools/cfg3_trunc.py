@@ -60,3 +60,15 @@ for label, T, U0 in [("real", tgt, f2.data), ("random", None, None)]:
         p = prof.cpu().numpy() / 60.0
         print(label, "ns", ns, f"total {p[:16].sum():.0f}", " ".join(f"{NAMES[i]}={p[i]:.0f}" for i in [10, 11, 1, 2, 3, 8, 4, 9, 6, 7]))
 Lb.tp_debug_set_als_ns(6)
+Lb.tp_debug_set_als_early_inv.argtypes = [ctypes.c_int]
+for ei in (1, 0, 1):
+    Lb.tp_debug_set_als_early_inv(ei)
+    for _ in range(3):
+        U.copy_(f2.data); cp._als_device(tgt, U, w["r"], als, None, info)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        U.copy_(f2.data); cp._als_device(tgt, U, w["r"], als, None, info)
+    e1.record(); torch.cuda.synchronize()
+    print("early_inv", ei, f"{e0.elapsed_time(e1) / 20 * 1e3:.1f} us per truncation", info.tolist(), cp.als_plan(tgt.qs, tgt.rank, w["r"]))
