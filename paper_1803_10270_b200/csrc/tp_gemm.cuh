@@ -136,11 +136,16 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 // 32 x 32, m8n8k4 DMMA), with a STAGES-deep cp.async ring of TK-deep K tiles in
 // dynamic shared memory and 16-byte copies along a contiguous, 16-byte aligned
 // M (A) / N (B) dimension.
-template <int STAGES, int TK>
+// AK / BK: operand stored K-contiguous in global memory (sAk == 1 / sBk == 1 with the
+// other stride != 1): the tile is kept [m][k] in shared memory (row stride TK + 4,
+// conflict-free fragments) and filled with 16-byte copies along K.
+template <int STAGES, int TK, bool AK = false, bool BK = false>
 static __global__ void __launch_bounds__(128) bgemm_pipe_kernel(const __grid_constant__ BGemm g) {
   extern __shared__ double gsm[];
-  double* As = gsm;                                  // [STAGES][TK][GB_LD]
-  double* Bs = gsm + (size_t)STAGES * TK * GB_LD;    // [STAGES][TK][GB_LD]
+  constexpr int LDK = TK + 4;
+  constexpr int SA = AK ? GB_TM * LDK : TK * GB_LD, SB = BK ? GB_TN * LDK : TK * GB_LD;   // per stage
+  double* As = gsm;                                  // [STAGES][SA]
+  double* Bs = gsm + (size_t)STAGES * SA;            // [STAGES][SB]
   const int ks = g.ksplit > 1 ? g.ksplit : 1;
   const int zz = blockIdx.z / ks, sidx = blockIdx.z - zz * ks;
   const int z1 = zz / g.nb2, z2 = zz % g.nb2;
@@ -192,10 +197,29 @@ static __global__ void __launch_bounds__(128) bgemm_pipe_kernel(const __grid_con
       }
     }
   };
+  // K-contiguous operand -> [i][k] tile (row stride LDK), 16-byte copies of k pairs
+  auto load_tile_k = [&](const double* X, long long sXi, int I, int i0, bool vec, double* dst, int k0) {
+#pragma unroll 2
+    for (int e = tid; e < GB_TM * TK / 2; e += 128) {
+      const int ii = e / (TK / 2), kk = 2 * (e % (TK / 2));
+      const int i = i0 + ii, k = k0 + kk;
+      double* d = dst + ii * LDK + kk;
+      if (vec && i < I && k + 1 < g.K) {
+        cp_async16(d, X + i * sXi + k);
+      } else {
+        cp_async8(d, X + ((i < I && k < g.K) ? i * sXi + k : 0), i < I && k < g.K);
+        cp_async8(d + 1, X + ((i < I && k + 1 < g.K) ? i * sXi + k + 1 : 0), i < I && k + 1 < g.K);
+      }
+    }
+  };
+  const bool ak_vec = AK && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (g.sAm % 2 == 0);
+  const bool bk_vec = BK && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) && (g.sBn % 2 == 0);
   auto issue = [&](int kt, int buf) {
     const int k0 = kt * TK;
-    load_tile(A, g.sAm, g.sAk, g.M, m0, a_m_fast, a_vec, As + (size_t)buf * TK * GB_LD, k0);
-    load_tile(B, g.sBn, g.sBk, g.N, n0, b_n_fast, b_vec, Bs + (size_t)buf * TK * GB_LD, k0);
+    if (AK) load_tile_k(A, g.sAm, g.M, m0, ak_vec, As + (size_t)buf * SA, k0);
+    else load_tile(A, g.sAm, g.sAk, g.M, m0, a_m_fast, a_vec, As + (size_t)buf * SA, k0);
+    if (BK) load_tile_k(B, g.sBn, g.N, n0, bk_vec, Bs + (size_t)buf * SB, k0);
+    else load_tile(B, g.sBn, g.sBk, g.N, n0, b_n_fast, b_vec, Bs + (size_t)buf * SB, k0);
   };
   // prologue: STAGES - 1 tiles in flight (one commit group per stage, possibly empty)
 #pragma unroll
@@ -209,16 +233,16 @@ static __global__ void __launch_bounds__(128) bgemm_pipe_kernel(const __grid_con
     __syncthreads();   // tile `it` visible to all; the buffer refilled below is free
     if (kt + STAGES - 1 < kt1) issue(kt + STAGES - 1, (it + STAGES - 1) % STAGES);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
-    const double* Ab = As + (size_t)buf * TK * GB_LD;
-    const double* Bb = Bs + (size_t)buf * TK * GB_LD;
+    const double* Ab = As + (size_t)buf * SA;
+    const double* Bb = Bs + (size_t)buf * SB;
 #pragma unroll
     for (int ksub = 0; ksub < TK; ksub += 4) {
       const int kr = ksub + (lane & 3), cc = lane >> 2;
       double fa[4], fb[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) fa[i] = Ab[kr * GB_LD + wm + 8 * i + cc];
+      for (int i = 0; i < 4; ++i) fa[i] = AK ? Ab[(wm + 8 * i + cc) * LDK + kr] : Ab[kr * GB_LD + wm + 8 * i + cc];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) fb[j] = Bb[kr * GB_LD + wn + 8 * j + cc];
+      for (int j = 0; j < 4; ++j) fb[j] = BK ? Bb[(wn + 8 * j + cc) * LDK + kr] : Bb[kr * GB_LD + wn + 8 * j + cc];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -274,11 +298,11 @@ static inline BGemm bgemm_desc(int M, int N, int K, const double* A, long long s
 }
 
 // split-K factor that fills the GPU (>= 2 CTAs per SM) for K-heavy batched GEMMs
-static inline int bgemm_pick_split(const BGemm& g, int nsm = 148, int min_ktiles = 8) {
+static inline int bgemm_pick_split(const BGemm& g, int nsm = 148, int min_ktiles = 8, int waves = 2) {
   const long long tiles = (long long)((g.N + GB_TN - 1) / GB_TN) * ((g.M + GB_TM - 1) / GB_TM) * g.nb1 * g.nb2;
   const int ktiles = (g.K + GB_TK - 1) / GB_TK;
   int s = 1;
-  while (tiles * s < 2LL * nsm && ktiles / (2 * s) >= min_ktiles) s *= 2;
+  while (tiles * s < (long long)waves * nsm && ktiles / (2 * s) >= min_ktiles) s *= 2;
   return s;
 }
 
@@ -286,15 +310,30 @@ static inline int bgemm_pick_split(const BGemm& g, int nsm = 148, int min_ktiles
 // 1 = 3-stage TK 16, 2 = 2-stage TK 32, 3 = 3-stage TK 32, 4 = 4-stage TK 16
 static int g_bgemm_variant = 1;
 
-template <int STAGES, int TK>
-static inline void bgemm_pipe_launch(dim3 grid, const BGemm& h, cudaStream_t st) {
-  const size_t smem = sizeof(double) * 2 * STAGES * TK * GB_LD;
+template <int STAGES, int TK, bool AK, bool BK>
+static inline void bgemm_pipe_launch_k(dim3 grid, const BGemm& h, cudaStream_t st) {
+  constexpr int LDK = TK + 4;
+  const size_t smem = sizeof(double) * STAGES * ((AK ? GB_TM * LDK : TK * GB_LD) + (BK ? GB_TN * LDK : TK * GB_LD));
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(bgemm_pipe_kernel<STAGES, TK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(bgemm_pipe_kernel<STAGES, TK, AK, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
-  bgemm_pipe_kernel<STAGES, TK><<<grid, 128, smem, st>>>(h);
+  bgemm_pipe_kernel<STAGES, TK, AK, BK><<<grid, 128, smem, st>>>(h);
+}
+
+// K-contiguous operands (stride 1 along K, not along M / N) take the [i][k] layout
+static int g_bgemm_klayout = 1;
+
+template <int STAGES, int TK>
+static inline void bgemm_pipe_launch(dim3 grid, const BGemm& h, cudaStream_t st) {
+  const bool ak = g_bgemm_klayout && h.sAm != 1 && h.sAk == 1;
+  const bool bk = g_bgemm_klayout && h.sBn != 1 && h.sBk == 1;
+  if (ak && bk) bgemm_pipe_launch_k<STAGES, TK, true, true>(grid, h, st);
+  else if (ak) bgemm_pipe_launch_k<STAGES, TK, true, false>(grid, h, st);
+  else if (bk) bgemm_pipe_launch_k<STAGES, TK, false, true>(grid, h, st);
+  else bgemm_pipe_launch_k<STAGES, TK, false, false>(grid, h, st);
 }
 
 static inline cudaError_t bgemm_launch(const BGemm& g, cudaStream_t st) {

@@ -652,7 +652,7 @@ __global__ void set_root_env(int k, int nn, int nb, double* Gh) {
 }
 
 // split-K partial tiles: bgemm_pick_split only splits below 2 x 148 x 2 CTAs of 64 x 64
-constexpr size_t HT_PART = (size_t)GB_TM * GB_TN * 4 * 148;
+constexpr size_t HT_PART = (size_t)GB_TM * GB_TN * 8 * 148;
 
 struct HtPlan {
   Tree T;
@@ -692,6 +692,7 @@ static void plan_ht(int d, int Q, int k, int nb, int r_max, HtPlan& P) {
 
 using namespace tp;
 
+static int g_split_waves = 4;   // debug hook: split-K until tiles x splits >= waves x 148 CTAs
 static int g_jac_sweeps = 30;
 static double g_jac_tol = 1e-16;
 static int* g_jac_count = nullptr;
@@ -706,6 +707,8 @@ void tp_debug_set_jacobi(int max_sweeps, double tol, int* count) {
 }
 // debug hook: batched-GEMM kernel variant of the hSVD chain (tp_gemm.cuh g_bgemm_variant)
 void tp_debug_set_bgemm_variant(int v) { g_bgemm_variant = v; }
+void tp_debug_set_ht_split_waves(int w) { g_split_waves = w; }
+void tp_debug_set_bgemm_klayout(int on) { g_bgemm_klayout = on; }
 // debug hook: frame-Gram factor by Cholesky (1, default) or eigh (0)
 void tp_debug_set_ht_chol(int on) { g_chol = on; }
 // debug hook: Jacobi kernel (0 = three-barrier rounds, 1 = double-buffered blocks, 2 = upper-triangle blocks, default)
@@ -776,7 +779,7 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
   auto add_gemm = [&](BGemm g, const std::vector<long long>& offs) {
     Call c{g, 0, 0};
     if (!offs.empty()) { c.tab = table(offs); c.use_tab = 1; c.g.nb1 = (int)(offs.size() / 3); }
-    const int ks = bgemm_pick_split(c.g);
+    const int ks = bgemm_pick_split(c.g, 148, 8, g_split_waves);
     if (ks > 1 && (size_t)c.g.M * c.g.N * c.g.nb1 * c.g.nb2 * ks <= HT_PART) { c.g.ksplit = ks; c.g.part = kpart; }
     calls.push_back(c);
     order.push_back((int)calls.size() - 1);
