@@ -261,3 +261,26 @@ def test_als_tiny8_variant(als_variant, qs, R, r):
 def test_als_auto_plan_config0_is_tiny8():
     from paper_1803_10270_b200 import cp as _cp
     assert _cp.als_plan((32,) * 6, 78, 6)["kernel"] == "als_tiny8"
+
+
+@pytest.mark.parametrize("early", [0, 1])
+@pytest.mark.parametrize("variant", [1, 4])
+def test_als_early_inverse_toggle(als_variant, variant, early):
+    """r <= 16 multi-CTA truncations with the exact inverse formed in phase A by warps
+    0-3 (default) and with the phase-B Newton-Schulz / exact solve (debug hook off)."""
+    import ctypes
+    from paper_1803_10270_b200 import _lib
+    L = _lib.lib()
+    L.tp_debug_set_als_early_inv.argtypes = [ctypes.c_int]
+    als_variant(variant, 0)
+    L.tp_debug_set_als_early_inv(early)
+    try:
+        rng = np.random.default_rng(40 + early)
+        qs, R, r = (64, 48, 33, 64, 20), 150, 12
+        V = rand_factors(rng, qs, R, 0.25)
+        init = [v[:, :r].copy() for v in V]
+        out, ref, trace, otrace = _als_case(V, init, 8, 1e-10)
+        assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+        np.testing.assert_allclose(trace, otrace, rtol=1e-8, atol=1e-12)
+    finally:
+        L.tp_debug_set_als_early_inv(1)
