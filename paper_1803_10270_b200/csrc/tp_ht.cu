@@ -583,17 +583,27 @@ __global__ void __launch_bounds__(256) form_st_kernel(int k, int ro, int nn, con
   if (ok[base]) {
     // Cholesky factor: S = L^-T W_keep (back substitution, 16 threads per column),
     // T = S^T M = W_keep^T L^T
+    // L, the kept columns of W and 1 / diag(L) staged in shared memory first (coalesced):
+    // the 64-step back substitution then runs on shared operands only
     const double* L = Vm + base * k * k;
     const double* W = Wg + base * k * k;
-    double* Sl = ss;   // [k][ro]
+    double* Sl = ss;                         // [k][ro]
+    double* Ls = Sl + (size_t)k * ro;        // [k][k + 1]
+    double* Ws = Ls + (size_t)k * (k + 1);   // [k][ro]
+    double* dinv = Ws + (size_t)k * ro;      // [k]
+    for (int e = threadIdx.x; e < k * k; e += 256) Ls[(e / k) * (k + 1) + e % k] = L[e];
+    for (int e = threadIdx.x; e < k * ro; e += 256) Ws[e] = W[(e / ro) * k + e % ro];
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += 256) dinv[i] = 1.0 / Ls[i * (k + 1) + i];
+    __syncthreads();
     const int c = threadIdx.x >> 4, part = threadIdx.x & 15;
     for (int i = k - 1; i >= 0; --i) {
       double acc = 0.0;
       if (c < ro)
-        for (int m = i + 1 + part; m < k; m += 16) acc = fma(L[m * k + i], Sl[m * ro + c], acc);
+        for (int m = i + 1 + part; m < k; m += 16) acc = fma(Ls[m * (k + 1) + i], Sl[m * ro + c], acc);
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (c < ro && part == 0) Sl[i * ro + c] = (c < kp) ? (W[i * k + c] - acc) / L[i * k + i] : 0.0;
+      if (c < ro && part == 0) Sl[i * ro + c] = (c < kp) ? (Ws[i * ro + c] - acc) * dinv[i] : 0.0;
       __syncthreads();
     }
     for (int e = threadIdx.x; e < k * ro; e += 256) S[base * k * ro + e] = Sl[e];
@@ -601,7 +611,7 @@ __global__ void __launch_bounds__(256) form_st_kernel(int k, int ro, int nn, con
       const int cc = e / k, a2 = e % k;
       double acc = 0.0;
       if (cc < kp)
-        for (int i = 0; i <= a2; ++i) acc = fma(W[i * k + cc], L[a2 * k + i], acc);
+        for (int i = 0; i <= a2; ++i) acc = fma(Ws[i * ro + cc], Ls[a2 * (k + 1) + i], acc);
       T[base * ro * k + e] = acc;
     }
     return;
@@ -916,7 +926,8 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
   cudaFuncSetAttribute(jac, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm);
   const size_t fsm = sizeof(double) * 3 * (size_t)k * (k + 1);
   cudaFuncSetAttribute(form_g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-  const size_t ssm = sizeof(double) * ((size_t)k + (size_t)k * ro);
+  const size_t ssm = sizeof(double) * ((size_t)k + 2 * (size_t)k * ro + (size_t)k * (k + 1) + (size_t)k);
+  cudaFuncSetAttribute(form_st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
   const size_t csm = sizeof(double) * ((size_t)k * (k + 1) + 2);
   cudaFuncSetAttribute(chol_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   const int nonroot = nb * (nn - 1);

@@ -7,7 +7,7 @@ int main() {
   double *A, *B, *C;
   cudaMalloc(&A, 8ull << 27); cudaMalloc(&B, 8ull << 27); cudaMalloc(&C, 8ull << 27);
   cudaMemset(A, 0, 8ull << 27); cudaMemset(B, 0, 8ull << 27);
-  struct S { int M, N, K, nb; } shapes[] = {{4096, 4096, 1024, 1}, {64, 64, 4096, 256}, {64, 64, 4096, 1024}, {128, 16, 128, 4}, {64, 4096, 64, 64}, {64, 64, 4096, 128}};
+  struct S { int M, N, K, nb; } shapes[] = {{4096, 4096, 1024, 1}, {64, 64, 4096, 256}, {64, 64, 4096, 1024}, {128, 16, 128, 4}, {64, 4096, 64, 64}, {64, 64, 4096, 128}, {64, 64, 64, 16384}, {64, 64, 64, 2048}};
   double* part; cudaMalloc(&part, 8ull << 26);
   for (auto sh : shapes) {
     BGemm g = bgemm_desc(sh.M, sh.N, sh.K, A, sh.K, 1, B, sh.N, 1, C, sh.N, 1);
