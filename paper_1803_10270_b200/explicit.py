@@ -17,6 +17,7 @@ single status check at the end.
 from __future__ import annotations
 
 import math
+import weakref
 from dataclasses import dataclass, field
 
 import torch
@@ -27,6 +28,9 @@ from .ht import HTTensor
 from .operators import SeparableOperator
 
 __all__ = ["ExplicitConfig", "ReductionRecord", "ab2_step", "startup_step", "tensor_rank", "run"]
+
+# captured AB2 steps of explicit.run, per operator (weak: dropped with the operator)
+_GRAPHS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 @dataclass
@@ -182,24 +186,37 @@ def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, 
         if callback:
             callback(n, cur)
     if use_graph:
-        # static state buffers; the captured step rotates them in place
-        pbuf, cbuf = prev.data.clone(), cur.data.clone()
-        slot = infos[n_eager + 1]
-        agg = torch.zeros(2, dtype=torch.int32, device=dev)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            P = CPTensor(cur.specs, data=pbuf, rank=r)
-            C = CPTensor(cur.specs, data=cbuf, rank=r)
-            tgt = ab2_target(P, C, L, config.dt)
-            nxt = cbuf.clone()
-            cp._als_device(tgt, nxt, r, config.als, None, slot)
-            agg.bitwise_or_(slot)
-            pbuf.copy_(cbuf)
-            cbuf.copy_(nxt)
+        # one captured AB2 step on static state buffers (rotated in place by the step),
+        # cached per (operator, shapes, step configuration): later runs copy their
+        # states in and replay -- every kernel of every step still executes
+        a = config.als
+        key = (tuple(cur.specs), r, float(config.dt), a.max_sweeps, float(a.tol), float(a.stall), a.seed,
+               a.reg, a.grid, str(cur.data.dtype), dev.index)
+        per_op = _GRAPHS.setdefault(L, {})
+        hit = per_op.get(key)
+        if hit is None:
+            pbuf, cbuf = prev.data.clone(), cur.data.clone()
+            slot = torch.zeros(2, dtype=torch.int32, device=dev)
+            agg = torch.zeros(2, dtype=torch.int32, device=dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                P = CPTensor(cur.specs, data=pbuf, rank=r)
+                C = CPTensor(cur.specs, data=cbuf, rank=r)
+                tgt = ab2_target(P, C, L, config.dt)
+                nxt = cbuf.clone()
+                cp._als_device(tgt, nxt, r, config.als, None, slot)
+                agg.bitwise_or_(slot)
+                pbuf.copy_(cbuf)
+                cbuf.copy_(nxt)
+            hit = per_op[key] = (g, pbuf, cbuf, agg)
+        g, pbuf, cbuf, agg = hit
+        pbuf.copy_(prev.data)
+        cbuf.copy_(cur.data)
+        agg.zero_()
         for _ in range(n_eager + 1, steps + 1):
             g.replay()
         infos[n_eager + 1].copy_(agg)
-        cur = CPTensor(cur.specs, data=cbuf, rank=r)
+        cur = CPTensor(cur.specs, data=cbuf.clone(), rank=r)
     bad = int(infos[:, 0].max().item())
     if bad & 2:
         raise cp.ConditioningError("normal equations produced non-finite coefficients")

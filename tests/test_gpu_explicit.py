@@ -163,3 +163,18 @@ def test_graph_replay_matches_eager(which, steps):
     a = explicit.run(f0, L, cfg, steps, graph=False)
     b = explicit.run(f0, L, cfg, steps, graph=True)
     assert torch.equal(a.data, b.data)
+
+
+def test_graph_cache_reuse_new_initial_state():
+    """The captured AB2 step is cached per operator/configuration; a second run with a
+    different initial state must replay on its own data (equal to the eager result)."""
+    import torch
+    w, S, L, cfg, _ = _cfg0_setup(8)
+    f0 = cp.CPTensor(S, w["ic"]["factors"])
+    g0 = cp.scale(f0, 0.5)
+    a1 = explicit.run(f0, L, cfg, 8, graph=True)
+    a2 = explicit.run(g0, L, cfg, 8, graph=True)     # cached graph, new states
+    b2 = explicit.run(g0, L, cfg, 8, graph=False)
+    b1 = explicit.run(f0, L, cfg, 8, graph=False)
+    assert torch.equal(a1.data, b1.data) and torch.equal(a2.data, b2.data)
+    assert not torch.equal(a1.data, a2.data)
