@@ -25,7 +25,8 @@ truncation across ranks with an NCCL all-reduce of the r x Q right-hand side per
 mode update (strong scaling, BASELINE configs[1]) -- latency-bound at this size
 (120 dependent all-reduces per 1.5 ms truncation), see DESIGN.md section 7.
 ``extra_configs`` reports device-resident throughput of configs 0, 2, 3 (rank 0,
-N = 1) and of config 4 (batch of 64 HT tensors sharded across ranks).
+N = 1) and of config 4 (batch of 64 HT tensors sharded across ranks), each with a
+bounded ``cpu_baseline`` sample of the oracle port on the host cores (N = 1).
 """
 
 from __future__ import annotations
@@ -120,6 +121,61 @@ def cpu_baseline_run(seconds: float = 12.0):
     return {"value": n * SWEEPS / el, "unit": "sweeps/s", "cores": cores, "kind": "port",
             "sample": f"{n} full cfg1 truncations ({n * SWEEPS} sweeps) of the oracle (numpy complex128, "
                       f"reference arithmetic), {el:.1f} s wall"}
+
+
+def extra_cpu_baselines():
+    """Bounded samples of the oracle port (numpy, real fp64 -- the reference's complex128
+    arithmetic is slower still) for the other BASELINE configs, on the host cores."""
+    from oracle import explicit as oex
+    from oracle import ht_hsvd as oht
+    from oracle import implicit as oim
+    from paper_1803_10270_b200 import workloads
+    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    out = {}
+
+    def rec(name, value, unit, sample):
+        out[name] = {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": sample}
+
+    try:
+        w = workloads.cfg0(0)
+        d = len(w["specs"])
+        a = list(-np.asarray(w["a"]))
+        mats = [[w["D"] if k == t else None for k in range(d)] for t in range(d)]
+        t0 = time.perf_counter()
+        oex.run_fused(w["ic"]["factors"], a, mats, w["dt"], w["r"], 100, w["sweeps"], w["lam"])
+        el = time.perf_counter() - t0
+        rec("cfg0_advection_explicit", 100 / el, "time-steps/s", f"the whole 100-step run, {el:.2f} s")
+        w = workloads.cfg3(0)
+        t0 = time.perf_counter()
+        oex.run_fused(w["factors"], w["weights"], w["mats"], w["dt"], w["r"], 30, w["sweeps"], w["lam"])
+        el = time.perf_counter() - t0
+        rec("cfg3_bgk_explicit", 30 / el, "time-steps/s", f"30 of 200 fused-AB2 steps, {el:.2f} s")
+        w = workloads.cfg2(0)
+        S, D, a2, dt = w["specs"], w["D"], w["a"], w["dt"]
+        d, q = len(S), S[0].Q
+        facs = [[None] * d] + [[D if k == t else None for k in range(d)] for t in range(d)]
+        tabs = oim.build_tables(facs, [1.0] + [dt * x for x in a2], [1.0] + [0.0] * d, [q] * d)
+        t0 = time.perf_counter()
+        oim.step(w["ic"]["factors"], tabs, 1, w["lam"])
+        el = time.perf_counter() - t0
+        rec("cfg2_implicit_euler", 1.0 / (el * w["sweeps"]), "time-steps/s",
+            f"1 of the {w['sweeps']} Gauss-Seidel sweeps of one step (direct dense solves), scaled; {el:.1f} s")
+        w = workloads.cfg4(0, batch=2)
+        nodes = oht.balanced_tree(w["d"])
+        t0 = time.perf_counter()
+        for b in range(2):
+            frames, transfers, li, ii = [None] * len(nodes), [None] * len(nodes), 0, 0
+            for t, nd in enumerate(nodes):
+                if oht.is_leaf(nd):
+                    frames[t] = w["frames"][b, li]; li += 1
+                else:
+                    transfers[t] = w["transfers"][b, ii][:, :, :1] if t == 0 else w["transfers"][b, ii]; ii += 1
+            oht.truncate((nodes, frames, transfers), 16, 0.0)
+        el = time.perf_counter() - t0
+        rec("cfg4_hsvd_batch64", 2 / el, "tensors/s", f"2 of the 64 tensors (one process, threaded BLAS), {el:.2f} s")
+    except Exception as e:  # noqa: BLE001  (a baseline must never break the bench line)
+        out["error"] = f"{type(e).__name__}: {e}"
+    return out
 
 
 def run_reference(args):
@@ -450,6 +506,10 @@ def run_ours(args):
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_run(args.cpu_seconds)
     extras = extra_configs(world, rank, dev) if not args.no_extra else {}
+    if rank == 0 and world == 1 and not args.no_cpu and not args.no_extra:
+        for name, cb in extra_cpu_baselines().items():
+            if name in extras:
+                extras[name]["cpu_baseline"] = cb
     if rank == 0:
         line["extra_configs"] = extras
         print(json.dumps(line), flush=True)
