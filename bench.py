@@ -411,6 +411,24 @@ def run_ours(args):
     ms_per_step = tot_ms / args.steps
     achieved_tf = FLOPS_PER_STEP / (ms_per_step / 1e3) / 1e12
 
+    # steady-state sweeps/s without setup: the same truncation with 10
+    # and with 20 sweeps, per-sweep time = difference / 10 (outside the timed K steps)
+    def t_sweeps(n_sw, reps=5):
+        c = cp.ALSApproxConfig(max_sweeps=n_sw, tol=0.0, stall=-np.inf, reg=LAM, grid=args.grid)
+        tt = 0.0
+        for _ in range(reps):
+            flush.fill_(1.0)
+            U.copy_(I0.data)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            cp._als_device(T, U, RANK_R, c, None, info)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            tt += a0.elapsed_time(a1)
+        return tt / reps
+    ms10, ms20 = t_sweeps(10), t_sweeps(20)
+    steady = 10.0 / ((ms20 - ms10) / 1e3) if ms20 > ms10 else None
+
     # ---- e2e: public API with pinned host buffers, H2D + call + D2H every step.
     # Two device buffer sets: the host->device copy of step i+1 runs on a copy
     # stream while step i computes (the production pipeline); every step's inputs
@@ -502,6 +520,8 @@ def run_ours(args):
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "wall_s_timed_region": t_wall,
+            "steady_state_sweeps_per_s": steady,
+            "setup_ms": (2 * ms10 - ms20) if steady else None,
         }
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_run(args.cpu_seconds)
