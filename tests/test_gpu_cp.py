@@ -284,3 +284,30 @@ def test_als_early_inverse_toggle(als_variant, variant, early):
         np.testing.assert_allclose(trace, otrace, rtol=1e-8, atol=1e-12)
     finally:
         L.tp_debug_set_als_early_inv(1)
+
+
+@pytest.mark.parametrize("qs,R,r", [((7,), 5, 2), ((9, 1), 4, 1), ((1, 1, 1), 3, 1), ((6, 5), 1, 1), ((8, 7, 6), 3, 5),
+                                    ((2, 3, 2, 3, 2, 3, 2, 3), 4, 3)])
+def test_als_edge_shapes(qs, R, r):
+    """Degenerate shapes the reference accepts: one mode, Q = 1 modes, rank-1 targets,
+    r > R (rank-deficient normal equations held by lambda), d = 8 (TP_MAXD).  (A Q = 1
+    mode with r > 1 makes the normal equations rank-deficient up to lambda: the fit is
+    then conditioned ~1/lambda and differs from the oracle at that level.)"""
+    rng = np.random.default_rng(len(qs) * 10 + R + r)
+    V = rand_factors(rng, qs, R, 0.5)
+    init = [rng.standard_normal((q, r)) * 0.3 for q in qs]
+    out, ref, trace, otrace = _als_case(V, init, 6, 1e-6)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+    # residual trace by the Gram identity: absolute floor ~sqrt(eps) ||V|| (SURVEY 8(d))
+    np.testing.assert_allclose(trace, otrace, rtol=1e-7, atol=1e-8 * max(1.0, float(np.sqrt(sum(
+        np.sum(v * v) for v in V)))))
+
+
+def test_als_rejects_bad_shapes():
+    rng = np.random.default_rng(0)
+    S = specs_for((4, 5))
+    T = cp.CPTensor(S, rand_factors(rng, (4, 5), 6, 0.5))
+    with pytest.raises(ValueError, match="init shape"):
+        cp.cp_approx_als(T, 3, cp.ALSApproxConfig(max_sweeps=2), init=cp.CPTensor(S, rand_factors(rng, (4, 5), 2, 1.0)))
+    with pytest.raises(ValueError):
+        cp.cp_approx_als(T, 40, cp.ALSApproxConfig(max_sweeps=2))   # r > 32: outside the fused kernels
