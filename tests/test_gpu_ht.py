@@ -167,12 +167,13 @@ def test_frame_factor_paths(chol):
         L.tp_debug_set_ht_chol(1)
 
 
-@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("impl", [0, 1, 2])
 @pytest.mark.parametrize("chol", [0, 1])
 @pytest.mark.parametrize("d,q,k,rmax,eps", [(4, 9, 7, 3, 0.0), (5, 20, 13, 6, 1e-3), (8, 70, 64, 16, 0.0)])
 def test_jacobi_kernels(impl, chol, d, q, k, rmax, eps):
-    """Both Jacobi eigensolvers (three-barrier and double-buffered one-barrier rounds),
-    with and without the Cholesky frame factor, odd and maximal k, against the oracle."""
+    """The three Jacobi eigensolvers (three-barrier rows/columns, double-buffered blocks,
+    upper-triangle blocks = default), with and without the Cholesky frame factor, odd and
+    maximal k, against the oracle."""
     import ctypes
     from paper_1803_10270_b200 import _lib
     L = _lib.lib()
@@ -190,7 +191,7 @@ def test_jacobi_kernels(impl, chol, d, q, k, rmax, eps):
         assert red.ranks == tuple(int(x) for x in ref_ranks(ref))
     finally:
         L.tp_debug_set_ht_chol(1)
-        L.tp_debug_set_jacobi_impl(1)
+        L.tp_debug_set_jacobi_impl(2)
 
 
 def ref_ranks(o):
