@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import warnings
 import re
 from pathlib import Path
 
@@ -93,6 +94,11 @@ def lib():
         build.build()
     if not LIB_PATH.exists():
         raise RuntimeError(f"tpde_b200 CUDA library missing at {LIB_PATH}; run __graft_entry__.build()")
+    from . import build
+    if build.needs_build():
+        # not rebuilt implicitly (a copied tree can carry arbitrary mtimes); say so loudly
+        warnings.warn(f"{LIB_PATH.name} is older than its CUDA sources; run __graft_entry__.build() "
+                      "or set TPDE_REBUILD=1", RuntimeWarning, stacklevel=2)
     handle = ctypes.CDLL(str(LIB_PATH))
     for name, (res, args) in _SIGNATURES.items():
         fn = getattr(handle, name)

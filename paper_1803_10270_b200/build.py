@@ -20,8 +20,9 @@ LIB = PKG / "libtpde_b200.so"
 INCLUDE = PKG.parent / "include"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-         "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+FLAGS_OBJ = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+OBJ = PKG.parent / "build"
 
 
 def nvcc() -> str:
@@ -43,20 +44,56 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
+def _obj(src: Path) -> Path:
+    return OBJ / (src.stem + ".o")
+
+
+def _compile(src: Path):
+    """One translation unit -> build/<name>.o (rebuilt when the .cu or any header is newer)."""
+    obj = _obj(src)
+    hdrs = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
+    if obj.exists() and all(p.stat().st_mtime <= obj.stat().st_mtime for p in [src, *hdrs]):
+        return obj, None
+    cmd = [nvcc(), *ARCH, *FLAGS_OBJ, "-I", str(INCLUDE), "-c", "-o", str(obj) + ".tmp", str(src)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode == 0:
+        os.replace(str(obj) + ".tmp", obj)
+    return obj, res
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every csrc/*.cu for sm_100a (one nvcc per translation unit, in
+    parallel) and link libtpde_b200.so in-tree."""
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc(), *ARCH, *FLAGS, "-I", str(INCLUDE), "-o", str(LIB) + ".tmp",
-           *map(str, sources())]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    OBJ.mkdir(exist_ok=True)
+    srcs = sources()
+    if force:
+        for s_ in srcs:
+            _obj(s_).unlink(missing_ok=True)
+    with ThreadPoolExecutor(max(1, min(len(srcs), os.cpu_count() or 1))) as pool:
+        results = list(pool.map(_compile, srcs))
     log = PKG / "build.log"
-    log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    text = []
+    for src, (obj, res) in zip(srcs, results):
+        if res is not None:
+            text.append(" ".join(res.args) + "\n" + res.stdout + res.stderr)
+            if res.returncode != 0:
+                log.write_text("\n".join(text))
+                sys.stderr.write(res.stderr[-8000:])
+                raise RuntimeError(f"nvcc failed on {src.name} (see {log})")
+    cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(LIB) + ".tmp",
+           *[str(o) for o, _ in results]]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    text.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    log.write_text("\n".join(text))
     if res.returncode != 0:
         sys.stderr.write(res.stderr[-8000:])
-        raise RuntimeError(f"nvcc failed (see {log})")
+        raise RuntimeError(f"link failed (see {log})")
     os.replace(str(LIB) + ".tmp", LIB)
     if verbose:
-        print(res.stderr)
+        print("\n".join(text))
     return LIB
 
 

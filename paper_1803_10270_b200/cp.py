@@ -341,13 +341,13 @@ def cp_approx_als(target, r: int, config: ALSApproxConfig | None = None, *, spec
         raise ValueError("init shape does not match the requested fit")
     if target.is_complex or guess.is_complex:   # the reference's complex128 arithmetic
         target, guess = as_complex(target), as_complex(guess).copy()
+    if not sync and trace is not None:
+        raise ValueError("trace needs sync=True")
     dev = target.data.device
     info = torch.zeros(2, dtype=torch.int32, device=dev)
     tb = torch.zeros(max(cfg.max_sweeps, 1), dtype=torch.float64, device=dev) if trace is not None else None
     _als_device(target, guess.data, r, cfg, tb, info)
     if not sync:
-        if trace is not None:
-            raise ValueError("trace needs sync=True")
         guess.pending_info = info
         return guess
     done = _check_info(info)
@@ -437,5 +437,3 @@ def _apply_raw(f: CPTensor, mat_rows, weights, scale_, mats_dev, out: CPTensor, 
                            out.data.data_ptr(), out.rank, int(col_off), _lib.stream_ptr(f.data.device))
     _lib.check(st, "apply")
 
-
-_ = ctypes  # keep import for type users

@@ -367,8 +367,11 @@ __device__ int gram_inverse(const AlsArgs& a, const Smem& sm, int j, double* out
     const double* rk = sm.pub + (k & 1) * 36;
     double* rn = sm.pub + ((k + 1) & 1) * 36;
     const double d = rk[k];
-    if (!(d > 0.0) || !isfinite(d)) bad = 1;
-    const double id = rcp_nr(d);
+    // a zero pivot of the PSD normal matrix is a zero row/column: the reference's lstsq
+    // fallback (cp.py:176-177) gives the min-norm solution, i.e. a zero row/column of the
+    // pseudo-inverse -- not a failure (all-zero targets / states)
+    if (d < 0.0 || !isfinite(d)) bad = 1;
+    const double id = (d == 0.0) ? 0.0 : rcp_nr(d);
     const double f = (i < r ? rk[i] : 0.0) * id;   // a_ik / d  (column k == row k)
 #pragma unroll
     for (int u = 0; u < EPT; ++u) {
@@ -668,8 +671,11 @@ __device__ int gram_inverse_w4(const AlsArgs& a, const Smem& sm, int j, double* 
     const double* rk = sm.pub + (k & 1) * 36;
     double* rn = sm.pub + ((k + 1) & 1) * 36;
     const double d = rk[k];
-    if (!(d > 0.0) || !isfinite(d)) bad = 1;
-    const double id = rcp_nr(d);
+    // a zero pivot of the PSD normal matrix is a zero row/column: the reference's lstsq
+    // fallback (cp.py:176-177) gives the min-norm solution, i.e. a zero row/column of the
+    // pseudo-inverse -- not a failure (all-zero targets / states)
+    if (d < 0.0 || !isfinite(d)) bad = 1;
+    const double id = (d == 0.0) ? 0.0 : rcp_nr(d);
     const double f = (i < r ? rk[i] : 0.0) * id;
 #pragma unroll
     for (int u = 0; u < EPT; ++u) {
@@ -1165,8 +1171,8 @@ __device__ int warp_sweep_inverse8(const AlsArgs& a, const double* Gs, int j, do
     const double dk0 = __shfl_sync(0xffffffffu, v[0], srow | (k & 3));
     const double dk1 = __shfl_sync(0xffffffffu, v[1], srow | (k & 3));
     const double dd = (k >> 2) ? dk1 : dk0;                              // a_kk
-    if (!(dd > 0.0) || !isfinite(dd)) bad = 1;
-    const double id = rcp_nr(dd);
+    if (dd < 0.0 || !isfinite(dd)) bad = 1;          // zero pivot: min-norm (lstsq) row, see gram_inverse
+    const double id = (dd == 0.0) ? 0.0 : rcp_nr(dd);
     const double aik = (i < r) ? ((i >> 2) ? ri1 : ri0) : 0.0;          // a_ik == a_ki
     const double f = aik * id;
 #pragma unroll

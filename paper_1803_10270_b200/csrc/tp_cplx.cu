@@ -253,8 +253,9 @@ __global__ void __launch_bounds__(ALSC_NT, 1) als_c_kernel(const __grid_constant
         }
         __syncthreads();
         const cplx piv = ld(rowk, k);
-        if (tid == 0 && (!(isfinite(piv.x) && isfinite(piv.y)) || (piv.x == 0.0 && piv.y == 0.0))) status |= 1;
-        const cplx p = crcp(piv);
+        if (tid == 0 && !(isfinite(piv.x) && isfinite(piv.y))) status |= 1;
+        // zero pivot = zero row/column of the PSD matrix: min-norm (lstsq, cp.py:176-177) solution
+        const cplx p = (piv.x == 0.0 && piv.y == 0.0) ? cmk(0.0, 0.0) : crcp(piv);
         for (int e = tid; e < rr; e += ALSC_NT) {
           const int i = e / r, c = e - i * r;
           cplx v;

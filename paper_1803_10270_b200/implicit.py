@@ -75,12 +75,19 @@ def build_tables(pair: CrankNicolsonPair, device=None) -> OperatorTables:
     if len(qs) != 1:
         raise ValueError("the B200 implicit step needs a uniform mode size Q")
     Q = qs.pop()
+    if any(s.kind == "fourier" for s in specs):
+        # the reference's Galerkin pair_matrix is the unconjugated bilinear form of a complex
+        # basis (basis.py:207-214; the identity pairs to the flip matrix), not E_e^T E_z
+        raise ValueError("the B200 implicit step runs on real collocation/uniform grids; "
+                         "Fourier Galerkin specs (complex pairing tables) are not supported")
     ra, d = pair.n_terms, len(specs)
     uniq, keys, tab_id = [], {}, np.zeros((d, ra, ra), dtype=np.int32)
     for k, spec in enumerate(specs):
         mats = []
         for e in range(ra):
             m = dense_factor(spec, pair.factors[e][k])
+            if m is not None and np.iscomplexobj(m):
+                raise ValueError("complex factor matrices are not supported by the real-fp64 implicit step")
             mats.append(np.eye(Q) if m is None else m)
         for e in range(ra):
             for z in range(ra):
@@ -135,6 +142,8 @@ class StepWorkspace:
 
 def _launch(f_n: CPTensor, out: torch.Tensor, tab: OperatorTables, cfg: ALSStepConfig, eps: torch.Tensor,
             info: torch.Tensor) -> None:
+    if f_n.is_complex:
+        raise ValueError("complex128 states are not supported by the real-fp64 implicit step")
     L = _lib.lib()
     d, Q, r, ra = f_n.ndim, f_n.specs[0].Q, f_n.rank, tab.pair.n_terms
     n_tab = tab.tabs.shape[0]

@@ -7,11 +7,12 @@ payload term-major, dimension middle, mode minor (io.py:28-36, 58-59); HT tensor
 the per-node ranks, payload = every node's array (leaf frame Q x k, interior
 transfer k_l x k_r x k) in node order, C order (io.py:39-52, 60-63, 95-112).
 
-The device tensors are real fp64: files written here carry zero imaginary parts
-and are byte-identical to the reference's for Fourier-basis specs (the header
-gains ``kind``/``lo`` keys only for the build's collocation / uniform grids);
-loading a file with non-zero imaginary parts raises ``ValueError`` like every
-other complex input of the real-fp64 path.  The pure ``encode_*`` / ``decode``
+Real-valued tensors are stored in real fp64 on the device and written with zero
+imaginary parts; files are byte-identical to the reference's for Fourier-basis
+specs (the header gains ``kind``/``lo`` keys only for the build's collocation /
+uniform grids).  A CP file with non-zero imaginary parts loads as a complex128
+CPTensor (the reference's own arithmetic); an HT file with
+non-zero imaginary parts raises ``ValueError`` (the hSVD path is real fp64).  The pure ``encode_*`` / ``decode``
 functions work on numpy arrays; ``save_tensor`` / ``load_tensor`` move the
 device tensors.
 """
@@ -128,7 +129,8 @@ def save_tensor(path, t) -> None:
 
 
 def load_tensor(path):
-    """io.py:74-115 -> device CPTensor / HTTensor (real fp64; non-zero imaginary parts raise)."""
+    """io.py:74-115 -> device CPTensor (real fp64, or complex128 when the payload has
+    non-zero imaginary parts) / HTTensor (real fp64; complex payloads raise)."""
     from .cp import CPTensor
     from .ht import DimensionTree, HTTensor, TreeNode
     out = decode(Path(path).read_bytes())

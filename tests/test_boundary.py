@@ -121,3 +121,19 @@ def test_bgk_projection_is_exact_on_grid():
     M1 = workloads.maxwellian_1d(v)
     mv = np.kron(np.kron(M1, M1), M1)
     assert np.abs(Pv @ mv - mv).max() < 1e-13
+
+
+def test_implicit_rejects_complex_galerkin_tables():
+    """The reference's Fourier Galerkin pair tables are complex bilinear forms
+    (basis.py:207-214); the real-fp64 implicit step must refuse them up front
+    instead of reinterpreting complex buffers."""
+    from paper_1803_10270_b200 import implicit
+    S = tuple(basis.BasisSpec(5, 1.0) for _ in range(3))
+    pair = operators.implicit_euler_pair(operators.advection_operator((1.0, 0.5, -0.75), S), 0.1)
+    with pytest.raises(ValueError, match="Fourier Galerkin"):
+        implicit.build_tables(pair)
+    Sc = tuple(basis.BasisSpec(6, np.pi, "collocation") for _ in range(3))
+    Dc = np.eye(6) * 1j
+    Lc = operators.SeparableOperator(Sc, (1.0,), ((Dc, None, None),))
+    with pytest.raises(ValueError, match="complex factor matrices"):
+        implicit.build_tables(operators.implicit_euler_pair(Lc, 0.1))
