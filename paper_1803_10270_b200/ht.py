@@ -20,7 +20,7 @@ from . import _lib
 from .cp import CPTensor
 
 __all__ = ["TreeNode", "DimensionTree", "balanced_tree", "HTTensor", "from_cp", "add", "scale",
-           "inner_product", "norm", "truncate", "truncate_batch", "apply_operator"]
+           "inner_product", "norm", "truncate", "truncate_batch", "apply_operator", "HTBatch", "truncate_packed"]
 
 
 @dataclass(frozen=True)
@@ -305,6 +305,96 @@ def truncate_batch(hs, r_max: int, eps: float):
                 transfers[i] = OB[b, s, :rk[node.left], :rk[node.right], :rk[i]].clone()
         outs.append(HTTensor(h.specs, tree, frames, transfers))
     return outs, [float(x) for x in est_h]
+
+
+class HTBatch:
+    """B200 extension of the reference API: ``nb`` HT tensors on one balanced tree,
+    held in the packed device layout of ``tp_ht_truncate_f64`` -- frames
+    ``(nb, n_leaves, Q, k)`` (leaves in tree order) and transfers
+    ``(nb, n_int, k, k, k)`` (interior nodes in tree order, the root's ``k x k x 1``
+    in the first ``k*k`` entries of its slot).  ``truncate_packed`` works on it with
+    no per-node copies; ``unpack()`` gives the reference-style HTTensor list."""
+
+    def __init__(self, specs, frames: torch.Tensor, transfers: torch.Tensor, ranks=None):
+        self.specs = tuple(specs)
+        self.tree = balanced_tree(len(self.specs))
+        n_leaf = sum(1 for n in self.tree.nodes if n.is_leaf)
+        if frames.dim() != 4 or frames.shape[1] != n_leaf or transfers.dim() != 5 \
+                or transfers.shape[1] != len(self.tree.nodes) - n_leaf or transfers.shape[0] != frames.shape[0]:
+            raise ValueError("packed HT batch layout mismatch")
+        if frames.dtype != torch.float64 or transfers.dtype != torch.float64:
+            raise ValueError("packed HT batch must be float64")
+        if any(s.Q != frames.shape[2] for s in self.specs):
+            raise ValueError("packed HT batch needs a uniform mode size Q")
+        self.frames, self.transfers = frames, transfers
+        k = frames.shape[3]
+        self.ranks = ranks if ranks is not None else torch.tensor(
+            [[1] + [k] * (len(self.tree.nodes) - 1)] * frames.shape[0], dtype=torch.int32)
+
+    @property
+    def nb(self) -> int:
+        return self.frames.shape[0]
+
+    @classmethod
+    def from_arrays(cls, specs, frames, transfers, non_blocking: bool = False) -> "HTBatch":
+        """Upload host arrays (numpy or pinned torch tensors) in two copies."""
+        dev = _lib.device()
+        f = torch.as_tensor(frames).to(dev, torch.float64, non_blocking=non_blocking)
+        t = torch.as_tensor(transfers).to(dev, torch.float64, non_blocking=non_blocking)
+        return cls(specs, f, t)
+
+    def unpack(self) -> list:
+        tree = self.tree
+        leaves = [i for i, n in enumerate(tree.nodes) if n.is_leaf]
+        ints = [i for i, n in enumerate(tree.nodes) if not n.is_leaf]
+        rk_all = self.ranks.cpu().numpy() if isinstance(self.ranks, torch.Tensor) else np.asarray(self.ranks)
+        kk = self.transfers.shape[2]
+        outs = []
+        for b in range(self.nb):
+            rk = rk_all[b]
+            frames = [None] * len(tree.nodes)
+            transfers = [None] * len(tree.nodes)
+            for s, i in enumerate(leaves):
+                frames[i] = self.frames[b, s, :, :rk[i]].clone()
+            for s, i in enumerate(ints):
+                node = tree.nodes[i]
+                if i == 0:
+                    blk = self.transfers[b, s].reshape(-1)[:kk * kk].view(kk, kk)
+                    transfers[i] = blk[:rk[node.left], :rk[node.right]].unsqueeze(2).clone()
+                else:
+                    transfers[i] = self.transfers[b, s, :rk[node.left], :rk[node.right], :rk[i]].clone()
+            outs.append(HTTensor(self.specs, tree, frames, transfers))
+        return outs
+
+
+def truncate_packed(batch: HTBatch, r_max: int, eps: float, out: HTBatch | None = None):
+    """hSVD truncation (ht.py:313-372) of a packed batch in one stream-ordered call.
+    Returns (HTBatch with ranks <= r_max, zero-padded to min(r_max, k); device tensor
+    of error estimates).  No host synchronisation; ``out`` may be reused."""
+    if r_max < 1:
+        raise ValueError("rank cap must be at least 1")
+    d, nb = len(batch.specs), batch.nb
+    Q, k = batch.frames.shape[2], batch.frames.shape[3]
+    ro = min(r_max, k)
+    dev = batch.frames.device
+    n_nodes = len(batch.tree.nodes)
+    if out is None:
+        OF = torch.zeros((nb, d, Q, ro), dtype=torch.float64, device=dev)
+        OB = torch.zeros((nb, d - 1, ro, ro, ro), dtype=torch.float64, device=dev)
+        out = HTBatch(batch.specs, OF, OB, torch.zeros((nb, n_nodes), dtype=torch.int32, device=dev))
+        out.est = torch.zeros(nb, dtype=torch.float64, device=dev)
+        out.norms = torch.zeros(nb, dtype=torch.float64, device=dev)
+    L = _lib.lib()
+    nbytes = L.tp_ht_truncate_ws_bytes(d, Q, k, nb)
+    if nbytes == 0:
+        raise ValueError(f"unsupported hSVD size d={d}, Q={Q}, k={k}")
+    ws = _lib.WORKSPACE.get(nbytes, dev)
+    st = L.tp_ht_truncate_f64(d, Q, k, nb, batch.frames.data_ptr(), batch.transfers.data_ptr(), int(r_max),
+                              float(eps), out.frames.data_ptr(), out.transfers.data_ptr(), out.ranks.data_ptr(),
+                              out.est.data_ptr(), out.norms.data_ptr(), ws.data_ptr(), ws.numel(),
+                              _lib.stream_ptr(dev))
+    _lib.check(st, "truncate")
+    return out, out.est
 
 
 def truncate(h: HTTensor, r_max: int, eps: float):

@@ -151,14 +151,56 @@ class ShardedALS:
         self.graph.replay()
 
 
+class GraphShardedALS:
+    """R-sharded truncation driver: the per-mode-update kernels plus the all-reduce of
+    ShardedALS, captured once as a CUDA graph and replayed per truncation."""
+
+    def __init__(self, V_local: CPTensor, r: int, config: ALSApproxConfig | None = None, group=None):
+        dist = torch.distributed.is_available() and torch.distributed.is_initialized()
+        self.world = torch.distributed.get_world_size(group) if dist else 1
+        self.comm = TorchDistComm(group) if dist else LocalComm()
+        self.ops = DeviceShardOps(V_local, r)
+        self.drv = ShardedALS(self.ops, self.comm, config)
+        self.d = V_local.ndim
+
+    def prepare(self, U: torch.Tensor):
+        self.U = U
+        self.drv.capture(U, self.d)
+
+    def run(self, U: torch.Tensor):
+        if U.data_ptr() != self.U.data_ptr():
+            raise ValueError("run() needs the buffer prepare() captured")
+        self.drv.replay()
+
+    def check(self):
+        self.ops.check()
+
+    def describe(self) -> str:
+        return "per mode update: shard rhs kernel, NCCL all-reduce of the r x Q block, replicated update; " \
+               "one CUDA graph per truncation"
+
+    def kernel_name(self) -> str:
+        return "tp_als_shard_* mode steps + NCCL all-reduce (per GPU)"
+
+    def launches_per_truncation(self) -> int:
+        return self.drv.cfg.max_sweeps * self.d * 6 + 2 * self.d
+
+
+def make_sharded_als(V_local: CPTensor, r: int, config: ALSApproxConfig | None = None, group=None):
+    """The R-sharded truncation driver for this process group."""
+    return GraphShardedALS(V_local, r, config, group)
+
+
 def sharded_cp_approx_als(V_local: CPTensor, init: CPTensor, config: ALSApproxConfig | None = None,
-                          group=None) -> CPTensor:
+                          group=None, check: bool = True) -> CPTensor:
     """R-sharded ``cp_approx_als``: every rank passes its slab of the target and the
-    same initial guess; every rank gets the full fit."""
+    same initial guess; every rank gets the full fit.  ``check=False`` defers the
+    status read (no host round trip)."""
     comm = TorchDistComm(group) if (torch.distributed.is_available() and torch.distributed.is_initialized()) \
         else LocalComm()
     ops = DeviceShardOps(V_local, init.rank)
     out = init.copy()
     ShardedALS(ops, comm, config).run(out.data, init.ndim)
-    ops.check()
+    if check:
+        ops.check()
     return out

@@ -197,3 +197,36 @@ def test_jacobi_kernels(impl, chol, d, q, k, rmax, eps):
 def ref_ranks(o):
     nodes, frames, transfers = o
     return [frames[i].shape[1] if oht.is_leaf(nd) else transfers[i].shape[2] for i, nd in enumerate(nodes)]
+
+
+def test_packed_batch_api_matches_list_api():
+    """ht.HTBatch / truncate_packed (packed device layout, no per-node copies) gives the
+    same tensors and estimates as truncate_batch on HTTensor lists, bitwise."""
+    import torch
+    rng = np.random.default_rng(31)
+    d, q, k, nb = 8, 24, 10, 5
+    os_ = [random_ht(rng, d, q, k) for _ in range(nb)]
+    hs = [to_dev(d, q, o) for o in os_]
+    outs, ests = ht.truncate_batch(hs, 4, 0.0)
+    nodes = oht.balanced_tree(d)
+    leaves = [i for i, nd in enumerate(nodes) if oht.is_leaf(nd)]
+    ints = [i for i, nd in enumerate(nodes) if not oht.is_leaf(nd)]
+    F = np.stack([np.stack([o[1][i] for i in leaves]) for o in os_])
+    B = np.zeros((nb, len(ints), k, k, k))
+    for b, o in enumerate(os_):
+        for s, i in enumerate(ints):
+            t = o[2][i]
+            if i == 0:
+                B[b, s].reshape(-1)[:k * k] = t[:, :, 0].reshape(-1)
+            else:
+                B[b, s] = t
+    batch = ht.HTBatch.from_arrays(specs(d, q), F, B)
+    pk, est = ht.truncate_packed(batch, 4, 0.0)
+    for b, h in enumerate(pk.unpack()):
+        assert abs(float(est[b]) - ests[b]) == 0.0
+        for u, v in zip(h.frames, outs[b].frames):
+            assert (u is None and v is None) or torch.equal(u, v)
+        for u, v in zip(h.transfers, outs[b].transfers):
+            assert (u is None and v is None) or torch.equal(u, v)
+        ref, oest = oht.truncate(os_[b], 4, 0.0)
+        assert metrics.ht_rel_diff(ref, h.to_oracle()) <= TOL
