@@ -208,6 +208,41 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
                          int orientation, const double* circ_eig, double* eps_conv, int* info, void* ws,
                          size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * R-sharded fused CP-ALS across GPUs (BASELINE cfg1 multi-GPU, SURVEY 8(e);
+ * the per-mode update of cp.py:310-320 with the target's R terms split over
+ * `ngpu` ranks).  ONE launch per GPU runs every sweep: each rank forms its
+ * R-slab's right-hand-side partials, all ranks exchange them through mapped
+ * peer memory (CUDA IPC over NVLink/NVSwitch) after an in-kernel cross-GPU
+ * barrier, and every rank reduces them in the same fixed order (rank-major,
+ * then cluster), so the replicated fit U is bitwise identical on all ranks.
+ * Fixed sweep count (tol = 0, stall = -inf semantics, no trace).
+ *   ngroups : groups of CTAs in THIS launch (1 on a real rank; > 1 runs several
+ *             ranks' groups co-resident in one launch -- the single-GPU test of
+ *             the exchange path); group g is rank rank0 + g
+ *   V, U, info, ws : per-group arrays (device pointers): slab (rank R_local,
+ *             CP layout), replicated guess/fit (rank r), int[2] status
+ *             {bits: 1 not PD, 2 non-finite, 4 peer timeout; sweeps}, workspace
+ *   peer    : ngpu device pointers, rank h's exchange buffer as mapped in this
+ *             process (tp_als_xg_peer_bytes each, zeroed once at allocation)
+ *   seq     : call sequence number >= 1, identical on all ranks, increasing
+ * ------------------------------------------------------------------------- */
+size_t tp_als_xg_ws_bytes(int d, const int* q, int R_local, int r, int ngpu, int ngroups);
+size_t tp_als_xg_peer_bytes(int d, const int* q, int R_local, int r, int ngpu, int ngroups);
+/* out[0] CTAs per rank, out[1] CTAs per cluster, out[2] clusters per rank, out[3] shared bytes */
+int tp_als_xg_plan(int d, const int* q, int R_local, int r, int ngpu, int ngroups, int* out);
+int tp_als_xg_f64(int d, const int* q, int R_local, int r, int sweeps, double reg, int reg_mode,
+                  int ngroups, const double* const* V, double* const* U, int* const* info,
+                  void* const* ws, size_t ws_bytes, int ngpu, int rank0, void* const* peer,
+                  long long seq, void* stream);
+/* device memory shared between ranks: cudaMalloc'd and zeroed, exported/imported
+ * as 64-byte CUDA IPC handles (exchanged by the caller, e.g. all_gather_object) */
+int tp_dev_alloc(size_t bytes, void** ptr);
+int tp_dev_free(void* ptr);
+int tp_ipc_handle(void* ptr, void* handle);
+int tp_ipc_open(const void* handle, void** ptr);
+int tp_ipc_close(void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

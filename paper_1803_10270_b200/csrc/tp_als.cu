@@ -486,16 +486,17 @@ __device__ __forceinline__ double2 mv_dot_abs(const double* M, int ld, const dou
 // symmetric-sweep inverse, whose owned rows are stored directly.
 template <int RM>
 __device__ bool solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, int E, int& status,
-                           unsigned int& ns_fail) {
+                           unsigned int& ns_fail, double* xprev = nullptr, int P = 0, int p = 0) {
   constexpr int TPO = RM / 8;
-  const int r = a.r, rh = pad4(r), P = gridDim.x, p = blockIdx.x, tid = threadIdx.x;
+  if (!xprev) { xprev = a.Xprev; P = gridDim.x; p = blockIdx.x; }   // (R-sharded kernel: its group's)
+  const int r = a.r, rh = pad4(r), tid = threadIdx.x;
   const int nv = a.ncolmax * r;
   double* zb = sm.vb;
   double* yb = sm.vb + nv;
   double* ub = sm.vb + 2 * nv;
   // warm starts are double-buffered by sweep parity: this sweep reads buffer
   // (sweep & 1) and writes the other, so results do not depend on CTA timing
-  double* Xn = a.Xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;
+  double* Xn = xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;
   bool ok = false;
   // after a failed Newton-Schulz check (ill-conditioned normal equations) this CTA
   // goes straight to the exact inverse for that mode in the next sweep, then
@@ -564,10 +565,12 @@ __device__ bool solve_mode(const AlsArgs& a, const Smem& sm, int j, int sweep, i
 // the mode solved last (A and X0 still in shared memory), phase A of the next
 // mode update (off the solve's critical path; the top CTAs own no Gram tiles).
 template <int RM>
-__device__ void ns_rows(const AlsArgs& a, const Smem& sm, int j, int sweep) {
+__device__ void ns_rows(const AlsArgs& a, const Smem& sm, int j, int sweep, double* xprev = nullptr, int P = 0,
+                        int p = 0) {
   constexpr int TPO = RM / 8;
-  const int r = a.r, rh = pad4(r), P = gridDim.x, p = blockIdx.x, tid = threadIdx.x;
-  double* Xn = a.Xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;
+  if (!xprev) { xprev = a.Xprev; P = gridDim.x; p = blockIdx.x; }
+  const int r = a.r, rh = pad4(r), tid = threadIdx.x;
+  double* Xn = xprev + ((size_t)((sweep + 1) & 1) * a.d + j) * r * rh;
   const int i_first = P - 1 - p;
   if (i_first >= r) return;
   const int nrows = (r - 1 - i_first) / P + 1;     // rows i_first, i_first + P, ...
@@ -1652,8 +1655,10 @@ __device__ inline Smem carve_cl(double* base, const AlsArgs& a, int Pr) {
 // U_k rows [qb0, qb0 + nb) -> sm.Us (row stride pad4(r)): bulk copy of the padded
 // copy, or plain loads from the user's U for the initial guess.  Rows
 // [nb, ceil4(nb)) are zeroed (K padding of the unpredicated DMMA loads).
-__device__ void cl_stage_u(const AlsArgs& a, const Smem& sm, int k, int qb0, int nb, uint32_t& phase, bool from_user) {
+__device__ void cl_stage_u(const AlsArgs& a, const Smem& sm, int k, int qb0, int nb, uint32_t& phase, bool from_user,
+                           const double* Uu = nullptr, const double* Upd = nullptr) {
   const int r = a.r, rh = pad4(r);
+  if (!Uu) { Uu = a.U; Upd = a.Upad; }
   __syncthreads();
   if (nb > 0) {
     if (!from_user) {
@@ -1661,12 +1666,12 @@ __device__ void cl_stage_u(const AlsArgs& a, const Smem& sm, int k, int qb0, int
         const uint32_t bytes = (uint32_t)(nb * rh) * 8u;
         fence_proxy_async();
         mbar_arrive_expect_tx(sm.bar, bytes);
-        bulk_g2s(sm.Us, a.Upad + a.offUp[k] + (size_t)qb0 * rh, bytes, sm.bar);
+        bulk_g2s(sm.Us, Upd + a.offUp[k] + (size_t)qb0 * rh, bytes, sm.bar);
       }
       mbar_wait(sm.bar, phase);
       phase ^= 1u;
     } else {
-      const double* Uk = a.U + a.offU[k] + (size_t)qb0 * r;
+      const double* Uk = Uu + a.offU[k] + (size_t)qb0 * r;
       for (int e = threadIdx.x; e < nb * r; e += ALS_NT) sm.Us[(e / r) * rh + e % r] = __ldcg(Uk + e);
     }
   }
@@ -1776,7 +1781,8 @@ __device__ void cl_partials(const AlsArgs& a, const Smem& sm, int k, int w, int 
 // barrier is needed.
 template <int RM>
 __device__ void cl_exchange(const AlsArgs& a, const Smem& sm, cg::cluster_group& cl, int k, int w, int cid, int Pr,
-                            uint32_t& ph, int& rows_mode, int rows_sweep) {
+                            uint32_t& ph, int& rows_mode, int rows_sweep, double* Gg = nullptr,
+                            double* xprev = nullptr, int Pg = 0, int pg = 0) {
   const int r = a.r, rr = r * r, Pq = a.Pq, stride = a.chunk, b = (int)cl.block_rank(), tid = threadIdx.x;
   const int mtr = (r + 7) / 8, nG = mtr * (mtr + 1) / 2, nGi = cid < nG ? (nG - 1 - cid) / Pr + 1 : 0;
   const int rw = r * w, L = rw + nGi * 64, L2 = (L + 1) & ~1;   // even: 16-byte bulk sizes
@@ -1793,12 +1799,12 @@ __device__ void cl_exchange(const AlsArgs& a, const Smem& sm, cg::cluster_group&
       }
   }
   if (rows_mode >= 0) {   // warm-start rows of the previous solve, while the peers' partials land
-    ns_rows<RM>(a, sm, rows_mode, rows_sweep);
+    ns_rows<RM>(a, sm, rows_mode, rows_sweep, xprev, Pg, pg);
     rows_mode = -1;
   }
   mbar_wait(sm.bar + 2, ph);
   ph ^= 1u;
-  double* Gk = a.G + (size_t)k * rr;
+  double* Gk = (Gg ? Gg : a.G) + (size_t)k * rr;
   for (int idx = tid; idx < L; idx += ALS_NT) {
     double v = 0.0;
     for (int src = 0; src < Pq; ++src)
@@ -1823,7 +1829,8 @@ __device__ void cl_exchange(const AlsArgs& a, const Smem& sm, cg::cluster_group&
 // YT[pc][cluster][row-in-pc][:] for phase B.  Shared loads use 32-bit
 // addresses and no predicates (zero padding rows/columns, discarded lanes).
 template <int RM>
-__device__ void cl_had_y(const AlsArgs& a, const Smem& sm, int j, int w, int b, int cid, int Pr) {
+__device__ void cl_had_y(const AlsArgs& a, const Smem& sm, int j, int w, int b, int cid, int Pr, double* Yg = nullptr) {
+  if (!Yg) Yg = a.Y;
   constexpr int NT = RM / 8;
   const int r = a.r, rh = pad4(r), ldw = a.ldw, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t cs32 = smem_u32(sm.Cs), ks = 8u * (uint32_t)(r * a.wmax);   // Cs[k]: r x w, stride w
@@ -1861,7 +1868,7 @@ __device__ void cl_had_y(const AlsArgs& a, const Smem& sm, int j, int w, int b, 
     if (s < nb) {
       const int rm = sm.rowmap[j * a.qmax + qb0 + s];
       const int pc = rm >> 16, ii = rm & 0xffff;
-      double* yrow = a.Y + (((size_t)pc * Pr + cid) * a.ncolmax + ii) * r;
+      double* yrow = Yg + (((size_t)pc * Pr + cid) * a.ncolmax + ii) * r;
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         const int ocol = n * 8 + 2 * (lane & 3);
@@ -2090,6 +2097,265 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
     if (prof_sink == 12345.0) a.prof[11] += 1;
   }
   cl.sync();   // no CTA may exit while peers can still address its shared memory
+}
+
+// ===========================================================================
+// R-sharded truncation across GPUs in ONE launch per GPU: the
+// cluster kernel above, with the target's R terms split over `ngpu` ranks.
+// Rank g holds its R-slab V_g (Pr clusters x Pq CTAs over it) and a replicated
+// copy of U, G and the warm starts.  Per mode update the only exchange is the
+// right-hand-side reduction: every rank's producers write their partials Y into
+// an exchange buffer that every peer maps (CUDA IPC over NVLink / NVSwitch);
+// after a cross-GPU barrier, consumer CTA p of EVERY rank bulk-copies its rows'
+// slices from all ranks' buffers (rank-major, then cluster -- the cluster
+// order of the single-GPU kernel), so every rank forms the identical U_j and
+// the second barrier of the mode update stays GPU-local.  Y is double-buffered
+// by mode-update parity: a rank can run one mode update ahead of a peer that is
+// still reading.
+//
+// The cross-GPU barrier: a GPU-local counter barrier, then the group leader
+// publishes a 64-bit tag into every rank's flag slot (st.release.sys through
+// the peer mapping), waits for all ranks' tags in its own slots
+// (ld.acquire.sys), and releases its group through a local go word.  Tags grow
+// monotonically across launches (seq << 20 | barrier index), so no flag is ever
+// reset while a peer may write it.  A 5 s spin limit turns a missing peer into
+// status bit 4 instead of a hung GPU.
+//
+// One launch may also hold several groups ("virtual ranks") of CTAs: the
+// single-GPU test of the exchange path, co-resident by the cooperative launch.
+// ===========================================================================
+
+constexpr int TP_MAXG = 8;
+
+struct XgGroup {
+  const double* V;
+  double *U, *Upad, *G, *Xprev;
+  unsigned int* bar;   // group-local grid-barrier counter (zeroed per launch)
+  int* info;
+};
+
+struct XgArgs {
+  int ngroups, ngpu, rank0, Pg;
+  unsigned long long seq_base;
+  long long yhalf;                         // doubles of one parity half of Y
+  XgGroup grp[TP_MAXG];
+  unsigned char* peer[TP_MAXG];            // every rank's exchange buffer (flags | go | Y[2])
+};
+
+constexpr int XG_HDR = 512;   // bytes: u64 flags[TP_MAXG], u64 go at [TP_MAXG]
+
+__device__ __forceinline__ unsigned long long ld_acq_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acq_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// all CTAs of all ranks (bar: this group's counter, Pg CTAs per group)
+__device__ __forceinline__ void xg_barrier(const XgArgs& x, int g, int p, unsigned int* bar, unsigned int& epoch,
+                                           int& status) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned int target = epoch * (unsigned)x.Pg;
+    const unsigned long long tag = x.seq_base + epoch;
+    const int rank = x.rank0 + g;
+    unsigned long long* myflags = reinterpret_cast<unsigned long long*>(x.peer[rank]);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+    const unsigned long long t0 = globaltimer();
+    bool late = false;
+    if (p == 0) {
+      unsigned int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+        if (globaltimer() - t0 > 5000000000ull) { late = true; break; }
+      } while ((int)(v - target) < 0);
+      __threadfence_system();
+      for (int h = 0; h < x.ngpu; ++h) {
+        unsigned long long* slot = reinterpret_cast<unsigned long long*>(x.peer[h]) + rank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(slot), "l"(tag) : "memory");
+      }
+      for (int h = 0; h < x.ngpu && !late; ++h)
+        while (ld_acq_sys_u64(myflags + h) < tag)
+          if (globaltimer() - t0 > 5000000000ull) { late = true; break; }
+      asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(myflags + TP_MAXG), "l"(tag) : "memory");
+    } else {
+      while (ld_acq_gpu_u64(myflags + TP_MAXG) < tag)
+        if (globaltimer() - t0 > 5000000000ull) { late = true; break; }
+    }
+    if (late) status |= 4;
+  }
+  __syncthreads();
+}
+
+// group-local grid barrier (Pg CTAs)
+__device__ __forceinline__ void group_barrier(unsigned int* ctr, unsigned int& epoch, int Pg) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned int target = epoch * (unsigned)Pg;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+
+template <int RM>
+__global__ void __launch_bounds__(ALS_NT, 1) als_xg(const __grid_constant__ AlsArgs a, const __grid_constant__ XgArgs x) {
+  extern __shared__ double smem[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int tid = threadIdx.x;
+  const int Pg = x.Pg, g = blockIdx.x / Pg, p = blockIdx.x - g * Pg, P = Pg;
+  const int Pq = a.Pq, b = (int)cl.block_rank(), cid = p / Pq, Pr = P / Pq;
+  const int ngpu = x.ngpu, rank = x.rank0 + g, PrT = Pr * ngpu;
+  const XgGroup& gr = x.grp[g];
+  const double* Vg = gr.V;
+  double* Ug = gr.U;
+  double* Upg = gr.Upad;
+  double* Gg = gr.G;
+  double* Xpg = gr.Xprev;
+  unsigned int* barg = gr.bar;
+  double* Ymine = reinterpret_cast<double*>(x.peer[rank] + XG_HDR);
+  const Smem sm = carve_cl(smem, a, PrT);
+  const int r = a.r, R = a.R, rr = r * r, rh = pad4(r), ldw = a.ldw;
+  const int c0 = (int)((long long)R * cid / Pr), c1 = (int)((long long)R * (cid + 1) / Pr), w = c1 - c0;
+  const int w4 = (w + 3) / 4 * 4;
+  unsigned int epoch = 0;   // arrivals on this group's counter (both barrier kinds); xg tags derive from it
+  int status = 0;
+  uint32_t bphase = 0, gphase = 0, xphase = 0, xpf = 0;
+  if (tid == 0) {
+    for (int q = 0; q < 5; ++q) mbar_init(sm.bar + q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int k = 0; k < a.d; ++k)
+    for (int s2 = tid; s2 < a.q[k]; s2 += ALS_NT) {
+      const int Qk = a.q[k];
+      const int pc = ((s2 + 1) * P + Qk - 1) / Qk - 1;
+      const int ii = s2 - (Qk * pc) / P;
+      sm.rowmap[k * a.qmax + s2] = (pc << 16) | ii;
+    }
+  for (int e = tid; e < (w4 - w) * rh; e += ALS_NT) sm.hadT[(size_t)w * rh + e] = 0.0;
+  for (int e = tid; e < a.sumqs * ldw; e += ALS_NT) sm.Vs[e] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < a.d; ++k) {
+    const int Qk = a.q[k], qb0 = Qk * b / Pq, nb = Qk * (b + 1) / Pq - qb0;
+    const double* Vk = Vg + a.offV[k] + (size_t)qb0 * R + c0;
+    double* vs = sm.Vs + a.qoffc[k];
+    for (int e = tid; e < nb * w; e += ALS_NT) {
+      const int s2 = e / w, c = e - s2 * w;
+      vs[s2 * ldw + c] = Vk[(size_t)s2 * R + c];
+    }
+  }
+  cl.sync();
+  for (int k = 0; k < a.d; ++k) {
+    const int Qk = a.q[k], qb0 = Qk * b / Pq, nb = Qk * (b + 1) / Pq - qb0;
+    cl_stage_u(a, sm, k, qb0, nb, bphase, true, Ug, Upg);
+    cl_partials<RM>(a, sm, k, w, nb, cid, Pr);
+    int none = -1;
+    cl_exchange<RM>(a, sm, cl, k, w, cid, Pr, xphase, none, 0, Gg, Xpg, P, p);
+  }
+  group_barrier(barg, epoch, Pg);
+  for (int e = tid; e < a.d * rr; e += ALS_NT) sm.Gs[e] = __ldcg(Gg + e);
+  __syncthreads();
+
+  int pending = -1, rows_mode = -1, rows_sweep = 0, upd = 0;
+  unsigned int ns_fail = 0;
+  const int nbk = a.ncolmax * r;
+  for (int sweep = 0; sweep < a.sweeps; ++sweep) {
+    for (int j = 0; j < a.d; ++j, ++upd) {
+      const int par = upd & 1;
+      // ---------------- phase A (local: this rank's R-slab)
+      if (pending >= 0) {
+        const int Qk = a.q[pending], qb0 = Qk * b / Pq, nb = Qk * (b + 1) / Pq - qb0;
+        cl_stage_u(a, sm, pending, qb0, nb, bphase, false, Ug, Upg);
+        cl_partials<RM>(a, sm, pending, w, nb, cid, Pr);
+        cl_exchange<RM>(a, sm, cl, pending, w, cid, Pr, xphase, rows_mode, rows_sweep, Gg, Xpg, P, p);
+      }
+      if (rows_mode >= 0) {
+        ns_rows<RM>(a, sm, rows_mode, rows_sweep, Xpg, P, p);
+        rows_mode = -1;
+      }
+      const bool warm_ns = sweep > 0 && a.ns_max > 0;
+      if (warm_ns && tid == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(sm.bar + 4, (uint32_t)(r * rh) * 8u);
+        bulk_g2s(sm.X0, Xpg + ((size_t)(sweep & 1) * a.d + j) * r * rh, (uint32_t)(r * rh) * 8u, sm.bar + 4);
+      }
+      const int Qj = a.q[j];
+      cl_had_y<RM>(a, sm, j, w, b, cid, Pr, Ymine + (size_t)par * x.yhalf);
+      xg_barrier(x, g, p, barg, epoch, status);   // every rank's partials of mode j are written
+      // ---------------- phase B: rows [s0, s1) of mode j from all ranks' partials
+      const int s0 = (int)((long long)Qj * p / P), s1 = (int)((long long)Qj * (p + 1) / P);
+      const int ncol = s1 - s0, E = ncol * r;
+      double* ystage = sm.Us;
+      if (tid == 0) {
+        const uint32_t ybytes = E > 0 ? (uint32_t)(Pr * nbk) * 8u : 0u;
+        const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(sm.bar + 1, gbytes);
+        if (gbytes) bulk_g2s(sm.Gs + (size_t)pending * rr, Gg + (size_t)pending * rr, gbytes, sm.bar + 1);
+        mbar_arrive_expect_tx(sm.bar, ybytes * (uint32_t)ngpu);
+        if (ybytes)
+          for (int h = 0; h < ngpu; ++h) {
+            const double* yh = reinterpret_cast<const double*>(x.peer[h] + XG_HDR) + (size_t)par * x.yhalf +
+                               (size_t)p * Pr * nbk;
+            bulk_g2s(ystage + (size_t)h * Pr * nbk, yh, ybytes, sm.bar);
+          }
+      }
+      mbar_wait(sm.bar + 1, gphase);
+      gphase ^= 1u;
+      if (warm_ns) { mbar_wait(sm.bar + 4, xpf); xpf ^= 1u; }
+      if (warm_ns) build_a<RM>(a, sm, j);
+      mbar_wait(sm.bar, bphase);
+      bphase ^= 1u;
+      for (int o = tid; o < E; o += ALS_NT) {   // rank-major, then cluster: the single-GPU order
+        double s0a = 0.0, s1a = 0.0;
+        int q = 0;
+        for (; q + 2 <= PrT; q += 2) {
+          s0a += ystage[(size_t)q * nbk + o];
+          s1a += ystage[(size_t)(q + 1) * nbk + o];
+        }
+        for (; q < PrT; ++q) s0a += ystage[(size_t)q * nbk + o];
+        sm.rb[o] = s0a + s1a;
+      }
+      __syncthreads();
+      if (solve_mode<RM>(a, sm, j, sweep, E, status, ns_fail, Xpg, P, p)) { rows_mode = j; rows_sweep = sweep; }
+      if (E > 0) {
+        const double* ub = sm.vb + 2 * a.ncolmax * r;
+        double* Uj = Ug + a.offU[j];
+        double* Up = Upg + a.offUp[j];
+        int nf = 0;
+        for (int e = tid; e < E; e += ALS_NT) {
+          const int sc = e / r, i = e - sc * r;
+          const double v = ub[e];
+          if (!isfinite(v)) nf = 1;
+          Uj[(size_t)(s0 + sc) * r + i] = v;
+          Up[(size_t)(s0 + sc) * rh + i] = v;
+        }
+        if (nf) atomicOr(gr.info, 2);
+      }
+      pending = j;
+      group_barrier(barg, epoch, Pg);
+    }
+  }
+  // no rank may leave (and reuse its exchange buffer in the next launch) while a
+  // peer can still read its partials
+  xg_barrier(x, g, p, barg, epoch, status);
+  if (status && tid == 0) atomicOr(gr.info, status);
+  if (p == 0 && tid == 0) gr.info[1] = a.sweeps;
+  cl.sync();
 }
 
 struct AlsPlan {
@@ -2621,5 +2887,223 @@ int tp_als_shard_update_f64(int d, const int* q, int Rl, const double* V, int r,
   if (e == cudaSuccess) e = gemm(r, Rl, Q, Uj, 1, r, V + s.offV[j], Rl, 1, C + (size_t)j * r * Rl, Rl, 1, cs);
   return cuda_status(e);
 }
+
+}  // extern "C"
+
+// ===========================================================================
+// Host side of the R-sharded fused truncation (als_xg).
+// ===========================================================================
+namespace tp {
+
+struct XgPlan {
+  AlsPlan pl;
+  int Pg = 0, Pr = 0, PrT = 0;
+  long long yhalf = 0;
+  size_t ws_group = 0, peer_bytes = 0;
+};
+
+static const void* xg_kernel_ptr(int rm) {
+  switch (rm) {
+    case 8: return (const void*)als_xg<8>;
+    case 16: return (const void*)als_xg<16>;
+    default: return (const void*)als_xg<32>;
+  }
+}
+
+// Pq = 4 CTAs per cluster (the single-GPU plan's choice for config 1); Pr clusters per
+// rank such that all ngroups x Pr clusters are co-resident and the rank-major
+// staging of ngpu x Pr partial slices fits; total clusters capped at 32 (the
+// single-GPU optimum), equal R-slabs preferred.
+static int plan_xg(int d, const int* q, int Rl, int r, int ngpu, int ngroups, XgPlan& xp) {
+  if (d < 1 || d > TP_MAXD || Rl < 1 || r < 1 || !q || ngpu < 1 || ngpu > TP_MAXG || ngroups < 1 ||
+      ngroups > ngpu)
+    return TP_EINVAL;
+  for (int k = 0; k < d; ++k) if (q[k] < 1) return TP_EINVAL;
+  AlsPlan& pl = xp.pl;
+  pl.rm = choose_rm(r);
+  if (!pl.rm || (r & 1)) return TP_EUNSUPPORTED;
+  int dev = 0, nsm = 148, smem_optin = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  } else {
+    cudaGetLastError();
+  }
+  if (smem_optin <= 0) smem_optin = 227 * 1024;
+  memset(&pl.a, 0, sizeof(pl.a));
+  AlsArgs& a = pl.a;
+  int qmin = q[0], qmax = 0;
+  long long ov = 0, ou = 0, oup = 0;
+  for (int k = 0; k < d; ++k) {
+    qmin = q[k] < qmin ? q[k] : qmin;
+    qmax = q[k] > qmax ? q[k] : qmax;
+    a.q[k] = q[k]; a.qs[k] = pad4(q[k]); a.offV[k] = ov; a.offU[k] = ou; a.offUp[k] = oup;
+    ov += (long long)q[k] * Rl; ou += (long long)q[k] * r; oup += (long long)q[k] * pad4(r);
+  }
+  a.d = d; a.R = Rl; a.r = r; a.qmax = qmax;
+  const int Pq = 4;
+  if (Pq > qmin) return TP_EUNSUPPORTED;
+  const void* fn = xg_kernel_ptr(pl.rm);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaGetLastError();
+  auto try_pr = [&](int Pr) -> bool {
+    const int P = Pr * Pq, PrT = Pr * ngpu, wmax = (Rl + Pr - 1) / Pr, ldw = pad4(wmax);
+    const int ncolmax = (qmax + P - 1) / P;
+    int sumnb = 0, nbmax = 0;
+    for (int k = 0; k < d; ++k) {
+      const int nb = (q[k] + Pq - 1) / Pq;
+      sumnb += (nb + 3) & ~3;
+      nbmax = nb > nbmax ? nb : nbmax;
+    }
+    sumnb += 8;
+    const int mtr = (r + 7) / 8, nG = mtr * (mtr + 1) / 2;
+    int chunk = r * wmax + ((nG + Pr - 1) / Pr) * 64;
+    chunk += chunk & 1;
+    const size_t smem = cl_smem_doubles(d, r, wmax, ldw, sumnb, nbmax, ncolmax, PrT, Pq, chunk, qmax) * sizeof(double);
+    if (smem > (size_t)smem_optin) return false;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = Pq; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(P * ngroups); cfg.blockDim = dim3(ALS_NT); cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int nclu = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclu, fn, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
+    if (nclu < Pr * ngroups) return false;
+    a.Pq = Pq; a.ldw = ldw; a.chunk = chunk; a.nbmax = nbmax; a.sumqs = sumnb;
+    a.wmax = wmax; a.ncolmax = ncolmax; a.P = P;
+    int qo = 0;
+    for (int k = 0; k < d; ++k) { a.qoffc[k] = qo; qo += (((q[k] + Pq - 1) / Pq + 3) & ~3) * ldw; }
+    pl.P = P; pl.Pr = Pr; pl.smem = smem; pl.variant = 6;
+    xp.Pg = P; xp.Pr = Pr; xp.PrT = PrT;
+    xp.yhalf = (long long)P * Pr * ncolmax * r;
+    xp.yhalf += xp.yhalf & 1;
+    return true;
+  };
+  int Pr = nsm / (Pq * ngroups);
+  if (Pr * ngpu > 32) Pr = 32 / ngpu > 0 ? 32 / ngpu : 1;
+  if (Pr > Rl) Pr = Rl;
+  bool ok = false;
+  for (; Pr >= 1 && !ok; --Pr) {
+    if (!try_pr(Pr)) continue;
+    ok = true;
+    const int wmax = (Rl + Pr - 1) / Pr;
+    if (Rl % Pr != 0)
+      for (int p2 = Pr - 1; p2 >= 1 && (Rl + p2 - 1) / p2 == wmax; --p2)
+        if (Rl % p2 == 0) {
+          if (!try_pr(p2)) try_pr(Pr);
+          break;
+        }
+  }
+  if (!ok) return TP_EUNSUPPORTED;
+  long long nup = 0;
+  for (int k = 0; k < d; ++k) nup += (long long)q[k] * pad4(r);
+  xp.ws_group = align_up(sizeof(double) * (size_t)d * r * r) + align_up(16 * sizeof(unsigned int)) +
+                align_up(sizeof(double) * 2 * (size_t)d * r * pad4(r)) + align_up(sizeof(double) * (size_t)nup) + 256;
+  xp.peer_bytes = XG_HDR + 2 * (size_t)xp.yhalf * sizeof(double);
+  a.ns_max = g_ns_max;
+  return TP_OK;
+}
+
+}  // namespace tp
+
+extern "C" {
+
+size_t tp_als_xg_ws_bytes(int d, const int* q, int R_local, int r, int ngpu, int ngroups) {
+  XgPlan xp;
+  return plan_xg(d, q, R_local, r, ngpu, ngroups, xp) == TP_OK ? xp.ws_group : 0;
+}
+
+size_t tp_als_xg_peer_bytes(int d, const int* q, int R_local, int r, int ngpu, int ngroups) {
+  XgPlan xp;
+  return plan_xg(d, q, R_local, r, ngpu, ngroups, xp) == TP_OK ? xp.peer_bytes : 0;
+}
+
+int tp_als_xg_plan(int d, const int* q, int R_local, int r, int ngpu, int ngroups, int* out) {
+  if (!out) return TP_EINVAL;
+  XgPlan xp;
+  const int st = plan_xg(d, q, R_local, r, ngpu, ngroups, xp);
+  if (st != TP_OK) return st;
+  out[0] = xp.Pg; out[1] = xp.pl.a.Pq; out[2] = xp.Pr; out[3] = (int)xp.pl.smem;
+  return TP_OK;
+}
+
+int tp_als_xg_f64(int d, const int* q, int R_local, int r, int sweeps, double reg, int reg_mode,
+                  int ngroups, const double* const* V, double* const* U, int* const* info,
+                  void* const* ws, size_t ws_bytes, int ngpu, int rank0, void* const* peer,
+                  long long seq, void* stream) {
+  if (!V || !U || !info || !ws || !peer || sweeps < 0 || !(reg >= 0.0) || rank0 < 0 || rank0 + ngroups > ngpu ||
+      seq < 1)
+    return TP_EINVAL;
+  XgPlan xp;
+  int st = plan_xg(d, q, R_local, r, ngpu, ngroups, xp);
+  if (st != TP_OK) return st;
+  if (ws_bytes < xp.ws_group) return TP_EWORKSPACE;
+  for (int h = 0; h < ngpu; ++h) if (!peer[h]) return TP_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  AlsArgs a = xp.pl.a;
+  a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = 0.0; a.stall = -INFINITY; a.need_resid = 0;
+  XgArgs x;
+  memset(&x, 0, sizeof(x));
+  x.ngroups = ngroups; x.ngpu = ngpu; x.rank0 = rank0; x.Pg = xp.Pg;
+  x.seq_base = (unsigned long long)seq << 20;
+  x.yhalf = xp.yhalf;
+  for (int h = 0; h < ngpu; ++h) x.peer[h] = static_cast<unsigned char*>(peer[h]);
+  long long nup = 0;
+  for (int k = 0; k < d; ++k) nup += (long long)q[k] * pad4(r);
+  for (int g = 0; g < ngroups; ++g) {
+    if (!V[g] || !U[g] || !info[g] || !ws[g]) return TP_EINVAL;
+    Carver cv(ws[g], ws_bytes);
+    XgGroup& gr = x.grp[g];
+    gr.V = V[g]; gr.U = U[g]; gr.info = info[g];
+    gr.G = cv.take<double>((size_t)d * r * r);
+    gr.bar = cv.take<unsigned int>(16);
+    gr.Xprev = cv.take<double>(2 * (size_t)d * r * pad4(r));
+    gr.Upad = cv.take<double>((size_t)nup);
+    cudaError_t e = cudaMemsetAsync(info[g], 0, 2 * sizeof(int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(gr.bar, 0, 16 * sizeof(unsigned int), s);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  const void* fn = xg_kernel_ptr(xp.pl.rm);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xp.pl.smem);
+  if (e != cudaSuccess) return cuda_status(e);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = a.Pq; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.gridDim = dim3(xp.Pg * ngroups); cfg.blockDim = dim3(ALS_NT); cfg.dynamicSmemBytes = xp.pl.smem; cfg.stream = s;
+  cfg.attrs = at; cfg.numAttrs = 2;
+  void* args[] = {&a, &x};
+  e = cudaLaunchKernelExC(&cfg, fn, args);
+  return cuda_status(e);
+}
+
+int tp_dev_alloc(size_t bytes, void** ptr) {
+  if (!ptr || bytes == 0) return TP_EINVAL;
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e == cudaSuccess) e = cudaMemset(*ptr, 0, bytes);
+  return cuda_status(e);
+}
+
+int tp_dev_free(void* ptr) { return cuda_status(cudaFree(ptr)); }
+
+int tp_ipc_handle(void* ptr, void* handle) {
+  if (!ptr || !handle) return TP_EINVAL;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e == cudaSuccess) memcpy(handle, &h, sizeof(h));
+  return cuda_status(e);
+}
+
+int tp_ipc_open(const void* handle, void** ptr) {
+  if (!ptr || !handle) return TP_EINVAL;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+int tp_ipc_close(void* ptr) { return cuda_status(cudaIpcCloseMemHandle(ptr)); }
 
 }  // extern "C"

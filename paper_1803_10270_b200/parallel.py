@@ -22,7 +22,8 @@ import torch
 from . import _lib
 from .cp import ALSApproxConfig, CPTensor
 
-__all__ = ["shard_range", "ShardedALS", "DeviceShardOps", "TorchDistComm", "LocalComm", "shard_batch"]
+__all__ = ["shard_range", "ShardedALS", "DeviceShardOps", "TorchDistComm", "LocalComm", "shard_batch",
+           "FusedShardedALS", "GraphShardedALS", "make_sharded_als", "sharded_cp_approx_als", "simulate_sharded_als"]
 
 
 def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -186,21 +187,205 @@ class GraphShardedALS:
         return self.drv.cfg.max_sweeps * self.d * 6 + 2 * self.d
 
 
-def make_sharded_als(V_local: CPTensor, r: int, config: ALSApproxConfig | None = None, group=None):
-    """The R-sharded truncation driver for this process group."""
+class FusedShardedALS:
+    """R-sharded truncation in ONE fused launch per GPU (``tp_als_xg_f64``): every
+    rank runs the cluster ALS kernel on its R-slab; the per-mode-update r x Q
+    right-hand-side exchange happens inside the kernel through peer-mapped
+    exchange buffers (CUDA IPC handles swapped once with all_gather_object) and an
+    in-kernel cross-GPU barrier -- no host round trip or NCCL call per mode update.
+    Every rank ends with the identical (bitwise) fit."""
+
+    def __init__(self, V_local: CPTensor, r: int, config: ALSApproxConfig | None = None, group=None):
+        import ctypes
+        self.cfg = config or ALSApproxConfig(max_sweeps=20, stall=-np.inf, reg=1e-10)
+        if self.cfg.tol > 0 or self.cfg.stall > -np.inf:
+            raise ValueError("the sharded ALS runs a fixed sweep count (tol=0, stall=-inf)")
+        dist = torch.distributed.is_available() and torch.distributed.is_initialized()
+        self.world = torch.distributed.get_world_size(group) if dist else 1
+        self.rank = torch.distributed.get_rank(group) if dist else 0
+        self.V, self.r, self.d = V_local, r, V_local.ndim
+        self.L = _lib.lib()
+        self.qs = _lib.int_array(V_local.qs)
+        L = self.L
+        nws = L.tp_als_xg_ws_bytes(self.d, self.qs, V_local.rank, r, self.world, 1)
+        npeer = L.tp_als_xg_peer_bytes(self.d, self.qs, V_local.rank, r, self.world, 1)
+        if nws == 0 or npeer == 0:
+            raise ValueError(f"unsupported sharded ALS size d={self.d}, R_l={V_local.rank}, r={r}")
+        dev = V_local.data.device
+        self.ws = torch.empty(nws, dtype=torch.uint8, device=dev)
+        self.info = torch.zeros(2, dtype=torch.int32, device=dev)
+        ptr = ctypes.c_void_p()
+        _lib.check(L.tp_dev_alloc(npeer, ctypes.byref(ptr)), "exchange buffer")
+        self._mine = ptr.value
+        self._opened = []
+        peers = [self._mine]
+        if self.world > 1:
+            h = (ctypes.c_char * 64)()
+            _lib.check(L.tp_ipc_handle(self._mine, h), "ipc handle")
+            handles = [None] * self.world
+            torch.distributed.all_gather_object(handles, bytes(h), group=group)
+            peers = []
+            for i, hb in enumerate(handles):
+                if i == self.rank:
+                    peers.append(self._mine)
+                    continue
+                p2 = ctypes.c_void_p()
+                _lib.check(L.tp_ipc_open(ctypes.c_char_p(hb), ctypes.byref(p2)), "ipc open")
+                self._opened.append(p2.value)
+                peers.append(p2.value)
+        self._peers = (ctypes.c_void_p * self.world)(*peers)
+        self.seq = 0
+        self.group = group
+        plan = (ctypes.c_int * 4)()
+        _lib.check(L.tp_als_xg_plan(self.d, self.qs, V_local.rank, r, self.world, 1, plan), "plan")
+        self.plan = {"ctas": plan[0], "cluster": plan[1], "clusters": plan[2], "smem_bytes": plan[3]}
+
+    def prepare(self, U: torch.Tensor):
+        pass
+
+    def run(self, U: torch.Tensor, V: CPTensor | None = None):
+        import ctypes
+        V = V or self.V
+        if V.rank != self.V.rank or V.qs != self.V.qs:
+            raise ValueError("slab shape differs from the planned one")
+        self.seq += 1
+        reg, mode = (1e-12, 1) if self.cfg.reg is None else (float(self.cfg.reg), 0)
+        one = lambda v: (ctypes.c_void_p * 1)(v)   # noqa: E731
+        st = self.L.tp_als_xg_f64(self.d, self.qs, V.rank, self.r, int(self.cfg.max_sweeps), reg, mode, 1,
+                                  one(V.data.data_ptr()), one(U.data_ptr()), one(self.info.data_ptr()),
+                                  one(self.ws.data_ptr()), self.ws.numel(), self.world, self.rank, self._peers,
+                                  self.seq, _lib.stream_ptr(U.device))
+        _lib.check(st, "sharded cp_approx_als")
+        return U
+
+    def check(self):
+        _check_xg_info(self.info)
+
+    def describe(self) -> str:
+        return (f"one fused launch per GPU: {self.plan['clusters']} clusters x {self.plan['cluster']} CTAs on the "
+                f"rank's R-slab, in-kernel exchange of the r x Q partials through peer-mapped memory, cross-GPU "
+                f"flag barrier once per mode update")
+
+    def kernel_name(self) -> str:
+        return f"tp::als_xg<32> ({self.plan['ctas']} CTAs per GPU, cluster {self.plan['cluster']})"
+
+    def launches_per_truncation(self) -> int:
+        return 1
+
+    def close(self):
+        if self._mine is None:
+            return
+        torch.cuda.synchronize()
+        if self.world > 1:
+            torch.distributed.barrier(group=self.group)
+        for p in self._opened:
+            self.L.tp_ipc_close(p)
+        self._opened = []
+        self.L.tp_dev_free(self._mine)
+        self._mine = None
+
+    def __del__(self):
+        try:
+            if self._mine is not None and self.world == 1:
+                self.L.tp_dev_free(self._mine)
+                self._mine = None
+        except Exception:
+            pass
+
+
+def _check_xg_info(info: torch.Tensor) -> None:
+    from .cp import ConditioningError
+    status = int(info[0].item())
+    if status & 4:
+        raise RuntimeError("sharded ALS: a peer rank did not reach the exchange barrier within 5 s")
+    if status & 2:
+        raise ConditioningError("normal equations produced non-finite coefficients")
+    if status & 1:
+        raise ConditioningError("regularised normal equations are not positive definite")
+
+
+def make_sharded_als(V_local: CPTensor, r: int, config: ALSApproxConfig | None = None, group=None,
+                     impl: str = "auto"):
+    """The R-sharded truncation driver: the fused one-launch kernel (``impl="fused"``,
+    the default when the size is supported) or the per-mode kernels + NCCL graph."""
+    if impl in ("auto", "fused"):
+        try:
+            return FusedShardedALS(V_local, r, config, group)
+        except ValueError:
+            if impl == "fused":
+                raise
     return GraphShardedALS(V_local, r, config, group)
+
+
+_DRIVERS: dict = {}
 
 
 def sharded_cp_approx_als(V_local: CPTensor, init: CPTensor, config: ALSApproxConfig | None = None,
                           group=None, check: bool = True) -> CPTensor:
     """R-sharded ``cp_approx_als``: every rank passes its slab of the target and the
-    same initial guess; every rank gets the full fit.  ``check=False`` defers the
-    status read (no host round trip)."""
-    comm = TorchDistComm(group) if (torch.distributed.is_available() and torch.distributed.is_initialized()) \
-        else LocalComm()
-    ops = DeviceShardOps(V_local, init.rank)
+    same initial guess; every rank gets the full fit.  The fused driver (and its
+    peer mappings) is cached per (shapes, config, group); ``check=False`` defers
+    the status read (no host round trip)."""
+    cfg = config or ALSApproxConfig(max_sweeps=20, stall=-np.inf, reg=1e-10)
+    key = (V_local.qs, V_local.rank, init.rank, cfg.max_sweeps, cfg.reg, id(group), V_local.data.device.index)
+    drv = _DRIVERS.get(key)
+    if drv is None:
+        try:
+            drv = FusedShardedALS(V_local, init.rank, cfg, group)
+        except ValueError:
+            drv = None
+        _DRIVERS[key] = drv
     out = init.copy()
-    ShardedALS(ops, comm, config).run(out.data, init.ndim)
+    if drv is None:
+        comm = TorchDistComm(group) if (torch.distributed.is_available() and torch.distributed.is_initialized()) \
+            else LocalComm()
+        ops = DeviceShardOps(V_local, init.rank)
+        ShardedALS(ops, comm, cfg).run(out.data, init.ndim)
+        if check:
+            ops.check()
+        return out
+    drv.run(out.data, V_local)
     if check:
-        ops.check()
+        drv.check()
     return out
+
+
+def simulate_sharded_als(V_factors, init_factors, shards: int, config: ALSApproxConfig | None = None,
+                         specs=None):
+    """Run the fused R-sharded kernel with ``shards`` ranks' CTA groups co-resident in
+    ONE launch on this GPU (each group its own slab, replicated state and exchange
+    buffer; the in-kernel exchange and barrier work exactly as across GPUs).
+    Returns the per-rank fits (device tensors in CP layout)."""
+    import ctypes
+    from .basis import BasisSpec
+    cfg = config or ALSApproxConfig(max_sweeps=20, stall=-np.inf, reg=1e-10)
+    V_factors = [np.asarray(v) for v in V_factors]
+    qs = [v.shape[0] for v in V_factors]
+    R = V_factors[0].shape[1]
+    r = init_factors[0].shape[1]
+    specs = specs or tuple(BasisSpec(q, np.pi, "collocation", lo=0.0) for q in qs)
+    L = _lib.lib()
+    d = len(qs)
+    spans = [shard_range(R, shards, g) for g in range(shards)]
+    if len({hi - lo for lo, hi in spans}) != 1:
+        raise ValueError("simulated shards need equal slabs (R divisible by shards)")
+    Rl = spans[0][1] - spans[0][0]
+    qa = _lib.int_array(qs)
+    nws = L.tp_als_xg_ws_bytes(d, qa, Rl, r, shards, shards)
+    npeer = L.tp_als_xg_peer_bytes(d, qa, Rl, r, shards, shards)
+    if nws == 0 or npeer == 0:
+        raise ValueError("unsupported simulated sharded ALS size")
+    dev = _lib.device()
+    Vs = [CPTensor(specs, [v[:, lo:hi] for v in V_factors]) for lo, hi in spans]
+    Us = [CPTensor(specs, init_factors).data for _ in range(shards)]
+    infos = [torch.zeros(2, dtype=torch.int32, device=dev) for _ in range(shards)]
+    wss = [torch.empty(nws, dtype=torch.uint8, device=dev) for _ in range(shards)]
+    peers = [torch.zeros(npeer, dtype=torch.uint8, device=dev) for _ in range(shards)]
+    arr = lambda ts: (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])   # noqa: E731
+    reg, mode = (1e-12, 1) if cfg.reg is None else (float(cfg.reg), 0)
+    st = L.tp_als_xg_f64(d, qa, Rl, r, int(cfg.max_sweeps), reg, mode, shards, arr([v.data for v in Vs]), arr(Us),
+                         arr(infos), arr(wss), nws, shards, 0, arr(peers), 1, _lib.stream_ptr(dev))
+    _lib.check(st, "simulated sharded ALS")
+    for inf in infos:
+        _check_xg_info(inf)
+    return Us

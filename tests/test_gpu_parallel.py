@@ -104,3 +104,69 @@ def test_captured_graph_replay_matches_eager():
     ref = ocp.als(V, [v[:, :r].copy() for v in V], 7, lam=1e-10)
     out = cp.CPTensor(S, data=U, rank=r).to_numpy()
     assert metrics.cp_rel_diff(ref, out) <= 1e-9
+
+
+# ---- fused one-launch R-sharded kernel (tp_als_xg_f64) ------------------------------
+
+def _unflat(u, qs, r):
+    u = u.cpu().numpy()
+    fac, off = [], 0
+    for q in qs:
+        fac.append(u[off:off + q * r].reshape(q, r))
+        off += q * r
+    return fac
+
+
+@pytest.mark.parametrize("shards", [1, 2, 4])
+@pytest.mark.parametrize("qs,R,r", [((20, 16, 24, 12), 48, 6), ((32, 40, 28), 64, 16), ((64,) * 4, 96, 32)])
+def test_fused_sharded_simulated_groups(shards, qs, R, r):
+    """`shards` ranks' CTA groups in ONE launch (the in-kernel peer exchange and
+    cross-group flag barrier exactly as across GPUs): every rank's fit is bitwise
+    identical and matches the oracle (cp.py:310-320) at <= 1e-9."""
+    rng = np.random.default_rng(R + r + shards)
+    V = [rng.standard_normal((q, R)) / 4 for q in qs]
+    init = [v[:, :r].copy() for v in V]
+    sweeps = 7
+    outs = parallel.simulate_sharded_als(V, init, shards, cp.ALSApproxConfig(max_sweeps=sweeps, stall=-np.inf,
+                                                                              reg=1e-10))
+    for u in outs[1:]:
+        assert torch.equal(u, outs[0])
+    ref = ocp.als(V, init, sweeps, lam=1e-10)
+    assert metrics.cp_rel_diff(ref, _unflat(outs[0], qs, r)) <= 1e-9
+
+
+@pytest.mark.parametrize("shards", [2, 4])
+def test_fused_sharded_config1(shards):
+    """BASELINE config 1 (d=6, Q=256, R=512 -> r=32, 20 sweeps) R-sharded over 2 / 4
+    simulated ranks: bitwise-identical replicas, oracle parity <= 1e-9."""
+    w = workloads.cfg1(seed=1)
+    outs = parallel.simulate_sharded_als(w["V"], w["init"], shards,
+                                         cp.ALSApproxConfig(max_sweeps=w["sweeps"], stall=-np.inf, reg=w["lam"]))
+    for u in outs[1:]:
+        assert torch.equal(u, outs[0])
+    ref = ocp.als(w["V"], w["init"], w["sweeps"], lam=w["lam"])
+    assert metrics.cp_rel_diff(ref, _unflat(outs[0], [256] * 6, 32)) <= 1e-9
+
+
+def test_fused_sharded_driver_world1_repeatable():
+    """FusedShardedALS on one rank (no process group): the public sharded API, repeated
+    calls (monotonic barrier tags across launches) give identical fits, oracle parity."""
+    rng = np.random.default_rng(8)
+    qs, R, r = (48, 40, 36, 44), 80, 12
+    S = tuple(BasisSpec(q, math.pi, "collocation", lo=0.0) for q in qs)
+    V = [rng.standard_normal((q, R)) / 4 for q in qs]
+    init = [v[:, :r].copy() for v in V]
+    cfg = cp.ALSApproxConfig(max_sweeps=6, stall=-np.inf, reg=1e-10)
+    Vt, It = cp.CPTensor(S, V), cp.CPTensor(S, init)
+    outs = [parallel.sharded_cp_approx_als(Vt, It, cfg) for _ in range(3)]
+    for o in outs[1:]:
+        assert torch.equal(o.data, outs[0].data)
+    ref = ocp.als(V, init, 6, lam=1e-10)
+    assert metrics.cp_rel_diff(ref, outs[0].to_numpy()) <= 1e-9
+    drv = parallel.make_sharded_als(Vt, r, cfg)
+    assert isinstance(drv, parallel.FusedShardedALS)
+    U = It.data.clone()
+    drv.run(U)
+    drv.check()
+    assert torch.equal(U, outs[0].data)
+    drv.close()
