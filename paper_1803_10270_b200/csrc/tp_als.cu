@@ -2136,6 +2136,7 @@ struct XgGroup {
 
 struct XgArgs {
   int ngroups, ngpu, rank0, Pg;
+  int CH;                                  // partial slices per staged chunk (two chunk slots)
   unsigned long long seq_base;
   long long yhalf;                         // doubles of one parity half of Y
   XgGroup grp[TP_MAXG];
@@ -2219,7 +2220,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_xg(const __grid_constant__ AlsA
   const int tid = threadIdx.x;
   const int Pg = x.Pg, g = blockIdx.x / Pg, p = blockIdx.x - g * Pg, P = Pg;
   const int Pq = a.Pq, b = (int)cl.block_rank(), cid = p / Pq, Pr = P / Pq;
-  const int ngpu = x.ngpu, rank = x.rank0 + g, PrT = Pr * ngpu;
+  const int ngpu = x.ngpu, rank = x.rank0 + g;
   const XgGroup& gr = x.grp[g];
   const double* Vg = gr.V;
   double* Ug = gr.U;
@@ -2228,13 +2229,13 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_xg(const __grid_constant__ AlsA
   double* Xpg = gr.Xprev;
   unsigned int* barg = gr.bar;
   double* Ymine = reinterpret_cast<double*>(x.peer[rank] + XG_HDR);
-  const Smem sm = carve_cl(smem, a, PrT);
+  const Smem sm = carve_cl(smem, a, 2 * x.CH);   // staging: max(U block rows, two chunk slots)
   const int r = a.r, R = a.R, rr = r * r, rh = pad4(r), ldw = a.ldw;
   const int c0 = (int)((long long)R * cid / Pr), c1 = (int)((long long)R * (cid + 1) / Pr), w = c1 - c0;
   const int w4 = (w + 3) / 4 * 4;
   unsigned int epoch = 0;   // arrivals on this group's counter (both barrier kinds); xg tags derive from it
   int status = 0;
-  uint32_t bphase = 0, gphase = 0, xphase = 0, xpf = 0;
+  uint32_t bphase = 0, gphase = 0, xphase = 0, xpf = 0, b3phase = 0;
   if (tid == 0) {
     for (int q = 0; q < 5; ++q) mbar_init(sm.bar + q, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -2300,35 +2301,45 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_xg(const __grid_constant__ AlsA
       const int s0 = (int)((long long)Qj * p / P), s1 = (int)((long long)Qj * (p + 1) / P);
       const int ncol = s1 - s0, E = ncol * r;
       double* ystage = sm.Us;
+      // rows' partial slices of all ranks (rank-major, then cluster), streamed through
+      // two chunk slots of CH slices (bar[0] / bar[3]); sequential fixed-order sums
+      const int CH = x.CH, nchp = (Pr + CH - 1) / CH, nchunk = E > 0 ? ngpu * nchp : 0;
+      auto issue = [&](int ci) {
+        const int h = ci / nchp, cc = (ci - h * nchp) * CH, n = min(CH, Pr - cc);
+        const double* src = reinterpret_cast<const double*>(x.peer[h] + XG_HDR) + (size_t)par * x.yhalf +
+                            ((size_t)p * Pr + cc) * nbk;
+        uint64_t* bb = (ci & 1) ? sm.bar + 3 : sm.bar;
+        mbar_arrive_expect_tx(bb, (uint32_t)(n * nbk) * 8u);
+        bulk_g2s(ystage + (size_t)(ci & 1) * CH * nbk, src, (uint32_t)(n * nbk) * 8u, bb);
+      };
       if (tid == 0) {
-        const uint32_t ybytes = E > 0 ? (uint32_t)(Pr * nbk) * 8u : 0u;
         const uint32_t gbytes = pending >= 0 ? (uint32_t)rr * 8u : 0u;
         fence_proxy_async();
         mbar_arrive_expect_tx(sm.bar + 1, gbytes);
         if (gbytes) bulk_g2s(sm.Gs + (size_t)pending * rr, Gg + (size_t)pending * rr, gbytes, sm.bar + 1);
-        mbar_arrive_expect_tx(sm.bar, ybytes * (uint32_t)ngpu);
-        if (ybytes)
-          for (int h = 0; h < ngpu; ++h) {
-            const double* yh = reinterpret_cast<const double*>(x.peer[h] + XG_HDR) + (size_t)par * x.yhalf +
-                               (size_t)p * Pr * nbk;
-            bulk_g2s(ystage + (size_t)h * Pr * nbk, yh, ybytes, sm.bar);
-          }
+        if (nchunk > 0) issue(0);
+        if (nchunk > 1) issue(1);
       }
+      for (int o = tid; o < E; o += ALS_NT) sm.rb[o] = 0.0;
       mbar_wait(sm.bar + 1, gphase);
       gphase ^= 1u;
       if (warm_ns) { mbar_wait(sm.bar + 4, xpf); xpf ^= 1u; }
       if (warm_ns) build_a<RM>(a, sm, j);
-      mbar_wait(sm.bar, bphase);
-      bphase ^= 1u;
-      for (int o = tid; o < E; o += ALS_NT) {   // rank-major, then cluster: the single-GPU order
-        double s0a = 0.0, s1a = 0.0;
-        int q = 0;
-        for (; q + 2 <= PrT; q += 2) {
-          s0a += ystage[(size_t)q * nbk + o];
-          s1a += ystage[(size_t)(q + 1) * nbk + o];
+      for (int ci = 0; ci < nchunk; ++ci) {
+        if (ci & 1) { mbar_wait(sm.bar + 3, b3phase); b3phase ^= 1u; }
+        else { mbar_wait(sm.bar, bphase); bphase ^= 1u; }
+        const int h = ci / nchp, cc = (ci - h * nchp) * CH, n = min(CH, Pr - cc);
+        const double* slot = ystage + (size_t)(ci & 1) * CH * nbk;
+        for (int o = tid; o < E; o += ALS_NT) {
+          double acc = sm.rb[o];
+          for (int q = 0; q < n; ++q) acc += slot[(size_t)q * nbk + o];
+          sm.rb[o] = acc;
         }
-        for (; q < PrT; ++q) s0a += ystage[(size_t)q * nbk + o];
-        sm.rb[o] = s0a + s1a;
+        __syncthreads();   // slot consumed before it is refilled
+        if (tid == 0 && ci + 2 < nchunk) {
+          fence_proxy_async();
+          issue(ci + 2);
+        }
       }
       __syncthreads();
       if (solve_mode<RM>(a, sm, j, sweep, E, status, ns_fail, Xpg, P, p)) { rows_mode = j; rows_sweep = sweep; }
@@ -2897,7 +2908,7 @@ namespace tp {
 
 struct XgPlan {
   AlsPlan pl;
-  int Pg = 0, Pr = 0, PrT = 0;
+  int Pg = 0, Pr = 0, PrT = 0, CH = 1;
   long long yhalf = 0;
   size_t ws_group = 0, peer_bytes = 0;
 };
@@ -2959,8 +2970,14 @@ static int plan_xg(int d, const int* q, int Rl, int r, int ngpu, int ngroups, Xg
     const int mtr = (r + 7) / 8, nG = mtr * (mtr + 1) / 2;
     int chunk = r * wmax + ((nG + Pr - 1) / Pr) * 64;
     chunk += chunk & 1;
-    const size_t smem = cl_smem_doubles(d, r, wmax, ldw, sumnb, nbmax, ncolmax, PrT, Pq, chunk, qmax) * sizeof(double);
+    // chunk slots: as many slices as fit twice into the U block staging (no extra smem)
+    const size_t ust = (size_t)(((nbmax + 3) & ~3) + 1) * pad4(r), nbk = (size_t)ncolmax * r;
+    int CH = (int)(ust / (2 * nbk));
+    if (CH < 1) CH = 1;
+    if (CH > Pr) CH = Pr;
+    const size_t smem = cl_smem_doubles(d, r, wmax, ldw, sumnb, nbmax, ncolmax, 2 * CH, Pq, chunk, qmax) * sizeof(double);
     if (smem > (size_t)smem_optin) return false;
+    (void)PrT;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -2975,7 +2992,7 @@ static int plan_xg(int d, const int* q, int Rl, int r, int ngpu, int ngroups, Xg
     int qo = 0;
     for (int k = 0; k < d; ++k) { a.qoffc[k] = qo; qo += (((q[k] + Pq - 1) / Pq + 3) & ~3) * ldw; }
     pl.P = P; pl.Pr = Pr; pl.smem = smem; pl.variant = 6;
-    xp.Pg = P; xp.Pr = Pr; xp.PrT = PrT;
+    xp.Pg = P; xp.Pr = Pr; xp.PrT = PrT; xp.CH = CH;
     xp.yhalf = (long long)P * Pr * ncolmax * r;
     xp.yhalf += xp.yhalf & 1;
     return true;
@@ -3045,7 +3062,7 @@ int tp_als_xg_f64(int d, const int* q, int R_local, int r, int sweeps, double re
   a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = 0.0; a.stall = -INFINITY; a.need_resid = 0;
   XgArgs x;
   memset(&x, 0, sizeof(x));
-  x.ngroups = ngroups; x.ngpu = ngpu; x.rank0 = rank0; x.Pg = xp.Pg;
+  x.ngroups = ngroups; x.ngpu = ngpu; x.rank0 = rank0; x.Pg = xp.Pg; x.CH = xp.CH;
   x.seq_base = (unsigned long long)seq << 20;
   x.yhalf = xp.yhalf;
   for (int h = 0; h < ngpu; ++h) x.peer[h] = static_cast<unsigned char*>(peer[h]);
