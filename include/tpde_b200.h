@@ -224,8 +224,8 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
  *             CP layout), replicated guess/fit (rank r), int[2] status
  *             {bits: 1 not PD, 2 non-finite, 4 peer timeout; sweeps}, workspace
  *   peer    : ngpu device pointers, rank h's exchange buffer as mapped in this
- *             process (tp_als_xg_peer_bytes each, zeroed once at allocation)
- *   seq     : call sequence number >= 1, identical on all ranks, increasing
+ *             process (tp_als_xg_peer_bytes each, zeroed once at allocation and
+ *             reused by every later call of the same ranks and sizes)
  * ------------------------------------------------------------------------- */
 size_t tp_als_xg_ws_bytes(int d, const int* q, int R_local, int r, int ngpu, int ngroups);
 size_t tp_als_xg_peer_bytes(int d, const int* q, int R_local, int r, int ngpu, int ngroups);
@@ -233,8 +233,7 @@ size_t tp_als_xg_peer_bytes(int d, const int* q, int R_local, int r, int ngpu, i
 int tp_als_xg_plan(int d, const int* q, int R_local, int r, int ngpu, int ngroups, int* out);
 int tp_als_xg_f64(int d, const int* q, int R_local, int r, int sweeps, double reg, int reg_mode,
                   int ngroups, const double* const* V, double* const* U, int* const* info,
-                  void* const* ws, size_t ws_bytes, int ngpu, int rank0, void* const* peer,
-                  long long seq, void* stream);
+                  void* const* ws, size_t ws_bytes, int ngpu, int rank0, void* const* peer, void* stream);
 /* device memory shared between ranks: cudaMalloc'd and zeroed, exported/imported
  * as 64-byte CUDA IPC handles (exchanged by the caller, e.g. all_gather_object) */
 int tp_dev_alloc(size_t bytes, void** ptr);

@@ -73,8 +73,7 @@ _SIGNATURES = {
     "tp_als_xg_ws_bytes": (_sz, [_i, _c_int_p, _i, _i, _i, _i]),
     "tp_als_xg_peer_bytes": (_sz, [_i, _c_int_p, _i, _i, _i, _i]),
     "tp_als_xg_plan": (_i, [_i, _c_int_p, _i, _i, _i, _i, _c_int_p]),
-    "tp_als_xg_f64": (_i, [_i, _c_int_p, _i, _i, _i, _d, _i, _i, _vp, _vp, _vp, _vp, _sz, _i, _i, _vp,
-                           ctypes.c_longlong, _vp]),
+    "tp_als_xg_f64": (_i, [_i, _c_int_p, _i, _i, _i, _d, _i, _i, _vp, _vp, _vp, _vp, _sz, _i, _i, _vp, _vp]),
     "tp_dev_alloc": (_i, [_sz, _vp]),
     "tp_dev_free": (_i, [_vp]),
     "tp_ipc_handle": (_i, [_vp, _vp]),

@@ -2113,13 +2113,13 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
 // by mode-update parity: a rank can run one mode update ahead of a peer that is
 // still reading.
 //
-// The cross-GPU barrier: a GPU-local counter barrier, then the group leader
-// publishes a 64-bit tag into every rank's flag slot (st.release.sys through
-// the peer mapping), waits for all ranks' tags in its own slots
-// (ld.acquire.sys), and releases its group through a local go word.  Tags grow
-// monotonically across launches (seq << 20 | barrier index), so no flag is ever
-// reset while a peer may write it.  A 5 s spin limit turns a missing peer into
-// status bit 4 instead of a hung GPU.
+// The cross-GPU barrier: every CTA of every rank adds one arrival to EVERY
+// rank's 64-bit arrival counter (red.release.sys through the peer mapping) and
+// polls its own rank's counter (ld.acquire.sys) -- one hop, like the single-GPU
+// grid barrier.  The counters are never reset (a fast peer may already be
+// counting the next launch): each launch reads its starting value from a word
+// its own previous launch left in the buffer header.  A 5 s spin limit turns a
+// missing peer into status bit 4 instead of a hung GPU.
 //
 // One launch may also hold several groups ("virtual ranks") of CTAs: the
 // single-GPU test of the exchange path, co-resident by the cooperative launch.
@@ -2137,13 +2137,12 @@ struct XgGroup {
 struct XgArgs {
   int ngroups, ngpu, rank0, Pg;
   int CH;                                  // partial slices per staged chunk (two chunk slots)
-  unsigned long long seq_base;
   long long yhalf;                         // doubles of one parity half of Y
   XgGroup grp[TP_MAXG];
-  unsigned char* peer[TP_MAXG];            // every rank's exchange buffer (flags | go | Y[2])
+  unsigned char* peer[TP_MAXG];            // every rank's exchange buffer (arrival counter | Y[2])
 };
 
-constexpr int XG_HDR = 512;   // bytes: u64 flags[TP_MAXG], u64 go at [TP_MAXG]
+constexpr int XG_HDR = 512;   // bytes: u64 arrival counter at [0], u64 its value after this rank's last launch at [1]
 
 __device__ __forceinline__ unsigned long long ld_acq_sys_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -2161,39 +2160,21 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// all CTAs of all ranks (bar: this group's counter, Pg CTAs per group)
-__device__ __forceinline__ void xg_barrier(const XgArgs& x, int g, int p, unsigned int* bar, unsigned int& epoch,
+// all CTAs of all ranks; xn counts this launch's cross barriers, base is the
+// counter value at launch start
+__device__ __forceinline__ void xg_barrier(const XgArgs& x, int g, unsigned long long base, unsigned int& xn,
                                            int& status) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    ++epoch;
-    const unsigned int target = epoch * (unsigned)x.Pg;
-    const unsigned long long tag = x.seq_base + epoch;
-    const int rank = x.rank0 + g;
-    unsigned long long* myflags = reinterpret_cast<unsigned long long*>(x.peer[rank]);
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+    ++xn;
+    const unsigned long long target = base + (unsigned long long)xn * (unsigned long long)(x.Pg * x.ngpu);
+    const unsigned long long* mine = reinterpret_cast<const unsigned long long*>(x.peer[x.rank0 + g]);
+    __threadfence();   // this CTA's partials (gathered by bar.sync) before the system-scope release
+    for (int h = 0; h < x.ngpu; ++h)
+      asm volatile("red.release.sys.global.add.u64 [%0], 1;\n" ::"l"(x.peer[h]) : "memory");
     const unsigned long long t0 = globaltimer();
-    bool late = false;
-    if (p == 0) {
-      unsigned int v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
-        if (globaltimer() - t0 > 5000000000ull) { late = true; break; }
-      } while ((int)(v - target) < 0);
-      __threadfence_system();
-      for (int h = 0; h < x.ngpu; ++h) {
-        unsigned long long* slot = reinterpret_cast<unsigned long long*>(x.peer[h]) + rank;
-        asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(slot), "l"(tag) : "memory");
-      }
-      for (int h = 0; h < x.ngpu && !late; ++h)
-        while (ld_acq_sys_u64(myflags + h) < tag)
-          if (globaltimer() - t0 > 5000000000ull) { late = true; break; }
-      asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(myflags + TP_MAXG), "l"(tag) : "memory");
-    } else {
-      while (ld_acq_gpu_u64(myflags + TP_MAXG) < tag)
-        if (globaltimer() - t0 > 5000000000ull) { late = true; break; }
-    }
-    if (late) status |= 4;
+    while (ld_acq_sys_u64(mine) < target)
+      if (globaltimer() - t0 > 5000000000ull) { status |= 4; break; }
   }
   __syncthreads();
 }
@@ -2233,7 +2214,8 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_xg(const __grid_constant__ AlsA
   const int r = a.r, R = a.R, rr = r * r, rh = pad4(r), ldw = a.ldw;
   const int c0 = (int)((long long)R * cid / Pr), c1 = (int)((long long)R * (cid + 1) / Pr), w = c1 - c0;
   const int w4 = (w + 3) / 4 * 4;
-  unsigned int epoch = 0;   // arrivals on this group's counter (both barrier kinds); xg tags derive from it
+  unsigned int epoch = 0, xn = 0;   // group-barrier epochs, cross barriers of this launch
+  const unsigned long long xbase = __ldcg(reinterpret_cast<const unsigned long long*>(x.peer[rank]) + 1);
   int status = 0;
   uint32_t bphase = 0, gphase = 0, xphase = 0, xpf = 0, b3phase = 0;
   if (tid == 0) {
@@ -2296,7 +2278,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_xg(const __grid_constant__ AlsA
       }
       const int Qj = a.q[j];
       cl_had_y<RM>(a, sm, j, w, b, cid, Pr, Ymine + (size_t)par * x.yhalf);
-      xg_barrier(x, g, p, barg, epoch, status);   // every rank's partials of mode j are written
+      xg_barrier(x, g, xbase, xn, status);   // every rank's partials of mode j are written
       // ---------------- phase B: rows [s0, s1) of mode j from all ranks' partials
       const int s0 = (int)((long long)Qj * p / P), s1 = (int)((long long)Qj * (p + 1) / P);
       const int ncol = s1 - s0, E = ncol * r;
@@ -2363,7 +2345,10 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_xg(const __grid_constant__ AlsA
   }
   // no rank may leave (and reuse its exchange buffer in the next launch) while a
   // peer can still read its partials
-  xg_barrier(x, g, p, barg, epoch, status);
+  xg_barrier(x, g, xbase, xn, status);
+  if (p == 0 && tid == 0)   // every CTA of this launch has read xbase (it passed the barrier above)
+    reinterpret_cast<unsigned long long*>(x.peer[rank])[1] =
+        xbase + (unsigned long long)xn * (unsigned long long)(x.Pg * x.ngpu);
   if (status && tid == 0) atomicOr(gr.info, status);
   if (p == 0 && tid == 0) gr.info[1] = a.sweeps;
   cl.sync();
@@ -3047,10 +3032,8 @@ int tp_als_xg_plan(int d, const int* q, int R_local, int r, int ngpu, int ngroup
 
 int tp_als_xg_f64(int d, const int* q, int R_local, int r, int sweeps, double reg, int reg_mode,
                   int ngroups, const double* const* V, double* const* U, int* const* info,
-                  void* const* ws, size_t ws_bytes, int ngpu, int rank0, void* const* peer,
-                  long long seq, void* stream) {
-  if (!V || !U || !info || !ws || !peer || sweeps < 0 || !(reg >= 0.0) || rank0 < 0 || rank0 + ngroups > ngpu ||
-      seq < 1)
+                  void* const* ws, size_t ws_bytes, int ngpu, int rank0, void* const* peer, void* stream) {
+  if (!V || !U || !info || !ws || !peer || sweeps < 0 || !(reg >= 0.0) || rank0 < 0 || rank0 + ngroups > ngpu)
     return TP_EINVAL;
   XgPlan xp;
   int st = plan_xg(d, q, R_local, r, ngpu, ngroups, xp);
@@ -3063,7 +3046,6 @@ int tp_als_xg_f64(int d, const int* q, int R_local, int r, int sweeps, double re
   XgArgs x;
   memset(&x, 0, sizeof(x));
   x.ngroups = ngroups; x.ngpu = ngpu; x.rank0 = rank0; x.Pg = xp.Pg; x.CH = xp.CH;
-  x.seq_base = (unsigned long long)seq << 20;
   x.yhalf = xp.yhalf;
   for (int h = 0; h < ngpu; ++h) x.peer[h] = static_cast<unsigned char*>(peer[h]);
   long long nup = 0;

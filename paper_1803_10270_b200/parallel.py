@@ -192,7 +192,8 @@ class FusedShardedALS:
     rank runs the cluster ALS kernel on its R-slab; the per-mode-update r x Q
     right-hand-side exchange happens inside the kernel through peer-mapped
     exchange buffers (CUDA IPC handles swapped once with all_gather_object) and an
-    in-kernel cross-GPU barrier -- no host round trip or NCCL call per mode update.
+    in-kernel cross-GPU barrier (one system-scope arrival per CTA on every rank's counter) -- no
+    host round trip or NCCL call per mode update.
     Every rank ends with the identical (bitwise) fit."""
 
     def __init__(self, V_local: CPTensor, r: int, config: ALSApproxConfig | None = None, group=None):
@@ -234,7 +235,6 @@ class FusedShardedALS:
                 self._opened.append(p2.value)
                 peers.append(p2.value)
         self._peers = (ctypes.c_void_p * self.world)(*peers)
-        self.seq = 0
         self.group = group
         plan = (ctypes.c_int * 4)()
         _lib.check(L.tp_als_xg_plan(self.d, self.qs, V_local.rank, r, self.world, 1, plan), "plan")
@@ -248,13 +248,12 @@ class FusedShardedALS:
         V = V or self.V
         if V.rank != self.V.rank or V.qs != self.V.qs:
             raise ValueError("slab shape differs from the planned one")
-        self.seq += 1
         reg, mode = (1e-12, 1) if self.cfg.reg is None else (float(self.cfg.reg), 0)
         one = lambda v: (ctypes.c_void_p * 1)(v)   # noqa: E731
         st = self.L.tp_als_xg_f64(self.d, self.qs, V.rank, self.r, int(self.cfg.max_sweeps), reg, mode, 1,
                                   one(V.data.data_ptr()), one(U.data_ptr()), one(self.info.data_ptr()),
                                   one(self.ws.data_ptr()), self.ws.numel(), self.world, self.rank, self._peers,
-                                  self.seq, _lib.stream_ptr(U.device))
+                                  _lib.stream_ptr(U.device))
         _lib.check(st, "sharded cp_approx_als")
         return U
 
@@ -264,7 +263,7 @@ class FusedShardedALS:
     def describe(self) -> str:
         return (f"one fused launch per GPU: {self.plan['clusters']} clusters x {self.plan['cluster']} CTAs on the "
                 f"rank's R-slab, in-kernel exchange of the r x Q partials through peer-mapped memory, cross-GPU "
-                f"flag barrier once per mode update")
+                f"counter barrier once per mode update")
 
     def kernel_name(self) -> str:
         return f"tp::als_xg<32> ({self.plan['ctas']} CTAs per GPU, cluster {self.plan['cluster']})"
@@ -384,7 +383,7 @@ def simulate_sharded_als(V_factors, init_factors, shards: int, config: ALSApprox
     arr = lambda ts: (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])   # noqa: E731
     reg, mode = (1e-12, 1) if cfg.reg is None else (float(cfg.reg), 0)
     st = L.tp_als_xg_f64(d, qa, Rl, r, int(cfg.max_sweeps), reg, mode, shards, arr([v.data for v in Vs]), arr(Us),
-                         arr(infos), arr(wss), nws, shards, 0, arr(peers), 1, _lib.stream_ptr(dev))
+                         arr(infos), arr(wss), nws, shards, 0, arr(peers), _lib.stream_ptr(dev))
     _lib.check(st, "simulated sharded ALS")
     for inf in infos:
         _check_xg_info(inf)
