@@ -5,7 +5,7 @@ SURVEY 8(c)): ``pairs[k][e, z] = A_{e,k}^T A_{z,k}`` is the discrete bilinear
 pairing that ``pair_matrix`` (basis.py:207-214) computes in closed form for the
 Galerkin basis.  ``orientation="reference"`` reproduces ``build_gamma``
 verbatim (implicit.py:134-153, which pairs the old iterate with the A-side
-index); ``orientation="corrected"`` is shim S7 (the normal equations of
+index; forcing block implicit.py:140-152); ``orientation="corrected"`` is shim S7 (the normal equations of
 ``min |A f_new - B f_old|^2``).  Solves are direct ``(M + lam I)`` solves
 (shim S6, replacing LSQR at implicit.py:156-164).
 """
@@ -55,8 +55,22 @@ def build_M(q, beta_new, tables):
     return m.reshape(r * qq, r * qq)
 
 
-def build_gamma(q, beta_new, beta_old, tables, orientation="corrected"):
-    """implicit.py:134-139 (no forcing)."""
+def forcing_block(q, beta_new, tables, forcing, dt):
+    """implicit.py:140-152: dt * sum_e eta_e sum_m (prod_{k!=q} beta_k^T S^e_k c_k)[i,m] (S^e_q c_q)[a,m],
+    with the source tables S^e_k = pair(E_e, I) (here A_{e,k}^T)."""
+    eta = tables["eta"]
+    proj = [np.einsum("esh,hm->esm", tables["source"][k], forcing[k], optimize=True) for k in range(len(beta_new))]
+    r = beta_new[q].shape[1]
+    rows = np.ones((len(eta), r, forcing[0].shape[1]))
+    for k in range(len(beta_new)):
+        if k == q:
+            continue
+        rows = rows * np.einsum("si,esm->eim", beta_new[k], proj[k], optimize=True)
+    return dt * np.einsum("e,eim,eam->ia", eta, rows, proj[q], optimize=True)
+
+
+def build_gamma(q, beta_new, beta_old, tables, orientation="corrected", forcing=None, dt=0.0):
+    """implicit.py:134-153 (forcing block: forcing_block)."""
     if orientation == "reference":
         had = term_grams(tables, beta_old, beta_new, q)
         gam = np.einsum("ez,ezji,ezca,cj->ia", tables["KR"], had, tables["pairs"][q],
@@ -67,6 +81,8 @@ def build_gamma(q, beta_new, beta_old, tables, orientation="corrected"):
                         beta_old[q], optimize=True)
     else:
         raise ValueError(orientation)
+    if forcing is not None:
+        gam = gam + forcing_block(q, beta_new, tables, forcing, dt)
     return gam.reshape(-1)
 
 
@@ -81,8 +97,9 @@ def converged(beta_int, beta_new):
 
 
 def step(f_n, tables, sweeps, lam, schedule="gauss-seidel", delta_beta=1.0, eps_tol=0.0,
-         orientation="corrected"):
-    """implicit.py:222-298 with direct solves; returns (factors, sweeps_done, eps_conv)."""
+         orientation="corrected", forcing=None, dt=0.0):
+    """implicit.py:222-298 with direct solves; returns (factors, sweeps_done, eps_conv).
+    ``forcing``: list of (Q_k, R_f) factors of the source term, scaled by ``dt``."""
     n = len(f_n)
     r = f_n[0].shape[1]
     beta_old = [fk.copy() for fk in f_n]
@@ -96,7 +113,7 @@ def step(f_n, tables, sweeps, lam, schedule="gauss-seidel", delta_beta=1.0, eps_
         for q in range(n):
             bn = beta_int if schedule == "jacobi" else beta_new
             m = build_M(q, bn, tables)
-            gam = build_gamma(q, bn, beta_old, tables, orientation)
+            gam = build_gamma(q, bn, beta_old, tables, orientation, forcing, dt)
             x = np.linalg.solve(m + lam * np.eye(m.shape[0]), gam)
             bq = x.reshape(r, -1).T                      # _unvec, implicit.py:218-219
             if schedule == "jacobi":

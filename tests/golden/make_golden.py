@@ -308,6 +308,77 @@ def gen_implicit():
     np.savez_compressed(OUT / "implicit.npz", **store)
 
 
+def gen_implicit_forced():
+    """Forced implicit steps through the reference ``implicit.step`` (forcing block
+    implicit.py:140-152) with S5/S6: Gauss-Seidel (4 fixed sweeps) and the reference
+    default Jacobi schedule (delta_beta = 4, eps_tol = 1e-4 -> the convergence stop),
+    each in the reference orientation (native build_gamma) and the corrected one
+    (S7 for the b_old block; the forcing block is the reference's own, taken as
+    build_gamma(forcing) - build_gamma(None))."""
+    store = {}
+    rng = np.random.default_rng(43)
+    q, d, r, rf, dt, lam = 6, 3, 2, 2, 5e-2, 1e-10
+    specs = tuple(spec(q) for _ in range(d))
+    D = fourier_diff_matrix(q)
+    a = np.array([1.0, 0.5, -0.75])
+    mats = [[None] * d] + [[D if k == i else None for k in range(d)] for i in range(d)]
+    eta = (1.0,) + tuple(dt * a)
+    zeta = (1.0,) + (0.0,) * d
+    ra = len(eta)
+    pairs, source = [], []
+    for k in range(d):
+        full = [np.eye(q) if mats[e][k] is None else mats[e][k] for e in range(ra)]
+        pairs.append(np.array([[full[e].T @ full[z] for z in range(ra)] for e in range(ra)], dtype=complex))
+        source.append(np.array([full[e].T for e in range(ra)], dtype=complex))
+    eta_c = np.asarray(eta, dtype=complex)
+    zeta_c = np.asarray(zeta, dtype=complex)
+    L = operators.SeparableOperator(specs, tuple(-a), tuple(tuple(FactorKind.DERIVATIVE if k == i else FactorKind.IDENTITY
+                                                                   for k in range(d)) for i in range(d)))
+    pair = operators.CrankNicolsonPair(specs, dt, eta, zeta, tuple(tuple(FactorKind.IDENTITY for _ in range(d))
+                                                                   for _ in range(ra)), L)
+    tables = implicit.OperatorTables(pair, pairs, source, np.outer(eta_c, eta_c), np.outer(eta_c, zeta_c))
+    f0 = real_cp(specs, r, rng)
+    forcing = real_cp(specs, rf, rng, 0.5)
+    orig_solve, orig_gamma = implicit.solve_beta, implicit.build_gamma
+
+    def direct(M, gamma, beta_init, config):                     # S6
+        return np.linalg.solve(M + lam * np.eye(M.shape[0]), gamma), 0, 0.0
+
+    def gamma_fixed(qq, beta_new, beta_old, tab, forcing=None):  # S7 + the reference forcing block
+        had = implicit._term_grams(tab, beta_new, beta_old, qq)
+        gam = np.einsum("ez,ezij,ezac,cj->ia", tab.KR, had, tab.pairs[qq], beta_old[qq], optimize=True).reshape(-1)
+        if forcing is not None:
+            gam = gam + (orig_gamma(qq, beta_new, beta_old, tab, forcing) - orig_gamma(qq, beta_new, beta_old, tab))
+        return gam
+
+    cases = {"gs": dict(eps_tol=0.0, max_sweeps=4, delta_beta=1.0, schedule="gauss-seidel"),
+             "jac": dict(eps_tol=1e-4, max_sweeps=60, delta_beta=4.0, schedule="jacobi")}
+    implicit.solve_beta = direct
+    try:
+        for name, kw in cases.items():
+            cfg = implicit.ALSStepConfig(dt=dt, **kw)
+            ws = object.__new__(implicit.StepWorkspace)
+            ws.pair, ws.config, ws.tables, ws._pool = pair, cfg, tables, None
+            log_r, log_c = {}, {}
+            implicit.build_gamma = orig_gamma
+            out_ref = implicit.step(f0, pair, forcing, cfg, workspace=ws, log=log_r)
+            implicit.build_gamma = gamma_fixed
+            out_fix = implicit.step(f0, pair, forcing, cfg, workspace=ws, log=log_c)
+            pack_cp(f"{name}_out_reference_orientation", out_ref, store)
+            pack_cp(f"{name}_out_corrected", out_fix, store)
+            store[f"{name}_sweeps"] = np.array([log_r["sweeps"], log_c["sweeps"]])
+            store[f"{name}_cfg"] = np.array([kw["eps_tol"], kw["max_sweeps"], kw["delta_beta"],
+                                             1.0 if kw["schedule"] == "jacobi" else 0.0])
+    finally:
+        implicit.solve_beta, implicit.build_gamma = orig_solve, orig_gamma
+    pack_cp("f0", f0, store)
+    pack_cp("forcing", forcing, store)
+    store["meta"] = np.array([q, d, r, dt, lam])
+    store["D"] = D
+    store["a"] = a
+    np.savez_compressed(OUT / "implicit_forced.npz", **store)
+
+
 def gen_io():
     """Reference-written tensor files (io.save_tensor, io.py:55-71) + their decoded arrays."""
     from tensorpde import io as rio
@@ -388,7 +459,8 @@ def gen_complex():
 
 GENERATORS = {"cp_als": lambda: gen_cp_als(), "ht": lambda: gen_ht(), "operators": lambda: gen_operators(),
               "explicit": lambda: gen_explicit(), "implicit": lambda: gen_implicit(), "io": lambda: gen_io(),
-              "diagnostics": lambda: gen_diagnostics(), "complex": lambda: gen_complex()}
+              "diagnostics": lambda: gen_diagnostics(), "complex": lambda: gen_complex(),
+              "implicit_forced": lambda: gen_implicit_forced()}
 
 
 if __name__ == "__main__":

@@ -142,3 +142,24 @@ def test_complex_rank_reduce_and_split_recipe_golden():
         traj.append(oex.ab2_split(traj[-2], traj[-1], w, mats, 1e-2, 3, red))
     for n, f in enumerate(traj):
         assert metrics.cp_rel_diff(unpack_cp(g, f"ex_step{n}"), f) <= 1e-10, n
+
+
+def test_implicit_forced_step_golden():
+    """Forced steps (implicit.py:140-152) of the real reference: Gauss-Seidel with fixed
+    sweeps and the default Jacobi schedule (delta_beta = 4) stopping on eps_tol, both
+    orientations; the oracle reproduces the sweep counts and the states."""
+    g = load_golden("implicit_forced")
+    q, d, r, dt, lam = g["meta"]
+    d = int(d)
+    D, a = g["D"], g["a"]
+    mats = [[None] * d] + [[D if k == i else None for k in range(d)] for i in range(d)]
+    tables = implicit.build_tables(mats, [1.0] + list(dt * a), [1.0] + [0.0] * d, [int(q)] * d)
+    f0, force = unpack_cp(g, "f0"), unpack_cp(g, "forcing")
+    for case in ("gs", "jac"):
+        eps_tol, max_sweeps, delta_beta, jac = g[f"{case}_cfg"]
+        for i, (orient, key) in enumerate((("reference", "out_reference_orientation"), ("corrected", "out_corrected"))):
+            out, done, _ = implicit.step(f0, tables, int(max_sweeps), lam, "jacobi" if jac else "gauss-seidel",
+                                         float(delta_beta), float(eps_tol), orient, forcing=force, dt=float(dt))
+            assert done == int(g[f"{case}_sweeps"][i]), (case, orient, done)
+            rel = metrics.cp_rel_diff(unpack_cp(g, f"{case}_{key}"), out)
+            assert rel < 1e-11, (case, orient, rel)
