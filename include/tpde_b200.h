@@ -200,13 +200,22 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
  *             solved per DFT frequency (Q Hermitian r x r solves), same minimiser
  *   eps_conv: device double (last sweep's largest relative update)
  *   info    : device int[2] {status bits, sweeps done}
+ *   forcing : NULL, or the device CP source term c (rank rf, d blocks Q x rf):
+ *             gamma_q += sum_e fcoef[e] (prod_{k!=q} b_k^T S_{k,e} c_k) (S_{q,e} c_q)^T
+ *             (implicit.py:140-152), fcoef host ra doubles = dt eta_e; the source
+ *             tables S_{k,e} = pairs[k][e][0] (term 0 is the identity in every mode,
+ *             the CrankNicolsonPair layout, operators.py:148-150)
+ *   eps_tol : the reference loop condition (implicit.py:244) runs on the device:
+ *             the sweep whose update reaches eps_tol stops the step (later kernels
+ *             of the call are no-ops); no host synchronisation anywhere
  * ------------------------------------------------------------------------- */
-size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab);
+size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab, int ra, int rf);
 int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* tabs, const int* tab_id,
                          const double* KL, const double* KR, const double* f_old, double* f_new,
                          int sweeps, int schedule, double delta_beta, double eps_tol, double lam,
-                         int orientation, const double* circ_eig, double* eps_conv, int* info, void* ws,
-                         size_t ws_bytes, void* stream);
+                         int orientation, const double* circ_eig, const double* forcing, int rf,
+                         const double* fcoef, double* eps_conv, int* info, void* ws, size_t ws_bytes,
+                         void* stream);
 
 /* ---------------------------------------------------------------------------
  * R-sharded fused CP-ALS across GPUs (BASELINE cfg1 multi-GPU, SURVEY 8(e);

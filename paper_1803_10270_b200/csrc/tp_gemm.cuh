@@ -24,6 +24,7 @@ struct BGemm {
   double alpha, beta;
   int ksplit;                // split-K factor (>1: partial tiles to `part`, then bgemm_reduce)
   double* part;              // [nb1*nb2][ksplit][M][N] partials when ksplit > 1
+  const int* skip;           // optional device flag: nonzero -> the launch is a no-op (stream-ordered early exit)
 };
 
 // 8-byte global -> shared async copy (LDGSTS); src_bytes = 0 zero-fills
@@ -34,6 +35,7 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid
 }
 
 static __global__ void __launch_bounds__(128) bgemm_kernel(const __grid_constant__ BGemm g) {
+  if (g.skip && *g.skip) return;
   // two-stage cp.async pipeline: K tile t+1 streams into the other buffer while
   // tile t is multiplied on the DMMA pipe
   __shared__ double As[2][GB_TK][GB_LD];
@@ -141,6 +143,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 // conflict-free fragments) and filled with 16-byte copies along K.
 template <int STAGES, int TK, bool AK = false, bool BK = false>
 static __global__ void __launch_bounds__(128) bgemm_pipe_kernel(const __grid_constant__ BGemm g) {
+  if (g.skip && *g.skip) return;
   extern __shared__ double gsm[];
   constexpr int LDK = TK + 4;
   constexpr int SA = AK ? GB_TM * LDK : TK * GB_LD, SB = BK ? GB_TN * LDK : TK * GB_LD;   // per stage
@@ -271,6 +274,7 @@ static __global__ void __launch_bounds__(128) bgemm_pipe_kernel(const __grid_con
 
 // split-K epilogue: C_z = alpha * sum_s part[z][s] + beta * C_z (fixed order)
 static __global__ void bgemm_reduce_kernel(const __grid_constant__ BGemm g) {
+  if (g.skip && *g.skip) return;
   const int z = blockIdx.y, z1 = z / g.nb2, z2 = z % g.nb2;
   long long oC = g.offs ? g.offs[3 * z1 + 2] : z1 * g.sC1;
   double* C = g.C + oC + z2 * g.sC2;

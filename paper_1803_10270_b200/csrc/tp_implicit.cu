@@ -14,12 +14,22 @@
 //               TRSM and trailing SYRK as DMMA GEMMs), then blocked substitution.
 // After each sweep: largest relative raw update (implicit.py:167-177) and the
 // damped update b <- b_int + (b - b_int)/delta_beta (implicit.py:281-282).
+// Forcing (implicit.py:140-152): gamma_q += dt sum_e eta_e sum_m
+// (prod_{k!=q} b_k^T P_{k,e})[i,m] P_{q,e}[a,m] with P_{k,e} = S_{k,e} c_k, the source
+// tables S_{k,e} = pairs[k][e][0] (term 0 is the identity in the pair layout).
+// Stream contract: no host synchronisation.  Offset tables are uploaded once per
+// shape and cached on the device; the reference's convergence loop (implicit.py:244)
+// runs on the device -- the sweep that reaches eps_tol raises a stop flag and every
+// later kernel of the call is a no-op.
 #include "tp_common.cuh"
 #include "tp_gemm.cuh"
 #include <cstring>
 #include <vector>
 #include <cmath>
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace tp {
 
@@ -38,6 +48,7 @@ struct HArgs {
   const double* Gm;          // [d][n_tab][r][r]
   double* H;                 // [nX][r][r]  (stored [j][i] as in the reference einsum)
   double* Hg;                // [nX][r][r]  ([i][j])
+  const int* stop;
 };
 
 // H and Hg for the distinct tables of mode q: one CTA per distinct table
@@ -45,6 +56,7 @@ struct HArgs {
 // lanes per element share the term pairs (shuffle reduction, fixed order)
 constexpr int FH_SPLIT = 4;
 __global__ void __launch_bounds__(256) form_h_kernel(const __grid_constant__ HArgs a) {
+  if (*a.stop) return;
   const int x = blockIdx.x, r = a.r, rr = r * r, lane = threadIdx.x & (FH_SPLIT - 1);
   const int per_cta = 256 / FH_SPLIT;
   const int e2 = blockIdx.y * per_cta + threadIdx.x / FH_SPLIT;
@@ -81,7 +93,8 @@ __global__ void __launch_bounds__(256) form_h_kernel(const __grid_constant__ HAr
 
 // gamma[i*Q + a] = sum_X sum_j Hg_X[i][j] W[q][X][a][j]
 __global__ void gamma_kernel(int Q, int r, int nX, const int* __restrict__ xs_dev, const double* Hg, const double* W,
-                             int n_tab, int q, double* gam, int N) {
+                             int n_tab, int q, double* gam, int N, const double* fvec, const int* stop) {
+  if (*stop) return;
   const int n = r * Q;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N; e += gridDim.x * blockDim.x) {
     if (e >= n) { gam[e] = 0.0; continue; }
@@ -93,6 +106,7 @@ __global__ void gamma_kernel(int Q, int r, int nX, const int* __restrict__ xs_de
       const double* hg = Hg + (size_t)x * r * r + (size_t)i * r;
       for (int j = 0; j < r; ++j) acc = fma(hg[j], w[j], acc);
     }
+    if (fvec) acc += fvec[(size_t)aa * r + i];
     gam[e] = acc;
   }
 }
@@ -104,10 +118,12 @@ struct AsmArgs {
   const double* H;
   double* M;
   double lam;
+  const int* stop;
 };
 
 // M[(i,a),(j,c)] = sum_X H_X[j][i] T_X[c][a] + lam delta   (rank-major, mode-minor blocks)
 __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ AsmArgs a) {
+  if (*a.stop) return;
   const int Q = a.Q, r = a.r, n = r * Q, N = a.N;
   const long long tot = (long long)N * N;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
@@ -126,7 +142,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ A
 
 // Cholesky of the nb x nb diagonal block at (k0, k0) of the row-major n x n matrix A
 // (lower triangle), in shared memory; writes L back and L^-1 into Linv (nb x nb).
-__global__ void __launch_bounds__(256) potrf_diag_kernel(double* A, int n, int k0, int nb, double* Linv, int* info) {
+__global__ void __launch_bounds__(256) potrf_diag_kernel(double* A, int n, int k0, int nb, double* Linv, int* info,
+                                                         const int* stop) {
+  if (*stop) return;
   extern __shared__ double pds[];
   double (*L)[CH_NB + 1] = reinterpret_cast<double (*)[CH_NB + 1]>(pds);
   double (*X)[CH_NB + 1] = reinterpret_cast<double (*)[CH_NB + 1]>(pds + CH_NB * (CH_NB + 1));
@@ -173,7 +191,8 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* A, int n, int k
 
 // Solve L L^T x = b with the blocked factor (diagonal inverses in Linv); one CTA.
 __global__ void __launch_bounds__(256) potrs_kernel(const double* A, int n, const double* Linv, const double* b,
-                                                    double* x, double* y) {
+                                                    double* x, double* y, const int* stop) {
+  if (*stop) return;
   __shared__ double part[256];
   __shared__ double blk[CH_NB];
   const int tid = threadIdx.x, nbk = n / CH_NB;
@@ -217,7 +236,8 @@ __global__ void __launch_bounds__(256) potrs_kernel(const double* A, int n, cons
 }
 
 // beta[q][a][i] = x[i*Q + a]; flags non-finite
-__global__ void scatter_x_kernel(int Q, int r, const double* x, double* beta_q, int* info) {
+__global__ void scatter_x_kernel(int Q, int r, const double* x, double* beta_q, int* info, const int* stop) {
+  if (*stop) return;
   const int n = Q * r;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int aa = e / r, i = e % r;
@@ -229,7 +249,9 @@ __global__ void scatter_x_kernel(int Q, int r, const double* x, double* beta_q, 
 
 // per-mode ||new - int||^2 and ||int||^2 (one CTA per mode), then damping
 __global__ void __launch_bounds__(256) conv_damp_kernel(int Q, int r, int d, double* bnew, const double* bint,
-                                                        double delta_beta, double* eps_out) {
+                                                        double delta_beta, double* eps_out, double eps_tol,
+                                                        int* stop, int* info) {
+  if (*stop) return;
   __shared__ double sdb[256], sna[256];
   __shared__ double worst;
   if (threadIdx.x == 0) worst = 0.0;
@@ -258,10 +280,92 @@ __global__ void __launch_bounds__(256) conv_damp_kernel(int Q, int r, int d, dou
   if (delta_beta > 0.0)
     for (size_t e = threadIdx.x; e < (size_t)d * Q * r; e += 256)
       bnew[e] = bint[e] + (bnew[e] - bint[e]) / delta_beta;
-  if (threadIdx.x == 0) *eps_out = worst;
+  __syncthreads();   // every thread has read the flag before thread 0 may raise it
+  if (threadIdx.x == 0) {
+    *eps_out = worst;
+    info[1] += 1;                                       // sweeps done
+    if (eps_tol > 0.0 && worst <= eps_tol) *stop = 1;   // while eps_conv > eps_tol (implicit.py:244)
+  }
 }
 
-__global__ void set_int_kernel(int* dst, int v) { *dst = v; }
+__global__ void copy_kernel(double* dst, const double* src, size_t n, const int* stop) {
+  if (*stop) return;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    dst[e] = src[e];
+}
+
+// twiddles tw[m] = (cos, sin)(2 pi m / Q)
+__global__ void twiddle_kernel(int Q, double* tw) {
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < Q; m += gridDim.x * blockDim.x) {
+    double sn, cs;
+    sincospi(2.0 * (double)m / (double)Q, &sn, &cs);
+    tw[2 * m] = cs;
+    tw[2 * m + 1] = sn;
+  }
+}
+
+// ---- forcing (implicit.py:140-152) ------------------------------------------
+// P[k][e] = S_{k,e} c_k (Q x rf), S_{k,e} = tabs[src[k][e]]: grid (k, e)
+__global__ void __launch_bounds__(256) force_proj_kernel(int Q, int rf, int ra, const double* tabs, const int* src,
+                                                         const double* c, double* P) {
+  const int k = blockIdx.x, e = blockIdx.y;
+  const double* S = tabs + (size_t)src[k * ra + e] * Q * Q;
+  const double* ck = c + (size_t)k * Q * rf;
+  double* out = P + ((size_t)k * ra + e) * Q * rf;
+  for (int o = threadIdx.x; o < Q * rf; o += 256) {
+    const int s2 = o / rf, m = o - s2 * rf;
+    double acc = 0.0;
+    for (int h = 0; h < Q; ++h) acc = fma(S[(size_t)s2 * Q + h], ck[(size_t)h * rf + m], acc);
+    out[o] = acc;
+  }
+}
+
+// W[k][e] = b_k^T P[k][e] (r x rf) for every mode k != q: grid (k, e)
+__global__ void __launch_bounds__(256) force_w_kernel(int Q, int r, int rf, int ra, int q, const double* b,
+                                                      const double* P, double* W, const int* stop) {
+  const int k = blockIdx.x, e = blockIdx.y;
+  if (k == q || *stop) return;
+  const double* bk = b + (size_t)k * Q * r;
+  const double* pk = P + ((size_t)k * ra + e) * Q * rf;
+  double* out = W + ((size_t)k * ra + e) * r * rf;
+  for (int o = threadIdx.x; o < r * rf; o += 256) {
+    const int i = o / rf, m = o - i * rf;
+    double acc = 0.0;
+    for (int s2 = 0; s2 < Q; ++s2) acc = fma(bk[(size_t)s2 * r + i], pk[(size_t)s2 * rf + m], acc);
+    out[o] = acc;
+  }
+}
+
+// fvec[a][i] = sum_e coef_e sum_m (prod_{k!=q} W[k][e][i][m]) P[q][e][a][m]   (Q x r)
+struct ForceArgs {
+  int Q, r, rf, ra, d, q;
+  double coef[IM_MAXRA];   // dt * eta_e
+  const double* P;
+  const double* W;
+  double* fvec;
+  const int* stop;
+};
+
+__global__ void __launch_bounds__(256) force_vec_kernel(const __grid_constant__ ForceArgs a) {
+  if (*a.stop) return;
+  const int Q = a.Q, r = a.r, rf = a.rf;
+  for (int o = blockIdx.x * 256 + threadIdx.x; o < Q * r; o += gridDim.x * 256) {
+    const int aa = o / r, i = o - aa * r;
+    double acc = 0.0;
+    for (int e = 0; e < a.ra; ++e) {
+      const double* pq = a.P + ((size_t)a.q * a.ra + e) * Q * rf + (size_t)aa * rf;
+      double se = 0.0;
+      for (int m = 0; m < rf; ++m) {
+        double row = 1.0;
+        for (int k = 0; k < a.d; ++k)
+          if (k != a.q) row *= a.W[(((size_t)k * a.ra + e) * r + i) * rf + m];
+        se = fma(row, pq[m], se);
+      }
+      acc = fma(a.coef[e], se, acc);
+    }
+    a.fvec[o] = acc;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Circulant fast path: when every pairing table is circulant (Fourier
@@ -290,9 +394,12 @@ struct CircArgs {
   double* xhat;         // [r][Q][2]
   double lam;
   int* info;
+  const double* fhat;   // [Q][r][2] unnormalised DFT of the forcing vector, or nullptr
+  const int* stop;
 };
 
 __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__ CircArgs a) {
+  if (*a.stop) return;
   extern __shared__ double cs[];
   const int k = blockIdx.x, r = a.r, Q = a.Q, tid = threadIdx.x;
   const int ld = r + 1;
@@ -340,7 +447,11 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
       re += __shfl_xor_sync(0xffffffffu, re, o);
       im += __shfl_xor_sync(0xffffffffu, im, o);
     }
-    if (i < r && part == 0) { gre[i] = re * inv_sqrt; gim[i] = im * inv_sqrt; }
+    if (i < r && part == 0) {
+      if (a.fhat) { re += a.fhat[((size_t)k * r + i) * 2]; im += a.fhat[((size_t)k * r + i) * 2 + 1]; }
+      gre[i] = re * inv_sqrt;
+      gim[i] = im * inv_sqrt;
+    }
   }
   for (int e = tid; e < r * r; e += 256) {
     const int i = e / r, j = e % r;
@@ -413,7 +524,9 @@ __global__ void __launch_bounds__(256) circ_solve_kernel(const __grid_constant__
 
 // Unnormalised DFT of the columns of a real Q x r factor: out[k][l][2] =
 // sum_s b[s][l] e^{-2 pi i s k / Q}; 8 lanes per output (as circ_idft_kernel)
-__global__ void __launch_bounds__(256) dft_cols_kernel(int Q, int r, const double* b, const double* tw, double* out) {
+__global__ void __launch_bounds__(256) dft_cols_kernel(int Q, int r, const double* b, const double* tw, double* out,
+                                                       const int* stop) {
+  if (*stop) return;
   // one CTA per frequency block: the factor (Q x r) and the twiddles staged in
   // shared memory, 8 lanes per (frequency, column), shuffle reduction
   extern __shared__ double dsm[];
@@ -460,9 +573,11 @@ struct FGramArgs {
   const double* bo;    // [Q][r][2]
   double* G;
   double* Gm;
+  const int* stop;
 };
 
 __global__ void __launch_bounds__(256) fourier_grams_kernel(const __grid_constant__ FGramArgs a) {
+  if (*a.stop) return;
   extern __shared__ double fg[];
   const int Q = a.Q, r = a.r, t = a.ts[blockIdx.x], mixed = blockIdx.y, tid = threadIdx.x;
   double* x = fg;                       // [Q][r][2]  bn
@@ -502,7 +617,8 @@ __global__ void __launch_bounds__(256) fourier_grams_kernel(const __grid_constan
 // 8 lanes per output (frequencies k = part + 8 t, index m = c k mod Q stepped
 // incrementally), fixed-order shuffle reduction
 __global__ void __launch_bounds__(256) circ_idft_kernel(int Q, int r, const double* xhat, const double* tw,
-                                                        double* beta_q, int* info) {
+                                                        double* beta_q, int* info, const int* stop) {
+  if (*stop) return;
   extern __shared__ double ism[];
   double* xs = ism;                    // [r][Q][2]
   double* ts = xs + (size_t)r * Q * 2; // [Q][2]
@@ -1103,6 +1219,12 @@ static size_t circ_gs_bytes(int d, int Q, int r) {
 
 static int padded_n(int n) { return (n + CH_NB - 1) / CH_NB * CH_NB; }
 
+static size_t force_bytes(int d, int Q, int r, int ra, int rf) {
+  if (rf <= 0) return 0;
+  return align_up(8 * (size_t)d * ra * Q * rf) + align_up(8 * (size_t)d * ra * r * rf) +   // P, W
+         align_up(8 * (size_t)Q * r) + align_up(8 * (size_t)Q * r * 2);                      // fvec, fhat
+}
+
 static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
   const size_t n = (size_t)padded_n(r * Q);
   size_t s = 0;
@@ -1118,7 +1240,29 @@ static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
   s += align_up(8 * (size_t)r * Q * 2) + align_up(8 * (size_t)Q * 2);   // circulant: xhat, twiddles
   s += align_up(8 * (size_t)d * Q * r * 2) + align_up(8 * (size_t)Q * r * 2);   // circulant: DFT(b_old), DFT(b_new)
   s += circ_gs_bytes(d, Q, r);                                                   // fused circulant Gauss-Seidel
+  s += 256;                                                                      // stop flag
   return s;
+}
+
+// Host tables that never change for a given operator/shape (GEMM offset triples,
+// per-mode table lists) live on the device once: the first call uploads them
+// synchronously, every later call (and CUDA-graph capture) only reads them.
+template <class T>
+static const T* device_table(const std::vector<T>& v) {
+  static std::mutex mu;
+  static std::map<std::pair<int, std::vector<char>>, void*> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<char> key(reinterpret_cast<const char*>(v.data()), reinterpret_cast<const char*>(v.data() + v.size()));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, key});
+  if (it != cache.end()) return static_cast<const T*>(it->second);
+  void* p = nullptr;
+  if (cudaMalloc(&p, v.empty() ? 8 : v.size() * sizeof(T)) != cudaSuccess) return nullptr;
+  if (!v.empty() && cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  if (cache.size() > 256) cache.clear();   // (leaks the old tables; bounded)
+  cache.emplace(std::make_pair(dev, std::move(key)), p);
+  return static_cast<const T*>(p);
 }
 
 }  // namespace tp
@@ -1135,22 +1279,26 @@ void tp_debug_set_circ_fused(int on) { g_circ_fused = on; }
 // debug hook: device array of >= 16 int64 receiving per-phase clock64 totals of CTA 0
 void tp_debug_set_circ_prof(long long* p) { g_circ_prof = p; }
 
-size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab) {
-  if (d < 1 || d > IM_MAXD || Q < 1 || r < 1 || n_tab < 1 || n_tab > IM_MAXT) return 0;
-  return implicit_bytes(d, Q, r, n_tab);
+size_t tp_implicit_ws_bytes(int d, int Q, int r, int n_tab, int ra, int rf) {
+  if (d < 1 || d > IM_MAXD || Q < 1 || r < 1 || n_tab < 1 || n_tab > IM_MAXT || ra < 1 || ra > IM_MAXRA || rf < 0)
+    return 0;
+  return implicit_bytes(d, Q, r, n_tab) + force_bytes(d, Q, r, ra, rf);
 }
 
 int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* tabs, const int* tab_id,
                          const double* KL, const double* KR, const double* f_old, double* f_new,
                          int sweeps, int schedule, double delta_beta, double eps_tol, double lam,
-                         int orientation, const double* circ_eig, double* eps_conv, int* info, void* ws,
-                         size_t ws_bytes, void* stream) {
+                         int orientation, const double* circ_eig, const double* forcing, int rf,
+                         const double* fcoef, double* eps_conv, int* info, void* ws, size_t ws_bytes,
+                         void* stream) {
   if (d < 1 || d > IM_MAXD || Q < 1 || r < 1 || ra < 1 || ra > IM_MAXRA || n_tab < 1 || n_tab > IM_MAXT) return TP_EINVAL;
   if (!tabs || !tab_id || !KL || !KR || !f_old || !f_new || !eps_conv || !info || sweeps < 0) return TP_EINVAL;
   if (!(delta_beta >= 1.0) || !(lam >= 0.0) || (schedule != 0 && schedule != 1)) return TP_EINVAL;
+  if (forcing && (rf < 1 || !fcoef)) return TP_EINVAL;
+  if (!forcing) rf = 0;
   for (int i = 0; i < d * ra * ra; ++i) if (tab_id[i] < 0 || tab_id[i] >= n_tab) return TP_EINVAL;
   const int n = padded_n(r * Q);   // system size incl. identity padding
-  if (!ws || ws_bytes < implicit_bytes(d, Q, r, n_tab)) return TP_EWORKSPACE;
+  if (!ws || ws_bytes < implicit_bytes(d, Q, r, n_tab) + force_bytes(d, Q, r, ra, rf)) return TP_EWORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   Carver cv(ws, ws_bytes);
   const size_t rr = (size_t)r * r, QR = (size_t)Q * r;
@@ -1169,23 +1317,28 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   double* y = cv.take<double>(n);
   double* bint = cv.take<double>((size_t)d * QR);
   double* bjac = cv.take<double>((size_t)d * QR);
-  int* xs_dev = cv.take<int>(IM_MAXT);
-  (void)xs_dev;
-  int* xs_modes = reinterpret_cast<int*>(Linv + (size_t)(n / CH_NB) * CH_NB * CH_NB);   // spare tail block
+  (void)cv.take<int>(IM_MAXT);
+  (void)cv.take<char>(256);
+  (void)cv.take<double>(6 * (size_t)d * IM_MAXT);
   double* xhat = cv.take<double>((size_t)r * Q * 2);
   double* tw = cv.take<double>((size_t)Q * 2);
   double* bho = cv.take<double>((size_t)d * Q * r * 2);
   double* bhn = cv.take<double>((size_t)Q * r * 2);
+  Carver cv_gs = cv;                  // the fused circulant kernel carves its scratch from here
+  (void)cv.take<char>(circ_gs_bytes(d, Q, r));
+  int* stop = cv.take<int>(64);
+  double* fP = rf ? cv.take<double>((size_t)d * ra * Q * rf) : nullptr;
+  double* fW = rf ? cv.take<double>((size_t)d * ra * r * rf) : nullptr;
+  double* fvec = rf ? cv.take<double>(QR) : nullptr;
+  double* fhat = rf ? cv.take<double>(QR * 2) : nullptr;
+  if (!cv.ok()) return TP_EWORKSPACE;
+  cudaError_t err;
+  err = cudaMemsetAsync(info, 0, 2 * sizeof(int), st);
+  if (err == cudaSuccess) err = cudaMemsetAsync(stop, 0, sizeof(int), st);
+  if (err != cudaSuccess) return cuda_status(err);
   if (circ_eig) {
-    std::vector<double> htw((size_t)Q * 2);
-    for (int m = 0; m < Q; ++m) {
-      htw[2 * m] = cos(2.0 * M_PI * m / Q);
-      htw[2 * m + 1] = sin(2.0 * M_PI * m / Q);
-    }
-    cudaError_t e0 = cudaMemcpyAsync(tw, htw.data(), htw.size() * sizeof(double), cudaMemcpyHostToDevice,
-                                     (cudaStream_t)stream);
-    if (e0 != cudaSuccess) return cuda_status(e0);
-    cudaStreamSynchronize((cudaStream_t)stream);   // htw is a host temporary
+    twiddle_kernel<<<(Q + 255) / 256, 256, 0, st>>>(Q, tw);
+    if ((err = cudaGetLastError()) != cudaSuccess) return cuda_status(err);
   }
 
   // distinct tables per mode
@@ -1198,12 +1351,30 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
         if (!seen[t]) { seen[t] = 1; used[k].push_back(t); }
       }
   }
-  cudaError_t err;
-  err = cudaMemsetAsync(info, 0, 2 * sizeof(int), st);
-  if (err != cudaSuccess) return cuda_status(err);
+  // forcing: P[k][e] = S_{k,e} c_k once per step (source table = pairs[k][e][0])
+  ForceArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  if (rf) {
+    std::vector<int> src((size_t)d * ra);
+    for (int k = 0; k < d; ++k)
+      for (int e = 0; e < ra; ++e) src[(size_t)k * ra + e] = tab_id[(k * ra + e) * ra + 0];
+    const int* dsrc = device_table(src);
+    if (!dsrc) return TP_ECUDA;
+    force_proj_kernel<<<dim3(d, ra), 256, 0, st>>>(Q, rf, ra, tabs, dsrc, forcing, fP);
+    fa.Q = Q; fa.r = r; fa.rf = rf; fa.ra = ra; fa.d = d;
+    for (int e = 0; e < ra; ++e) fa.coef[e] = fcoef[e];
+    fa.P = fP; fa.W = fW; fa.fvec = fvec; fa.stop = stop;
+  }
+  // the forcing term of mode q into fvec ([Q][r]) from the current iterate
+  auto force_mode = [&](int q) -> cudaError_t {
+    force_w_kernel<<<dim3(d, ra), 256, 0, st>>>(Q, r, rf, ra, q, f_new, fP, fW, stop);
+    fa.q = q;
+    force_vec_kernel<<<(int)((QR + 255) / 256), 256, 0, st>>>(fa);
+    return cudaGetLastError();
+  };
 
   // fused circulant Gauss-Seidel step (one cooperative launch) when it applies
-  bool fused = g_circ_fused && circ_eig && schedule == 0 && delta_beta == 1.0 && r <= CG_MAXR;
+  bool fused = g_circ_fused && circ_eig && schedule == 0 && delta_beta == 1.0 && r <= CG_MAXR && !rf;
   for (int k = 0; k < d && fused; ++k) fused = used[k].size() <= (size_t)CG_MAXX;
   if (fused) {
     const int nf = Q / 2 + 1;
@@ -1230,13 +1401,13 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
       ga->pbeg[k][used[k].size()] = (short)np;
     }
     ga->eig = circ_eig; ga->tw = tw; ga->f_old = f_old; ga->f_new = f_new;
-    ga->X = cv.take<double>((size_t)d * nf * r * 2);
-    ga->Bo = cv.take<double>((size_t)d * nf * r * 2);
-    ga->H = cv.take<double>((size_t)CG_MAXX * r * r);
-    ga->Hg = cv.take<double>((size_t)CG_MAXX * r * r);
-    ga->part = cv.take<double>((size_t)d * nf * 2 * CG_MAXX * r * r);
-    ga->convp = cv.take<double>((size_t)d * nf * 2);
-    ga->bar = cv.take<unsigned int>(32);
+    ga->X = cv_gs.take<double>((size_t)d * nf * r * 2);
+    ga->Bo = cv_gs.take<double>((size_t)d * nf * r * 2);
+    ga->H = cv_gs.take<double>((size_t)CG_MAXX * r * r);
+    ga->Hg = cv_gs.take<double>((size_t)CG_MAXX * r * r);
+    ga->part = cv_gs.take<double>((size_t)d * nf * 2 * CG_MAXX * r * r);
+    ga->convp = cv_gs.take<double>((size_t)d * nf * 2);
+    ga->bar = cv_gs.take<unsigned int>(32);
     ga->stop = reinterpret_cast<int*>(ga->bar + 16);
     ga->G = G; ga->Gm = Gm; ga->eps_out = eps_conv; ga->info = info; ga->prof = g_circ_prof;
     int nsm = 0, dev = 0;
@@ -1272,6 +1443,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     for (int t : used[k]) {
       BGemm g = bgemm_desc(Q, r, Q, tabs + (size_t)t * Q * Q, transT ? 1 : Q, transT ? Q : 1, bsrc + (size_t)k * QR,
                            r, 1, dst + ((size_t)k * n_tab + t) * QR, r, 1);
+      g.skip = stop;
       const int ks = bgemm_pick_split(g, 148, 2);
       if (ks > 1 && (size_t)g.M * g.N * ks <= IM_KPART * (size_t)n_tab * QR) { g.ksplit = ks; g.part = kpart; }
       cudaError_t e = bgemm_launch(g, st);
@@ -1294,11 +1466,8 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
                                (long long)((k * n_tab + t) * rr)});
     }
   }
-  long long* dgofs = reinterpret_cast<long long*>(xs_modes + (size_t)d * IM_MAXT);
-  err = cudaMemcpyAsync(dgofs, gofs.data(), gofs.size() * sizeof(long long), cudaMemcpyHostToDevice, st);
-  if (err != cudaSuccess) return cuda_status(err);
-  err = cudaStreamSynchronize(st);   // gofs is a host temporary
-  if (err != cudaSuccess) return cuda_status(err);
+  const long long* dgofs = device_table(gofs);
+  if (!dgofs) return TP_ECUDA;
   auto refresh_mode = [&](int k) -> cudaError_t {
     const int nt = (int)used[k].size();
     const long long* o1 = dgofs + gofs_at[k];
@@ -1313,6 +1482,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     g4.offs = o2; g4.nb1 = nt;
     // latency-bound small GEMMs (K = Q): split K so each CTA walks 2 tiles
     for (BGemm* g : {&g1, &g2, &g3, &g4}) {
+      g->skip = stop;
       const int ks = bgemm_pick_split(*g, 148, 2);
       if (ks > 1 && (size_t)g->M * g->N * g->nb1 * g->nb2 * ks <= IM_KPART * (size_t)n_tab * QR) {
         g->ksplit = ks;
@@ -1336,18 +1506,19 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
     cudaFuncSetAttribute(fourier_grams_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fg_smem);
     // DFT of every mode of b_old once per step
     for (int k = 0; k < d; ++k)
-      dft_cols_kernel<<<dft_blocks, 256, dft_smem, st>>>(Q, r, f_old + (size_t)k * QR, tw, bho + (size_t)k * QR * 2);
+      dft_cols_kernel<<<dft_blocks, 256, dft_smem, st>>>(Q, r, f_old + (size_t)k * QR, tw, bho + (size_t)k * QR * 2,
+                                                         stop);
   }
   // Circulant tables: the Grams of mode k from Fourier coefficients (one DFT of
   // b_new[k], one launch for G and Gm of all its tables) instead of four GEMMs
   auto refresh_fourier = [&](int k) -> cudaError_t {
-    dft_cols_kernel<<<dft_blocks, 256, dft_smem, st>>>(Q, r, f_new + (size_t)k * QR, tw, bhn);
-    FGramArgs fa;
-    memset(&fa, 0, sizeof(fa));
-    fa.Q = Q; fa.r = r; fa.k = k; fa.n_tab = n_tab; fa.conj_tilde = tr;
-    for (size_t i = 0; i < used[k].size(); ++i) fa.ts[i] = used[k][i];
-    fa.eig = circ_eig; fa.bn = bhn; fa.bo = bho + (size_t)k * QR * 2; fa.G = G; fa.Gm = Gm;
-    fourier_grams_kernel<<<dim3((unsigned)used[k].size(), 2, (unsigned)((4 * r * r + 255) / 256)), 256, fg_smem, st>>>(fa);
+    dft_cols_kernel<<<dft_blocks, 256, dft_smem, st>>>(Q, r, f_new + (size_t)k * QR, tw, bhn, stop);
+    FGramArgs ga2;
+    memset(&ga2, 0, sizeof(ga2));
+    ga2.Q = Q; ga2.r = r; ga2.k = k; ga2.n_tab = n_tab; ga2.conj_tilde = tr;
+    for (size_t i = 0; i < used[k].size(); ++i) ga2.ts[i] = used[k][i];
+    ga2.eig = circ_eig; ga2.bn = bhn; ga2.bo = bho + (size_t)k * QR * 2; ga2.G = G; ga2.Gm = Gm; ga2.stop = stop;
+    fourier_grams_kernel<<<dim3((unsigned)used[k].size(), 2, (unsigned)((4 * r * r + 255) / 256)), 256, fg_smem, st>>>(ga2);
     return cudaGetLastError();
   };
   auto refresh_any = [&](int k) -> cudaError_t { return circ_eig ? refresh_fourier(k) : refresh_mode(k); };
@@ -1360,24 +1531,23 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   ha.d = d; ha.ra = ra; ha.r = r; ha.n_tab = n_tab;
   for (int i = 0; i < d * ra * ra; ++i) ha.tab[i] = tab_id[i];
   for (int i = 0; i < ra * ra; ++i) { ha.KL[i] = KL[i]; ha.KR[i] = KR[i]; }
-  ha.G = G; ha.Gm = Gm; ha.H = H; ha.Hg = Hg;
+  ha.G = G; ha.Gm = Gm; ha.H = H; ha.Hg = Hg; ha.stop = stop;
   AsmArgs as;
   memset(&as, 0, sizeof(as));
-  as.Q = Q; as.r = r; as.N = n; as.tabs = tabs; as.H = H; as.M = M; as.lam = lam;
+  as.Q = Q; as.r = r; as.N = n; as.tabs = tabs; as.H = H; as.M = M; as.lam = lam; as.stop = stop;
   // xs tables are uploaded per mode into a small device array (stream-ordered)
   std::vector<int> xs_all((size_t)d * IM_MAXT, 0);
   for (int k = 0; k < d; ++k)
     for (size_t i = 0; i < used[k].size(); ++i) xs_all[(size_t)k * IM_MAXT + i] = used[k][i];
-  err = cudaMemcpyAsync(xs_modes, xs_all.data(), xs_all.size() * sizeof(int), cudaMemcpyHostToDevice, st);
-  if (err != cudaSuccess) return cuda_status(err);
+  const int* xs_modes = device_table(xs_all);
+  if (!xs_modes) return TP_ECUDA;
   const int nbk = n / CH_NB;
   const int pd_smem = (int)(sizeof(double) * 2 * CH_NB * (CH_NB + 1));
   cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pd_smem);
   const int asm_blocks = (int)(((long long)n * n + 255) / 256 < 148 * 32 ? ((long long)n * n + 255) / 256 : 148 * 32);
-  int done = 0;
+  const int cp_blocks = (int)((d * QR + 255) / 256 < 1184 ? (d * QR + 255) / 256 : 1184);
   for (int sweep = 0; sweep < sweeps; ++sweep) {
-    err = cudaMemcpyAsync(bint, f_new, sizeof(double) * d * QR, cudaMemcpyDeviceToDevice, st);
-    if (err != cudaSuccess) return cuda_status(err);
+    copy_kernel<<<cp_blocks, 256, 0, st>>>(bint, f_new, (size_t)d * QR, stop);
     for (int q = 0; q < d; ++q) {
       ha.q = q; ha.nX = (int)used[q].size();
       for (int i = 0; i < ha.nX; ++i) ha.xs[i] = used[q][i];
@@ -1391,6 +1561,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
         ha.pbeg[ha.nX] = (short)np;
       }
       double* dst = (schedule == 0 ? f_new : bjac) + (size_t)q * QR;
+      if (rf && (err = force_mode(q)) != cudaSuccess) return cuda_status(err);
       if (circ_eig) {
         CircArgs ca;
         memset(&ca, 0, sizeof(ca));
@@ -1400,49 +1571,51 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
         for (int i = 0; i < ra * ra; ++i) { ca.KL[i] = KL[i]; ca.KR[i] = KR[i]; }
         ca.G = G; ca.Gm = Gm; ca.W = W;
         ca.H = H; ca.eig = circ_eig; ca.gam = gam; ca.tw = tw; ca.xhat = xhat; ca.lam = lam; ca.info = info;
-        ca.Hg = Hg; ca.bho = bho + (size_t)q * QR * 2; ca.conj_tilde = tr;
+        ca.Hg = Hg; ca.bho = bho + (size_t)q * QR * 2; ca.conj_tilde = tr; ca.stop = stop;
+        if (rf) {
+          dft_cols_kernel<<<dft_blocks, 256, dft_smem, st>>>(Q, r, fvec, tw, fhat, stop);
+          ca.fhat = fhat;
+        }
         form_h_kernel<<<dim3(ha.nX, (r * r + 256 / FH_SPLIT - 1) / (256 / FH_SPLIT)), 256, 0, st>>>(ha);
         const size_t csm = sizeof(double) * (2 * (size_t)r * (r + 1) + 4 * (size_t)r + 2 * (size_t)ha.nX * r * r +
                                              2 * (size_t)ha.nX);
         cudaFuncSetAttribute(circ_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
         circ_solve_kernel<<<Q, 256, csm, st>>>(ca);
-        circ_idft_kernel<<<(int)((8 * QR + 255) / 256), 256, idft_smem, st>>>(Q, r, xhat, tw, dst, info);
+        circ_idft_kernel<<<(int)((8 * QR + 255) / 256), 256, idft_smem, st>>>(Q, r, xhat, tw, dst, info, stop);
       } else {
       form_h_kernel<<<dim3(ha.nX, (r * r + 256 / FH_SPLIT - 1) / (256 / FH_SPLIT)), 256, 0, st>>>(ha);
-      gamma_kernel<<<(n + 255) / 256, 256, 0, st>>>(Q, r, ha.nX, xs_modes + (size_t)q * IM_MAXT, Hg, W, n_tab, q, gam, n);
+      gamma_kernel<<<(n + 255) / 256, 256, 0, st>>>(Q, r, ha.nX, xs_modes + (size_t)q * IM_MAXT, Hg, W, n_tab, q, gam, n,
+                                                    rf ? fvec : nullptr, stop);
       as.nX = ha.nX;
       for (int i = 0; i < as.nX; ++i) as.xs[i] = used[q][i];
       assemble_kernel<<<asm_blocks, 256, 0, st>>>(as);
       for (int kb = 0; kb < nbk; ++kb) {
         const int k0 = kb * CH_NB, rest = n - k0 - CH_NB;
-        potrf_diag_kernel<<<1, 256, pd_smem, st>>>(M, n, k0, CH_NB, Linv + (size_t)kb * CH_NB * CH_NB, info);
+        potrf_diag_kernel<<<1, 256, pd_smem, st>>>(M, n, k0, CH_NB, Linv + (size_t)kb * CH_NB * CH_NB, info, stop);
         if (rest > 0) {
           // panel: A21 <- A21 L11^-T   (in place: each row block is read fully before written)
           BGemm gp = bgemm_desc(rest, CH_NB, CH_NB, M + (size_t)(k0 + CH_NB) * n + k0, n, 1,
                                 Linv + (size_t)kb * CH_NB * CH_NB, 1, CH_NB, M + (size_t)(k0 + CH_NB) * n + k0, n, 1);
+          gp.skip = stop;
           if ((err = bgemm_launch(gp, st)) != cudaSuccess) return cuda_status(err);
           // trailing: A22 <- A22 - A21 A21^T
           BGemm gs = bgemm_desc(rest, rest, CH_NB, M + (size_t)(k0 + CH_NB) * n + k0, n, 1,
                                 M + (size_t)(k0 + CH_NB) * n + k0, 1, n, M + (size_t)(k0 + CH_NB) * n + k0 + CH_NB, n, 1);
-          gs.alpha = -1.0; gs.beta = 1.0;
+          gs.alpha = -1.0; gs.beta = 1.0; gs.skip = stop;
           if ((err = bgemm_launch(gs, st)) != cudaSuccess) return cuda_status(err);
         }
       }
-      potrs_kernel<<<1, 256, 0, st>>>(M, n, Linv, gam, x, y);
-      scatter_x_kernel<<<(int)((QR + 255) / 256), 256, 0, st>>>(Q, r, x, dst, info);
+      potrs_kernel<<<1, 256, 0, st>>>(M, n, Linv, gam, x, y, stop);
+      scatter_x_kernel<<<(int)((QR + 255) / 256), 256, 0, st>>>(Q, r, x, dst, info, stop);
       }
       if (schedule == 0)
         if ((err = refresh_any(q)) != cudaSuccess) return cuda_status(err);
     }
-    if (schedule == 1) {
-      err = cudaMemcpyAsync(f_new, bjac, sizeof(double) * d * QR, cudaMemcpyDeviceToDevice, st);
-      if (err != cudaSuccess) return cuda_status(err);
-    }
+    if (schedule == 1) copy_kernel<<<cp_blocks, 256, 0, st>>>(f_new, bjac, (size_t)d * QR, stop);
     // delta_beta == 1: the damped update b_int + (b - b_int) equals b up to the last
     // ulp, so the Gauss-Seidel iterate and its cached Grams are kept as they are
     const bool damp = !(delta_beta == 1.0 && schedule == 0);
-    conv_damp_kernel<<<1, 256, 0, st>>>(Q, r, d, f_new, bint, damp ? delta_beta : 0.0, eps_conv);
-    done = sweep + 1;
+    conv_damp_kernel<<<1, 256, 0, st>>>(Q, r, d, f_new, bint, damp ? delta_beta : 0.0, eps_conv, eps_tol, stop, info);
     // the damped iterate b_int + (b - b_int)/delta_beta differs from the raw
     // solve (also by rounding when delta_beta == 1): refresh every mode's Grams
     if (damp)
@@ -1450,15 +1623,7 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
         if ((err = refresh_any(k)) != cudaSuccess) return cuda_status(err);
     err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_status(err);
-    if (eps_tol > 0.0) {   // reference loop condition (implicit.py:244): one host read per sweep
-      double eps_h = 0.0;
-      err = cudaMemcpyAsync(&eps_h, eps_conv, sizeof(double), cudaMemcpyDeviceToHost, st);
-      if (err == cudaSuccess) err = cudaStreamSynchronize(st);
-      if (err != cudaSuccess) return cuda_status(err);
-      if (eps_h <= eps_tol) break;
-    }
   }
-  set_int_kernel<<<1, 1, 0, st>>>(info + 1, done);
   return cuda_status(cudaGetLastError());
 }
 

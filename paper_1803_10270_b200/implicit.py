@@ -140,17 +140,32 @@ class StepWorkspace:
         return False
 
 
+def _check_forcing(forcing: CPTensor | None, f_n: CPTensor, pair: CrankNicolsonPair) -> None:
+    if forcing is None:
+        return
+    if not isinstance(forcing, CPTensor):
+        raise TypeError("forcing must be a CPTensor")
+    if forcing.specs != f_n.specs:
+        raise ValueError("forcing lives on a different basis")
+    if forcing.is_complex:
+        raise ValueError("complex128 forcing is not supported by the real-fp64 implicit step")
+    if any(dense_factor(s, m) is not None for s, m in zip(pair.specs, pair.factors[0])):
+        # the source tables pair(E_e, I) are read as pairs[k][e][0]
+        raise ValueError("forcing needs term 0 of the pair to be the identity (crank_nicolson_pair layout)")
+
+
 def _launch(f_n: CPTensor, out: torch.Tensor, tab: OperatorTables, cfg: ALSStepConfig, eps: torch.Tensor,
-            info: torch.Tensor) -> None:
+            info: torch.Tensor, forcing: CPTensor | None = None) -> None:
     if f_n.is_complex:
         raise ValueError("complex128 states are not supported by the real-fp64 implicit step")
     L = _lib.lib()
     d, Q, r, ra = f_n.ndim, f_n.specs[0].Q, f_n.rank, tab.pair.n_terms
     n_tab = tab.tabs.shape[0]
+    rf = forcing.rank if forcing is not None else 0
     use_circ = tab.circ_eig is not None and cfg.solver in ("auto", "circulant")
     if cfg.solver == "circulant" and tab.circ_eig is None:
         raise ValueError("solver='circulant' needs circulant pairing tables (periodic collocation factors)")
-    nbytes = L.tp_implicit_ws_bytes(d, Q, r, n_tab)
+    nbytes = L.tp_implicit_ws_bytes(d, Q, r, n_tab, ra, rf)
     if nbytes == 0:
         raise ValueError(f"unsupported implicit-step size d={d}, Q={Q}, r={r}, tables={n_tab}")
     ws = _lib.WORKSPACE.get(nbytes, f_n.data.device)
@@ -160,6 +175,8 @@ def _launch(f_n: CPTensor, out: torch.Tensor, tab: OperatorTables, cfg: ALSStepC
                                 0 if cfg.schedule == "gauss-seidel" else 1, float(cfg.delta_beta),
                                 float(cfg.eps_tol), float(cfg.lam), 1 if cfg.orientation == "reference" else 0,
                                 tab.circ_eig.data_ptr() if use_circ else None,
+                                forcing.data.data_ptr() if rf else None, rf,
+                                _lib.double_array([tab.pair.dt * float(complex(x).real) for x in tab.pair.eta]),
                                 eps.data_ptr(), info.data_ptr(), ws.data_ptr(), ws.numel(),
                                 _lib.stream_ptr(f_n.data.device))
     _lib.check(st, "implicit.step")
@@ -167,16 +184,24 @@ def _launch(f_n: CPTensor, out: torch.Tensor, tab: OperatorTables, cfg: ALSStepC
 
 def step(f_n: CPTensor, pair: CrankNicolsonPair, forcing: CPTensor | None, config: ALSStepConfig,
          workspace: StepWorkspace | None = None, log: dict | None = None) -> CPTensor:
-    """Advance one implicit step at fixed separation rank (implicit.py:222-301)."""
-    if forcing is not None:
-        raise NotImplementedError("forcing terms (implicit.py:140-152) are outside the B200 hot path")
+    """Advance one implicit step at fixed separation rank (implicit.py:222-301), with the
+    source term ``forcing`` (implicit.py:140-152) when given.
+
+    ``log`` receives the reference's keys (implicit.py:289-297): ``sweeps``,
+    ``eps_conv`` and ``converged`` as computed on the device, ``solve_seconds`` =
+    device time of the whole step (CUDA events; assembly and solve are fused
+    into the same kernels, so ``assembly_seconds`` is None), ``lsqr_iterations``
+    None (direct Cholesky solves) and ``direct_solves`` = sweeps x d."""
     ws = workspace or StepWorkspace(pair, config)
+    _check_forcing(forcing, f_n, pair)
     dev = f_n.data.device
     out = f_n.data.clone()
     eps = torch.full((1,), float("inf"), dtype=torch.float64, device=dev)
     info = torch.zeros(2, dtype=torch.int32, device=dev)
-    t0 = time.perf_counter()
-    _launch(f_n, out, ws.tables, config, eps, info)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _launch(f_n, out, ws.tables, config, eps, info, forcing)
+    e1.record()
     status, sweeps = (int(v) for v in info.tolist())
     eps_conv = float(eps.item())
     if status & 2:
@@ -187,22 +212,25 @@ def step(f_n: CPTensor, pair: CrankNicolsonPair, forcing: CPTensor | None, confi
     if not did_converge:
         logger.warning("sweep cap %d hit with update %.3e > %.3e", config.max_sweeps, eps_conv, config.eps_tol)
     if log is not None:
-        log.update(sweeps=sweeps, eps_conv=eps_conv, converged=did_converge,
-                   assembly_seconds=0.0, solve_seconds=time.perf_counter() - t0, lsqr_iterations=0)
+        e1.synchronize()
+        log.update(sweeps=sweeps, eps_conv=eps_conv, converged=did_converge, assembly_seconds=None,
+                   solve_seconds=e0.elapsed_time(e1) / 1e3, lsqr_iterations=None, direct_solves=sweeps * f_n.ndim)
     return CPTensor(f_n.specs, data=out, rank=f_n.rank)
 
 
 def run(f0: CPTensor, pair: CrankNicolsonPair, config: ALSStepConfig, steps: int,
-        workspace: StepWorkspace | None = None) -> CPTensor:
-    """``steps`` implicit steps, stream-ordered, one status check at the end."""
+        workspace: StepWorkspace | None = None, forcing: CPTensor | None = None) -> CPTensor:
+    """``steps`` implicit steps, stream-ordered (no host synchronisation inside a step;
+    convergence is decided on the device), one status check at the end."""
     ws = workspace or StepWorkspace(pair, config)
+    _check_forcing(forcing, f0, pair)
     dev = f0.data.device
     eps = torch.zeros(1, dtype=torch.float64, device=dev)
     infos = torch.zeros((max(steps, 1), 2), dtype=torch.int32, device=dev)
     cur = f0
     for n in range(steps):
         out = cur.data.clone()
-        _launch(cur, out, ws.tables, config, eps, infos[n])
+        _launch(cur, out, ws.tables, config, eps, infos[n], forcing)
         cur = CPTensor(f0.specs, data=out, rank=f0.rank)
     bad = int(infos[:, 0].max().item())
     if bad:

@@ -171,3 +171,84 @@ def test_config2_steps_fused_vs_unfused(circ_fused, fused):
     for _ in range(2):
         ref, _, _ = oim.step(ref, tab, w["sweeps"], w["lam"])
     assert metrics.cp_rel_diff(ref, out) <= 1e-8
+
+
+@pytest.mark.parametrize("solver", ["dense", "circulant"])
+@pytest.mark.parametrize("case", ["gs", "jac"])
+@pytest.mark.parametrize("orientation,key", [("reference", "out_reference_orientation"),
+                                             ("corrected", "out_corrected")])
+def test_forced_step_golden(solver, case, orientation, key):
+    """Forced implicit steps of the real reference (tests/golden/implicit_forced.npz,
+    forcing block implicit.py:140-152): Gauss-Seidel with fixed sweeps, and the
+    default Jacobi schedule (delta_beta = 4) whose eps_tol stop is decided on the
+    device -- the sweep count must equal the reference's."""
+    g = load_golden("implicit_forced")
+    q, d, r, dt, lam = g["meta"]
+    q, d = int(q), int(d)
+    eps_tol, max_sweeps, delta_beta, jac = g[f"{case}_cfg"]
+    S = col_specs(d, q)
+    pair = euler_pair(S, g["D"], g["a"], float(dt))
+    cfg = implicit.ALSStepConfig(dt=float(dt), eps_tol=float(eps_tol), max_sweeps=int(max_sweeps),
+                                 delta_beta=float(delta_beta), schedule="jacobi" if jac else "gauss-seidel",
+                                 lam=float(lam), orientation=orientation, solver=solver)
+    log = {}
+    out = implicit.step(cp.CPTensor(S, unpack_cp(g, "f0")), pair, cp.CPTensor(S, unpack_cp(g, "forcing")), cfg,
+                        log=log)
+    idx = 0 if orientation == "reference" else 1
+    assert log["sweeps"] == int(g[f"{case}_sweeps"][idx])
+    assert log["lsqr_iterations"] is None and log["solve_seconds"] > 0
+    rel = metrics.cp_rel_diff(unpack_cp(g, f"{case}_{key}"), out.to_numpy())
+    assert rel <= 1e-9, rel
+
+
+@pytest.mark.parametrize("solver", ["dense", "circulant"])
+def test_forced_step_matches_oracle_larger(solver):
+    rng = np.random.default_rng(17)
+    d, q, r, rf, dt, sweeps = 4, 16, 4, 3, 2e-2, 6
+    a = (1.0, 0.5, -0.75, 0.25)
+    D = fourier_diff_matrix(q)
+    S = col_specs(d, q)
+    f0 = [rng.standard_normal((q, r)) for _ in range(d)]
+    c = [0.3 * rng.standard_normal((q, rf)) for _ in range(d)]
+    cfg = implicit.ALSStepConfig(dt=dt, eps_tol=0.0, max_sweeps=sweeps, delta_beta=1.0, schedule="gauss-seidel",
+                                 lam=1e-10, solver=solver)
+    out = implicit.step(cp.CPTensor(S, f0), euler_pair(S, D, a, dt), cp.CPTensor(S, c), cfg)
+    ref, _, _ = oim.step(f0, oracle_tables(d, q, D, a, dt), sweeps, 1e-10, forcing=c, dt=dt)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= 1e-9
+
+
+def test_implicit_run_is_stream_ordered_and_capturable():
+    """No host synchronisation inside implicit.step's launch: with eps_tol > 0 (the
+    device-side stop) the dense path can be captured in a CUDA graph and replayed,
+    bitwise equal to eager."""
+    import torch
+    rng = np.random.default_rng(23)
+    d, q, r, dt = 3, 12, 3, 2e-2
+    a = (1.0, 0.5, -0.75)
+    S = col_specs(d, q)
+    D = fourier_diff_matrix(q)
+    pair = euler_pair(S, D, a, dt)
+    cfg = implicit.ALSStepConfig(dt=dt, eps_tol=1e-6, max_sweeps=40, delta_beta=4.0, schedule="jacobi",
+                                 lam=1e-10, solver="dense")
+    ws = implicit.StepWorkspace(pair, cfg)
+    f0 = cp.CPTensor(S, [rng.standard_normal((q, r)) for _ in range(d)])
+    eager = implicit.run(f0, pair, cfg, 2, workspace=ws)
+    out = f0.data.clone()
+    eps = torch.zeros(1, dtype=torch.float64, device=out.device)
+    info = torch.zeros(2, dtype=torch.int32, device=out.device)
+    implicit._launch(f0, out, ws.tables, cfg, eps, info)      # warm-up: tables cached, workspace sized
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            out.copy_(f0.data)
+            implicit._launch(f0, out, ws.tables, cfg, eps, info)
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    one = implicit.run(f0, pair, cfg, 1, workspace=ws)
+    assert torch.equal(out, one.data)
+    assert 0 < int(info[1].item()) < 40
+    assert eager.data.shape == one.data.shape
