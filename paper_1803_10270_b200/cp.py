@@ -286,7 +286,7 @@ def _als_device(target: CPTensor, U: torch.Tensor, r: int, cfg: ALSApproxConfig,
         return
     nbytes = L.tp_cp_als_ws_bytes(d, qs, target.rank, r, cfg.grid)
     if nbytes == 0:
-        raise ValueError(f"unsupported ALS size: d={d}, R={target.rank}, r={r} (r <= 32, d <= 8)")
+        raise ValueError(f"unsupported ALS size: d={d}, R={target.rank}, r={r} (r <= 160, d <= 8)")
     ws = _lib.WORKSPACE.get(nbytes, target.data.device)
     reg, mode = (_REG, 1) if cfg.reg is None else (float(cfg.reg), 0)
     st = L.tp_cp_als_f64(d, qs, target.rank, target.data.data_ptr(), r, U.data_ptr(), int(cfg.max_sweeps),
@@ -303,7 +303,7 @@ def als_plan(qs, R: int, r: int, grid: int = 0) -> dict:
     st = _lib.lib().tp_cp_als_plan(len(qs), _lib.int_array(qs), R, r, grid, out)
     _lib.check(st, "als_plan")
     variant = {0: "als_persistent", 1: "als_cluster", 2: "als_small", 3: "als_persistent_cluster",
-               5: "als_tiny8"}[out[0]]
+               5: "als_tiny8", 7: "als_generic"}[out[0]]
     return {"kernel": variant, "ctas": out[1], "cluster": out[2], "smem_bytes": out[3]}
 
 

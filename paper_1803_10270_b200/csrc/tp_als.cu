@@ -36,6 +36,12 @@ namespace tp {
 int inner_tiles(int ra, int rb, int same);
 int launch_inner(int d, const int* q, int ra, const double* A, int rb, const double* B, int same,
                  double* out, double* partial, cudaStream_t st);
+// size-unbounded streamed variant (tp_als_gen.cu): r > 32 or targets beyond shared memory
+int als_generic_supported(int d, const int* q, int R, int r);
+size_t als_generic_ws_bytes(int d, const int* q, int R, int r);
+int als_generic_run(int d, const int* q, int R, const double* V, int r, double* U, int sweeps, double reg,
+                    int reg_mode, double tol, double stall, double* trace, int* info, void* ws, size_t ws_bytes,
+                    cudaStream_t st);
 
 constexpr int ALS_NT = 256;
 constexpr int ALS_NW = ALS_NT / 32;
@@ -2363,7 +2369,8 @@ struct AlsPlan {
 
 static int g_early_inv = 1;   // debug hook: early exact inverse in the clustered R-slab kernel (r <= 16)
 static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 force als_cluster, 3 force als_small,
-                            // 4 force als_persistent as one cluster (grid = cluster size), 5 force als_tiny8
+                            // 4 force als_persistent as one cluster (grid = cluster size), 5 force als_tiny8,
+                            // 7 force the streamed generic variant (tp_als_gen.cu)
 static int g_cluster = 0;   // debug hook: cluster size (0 = auto)
 
 static int choose_rm(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : 0)); }
@@ -2653,7 +2660,11 @@ void tp_debug_set_als_early_inv(int on) { g_early_inv = on; }
 int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out) {
   if (!out) return TP_EINVAL;
   AlsPlan pl;
-  const int st = plan_als(d, q, R, r, grid, pl);
+  const int st = g_variant == 7 ? TP_EUNSUPPORTED : plan_als(d, q, R, r, grid, pl);
+  if (st == TP_EUNSUPPORTED && als_generic_supported(d, q, R, r)) {   // streamed generic variant
+    out[0] = 7; out[1] = 0; out[2] = 1; out[3] = 0;
+    return TP_OK;
+  }
   if (st != TP_OK) return st;
   out[0] = pl.variant; out[1] = pl.P; out[2] = (pl.variant == 1 || pl.variant == 3) ? pl.a.Pq : 1; out[3] = (int)pl.smem;
   return TP_OK;
@@ -2661,7 +2672,9 @@ int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out) {
 
 size_t tp_cp_als_ws_bytes(int d, const int* q, int R, int r, int grid) {
   AlsPlan pl;
-  if (plan_als(d, q, R, r, grid, pl) != TP_OK) return 0;
+  const int st = g_variant == 7 ? TP_EUNSUPPORTED : plan_als(d, q, R, r, grid, pl);
+  if (st == TP_EUNSUPPORTED) return als_generic_ws_bytes(d, q, R, r);
+  if (st != TP_OK) return 0;
   return pl.ws_total;
 }
 
@@ -2670,7 +2683,10 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
                   double* trace, int* info, int grid, void* ws, size_t ws_bytes, void* stream) {
   if (!V || !U || !info || sweeps < 0 || !(reg >= 0.0)) return TP_EINVAL;
   AlsPlan pl;
-  int st = plan_als(d, q, R, r, grid, pl);
+  int st = g_variant == 7 ? TP_EUNSUPPORTED : plan_als(d, q, R, r, grid, pl);
+  if (st == TP_EUNSUPPORTED && als_generic_supported(d, q, R, r))
+    return als_generic_run(d, q, R, V, r, U, sweeps, reg, reg_mode, tol, stall, trace, info, ws, ws_bytes,
+                           (cudaStream_t)stream);
   if (st != TP_OK) return st;
   if (!ws || ws_bytes < pl.ws_total) return TP_EWORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;

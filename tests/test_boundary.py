@@ -30,7 +30,8 @@ def test_invalid_arguments_rejected_without_gpu():
     assert L.tp_cp_inner_f64(0, q, 1, None, 1, None, 0, None, None, 0, None) == _lib.TP_EINVAL
     assert L.tp_cp_als_f64(2, q, 4, None, 2, None, 1, 1e-10, 0, 0.0, 0.0, None, None, 0, None, 0,
                            None) == _lib.TP_EINVAL
-    assert L.tp_cp_als_ws_bytes(2, q, 4, 40, 0) == 0  # r > 32 unsupported
+    assert L.tp_cp_als_ws_bytes(2, q, 4, 40, 0) > 0    # r > 32: the streamed generic variant
+    assert L.tp_cp_als_ws_bytes(2, q, 4, 200, 0) == 0  # r > 160 unsupported
 
 
 def test_cptensor_validation_mirrors_reference():

@@ -310,7 +310,7 @@ def test_als_rejects_bad_shapes():
     with pytest.raises(ValueError, match="init shape"):
         cp.cp_approx_als(T, 3, cp.ALSApproxConfig(max_sweeps=2), init=cp.CPTensor(S, rand_factors(rng, (4, 5), 2, 1.0)))
     with pytest.raises(ValueError):
-        cp.cp_approx_als(T, 40, cp.ALSApproxConfig(max_sweeps=2))   # r > 32: outside the fused kernels
+        cp.cp_approx_als(T, 200, cp.ALSApproxConfig(max_sweeps=2))   # r > 160: outside every variant
 
 
 @pytest.mark.parametrize("variant,cluster", [(0, 0), (1, 0), (2, 0), (3, 0), (4, 0), (5, 0)])
@@ -335,3 +335,67 @@ def test_als_zero_target_returns_zero(als_variant, variant, cluster, reg):
         outc = cp.cp_approx_als(Tc, r, cp.ALSApproxConfig(max_sweeps=3, stall=-np.inf, reg=reg),
                                 init=cp.as_complex(init))
         assert torch.count_nonzero(outc.data).item() == 0
+
+
+# ---- streamed generic variant (r > 32, targets beyond shared memory) ----------------
+
+@pytest.mark.parametrize("r,R,sweeps", [(40, 4096, 3), (64, 4096, 2)])
+def test_als_generic_large_rank_and_input(r, R, sweeps):
+    """r = 40 / 64 and R = 4096 at Q = 256, d = 6 (beyond the fused kernels' r <= 32 and
+    their aggregate-shared-memory limit): the streamed variant, oracle parity <= 1e-9."""
+    qs = (256,) * 6
+    assert cp.als_plan(qs, R, r)["kernel"] == "als_generic"
+    rng = np.random.default_rng(r + R)
+    V = [rng.standard_normal((q, R)) / 16 for q in qs]
+    init = [v[:, :r].copy() for v in V]
+    out = cp.cp_approx_als(cp.CPTensor(specs_for(qs), V), r,
+                           cp.ALSApproxConfig(max_sweeps=sweeps, stall=-np.inf, reg=1e-10),
+                           init=cp.CPTensor(specs_for(qs), init))
+    ref = ocp.als(V, init, sweeps, lam=1e-10)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+
+
+def test_als_fused_limit_large_R_streams():
+    """R = 4096 with r = 32 no longer fits the fused kernels' shared memory: the plan
+    falls back to the streamed variant instead of raising."""
+    assert cp.als_plan((256,) * 6, 4096, 32)["kernel"] == "als_generic"
+
+
+@pytest.mark.parametrize("reg", [1e-10, None])
+@pytest.mark.parametrize("qs,R,r", [((12, 9, 10, 8), 30, 7), ((20, 16, 24), 50, 33), ((16,) * 5, 40, 48)])
+def test_als_generic_forced_matches_oracle(als_variant, qs, R, r, reg):
+    """The generic variant forced (debug hook 7) on small shapes, both regulariser
+    rules, with the residual trace (device-side Gram identity)."""
+    als_variant(7, 0)
+    rng = np.random.default_rng(R + r)
+    V = rand_factors(rng, qs, R, 0.3)
+    init = [rng.standard_normal((q, r)) * 0.3 for q in qs]
+    S = specs_for(qs)
+    trace = []
+    cfg = cp.ALSApproxConfig(max_sweeps=6, stall=-np.inf, reg=reg)
+    out = cp.cp_approx_als(cp.CPTensor(S, V), r, cfg, init=cp.CPTensor(S, init), trace=trace)
+    otrace = []
+    ref = ocp.als(V, init, 6, lam=reg, trace=otrace)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+    np.testing.assert_allclose(trace, otrace, rtol=1e-7, atol=1e-8)
+    assert len(trace) == 6
+
+
+def test_als_generic_stall_and_zero_target(als_variant):
+    """Stopping rules decided on the device (cp.py:329-332): the generic variant stops
+    at the same sweep as the fused kernels; an all-zero target gives a zero fit."""
+    rng = np.random.default_rng(5)
+    qs, R, r = (14, 12, 10), 20, 3
+    S = specs_for(qs)
+    V = rand_factors(rng, qs, R, 0.5)
+    init = [v[:, :r].copy() for v in V]
+    cfg = cp.ALSApproxConfig(max_sweeps=200, stall=1e-6, reg=1e-10)
+    t_fused, t_gen = [], []
+    a = cp.cp_approx_als(cp.CPTensor(S, V), r, cfg, init=cp.CPTensor(S, init), trace=t_fused)
+    als_variant(7, 0)
+    b = cp.cp_approx_als(cp.CPTensor(S, V), r, cfg, init=cp.CPTensor(S, init), trace=t_gen)
+    assert len(t_fused) == len(t_gen) < 200
+    assert metrics.cp_rel_diff(a.to_numpy(), b.to_numpy()) <= 1e-9
+    Z = cp.CPTensor(S, [np.zeros((q, R)) for q in qs])
+    z = cp.cp_approx_als(Z, r, cp.ALSApproxConfig(max_sweeps=3, stall=-np.inf), init=cp.CPTensor(S, init))
+    assert torch.count_nonzero(z.data).item() == 0

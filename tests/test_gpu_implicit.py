@@ -228,7 +228,7 @@ def test_implicit_run_is_stream_ordered_and_capturable():
     S = col_specs(d, q)
     D = fourier_diff_matrix(q)
     pair = euler_pair(S, D, a, dt)
-    cfg = implicit.ALSStepConfig(dt=dt, eps_tol=1e-6, max_sweeps=40, delta_beta=4.0, schedule="jacobi",
+    cfg = implicit.ALSStepConfig(dt=dt, eps_tol=1e-4, max_sweeps=200, delta_beta=4.0, schedule="jacobi",
                                  lam=1e-10, solver="dense")
     ws = implicit.StepWorkspace(pair, cfg)
     f0 = cp.CPTensor(S, [rng.standard_normal((q, r)) for _ in range(d)])
@@ -250,5 +250,5 @@ def test_implicit_run_is_stream_ordered_and_capturable():
     torch.cuda.synchronize()
     one = implicit.run(f0, pair, cfg, 1, workspace=ws)
     assert torch.equal(out, one.data)
-    assert 0 < int(info[1].item()) < 40
+    assert 0 < int(info[1].item()) < 200      # stopped on the device by eps_tol
     assert eager.data.shape == one.data.shape
