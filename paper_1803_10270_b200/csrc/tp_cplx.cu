@@ -342,8 +342,17 @@ int tp_cp_apply_c128(int d, const int* q, int r_in, const double* F, int n_terms
                      double scale_re, double scale_im, const int* mat_idx, const double* mats,
                      const long long* mat_off, int n_mats, double* out, int R_out, int col_off, void* stream) {
   if (d < 1 || d > TP_MAXD || r_in < 1 || n_terms < 1 || !F || !out || !q || !weights) return TP_EINVAL;
-  if (n_terms > APC_MAXT) return TP_EUNSUPPORTED;
-  if (col_off < 0 || col_off + n_terms * r_in > R_out) return TP_EINVAL;
+  if (col_off < 0 || col_off + (long long)n_terms * r_in > R_out) return TP_EINVAL;
+  if (n_terms > APC_MAXT) {   // consecutive launches of at most APC_MAXT terms (weights are re/im pairs)
+    for (int t0 = 0; t0 < n_terms; t0 += APC_MAXT) {
+      const int nt = n_terms - t0 < APC_MAXT ? n_terms - t0 : APC_MAXT;
+      const int st = tp_cp_apply_c128(d, q, r_in, F, nt, weights + 2 * (size_t)t0, scale_re, scale_im,
+                                      mat_idx ? mat_idx + (size_t)t0 * d : nullptr, mats, mat_off, n_mats, out, R_out,
+                                      col_off + t0 * r_in, stream);
+      if (st != TP_OK) return st;
+    }
+    return TP_OK;
+  }
   ApplyCArgs a;
   memset(&a, 0, sizeof(a));
   a.d = d; a.r_in = r_in; a.R_out = R_out; a.col_off = col_off; a.n_terms = n_terms;

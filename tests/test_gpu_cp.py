@@ -399,3 +399,24 @@ def test_als_generic_stall_and_zero_target(als_variant):
     Z = cp.CPTensor(S, [np.zeros((q, R)) for q in qs])
     z = cp.cp_approx_als(Z, r, cp.ALSApproxConfig(max_sweeps=3, stall=-np.inf), init=cp.CPTensor(S, init))
     assert torch.count_nonzero(z.data).item() == 0
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_apply_more_than_64_terms(cplx):
+    """Operators with more terms than one kernel argument block holds (100 > 64):
+    consecutive launches, same term-major output (operators.py:48-62)."""
+    rng = np.random.default_rng(77)
+    qs, r, nt = (6, 5, 7), 2, 100
+    S = specs_for(qs)
+    mats = [[rng.standard_normal((q, q)) if (t + k) % 3 == 0 else None for k, q in enumerate(qs)] for t in range(nt)]
+    w = list(rng.standard_normal(nt))
+    if cplx:
+        w = [x + 0.5j * x for x in w]
+    L = operators.SeparableOperator(S, tuple(w), tuple(tuple(m) for m in mats))
+    f = rand_factors(rng, qs, r, 1.0)
+    out = operators.apply(L, cp.CPTensor(S, f))
+    ref = oops.apply(w, mats, [x.astype(np.complex128) if cplx else x for x in f])
+    assert out.rank == nt * r
+    got = out.to_numpy()
+    for k in range(len(qs)):
+        np.testing.assert_allclose(got[k], ref[k], rtol=1e-12, atol=1e-12)
