@@ -178,6 +178,17 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
                        int r_max, double eps, double* out_frames, double* out_transfers,
                        int* out_ranks, double* est, double* norms,
                        void* ws, size_t ws_bytes, void* stream);
+/* Any binary dimension tree (ht.py:55-76 DimensionTree): n_nodes nodes in the
+ * caller's order with nodes[0] the root, given as host arrays parent/left/right
+ * (-1 = none); frames are packed in leaf order, transfers in interior-node order
+ * (node order), the root's k x k x 1 transfer in the first k*k entries of its slot.
+ * Same outputs as tp_ht_truncate_f64 (which is this call on balanced_tree(d)). */
+size_t tp_ht_truncate_tree_ws_bytes(int n_nodes, const int* parent, const int* left, const int* right, int Q, int k,
+                                    int nb);
+int tp_ht_truncate_tree_f64(int n_nodes, const int* parent, const int* left, const int* right, int Q, int k, int nb,
+                            const double* frames, const double* transfers, int r_max, double eps,
+                            double* out_frames, double* out_transfers, int* out_ranks, double* est, double* norms,
+                            void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Fixed-rank implicit ALS step (implicit.step, implicit.py:222-301) for an

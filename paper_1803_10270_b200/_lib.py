@@ -80,6 +80,9 @@ _SIGNATURES = {
     "tp_ipc_open": (_i, [_vp, _vp]),
     "tp_ipc_close": (_i, [_vp]),
     "tp_ht_truncate_ws_bytes": (_sz, [_i, _i, _i, _i]),
+    "tp_ht_truncate_tree_ws_bytes": (_sz, [_i, _c_int_p, _c_int_p, _c_int_p, _i, _i, _i]),
+    "tp_ht_truncate_tree_f64": (_i, [_i, _c_int_p, _c_int_p, _c_int_p, _i, _i, _i, _vp, _vp, _i, _d, _vp, _vp, _vp,
+                                     _vp, _vp, _vp, _sz, _vp]),
     "tp_ht_truncate_f64": (_i, [_i, _i, _i, _i, _vp, _vp, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "tp_implicit_ws_bytes": (_sz, [_i, _i, _i, _i, _i, _i]),
     "tp_implicit_step_f64": (_i, [_i, _i, _i, _i, _i, _vp, _c_int_p, _c_double_p, _c_double_p, _vp, _vp, _i, _i,

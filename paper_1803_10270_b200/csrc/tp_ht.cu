@@ -670,9 +670,48 @@ struct HtPlan {
   size_t big, off_n, total;
 };
 
-static void plan_ht(int d, int Q, int k, int nb, int r_max, HtPlan& P) {
-  memset(&P.T, 0, sizeof(P.T));
-  build_tree(P.T, 0, d, -1, 0);
+// any binary dimension tree (ht.py:55-76) given as parallel arrays, nodes[0] the
+// root; leaf / interior slots in node order (the packed batch layout)
+static int finish_tree(Tree& T, int i, int dep) {
+  T.depth[i] = dep;
+  if (T.left[i] < 0) { T.height[i] = 0; T.dims[i] = 1; }
+  else {
+    const int hl = finish_tree(T, T.left[i], dep + 1), hr = finish_tree(T, T.right[i], dep + 1);
+    T.height[i] = 1 + (hl > hr ? hl : hr);
+    T.dims[i] = T.dims[T.left[i]] + T.dims[T.right[i]];
+  }
+  if (T.height[i] > T.H) T.H = T.height[i];
+  return T.height[i];
+}
+
+static int tree_from_arrays(int n, const int* parent, const int* left, const int* right, Tree& T) {
+  if (n < 3 || n > 31 || !parent || !left || !right || parent[0] != -1) return TP_EINVAL;
+  memset(&T, 0, sizeof(T));
+  T.n = n;
+  int seen[32] = {0};
+  for (int i = 0; i < n; ++i) {
+    const bool leaf = left[i] < 0;
+    if (leaf != (right[i] < 0)) return TP_EINVAL;
+    if (i > 0 && (parent[i] < 0 || parent[i] >= n)) return TP_EINVAL;
+    T.parent[i] = parent[i]; T.left[i] = left[i]; T.right[i] = right[i];
+    if (!leaf) {
+      if (left[i] >= n || right[i] >= n || left[i] == right[i] || parent[left[i]] != i || parent[right[i]] != i)
+        return TP_EINVAL;
+      if (seen[left[i]]++ || seen[right[i]]++) return TP_EINVAL;
+      T.slot[i] = T.nint++;
+    } else {
+      T.slot[i] = T.nleaf++;
+    }
+  }
+  for (int i = 1; i < n; ++i) if (seen[i] != 1) return TP_EINVAL;   // every non-root node has one parent
+  if (T.nleaf != T.nint + 1) return TP_EINVAL;
+  finish_tree(T, 0, 0);
+  return TP_OK;
+}
+
+static void plan_ht_tree(const Tree& T, int Q, int k, int nb, int r_max, HtPlan& P) {
+  P.T = T;
+  const int d = T.nleaf;
   P.d = d; P.Q = Q; P.k = k; P.nb = nb;
   P.ro = r_max < k ? r_max : k;
   int maxw = 1;
@@ -696,6 +735,13 @@ static void plan_ht(int d, int Q, int k, int nb, int r_max, HtPlan& P) {
   P.total = align_up(8 * nb * nn * kk) * 5 + align_up(8 * nb * nn * k) * 2 + align_up(8 * nb * nn * (size_t)k * P.ro) * 2 +
             2 * align_up(4 * nb * nn) + align_up(8 * nb * nn) + 3 * align_up(8 * P.big) + align_up(8 * P.off_n) + 256 +
             align_up(8 * HT_PART);
+}
+
+static void plan_ht(int d, int Q, int k, int nb, int r_max, HtPlan& P) {
+  Tree T;
+  memset(&T, 0, sizeof(T));
+  build_tree(T, 0, d, -1, 0);
+  plan_ht_tree(T, Q, k, nb, r_max, P);
 }
 
 }  // namespace tp
@@ -731,17 +777,55 @@ size_t tp_ht_truncate_ws_bytes(int d, int Q, int k, int nb) {
   return P.total;
 }
 
+static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* frames, const double* transfers,
+                            int r_max, double eps, double* out_frames, double* out_transfers, int* out_ranks,
+                            double* est, double* norms, void* ws, size_t ws_bytes, void* stream);
+
 int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const double* transfers,
                        int r_max, double eps, double* out_frames, double* out_transfers,
                        int* out_ranks, double* est, double* norms,
                        void* ws, size_t ws_bytes, void* stream) {
+  if (d < 2 || d > 16) return TP_EINVAL;
+  Tree T;
+  memset(&T, 0, sizeof(T));
+  build_tree(T, 0, d, -1, 0);
+  return ht_truncate_impl(T, Q, k, nb, frames, transfers, r_max, eps, out_frames, out_transfers, out_ranks, est,
+                          norms, ws, ws_bytes, stream);
+}
+
+size_t tp_ht_truncate_tree_ws_bytes(int n_nodes, const int* parent, const int* left, const int* right, int Q, int k,
+                                    int nb) {
+  Tree T;
+  if (tree_from_arrays(n_nodes, parent, left, right, T) != TP_OK || Q < 1 || k < 1 || k > 64 || nb < 1) return 0;
+  HtPlan P;
+  plan_ht_tree(T, Q, k, nb, k, P);
+  return P.total;
+}
+
+int tp_ht_truncate_tree_f64(int n_nodes, const int* parent, const int* left, const int* right, int Q, int k, int nb,
+                            const double* frames, const double* transfers, int r_max, double eps,
+                            double* out_frames, double* out_transfers, int* out_ranks, double* est, double* norms,
+                            void* ws, size_t ws_bytes, void* stream) {
+  Tree T;
+  const int st = tree_from_arrays(n_nodes, parent, left, right, T);
+  if (st != TP_OK) return st;
+  return ht_truncate_impl(T, Q, k, nb, frames, transfers, r_max, eps, out_frames, out_transfers, out_ranks, est,
+                          norms, ws, ws_bytes, stream);
+}
+
+}  // extern "C"
+
+static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* frames, const double* transfers,
+                            int r_max, double eps, double* out_frames, double* out_transfers, int* out_ranks,
+                            double* est, double* norms, void* ws, size_t ws_bytes, void* stream) {
+  const int d = TT.nleaf;
   if (d < 2 || d > 16 || Q < 1 || k < 1 || nb < 1 || r_max < 1 || !(eps >= 0.0)) return TP_EINVAL;
   if (!frames || !transfers || !out_frames || !out_transfers || !out_ranks || !est || !norms) return TP_EINVAL;
   if (k > 64) return TP_EUNSUPPORTED;
   HtPlan P;
-  plan_ht(d, Q, k, nb, r_max, P);
+  plan_ht_tree(TT, Q, k, nb, r_max, P);
   HtPlan P0;
-  plan_ht(d, Q, k, nb, k, P0);
+  plan_ht_tree(TT, Q, k, nb, k, P0);
   if (!ws || ws_bytes < P0.total) return TP_EWORKSPACE;
   const Tree& T = P.T;
   const int nn = T.n, ro = P.ro;
@@ -975,5 +1059,3 @@ int tp_ht_truncate_f64(int d, int Q, int k, int nb, const double* frames, const 
   }
   return TP_OK;
 }
-
-}  // extern "C"

@@ -255,6 +255,36 @@ def _pack_batch(hs):
     return F, B, Q, k, leaves, ints
 
 
+def _tree_arrays(tree: DimensionTree):
+    n = len(tree.nodes)
+    return (n, _lib.int_array([nd.parent for nd in tree.nodes]), _lib.int_array([nd.left for nd in tree.nodes]),
+            _lib.int_array([nd.right for nd in tree.nodes]))
+
+
+def _launch_truncate(tree: DimensionTree, Q, k, nb, F, B, r_max, eps, OF, OB, ranks, est, norms, dev, what):
+    """tp_ht_truncate_f64 on balanced trees, tp_ht_truncate_tree_f64 on any other tree."""
+    L = _lib.lib()
+    d = tree.ndim
+    if tree == balanced_tree(d):
+        nbytes = L.tp_ht_truncate_ws_bytes(d, Q, k, nb)
+        if nbytes == 0:
+            raise ValueError(f"unsupported hSVD size d={d}, Q={Q}, k={k}")
+        ws = _lib.WORKSPACE.get(nbytes, dev)
+        st = L.tp_ht_truncate_f64(d, Q, k, nb, F.data_ptr(), B.data_ptr(), int(r_max), float(eps), OF.data_ptr(),
+                                  OB.data_ptr(), ranks.data_ptr(), est.data_ptr(), norms.data_ptr(), ws.data_ptr(),
+                                  ws.numel(), _lib.stream_ptr(dev))
+    else:
+        n, par, lft, rgt = _tree_arrays(tree)
+        nbytes = L.tp_ht_truncate_tree_ws_bytes(n, par, lft, rgt, Q, k, nb)
+        if nbytes == 0:
+            raise ValueError(f"unsupported hSVD size / tree: nodes={n}, Q={Q}, k={k}")
+        ws = _lib.WORKSPACE.get(nbytes, dev)
+        st = L.tp_ht_truncate_tree_f64(n, par, lft, rgt, Q, k, nb, F.data_ptr(), B.data_ptr(), int(r_max), float(eps),
+                                       OF.data_ptr(), OB.data_ptr(), ranks.data_ptr(), est.data_ptr(), norms.data_ptr(),
+                                       ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev))
+    _lib.check(st, what)
+
+
 def truncate_batch(hs, r_max: int, eps: float):
     """hSVD-truncate a batch of HT tensors on the same tree in one call.
     Returns (list of HTTensor, list of error estimates)."""
@@ -267,9 +297,6 @@ def truncate_batch(hs, r_max: int, eps: float):
     if tree.nodes[0].is_leaf:
         return [h.copy() for h in hs], [0.0] * len(hs)
     F, B, Q, k, leaves, ints = _pack_batch(hs)
-    d = tree.ndim
-    if tree != balanced_tree(d):
-        raise ValueError("the B200 hSVD kernel supports the balanced dimension tree (ht.balanced_tree)")
     nb = len(hs)
     ro = min(r_max, k)
     dev = F.device
@@ -278,15 +305,7 @@ def truncate_batch(hs, r_max: int, eps: float):
     ranks = torch.zeros((nb, len(tree.nodes)), dtype=torch.int32, device=dev)
     est = torch.zeros(nb, dtype=torch.float64, device=dev)
     norms = torch.zeros(nb, dtype=torch.float64, device=dev)
-    L = _lib.lib()
-    nbytes = L.tp_ht_truncate_ws_bytes(d, Q, k, nb)
-    if nbytes == 0:
-        raise ValueError(f"unsupported hSVD size d={d}, Q={Q}, k={k}")
-    ws = _lib.WORKSPACE.get(nbytes, dev)
-    st = L.tp_ht_truncate_f64(d, Q, k, nb, F.data_ptr(), B.data_ptr(), int(r_max), float(eps), OF.data_ptr(),
-                              OB.data_ptr(), ranks.data_ptr(), est.data_ptr(), norms.data_ptr(), ws.data_ptr(),
-                              ws.numel(), _lib.stream_ptr(dev))
-    _lib.check(st, "truncate")
+    _launch_truncate(tree, Q, k, nb, F, B, r_max, eps, OF, OB, ranks, est, norms, dev, "truncate")
     ranks_h = ranks.cpu().numpy()
     est_h = est.cpu().numpy()
     outs = []
@@ -412,7 +431,6 @@ def norm(h: HTTensor) -> float:
 
 def _norms_batch(hs):
     F, B, Q, k, leaves, ints = _pack_batch(hs)
-    d = hs[0].tree.ndim
     nb = len(hs)
     dev = F.device
     OF = torch.zeros((nb, len(leaves), Q, 1), dtype=torch.float64, device=dev)
@@ -420,13 +438,7 @@ def _norms_batch(hs):
     ranks = torch.zeros((nb, len(hs[0].tree.nodes)), dtype=torch.int32, device=dev)
     est = torch.zeros(nb, dtype=torch.float64, device=dev)
     norms = torch.zeros(nb, dtype=torch.float64, device=dev)
-    L = _lib.lib()
-    nbytes = L.tp_ht_truncate_ws_bytes(d, Q, k, nb)
-    ws = _lib.WORKSPACE.get(nbytes, dev)
-    st = L.tp_ht_truncate_f64(d, Q, k, nb, F.data_ptr(), B.data_ptr(), 1, 0.0, OF.data_ptr(), OB.data_ptr(),
-                              ranks.data_ptr(), est.data_ptr(), norms.data_ptr(), ws.data_ptr(), ws.numel(),
-                              _lib.stream_ptr(dev))
-    _lib.check(st, "norm")
+    _launch_truncate(hs[0].tree, Q, k, nb, F, B, 1, 0.0, OF, OB, ranks, est, norms, dev, "norm")
     return norms.cpu().numpy()
 
 

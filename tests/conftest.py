@@ -33,3 +33,22 @@ def unpack_ht(store, prefix, nodes):
     frames = [store.get(f"{prefix}_F{i}") for i in range(len(nodes))]
     transfers = [store.get(f"{prefix}_B{i}") for i in range(len(nodes))]
     return frames, transfers
+
+
+def tree_nodes(store, name):
+    """(dims, parent, left, right) node tuples of a golden tree (dims rebuilt from the leaves)."""
+    arr = store[f"{name}_tree"]
+    leafdim = store[f"{name}_dims"]
+    n = len(arr)
+    dims = [None] * n
+
+    def walk(i):
+        p, lf, rt = (int(x) for x in arr[i])
+        if lf < 0:
+            dims[i] = (int(leafdim[i]),)
+        else:
+            dims[i] = walk(lf) + walk(rt)
+        return dims[i]
+
+    walk(0)
+    return [(dims[i], int(arr[i][0]), int(arr[i][1]), int(arr[i][2])) for i in range(n)]

@@ -176,6 +176,58 @@ def gen_ht():
     np.savez_compressed(OUT / "ht.npz", **store)
 
 
+def _tree(ndim, split):
+    """DimensionTree built in preorder with a custom split rule (ht.py:55-76 accepts any)."""
+    nodes = []
+
+    def build(dims, parent):
+        idx = len(nodes)
+        nodes.append(None)
+        if len(dims) == 1:
+            nodes[idx] = ht.TreeNode(dims, parent, -1, -1)
+        else:
+            cut = split(len(dims))
+            left = build(dims[:cut], idx)
+            right = build(dims[cut:], idx)
+            nodes[idx] = ht.TreeNode(dims, parent, left, right)
+        return idx
+
+    build(tuple(range(ndim)), -1)
+    return ht.DimensionTree(tuple(nodes))
+
+
+def gen_ht_trees():
+    """hSVD truncation (ht.py:313-372) of the reference on NON-balanced dimension trees:
+    left and right caterpillars and a 1/3-2/3 split, random frames/transfers."""
+    store = {}
+    cases = [("cat_left", 5, 7, 4, 2, 0.0, 31, lambda n: n - 1),
+             ("cat_right", 6, 6, 5, 3, 0.0, 32, lambda n: 1),
+             ("third", 7, 8, 5, 3, 1e-3, 33, lambda n: max(1, n // 3))]
+    names = []
+    for name, d, q, rin, rmax, eps, seed, split in cases:
+        rng = np.random.default_rng(seed)
+        specs = tuple(spec(q) for _ in range(d))
+        tree = _tree(d, split)
+        frames = [None] * len(tree.nodes)
+        transfers = [None] * len(tree.nodes)
+        for i, node in enumerate(tree.nodes):
+            if node.is_leaf:
+                frames[i] = rng.standard_normal((q, rin))
+            else:
+                transfers[i] = rng.standard_normal((rin, rin, 1 if i == 0 else rin))
+        h = ht.HTTensor(specs, tree, frames, transfers)
+        red, est = ht.truncate(h, rmax, eps)
+        pack_ht(f"{name}_in", h, store)
+        pack_ht(f"{name}_out", red, store)
+        store[f"{name}_tree"] = np.array([[n.parent, n.left, n.right] for n in tree.nodes])
+        store[f"{name}_dims"] = np.array([n.dims[0] if n.is_leaf else -1 for n in tree.nodes])
+        store[f"{name}_meta"] = np.array([d, q, rin, rmax, eps, est])
+        store[f"{name}_norm_in"] = np.array(ht.norm(h))
+        names.append(name)
+    store["names"] = np.array(names)
+    np.savez_compressed(OUT / "ht_trees.npz", **store)
+
+
 def gen_operators():
     store = {}
     rng = np.random.default_rng(21)
@@ -460,7 +512,7 @@ def gen_complex():
 GENERATORS = {"cp_als": lambda: gen_cp_als(), "ht": lambda: gen_ht(), "operators": lambda: gen_operators(),
               "explicit": lambda: gen_explicit(), "implicit": lambda: gen_implicit(), "io": lambda: gen_io(),
               "diagnostics": lambda: gen_diagnostics(), "complex": lambda: gen_complex(),
-              "implicit_forced": lambda: gen_implicit_forced()}
+              "implicit_forced": lambda: gen_implicit_forced(), "ht_trees": lambda: gen_ht_trees()}
 
 
 if __name__ == "__main__":

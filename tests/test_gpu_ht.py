@@ -230,3 +230,58 @@ def test_packed_batch_api_matches_list_api():
             assert (u is None and v is None) or torch.equal(u, v)
         ref, oest = oht.truncate(os_[b], 4, 0.0)
         assert metrics.ht_rel_diff(ref, h.to_oracle()) <= TOL
+
+
+def _dev_tree(nodes):
+    return ht.DimensionTree(tuple(ht.TreeNode(tuple(dm), p, lf, rt) for dm, p, lf, rt in nodes))
+
+
+def test_truncate_nonbalanced_trees_golden():
+    """Caterpillar / uneven dimension trees (reference ht.py:55-76 accepts any binary
+    tree): tp_ht_truncate_tree_f64 against the reference's own truncations."""
+    from conftest import tree_nodes
+    g = load_golden("ht_trees")
+    for name in g["names"]:
+        name = str(name)
+        nodes = tree_nodes(g, name)
+        d, q, rin, rmax, eps, est = g[f"{name}_meta"]
+        d, q = int(d), int(q)
+        fin, tin = unpack_ht(g, f"{name}_in", nodes)
+        fout, tout = unpack_ht(g, f"{name}_out", nodes)
+        h = ht.HTTensor(specs(d, q), _dev_tree(nodes), fin, tin)
+        red, my_est = ht.truncate(h, int(rmax), float(eps))
+        assert abs(my_est - est) <= 1e-8 * max(1.0, float(g[f"{name}_norm_in"])), (name, my_est, est)
+        assert metrics.ht_rel_diff((nodes, fout, tout), red.to_oracle()) <= TOL, name
+        assert abs(ht.norm(h) - float(g[f"{name}_norm_in"])) <= 1e-12 * float(g[f"{name}_norm_in"])
+
+
+@pytest.mark.parametrize("split", ["left", "right", "third"])
+def test_truncate_nonbalanced_batch_matches_oracle(split):
+    rng = np.random.default_rng(55)
+    d, q, k = 8, 20, 12
+    cut = {"left": lambda n: n - 1, "right": lambda n: 1, "third": lambda n: max(1, n // 3)}[split]
+    nodes = []
+
+    def build(dims, parent):
+        idx = len(nodes)
+        nodes.append(None)
+        if len(dims) == 1:
+            nodes[idx] = (dims, parent, -1, -1)
+        else:
+            c = cut(len(dims))
+            lf = build(dims[:c], idx)
+            rt = build(dims[c:], idx)
+            nodes[idx] = (dims, parent, lf, rt)
+        return idx
+    build(tuple(range(d)), -1)
+    os_ = []
+    for _ in range(3):
+        frames = [rng.standard_normal((q, k)) if nd[2] < 0 else None for nd in nodes]
+        transfers = [None if nd[2] < 0 else rng.standard_normal((k, k, 1 if i == 0 else k)) for i, nd in enumerate(nodes)]
+        os_.append((nodes, frames, transfers))
+    tree = _dev_tree(nodes)
+    outs, ests = ht.truncate_batch([ht.HTTensor(specs(d, q), tree, o[1], o[2]) for o in os_], 5, 0.0)
+    for o, out, e in zip(os_, outs, ests):
+        ref, oest = oht.truncate(o, 5, 0.0)
+        assert abs(e - oest) <= 1e-8 * max(1.0, oht.norm(o))
+        assert metrics.ht_rel_diff(ref, out.to_oracle()) <= TOL

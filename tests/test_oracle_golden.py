@@ -163,3 +163,18 @@ def test_implicit_forced_step_golden():
             assert done == int(g[f"{case}_sweeps"][i]), (case, orient, done)
             rel = metrics.cp_rel_diff(unpack_cp(g, f"{case}_{key}"), out)
             assert rel < 1e-11, (case, orient, rel)
+
+
+def test_ht_truncate_nonbalanced_trees_golden():
+    """Reference hSVD on caterpillar and uneven dimension trees (ht.py:55-76, 313-372)."""
+    from conftest import tree_nodes, unpack_ht
+    g = load_golden("ht_trees")
+    for name in g["names"]:
+        name = str(name)
+        nodes = tree_nodes(g, name)
+        d, q, rin, rmax, eps, est = g[f"{name}_meta"]
+        fin, tin = unpack_ht(g, f"{name}_in", nodes)
+        fout, tout = unpack_ht(g, f"{name}_out", nodes)
+        red, oest = ht_hsvd.truncate((nodes, fin, tin), int(rmax), float(eps))
+        assert abs(oest - est) <= 1e-10 * max(1.0, float(g[f"{name}_norm_in"])), (name, oest, est)
+        assert metrics.ht_rel_diff((nodes, fout, tout), red) <= 1e-10, name
