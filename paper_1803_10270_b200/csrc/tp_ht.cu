@@ -23,6 +23,9 @@
 
 namespace tp {
 
+cudaError_t launch_tridiag_eigh(int nmat, int k, int nn, int first, int per, const double* Ain, double* Vout,
+                                double* wout, int nvec, const int* skip, cudaStream_t st);
+
 struct Tree {
   int n = 0, nleaf = 0, nint = 0, H = 0;
   int parent[32], left[32], right[32], slot[32], height[32], depth[32], dims[32];
@@ -754,6 +757,7 @@ static double g_jac_tol = 1e-16;
 static int* g_jac_count = nullptr;
 static int g_chol = 1;   // debug hook: 0 = eigh of every frame Gram (reference path)
 static int g_jac_db = 2;  // debug hook: 0 = three-barrier rows/columns, 1 = double-buffered blocks, 2 = upper-triangle blocks (default)
+static int g_eig_tridiag = 1;   // debug hook: node-Gram eigensolver 1 = tridiagonal (default), 0 = Jacobi (g_jac_db)
 
 extern "C" {
 
@@ -769,6 +773,8 @@ void tp_debug_set_bgemm_klayout(int on) { g_bgemm_klayout = on; }
 void tp_debug_set_ht_chol(int on) { g_chol = on; }
 // debug hook: Jacobi kernel (0 = three-barrier rounds, 1 = double-buffered blocks, 2 = upper-triangle blocks, default)
 void tp_debug_set_jacobi_impl(int db) { g_jac_db = db; }
+// debug hook: node-Gram eigensolver (1 = Householder tridiagonal + bisection + inverse iteration, 0 = Jacobi)
+void tp_debug_set_eig_tridiag(int on) { g_eig_tridiag = on; }
 
 size_t tp_ht_truncate_ws_bytes(int d, int Q, int k, int nb) {
   if (d < 2 || d > 16 || Q < 1 || k < 1 || k > 64 || nb < 1) return 0;
@@ -1042,9 +1048,13 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
       form_g_kernel<<<nonroot, 256, fsm, st>>>(k, nn, Vm, lam, Gh, Gt, cholok);
       e = cudaGetLastError();
     } else if (id == -4) {
-      jac<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Gt, Wg, sig, g_jac_sweeps, g_jac_tol, g_jac_count,
-                                                        nullptr);
-      e = cudaGetLastError();
+      if (g_eig_tridiag) {   // eigenvalues + the ro kept eigenvectors: tridiagonalisation (tp_eigh.cu)
+        e = launch_tridiag_eigh(nonroot, k, nn, 1, nn - 1, Gt, Wg, sig, P.ro, nullptr, st);
+      } else {
+        jac<<<nonroot, JAC_NT, jsm, st>>>(k, nn, 1, nn - 1, Gt, Wg, sig, g_jac_sweeps, g_jac_tol, g_jac_count,
+                                                          nullptr);
+        e = cudaGetLastError();
+      }
     } else if (id == -5) {
       keep_rule_kernel<<<(nonroot + 127) / 128, 128, 0, st>>>(k, nn, nb, d, eps, r_max, sig, Mf, keep, disc);
       e = cudaGetLastError();

@@ -285,3 +285,42 @@ def test_truncate_nonbalanced_batch_matches_oracle(split):
         ref, oest = oht.truncate(o, 5, 0.0)
         assert abs(e - oest) <= 1e-8 * max(1.0, oht.norm(o))
         assert metrics.ht_rel_diff(ref, out.to_oracle()) <= TOL
+
+
+@pytest.mark.parametrize("tridiag", [1, 0])
+@pytest.mark.parametrize("d,q,k,rmax,eps", [(4, 9, 7, 3, 0.0), (5, 20, 13, 6, 1e-3), (8, 70, 64, 16, 0.0),
+                                            (6, 12, 3, 2, 0.0), (3, 30, 33, 33, 0.0)])
+def test_node_gram_eigensolvers(tridiag, d, q, k, rmax, eps):
+    """Node-Gram eigensolver: Householder tridiagonalisation + multisection + inverse
+    iteration (default) and the cyclic Jacobi kernel, against the oracle."""
+    import ctypes
+    from paper_1803_10270_b200 import _lib
+    L = _lib.lib()
+    L.tp_debug_set_eig_tridiag.argtypes = [ctypes.c_int]
+    L.tp_debug_set_eig_tridiag(tridiag)
+    try:
+        rng = np.random.default_rng(200 + k)
+        o = random_ht(rng, d, q, k)
+        red, est = ht.truncate(to_dev(d, q, o), rmax, eps)
+        ref, oest = oht.truncate(o, rmax, eps)
+        assert abs(est - oest) <= 1e-8 * max(1.0, oht.norm(o))
+        assert metrics.ht_rel_diff(ref, red.to_oracle()) <= TOL
+        assert red.ranks == tuple(int(x) for x in ref_ranks(ref))
+    finally:
+        L.tp_debug_set_eig_tridiag(1)
+
+
+def test_tridiag_eigensolver_clustered_spectrum():
+    """Inflated ranks (h + h + h: repeated singular structure) and a tensor with equal
+    leaf frames: clustered / repeated node-Gram eigenvalues go through the
+    Gram-Schmidt re-iteration; the truncation stays exact."""
+    rng = np.random.default_rng(71)
+    d, q = 6, 11
+    f = [rng.standard_normal((q, 3)) for _ in range(d)]
+    f = [np.hstack([x[:, :1], x[:, :1] * 1.0000001, x[:, 2:]]) for x in f]   # near-equal columns
+    h = ht.from_cp(cp.CPTensor(specs(d, q), f))
+    h3 = ht.add(ht.add(h, h), h)
+    red, est = ht.truncate(h3, 3, 0.0)
+    ref, oest = oht.truncate(h3.to_oracle(), 3, 0.0)
+    assert abs(est - oest) <= 1e-7 * oht.norm(ref)
+    assert metrics.ht_rel_diff(ref, red.to_oracle()) <= 1e-8
