@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(256) chol_frame_kernel(int k, int nn, const do
 // G_t = diag(sqrt(l)) V^T Gh V diag(sqrt(l)) for every non-root node (one CTA each);
 // nodes with a Cholesky factor (ok) use G_t = L^T Gh L
 __global__ void __launch_bounds__(256) form_g_kernel(int k, int nn, const double* Vm, const double* lam,
-                                                     const double* Gh, double* G, const int* ok) {
+                                                     const double* Gh, double* G, const int* ok, const int* bound) {
   extern __shared__ double fs[];
   const int z = blockIdx.x, per = nn - 1;
   const size_t base = (size_t)(z / per) * nn + 1 + z % per;
@@ -537,14 +537,19 @@ __global__ void __launch_bounds__(256) form_g_kernel(int k, int nn, const double
     double acc = 0.0;
     for (int j = 0; j < k; ++j) acc = fma(P[m * ld + j], V[j * ld + n], acc);
     if (ok[base]) { G[base * k * k + e] = acc; continue; }
-    const double sm = sqrt(fmax(lam[base * k + m], 0.0)), sn = sqrt(fmax(lam[base * k + n], 0.0));
+    const int bt = bound[1 + z % per];
+    const double sm = m < bt ? sqrt(fmax(lam[base * k + m], 0.0)) : 0.0;
+    const double sn = n < bt ? sqrt(fmax(lam[base * k + n], 0.0)) : 0.0;
     G[base * k * k + e] = acc * sm * sn;
   }
 }
 
 // keep rule (ht.py:349-358) per (tensor, non-root node); discarded mass; ranks
+// bound[t]: structural rank of node t (leaves min(Q, k), interior min(k, bound_l bound_r))
+// -- the rank the reference's QR orthogonalisation (ht.py:294-310) leaves; eigenvalues
+// past it are rounding noise of the Gramian gauge and are never kept
 __global__ void keep_rule_kernel(int k, int nn, int nb, int ndim, double eps, int r_max, const double* sig,
-                                 const double* Mf, int* keep, double* disc) {
+                                 const double* Mf, int* keep, double* disc, const int* bound) {
   const int z = blockIdx.x * blockDim.x + threadIdx.x;
   const int per = nn - 1;
   if (z >= nb * per) return;
@@ -556,7 +561,7 @@ __global__ void keep_rule_kernel(int k, int nn, int nb, int ndim, double eps, in
   double tail = 0.0;
   while (kp > 1) {
     const double step = fmax(s[kp - 1], 0.0);
-    if (kp > r_max || tail + step <= budget) { tail += step; --kp; }
+    if (kp > r_max || kp > bound[t] || tail + step <= budget) { tail += step; --kp; }
     else break;
   }
   keep[b * nn + t] = kp;
@@ -578,7 +583,7 @@ __global__ void finish_kernel(int k, int nn, int nb, const double* Mf, const int
 // S_t = V diag(l^+1/2) W[:, :keep] (k x ro, zero columns beyond keep); T_t = S_t^T M_t (ro x k)
 __global__ void __launch_bounds__(256) form_st_kernel(int k, int ro, int nn, const double* Vm, const double* lam,
                                                       const double* Wg, const int* keep, const double* Mf,
-                                                      double* S, double* T, const int* ok) {
+                                                      double* S, double* T, const int* ok, const int* bound) {
   extern __shared__ double ss[];
   const int z = blockIdx.x, per = nn - 1;
   const size_t base = (size_t)(z / per) * nn + 1 + z % per;
@@ -624,7 +629,7 @@ __global__ void __launch_bounds__(256) form_st_kernel(int k, int ro, int nn, con
   const double lmax = fmax(lam[base * k], 0.0);
   for (int m = threadIdx.x; m < k; m += 256) {
     const double l = lam[base * k + m];
-    mu[m] = (l > lmax * 1e-14 && l > 0.0) ? 1.0 / sqrt(l) : 0.0;
+    mu[m] = (m < bound[1 + z % per] && l > lmax * 1e-14 && l > 0.0) ? 1.0 / sqrt(l) : 0.0;
   }
   __syncthreads();
   const double* V = Vm + base * k * k;
@@ -998,10 +1003,19 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
   }
 
   if (hoffs.size() > P0.off_n) return TP_EWORKSPACE;
-  cudaError_t e = cudaMemcpyAsync(doffs, hoffs.data(), hoffs.size() * sizeof(long long), cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_status(e);
-  const double onev = 1.0;
-  e = cudaMemcpyAsync(one, &onev, sizeof(double), cudaMemcpyHostToDevice, st);
+  // offset tables and the structural rank bounds: uploaded once per shape and cached on
+  // the device (no pageable copies: the call is stream-ordered and graph-capturable)
+  std::vector<int> hb(nn, k);
+  for (int t = nn - 1; t >= 0; --t)
+    hb[t] = T.left[t] < 0 ? (Q < k ? Q : k)
+                          : ((long long)hb[T.left[t]] * hb[T.right[t]] < k ? hb[T.left[t]] * hb[T.right[t]] : k);
+  hb[0] = 1;
+  const int* bound = device_table(hb);
+  const long long* dtab = device_table(hoffs);
+  const double* one_c = device_table(std::vector<double>{1.0});
+  if (!bound || !dtab || !one_c) return TP_ECUDA;
+  (void)doffs;
+  cudaError_t e = cudaMemcpyAsync(one, one_c, sizeof(double), cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return cuda_status(e);
   e = cudaMemsetAsync(Gh, 0, sizeof(double) * (size_t)nb * nn * kk, st);
   if (e != cudaSuccess) return cuda_status(e);
@@ -1024,12 +1038,12 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
   for (int id : order) {
     if (id >= 0) {
       BGemm g = calls[id].g;
-      if (calls[id].use_tab) g.offs = doffs + calls[id].tab;
+      if (calls[id].use_tab) g.offs = dtab + calls[id].tab;
       e = bgemm_launch(g, st);
     } else if (id <= -100) {
       const Tr& tr = trs[-100 - id];
       dim3 grid(64, tr.n);
-      transpose12_kernel<<<grid, 256, 0, st>>>(k, tr.kt, doffs + tr.tab, transfers, big3, k3);
+      transpose12_kernel<<<grid, 256, 0, st>>>(k, tr.kt, dtab + tr.tab, transfers, big3, k3);
       e = cudaGetLastError();
     } else if (id == -1) {
       if (g_chol) {
@@ -1045,7 +1059,7 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
       set_root_env<<<(nb + 127) / 128, 128, 0, st>>>(k, nn, nb, Gh);
       e = cudaGetLastError();
     } else if (id == -3) {
-      form_g_kernel<<<nonroot, 256, fsm, st>>>(k, nn, Vm, lam, Gh, Gt, cholok);
+      form_g_kernel<<<nonroot, 256, fsm, st>>>(k, nn, Vm, lam, Gh, Gt, cholok, bound);
       e = cudaGetLastError();
     } else if (id == -4) {
       if (g_eig_tridiag) {   // eigenvalues + the ro kept eigenvectors: tridiagonalisation (tp_eigh.cu)
@@ -1056,10 +1070,10 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
         e = cudaGetLastError();
       }
     } else if (id == -5) {
-      keep_rule_kernel<<<(nonroot + 127) / 128, 128, 0, st>>>(k, nn, nb, d, eps, r_max, sig, Mf, keep, disc);
+      keep_rule_kernel<<<(nonroot + 127) / 128, 128, 0, st>>>(k, nn, nb, d, eps, r_max, sig, Mf, keep, disc, bound);
       e = cudaGetLastError();
     } else if (id == -6) {
-      form_st_kernel<<<nonroot, 256, ssm, st>>>(k, ro, nn, Vm, lam, Wg, keep, Mf, S, Tm, cholok);
+      form_st_kernel<<<nonroot, 256, ssm, st>>>(k, ro, nn, Vm, lam, Wg, keep, Mf, S, Tm, cholok, bound);
       e = cudaGetLastError();
     } else if (id == -7) {
       finish_kernel<<<(nb + 127) / 128, 128, 0, st>>>(k, nn, nb, Mf, keep, disc, est, norms, out_ranks);

@@ -1244,26 +1244,7 @@ static size_t implicit_bytes(int d, int Q, int r, int n_tab) {
   return s;
 }
 
-// Host tables that never change for a given operator/shape (GEMM offset triples,
-// per-mode table lists) live on the device once: the first call uploads them
-// synchronously, every later call (and CUDA-graph capture) only reads them.
-template <class T>
-static const T* device_table(const std::vector<T>& v) {
-  static std::mutex mu;
-  static std::map<std::pair<int, std::vector<char>>, void*> cache;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::vector<char> key(reinterpret_cast<const char*>(v.data()), reinterpret_cast<const char*>(v.data() + v.size()));
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find({dev, key});
-  if (it != cache.end()) return static_cast<const T*>(it->second);
-  void* p = nullptr;
-  if (cudaMalloc(&p, v.empty() ? 8 : v.size() * sizeof(T)) != cudaSuccess) return nullptr;
-  if (!v.empty() && cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-  if (cache.size() > 256) cache.clear();   // (leaks the old tables; bounded)
-  cache.emplace(std::make_pair(dev, std::move(key)), p);
-  return static_cast<const T*>(p);
-}
+
 
 }  // namespace tp
 
