@@ -178,12 +178,15 @@ __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int 
   // ---- 2. eigenvalues: multisection, 4 lanes per eigenvalue
   {
     const double pivmin = scal[4];
+    // absolute tolerance ~ ulp ||T|| (dstebz's default abstol): what a backward-stable
+    // eigensolver resolves; ~22 multisection steps from the Gershgorin interval
+    const double atol = 2.0 * DBL_EPSILON * scal[5] + pivmin;
     for (int i0 = 0; i0 < n; i0 += TE_NT / 4) {
       const int idx = i0 + (tid >> 2), part = tid & 3;
       double a = scal[2], b = scal[3];
       for (int it = 0; it < 64; ++it) {
         // warp-uniform exit (the shuffles below need every lane)
-        if (__all_sync(0xffffffffu, b - a <= 2.0 * DBL_EPSILON * fmax(fabs(a), fabs(b)) + pivmin)) break;
+        if (__all_sync(0xffffffffu, b - a <= atol)) break;
         const double x = a + (double)(part + 1) * (b - a) * 0.2;
         const int c = idx < n ? sturm_count(dg, e2, n, x, pivmin) : 0;
         // new interval: largest x_l with count <= idx, smallest with count > idx

@@ -561,7 +561,7 @@ __global__ void keep_rule_kernel(int k, int nn, int nb, int ndim, double eps, in
   double tail = 0.0;
   while (kp > 1) {
     const double step = fmax(s[kp - 1], 0.0);
-    if (kp > r_max || kp > bound[t] || tail + step <= budget) { tail += step; --kp; }
+    if (kp > r_max || kp > bound[nn + t] || tail + step <= budget) { tail += step; --kp; }
     else break;
   }
   keep[b * nn + t] = kp;
@@ -1005,12 +1005,26 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
   if (hoffs.size() > P0.off_n) return TP_EWORKSPACE;
   // offset tables and the structural rank bounds: uploaded once per shape and cached on
   // the device (no pageable copies: the call is stream-ordered and graph-capturable)
-  std::vector<int> hb(nn, k);
+  // hb: rank of the node's frame (subtree matricization); cb: rank bound of the complement;
+  // the node Gram's rank is <= min(hb, cb) -- eigenvalues past it are exactly zero in the
+  // reference's arithmetic (dropped by its keep rule) and rounding noise here
+  std::vector<int> hb(nn, k), cb(nn, k), bnd(2 * nn, k);
   for (int t = nn - 1; t >= 0; --t)
     hb[t] = T.left[t] < 0 ? (Q < k ? Q : k)
                           : ((long long)hb[T.left[t]] * hb[T.right[t]] < k ? hb[T.left[t]] * hb[T.right[t]] : k);
-  hb[0] = 1;
-  const int* bound = device_table(hb);
+  for (int t = 0; t < nn; ++t) {
+    if (T.left[t] < 0) continue;
+    const int l = T.left[t], r = T.right[t];
+    const long long cl = (t == 0) ? hb[r] : (long long)cb[t] * hb[r], cr = (t == 0) ? hb[l] : (long long)cb[t] * hb[l];
+    cb[l] = cl < k ? (int)cl : k;
+    cb[r] = cr < k ? (int)cr : k;
+  }
+  for (int t = 0; t < nn; ++t) {
+    bnd[t] = hb[t];                                    // frame-Gram pseudo-inverse (form_g, form_st)
+    bnd[nn + t] = hb[t] < cb[t] ? hb[t] : cb[t];       // node-Gram keep bound (keep_rule)
+  }
+  bnd[0] = bnd[nn] = 1;
+  const int* bound = device_table(bnd);
   const long long* dtab = device_table(hoffs);
   const double* one_c = device_table(std::vector<double>{1.0});
   if (!bound || !dtab || !one_c) return TP_ECUDA;
