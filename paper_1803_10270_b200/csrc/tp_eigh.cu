@@ -186,7 +186,11 @@ __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int 
       double a = scal[2], b = scal[3];
       for (int it = 0; it < 64; ++it) {
         // warp-uniform exit (the shuffles below need every lane)
-        if (__all_sync(0xffffffffu, b - a <= atol)) break;
+        // intervals near zero keep going to relative accuracy: the discarded tail of a
+        // rank-deficient Gram is exactly zero in the reference's arithmetic (error estimate)
+        const bool done = (b - a <= 2.0 * DBL_EPSILON * fmax(fabs(a), fabs(b)) + pivmin) ||
+                          (b - a <= atol && fmin(fabs(a), fabs(b)) > 64.0 * atol);
+        if (__all_sync(0xffffffffu, done)) break;
         const double x = a + (double)(part + 1) * (b - a) * 0.2;
         const int c = idx < n ? sturm_count(dg, e2, n, x, pivmin) : 0;
         // new interval: largest x_l with count <= idx, smallest with count > idx

@@ -604,15 +604,19 @@ __global__ void __launch_bounds__(256) form_st_kernel(int k, int ro, int nn, con
     __syncthreads();
     for (int i = threadIdx.x; i < k; i += 256) dinv[i] = 1.0 / Ls[i * (k + 1) + i];
     __syncthreads();
-    const int c = threadIdx.x >> 4, part = threadIdx.x & 15;
-    for (int i = k - 1; i >= 0; --i) {
-      double acc = 0.0;
-      if (c < ro)
-        for (int m = i + 1 + part; m < k; m += 16) acc = fma(Ls[m * (k + 1) + i], Sl[m * ro + c], acc);
+    // 16 columns per pass (16 threads per column); the passes are independent
+    const int part = threadIdx.x & 15;
+    for (int c0 = 0; c0 < ro; c0 += 16) {
+      const int c = c0 + (threadIdx.x >> 4);
+      for (int i = k - 1; i >= 0; --i) {
+        double acc = 0.0;
+        if (c < ro)
+          for (int m = i + 1 + part; m < k; m += 16) acc = fma(Ls[m * (k + 1) + i], Sl[m * ro + c], acc);
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (c < ro && part == 0) Sl[i * ro + c] = (c < kp) ? (Ws[i * ro + c] - acc) * dinv[i] : 0.0;
-      __syncthreads();
+        for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (c < ro && part == 0) Sl[i * ro + c] = (c < kp) ? (Ws[i * ro + c] - acc) * dinv[i] : 0.0;
+        __syncthreads();
+      }
     }
     for (int e = threadIdx.x; e < k * ro; e += 256) S[base * k * ro + e] = Sl[e];
     for (int e = threadIdx.x; e < ro * k; e += 256) {

@@ -62,7 +62,9 @@ def test_truncate_golden_cases():
 
 @pytest.mark.parametrize("d,q,k,rmax,eps", [(2, 9, 5, 3, 0.0), (3, 7, 6, 4, 0.0), (4, 10, 8, 3, 0.0),
                                             (5, 6, 7, 7, 1e-2), (6, 12, 9, 4, 0.0), (7, 8, 6, 2, 0.0),
-                                            (8, 16, 12, 5, 0.0), (8, 20, 16, 16, 1e-3)])
+                                            (8, 16, 12, 5, 0.0), (8, 20, 16, 16, 1e-3),
+                                            (3, 30, 30, 30, 0.0), (4, 40, 20, 17, 0.0), (8, 20, 20, 20, 0.0),
+                                            (5, 30, 40, 33, 0.0)])
 def test_truncate_matches_oracle(d, q, k, rmax, eps):
     rng = np.random.default_rng(d * 100 + k)
     o = random_ht(rng, d, q, k)
@@ -188,7 +190,12 @@ def test_jacobi_kernels(impl, chol, d, q, k, rmax, eps):
         ref, oest = oht.truncate(o, rmax, eps)
         assert abs(est - oest) <= 1e-8 * max(1.0, oht.norm(o))
         assert metrics.ht_rel_diff(ref, red.to_oracle()) <= TOL
-        assert red.ranks == tuple(int(x) for x in ref_ranks(ref))
+        if k <= q:
+            assert red.ranks == tuple(int(x) for x in ref_ranks(ref))
+        else:
+            # k > Q: node Grams past the structural rank hold rounding noise, which the
+            # reference keeps when it happens to be positive (eps = 0); never kept here
+            assert all(a <= b for a, b in zip(red.ranks, ref_ranks(ref)))
     finally:
         L.tp_debug_set_ht_chol(1)
         L.tp_debug_set_jacobi_impl(2)
@@ -305,7 +312,12 @@ def test_node_gram_eigensolvers(tridiag, d, q, k, rmax, eps):
         ref, oest = oht.truncate(o, rmax, eps)
         assert abs(est - oest) <= 1e-8 * max(1.0, oht.norm(o))
         assert metrics.ht_rel_diff(ref, red.to_oracle()) <= TOL
-        assert red.ranks == tuple(int(x) for x in ref_ranks(ref))
+        if k <= q:
+            assert red.ranks == tuple(int(x) for x in ref_ranks(ref))
+        else:
+            # k > Q: node Grams past the structural rank hold rounding noise, which the
+            # reference keeps when it happens to be positive (eps = 0); never kept here
+            assert all(a <= b for a, b in zip(red.ranks, ref_ranks(ref)))
     finally:
         L.tp_debug_set_eig_tridiag(1)
 
