@@ -22,6 +22,7 @@
 // All cross-CTA reductions use a fixed order: results are bitwise
 // reproducible for a fixed grid size.
 #include "tp_common.cuh"
+#include "tp_als_rows.cuh"
 #include <cooperative_groups.h>
 #include <cstring>
 #include <cstdlib>
@@ -2362,6 +2363,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_xg(const __grid_constant__ AlsA
 
 struct AlsPlan {
   AlsArgs a;
+  RowsPlan rows;            // variant 8: cluster-row kernel (tp_als_rows.cu)
   int P, rm, variant, Pr;   // variant 0: als_persistent, 1: als_cluster (P = Pr * a.Pq), 2: als_small,
                             // 3: als_persistent as one cluster of P CTAs, 5: als_tiny8 (r <= 8, one CTA)
   size_t smem, ws_inner, ws_total, ydoubles;
@@ -2372,6 +2374,8 @@ static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 for
                             // 4 force als_persistent as one cluster (grid = cluster size), 5 force als_tiny8,
                             // 7 force the streamed generic variant (tp_als_gen.cu)
 static int g_cluster = 0;   // debug hook: cluster size (0 = auto)
+static int g_rows = 0;      // debug hook: cluster-row kernel for large truncations (variant 8 forces it)
+static int g_rows_p = 0;    // debug hook: cluster count of the cluster-row kernel (0 = auto)
 
 static int choose_rm(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : 0)); }
 
@@ -2516,7 +2520,7 @@ static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
   PlanKey key;
   memset(&key, 0, sizeof(key));
   if (cudaGetDevice(&key.dev) != cudaSuccess) { cudaGetLastError(); key.dev = -1; }
-  key.d = d; key.R = R; key.r = r; key.grid = grid; key.variant = g_variant * 2 + g_early_inv; key.cluster = g_cluster;
+  key.d = d; key.R = R; key.r = r; key.grid = grid; key.variant = g_variant * 2 + g_early_inv + 1000 * g_rows + 100000 * g_rows_p; key.cluster = g_cluster;
   for (int k = 0; k < d; ++k) key.q[k] = q[k];
   {
     std::lock_guard<std::mutex> lk(mu);
@@ -2599,6 +2603,18 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
     AlsPlan cp = pl;
     if (plan_persistent_cluster(d, q, R, r, 16, smem_optin, cp) == TP_OK) { pl = cp; return TP_OK; }
   }
+  // large truncations: the cluster-row kernel (one flag exchange + two cluster barriers per
+  // mode update instead of two grid barriers)
+  if (g_variant == 8 || (g_variant == 0 && grid <= 0 && P >= 64 && g_rows)) {
+    AlsPlan cp = pl;
+    if (als_rows_plan(d, q, R, r, g_cluster > 0 ? g_cluster : 0, g_rows_p, cp.rows) == TP_OK) {
+      cp.variant = 8; cp.P = cp.rows.a.S * cp.rows.a.P; cp.Pr = cp.rows.a.P; cp.smem = cp.rows.smem;
+      cp.ws_total = cp.rows.ws;
+      pl = cp;
+      return TP_OK;
+    }
+    if (g_variant == 8) return TP_EUNSUPPORTED;
+  }
   // large truncations: the cluster variant (fewer bytes per CTA per mode update)
   const bool want = g_variant == 2 || (g_variant == 0 && grid <= 0 && P >= 64 && g_cluster >= 0);
   if (want) {
@@ -2656,6 +2672,7 @@ void tp_debug_set_als_ns(int n) { g_ns_max = n; }
 // debug hook: kernel variant (0 auto, 1 als_persistent, 2 als_cluster) and cluster size (0 auto, -1 never)
 void tp_debug_set_als_variant(int variant, int cluster) { g_variant = variant; g_cluster = cluster; }
 void tp_debug_set_als_early_inv(int on) { g_early_inv = on; }
+void tp_debug_set_als_rows(int on, int nclusters) { g_rows = on; g_rows_p = nclusters; }
 
 int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out) {
   if (!out) return TP_EINVAL;
@@ -2666,7 +2683,9 @@ int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out) {
     return TP_OK;
   }
   if (st != TP_OK) return st;
-  out[0] = pl.variant; out[1] = pl.P; out[2] = (pl.variant == 1 || pl.variant == 3) ? pl.a.Pq : 1; out[3] = (int)pl.smem;
+  out[0] = pl.variant; out[1] = pl.P;
+  out[2] = (pl.variant == 1 || pl.variant == 3) ? pl.a.Pq : (pl.variant == 8 ? pl.rows.a.S : 1);
+  out[3] = (int)pl.smem;
   return TP_OK;
 }
 
@@ -2690,6 +2709,9 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
   if (st != TP_OK) return st;
   if (!ws || ws_bytes < pl.ws_total) return TP_EWORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
+  if (pl.variant == 8)
+    return als_rows_run(pl.rows, V, U, sweeps, reg, reg_mode, tol, stall, trace, info, ws, ws_bytes, s, g_prof,
+                        g_prof_cta < 0 ? pl.P + g_prof_cta : g_prof_cta, g_ns_max > 0);
   AlsArgs& a = pl.a;
   Carver cv(ws, ws_bytes);
   a.G = cv.take<double>((size_t)d * r * r);
