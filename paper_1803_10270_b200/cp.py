@@ -303,7 +303,7 @@ def als_plan(qs, R: int, r: int, grid: int = 0) -> dict:
     st = _lib.lib().tp_cp_als_plan(len(qs), _lib.int_array(qs), R, r, grid, out)
     _lib.check(st, "als_plan")
     variant = {0: "als_persistent", 1: "als_cluster", 2: "als_small", 3: "als_persistent_cluster",
-               5: "als_tiny8", 7: "als_generic"}[out[0]]
+               5: "als_tiny8", 7: "als_generic", 8: "als_rows"}[out[0]]
     return {"kernel": variant, "ctas": out[1], "cluster": out[2], "smem_bytes": out[3]}
 
 
@@ -313,6 +313,8 @@ def _check_info(info: torch.Tensor) -> int:
         raise ConditioningError("normal equations produced non-finite coefficients")
     if status & 1:
         raise ConditioningError("regularised normal equations are not positive definite")
+    if status & 4:
+        raise RuntimeError("ALS kernel: a cooperating CTA never arrived (cross-CTA wait timed out)")
     return done
 
 

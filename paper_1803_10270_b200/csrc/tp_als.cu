@@ -2374,7 +2374,7 @@ static int g_variant = 0;   // debug hook: 0 auto, 1 force als_persistent, 2 for
                             // 4 force als_persistent as one cluster (grid = cluster size), 5 force als_tiny8,
                             // 7 force the streamed generic variant (tp_als_gen.cu)
 static int g_cluster = 0;   // debug hook: cluster size (0 = auto)
-static int g_rows = 0;      // debug hook: cluster-row kernel for large truncations (variant 8 forces it)
+static int g_rows = 1;      // debug hook: cluster-row kernel for large truncations (variant 8 forces it)
 static int g_rows_p = 0;    // debug hook: cluster count of the cluster-row kernel (0 = auto)
 
 static int choose_rm(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : 0)); }

@@ -51,7 +51,7 @@ constexpr int RW_PMAX = 16;   // max clusters (R-slabs)
 __host__ __device__ inline int rw_pad4(int n) { return n + (((4 - n % 16) + 16) % 16); }
 
 struct RwSmem {
-  double *Vs, *hadT, *Cown, *Gp, *inbox, *Us, *Am, *X0, *X1, *scr, *rb, *gpub, *part, *pub, *scal;
+  double *Vs, *hadT, *Cown, *Gown, *Apk, *inbox, *Us, *Am, *X0, *X1, *scr, *rb, *gpub, *part, *pub, *scal;
   uint64_t* bar;   // [0]: warm-start prefetch, [1]: inbox (partials), [2]: publishes
   // integer tables (no runtime divisions in the hot loops)
   int* gposT;      // [r][r]: owner-major packed position of Gram entry (i, c)
@@ -59,19 +59,21 @@ struct RwSmem {
   int* nbT;        // [d]: rows of this CTA's block of mode k
   int* qb0T;       // [d]: first row of the block
   int* ocT;        // [S + 1]: first slab column owned by rank q
+  int* gdiag;      // [gstride]: 1 where this rank's packed Gram entry is diagonal
 };
-
-__host__ __device__ inline int rw_nbr(const RowsArgs& a) { return (a.nb4max + 7) & ~7; }   // Us / rb rows
-__host__ __device__ inline int rw_tbl(const RowsArgs& a) {
-  const int m = a.wcol > rw_nbr(a) ? a.wcol : rw_nbr(a);
-  return m * a.r;
-}
-__host__ __device__ inline size_t rw_int_doubles(const RowsArgs& a) {
-  return (size_t)(a.r * a.r + rw_tbl(a) + 2 * TP_MAXD + a.S + 1 + 1) / 2 + 1;
-}
 
 // region sizes rounded to even doubles: every region starts 16-byte aligned (v2 / bulk copies)
 __host__ __device__ inline size_t rw_ev(size_t n) { return (n + 1) & ~(size_t)1; }
+__host__ __device__ inline int rw_nbr(const RowsArgs& a) { return (a.nb4max + 7) & ~7; }   // Us / rb rows
+__host__ __device__ inline int rw_tbl(const RowsArgs& a) {
+  int m = a.wcol > rw_nbr(a) ? a.wcol : rw_nbr(a);
+  if (m < a.r) m = a.r;
+  return m * a.r;
+}
+__host__ __device__ inline size_t rw_int_doubles(const RowsArgs& a) {
+  return rw_ev((size_t)(a.r * a.r + rw_tbl(a) + 2 * TP_MAXD + a.S + 1 + a.gstride + 1) / 2 + 1);
+}
+
 
 // scratch, reused by phase: exchange staging (C^T partial [0, cst_len), Gram blocks after it);
 // split-K partials of the rhs product [0, ysplit); Newton-Schulz temporary [0, RM rh);
@@ -83,13 +85,15 @@ __host__ __device__ inline size_t rw_x0off(int RM, int r) {
 __host__ __device__ inline size_t rw_scr_doubles(const RowsArgs& a, int RM) {
   const size_t x = (size_t)a.cst_len + (size_t)a.S * a.gstride;
   const size_t z = rw_x0off(RM, a.r) + (size_t)RM * rw_pad4(a.r);
-  return x > z ? x : z;
+  const size_t g = (size_t)a.P * rw_ev((size_t)rw_nbr(a) * a.r);   // the P gathered rhs slots
+  const size_t m = x > z ? x : z;
+  return m > g ? m : g;
 }
 
 __host__ __device__ inline size_t rw_smem_doubles(const RowsArgs& a, int RM) {
   const size_t rh = rw_pad4(a.r);
   return 4 + rw_int_doubles(a) + rw_ev(a.vtot) + rw_ev((size_t)a.kpad * rh) + rw_ev((size_t)a.d * a.wcol * a.r) +
-         rw_ev((size_t)a.d * a.S * a.gstride) + rw_ev((size_t)a.S * a.piece) + rw_ev((size_t)rw_nbr(a) * rh) +
+         rw_ev((size_t)a.d * a.gstride) + rw_ev((size_t)a.S * a.gstride) + rw_ev((size_t)a.S * a.piece) + rw_ev((size_t)rw_nbr(a) * rh) +
          2 * rw_ev((size_t)RM * rh) + rw_ev(rw_scr_doubles(a, RM)) + rw_ev((size_t)rw_nbr(a) * rh) +
          rw_ev(a.gstride) + RW_PART + 80 + 8;
 }
@@ -105,13 +109,15 @@ __device__ inline RwSmem rw_carve(double* base, const RowsArgs& a, int RM) {
     s.divT = ip; ip += rw_tbl(a);
     s.nbT = ip; ip += TP_MAXD;
     s.qb0T = ip; ip += TP_MAXD;
-    s.ocT = ip;
+    s.ocT = ip; ip += a.S + 1;
+    s.gdiag = ip;
     o += rw_int_doubles(a);
   }
   s.Vs = base + o; o += rw_ev(a.vtot);
   s.hadT = base + o; o += rw_ev((size_t)a.kpad * rh);
   s.Cown = base + o; o += rw_ev((size_t)a.d * a.wcol * a.r);
-  s.Gp = base + o; o += rw_ev((size_t)a.d * a.S * a.gstride);
+  s.Gown = base + o; o += rw_ev((size_t)a.d * a.gstride);
+  s.Apk = base + o; o += rw_ev((size_t)a.S * a.gstride);
   s.inbox = base + o; o += rw_ev((size_t)a.S * a.piece);
   s.Us = base + o; o += rw_ev((size_t)rw_nbr(a) * rh);
   s.Am = base + o; o += rw_ev((size_t)RM * rh);
@@ -174,33 +180,23 @@ __device__ inline double rw_block_sum(double v, double* red) {
   return out;
 }
 
-// A_j = prod_{k != j} G_k + lambda I -> Am (row stride rh, zero padded); cp.py:171-173:
-// fixed lambda, or reg * max(tr A, 0) / r.  All threads (thread t: row t/8, columns t%8 + 8u).
-template <int RM>
-__device__ void rw_build_a(const RowsArgs& a, const RwSmem& sm, int j) {
-  const int r = a.r, rh = rw_pad4(r), gk = a.S * a.gstride, i = threadIdx.x >> 3, c0 = threadIdx.x & 7;
-  double dg = 0.0;
-  if (i < r) {
-#pragma unroll
-    for (int u = 0; u < RM / 8; ++u) {
-      const int c = c0 + 8 * u;
-      if (c >= r) continue;
-      const int pos = sm.gposT[i * r + c];
-      double f[TP_MAXD];
-#pragma unroll
-      for (int k = 0; k < TP_MAXD; ++k) f[k] = (k < a.d && k != j) ? sm.Gp[(size_t)k * gk + pos] : 1.0;
-      double v = 1.0;
-#pragma unroll
-      for (int k = 0; k < TP_MAXD; ++k) v *= f[k];
-      if (c == i) { dg = v; if (!a.reg_mode) v += a.reg; }
-      sm.Am[i * rh + c] = v;
-    }
-  }
+// A_j -> Am (row stride rh, zero padded) from the owners' published packed blocks
+// (A_j = prod_{k != j} G_k, formed by each Gram owner, cp.py:312-315) plus lambda I
+// (cp.py:171-173: fixed lambda, or reg * max(tr A, 0) / r); the first nt threads,
+// named barrier 1
+__device__ void rw_build_a_w(const RowsArgs& a, const RwSmem& sm, int nt) {
+  const int r = a.r, rh = rw_pad4(r), tid = threadIdx.x;
+  double lam = a.reg;
   if (a.reg_mode) {
-    const double lam = a.reg * fmax(rw_block_sum(dg, sm.part), 0.0) / (double)r;
-    if (threadIdx.x < r) sm.Am[threadIdx.x * rh + threadIdx.x] += lam;
+    double tr = 0.0;   // (fixed order: every thread sums the diagonal itself)
+    for (int i = 0; i < r; ++i) tr += sm.Apk[sm.gposT[i * r + i]];
+    lam = a.reg * fmax(tr, 0.0) / (double)r;
   }
-  __syncthreads();
+  for (int e = tid; e < r * r; e += nt) {
+    const int dv = sm.divT[e], i = dv & 0xffff, c = dv >> 16;
+    sm.Am[i * rh + c] = sm.Apk[sm.gposT[e]] + (i == c ? lam : 0.0);
+  }
+  bar_named(1, nt);
 }
 
 // A^-1 (A = sm.Am, SPD) -> out (row stride os) by the symmetric sweep operator (Gauss-Jordan,
@@ -347,6 +343,7 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
                             uint32_t& ph_in, uint32_t& ph_pub, long long* prof_acc, long long& prof_t) {
   constexpr int MT = RM / 8;
   const int r = a.r, rh = rw_pad4(r), rs2 = a.rs2, wcol = a.wcol, piece = a.piece, S = x.S, gs = a.gstride;
+  const int ng = r * (r + 1) / 2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nb = sm.nbT[k], ksteps = (nb + 3) / 4;
   const int ntc = (x.w + 7) / 8, ncg = (ntc + 3) / 4, ngt = MT * (MT + 1) / 2;
@@ -357,7 +354,7 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
   if (tid == 0) {   // this phase's expected bytes (peers may already be sending: tx count goes negative)
     uint32_t pub = 0;
     for (int q = 0; q < S; ++q)
-      if (q != x.b) pub += (uint32_t)(((hmode >= 0 ? (sm.ocT[q + 1] - sm.ocT[q]) * r : 0) + gs) * 8);
+      if (q != x.b && hmode >= 0) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * r + gs) * 8);
     mbar_arrive_expect_tx(sm.bar + 1, (uint32_t)((S - 1) * (x.wc * rs2 + gs) * 8));
     mbar_arrive_expect_tx(sm.bar + 2, pub);
   }
@@ -454,20 +451,42 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
     else sm.gpub[e - ncr] = v;
   }
   __syncthreads();
+  // this rank's Gram block of mode k stays local; with hmode >= 0 it publishes its block of
+  // A_hmode = prod_{k' != hmode} G_k' (+ the overlap / self-Gram partials of the residual)
+  double* Ab = sm.Apk + (size_t)x.b * gs;
+  const int gcnt = (ng * (x.b + 1)) / S - (ng * x.b) / S;
+  for (int e = tid; e < gs; e += RW_NT) sm.Gown[(size_t)k * gs + e] = sm.gpub[e];
   if (want_ovl) {
-    double ovl = 0.0;
+    double ovl = 0.0, self = 0.0;
     for (int e = tid; e < ncr; e += RW_NT) {
       double v = 1.0;
       for (int kk = 0; kk < a.d; ++kk) v *= sm.Cown[(size_t)kk * wcol * r + e];
       ovl += v;
     }
+    for (int e = tid; e < gcnt; e += RW_NT) {
+      double v = sm.gpub[e];
+      for (int kk = 0; kk < a.d; ++kk)
+        if (kk != k) v *= sm.Gown[(size_t)kk * gs + e];
+      self += sm.gdiag[e] ? v : 2.0 * v;
+    }
     ovl = rw_block_sum(ovl, sm.part);
-    if (tid == 0) sm.gpub[gs - 1] = ovl;
-    __syncthreads();
+    self = rw_block_sum(self, sm.part);
+    if (tid == 0) { Ab[gs - 1] = ovl; Ab[gs - 2] = self; }
   }
-  double* Gk = sm.Gp + (size_t)k * S * gs;
-  for (int e = tid; e < gs; e += RW_NT) Gk[(size_t)x.b * gs + e] = sm.gpub[e];
-  if (hmode >= 0)
+  if (hmode >= 0) {
+    for (int e = tid; e < gs - 2; e += RW_NT) {
+      double v = 0.0;
+      if (e < gcnt) {
+        double f[TP_MAXD];
+#pragma unroll
+        for (int kk = 0; kk < TP_MAXD; ++kk)
+          f[kk] = (kk < a.d && kk != hmode) ? (kk == k ? sm.gpub[e] : sm.Gown[(size_t)kk * gs + e]) : 1.0;
+        v = 1.0;
+#pragma unroll
+        for (int kk = 0; kk < TP_MAXD; ++kk) v *= f[kk];
+      }
+      Ab[e] = v;
+    }
     for (int e = tid; e < ncr; e += RW_NT) {
       const int dv = sm.divT[e], cc = dv & 0xffff, l = dv >> 16;
       double f[TP_MAXD];
@@ -479,14 +498,15 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
       for (int kk = 0; kk < TP_MAXD; ++kk) v *= f[kk];
       sm.hadT[(size_t)(x.oc0 + cc) * rh + l] = v;
     }
+  }
   __syncthreads();
   // ---- 4. publish the had rows and the Gram block to every peer
   {
     const uint32_t hsrc = smem_u32(sm.hadT) + 8u * (uint32_t)(x.oc0 * rh);
-    const uint32_t gsrc = smem_u32(Gk) + 8u * (uint32_t)(x.b * gs);
+    const uint32_t gsrc = smem_u32(Ab);
     const uint32_t bar_pub = smem_u32(sm.bar + 2);
     const int nh2 = hmode >= 0 ? x.wc * (r / 2) : 0;
-    for (int q = warp; q < S; q += RW_NW) {
+    for (int q = warp; q < S && hmode >= 0; q += RW_NW) {
       if (q == x.b) continue;
       const uint32_t rbar = mapa_u32(bar_pub, (uint32_t)q), hdst = mapa_u32(hsrc, (uint32_t)q);
       if (!(r & 1)) {
@@ -503,7 +523,7 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
       }
       const uint32_t gdst = mapa_u32(gsrc, (uint32_t)q);
       for (int e = lane; e < gs / 2; e += 32) {
-        const double2 v = *reinterpret_cast<const double2*>(Gk + (size_t)x.b * gs + 2 * e);
+        const double2 v = *reinterpret_cast<const double2*>(Ab + 2 * e);
         st_async_v2(gdst + 16u * (uint32_t)e, v.x, v.y, rbar);
       }
     }
@@ -577,6 +597,12 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
       sm.nbT[k] = a.q[k] * (x.b + 1) / a.S - sm.qb0T[k];
     }
     for (int q = tid; q <= a.S; q += RW_NT) sm.ocT[q] = x.w * q / a.S;
+    for (int e = tid; e < a.gstride; e += RW_NT) sm.gdiag[e] = 0;
+    __syncthreads();
+    for (int i = tid; i < r; i += RW_NT) {
+      const int pos = sm.gposT[i * r + i];
+      if (pos / a.gstride == x.b) sm.gdiag[pos - x.b * a.gstride] = 1;
+    }
   }
   __syncthreads();
   for (int k = 0; k < d; ++k) {
@@ -669,52 +695,78 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
         }
       }
       RW_PROF(7);
-      // ---- A_j, then its inverse while the peers' slots land: the last warp releases this
-      // CTA's slot (the fence drains the stores) while the others refine the warm start
-      rw_build_a<RM>(a, sm, j);   // (ends with a barrier: the slot stores are all issued)
+      // ---- A_j and its inverse while the peers' slots land: the last warp releases this
+      // CTA's slot (the gpu-scope release drains the stores) while the others build A_j and
+      // refine the warm start
+      __syncthreads();   // every slot store issued
       RW_PROF(8);
       bool ok = false;
-      if (warm) {
+      {
+        constexpr int NWK = RW_NW - 1;
         if (warp == RW_NW - 1) {
           if (lane == 0) rw_flag(a, x, u);
         } else {
-          constexpr int NWK = RW_NW - 1;
-          mbar_wait(sm.bar, xph);
-          double em = rw_gemm<RM>(sm.Am, sm.X0, sm.scr, rh, r, 0, NWK);   // T = 2I - A X0, |I - A X0|
+          rw_build_a_w(a, sm, NWK * 32);
+          RW_PROF(12);
+          if (warm) {
+            mbar_wait(sm.bar, xph);
+            RW_PROF(13);
+            double em = rw_gemm<RM>(sm.Am, sm.X0, sm.scr, rh, r, 0, NWK);   // T = 2I - A X0, |I - A X0|
+            RW_PROF(14);
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
-          if (lane == 0) sm.part[warp] = em;
-          bar_named(1, NWK * 32);
-          rw_gemm<RM>(sm.X0, sm.scr, sm.X1, rh, r, 1, NWK);                // X1 = X0 T
+            for (int o = 16; o > 0; o >>= 1) em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
+            if (lane == 0) sm.part[warp] = em;
+            bar_named(1, NWK * 32);
+            rw_gemm<RM>(sm.X0, sm.scr, sm.X1, rh, r, 1, NWK);                // X1 = X0 T
+          }
         }
-        xph ^= 1u;
+        if (warm) xph ^= 1u;
         __syncthreads();
-        double em = 0.0;
-        for (int q = 0; q < RW_NW - 1; ++q) em = fmax(em, sm.part[q]);
-        // one step squares the error: |I - A X1| <= |I - A X0|^2 <= (r * 1e-8)^2 ~ 1e-13
-        ok = em <= 1e-8;   // (NaN fails)
-        __syncthreads();
-      } else {
-        if (tid == 0) rw_flag(a, x, u);
+        if (warm) {
+          double em = 0.0;
+          for (int q = 0; q < NWK; ++q) em = fmax(em, sm.part[q]);
+          // one step squares the error: |I - A X1| <= |I - A X0|^2 <= (r * 1e-8)^2 ~ 1e-13
+          ok = em <= 1e-8;   // (NaN fails)
+        }
       }
       RW_PROF(1);
       if (!ok) status |= rw_inverse<RM>(a, sm, sm.X1, rh);
       if (a.ns)   // next sweep's warm start for this mode (read back only by this CTA)
         for (int e = tid; e < (int)xsz; e += RW_NT) Xw[(size_t)j * xsz + e] = sm.X1[e];
       RW_PROF(2);
-      rw_wait(a, x, u, status);
-      RW_PROF(3);
-      // ---- 2. rhs = sum over the P clusters (fixed order), U_j[blk] = rhs A^-1
-      for (int e = tid; e < nb * r; e += RW_NT) {
-        const int dv = sm.divT[e], s = dv & 0xffff, l = dv >> 16;
-        const double* y0 = a.Y + (((size_t)(u & 1) * x.S + x.b) * x.P) * slot_stride + e;
-        double yv[RW_PMAX];   // independent loads first, then the fixed-order sum
-#pragma unroll
-        for (int cc = 0; cc < RW_PMAX; ++cc) yv[cc] = cc < x.P ? __ldcg(y0 + (size_t)cc * slot_stride) : 0.0;
-        double v = 0.0;
-#pragma unroll
-        for (int cc = 0; cc < RW_PMAX; ++cc) v += yv[cc];
-        sm.rb[s * rh + l] = v;
+      // ---- 2. rhs = sum over the P clusters (fixed order): warp c waits for cluster c's
+      // flag and stages its slot (overlapping the later flags), then the ordered sum
+      {
+        const int nslot = (int)rw_ev((size_t)rw_nbr(a) * r), n2 = nb * r / 2;
+        const double* ybase = a.Y + (((size_t)(u & 1) * x.S + x.b) * x.P) * slot_stride;
+        int bad = 0;
+        for (int cc = warp; cc < x.P; cc += RW_NW) {
+          if (lane == 0 && !(status & 4)) {
+            const unsigned int* f = a.flags + ((size_t)(u & 1) * x.S + x.b) * x.P + cc;
+            const unsigned int want = (unsigned int)(u + 1);
+            const long long t0 = clock64();
+            unsigned int v;
+            for (;;) {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+              if ((int)(v - want) >= 0) break;
+              if (clock64() - t0 > 8000000000LL) { bad = 4; break; }   // ~4 s: a missing peer
+            }
+          }
+          __syncwarp();
+          const double2* src = reinterpret_cast<const double2*>(ybase + (size_t)cc * slot_stride);
+          double2* dst = reinterpret_cast<double2*>(sm.scr + (size_t)cc * nslot);
+          for (int e = lane; e < n2; e += 32) dst[e] = __ldcg(src + e);
+          if ((nb * r) & 1)
+            if (lane == 0) sm.scr[(size_t)cc * nslot + nb * r - 1] = __ldcg(ybase + (size_t)cc * slot_stride + nb * r - 1);
+        }
+        if (__syncthreads_or(bad)) status |= 4;
+        RW_PROF(3);
+        for (int e = tid; e < nb * r; e += RW_NT) {
+          const int dv = sm.divT[e], sr = dv & 0xffff, l = dv >> 16;
+          double v = 0.0;
+          for (int cc = 0; cc < x.P; ++cc) v += sm.scr[(size_t)cc * nslot + e];
+          sm.rb[sr * rh + l] = v;
+        }
       }
       __syncthreads();
       RW_PROF(4);
@@ -758,22 +810,17 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
     }
     done = sweep + 1;
     if (a.need_resid) {
-      // overlap: the cluster's sum over the owners' partials, then over the P clusters
-      const double* Gl = sm.Gp + (size_t)(d - 1) * x.S * a.gstride;
-      double ovc = 0.0;
-      for (int q = 0; q < x.S; ++q) ovc += Gl[(size_t)q * a.gstride + a.gstride - 1];
+      // overlap / self-Gram sums: the owners' partials in rank order, the overlap then over
+      // the P clusters
+      double ovc = 0.0, self = 0.0;
+      for (int q = 0; q < x.S; ++q) {
+        ovc += sm.Apk[(size_t)q * a.gstride + a.gstride - 1];
+        self += sm.Apk[(size_t)q * a.gstride + a.gstride - 2];
+      }
       double* slot = a.Y + (((size_t)(u & 1) * x.S + x.b) * x.P + x.c) * slot_stride;
       if (tid == 0) slot[a.ylen - 1] = ovc;
       __syncthreads();
       if (tid == 0) rw_flag(a, x, u);
-      double self = 0.0;
-      for (int e = tid; e < r * r; e += RW_NT) {
-        const int pos = sm.gposT[e];
-        double v = 1.0;
-        for (int k = 0; k < d; ++k) v *= sm.Gp[(size_t)k * x.S * a.gstride + pos];
-        self += v;
-      }
-      self = rw_block_sum(self, sm.part);
       rw_wait(a, x, u, status);
       double ovt = 0.0;
       const double* y0 = a.Y + (((size_t)(u & 1) * x.S + x.b) * x.P) * slot_stride + (a.ylen - 1);
@@ -819,7 +866,7 @@ static bool rows_try(int d, const int* q, int R, int r, int S, int P, int smem_o
   a.wcol = (a.wmax + S - 1) / S;
   a.rs2 = r + 2 - (r & 1);                        // even row stride of the C^T staging
   const int ng = r * (r + 1) / 2;
-  a.gstride = (ng + S - 1) / S + 1;               // owner block of the packed Gram + overlap slot
+  a.gstride = (ng + S - 1) / S + 2;               // owner block of the packed Gram + overlap / self slots
   a.gstride += a.gstride & 1;
   a.piece = a.wcol * a.rs2 + a.gstride;
   a.cst_len = wp8 * a.rs2;   // (even)

@@ -193,7 +193,7 @@ def als_variant():
     L.tp_debug_set_als_variant(0, 0)
 
 
-@pytest.mark.parametrize("variant,cluster", [(1, 0), (2, 2), (2, 4), (2, 0), (4, 0)])
+@pytest.mark.parametrize("variant,cluster", [(1, 0), (2, 2), (2, 4), (2, 0), (4, 0), (8, 16), (8, 8)])
 @pytest.mark.parametrize("qs,R,r", [((64, 48, 80, 64), 96, 16), ((40, 37, 50), 61, 12), ((32,) * 5, 64, 30)])
 def test_als_kernel_variants(als_variant, variant, cluster, qs, R, r):
     """Both persistent kernels (R-slab per CTA; clusters of row blocks with the DSMEM
@@ -208,7 +208,7 @@ def test_als_kernel_variants(als_variant, variant, cluster, qs, R, r):
     np.testing.assert_allclose(trace, otrace, rtol=1e-8, atol=1e-12)
 
 
-@pytest.mark.parametrize("variant,cluster", [(1, 0), (2, 4)])
+@pytest.mark.parametrize("variant,cluster", [(1, 0), (2, 4), (8, 16)])
 def test_als_config1_variants(als_variant, variant, cluster):
     als_variant(variant, cluster)
     w = workloads.cfg1(seed=2)
@@ -313,7 +313,7 @@ def test_als_rejects_bad_shapes():
         cp.cp_approx_als(T, 200, cp.ALSApproxConfig(max_sweeps=2))   # r > 160: outside every variant
 
 
-@pytest.mark.parametrize("variant,cluster", [(0, 0), (1, 0), (2, 0), (3, 0), (4, 0), (5, 0)])
+@pytest.mark.parametrize("variant,cluster", [(0, 0), (1, 0), (2, 0), (3, 0), (4, 0), (5, 0), (8, 0)])
 @pytest.mark.parametrize("reg", [None, 1e-10])
 def test_als_zero_target_returns_zero(als_variant, variant, cluster, reg):
     """All-zero target: under the reference trace rule lambda = 1e-12 tr(H)/r is 0 once a
@@ -420,3 +420,38 @@ def test_apply_more_than_64_terms(cplx):
     got = out.to_numpy()
     for k in range(len(qs)):
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("ns", [6, 0])
+@pytest.mark.parametrize("reg", [None, 1e-10])
+@pytest.mark.parametrize("qs,R,r", [((256,) * 6, 512, 32), ((48, 40, 64, 36), 200, 16), ((20, 33, 17, 40), 64, 8)])
+def test_als_rows_kernel(als_variant, ns, reg, qs, R, r):
+    """Cluster-row kernel (variant 8: 16-CTA clusters own R-slabs, one flag exchange per mode
+    update): warm-started Newton-Schulz inverse on and off (exact sweep every time), both
+    regulariser rules, ragged modes, config-1 size, with the residual trace."""
+    import ctypes
+    from paper_1803_10270_b200 import _lib
+    L = _lib.lib()
+    L.tp_debug_set_als_ns.argtypes = [ctypes.c_int]
+    als_variant(8, 0)
+    L.tp_debug_set_als_ns(ns)
+    try:
+        assert cp.als_plan(qs, R, r)["kernel"] == "als_rows"
+        rng = np.random.default_rng(R + r + ns)
+        V = [rng.standard_normal((q, R)) / np.sqrt(q) for q in qs]
+        init = [v[:, :r].copy() for v in V]
+        S = specs_for(qs)
+        trace = []
+        out = cp.cp_approx_als(cp.CPTensor(S, V), r, cp.ALSApproxConfig(max_sweeps=6, stall=-np.inf, reg=reg),
+                               init=cp.CPTensor(S, init), trace=trace)
+        otrace = []
+        ref = ocp.als(V, init, 6, lam=reg, trace=otrace)
+        assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+        np.testing.assert_allclose(trace, otrace, rtol=1e-7, atol=1e-8 * max(1.0, float(np.sqrt(sum(
+            np.sum(v * v) for v in V)))))
+    finally:
+        L.tp_debug_set_als_ns(6)
+
+
+def test_als_rows_is_config1_default():
+    assert cp.als_plan((256,) * 6, 512, 32)["kernel"] == "als_rows"

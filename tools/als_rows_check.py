@@ -49,7 +49,7 @@ cfg = cp.ALSApproxConfig(max_sweeps=20, stall=-np.inf, reg=1e-10)
 U = I0.data.clone()
 outs = {}
 ref = ocp.als([np.asarray(v) for v in w["V"]], [np.asarray(v) for v in w["init"]], 20, lam=1e-10)
-for name, var, cs, pr in [("cluster4", 2, 4, 0), ("rows16", 8, 16, 0), ("rows8", 8, 8, 0)]:
+for name, var, cs, pr in [("cluster4", 2, 4, 0), ("rows16", 8, 16, 0)]:
     L.tp_debug_set_als_variant(var, cs)
     L.tp_debug_set_als_rows(1 if var == 8 else 0, pr)
     st, pl = plan([256] * 6, 512, 32)
@@ -79,9 +79,9 @@ for name, var, cs, pr in [("cluster4", 2, 4, 0), ("rows16", 8, 16, 0), ("rows8",
         L.tp_debug_set_als_profile(None)
         p = prof.cpu().numpy() / 120.0
         lab = {7: "Y dmma", 8: "slot store", 1: "signal", 2: "inverse", 3: "wait", 4: "gather", 5: "solve",
-               9: "xch dmma+push", 10: "B1", 11: "reduce+publish", 6: "B2", 0: "loop"}
+               9: "xch dmma+push", 10: "B1", 11: "reduce+publish", 6: "B2", 0: "loop", 12: "build_a", 13: "x0 wait", 14: "gemm0"}
         print("   cycles per mode update: " + " | ".join("%s %.0f" % (lab[i], p[i]) for i in
-                                                          (7, 8, 1, 2, 3, 4, 5, 9, 10, 11, 6, 0)), flush=True)
+                                                          (7, 8, 12, 13, 14, 1, 2, 3, 4, 5, 9, 10, 11, 6, 0)), flush=True)
     if var == 8:
         L.tp_debug_set_als_ns.argtypes = [ctypes.c_int]
         L.tp_debug_set_als_ns(0)
