@@ -29,16 +29,16 @@ __device__ __forceinline__ int sturm_count(const double* dg, const double* e2, i
   int c = q < 0.0;
   for (int t = 1; t < n; ++t) {
     if (fabs(q) < pivmin) q = -pivmin;
-    q = (dg[t] - x) - e2[t - 1] / q;
+    q = (dg[t] - x) - e2[t - 1] * rcp_nr(q);   // (<= 1 ulp: the count is backward stable)
     c += q < 0.0;
   }
   return c;
 }
 
-// LU with partial pivoting of T - lam I (tridiagonal: diag dg, off-diagonal of),
-// then solve in place for b; zero pivots replaced by eps3 (dlagtf / dlagts).
-__device__ void tri_solve(const double* dg, const double* of, int n, double lam, double eps3, double* b,
-                          double* u0, double* u1, double* u2, double* ml, unsigned char* piv) {
+// LU with partial pivoting of T - lam I (tridiagonal: diag dg, off-diagonal of); zero
+// pivots replaced by eps3 (dlagtf).  u0 holds the reciprocal pivots.
+__device__ void tri_factor(const double* dg, const double* of, int n, double lam, double eps3, double* u0, double* u1,
+                           double* u2, double* ml, unsigned char* piv) {
   double a = dg[0] - lam;
   double c = n > 1 ? of[0] : 0.0;
   for (int i = 0; i < n - 1; ++i) {
@@ -46,31 +46,34 @@ __device__ void tri_solve(const double* dg, const double* of, int n, double lam,
     const double cn = (i + 1 < n - 1) ? of[i + 1] : 0.0;  // next super-diagonal
     if (fabs(a) >= fabs(bi)) {   // no interchange
       piv[i] = 0;
-      const double aa = (a == 0.0) ? eps3 : a;
-      const double m = bi / aa;
-      u0[i] = aa; u1[i] = c; u2[i] = 0.0; ml[i] = m;
+      const double ia = rcp_nr((a == 0.0) ? eps3 : a);
+      const double m = bi * ia;
+      u0[i] = ia; u1[i] = c; u2[i] = 0.0; ml[i] = m;
       a = dn - m * c;
       c = cn;
     } else {                     // swap rows i, i+1
       piv[i] = 1;
-      const double m = a / bi;
-      u0[i] = bi; u1[i] = dn; u2[i] = cn; ml[i] = m;
+      const double m = a * rcp_nr(bi);
+      u0[i] = rcp_nr(bi); u1[i] = dn; u2[i] = cn; ml[i] = m;
       a = c - m * dn;
       c = -m * cn;
     }
   }
-  u0[n - 1] = (a == 0.0) ? eps3 : a;
-  // forward: L y = P b
-  for (int i = 0; i < n - 1; ++i) {
+  u0[n - 1] = rcp_nr((a == 0.0) ? eps3 : a);
+}
+
+// solve in place for b with the factors of tri_factor (dlagts)
+__device__ void tri_apply(int n, double* b, const double* u0, const double* u1, const double* u2, const double* ml,
+                          const unsigned char* piv) {
+  for (int i = 0; i < n - 1; ++i) {   // forward: L y = P b
     if (piv[i]) { const double t = b[i]; b[i] = b[i + 1]; b[i + 1] = t; }
     b[i + 1] -= ml[i] * b[i];
   }
-  // back: U x = y
-  for (int i = n - 1; i >= 0; --i) {
+  for (int i = n - 1; i >= 0; --i) {   // back: U x = y
     double s = b[i];
     if (i + 1 < n) s -= u1[i] * b[i + 1];
     if (i + 2 < n) s -= u2[i] * b[i + 2];
-    b[i] = s / u0[i];
+    b[i] = s * u0[i];
   }
 }
 
@@ -210,65 +213,57 @@ __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int 
   const double tn = scal[5];
   const double eps3 = fmax(DBL_EPSILON * tn, DBL_MIN);
   const double ortol = 1e-3 * tn;
+  // shifts (equal eigenvalues perturbed apart, dstein: 10 eps3) and clusters (consecutive
+  // kept eigenvalues closer than ortol share a cluster: cs[t] = its first member)
+  double* shf = scal + 8;                          // [nvec]
+  int* cs = reinterpret_cast<int*>(shf + nvec);    // [nvec]
   if (tid < nvec) {
     const int t = tid;
     double lt = lam[n - 1 - t];
+    for (int q = 1; q <= t; ++q)
+      if (fabs(lam[n - 1 - t + q] - lt) < 10.0 * eps3) lt -= 10.0 * eps3 * q; else break;
+    shf[t] = lt;
+    int c0 = t;
+    while (c0 > 0 && lam[n - c0] - lam[n - 1 - c0] < ortol) --c0;
+    cs[t] = c0;
     double* zt = Z + (size_t)t * n;
-    double u0[TE_KMAX], u1[TE_KMAX], u2[TE_KMAX], ml[TE_KMAX];
-    unsigned char piv[TE_KMAX];
-    // perturb equal eigenvalues apart (dstein: 10 eps3)
-    for (int s = 1; s <= t; ++s)
-      if (fabs(lam[n - 1 - t + s] - lt) < 10.0 * eps3) lt -= 10.0 * eps3 * s; else break;
     for (int i = 0; i < n; ++i) zt[i] = 1.0 + 0.0625 * (double)((i * 37 + t * 11) % 13) / 13.0;
-    for (int it = 0; it < 3; ++it) {
-      tri_solve(dg, of, n, lt, eps3, zt, u0, u1, u2, ml, piv);
+  }
+  __syncthreads();
+  // inverse iteration, all kept vectors at once (one thread each), each solve preceded by
+  // modified Gram-Schmidt of the cluster members against their earlier members (dstein),
+  // done by warp 0 with the vectors spread over the lanes
+  double u0[TE_KMAX], u1[TE_KMAX], u2[TE_KMAX], ml[TE_KMAX];   // this thread's LU of T - shift I
+  unsigned char piv[TE_KMAX];
+  if (tid < nvec) tri_factor(dg, of, n, shf[tid], eps3, u0, u1, u2, ml, piv);
+  for (int it = 0; it < 4; ++it) {
+    if (warp == 0) {
+      for (int t = 1; t < nvec; ++t) {
+        double* zs = Z + (size_t)t * n;
+        for (int q = cs[t]; q < t; ++q) {
+          const double* zq = Z + (size_t)q * n;
+          double dot = 0.0, nq = 0.0;
+          for (int i = lane; i < n; i += 32) { dot = fma(zq[i], zs[i], dot); nq = fma(zq[i], zq[i], nq); }
+          dot = warp_sum(dot);
+          nq = warp_sum(nq);
+          const double f = nq > 0.0 ? dot / nq : 0.0;
+          for (int i = lane; i < n; i += 32) zs[i] = fma(-f, zq[i], zs[i]);
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+    if (it == 3) break;   // (the last pass only orthogonalises)
+    if (tid < nvec) {
+      double* zt = Z + (size_t)tid * n;
+      tri_apply(n, zt, u0, u1, u2, ml, piv);
       double mx = 0.0;
       for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(zt[i]));
       const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
       for (int i = 0; i < n; ++i) zt[i] *= inv;
     }
+    __syncthreads();
   }
-  __syncthreads();
-  // clusters: re-iterate members with Gram-Schmidt against the earlier ones (thread 0,
-  // rare: only eigenvalues closer than 1e-3 ||T||)
-  if (tid == 0) {
-    double u0[TE_KMAX], u1[TE_KMAX], u2[TE_KMAX], ml[TE_KMAX];
-    unsigned char piv[TE_KMAX];
-    int c0 = 0;
-    for (int t = 1; t <= nvec; ++t) {
-      const bool split = (t == nvec) || (lam[n - t] - lam[n - 1 - t] >= ortol);
-      if (!split) continue;
-      if (t - c0 > 1) {   // members c0 .. t-1
-        for (int s = c0; s < t; ++s) {
-          double* zs = Z + (size_t)s * n;
-          double lt = lam[n - 1 - s] - 10.0 * eps3 * (s - c0);
-          for (int it = 0; it < 3; ++it) {
-            for (int q = c0; q < s; ++q) {   // MGS against the finished members
-              const double* zq = Z + (size_t)q * n;
-              double dot = 0.0, nq = 0.0;
-              for (int i = 0; i < n; ++i) { dot = fma(zq[i], zs[i], dot); nq = fma(zq[i], zq[i], nq); }
-              const double f = dot / nq;
-              for (int i = 0; i < n; ++i) zs[i] = fma(-f, zq[i], zs[i]);
-            }
-            tri_solve(dg, of, n, lt, eps3, zs, u0, u1, u2, ml, piv);
-            double mx = 0.0;
-            for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(zs[i]));
-            const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
-            for (int i = 0; i < n; ++i) zs[i] *= inv;
-          }
-          for (int q = c0; q < s; ++q) {
-            const double* zq = Z + (size_t)q * n;
-            double dot = 0.0, nq = 0.0;
-            for (int i = 0; i < n; ++i) { dot = fma(zq[i], zs[i], dot); nq = fma(zq[i], zq[i], nq); }
-            const double f = dot / nq;
-            for (int i = 0; i < n; ++i) zs[i] = fma(-f, zq[i], zs[i]);
-          }
-        }
-      }
-      c0 = t;
-    }
-  }
-  __syncthreads();
   // ---- 4. normalise, back-transform z <- H_0 .. H_{n-3} z (16 lanes per vector)
   for (int v0 = 0; v0 < nvec; v0 += TE_NT / 16) {
     const int t = v0 + (tid >> 4), sl = tid & 15;
@@ -313,7 +308,7 @@ __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int 
 }
 
 size_t tridiag_eigh_smem(int k, int nvec) {
-  return sizeof(double) * ((size_t)k * (k + 1) + 7 * (size_t)k + (size_t)nvec * k + 8);
+  return sizeof(double) * ((size_t)k * (k + 1) + 7 * (size_t)k + (size_t)nvec * k + 8 + 2 * (size_t)nvec);
 }
 
 cudaError_t launch_tridiag_eigh(int nmat, int k, int nn, int first, int per, const double* Ain, double* Vout,
