@@ -374,15 +374,24 @@ def _relative_error(f: CPTensor, g: CPTensor, nf: float) -> float:
     return float(math.sqrt(max(d, 0.0)) / nf)
 
 
-def rank_reduce_als(f: CPTensor, r_target: int, eps: float, config: ALSApproxConfig | None = None) -> CPTensor:
+def rank_reduce_als(f: CPTensor, r_target: int, eps: float, config: ALSApproxConfig | None = None, *,
+                    draws: str = "auto") -> CPTensor:
     """Adaptive rank 1..r_target, warm start + one fresh random term (cp.py:337-366).
-    Complex targets draw the reference's complex random terms from the same
-    generator sequence; real targets draw real terms (real fp64 path)."""
+
+    ``draws="reference"``: the reference's complex random terms from the same generator
+    sequence for every target (real targets then fit in complex128, exactly as the
+    reference does: its result is complex).  ``draws="auto"`` (default): complex draws
+    for complex targets, real N(0,1) draws for real targets (the real fp64 kernels; a
+    documented deviation)."""
     if r_target < 1:
         raise ValueError("target rank must be at least 1")
+    if draws not in ("auto", "reference"):
+        raise ValueError(f"draws must be 'auto' or 'reference', not {draws!r}")
     cfg = config or ALSApproxConfig()
     nf = norm(f)
-    cz = f.is_complex
+    cz = f.is_complex or draws == "reference"
+    if cz:
+        f = as_complex(f)
     zero = CPTensor(f.specs, [np.zeros((s.Q, 1)) for s in f.specs])
     if cz:
         zero = as_complex(zero)

@@ -42,6 +42,7 @@ class ExplicitConfig:
     startup: str = "rk2"
     als: ALSApproxConfig = field(default_factory=ALSApproxConfig)
     recipe: str = "split"       # "split" (reference) or "fused" (BASELINE cfg0/cfg3)
+    draws: str = "auto"         # rank_reduce_als random terms: "reference" = complex (cp.py:356-360)
 
     def __post_init__(self):
         if self.dt <= 0:
@@ -54,6 +55,8 @@ class ExplicitConfig:
             raise ValueError(f"unknown startup rule {self.startup!r}")
         if self.recipe not in ("split", "fused"):
             raise ValueError(f"unknown recipe {self.recipe!r}")
+        if self.draws not in ("auto", "reference"):
+            raise ValueError(f"unknown draws {self.draws!r}")
 
 
 @dataclass
@@ -83,7 +86,7 @@ def _reduce(f, config: ExplicitConfig, stage: str, log, init=None):
         if config.recipe == "fused" and init is not None and init.rank == config.r_max:
             red = cp.cp_approx_als(f, config.r_max, config.als, init=init)
         else:
-            red = rank_reduce_als(f, config.r_max, config.eps_rank, config.als)
+            red = rank_reduce_als(f, config.r_max, config.eps_rank, config.als, draws=config.draws)
         if log is not None:
             log.append(ReductionRecord(stage, f.rank, red.rank, _gap(f, red)))
         return red

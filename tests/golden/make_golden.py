@@ -489,6 +489,12 @@ def gen_complex():
     red = cp.rank_reduce_als(f, 3, 1e-9)
     pack_cp("rr_f", f, store)
     pack_cp("rr_out", red, store)
+    # a REAL target (exactly rank 2): the reference still draws complex random terms, so its
+    # fit is complex -- pins rank_reduce_als(..., draws="reference") on real data
+    fr = cp.CPTensor(specs, [np.random.default_rng(43).standard_normal((s.Q, 2)) for s in specs])
+    redr = cp.rank_reduce_als(fr, 3, 1e-9)
+    pack_cp("rrr_f", fr, store)
+    pack_cp("rrr_out", redr, store)
     # explicit split recipe: 2-D sheared advection, Galerkin Q = 9
     specs2 = (BasisSpec(9, 3.0), BasisSpec(9, 3.0))
     op = operators.advection_operator(spiral_matrix(2, 2.0), specs2)

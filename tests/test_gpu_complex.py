@@ -132,6 +132,24 @@ def test_complex_rank_reduce_golden():
     assert metrics.cp_rel_diff(gold, got) <= 2e-8
 
 
+def test_rank_reduce_reference_draws_real_target_golden():
+    """rank_reduce_als(..., draws="reference") on a REAL target: the reference's complex
+    random terms (cp.py:356-360), so the fit is complex like the reference's; pinned to
+    the reference's own output (tests/golden/make_golden.py gen_complex, rrr_*)."""
+    g = load_golden("complex")
+    S = (BasisSpec(5, 1.5), BasisSpec(7, 2.0), BasisSpec(3, 0.8))
+    f = unpack_cp(g, "rrr_f")
+    assert not any(np.iscomplexobj(x) and np.any(x.imag) for x in f)
+    out = cp.rank_reduce_als(cp.CPTensor(S, f), 3, 1e-9, draws="reference")
+    gold = unpack_cp(g, "rrr_out")
+    assert out.is_complex and out.rank == gold[0].shape[1]
+    got = out.to_numpy()
+    assert metrics.cp_rel_diff(f, got) <= 1.5 * metrics.cp_rel_diff(f, gold) + 1e-12
+    assert metrics.cp_rel_diff(gold, got) <= 2e-8
+    with pytest.raises(ValueError, match="draws"):
+        cp.rank_reduce_als(cp.CPTensor(S, f), 3, 1e-9, draws="nope")
+
+
 def test_complex_explicit_split_recipe_golden():
     """The reference's explicit recipe (explicit.py:85-103, rank_reduce_als at every
     stage) on the complex Galerkin basis, 2-D sheared advection, RK2 + 2 AB2 steps."""
