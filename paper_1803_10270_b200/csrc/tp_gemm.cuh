@@ -25,6 +25,10 @@ struct BGemm {
   int ksplit;                // split-K factor (>1: partial tiles to `part`, then bgemm_reduce)
   double* part;              // [nb1*nb2][ksplit][M][N] partials when ksplit > 1
   const int* skip;           // optional device flag: nonzero -> the launch is a no-op (stream-ordered early exit)
+  // two-level K addressing of a K-contiguous B (pipelined kernel only): k -> (k / kinB) * sBk1 + k % kinB,
+  // e.g. the (a, j) pairs of a transfer tensor B[a][b][j] read for fixed b without a transpose
+  int kinB;                  // 0: plain k * sBk
+  long long sBk1;
 };
 
 // 8-byte global -> shared async copy (LDGSTS); src_bytes = 0 zero-fills
@@ -201,17 +205,20 @@ static __global__ void __launch_bounds__(128) bgemm_pipe_kernel(const __grid_con
     }
   };
   // K-contiguous operand -> [i][k] tile (row stride LDK), 16-byte copies of k pairs
-  auto load_tile_k = [&](const double* X, long long sXi, int I, int i0, bool vec, double* dst, int k0) {
+  auto load_tile_k = [&](const double* X, long long sXi, int I, int i0, bool vec, double* dst, int k0, int kin,
+                         long long sk1) {
+    // (kin > 0: the k-tile lies inside one run of kin contiguous k, kin a multiple of TK)
+    const long long kb = kin > 0 ? (long long)(k0 / kin) * sk1 + (k0 % kin) - k0 : 0;
 #pragma unroll 2
     for (int e = tid; e < GB_TM * TK / 2; e += 128) {
       const int ii = e / (TK / 2), kk = 2 * (e % (TK / 2));
       const int i = i0 + ii, k = k0 + kk;
       double* d = dst + ii * LDK + kk;
       if (vec && i < I && k + 1 < g.K) {
-        cp_async16(d, X + i * sXi + k);
+        cp_async16(d, X + i * sXi + k + kb);
       } else {
-        cp_async8(d, X + ((i < I && k < g.K) ? i * sXi + k : 0), i < I && k < g.K);
-        cp_async8(d + 1, X + ((i < I && k + 1 < g.K) ? i * sXi + k + 1 : 0), i < I && k + 1 < g.K);
+        cp_async8(d, X + ((i < I && k < g.K) ? i * sXi + k + kb : 0), i < I && k < g.K);
+        cp_async8(d + 1, X + ((i < I && k + 1 < g.K) ? i * sXi + k + 1 + kb : 0), i < I && k + 1 < g.K);
       }
     }
   };
@@ -219,9 +226,9 @@ static __global__ void __launch_bounds__(128) bgemm_pipe_kernel(const __grid_con
   const bool bk_vec = BK && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) && (g.sBn % 2 == 0);
   auto issue = [&](int kt, int buf) {
     const int k0 = kt * TK;
-    if (AK) load_tile_k(A, g.sAm, g.M, m0, ak_vec, As + (size_t)buf * SA, k0);
+    if (AK) load_tile_k(A, g.sAm, g.M, m0, ak_vec, As + (size_t)buf * SA, k0, 0, 0);
     else load_tile(A, g.sAm, g.sAk, g.M, m0, a_m_fast, a_vec, As + (size_t)buf * SA, k0);
-    if (BK) load_tile_k(B, g.sBn, g.N, n0, bk_vec, Bs + (size_t)buf * SB, k0);
+    if (BK) load_tile_k(B, g.sBn, g.N, n0, bk_vec, Bs + (size_t)buf * SB, k0, g.kinB, g.sBk1);
     else load_tile(B, g.sBn, g.sBk, g.N, n0, b_n_fast, b_vec, Bs + (size_t)buf * SB, k0);
   };
   // prologue: STAGES - 1 tiles in flight (one commit group per stage, possibly empty)
@@ -346,7 +353,10 @@ static inline cudaError_t bgemm_launch(const BGemm& g, cudaStream_t st) {
   BGemm h = g;
   h.ksplit = ks;
   dim3 grid((g.N + GB_TN - 1) / GB_TN, (g.M + GB_TM - 1) / GB_TM, g.nb1 * g.nb2 * ks);
-  switch (g_bgemm_variant) {
+  // two-level K addressing exists in the K-contiguous path of the pipelined kernels only
+  const int variant = (g.kinB > 0 && (g_bgemm_variant == 0 || g.sBk != 1 || g.kinB % 32 != 0)) ? 1 : g_bgemm_variant;
+  if (g.kinB > 0 && (g.sBk != 1 || g.kinB % 16 != 0)) return cudaErrorInvalidValue;
+  switch (variant) {
     case 1: bgemm_pipe_launch<3, 16>(grid, h, st); break;
     case 2: bgemm_pipe_launch<2, 32>(grid, h, st); break;
     case 3: bgemm_pipe_launch<3, 32>(grid, h, st); break;

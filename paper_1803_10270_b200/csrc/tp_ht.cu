@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(256) form_g_kernel(int k, int nn, const double
 // -- the rank the reference's QR orthogonalisation (ht.py:294-310) leaves; eigenvalues
 // past it are rounding noise of the Gramian gauge and are never kept
 __global__ void keep_rule_kernel(int k, int nn, int nb, int ndim, double eps, int r_max, const double* sig,
-                                 const double* Mf, int* keep, double* disc, const int* bound) {
+                                 const double* Mf, int* keep, double* disc, const int* bound, double* Wz, int ro) {
   const int z = blockIdx.x * blockDim.x + threadIdx.x;
   const int per = nn - 1;
   if (z >= nb * per) return;
@@ -566,6 +566,11 @@ __global__ void keep_rule_kernel(int k, int nn, int nb, int ndim, double eps, in
   }
   keep[b * nn + t] = kp;
   disc[b * nn + t] = tail;
+  if (Wz) {   // discarded eigenvectors -> zero columns (the GEMM formation of S_t / T_t)
+    double* W = Wz + ((size_t)b * nn + t) * k * k;
+    for (int i = 0; i < k; ++i)
+      for (int c = kp; c < ro; ++c) W[(size_t)i * k + c] = 0.0;
+  }
 }
 
 __global__ void finish_kernel(int k, int nn, int nb, const double* Mf, const int* keep, const double* disc,
@@ -578,6 +583,63 @@ __global__ void finish_kernel(int k, int nn, int nb, const double* Mf, const int
   norms[b] = sqrt(fmax(Mf[(size_t)b * nn * k * k], 0.0));
   out_ranks[b * nn] = 1;
   for (int t = 1; t < nn; ++t) out_ranks[b * nn + t] = keep[b * nn + t];
+}
+
+// Frame factor F (M_t = F F^T on its range) and its pseudo-inverse Fi for every non-root
+// node, so that the node Gram G_t = F^T Gh F and the kept basis S_t = Fi^T W_keep,
+// T_t = W_keep^T F^T become batched DMMA GEMMs: Cholesky nodes F = L, Fi = L^-1 (column-
+// parallel forward substitution, 4 threads per column); eigh nodes F = V diag(s),
+// Fi = diag(mu) V^T with s = sqrt(l), mu = 1/sqrt(l) on the kept range (m < bound,
+// l > 1e-14 l_max, the thresholded pseudo-inverse of form_st) and 0 elsewhere.
+__global__ void __launch_bounds__(256) frame_factor_kernel(int k, int nn, const double* Vm, const double* lam,
+                                                           const int* ok, const int* bound, double* Ff, double* Fi) {
+  extern __shared__ double ffs[];
+  const int z = blockIdx.x, per = nn - 1, tid = threadIdx.x;
+  const size_t base = (size_t)(z / per) * nn + 1 + z % per;
+  const double* V = Vm + base * k * k;
+  double* F = Ff + base * k * k;
+  double* X = Fi + base * k * k;
+  if (!ok[base]) {
+    const double lmax = fmax(lam[base * k], 0.0);
+    const int bt = bound[1 + z % per];
+    for (int e = tid; e < k * k; e += 256) {
+      const int i = e / k, m = e - i * k;
+      const double l = lam[base * k + m];
+      const bool keep = m < bt && l > lmax * 1e-14 && l > 0.0;
+      const double v = V[e];
+      F[e] = keep ? v * sqrt(l) : 0.0;                   // F[i][m]
+      X[(size_t)m * k + i] = keep ? v / sqrt(l) : 0.0;   // Fi[m][i]
+    }
+    return;
+  }
+  const int ld = k + 1;
+  double* L = ffs;               // [k][k + 1]
+  double* dinv = L + (size_t)k * ld;
+  for (int e = tid; e < k * k; e += 256) {
+    const int i = e / k, c = e - i * k;
+    const double v = (c <= i) ? V[e] : 0.0;
+    L[i * ld + c] = v;
+    F[e] = v;
+  }
+  __syncthreads();
+  for (int i = tid; i < k; i += 256) dinv[i] = 1.0 / L[i * ld + i];
+  __syncthreads();
+  // X = L^-1, column c by 4 threads: X[i][c] = (delta_ic - sum_{c<=m<i} L[i][m] X[m][c]) / L[i][i]
+  double* Xs = dinv + k;         // [k][k + 1]
+  for (int c0 = 0; c0 < k; c0 += 64) {
+    const int c = c0 + (tid >> 2), part = tid & 3;
+    for (int i = 0; i < k; ++i) {
+      double acc = 0.0;
+      if (c < k && i > c)
+        for (int m = c + part; m < i; m += 4) acc = fma(L[i * ld + m], Xs[m * ld + c], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (c < k && part == 0) Xs[i * ld + c] = (i < c) ? 0.0 : ((i == c ? 1.0 : 0.0) - acc) * dinv[i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += 256) X[e] = Xs[(e / k) * ld + e % k];
 }
 
 // S_t = V diag(l^+1/2) W[:, :keep] (k x ro, zero columns beyond keep); T_t = S_t^T M_t (ro x k)
@@ -741,8 +803,9 @@ static void plan_ht_tree(const Tree& T, int Q, int k, int nb, int r_max, HtPlan&
   const size_t k3 = (size_t)k * k * k;
   size_t big = (size_t)nb * maxw * k3;
   const size_t proj = (size_t)nb * P.T.nint * (size_t)k * k * P.ro;
-  P.big = big > proj ? big : proj;
   const size_t nn = P.T.n, kk = (size_t)k * k;
+  P.big = big > proj ? big : proj;
+  if (P.big < 2 * (size_t)nb * nn * kk) P.big = 2 * (size_t)nb * nn * kk;   // F and Fi of every node (big3)
   P.off_n = (size_t)nb * (P.T.nleaf + P.T.nint) * 3 * 8 * 8;   // generous offset-table space
   P.total = align_up(8 * nb * nn * kk) * 5 + align_up(8 * nb * nn * k) * 2 + align_up(8 * nb * nn * (size_t)k * P.ro) * 2 +
             2 * align_up(4 * nb * nn) + align_up(8 * nb * nn) + 3 * align_up(8 * P.big) + align_up(8 * P.off_n) + 256 +
@@ -765,6 +828,7 @@ static int g_jac_sweeps = 30;
 static double g_jac_tol = 1e-16;
 static int* g_jac_count = nullptr;
 static int g_chol = 1;   // debug hook: 0 = eigh of every frame Gram (reference path)
+static int g_form_gemm = 1;   // debug hook: 0 = node Grams / kept bases by the one-CTA form_g / form_st kernels
 static int g_jac_db = 2;  // debug hook: 0 = three-barrier rows/columns, 1 = double-buffered blocks, 2 = upper-triangle blocks (default)
 static int g_eig_tridiag = 1;   // debug hook: node-Gram eigensolver 1 = tridiagonal (default), 0 = Jacobi (g_jac_db)
 
@@ -780,6 +844,7 @@ void tp_debug_set_ht_split_waves(int w) { g_split_waves = w; }
 void tp_debug_set_bgemm_klayout(int on) { g_bgemm_klayout = on; }
 // debug hook: frame-Gram factor by Cholesky (1, default) or eigh (0)
 void tp_debug_set_ht_chol(int on) { g_chol = on; }
+void tp_debug_set_ht_form_gemm(int on) { g_form_gemm = on; }
 // debug hook: Jacobi kernel (0 = three-barrier rounds, 1 = double-buffered blocks, 2 = upper-triangle blocks, default)
 void tp_debug_set_jacobi_impl(int db) { g_jac_db = db; }
 // debug hook: node-Gram eigensolver (1 = Householder tridiagonal + bisection + inverse iteration, 0 = Jacobi)
@@ -948,7 +1013,7 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
           oGl.insert(oGl.end(), {zb, BT(b, t), MF(b, T.left[t])});                // Gh_l = Y B^T
           oZ.insert(oZ.end(), {MF(b, T.left[t]), zb, zb});                        // Z'[b'] = M_l X[:, b', :]
           oTr.insert(oTr.end(), {BT(b, t), 0, 0});
-          oGr.insert(oGr.end(), {zb, zb, MF(b, T.right[t])});                     // Gh_r = Z' Bp^T
+          oGr.insert(oGr.end(), {zb, (kt == 1 || kt % 16 == 0) ? BT(b, t) : zb, MF(b, T.right[t])});   // Gh_r
         }
       const long long kkt = (long long)k * kt;
       BGemm gX = bgemm_desc(k * k, kt, kt, transfers, kt, 1, Gh, kt, 1, big1, kt, 1);
@@ -961,16 +1026,51 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
       BGemm gZ = bgemm_desc(k, kt, k, Mf, k, 1, big1, kkt, 1, big2, kt, 1);
       gZ.nb2 = k; gZ.sA2 = 0; gZ.sB2 = kt; gZ.sC2 = kkt;
       add_gemm(gZ, oZ);
-      trs.push_back({kt, table(oTr), (int)(oTr.size() / 3)});
-      order.push_back(-100 - (int)(trs.size() - 1));
-      BGemm gGr = bgemm_desc(k, k, k * kt, big2, kkt, 1, big3, 1, kkt, Gh, k, 1);
+      // Gh_r[b][b'] = sum_{a,j} Z'[b][a][j] B[a][b'][j]: B read in place, K = (a, j) by the
+      // two-level K addressing (no transposed copy of B)
+      // (k-tiles must not straddle two runs of kt: otherwise the transposed copy Bp[b][a][j])
+      BGemm gGr;
+      if (kt == 1) {
+        gGr = bgemm_desc(k, k, k, big2, kkt, 1, transfers, k, 1, Gh, k, 1);
+      } else if (kt % 16 == 0) {
+        gGr = bgemm_desc(k, k, k * kt, big2, kkt, 1, transfers, 1, kt, Gh, k, 1);
+        gGr.kinB = kt;
+        gGr.sBk1 = (long long)k * kt;
+      } else {
+        trs.push_back({kt, table(oTr), (int)(oTr.size() / 3)});
+        order.push_back(-100 - (int)(trs.size() - 1));
+        gGr = bgemm_desc(k, k, k * kt, big2, kkt, 1, big3, 1, kkt, Gh, k, 1);
+      }
       add_gemm(gGr, oGr);
     }
   }
-  add_stage(-3);   // G_t = L^1/2 V^T Gh V L^1/2
+  // node Grams G_t = F^T Gh F, then S_t = Fi^T W_keep, T_t = W_keep^T F^T as batched GEMMs over
+  // every non-root node (F, Fi from frame_factor_kernel in the big3 scratch; P in big1)
+  const long long nodes_kk = (long long)nb * nn * kk;
+  std::vector<long long> oP, oG, oS, oT;
+  for (int b = 0; b < nb; ++b)
+    for (int t = 1; t < nn; ++t) {
+      const long long nd = ((long long)b * nn + t) * kk;
+      oP.insert(oP.end(), {nd, nd, nd});                                                   // P = F^T Gh
+      oG.insert(oG.end(), {nd, nd, nd});                                                   // G = P F
+      oS.insert(oS.end(), {nd, nd, ((long long)b * nn + t) * k * ro});                     // S = Fi^T W
+      oT.insert(oT.end(), {nd, nd, ((long long)b * nn + t) * ro * k});                     // T = W^T F^T
+    }
+  if (g_form_gemm) {
+    add_stage(-8);   // F, Fi
+    add_gemm(bgemm_desc(k, k, k, big3, 1, k, Gh, k, 1, big1, k, 1), oP);
+    add_gemm(bgemm_desc(k, k, k, big1, k, 1, big3, k, 1, Gt, k, 1), oG);
+  } else {
+    add_stage(-3);   // G_t = L^1/2 V^T Gh V L^1/2
+  }
   add_stage(-4);   // eigh(G_t)
   add_stage(-5);   // keep rule
-  add_stage(-6);   // S_t, T_t
+  if (g_form_gemm) {
+    add_gemm(bgemm_desc(k, ro, k, big3 + nodes_kk, 1, k, Wg, k, 1, S, ro, 1), oS);
+    add_gemm(bgemm_desc(ro, k, k, Wg, 1, k, big3, 1, k, Tm, k, 1), oT);
+  } else {
+    add_stage(-6);   // S_t, T_t
+  }
   add_stage(-7);   // est, norms, ranks
   // ---- 4. projection
   {
@@ -1050,6 +1150,8 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
   cudaFuncSetAttribute(form_g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
   const size_t ssm = sizeof(double) * ((size_t)k + 2 * (size_t)k * ro + (size_t)k * (k + 1) + (size_t)k);
   cudaFuncSetAttribute(form_st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+  const size_t ffsm = sizeof(double) * (2 * (size_t)k * (k + 1) + (size_t)k);
+  cudaFuncSetAttribute(frame_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffsm);
   const size_t csm = sizeof(double) * ((size_t)k * (k + 1) + 2);
   cudaFuncSetAttribute(chol_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   const int nonroot = nb * (nn - 1);
@@ -1088,7 +1190,11 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
         e = cudaGetLastError();
       }
     } else if (id == -5) {
-      keep_rule_kernel<<<(nonroot + 127) / 128, 128, 0, st>>>(k, nn, nb, d, eps, r_max, sig, Mf, keep, disc, bound);
+      keep_rule_kernel<<<(nonroot + 127) / 128, 128, 0, st>>>(k, nn, nb, d, eps, r_max, sig, Mf, keep, disc, bound,
+                                                               g_form_gemm ? Wg : nullptr, ro);
+      e = cudaGetLastError();
+    } else if (id == -8) {
+      frame_factor_kernel<<<nonroot, 256, ffsm, st>>>(k, nn, Vm, lam, cholok, bound, big3, big3 + nodes_kk);
       e = cudaGetLastError();
     } else if (id == -6) {
       form_st_kernel<<<nonroot, 256, ssm, st>>>(k, ro, nn, Vm, lam, Wg, keep, Mf, S, Tm, cholok, bound);

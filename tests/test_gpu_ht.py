@@ -145,15 +145,20 @@ def test_from_cp_add_scale_apply():
     _ = ocp
 
 
+@pytest.mark.parametrize("form_gemm", [1, 0])
 @pytest.mark.parametrize("chol", [0, 1])
-def test_frame_factor_paths(chol):
+def test_frame_factor_paths(chol, form_gemm):
     """Frame-Gram square-root factor by Cholesky (default) or eigh (reference path),
-    with one rank-deficient leaf so both paths run inside one truncation."""
+    with one rank-deficient leaf so both paths run inside one truncation; node Grams and
+    kept bases as batched GEMMs over F / pseudo-inverse Fi (default) or by the one-CTA
+    form_g / form_st kernels."""
     import ctypes
     from paper_1803_10270_b200 import _lib
     L = _lib.lib()
     L.tp_debug_set_ht_chol.argtypes = [ctypes.c_int]
+    L.tp_debug_set_ht_form_gemm.argtypes = [ctypes.c_int]
     L.tp_debug_set_ht_chol(chol)
+    L.tp_debug_set_ht_form_gemm(form_gemm)
     try:
         rng = np.random.default_rng(21)
         d, q, k = 6, 14, 8
@@ -167,6 +172,7 @@ def test_frame_factor_paths(chol):
         assert metrics.ht_rel_diff(ref, red.to_oracle()) <= TOL
     finally:
         L.tp_debug_set_ht_chol(1)
+        L.tp_debug_set_ht_form_gemm(1)
 
 
 @pytest.mark.parametrize("impl", [0, 1, 2])
