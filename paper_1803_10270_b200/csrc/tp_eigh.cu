@@ -101,31 +101,30 @@ __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int 
   }
   __syncthreads();
   // ---- 1. Householder tridiagonalisation
+  // three barriers per reflector: (reflector by warp 0) | p = tau A22 v | rank-2 update;
+  // K = tau/2 p.v is formed redundantly by every warp (no barrier)
   for (int j = 0; j + 2 < n; ++j) {
     const int m = n - j - 1;   // length of x = A[j+1 .., j]
     if (warp == 0) {
       double s = 0.0;
       for (int i = 1 + lane; i < m; i += 32) { const double x = A[(j + 1 + i) * ld + j]; s = fma(x, x, s); }
       s = warp_sum(s);
-      if (lane == 0) {
-        const double alpha = A[(j + 1) * ld + j];
-        double t = 0.0, sc = 0.0, beta = alpha;
-        if (s > 0.0) {
-          beta = -copysign(sqrt(fma(alpha, alpha, s)), alpha);
-          t = (beta - alpha) / beta;
-          sc = 1.0 / (alpha - beta);
-        }
-        tau[j] = t; of[j] = beta; scal[0] = sc;
+      const double alpha = A[(j + 1) * ld + j];
+      double t = 0.0, sc = 0.0, beta = alpha;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, s)), alpha);
+        t = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+      if (lane == 0) { tau[j] = t; of[j] = beta; }
+      for (int i = lane; i < m; i += 32) {
+        const double v = (i == 0) ? 1.0 : A[(j + 1 + i) * ld + j] * sc;
+        vb[i] = v;
+        if (i > 0) A[(j + 1 + i) * ld + j] = v;
       }
     }
     __syncthreads();
-    const double t = tau[j], sc = scal[0];
-    for (int i = tid; i < m; i += TE_NT) {
-      const double v = (i == 0) ? 1.0 : A[(j + 1 + i) * ld + j] * sc;
-      vb[i] = v;
-      if (i > 0) A[(j + 1 + i) * ld + j] = v;
-    }
-    __syncthreads();
+    const double t = tau[j];
     if (t != 0.0) {
       // p = tau A22 v, 4 lanes per row
       {
@@ -140,19 +139,19 @@ __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int 
         if (row < m && part == 0) pv[row] = t * acc;
       }
       __syncthreads();
-      if (warp == 0) {
-        double s = 0.0;
-        for (int i = lane; i < m; i += 32) s = fma(pv[i], vb[i], s);
-        s = warp_sum(s);
-        if (lane == 0) scal[1] = 0.5 * t * s;
-      }
-      __syncthreads();
-      const double K = scal[1];
-      for (int e = tid; e < m * m; e += TE_NT) {
-        const int i = e / m, c = e - i * m;
-        const double wi = pv[i] - K * vb[i], wc = pv[c] - K * vb[c];
-        double* a = A + (size_t)(j + 1 + i) * ld + (j + 1 + c);
-        *a = fma(-vb[i], wc, fma(-wi, vb[c], *a));
+      double ks = 0.0;
+      for (int i = lane; i < m; i += 32) ks = fma(pv[i], vb[i], ks);
+      const double K = 0.5 * t * warp_sum(ks);
+      {   // rank-2 update, 4 threads per row (no runtime divisions)
+        const int row = tid >> 2, part = tid & 3;
+        for (int i = row; i < m; i += TE_NT / 4) {
+          const double vi = vb[i], wi = pv[i] - K * vi;
+          double* ar = A + (size_t)(j + 1 + i) * ld + (j + 1);
+          for (int c = part; c < m; c += 4) {
+            const double wc = pv[c] - K * vb[c];
+            ar[c] = fma(-vi, wc, fma(-wi, vb[c], ar[c]));
+          }
+        }
       }
       __syncthreads();
     }
@@ -236,7 +235,7 @@ __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int 
   double u0[TE_KMAX], u1[TE_KMAX], u2[TE_KMAX], ml[TE_KMAX];   // this thread's LU of T - shift I
   unsigned char piv[TE_KMAX];
   if (tid < nvec) tri_factor(dg, of, n, shf[tid], eps3, u0, u1, u2, ml, piv);
-  for (int it = 0; it < 4; ++it) {
+  for (int it = 0; it < 3; ++it) {
     if (warp == 0) {
       for (int t = 1; t < nvec; ++t) {
         double* zs = Z + (size_t)t * n;
@@ -253,7 +252,7 @@ __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int 
       }
     }
     __syncthreads();
-    if (it == 3) break;   // (the last pass only orthogonalises)
+    if (it == 2) break;   // (the last pass only orthogonalises)
     if (tid < nvec) {
       double* zt = Z + (size_t)tid * n;
       tri_apply(n, zt, u0, u1, u2, ml, piv);

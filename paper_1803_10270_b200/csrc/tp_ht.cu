@@ -490,10 +490,12 @@ __global__ void __launch_bounds__(256) chol_frame_kernel(int k, int nn, const do
     for (int i = j + 1 + tid; i < k; i += 256) A[i * ld + j] *= inv;
     if (tid == 0) A[j * ld + j] = dj;
     __syncthreads();
-    const int n = k - 1 - j;   // trailing lower triangle (i >= c > j)
-    for (int e = tid; e < n * n; e += 256) {
-      const int i = j + 1 + e / n, c = j + 1 + e % n;
-      if (c <= i) A[i * ld + c] = fma(-A[i * ld + j], A[c * ld + j], A[i * ld + c]);
+    {   // trailing lower triangle (i >= c > j), 4 threads per row (no runtime divisions)
+      const int row = tid >> 2, part = tid & 3;
+      for (int i = j + 1 + row; i < k; i += 64) {
+        const double aij = A[i * ld + j];
+        for (int c = j + 1 + part; c <= i; c += 4) A[i * ld + c] = fma(-aij, A[c * ld + j], A[i * ld + c]);
+      }
     }
     __syncthreads();
   }
