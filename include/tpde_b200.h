@@ -85,6 +85,20 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
  * out[1] CTAs, out[2] CTAs per cluster, out[3] shared bytes/CTA. */
 int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out);
 
+/* Fused operator apply + truncation (replaces explicit.py:91-93 /
+ * 99-103 target assembly + cp.py:266-334 for the one-CTA problems): the ALS target
+ *   V = [A | scale * L(w)],  w = [ws0 W0 | ws1 W1]  (ws* on mode 0; W1 may be NULL),
+ * L = sum_t w0[t] (x)_k E_{t,k} (w0 already includes `scale`; mat_idx[t*d + k] indexes
+ * mat_off, -1 = identity; the matrices Q_k x Q_k row-major in `mats`, device), is formed
+ * inside the kernel from A (rank ra), W0/W1 (rank rw) and the matrices -- L w is never
+ * written to memory.  Bitwise equal to materialising the target with tp_cp_apply_f64 and
+ * calling tp_cp_als_f64 with tol = 0, stall = -inf, trace = NULL.  Returns
+ * TP_EUNSUPPORTED when the problem does not fit the one-CTA kernel. */
+int tp_cp_als_recipe_f64(int d, const int* q, int r, const double* A, int ra, const double* W0, double ws0,
+                         const double* W1, double ws1, int rw, int n_terms, const double* w0, const int* mat_idx,
+                         const double* mats, const long long* mat_off, int n_mats, double* U, int sweeps, double reg,
+                         int reg_mode, int* info, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Input-rank-sharded CP-ALS mode steps (BASELINE cfg1 multi-GPU).
  * A rank holds the target slab V (rank R_l = its share of the R input terms,

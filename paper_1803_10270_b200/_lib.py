@@ -56,6 +56,8 @@ _SIGNATURES = {
     "tp_cp_als_ws_bytes": (_sz, [_i, _c_int_p, _i, _i, _i]),
     "tp_cp_als_plan": (_i, [_i, _c_int_p, _i, _i, _i, _c_int_p]),
     "tp_cp_als_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _i, _d, _i, _d, _d, _vp, _vp, _i, _vp, _sz, _vp]),
+    "tp_cp_als_recipe_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _d, _vp, _d, _i, _i, _c_double_p, _c_int_p, _vp,
+                                  _c_ll_p, _i, _vp, _i, _d, _i, _vp, _vp, _sz, _vp]),
     "tp_cp_contract_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _vp, _vp, _vp]),
     "tp_cp_apply_f64": (_i, [_i, _c_int_p, _i, _vp, _i, _c_double_p, _d, _c_int_p, _vp, _c_ll_p, _i,
                              _vp, _i, _i, _vp]),

@@ -87,7 +87,101 @@ struct AlsArgs {
   int clustered;           // als_persistent launched as ONE cluster of P CTAs: cluster barriers
   int local_gram;          // als_persistent: every CTA forms the whole Gram of the pending mode
   int early_inv;           // als_persistent, r <= 16: exact A_j^-1 formed in phase A by warps 0-3
+  // in-kernel target: V = [A | term-major scale * L(w)], w = [ws0 W0 | ws1 W1]
+  // (mode-0 scales), assembled from the un-applied states and the operator's matrices in
+  // the kernel's setup instead of reading a materialised L w (explicit.py:91-93 / 99-103)
+  int rcp;                 // 1: a.V unused, V from the recipe below
+  int rcp_ra, rcp_rw, rcp_nw, rcp_nt;
+  const double* rcpA;      // [Q_k x ra] mode-major
+  const double* rcpW[2];   // [Q_k x rw] mode-major
+  double rcp_ws[2];
+  const double* rcp_w0;    // [nt] scale * weight (mode 0), device
+  const long long* rcp_moff;   // [nt][d] matrix element offsets, -1 = identity, device
+  const double* rcp_mats;
 };
+
+// The whole recipe target into dst (mode k at rows qo[k], row stride ldd) by the CTA's
+// NTHR threads: (1) A blocks copied and the scaled w blocks of every mode staged in tmp
+// (one global round trip for all modes); (2) identity segments copied from tmp, operator
+// segments as matvecs with the matrix rows read straight from global memory (independent
+// loads, unrolled).  Same products, same sequential fma order as cp.concat +
+// cp_apply_kernel: bitwise equal to the materialised target.  Per-element fallback
+// (rcp_value) when the w blocks do not fit tmp.
+__device__ double rcp_value(const AlsArgs& a, int k, int s, int c);
+template <int NTHR>
+__device__ void rcp_fill(const AlsArgs& a, double* dst, int ldd, const int* qo, double* tmp, int tmp_cap) {
+  const int d = a.d, ra = a.rcp_ra, rw = a.rcp_rw, wt = a.rcp_nw * a.rcp_rw, tid = threadIdx.x;
+  int sumq = 0;
+  for (int k = 0; k < d; ++k) sumq += a.q[k];
+  if (sumq * wt > tmp_cap) {
+    const int R = ra + a.rcp_nt * wt;
+    for (int k = 0; k < d; ++k)
+      for (int e = tid; e < a.q[k] * R; e += NTHR)
+        dst[(size_t)(qo[k] + e / R) * ldd + e % R] = rcp_value(a, k, e / R, e % R);
+    __syncthreads();
+    return;
+  }
+  long long oA = 0, oW = 0;
+  int ot = 0;
+  for (int k = 0; k < d; ++k) {
+    const int Q = a.q[k];
+    for (int e = tid; e < Q * wt; e += NTHR) {
+      const int u = e / wt, l = e - u * wt, blk = l / rw, j = l - blk * rw;
+      tmp[ot + e] = ((k == 0) ? a.rcp_ws[blk] : 1.0) * a.rcpW[blk][oW + (long long)u * rw + j];
+    }
+    for (int e = tid; e < Q * ra; e += NTHR) dst[(size_t)(qo[k] + e / ra) * ldd + e % ra] = a.rcpA[oA + e];
+    oA += (long long)Q * ra; oW += (long long)Q * rw; ot += Q * wt;
+  }
+  __syncthreads();
+  ot = 0;
+  for (int k = 0; k < d; ++k) {
+    const int Q = a.q[k];
+    const double* tW = tmp + ot;
+    for (int t = 0; t < a.rcp_nt; ++t) {
+      const long long mo = a.rcp_moff[t * d + k];
+      const double sc = (k == 0) ? a.rcp_w0[t] : 1.0;
+      double* col = dst + (size_t)qo[k] * ldd + ra + t * wt;
+      if (mo < 0) {
+        for (int e = tid; e < Q * wt; e += NTHR) col[(size_t)(e / wt) * ldd + e % wt] = sc * tW[e];
+        continue;
+      }
+      for (int e = tid; e < Q * wt; e += NTHR) {
+        const int sr = e / wt, l = e - sr * wt;
+        const double* E = a.rcp_mats + mo + (long long)sr * Q;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int u = 0; u < Q; ++u) acc = fma(__ldg(E + u), tW[u * wt + l], acc);
+        col[(size_t)sr * ldd + l] = sc * acc;
+      }
+    }
+    ot += Q * wt;
+  }
+  __syncthreads();
+}
+
+// V_k[s][c] of the recipe target, bitwise equal to the materialised one (cp.concat of w,
+// then cp_apply_kernel: same scale products, same sequential fma order of the matvec)
+__device__ inline double rcp_value(const AlsArgs& a, int k, int s, int c) {
+  long long oA = 0, oW = 0;
+  for (int kk = 0; kk < k; ++kk) { oA += (long long)a.q[kk] * a.rcp_ra; oW += (long long)a.q[kk] * a.rcp_rw; }
+  if (c < a.rcp_ra) return a.rcpA[oA + (long long)s * a.rcp_ra + c];
+  c -= a.rcp_ra;
+  const int wt = a.rcp_nw * a.rcp_rw, t = c / wt, l = c - t * wt, blk = l / a.rcp_rw, j = l - blk * a.rcp_rw;
+  const double* W = a.rcpW[blk] + oW;
+  const double ws = (k == 0) ? a.rcp_ws[blk] : 1.0;
+  const long long mo = a.rcp_moff[t * a.d + k];
+  double v;
+  if (mo < 0) {
+    v = ws * W[(long long)s * a.rcp_rw + j];
+  } else {
+    const int Q = a.q[k];
+    const double* E = a.rcp_mats + mo + (long long)s * Q;
+    double acc = 0.0;
+    for (int u = 0; u < Q; ++u) acc = fma(__ldg(E + u), ws * W[(long long)u * a.rcp_rw + j], acc);
+    v = acc;
+  }
+  return ((k == 0) ? a.rcp_w0[t] : 1.0) * v;
+}
 
 struct Smem {
   uint64_t* bar;        // bar[0]: U staging / Y slices, bar[1]: Gram
@@ -1434,13 +1528,15 @@ __global__ void __launch_bounds__(TINY_NT, 1) als_tiny8(const __grid_constant__ 
   const size_t total = tiny_smem_doubles(d, r, td);
   for (size_t e = tid; e < total; e += TINY_NT) smem[e] = 0.0;   // all padding stays zero
   __syncthreads();
+  if (a.rcp) rcp_fill<TINY_NT>(a, Vs, Rs, td.qo, Cs, d * 8 * Rs);   // (Cs: free scratch until the crosses)
   for (int k = 0; k < d; ++k) {
     const int Q = a.q[k];
     const double* Vk = a.V + a.offV[k];
-    for (int e = tid; e < Q * R; e += TINY_NT) {
-      const int s = e / R, c = e - s * R;
-      Vs[(size_t)(td.qo[k] + s) * Rs + c] = Vk[e];
-    }
+    if (!a.rcp)
+      for (int e = tid; e < Q * R; e += TINY_NT) {
+        const int s = e / R, c = e - s * R;
+        Vs[(size_t)(td.qo[k] + s) * Rs + c] = Vk[e];
+      }
     const double* Uk = a.U + a.offU[k];
     for (int e = tid; e < Q * r; e += TINY_NT) {
       const int s = e / r, l = e - s * r;
@@ -2780,6 +2876,65 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
   else
     e = cudaLaunchCooperativeKernel(fn, dim3(pl.P), dim3(nt), args, pl.smem, s);
   return cuda_status(e);
+}
+
+// Fused operator apply + truncation for the one-CTA kernel: the target
+// [A | scale * L(w)], w = [ws0 W0 | ws1 W1], is assembled inside als_tiny8 from the states
+// and the operator's matrices (never written to global memory).  Fixed sweep count, no
+// trace.  TP_EUNSUPPORTED when the plan is not the one-CTA kernel (the caller then
+// materialises the target and calls tp_cp_als_f64).
+int tp_cp_als_recipe_f64(int d, const int* q, int r, const double* A, int ra, const double* W0, double ws0,
+                         const double* W1, double ws1, int rw, int n_terms, const double* w0, const int* mat_idx,
+                         const double* mats, const long long* mat_off, int n_mats, double* U, int sweeps, double reg,
+                         int reg_mode, int* info, void* ws, size_t ws_bytes, void* stream) {
+  if (!A || !W0 || !U || !info || sweeps < 0 || !(reg >= 0.0) || ra < 1 || rw < 1 || n_terms < 1 || n_terms > 64 ||
+      d < 1 || d > TP_MAXD)
+    return TP_EINVAL;
+  const int nw = W1 ? 2 : 1;
+  const int R = ra + n_terms * nw * rw;
+  AlsPlan pl;
+  int st = plan_als(d, q, R, r, 0, pl);
+  if (st != TP_OK) return st;
+  if (pl.variant != 5) return TP_EUNSUPPORTED;
+  if (!ws || ws_bytes < pl.ws_total) return TP_EWORKSPACE;
+  std::vector<double> hw(w0, w0 + n_terms);
+  std::vector<long long> hm((size_t)n_terms * d, -1);
+  for (int t = 0; t < n_terms; ++t)
+    for (int k = 0; k < d; ++k) {
+      const int m = mat_idx[t * d + k];
+      if (m >= 0) {
+        if (m >= n_mats || !mats) return TP_EINVAL;
+        hm[(size_t)t * d + k] = mat_off[m];
+      }
+    }
+  const double* dw = device_table(hw);
+  const long long* dm = device_table(hm);
+  if (!dw || !dm) return TP_ECUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  AlsArgs& a = pl.a;
+  Carver cv(ws, ws_bytes);
+  a.G = cv.take<double>((size_t)d * r * r);
+  a.Y = cv.take<double>(pl.ydoubles);
+  a.ovl = cv.take<double>(pl.P);
+  double* nsq = cv.take<double>(1);
+  (void)cv.take<double>(pl.ws_inner / sizeof(double));
+  a.bar_ctr = cv.take<unsigned int>(16);
+  a.Xprev = cv.take<double>(2 * (size_t)d * r * pad4(r));
+  a.ns_max = g_ns_max;
+  a.V = nullptr; a.U = U; a.trace = nullptr; a.info = info;
+  a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = 0.0; a.stall = -INFINITY;
+  a.need_resid = 0;
+  a.norm_sq = nsq;
+  a.prof = g_prof; a.prof_cta = 0; a.dbg_skip = g_skip;
+  a.rcp = 1; a.rcp_ra = ra; a.rcp_rw = rw; a.rcp_nw = nw; a.rcp_nt = n_terms;
+  a.rcpA = A; a.rcpW[0] = W0; a.rcpW[1] = W1; a.rcp_ws[0] = ws0; a.rcp_ws[1] = ws1;
+  a.rcp_w0 = dw; a.rcp_moff = dm; a.rcp_mats = mats;
+  cudaError_t e = cudaMemsetAsync(info, 0, 2 * sizeof(int), s);
+  if (e != cudaSuccess) return cuda_status(e);
+  e = cudaFuncSetAttribute((const void*)als_tiny8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  if (e != cudaSuccess) return cuda_status(e);
+  void* args[] = {&a};
+  return cuda_status(cudaLaunchKernel((const void*)als_tiny8, dim3(1), dim3(TINY_NT), args, pl.smem, s));
 }
 
 }  // extern "C"

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 
 import torch
 
-from . import cp, ht, operators
+from . import _lib, cp, ht, operators
 from .cp import ALSApproxConfig, CPTensor, inner_product, rank_reduce_als
 from .ht import HTTensor
 from .operators import SeparableOperator
@@ -104,6 +104,43 @@ def _ops(f):
     raise TypeError(f"unsupported tensor type {type(f).__name__}")
 
 
+def _fused_trunc(A: CPTensor, Ws, L: SeparableOperator, scale: float, init: CPTensor, r: int,
+                 acfg: ALSApproxConfig, info) -> torch.Tensor | None:
+    """Apply + truncation in ONE launch when the problem fits the one-CTA kernel
+    (``tp_cp_als_recipe_f64``): the target [A | scale L(w)],
+    w = [c0 W0 | c1 W1], is assembled inside the kernel from the states and the
+    operator's matrices.  Returns the fitted factor buffer, or None when the fused
+    path does not apply (the caller materialises the target)."""
+    if (A.is_complex or any(w.is_complex for w, _ in Ws) or acfg.tol > 0 or acfg.stall > -math.inf or
+            acfg.grid or L.n_terms > 64 or init.rank != r):
+        return None
+    buf, offs, rows, weights = operators.device_tables(L, A.data.device)
+    if buf.is_complex() or any(isinstance(x, complex) for x in weights):
+        return None
+    rw = Ws[0][0].rank
+    R = A.rank + L.n_terms * len(Ws) * rw
+    Lb = _lib.lib()
+    qs = _lib.int_array(A.qs)
+    nbytes = Lb.tp_cp_als_ws_bytes(A.ndim, qs, R, r, 0)
+    if nbytes == 0:
+        return None
+    ws = _lib.WORKSPACE.get(nbytes, A.data.device)
+    U = init.data.clone()
+    idx = [(-1 if m is None else int(m)) for row in rows for m in row]
+    reg, mode = (cp._REG, 1) if acfg.reg is None else (float(acfg.reg), 0)
+    W1 = Ws[1][0].data.data_ptr() if len(Ws) > 1 else None
+    st = Lb.tp_cp_als_recipe_f64(A.ndim, qs, r, A.data.data_ptr(), A.rank, Ws[0][0].data.data_ptr(), float(Ws[0][1]),
+                                 W1, float(Ws[1][1]) if len(Ws) > 1 else 0.0, rw, L.n_terms,
+                                 _lib.double_array([scale * float(w) for w in weights]), _lib.int_array(idx),
+                                 buf.data_ptr(), _lib.ll_array(offs), len(offs), U.data_ptr(), int(acfg.max_sweeps),
+                                 reg, mode, info.data_ptr(), ws.data_ptr(), ws.numel(),
+                                 _lib.stream_ptr(A.data.device))
+    if st == _lib.TP_EUNSUPPORTED:
+        return None
+    _lib.check(st, "cp_approx_als (fused apply)")
+    return U
+
+
 def ab2_target(f_n: CPTensor, f_n1: CPTensor, L: SeparableOperator, dt: float) -> CPTensor:
     """Exact AB2 update ``f1 + dt/2 L(3 f1 - f0)`` in one device buffer:
     columns [f1 | term-major L(w)], w = [3 f1 | -f0] (explicit.py:91-93 arithmetic)."""
@@ -147,7 +184,7 @@ def startup_step(f_0, L: SeparableOperator, config: ExplicitConfig, log: list | 
 
 
 def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, callback=None,
-        graph: bool = True) -> CPTensor:
+        graph: bool = True, fused: bool = True) -> CPTensor:
     """Fused-recipe CP trajectory (RK2 startup + AB2), fully stream-ordered:
     one fused-ALS launch per update, status words gathered on the device and
     checked once at the end (no per-step host synchronisation).
@@ -156,7 +193,12 @@ def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, 
     assembly, truncation, state rotation) is captured into a CUDA graph and
     replayed for the remaining steps -- no per-step host launch overhead.  The
     replayed kernels are the eager ones on the same data: results are bitwise
-    identical to ``graph=False``."""
+    identical to ``graph=False``.
+
+    ``fused`` (default): when the problem fits the one-CTA kernel, every truncation is
+    ONE launch that assembles its target [f1 | dt/2 L(3 f1 - f0)] from the two states and
+    the operator's matrices (``tp_cp_als_recipe_f64``) -- L w is never
+    materialised; bitwise equal to ``fused=False``."""
     if config.recipe != "fused" or not isinstance(f0, CPTensor):
         prev, cur = f0, startup_step(f0, L, config)
         for n in range(2, steps + 1):
@@ -175,8 +217,24 @@ def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, 
         cp._als_device(target, out.data, r, config.als, None, infos[slot])
         return out
 
-    half = trunc(_euler_target(f0, f0, L, 0.5 * config.dt), f0, 0)
-    cur = trunc(_euler_target(f0, half, L, config.dt), f0, 1)
+    # one launch per truncation with the target assembled in the kernel (f1) when it fits
+    Uh = _fused_trunc(f0, [(f0, 1.0)], L, 0.5 * config.dt, f0, r, config.als, infos[0]) if fused else None
+    fuse = Uh is not None
+
+    def euler(a: CPTensor, g: CPTensor, h: float, init: CPTensor, slot: int) -> CPTensor:
+        if fuse:
+            U = _fused_trunc(a, [(g, 1.0)], L, h, init, r, config.als, infos[slot])
+            return CPTensor(a.specs, data=U, rank=r)
+        return trunc(_euler_target(a, g, L, h), init, slot)
+
+    def ab2(p: CPTensor, c: CPTensor, slot: int) -> CPTensor:
+        if fuse:
+            U = _fused_trunc(c, [(c, 3.0), (p, -1.0)], L, 0.5 * config.dt, c, r, config.als, infos[slot])
+            return CPTensor(c.specs, data=U, rank=r)
+        return trunc(ab2_target(p, c, L, config.dt), c, slot)
+
+    half = CPTensor(f0.specs, data=Uh, rank=r) if fuse else trunc(_euler_target(f0, f0, L, 0.5 * config.dt), f0, 0)
+    cur = euler(f0, half, config.dt, f0, 1)
     prev = f0
     if callback:
         callback(1, cur)
@@ -184,7 +242,7 @@ def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, 
         L.n_terms * 2 * r + r > r
     n_eager = 2 if use_graph else steps
     for n in range(2, n_eager + 1):
-        nxt = trunc(ab2_target(prev, cur, L, config.dt), cur, n)
+        nxt = ab2(prev, cur, n)
         prev, cur = cur, nxt
         if callback:
             callback(n, cur)
@@ -194,7 +252,7 @@ def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, 
         # states in and replay -- every kernel of every step still executes
         a = config.als
         key = (tuple(cur.specs), r, float(config.dt), a.max_sweeps, float(a.tol), float(a.stall), a.seed,
-               a.reg, a.grid, str(cur.data.dtype), dev.index)
+               a.reg, a.grid, str(cur.data.dtype), dev.index, fuse)
         per_op = _GRAPHS.setdefault(L, {})
         hit = per_op.get(key)
         if hit is None:
@@ -205,9 +263,12 @@ def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, 
             with torch.cuda.graph(g):
                 P = CPTensor(cur.specs, data=pbuf, rank=r)
                 C = CPTensor(cur.specs, data=cbuf, rank=r)
-                tgt = ab2_target(P, C, L, config.dt)
-                nxt = cbuf.clone()
-                cp._als_device(tgt, nxt, r, config.als, None, slot)
+                if fuse:
+                    nxt = _fused_trunc(C, [(C, 3.0), (P, -1.0)], L, 0.5 * config.dt, C, r, config.als, slot)
+                else:
+                    tgt = ab2_target(P, C, L, config.dt)
+                    nxt = cbuf.clone()
+                    cp._als_device(tgt, nxt, r, config.als, None, slot)
                 agg.bitwise_or_(slot)
                 pbuf.copy_(cbuf)
                 cbuf.copy_(nxt)

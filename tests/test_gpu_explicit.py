@@ -178,3 +178,41 @@ def test_graph_cache_reuse_new_initial_state():
     b1 = explicit.run(f0, L, cfg, 8, graph=False)
     assert torch.equal(a1.data, b1.data) and torch.equal(a2.data, b2.data)
     assert not torch.equal(a1.data, a2.data)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_fused_apply_truncation_bitwise(graph):
+    """with the one-CTA kernel every truncation of explicit.run assembles its
+    target [f1 | dt/2 L(3 f1 - f0)] inside the kernel from the states and the operator's
+    matrices (tp_cp_als_recipe_f64, L w never materialised); the trajectory is bitwise
+    equal to materialising the target with the apply kernel first."""
+    import torch
+    w, S, L, cfg, _ = _cfg0_setup(10)
+    f0 = cp.CPTensor(S, w["ic"]["factors"])
+    assert cp.als_plan(f0.qs, f0.rank + L.n_terms * 2 * f0.rank, f0.rank)["kernel"] == "als_tiny8"
+    a = explicit.run(f0, L, cfg, 10, graph=graph, fused=True)
+    b = explicit.run(f0, L, cfg, 10, graph=graph, fused=False)
+    assert torch.equal(a.data, b.data)
+
+
+def test_fused_apply_entry_matches_materialised():
+    """tp_cp_als_recipe_f64 directly on a random two-block recipe with a mix of identity and
+    dense operator factors (incl. several matrices on one mode): bitwise equal to
+    cp.concat + operators.apply_into + cp.cp_approx_als."""
+    import torch
+    rng = np.random.default_rng(5)
+    qs, r = (9, 12, 7, 10), 5
+    S = tuple(BasisSpec(q, 1.0, "collocation") for q in qs)
+    f1 = cp.CPTensor(S, [rng.standard_normal((q, r)) for q in qs])
+    f0 = cp.CPTensor(S, [rng.standard_normal((q, r)) for q in qs])
+    mats = [[rng.standard_normal((q, q)) / q if (t + k) % 3 == 0 else None for k, q in enumerate(qs)]
+            for t in range(5)]
+    L = operators.SeparableOperator(S, tuple(rng.uniform(-1, 1, 5)), tuple(tuple(m) for m in mats))
+    acfg = cp.ALSApproxConfig(max_sweeps=7, stall=-np.inf, reg=1e-10)
+    info = torch.zeros(2, dtype=torch.int32, device=f1.data.device)
+    U = explicit._fused_trunc(f1, [(f1, 3.0), (f0, -1.0)], L, 0.05, f1, r, acfg, info)
+    assert U is not None
+    tgt = explicit.ab2_target(f0, f1, L, 0.1)
+    ref = cp.cp_approx_als(tgt, r, acfg, init=f1)
+    assert int(info[0]) == 0
+    assert torch.equal(U, ref.data)
