@@ -36,6 +36,8 @@ namespace tp {
 constexpr int IM_MAXD = 8, IM_MAXRA = 16, IM_MAXT = 64;
 constexpr size_t IM_KPART = 8;   // split-K partial space, in units of n_tab * Q * r doubles
 constexpr int CH_NB = 64;   // Cholesky block size
+constexpr int CH_LD = CH_NB + 4;   // row stride == 4 (mod 16): conflict-free 4-threads-per-row access
+static long long* g_dense_prof = nullptr;   // debug hook: clock64 phase totals of the diagonal-block kernel
 
 struct HArgs {
   int d, ra, r, q, n_tab, nX;
@@ -142,96 +144,161 @@ __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ A
 
 // Cholesky of the nb x nb diagonal block at (k0, k0) of the row-major n x n matrix A
 // (lower triangle), in shared memory; writes L back and L^-1 into Linv (nb x nb).
+// Two barriers per pivot, trailing update with 4 threads per row (no runtime divisions);
+// L^-1 by column-parallel forward substitution, 4 threads per column.
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* A, int n, int k0, int nb, double* Linv, int* info,
-                                                         const int* stop) {
+                                                         const int* stop, long long* prof = nullptr) {
   if (*stop) return;
+  long long t0 = clock64(), t1 = 0, t2 = 0, t3 = 0;
+  (void)nb;   // == CH_NB (compile-time extents below)
   extern __shared__ double pds[];
-  double (*L)[CH_NB + 1] = reinterpret_cast<double (*)[CH_NB + 1]>(pds);
-  double (*X)[CH_NB + 1] = reinterpret_cast<double (*)[CH_NB + 1]>(pds + CH_NB * (CH_NB + 1));
-  const int tid = threadIdx.x;
-  for (int e = tid; e < nb * nb; e += 256) {
-    const int i = e / nb, j = e % nb;
+  double (*L)[CH_LD] = reinterpret_cast<double (*)[CH_LD]>(pds);
+  double (*X)[CH_LD] = reinterpret_cast<double (*)[CH_LD]>(pds + CH_NB * CH_LD);
+  double* dinv = pds + 2 * CH_NB * CH_LD;
+  const int tid = threadIdx.x, row = tid >> 2, part = tid & 3;
+  for (int e = tid; e < CH_NB * CH_NB; e += 256) {
+    const int i = e / CH_NB, j = e - i * CH_NB;
     L[i][j] = (j <= i) ? A[(size_t)(k0 + i) * n + k0 + j] : 0.0;
   }
   __syncthreads();
+  __shared__ double ldg[CH_NB];
+  // left-looking (Crout) columns: one barrier per pivot; every 4-thread row group forms the
+  // pivot's diagonal sum itself (no broadcast), then its row's entry of column j
+  t1 = clock64();
   int bad = 0;
-  for (int j = 0; j < nb; ++j) {
-    const double djj = L[j][j];
+  for (int j = 0; j < CH_NB; ++j) {
+    double dsum = 0.0, rsum = 0.0;
+    const int i = j + 1 + row;   // this group's row below the pivot (row < 63 - j)
+    const bool act = i < CH_NB;
+    if (act || row == 0) {   // groups past the last row skip their loads (shared bandwidth)
+      double d1 = 0.0, d2 = 0.0, d3 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
+      const int ia = act ? i : j;
+      int m = part;
+      for (; m + 12 < j; m += 16) {
+        const double a0 = L[j][m], a1 = L[j][m + 4], a2 = L[j][m + 8], a3 = L[j][m + 12];
+        const double b0 = L[ia][m], b1 = L[ia][m + 4], b2 = L[ia][m + 8], b3 = L[ia][m + 12];
+        dsum = fma(a0, a0, dsum); d1 = fma(a1, a1, d1); d2 = fma(a2, a2, d2); d3 = fma(a3, a3, d3);
+        rsum = fma(b0, a0, rsum); r1 = fma(b1, a1, r1); r2 = fma(b2, a2, r2); r3 = fma(b3, a3, r3);
+      }
+      for (; m < j; m += 4) {
+        const double a0 = L[j][m], b0 = L[ia][m];
+        dsum = fma(a0, a0, dsum);
+        rsum = fma(b0, a0, rsum);
+      }
+      dsum = (dsum + d1) + (d2 + d3);
+      rsum = act ? (rsum + r1) + (r2 + r3) : 0.0;
+    }
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
+    rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
+    rsum += __shfl_xor_sync(0xffffffffu, rsum, 2);
+    const double djj = L[j][j] - dsum;   // (L[j][j] keeps A's value until after the loop)
     if (!(djj > 0.0) || !isfinite(djj)) bad = 1;
-    const double d = sqrt(fabs(djj));
-    const double inv = 1.0 / d;
-    __syncthreads();
-    if (tid == 0) L[j][j] = d;
-    for (int i = j + 1 + tid; i < nb; i += 256) L[i][j] *= inv;
-    __syncthreads();
-    const int m = nb - j - 1;
-    for (int e = tid; e < m * m; e += 256) {
-      const int i = j + 1 + e / m, c = j + 1 + e % m;
-      if (c <= i) L[i][c] = fma(-L[i][j], L[c][j], L[i][c]);
+    const double inv = (djj > 0.0) ? rsqrt_nr(djj) : 1.0 / sqrt(fabs(djj));
+    // column j below the diagonal is read and written only by its own row group in this
+    // iteration: one barrier per pivot (before the next column reads it)
+    if (part == 0) {
+      if (act) L[i][j] = (L[i][j] - rsum) * inv;
+      if (row == 0) { ldg[j] = djj * inv; dinv[j] = inv; }
     }
     __syncthreads();
   }
+  for (int j = tid; j < CH_NB; j += 256) L[j][j] = ldg[j];
+  __syncthreads();
+  t2 = clock64();
   if (bad && tid == 0) atomicOr(info, 1);
-  // X = L^-1 by column-parallel forward substitution
-  if (tid < nb) {
-    const int c = tid;
-    for (int i = 0; i < nb; ++i) {
-      double acc = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) acc = fma(-L[i][k], X[k][c], acc);
-      X[i][c] = (i < c) ? 0.0 : acc / L[i][i];
+  // X = L^-1: X[i][c] = (delta_ic - sum_{c <= m < i} L[i][m] X[m][c]) / L[i][i]
+  for (int c0 = 0; c0 < CH_NB; c0 += 64) {
+    const int c = c0 + row;
+    for (int i = 0; i < CH_NB; ++i) {
+      double acc = 0.0;
+      if (c < CH_NB && i > c) {
+        double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int m = c + part;
+        for (; m + 12 < i; m += 16) {
+          acc = fma(L[i][m], X[m][c], acc);
+          a1 = fma(L[i][m + 4], X[m + 4][c], a1);
+          a2 = fma(L[i][m + 8], X[m + 8][c], a2);
+          a3 = fma(L[i][m + 12], X[m + 12][c], a3);
+        }
+        for (; m < i; m += 4) acc = fma(L[i][m], X[m][c], acc);
+        acc = (acc + a1) + (a2 + a3);
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (c < CH_NB && part == 0) X[i][c] = (i < c) ? 0.0 : ((i == c ? 1.0 : 0.0) - acc) * dinv[i];
+      __syncwarp();
     }
   }
   __syncthreads();
-  for (int e = tid; e < nb * nb; e += 256) {
-    const int i = e / nb, j = e % nb;
+  for (int e = tid; e < CH_NB * CH_NB; e += 256) {
+    const int i = e / CH_NB, j = e - i * CH_NB;
     if (j <= i) A[(size_t)(k0 + i) * n + k0 + j] = L[i][j];
     Linv[e] = X[i][j];
   }
+  if (prof && tid == 0) {
+    t3 = clock64();
+    atomicAdd((unsigned long long*)prof + 0, (unsigned long long)(t1 - t0));
+    atomicAdd((unsigned long long*)prof + 1, (unsigned long long)(t2 - t1));
+    atomicAdd((unsigned long long*)prof + 2, (unsigned long long)(t3 - t2));
+    atomicAdd((unsigned long long*)prof + 3, 1ull);
+  }
 }
 
-// Solve L L^T x = b with the blocked factor (diagonal inverses in Linv); one CTA.
-__global__ void __launch_bounds__(256) potrs_kernel(const double* A, int n, const double* Linv, const double* b,
-                                                    double* x, double* y, const int* stop) {
+// Blocked triangular solves L L^T x = b over many CTAs, one launch per 64-row block
+// (right-looking: each block's result updates the remaining right-hand side).
+// forward block k: yf_k = Linv_k y_k; y_i -= L_ik yf_k for the rows below (y updated in place)
+__global__ void __launch_bounds__(256) fwd_block_kernel(const double* A, int n, int k0, const double* Linv_k, double* y,
+                                                        double* yf, const int* stop) {
   if (*stop) return;
-  __shared__ double part[256];
-  __shared__ double blk[CH_NB];
-  const int tid = threadIdx.x, nbk = n / CH_NB;
-  // forward: y_k = Linv_k (b_k - sum_{j<k} L_kj y_j)
-  for (int k = 0; k < nbk; ++k) {
-    const int r0 = k * CH_NB;
-    // partial sums: 4 threads per row
-    const int row = tid >> 2, sub = tid & 3;
+  __shared__ double yk[CH_NB], yn[CH_NB];
+  const int tid = threadIdx.x, row = tid >> 2, part = tid & 3;
+  if (tid < CH_NB) yk[tid] = y[k0 + tid];
+  __syncthreads();
+  {
     double acc = 0.0;
-    for (int c = sub; c < r0; c += 4) acc = fma(A[(size_t)(r0 + row) * n + c], y[c], acc);
-    part[tid] = acc;
-    __syncthreads();
-    if (tid < CH_NB) blk[tid] = b[r0 + tid] - (((part[4 * tid] + part[4 * tid + 1]) + part[4 * tid + 2]) + part[4 * tid + 3]);
-    __syncthreads();
-    if (tid < CH_NB) {
-      const double* li = Linv + (size_t)k * CH_NB * CH_NB + (size_t)tid * CH_NB;
-      double s = 0.0;
-      for (int c = 0; c <= tid; ++c) s = fma(li[c], blk[c], s);
-      y[r0 + tid] = s;
-    }
-    __syncthreads();
+    for (int c = part; c <= row; c += 4) acc = fma(Linv_k[row * CH_NB + c], yk[c], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (part == 0) yn[row] = acc;
   }
-  // backward: x_k = Linv_k^T (y_k - sum_{j>k} L_jk^T x_j)
-  for (int k = nbk - 1; k >= 0; --k) {
-    const int r0 = k * CH_NB;
-    const int col = tid >> 2, sub = tid & 3;
+  __syncthreads();
+  if (blockIdx.x == 0 && tid < CH_NB) yf[k0 + tid] = yn[tid];
+  const int rest = n - k0 - CH_NB;
+  for (int i = blockIdx.x * 64 + row; i < rest; i += gridDim.x * 64) {
+    const double* Li = A + (size_t)(k0 + CH_NB + i) * n + k0;
     double acc = 0.0;
-    for (int rr = r0 + CH_NB + sub; rr < n; rr += 4) acc = fma(A[(size_t)rr * n + r0 + col], x[rr], acc);
-    part[tid] = acc;
-    __syncthreads();
-    if (tid < CH_NB) blk[tid] = y[r0 + tid] - (((part[4 * tid] + part[4 * tid + 1]) + part[4 * tid + 2]) + part[4 * tid + 3]);
-    __syncthreads();
-    if (tid < CH_NB) {
-      const double* lk = Linv + (size_t)k * CH_NB * CH_NB;
-      double s = 0.0;
-      for (int c = tid; c < CH_NB; ++c) s = fma(lk[(size_t)c * CH_NB + tid], blk[c], s);
-      x[r0 + tid] = s;
-    }
-    __syncthreads();
+#pragma unroll 4
+    for (int c = part; c < CH_NB; c += 4) acc = fma(Li[c], yn[c], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (part == 0) y[k0 + CH_NB + i] -= acc;
+  }
+}
+
+// backward block j: x_j = Linv_j^T v_j; v_i -= (L_ji)^T x_j for the rows above (v in place)
+__global__ void __launch_bounds__(256) bwd_block_kernel(const double* A, int n, int j0, const double* Linv_j, double* v,
+                                                        double* x, const int* stop) {
+  if (*stop) return;
+  __shared__ double vj[CH_NB], xj[CH_NB];
+  const int tid = threadIdx.x, row = tid >> 2, part = tid & 3;
+  if (tid < CH_NB) vj[tid] = v[j0 + tid];
+  __syncthreads();
+  {
+    double acc = 0.0;   // x[c] = sum_{m >= c} Linv[m][c] v[m]
+    for (int m = row + part; m < CH_NB; m += 4) acc = fma(Linv_j[m * CH_NB + row], vj[m], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (part == 0) xj[row] = acc;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid < CH_NB) x[j0 + tid] = xj[tid];
+  for (int i = blockIdx.x * 256 + tid; i < j0; i += gridDim.x * 256) {
+    const double* Lc = A + (size_t)j0 * n + i;   // column i of block row j
+    double acc = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < CH_NB; ++c) acc = fma(Lc[(size_t)c * n], xj[c], acc);
+    v[i] -= acc;
   }
 }
 
@@ -1257,6 +1324,7 @@ extern "C" {
 
 // debug hook: fused circulant Gauss-Seidel kernel on (1, default) / off (0)
 void tp_debug_set_circ_fused(int on) { g_circ_fused = on; }
+void tp_debug_set_dense_prof(long long* p) { g_dense_prof = p; }
 // debug hook: device array of >= 16 int64 receiving per-phase clock64 totals of CTA 0
 void tp_debug_set_circ_prof(long long* p) { g_circ_prof = p; }
 
@@ -1523,7 +1591,21 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
   const int* xs_modes = device_table(xs_all);
   if (!xs_modes) return TP_ECUDA;
   const int nbk = n / CH_NB;
-  const int pd_smem = (int)(sizeof(double) * 2 * CH_NB * (CH_NB + 1));
+  const int pd_smem = (int)(sizeof(double) * (2 * CH_NB * CH_LD + CH_NB));
+  // lower-tile offset tables of the trailing SYRK per block step (uploaded once, cached)
+  std::vector<std::pair<const long long*, int>> syrk_tab(nbk);
+  for (int kb = 0; kb < nbk; ++kb) {
+    const int k0 = kb * CH_NB, nt = (n - k0 - CH_NB) / CH_NB;
+    std::vector<long long> o;
+    for (int ti = 0; ti < nt; ++ti)
+      for (int tj = 0; tj <= ti; ++tj) {
+        const long long ri = k0 + CH_NB + (long long)ti * CH_NB, rj = k0 + CH_NB + (long long)tj * CH_NB;
+        o.insert(o.end(), {ri * n + k0, rj * n + k0, ri * n + rj});
+      }
+    syrk_tab[kb] = {o.empty() ? nullptr : device_table(o), (int)(o.size() / 3)};
+    if (!o.empty() && !syrk_tab[kb].first) return TP_ECUDA;
+  }
+  const int fb_grid = (n + 63) / 64 < 148 ? (n + 63) / 64 : 148;
   cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pd_smem);
   const int asm_blocks = (int)(((long long)n * n + 255) / 256 < 148 * 32 ? ((long long)n * n + 255) / 256 : 148 * 32);
   const int cp_blocks = (int)((d * QR + 255) / 256 < 1184 ? (d * QR + 255) / 256 : 1184);
@@ -1570,23 +1652,31 @@ int tp_implicit_step_f64(int d, int Q, int r, int ra, int n_tab, const double* t
       as.nX = ha.nX;
       for (int i = 0; i < as.nX; ++i) as.xs[i] = used[q][i];
       assemble_kernel<<<asm_blocks, 256, 0, st>>>(as);
+      // right-looking blocked Cholesky; the forward solve rides along (each block's panel is
+      // final once its panel GEMM ran)
+      err = cudaMemcpyAsync(y, gam, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+      if (err != cudaSuccess) return cuda_status(err);
       for (int kb = 0; kb < nbk; ++kb) {
         const int k0 = kb * CH_NB, rest = n - k0 - CH_NB;
-        potrf_diag_kernel<<<1, 256, pd_smem, st>>>(M, n, k0, CH_NB, Linv + (size_t)kb * CH_NB * CH_NB, info, stop);
+        potrf_diag_kernel<<<1, 256, pd_smem, st>>>(M, n, k0, CH_NB, Linv + (size_t)kb * CH_NB * CH_NB, info, stop,
+                                                   g_dense_prof);
         if (rest > 0) {
           // panel: A21 <- A21 L11^-T   (in place: each row block is read fully before written)
           BGemm gp = bgemm_desc(rest, CH_NB, CH_NB, M + (size_t)(k0 + CH_NB) * n + k0, n, 1,
                                 Linv + (size_t)kb * CH_NB * CH_NB, 1, CH_NB, M + (size_t)(k0 + CH_NB) * n + k0, n, 1);
           gp.skip = stop;
           if ((err = bgemm_launch(gp, st)) != cudaSuccess) return cuda_status(err);
-          // trailing: A22 <- A22 - A21 A21^T
-          BGemm gs = bgemm_desc(rest, rest, CH_NB, M + (size_t)(k0 + CH_NB) * n + k0, n, 1,
-                                M + (size_t)(k0 + CH_NB) * n + k0, 1, n, M + (size_t)(k0 + CH_NB) * n + k0 + CH_NB, n, 1);
+          // trailing SYRK on the lower 64 x 64 tiles only: A22 <- A22 - A21 A21^T
+          BGemm gs = bgemm_desc(CH_NB, CH_NB, CH_NB, M, n, 1, M, 1, n, M, n, 1);
           gs.alpha = -1.0; gs.beta = 1.0; gs.skip = stop;
+          gs.offs = syrk_tab[kb].first; gs.nb1 = syrk_tab[kb].second;
           if ((err = bgemm_launch(gs, st)) != cudaSuccess) return cuda_status(err);
         }
+        fwd_block_kernel<<<fb_grid, 256, 0, st>>>(M, n, k0, Linv + (size_t)kb * CH_NB * CH_NB, y, x, stop);
       }
-      potrs_kernel<<<1, 256, 0, st>>>(M, n, Linv, gam, x, y, stop);
+      for (int kb = nbk - 1; kb >= 0; --kb)
+        bwd_block_kernel<<<fb_grid, 256, 0, st>>>(M, n, kb * CH_NB, Linv + (size_t)kb * CH_NB * CH_NB, x, y, stop);
+      std::swap(x, y);   // the solution is in y; scatter reads x
       scatter_x_kernel<<<(int)((QR + 255) / 256), 256, 0, st>>>(Q, r, x, dst, info, stop);
       }
       if (schedule == 0)

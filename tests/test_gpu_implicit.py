@@ -86,6 +86,24 @@ def test_config2_full_size_step(solver):
     assert rel <= 1e-8, rel
 
 
+def test_dense_cholesky_blocked():
+    """Dense solver: blocked Cholesky (left-looking diagonal blocks) with the lower-tile SYRK
+    and the multi-CTA block solves on a system of several 64-blocks (r Q = 6 x 48 = 288 ->
+    padded 320), vs the oracle."""
+    if True:
+        rng = np.random.default_rng(17)
+        d, q, r, dt, sweeps = 3, 48, 6, 2e-2, 3
+        a = (1.0, -0.5, 0.75)
+        D = fourier_diff_matrix(q)
+        S = col_specs(d, q)
+        f0 = [rng.standard_normal((q, r)) for _ in range(d)]
+        cfg = implicit.ALSStepConfig(dt=dt, eps_tol=0.0, max_sweeps=sweeps, delta_beta=1.0,
+                                     schedule="gauss-seidel", lam=1e-10, solver="dense")
+        out = implicit.step(cp.CPTensor(S, f0), euler_pair(S, D, a, dt), None, cfg)
+        ref, _, _ = oim.step(f0, oracle_tables(d, q, D, a, dt), sweeps, 1e-10)
+        assert metrics.cp_rel_diff(ref, out.to_numpy()) <= 1e-9
+
+
 def test_config_validation():
     with pytest.raises(ValueError, match="schedule"):
         implicit.ALSStepConfig(dt=0.1, schedule="sor")
