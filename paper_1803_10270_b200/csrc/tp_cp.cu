@@ -163,6 +163,7 @@ struct ApplyArgs {
 // the argument block (~5 KB) is passed by value (CUDA >= 12.1 allows 32 KB of
 // kernel parameters), so the launch is capturable in a CUDA graph.
 __global__ void __launch_bounds__(256) cp_apply_kernel(const __grid_constant__ ApplyArgs a) {
+  extern __shared__ double aps[];
   const int t = blockIdx.x, k = blockIdx.y;
   const int Q = a.q[k], r = a.r_in;
   const double* Fk = a.F + a.offF[k];
@@ -170,9 +171,30 @@ __global__ void __launch_bounds__(256) cp_apply_kernel(const __grid_constant__ A
   const long long mo = a.moff[t][k];
   const double sc = (k == 0) ? a.w0[t] : 1.0;
   const int col = a.col_off + t * r;
-  const int n = Q * r;
-  for (int e = blockIdx.z * blockDim.x + threadIdx.x; e < n; e += gridDim.z * blockDim.x) {
-    const int s = e / r, c = e % r;
+  // this CTA's rows [s0, s1) of the (term, mode) block
+  const int s0 = (int)((long long)Q * blockIdx.z / gridDim.z), s1 = (int)((long long)Q * (blockIdx.z + 1) / gridDim.z);
+  const int nr = s1 - s0;
+  if (mo >= 0 && (size_t)(nr * Q + Q * r) * sizeof(double) <= 48 * 1024) {
+    // operator rows and the factor staged in shared memory (coalesced), then the same
+    // sequential-fma matvec as the direct path (bitwise identical)
+    double* Es = aps;              // [nr][Q]
+    double* Fs = aps + nr * Q;     // [Q][r]
+    const double* E = a.mats + mo + (long long)s0 * Q;
+    for (int e = threadIdx.x; e < nr * Q; e += 256) Es[e] = __ldg(E + e);
+    for (int e = threadIdx.x; e < Q * r; e += 256) Fs[e] = __ldg(Fk + e);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * r; e += 256) {
+      const int sl = e / r, c = e - sl * r;
+      const double* er = Es + sl * Q;
+      double acc = 0.0;
+#pragma unroll 4
+      for (int u = 0; u < Q; ++u) acc = fma(er[u], Fs[u * r + c], acc);
+      Ok[(long long)(s0 + sl) * a.R_out + col + c] = sc * acc;
+    }
+    return;
+  }
+  for (int e = threadIdx.x; e < nr * r; e += blockDim.x) {
+    const int s = s0 + e / r, c = e % r;
     double v;
     if (mo < 0) {
       v = Fk[(long long)s * r + c];
@@ -309,8 +331,9 @@ int tp_cp_apply_f64(int d, const int* q, int r_in, const double* F, int n_terms,
   cudaStream_t st = (cudaStream_t)stream;
   int zb = (qmax * r_in + 255) / 256;
   zb = zb < 1 ? 1 : (zb > 64 ? 64 : zb);
+  if (zb > qmax) zb = qmax;
   dim3 grid(n_terms, d, zb);
-  cp_apply_kernel<<<grid, 256, 0, st>>>(a);
+  cp_apply_kernel<<<grid, 256, 48 * 1024, st>>>(a);
   return cuda_status(cudaGetLastError());
 }
 
