@@ -80,7 +80,8 @@ __device__ void tri_apply(int n, double* b, const double* u0, const double* u1, 
 __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int first, int per, const double* Ain,
                                                              double* Vout, double* wout, int nvec, const int* skip) {
   extern __shared__ double tes[];
-  const int n = k, ld = n + 1, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // row stride == 4 (mod 16): the 4-threads-per-row accesses hit distinct banks
+  const int n = k, ld = n + (((4 - n % 16) + 16) % 16), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* A = tes;                        // [n][ld]; column j below the subdiagonal keeps reflector j
   double* tau = A + (size_t)n * ld;       // [n]
   double* dg = tau + n;                   // [n] diagonal of T
@@ -307,7 +308,8 @@ __global__ void __launch_bounds__(TE_NT) tridiag_eigh_kernel(int k, int nn, int 
 }
 
 size_t tridiag_eigh_smem(int k, int nvec) {
-  return sizeof(double) * ((size_t)k * (k + 1) + 7 * (size_t)k + (size_t)nvec * k + 8 + 2 * (size_t)nvec);
+  const size_t ld = (size_t)k + (((4 - k % 16) + 16) % 16);
+  return sizeof(double) * ((size_t)k * ld + 7 * (size_t)k + (size_t)nvec * k + 8 + 2 * (size_t)nvec);
 }
 
 cudaError_t launch_tridiag_eigh(int nmat, int k, int nn, int first, int per, const double* Ain, double* Vout,

@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(JAC_NT) jacobi_sym_kernel(int k, int nn, int f
 // the reference (pseudo-inverse square root): ok[node] = 0.
 __global__ void __launch_bounds__(256) chol_frame_kernel(int k, int nn, const double* Mf, double* Lout, int* ok) {
   extern __shared__ double cs_[];
-  const int z = blockIdx.x, per = nn - 1, ld = k + 1, tid = threadIdx.x;
+  const int z = blockIdx.x, per = nn - 1, ld = k + (((4 - k % 16) + 16) % 16), tid = threadIdx.x;
   const size_t base = (size_t)(z / per) * nn + 1 + z % per;
   double* A = cs_;
   double* dmax = A + (size_t)k * ld;
@@ -1154,7 +1154,7 @@ static int ht_truncate_impl(const Tree& TT, int Q, int k, int nb, const double* 
   cudaFuncSetAttribute(form_st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
   const size_t ffsm = sizeof(double) * (2 * (size_t)k * (k + 1) + (size_t)k);
   cudaFuncSetAttribute(frame_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffsm);
-  const size_t csm = sizeof(double) * ((size_t)k * (k + 1) + 2);
+  const size_t csm = sizeof(double) * ((size_t)k * (k + (((4 - k % 16) + 16) % 16)) + 2);
   cudaFuncSetAttribute(chol_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   const int nonroot = nb * (nn - 1);
   for (int id : order) {
