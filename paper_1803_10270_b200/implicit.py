@@ -21,6 +21,7 @@ import torch
 
 from . import _lib
 from ._lib import StepFailure
+from .basis import BasisSpec
 from .cp import CPTensor
 from .operators import CrankNicolsonPair, dense_factor
 
@@ -67,14 +68,22 @@ class OperatorTables:
     KL: np.ndarray
     KR: np.ndarray
     circ_eig: torch.Tensor | None = None   # (n_tab, Q, 2) eigenvalues if every table is circulant
+    qs: tuple = ()                          # true mode sizes (modes zero-padded to max(qs) when they differ)
+
+    def _replace_qs(self) -> "OperatorTables":
+        """The same tables for the padded (uniform) launch."""
+        from dataclasses import replace
+        return replace(self, qs=())
 
 
 def build_tables(pair: CrankNicolsonPair, device=None) -> OperatorTables:
+    """Pairing tables pairs[k][e][z] = E_{e,k}^T E_{z,k} (implicit.py:77-108), deduplicated.
+    Modes of different sizes are zero-padded to Q = max Q_k: a padded table is zero on the
+    padding rows/columns, so the padded normal equations decouple there (lambda I, zero
+    right-hand side) and the padding rows of the iterate stay exactly zero."""
     specs = pair.specs
-    qs = {s.Q for s in specs}
-    if len(qs) != 1:
-        raise ValueError("the B200 implicit step needs a uniform mode size Q")
-    Q = qs.pop()
+    qtrue = tuple(s.Q for s in specs)
+    Q = max(qtrue)
     if any(s.kind == "fourier" for s in specs):
         # the reference's Galerkin pair_matrix is the unconjugated bilinear form of a complex
         # basis (basis.py:207-214; the identity pairs to the flip matrix), not E_e^T E_z
@@ -88,10 +97,11 @@ def build_tables(pair: CrankNicolsonPair, device=None) -> OperatorTables:
             m = dense_factor(spec, pair.factors[e][k])
             if m is not None and np.iscomplexobj(m):
                 raise ValueError("complex factor matrices are not supported by the real-fp64 implicit step")
-            mats.append(np.eye(Q) if m is None else m)
+            mats.append(np.eye(spec.Q) if m is None else m)
         for e in range(ra):
             for z in range(ra):
-                t = np.ascontiguousarray(mats[e].T @ mats[z])
+                t = np.zeros((Q, Q))
+                t[:spec.Q, :spec.Q] = mats[e].T @ mats[z]
                 key = t.tobytes()
                 if key not in keys:
                     keys[key] = len(uniq)
@@ -108,7 +118,7 @@ def build_tables(pair: CrankNicolsonPair, device=None) -> OperatorTables:
     if all(is_circulant(t) for t in uniq):
         lam = np.stack([np.fft.fft(t[:, 0]) for t in uniq])          # lambda_t(k) = sum_m t[m,0] e^{-2 pi i mk/Q}
         circ = torch.as_tensor(np.stack([lam.real, lam.imag], axis=-1)).to(dev)
-    return OperatorTables(pair, tabs, tab_id, np.outer(eta, eta), np.outer(eta, zeta), circ)
+    return OperatorTables(pair, tabs, tab_id, np.outer(eta, eta), np.outer(eta, zeta), circ, qtrue)
 
 
 def is_circulant(t: np.ndarray, rtol: float = 1e-13) -> bool:
@@ -159,7 +169,15 @@ def _launch(f_n: CPTensor, out: torch.Tensor, tab: OperatorTables, cfg: ALSStepC
     if f_n.is_complex:
         raise ValueError("complex128 states are not supported by the real-fp64 implicit step")
     L = _lib.lib()
-    d, Q, r, ra = f_n.ndim, f_n.specs[0].Q, f_n.rank, tab.pair.n_terms
+    d, r, ra = f_n.ndim, f_n.rank, tab.pair.n_terms
+    Q = max(tab.qs) if tab.qs else f_n.specs[0].Q
+    if tab.qs and len(set(tab.qs)) > 1:   # zero-padded modes (build_tables): pad in, solve, unpad
+        fp = _pad_modes(f_n, Q)
+        outp = fp.data.clone()
+        fcp = _pad_modes(forcing, Q) if forcing is not None else None
+        _launch(fp, outp.view(-1), tab._replace_qs(), cfg, eps, info, fcp)
+        _unpad_modes(outp, f_n, Q, out)
+        return
     n_tab = tab.tabs.shape[0]
     rf = forcing.rank if forcing is not None else 0
     use_circ = tab.circ_eig is not None and cfg.solver in ("auto", "circulant")
@@ -180,6 +198,24 @@ def _launch(f_n: CPTensor, out: torch.Tensor, tab: OperatorTables, cfg: ALSStepC
                                 eps.data_ptr(), info.data_ptr(), ws.data_ptr(), ws.numel(),
                                 _lib.stream_ptr(f_n.data.device))
     _lib.check(st, "implicit.step")
+
+
+def _pad_modes(f: CPTensor, Q: int) -> CPTensor:
+    """Mode-major copy with every mode zero-padded to Q rows (device copies)."""
+    r = f.rank
+    out = torch.zeros(len(f.specs) * Q * r, dtype=f.data.dtype, device=f.data.device)
+    off = 0
+    for k, s in enumerate(f.specs):
+        out[k * Q * r:k * Q * r + s.Q * r] = f.data[off:off + s.Q * r]
+        off += s.Q * r
+    return CPTensor(tuple(BasisSpec(Q, 1.0, "collocation") for _ in f.specs), data=out, rank=r)
+
+
+def _unpad_modes(src: torch.Tensor, like: CPTensor, Q: int, out: torch.Tensor) -> None:
+    r, off = like.rank, 0
+    for k, s in enumerate(like.specs):
+        out[off:off + s.Q * r] = src[k * Q * r:k * Q * r + s.Q * r]
+        off += s.Q * r
 
 
 def step(f_n: CPTensor, pair: CrankNicolsonPair, forcing: CPTensor | None, config: ALSStepConfig,

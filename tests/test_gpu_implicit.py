@@ -104,6 +104,30 @@ def test_dense_cholesky_blocked():
         assert metrics.cp_rel_diff(ref, out.to_numpy()) <= 1e-9
 
 
+@pytest.mark.parametrize("schedule,delta", [("gauss-seidel", 1.0), ("jacobi", 4.0)])
+def test_step_nonuniform_mode_sizes(schedule, delta):
+    """Modes of different sizes (Q = 12, 20, 9, 16): zero-padded tables and states inside
+    implicit.step (the padding rows decouple and stay zero), vs the oracle on the true sizes."""
+    rng = np.random.default_rng(23)
+    qs, r, dt, sweeps = (12, 20, 9, 16), 4, 2e-2, 4
+    a = (1.0, 0.5, -0.75, 0.25)
+    d = len(qs)
+    S = tuple(BasisSpec(q, math.pi, "collocation", lo=0.0) for q in qs)
+    Ds = [fourier_diff_matrix(q) for q in qs]
+    L = operators.SeparableOperator(S, tuple(-np.asarray(a)),
+                                    tuple(tuple(Ds[k] if k == t else None for k in range(d)) for t in range(d)))
+    pair = operators.implicit_euler_pair(L, dt)
+    f0 = [rng.standard_normal((q, r)) for q in qs]
+    cfg = implicit.ALSStepConfig(dt=dt, eps_tol=0.0, max_sweeps=sweeps, delta_beta=delta, schedule=schedule,
+                                 lam=1e-10)
+    out = implicit.step(cp.CPTensor(S, f0), pair, None, cfg)
+    assert out.qs == qs
+    mats = [[None] * d] + [[Ds[k] if k == i else None for k in range(d)] for i in range(d)]
+    tabs = oim.build_tables(mats, [1.0] + list(dt * np.asarray(a)), [1.0] + [0.0] * d, list(qs))
+    ref, _, _ = oim.step(f0, tabs, sweeps, 1e-10, schedule=schedule, delta_beta=delta)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= 1e-9
+
+
 def test_config_validation():
     with pytest.raises(ValueError, match="schedule"):
         implicit.ALSStepConfig(dt=0.1, schedule="sor")
