@@ -455,3 +455,30 @@ def test_als_rows_kernel(als_variant, ns, reg, qs, R, r):
 
 def test_als_rows_is_config1_default():
     assert cp.als_plan((256,) * 6, 512, 32)["kernel"] == "als_rows"
+
+
+@pytest.mark.parametrize("variant,cluster", [(0, 0), (1, 0), (8, 0)])
+def test_als_near_singular_gram_trace_rule(als_variant, variant, cluster):
+    """Near-singular normal equations under the reference trace rule (cp.py:171-173:
+    lambda = 1e-12 tr(A)/r): two init columns equal up to 1e-13 make every Gram product
+    numerically rank deficient (cond ~1e12).  np.linalg.solve succeeds there (no lstsq
+    fallback), so the fit must exist, stay finite and agree with the oracle within the
+    problem's own sensitivity (the oracle against itself on a 1e-13-perturbed init)."""
+    als_variant(variant, cluster)
+    rng = np.random.default_rng(31)
+    qs, R, r = (40, 36, 48, 40), 64, 6
+    V = rand_factors(rng, qs, R, 0.3)
+    init = [v[:, :r].copy() for v in V]
+    for f in init:
+        f[:, 1] = f[:, 0] * (1.0 + 1e-13)
+    out, ref, trace, otrace = _als_case(V, init, 5, None)
+    assert np.all(np.isfinite(out.data.cpu().numpy()))
+    # the problem's own sensitivity: the oracle on a 1e-13-perturbed init (SURVEY 8(d))
+    init_p = [f * (1.0 + 1e-13 * np.random.default_rng(5).standard_normal(f.shape)) for f in init]
+    ptrace = []
+    pref = ocp.als(V, init_p, 5, lam=None, trace=ptrace)
+    sens_t = float(np.max(np.abs(np.array(ptrace) - np.array(otrace)) / np.array(otrace)))
+    sens_f = metrics.cp_rel_diff(ref, pref)
+    assert sens_t > 1e-7   # (really ill-conditioned: the reference's own rounding moves the fit)
+    assert float(np.max(np.abs(np.array(trace) - np.array(otrace)) / np.array(otrace))) <= 10 * sens_t
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= 10 * sens_f
