@@ -564,7 +564,10 @@ def run_fused(args, world, rank, local, dev):
             It = cp.CPTensor(specs, data=dI[b], rank=RANK_R)
             o = cp.cp_approx_als(Tt, RANK_R, cfg, init=It, sync=False)
             consumed[b].record(stream)
-            hOut.copy_(o.data, non_blocking=True)
+            # the fit's device->host read on the copy stream, overlapping the next truncation
+            with torch.cuda.stream(s_copy):
+                s_copy.wait_event(consumed[b])
+                hOut.copy_(o.data, non_blocking=True)
             outs.append(o)
 
     e2e_run(max(2, args.warmup))
@@ -574,7 +577,7 @@ def run_fused(args, world, rank, local, dev):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         e2e_run(args.steps)
-        s_copy.synchronize()
+        stream.wait_stream(s_copy)   # the last device->host read is inside the timed region
         e1.record(stream)
         torch.cuda.synchronize()
         for o in outs:       # deferred status checks (ConditioningError would raise here)
