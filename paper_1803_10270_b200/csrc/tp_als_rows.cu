@@ -346,37 +346,43 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
   const int ng = r * (r + 1) / 2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nb = sm.nbT[k], ksteps = (nb + 3) / 4;
-  const int ntc = (x.w + 7) / 8, ncg = (ntc + 3) / 4, ngt = MT * (MT + 1) / 2;
+  const int ntc = (x.w + 7) / 8, ncg = (ntc + 1) / 2, ngt = MT * (MT + 1) / 2;   // C items: 2 column tiles
   const int nci = MT * ncg, nitems = nci + ngt;
-  double* cst = sm.scr;                  // [w][rs2]
-  double* gst = sm.scr + a.cst_len;      // [S][gs]
+  // partial staging: shared memory (st.async pushes) or this exchange's global block (gpush:
+  // TMA copies from L2 into the owners' inboxes)
+  double* stg = a.gpush ? a.Cg + (((size_t)ph_in * x.P + x.c) * S + x.b) * (size_t)(a.cst_len + S * gs) : sm.scr;
+  double* cst = stg;                     // [w][rs2]
+  double* gst = stg + a.cst_len;         // [S][gs]
   const uint32_t us32 = smem_u32(sm.Us), vs32 = smem_u32(sm.Vs + (size_t)a.vrow[k] * a.ldw);
   if (tid == 0) {   // this phase's expected bytes (peers may already be sending: tx count goes negative)
     uint32_t pub = 0;
-    for (int q = 0; q < S; ++q)
-      if (q != x.b && hmode >= 0) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * r + gs) * 8);
-    mbar_arrive_expect_tx(sm.bar + 1, (uint32_t)((S - 1) * (x.wc * rs2 + gs) * 8));
+    for (int q = 0; q < S; ++q) {
+      if (hmode < 0) break;
+      if (a.mc) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * rh + gs) * 8);   // every owner, self incl.
+      else if (q != x.b) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * r + gs) * 8);
+    }
+    mbar_arrive_expect_tx(sm.bar + 1, (uint32_t)((a.gpush ? S : S - 1) * (x.wc * rs2 + gs) * 8));
     mbar_arrive_expect_tx(sm.bar + 2, pub);
   }
   // ---- 1. partials into local staging
   for (int it = warp; it < nitems; it += RW_NW) {
     if (it < nci) {
-      const int m = it / MT, n = it - m * MT;   // m: group of up to 4 slab-column tiles, n: l tile
-      uint32_t bb[4], bst[4];
+      const int m = it / MT, n = it - m * MT;   // m: pair of slab-column tiles, n: l tile
+      uint32_t bb[2], bst[2];
       const uint32_t a_l = us32 + 8u * (uint32_t)(n * 8 + (lane >> 2));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int ct = 4 * m + u;
+      for (int u = 0; u < 2; ++u) {
+        int ct = 2 * m + u;
         if (ct >= ntc) ct = ntc - 1;
         bb[u] = vs32 + 8u * (uint32_t)(ct * 8 + (lane >> 2));
         bst[u] = 8u * (uint32_t)a.ldw;
       }
-      double acc[4][2];
-      rw_chains<4>(a_l, 8u * (uint32_t)rh, bb, bst, ksteps, acc);
+      double acc[2][2];
+      rw_chains<2>(a_l, 8u * (uint32_t)rh, bb, bst, ksteps, acc);
       const int l = n * 8 + (lane >> 2);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int ct = 4 * m + u;
+      for (int u = 0; u < 2; ++u) {
+        const int ct = 2 * m + u;
         if (ct >= ntc || l >= r) continue;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -401,7 +407,24 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
   }
   __syncthreads();
   // ---- 2. pushes: owner q <- (C^T rows [oc0(q), oc1(q)), Gram block q) into its slot b
-  {
+  if (a.gpush) {
+    if (warp == 0 && lane < S) {   // lane q: this CTA's two blocks for owner q (self included)
+      const int q = lane, q0 = sm.ocT[q], nq = sm.ocT[q + 1] - q0;
+      const uint32_t dst = mapa_u32(smem_u32(sm.inbox) + 8u * (uint32_t)(x.b * piece), (uint32_t)q);
+      const uint32_t rbar = mapa_u32(smem_u32(sm.bar + 1), (uint32_t)q);
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      if (nq > 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+            "l"(cst + (size_t)q0 * rs2), "r"((uint32_t)(nq * rs2 * 8)), "r"(rbar)
+            : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              dst + 8u * (uint32_t)(wcol * rs2)),
+          "l"(gst + (size_t)q * gs), "r"((uint32_t)(gs * 8)), "r"(rbar)
+          : "memory");
+    }
+  } else {
     const uint32_t slot = smem_u32(sm.inbox) + 8u * (uint32_t)(x.b * piece);
     const uint32_t bar_in = smem_u32(sm.bar + 1);
     for (int q = warp; q < S; q += RW_NW) {
@@ -443,7 +466,7 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
     double pv[16];
 #pragma unroll
     for (int src = 0; src < 16; ++src)
-      pv[src] = src >= S ? 0.0 : (src == x.b ? sm.scr[own] : sm.inbox[(size_t)src * piece + ii]);
+      pv[src] = src >= S ? 0.0 : ((src == x.b && !a.gpush) ? sm.scr[own] : sm.inbox[(size_t)src * piece + ii]);
     double v = 0.0;
 #pragma unroll
     for (int src = 0; src < 16; ++src) v += pv[src];
@@ -454,6 +477,9 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
   // this rank's Gram block of mode k stays local; with hmode >= 0 it publishes its block of
   // A_hmode = prod_{k' != hmode} G_k' (+ the overlap / self-Gram partials of the residual)
   double* Ab = sm.Apk + (size_t)x.b * gs;
+  // multicast staging of this exchange (double-buffered by exchange parity)
+  double* Hgc = a.mc ? a.Hg + ((size_t)ph_pub * x.P + x.c) * (size_t)a.kpad * rh : nullptr;
+  double* Agc = a.mc ? a.Ag + ((size_t)ph_pub * x.P + x.c) * (size_t)S * gs : nullptr;
   const int gcnt = (ng * (x.b + 1)) / S - (ng * x.b) / S;
   for (int e = tid; e < gs; e += RW_NT) sm.Gown[(size_t)k * gs + e] = sm.gpub[e];
   if (want_ovl) {
@@ -496,12 +522,39 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
       double v = 1.0;
 #pragma unroll
       for (int kk = 0; kk < TP_MAXD; ++kk) v *= f[kk];
-      sm.hadT[(size_t)(x.oc0 + cc) * rh + l] = v;
+      if (a.mc) Hgc[(size_t)(x.oc0 + cc) * rh + l] = v;
+      else sm.hadT[(size_t)(x.oc0 + cc) * rh + l] = v;
+    }
+    if (a.mc) {
+      for (int e = tid; e < x.wc * (rh - r); e += RW_NT) {   // zero row padding (multicast whole rows)
+        const int cc = e / (rh - r), l = r + e - cc * (rh - r);
+        Hgc[(size_t)(x.oc0 + cc) * rh + l] = 0.0;
+      }
+      for (int e = tid; e < gs; e += RW_NT) Agc[(size_t)x.b * gs + e] = Ab[e];
     }
   }
   __syncthreads();
   // ---- 4. publish the had rows and the Gram block to every peer
-  {
+  if (a.mc) {
+    // one TMA multicast per block: read once from L2, delivered into every CTA's had rows /
+    // A block (same offsets), completing on each CTA's publish mbarrier
+    if (hmode >= 0 && tid == 0) {
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      const uint16_t mask = (uint16_t)((1u << S) - 1u);
+      const uint32_t bar_pub = smem_u32(sm.bar + 2);
+      if (x.wc > 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, "
+            "[%3], %4;\n" ::"r"(smem_u32(sm.hadT) + 8u * (uint32_t)(x.oc0 * rh)),
+            "l"(Hgc + (size_t)x.oc0 * rh), "r"((uint32_t)(x.wc * rh * 8)), "r"(bar_pub), "h"(mask)
+            : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, "
+          "[%3], %4;\n" ::"r"(smem_u32(Ab)),
+          "l"(Agc + (size_t)x.b * gs), "r"((uint32_t)(gs * 8)), "r"(bar_pub), "h"(mask)
+          : "memory");
+    }
+  } else {
     const uint32_t hsrc = smem_u32(sm.hadT) + 8u * (uint32_t)(x.oc0 * rh);
     const uint32_t gsrc = smem_u32(Ab);
     const uint32_t bar_pub = smem_u32(sm.bar + 2);
@@ -731,8 +784,6 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
       }
       RW_PROF(1);
       if (!ok) status |= rw_inverse<RM>(a, sm, sm.X1, rh);
-      if (a.ns)   // next sweep's warm start for this mode (read back only by this CTA)
-        for (int e = tid; e < (int)xsz; e += RW_NT) Xw[(size_t)j * xsz + e] = sm.X1[e];
       RW_PROF(2);
       // ---- 2. rhs = sum over the P clusters (fixed order): warp c waits for cluster c's
       // flag and stages its slot (overlapping the later flags), then the ordered sum
@@ -740,6 +791,10 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
         const int nslot = (int)rw_ev((size_t)rw_nbr(a) * r), n2 = nb * r / 2;
         const double* ybase = a.Y + (((size_t)(u & 1) * x.S + x.b) * x.P) * slot_stride;
         int bad = 0;
+        // next sweep's warm start for this mode (read back only by this CTA) by the last
+        // warp, while the others wait for the flags (P <= 7: the last warp polls none)
+        if (a.ns && warp == RW_NW - 1)
+          for (int e = lane; e < (int)xsz; e += 32) Xw[(size_t)j * xsz + e] = sm.X1[e];
         for (int cc = warp; cc < x.P; cc += RW_NW) {
           if (lane == 0 && !(status & 4)) {
             const unsigned int* f = a.flags + ((size_t)(u & 1) * x.S + x.b) * x.P + cc;
@@ -845,6 +900,9 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
   cluster_barrier();   // no CTA exits while a peer may still store into its shared memory
 }
 
+static int g_rows_mc = 1;   // debug hook: 0 = publishes by st.async remote stores
+static int g_rows_gpush = 0;   // debug hook: 1 = partial pushes as global staging + TMA copies (measured no faster)
+
 static const void* rows_kernel(int rm) {
   switch (rm) {
     case 8: return (const void*)als_rows<8>;
@@ -925,7 +983,10 @@ int als_rows_plan(int d, const int* q, int R, int r, int S_force, int P_force, R
         pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
         pl.ws = align_up(sizeof(double) * 2 * (size_t)S * P * pl.a.ylen) + align_up(sizeof(unsigned int) * 2 * S * P) +
                 align_up(sizeof(double)) + pl.ws_inner +
-                align_up(sizeof(double) * (size_t)S * P * d * pl.rm * rw_pad4(r)) + 256;
+                align_up(sizeof(double) * (size_t)S * P * d * pl.rm * rw_pad4(r)) +
+                align_up(sizeof(double) * 2 * (size_t)P * pl.a.kpad * rw_pad4(r)) +
+                align_up(sizeof(double) * 2 * (size_t)P * S * pl.a.gstride) +
+                align_up(sizeof(double) * 2 * (size_t)P * S * (pl.a.cst_len + S * pl.a.gstride)) + 256;
         return TP_OK;
       }
     }
@@ -945,7 +1006,12 @@ int als_rows_run(const RowsPlan& plan, const double* V, double* U, int sweeps, d
   double* nsq = cv.take<double>(1);
   double* part = cv.take<double>(plan.ws_inner / sizeof(double));
   a.Xw = cv.take<double>((size_t)a.S * a.P * a.d * plan.rm * rw_pad4(a.r));
+  a.Hg = cv.take<double>(2 * (size_t)a.P * a.kpad * rw_pad4(a.r));
+  a.Ag = cv.take<double>(2 * (size_t)a.P * a.S * a.gstride);
   a.ns = ns;
+  a.mc = g_rows_mc;
+  a.Cg = cv.take<double>(2 * (size_t)a.P * a.S * (a.cst_len + a.S * a.gstride));
+  a.gpush = g_rows_gpush;
   a.V = V; a.U = U; a.trace = trace; a.info = info; a.norm_sq = nsq;
   a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = tol; a.stall = stall;
   a.need_resid = (trace != nullptr) || (tol > 0.0) || (stall > -INFINITY);
@@ -978,3 +1044,6 @@ int als_rows_run(const RowsPlan& plan, const double* V, double* U, int sweeps, d
 }
 
 }  // namespace tp
+
+extern "C" void tp_debug_set_als_rows_mc(int on) { tp::g_rows_mc = on; }
+extern "C" void tp_debug_set_als_rows_gpush(int on) { tp::g_rows_gpush = on; }

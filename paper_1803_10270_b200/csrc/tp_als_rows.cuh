@@ -17,6 +17,11 @@ struct RowsArgs {
   double* Y;                        // [2][S][P][ylen] right-hand-side slots (parity of the round)
   unsigned int* flags;              // [2][S][P] round number + 1 once the slot is written
   double* Xw;                       // [CTA][d][RM][pad4(r)] per-CTA warm-start inverses
+  double* Hg;                       // [2][P][kpad][pad4(r)] had publish staging (multicast source)
+  double* Ag;                       // [2][P][S][gstride] A-block publish staging
+  int mc;                           // publishes by TMA multicast from global staging (else st.async)
+  double* Cg;                       // [2][P][S][cst_len + S gstride] push staging (gpush)
+  int gpush;                        // pushes as global staging + TMA copies into the owners' inboxes
   const double* norm_sq;
   double* trace;
   int* info;

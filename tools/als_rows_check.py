@@ -49,7 +49,13 @@ cfg = cp.ALSApproxConfig(max_sweeps=20, stall=-np.inf, reg=1e-10)
 U = I0.data.clone()
 outs = {}
 ref = ocp.als([np.asarray(v) for v in w["V"]], [np.asarray(v) for v in w["init"]], 20, lam=1e-10)
-for name, var, cs, pr in [("cluster4", 2, 4, 0), ("rows16", 8, 16, 0)]:
+L.tp_debug_set_als_rows_mc.argtypes = [ctypes.c_int]
+L.tp_debug_set_als_rows_gpush.argtypes = [ctypes.c_int]
+for name, var, cs, pr in [("cluster4", 2, 4, 0), ("rows16", 8, 16, 0), ("rows16-dsm", 8, 16, -2),
+                          ("rows16-mc", 8, 16, -1)]:
+    L.tp_debug_set_als_rows_mc(0 if pr == -2 else 1)
+    L.tp_debug_set_als_rows_gpush(0 if pr < 0 else 1)
+    pr = max(pr, 0)
     L.tp_debug_set_als_variant(var, cs)
     L.tp_debug_set_als_rows(1 if var == 8 else 0, pr)
     st, pl = plan([256] * 6, 512, 32)
@@ -102,4 +108,6 @@ for var, cs in [(2, 4), (8, 16)]:
     out2 = cp.cp_approx_als(T, 32, cp.ALSApproxConfig(max_sweeps=50, tol=0.0, stall=1e-3, reg=1e-10), init=I0, trace=(tr2 := []))
     print("variant", var, "trace", ["%.12e" % t for t in tr[:3]], "...", "%.12e" % tr[-1], " stall-stop sweeps", len(tr2), flush=True)
 L.tp_debug_set_als_variant(0, 0)
-L.tp_debug_set_als_rows(0, 0)
+L.tp_debug_set_als_rows(1, 0)
+L.tp_debug_set_als_rows_mc(1)
+L.tp_debug_set_als_rows_gpush(1)
