@@ -139,6 +139,15 @@ __device__ __forceinline__ void st_cluster_v2(uint32_t addr, double x, double y)
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(x), "d"(y) : "memory");
 }
 
+__device__ __forceinline__ void sts64(uint32_t addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ double2 lds2x64(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 // remote stores that complete bytes on the receiver's mbarrier (point-to-point, no barrier)
 __device__ __forceinline__ void st_async_v2(uint32_t addr, double x, double y, uint32_t rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
@@ -194,7 +203,7 @@ __device__ void rw_build_a_w(const RowsArgs& a, const RwSmem& sm, int nt) {
   }
   for (int e = tid; e < r * r; e += nt) {
     const int dv = sm.divT[e], i = dv & 0xffff, c = dv >> 16;
-    sm.Am[i * rh + c] = sm.Apk[sm.gposT[e]] + (i == c ? lam : 0.0);
+    sts64(smem_u32(sm.Am) + 8u * (uint32_t)(i * rh + c), lds64(smem_u32(sm.Apk) + 8u * (uint32_t)sm.gposT[e]) + (i == c ? lam : 0.0));
   }
   bar_named(1, nt);
 }
@@ -258,7 +267,7 @@ template <int RM>
 __device__ double rw_gemm(const double* A, const double* B, double* out, int rh, int r, int mode, int nw) {
   constexpr int MT = RM / 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t a32 = smem_u32(A), b32 = smem_u32(B);
+  const uint32_t a32 = smem_u32(A), b32 = smem_u32(B), o32 = smem_u32(out);
   double emax = 0.0;
   for (int it = warp; it < MT * MT; it += nw) {
     const int m = it / MT, n = it - m * MT;
@@ -279,10 +288,10 @@ __device__ double rw_gemm(const double* A, const double* B, double* out, int rh,
       const int c = n * 8 + 2 * (lane & 3) + h;
       const double dl = (i == c) ? 1.0 : 0.0;
       if (mode == 0) {
-        out[i * rh + c] = 2.0 * dl - acc[h];
+        sts64(o32 + 8u * (uint32_t)(i * rh + c), 2.0 * dl - acc[h]);
         if (i < r && c < r) emax = fmax(emax, fabs(dl - acc[h]));
       } else {
-        out[i * rh + c] = acc[h];
+        sts64(o32 + 8u * (uint32_t)(i * rh + c), acc[h]);
       }
     }
   }
@@ -348,11 +357,9 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
   const int nb = sm.nbT[k], ksteps = (nb + 3) / 4;
   const int ntc = (x.w + 7) / 8, ncg = (ntc + 1) / 2, ngt = MT * (MT + 1) / 2;   // C items: 2 column tiles
   const int nci = MT * ncg, nitems = nci + ngt;
-  // partial staging: shared memory (st.async pushes) or this exchange's global block (gpush:
-  // TMA copies from L2 into the owners' inboxes)
-  double* stg = a.gpush ? a.Cg + (((size_t)ph_in * x.P + x.c) * S + x.b) * (size_t)(a.cst_len + S * gs) : sm.scr;
-  double* cst = stg;                     // [w][rs2]
-  double* gst = stg + a.cst_len;         // [S][gs]
+  double* cst = sm.scr;                  // [w][rs2] partial staging
+  double* gst = sm.scr + a.cst_len;      // [S][gs]
+  const uint32_t cst32 = smem_u32(cst), gst32 = smem_u32(gst);
   const uint32_t us32 = smem_u32(sm.Us), vs32 = smem_u32(sm.Vs + (size_t)a.vrow[k] * a.ldw);
   if (tid == 0) {   // this phase's expected bytes (peers may already be sending: tx count goes negative)
     uint32_t pub = 0;
@@ -361,7 +368,7 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
       if (a.mc) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * rh + gs) * 8);   // every owner, self incl.
       else if (q != x.b) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * r + gs) * 8);
     }
-    mbar_arrive_expect_tx(sm.bar + 1, (uint32_t)((a.gpush ? S : S - 1) * (x.wc * rs2 + gs) * 8));
+    mbar_arrive_expect_tx(sm.bar + 1, (uint32_t)((S - 1) * (x.wc * rs2 + gs) * 8));
     mbar_arrive_expect_tx(sm.bar + 2, pub);
   }
   // ---- 1. partials into local staging
@@ -387,7 +394,7 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = ct * 8 + 2 * (lane & 3) + h;
-          if (c < x.w) cst[c * rs2 + l] = acc[u][h];
+          if (c < x.w) sts64(cst32 + 8u * (uint32_t)(c * rs2 + l), acc[u][h]);
         }
       }
     } else {
@@ -401,30 +408,13 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = tj * 8 + 2 * (lane & 3) + h;
-        if (i < r && c < r && i <= c) gst[sm.gposT[i * r + c]] = acc[0][h];
+        if (i < r && c < r && i <= c) sts64(gst32 + 8u * (uint32_t)sm.gposT[i * r + c], acc[0][h]);
       }
     }
   }
   __syncthreads();
   // ---- 2. pushes: owner q <- (C^T rows [oc0(q), oc1(q)), Gram block q) into its slot b
-  if (a.gpush) {
-    if (warp == 0 && lane < S) {   // lane q: this CTA's two blocks for owner q (self included)
-      const int q = lane, q0 = sm.ocT[q], nq = sm.ocT[q + 1] - q0;
-      const uint32_t dst = mapa_u32(smem_u32(sm.inbox) + 8u * (uint32_t)(x.b * piece), (uint32_t)q);
-      const uint32_t rbar = mapa_u32(smem_u32(sm.bar + 1), (uint32_t)q);
-      asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      if (nq > 0)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-            "l"(cst + (size_t)q0 * rs2), "r"((uint32_t)(nq * rs2 * 8)), "r"(rbar)
-            : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-              dst + 8u * (uint32_t)(wcol * rs2)),
-          "l"(gst + (size_t)q * gs), "r"((uint32_t)(gs * 8)), "r"(rbar)
-          : "memory");
-    }
-  } else {
+  {
     const uint32_t slot = smem_u32(sm.inbox) + 8u * (uint32_t)(x.b * piece);
     const uint32_t bar_in = smem_u32(sm.bar + 1);
     for (int q = warp; q < S; q += RW_NW) {
@@ -432,15 +422,15 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
       const int q0 = sm.ocT[q], nq = sm.ocT[q + 1] - q0;
       const int nc2 = nq * rs2 / 2;
       const uint32_t dst = mapa_u32(slot, (uint32_t)q), rbar = mapa_u32(bar_in, (uint32_t)q);
-      const double* src = cst + (size_t)q0 * rs2;
+      const uint32_t src = cst32 + 8u * (uint32_t)(q0 * rs2);
       for (int e = lane; e < nc2; e += 32) {
-        const double2 v = *reinterpret_cast<const double2*>(src + 2 * e);
+        const double2 v = lds2x64(src + 16u * (uint32_t)e);
         st_async_v2(dst + 16u * (uint32_t)e, v.x, v.y, rbar);
       }
-      const double* gsrc = gst + (size_t)q * gs;
+      const uint32_t gsrc = gst32 + 8u * (uint32_t)(q * gs);
       const uint32_t gdst = dst + 8u * (uint32_t)(wcol * rs2);
       for (int e = lane; e < gs / 2; e += 32) {
-        const double2 v = *reinterpret_cast<const double2*>(gsrc + 2 * e);
+        const double2 v = lds2x64(gsrc + 16u * (uint32_t)e);
         st_async_v2(gdst + 16u * (uint32_t)e, v.x, v.y, rbar);
       }
     }
@@ -463,17 +453,20 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
       ii = wcol * rs2 + (e - ncr);
       own = a.cst_len + x.b * gs + (e - ncr);
     }
+    // all S contributions issued together through 32-bit shared addresses, summed in rank order
+    const uint32_t ib = smem_u32(sm.inbox) + 8u * (uint32_t)ii, pst = 8u * (uint32_t)piece;
+    const double ownv = lds64(cst32 + 8u * (uint32_t)own);
     double pv[16];
 #pragma unroll
-    for (int src = 0; src < 16; ++src)
-      pv[src] = src >= S ? 0.0 : ((src == x.b && !a.gpush) ? sm.scr[own] : sm.inbox[(size_t)src * piece + ii]);
+    for (int src = 0; src < 16; ++src) pv[src] = src < S ? lds64(ib + (uint32_t)src * pst) : 0.0;
     double v = 0.0;
 #pragma unroll
-    for (int src = 0; src < 16; ++src) v += pv[src];
+    for (int src = 0; src < 16; ++src) v += (src == x.b) ? ownv : pv[src];
     if (isc) Ck[e] = v;
     else sm.gpub[e - ncr] = v;
   }
   __syncthreads();
+  RW_PROF(12);
   // this rank's Gram block of mode k stays local; with hmode >= 0 it publishes its block of
   // A_hmode = prod_{k' != hmode} G_k' (+ the overlap / self-Gram partials of the residual)
   double* Ab = sm.Apk + (size_t)x.b * gs;
@@ -497,43 +490,49 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
     }
     ovl = rw_block_sum(ovl, sm.part);
     self = rw_block_sum(self, sm.part);
-    if (tid == 0) { Ab[gs - 1] = ovl; Ab[gs - 2] = self; }
+    if (tid == 0) {
+      Ab[gs - 1] = ovl; Ab[gs - 2] = self;
+      if (a.mc) { Agc[(size_t)x.b * gs + gs - 1] = ovl; Agc[(size_t)x.b * gs + gs - 2] = self; }
+    }
   }
   if (hmode >= 0) {
+    // (32-bit shared addresses: one IMAD per operand instead of 64-bit generic address math)
+    const uint32_t gown32 = smem_u32(sm.Gown), cown32 = smem_u32(sm.Cown);
+    const uint32_t gstep = 8u * (uint32_t)gs, cstep = 8u * (uint32_t)(wcol * r);
     for (int e = tid; e < gs - 2; e += RW_NT) {
       double v = 0.0;
       if (e < gcnt) {
         double f[TP_MAXD];
 #pragma unroll
         for (int kk = 0; kk < TP_MAXD; ++kk)
-          f[kk] = (kk < a.d && kk != hmode) ? (kk == k ? sm.gpub[e] : sm.Gown[(size_t)kk * gs + e]) : 1.0;
+          f[kk] = (kk < a.d && kk != hmode)
+                      ? (kk == k ? sm.gpub[e] : lds64(gown32 + (uint32_t)kk * gstep + 8u * (uint32_t)e))
+                      : 1.0;
         v = 1.0;
 #pragma unroll
         for (int kk = 0; kk < TP_MAXD; ++kk) v *= f[kk];
       }
       Ab[e] = v;
+      if (a.mc) Agc[(size_t)x.b * gs + e] = v;
     }
     for (int e = tid; e < ncr; e += RW_NT) {
       const int dv = sm.divT[e], cc = dv & 0xffff, l = dv >> 16;
       double f[TP_MAXD];
 #pragma unroll
       for (int kk = 0; kk < TP_MAXD; ++kk)
-        f[kk] = (kk < a.d && kk != hmode) ? sm.Cown[(size_t)kk * wcol * r + e] : 1.0;
+        f[kk] = (kk < a.d && kk != hmode) ? lds64(cown32 + (uint32_t)kk * cstep + 8u * (uint32_t)e) : 1.0;
       double v = 1.0;
 #pragma unroll
       for (int kk = 0; kk < TP_MAXD; ++kk) v *= f[kk];
       if (a.mc) Hgc[(size_t)(x.oc0 + cc) * rh + l] = v;
       else sm.hadT[(size_t)(x.oc0 + cc) * rh + l] = v;
     }
-    if (a.mc) {
-      for (int e = tid; e < x.wc * (rh - r); e += RW_NT) {   // zero row padding (multicast whole rows)
-        const int cc = e / (rh - r), l = r + e - cc * (rh - r);
-        Hgc[(size_t)(x.oc0 + cc) * rh + l] = 0.0;
-      }
-      for (int e = tid; e < gs; e += RW_NT) Agc[(size_t)x.b * gs + e] = Ab[e];
-    }
+    if (a.mc)   // zero row padding (multicast whole rows)
+      for (int cc = tid; cc < x.wc; cc += RW_NT)
+        for (int l = r; l < rh; ++l) Hgc[(size_t)(x.oc0 + cc) * rh + l] = 0.0;
   }
   __syncthreads();
+  RW_PROF(13);
   // ---- 4. publish the had rows and the Gram block to every peer
   if (a.mc) {
     // one TMA multicast per block: read once from L2, delivered into every CTA's had rows /
@@ -760,12 +759,9 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
           if (lane == 0) rw_flag(a, x, u);
         } else {
           rw_build_a_w(a, sm, NWK * 32);
-          RW_PROF(12);
           if (warm) {
             mbar_wait(sm.bar, xph);
-            RW_PROF(13);
             double em = rw_gemm<RM>(sm.Am, sm.X0, sm.scr, rh, r, 0, NWK);   // T = 2I - A X0, |I - A X0|
-            RW_PROF(14);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
             if (lane == 0) sm.part[warp] = em;
@@ -818,9 +814,14 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
         RW_PROF(3);
         for (int e = tid; e < nb * r; e += RW_NT) {
           const int dv = sm.divT[e], sr = dv & 0xffff, l = dv >> 16;
+          const uint32_t y32 = smem_u32(sm.scr) + 8u * (uint32_t)e, ystep = 8u * (uint32_t)nslot;
+          double yv[RW_PMAX];
+#pragma unroll
+          for (int cc = 0; cc < RW_PMAX; ++cc) yv[cc] = cc < x.P ? lds64(y32 + (uint32_t)cc * ystep) : 0.0;
           double v = 0.0;
-          for (int cc = 0; cc < x.P; ++cc) v += sm.scr[(size_t)cc * nslot + e];
-          sm.rb[sr * rh + l] = v;
+#pragma unroll
+          for (int cc = 0; cc < RW_PMAX; ++cc) v += yv[cc];
+          sts64(smem_u32(sm.rb) + 8u * (uint32_t)(sr * rh + l), v);
         }
       }
       __syncthreads();
@@ -844,9 +845,10 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
           for (int h = 0; h < 2; ++h) {
             const int i = n * 8 + 2 * (lane & 3) + h;
             const double v = h ? acc1 : acc0;
-            if (s >= nb && i < r && s < rw_nbr(a)) sm.Us[s * rh + i] = 0.0;   // K padding of the next partials
+            const uint32_t ua = smem_u32(sm.Us) + 8u * (uint32_t)(s * rh + i);
+            if (s >= nb && i < r && s < rw_nbr(a)) sts64(ua, 0.0);   // K padding of the next partials
             if (s < nb && i < r) {
-              sm.Us[s * rh + i] = v;
+              sts64(ua, v);
               if (!isfinite(v)) nf = 1;
               if (nwrite) a.U[a.offU[j] + (size_t)(qb0 + s) * r + i] = v;
             }
@@ -901,7 +903,6 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
 }
 
 static int g_rows_mc = 1;   // debug hook: 0 = publishes by st.async remote stores
-static int g_rows_gpush = 0;   // debug hook: 1 = partial pushes as global staging + TMA copies (measured no faster)
 
 static const void* rows_kernel(int rm) {
   switch (rm) {
@@ -985,8 +986,7 @@ int als_rows_plan(int d, const int* q, int R, int r, int S_force, int P_force, R
                 align_up(sizeof(double)) + pl.ws_inner +
                 align_up(sizeof(double) * (size_t)S * P * d * pl.rm * rw_pad4(r)) +
                 align_up(sizeof(double) * 2 * (size_t)P * pl.a.kpad * rw_pad4(r)) +
-                align_up(sizeof(double) * 2 * (size_t)P * S * pl.a.gstride) +
-                align_up(sizeof(double) * 2 * (size_t)P * S * (pl.a.cst_len + S * pl.a.gstride)) + 256;
+                align_up(sizeof(double) * 2 * (size_t)P * S * pl.a.gstride) + 256;
         return TP_OK;
       }
     }
@@ -1010,8 +1010,6 @@ int als_rows_run(const RowsPlan& plan, const double* V, double* U, int sweeps, d
   a.Ag = cv.take<double>(2 * (size_t)a.P * a.S * a.gstride);
   a.ns = ns;
   a.mc = g_rows_mc;
-  a.Cg = cv.take<double>(2 * (size_t)a.P * a.S * (a.cst_len + a.S * a.gstride));
-  a.gpush = g_rows_gpush;
   a.V = V; a.U = U; a.trace = trace; a.info = info; a.norm_sq = nsq;
   a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = tol; a.stall = stall;
   a.need_resid = (trace != nullptr) || (tol > 0.0) || (stall > -INFINITY);
@@ -1046,4 +1044,3 @@ int als_rows_run(const RowsPlan& plan, const double* V, double* U, int sweeps, d
 }  // namespace tp
 
 extern "C" void tp_debug_set_als_rows_mc(int on) { tp::g_rows_mc = on; }
-extern "C" void tp_debug_set_als_rows_gpush(int on) { tp::g_rows_gpush = on; }

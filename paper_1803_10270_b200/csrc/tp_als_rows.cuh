@@ -20,8 +20,6 @@ struct RowsArgs {
   double* Hg;                       // [2][P][kpad][pad4(r)] had publish staging (multicast source)
   double* Ag;                       // [2][P][S][gstride] A-block publish staging
   int mc;                           // publishes by TMA multicast from global staging (else st.async)
-  double* Cg;                       // [2][P][S][cst_len + S gstride] push staging (gpush)
-  int gpush;                        // pushes as global staging + TMA copies into the owners' inboxes
   const double* norm_sq;
   double* trace;
   int* info;

@@ -422,7 +422,7 @@ def test_apply_more_than_64_terms(cplx):
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-12, atol=1e-12)
 
 
-@pytest.mark.parametrize("comm", ["mc", "dsmem", "gpush"])
+@pytest.mark.parametrize("comm", ["mc", "dsmem"])
 @pytest.mark.parametrize("ns", [6, 0])
 @pytest.mark.parametrize("reg", [None, 1e-10])
 @pytest.mark.parametrize("qs,R,r", [((256,) * 6, 512, 32), ((48, 40, 64, 36), 200, 16), ((20, 33, 17, 40), 64, 8)])
@@ -437,9 +437,7 @@ def test_als_rows_kernel(als_variant, comm, ns, reg, qs, R, r):
     als_variant(8, 0)
     L.tp_debug_set_als_ns(ns)
     L.tp_debug_set_als_rows_mc.argtypes = [ctypes.c_int]
-    L.tp_debug_set_als_rows_gpush.argtypes = [ctypes.c_int]
     L.tp_debug_set_als_rows_mc(0 if comm == "dsmem" else 1)    # cluster publishes: TMA multicast / st.async
-    L.tp_debug_set_als_rows_gpush(1 if comm == "gpush" else 0)  # partial pushes: L2 + TMA / st.async
     try:
         assert cp.als_plan(qs, R, r)["kernel"] == "als_rows"
         rng = np.random.default_rng(R + r + ns)
@@ -457,7 +455,6 @@ def test_als_rows_kernel(als_variant, comm, ns, reg, qs, R, r):
     finally:
         L.tp_debug_set_als_ns(6)
         L.tp_debug_set_als_rows_mc(1)
-        L.tp_debug_set_als_rows_gpush(0)
 
 
 def test_als_rows_is_config1_default():

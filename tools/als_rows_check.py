@@ -50,11 +50,8 @@ U = I0.data.clone()
 outs = {}
 ref = ocp.als([np.asarray(v) for v in w["V"]], [np.asarray(v) for v in w["init"]], 20, lam=1e-10)
 L.tp_debug_set_als_rows_mc.argtypes = [ctypes.c_int]
-L.tp_debug_set_als_rows_gpush.argtypes = [ctypes.c_int]
-for name, var, cs, pr in [("cluster4", 2, 4, 0), ("rows16", 8, 16, 0), ("rows16-dsm", 8, 16, -2),
-                          ("rows16-mc", 8, 16, -1)]:
+for name, var, cs, pr in [("rows16", 8, 16, 0)]:
     L.tp_debug_set_als_rows_mc(0 if pr == -2 else 1)
-    L.tp_debug_set_als_rows_gpush(0 if pr < 0 else 1)
     pr = max(pr, 0)
     L.tp_debug_set_als_variant(var, cs)
     L.tp_debug_set_als_rows(1 if var == 8 else 0, pr)
@@ -85,9 +82,9 @@ for name, var, cs, pr in [("cluster4", 2, 4, 0), ("rows16", 8, 16, 0), ("rows16-
         L.tp_debug_set_als_profile(None)
         p = prof.cpu().numpy() / 120.0
         lab = {7: "Y dmma", 8: "slot store", 1: "signal", 2: "inverse", 3: "wait", 4: "gather", 5: "solve",
-               9: "xch dmma+push", 10: "B1", 11: "reduce+publish", 6: "B2", 0: "loop", 12: "build_a", 13: "x0 wait", 14: "gemm0"}
+               9: "xch dmma+push", 10: "B1", 11: "reduce+publish", 6: "B2", 0: "loop", 12: "owner sums", 13: "A/H blocks"}
         print("   cycles per mode update: " + " | ".join("%s %.0f" % (lab[i], p[i]) for i in
-                                                          (7, 8, 12, 13, 14, 1, 2, 3, 4, 5, 9, 10, 11, 6, 0)), flush=True)
+                                                          (7, 8, 1, 2, 3, 4, 5, 9, 10, 12, 13, 11, 6, 0)), flush=True)
     if var == 8:
         L.tp_debug_set_als_ns.argtypes = [ctypes.c_int]
         L.tp_debug_set_als_ns(0)
@@ -110,4 +107,3 @@ for var, cs in [(2, 4), (8, 16)]:
 L.tp_debug_set_als_variant(0, 0)
 L.tp_debug_set_als_rows(1, 0)
 L.tp_debug_set_als_rows_mc(1)
-L.tp_debug_set_als_rows_gpush(1)
