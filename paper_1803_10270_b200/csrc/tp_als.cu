@@ -2610,7 +2610,8 @@ struct PlanKey {
 };
 
 static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
-  if (d < 1 || d > TP_MAXD || R < 1 || r < 1 || !q) return TP_EINVAL;
+  if (d < 1 || R < 1 || r < 1 || !q) return TP_EINVAL;
+  if (d > TP_MAXD) return TP_EUNSUPPORTED;   // (the streamed variant takes up to TP_MAXD_GEN modes)
   static std::mutex mu;
   static std::vector<std::pair<PlanKey, AlsPlan>> cache;
   PlanKey key;
@@ -2633,7 +2634,8 @@ static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
 }
 
 static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
-  if (d < 1 || d > TP_MAXD || R < 1 || r < 1 || !q) return TP_EINVAL;
+  if (d < 1 || R < 1 || r < 1 || !q) return TP_EINVAL;
+  if (d > TP_MAXD) return TP_EUNSUPPORTED;
   for (int k = 0; k < d; ++k) if (q[k] < 1) return TP_EINVAL;
   pl.rm = choose_rm(r);
   if (!pl.rm) return TP_EUNSUPPORTED;
@@ -2888,8 +2890,9 @@ int tp_cp_als_recipe_f64(int d, const int* q, int r, const double* A, int ra, co
                          const double* mats, const long long* mat_off, int n_mats, double* U, int sweeps, double reg,
                          int reg_mode, int* info, void* ws, size_t ws_bytes, void* stream) {
   if (!A || !W0 || !U || !info || sweeps < 0 || !(reg >= 0.0) || ra < 1 || rw < 1 || n_terms < 1 || n_terms > 64 ||
-      d < 1 || d > TP_MAXD)
+      d < 1)
     return TP_EINVAL;
+  if (d > TP_MAXD) return TP_EUNSUPPORTED;
   const int nw = W1 ? 2 : 1;
   const int R = ra + n_terms * nw * rw;
   AlsPlan pl;

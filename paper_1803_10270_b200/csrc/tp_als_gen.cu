@@ -195,7 +195,7 @@ static GenLayout gen_layout(int d, const int* q, int R, int r) {
 }
 
 int als_generic_supported(int d, const int* q, int R, int r) {
-  if (d < 1 || d > TP_MAXD || R < 1 || r < 1 || r > ALSG_RMAX || !q) return 0;
+  if (d < 1 || d > TP_MAXD_GEN || R < 1 || r < 1 || r > ALSG_RMAX || !q) return 0;
   for (int k = 0; k < d; ++k) if (q[k] < 1) return 0;
   return 1;
 }
@@ -231,7 +231,7 @@ int als_generic_run(int d, const int* q, int R, const double* V, int r, double* 
   int qmax = 0;
   for (int k = 0; k < d; ++k) qmax = q[k] > qmax ? q[k] : qmax;
   const size_t part_doubles = 16 * (size_t)r * (r > qmax ? r : qmax);
-  long long offV[TP_MAXD], offU[TP_MAXD];
+  long long offV[TP_MAXD_GEN], offU[TP_MAXD_GEN];
   long long ov = 0, ou = 0;
   for (int k = 0; k < d; ++k) { offV[k] = ov; offU[k] = ou; ov += (long long)q[k] * R; ou += (long long)q[k] * r; }
   const bool need_resid = trace || tol > 0.0 || stall > -INFINITY;

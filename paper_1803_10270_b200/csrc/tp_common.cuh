@@ -9,7 +9,8 @@
 #include <vector>
 #include "../../include/tpde_b200.h"
 
-#define TP_MAXD 8          // max modes of a CP tensor handled by the ALS kernels
+#define TP_MAXD 8          // max modes of a CP tensor handled by the fused ALS kernels
+#define TP_MAXD_GEN 16     // max modes of the streamed ALS, inner product, apply and contraction kernels
 #define TP_RMAX 32         // max fitted rank in the warp-register Cholesky
 
 namespace tp {

@@ -34,8 +34,8 @@ constexpr int IP_LD = 36;     // padded smem row (conflict-free fragment loads)
 
 struct InnerArgs {
   int d, ra, rb, same, ntl, ntm;
-  int q[TP_MAXD];
-  long long offA[TP_MAXD], offB[TP_MAXD];
+  int q[TP_MAXD_GEN];
+  long long offA[TP_MAXD_GEN], offB[TP_MAXD_GEN];
   const double* A;
   const double* B;
   double* partial;
@@ -151,13 +151,13 @@ constexpr int AP_MAXT = 64;
 
 struct ApplyArgs {
   int d, r_in, R_out, col_off, n_terms;
-  int q[TP_MAXD];
-  long long offF[TP_MAXD], offO[TP_MAXD];
+  int q[TP_MAXD_GEN];
+  long long offF[TP_MAXD_GEN], offO[TP_MAXD_GEN];
   const double* F;
   double* out;
   const double* mats;
   double w0[AP_MAXT];                 // scale * weight per term (mode 0 only)
-  long long moff[AP_MAXT][TP_MAXD];   // matrix element offset, -1 = identity
+  long long moff[AP_MAXT][TP_MAXD_GEN];   // matrix element offset, -1 = identity
 };
 
 // the argument block (~5 KB) is passed by value (CUDA >= 12.1 allows 32 KB of
@@ -219,7 +219,7 @@ using namespace tp;
 // in shared memory, fixed-order block reduction.
 constexpr int CT_NT = 256;
 
-struct QOff { int v[TP_MAXD + 1]; };
+struct QOff { int v[TP_MAXD_GEN + 1]; };
 
 __global__ void __launch_bounds__(CT_NT) cp_contract_kernel(int d, const __grid_constant__ QOff qo_, int sumq, int R,
                                                             const double* __restrict__ F,
@@ -285,7 +285,7 @@ size_t tp_cp_inner_ws_bytes(int d, const int* q, int ra, int rb) {
 
 int tp_cp_inner_f64(int d, const int* q, int ra, const double* A, int rb, const double* B,
                     int same, double* out, void* ws, size_t ws_bytes, void* stream) {
-  if (d < 1 || d > TP_MAXD || ra < 1 || rb < 1 || !A || !B || !out || !q) return TP_EINVAL;
+  if (d < 1 || d > TP_MAXD_GEN || ra < 1 || rb < 1 || !A || !B || !out || !q) return TP_EINVAL;
   for (int k = 0; k < d; ++k) if (q[k] < 1) return TP_EINVAL;
   if (same && (ra != rb || A != B)) return TP_EINVAL;
   if (ws_bytes < sizeof(double) * (size_t)inner_tiles(ra, rb, same)) return TP_EWORKSPACE;
@@ -296,7 +296,7 @@ int tp_cp_apply_f64(int d, const int* q, int r_in, const double* F, int n_terms,
                     const double* weights, double scale, const int* mat_idx,
                     const double* mats, const long long* mat_off, int n_mats,
                     double* out, int R_out, int col_off, void* stream) {
-  if (d < 1 || d > TP_MAXD || r_in < 1 || n_terms < 1 || !F || !out || !q || !weights) return TP_EINVAL;
+  if (d < 1 || d > TP_MAXD_GEN || r_in < 1 || n_terms < 1 || !F || !out || !q || !weights) return TP_EINVAL;
   if (col_off < 0 || col_off + (long long)n_terms * r_in > R_out) return TP_EINVAL;
   if (n_terms > AP_MAXT) {   // more terms than one argument block holds: consecutive launches
     for (int t0 = 0; t0 < n_terms; t0 += AP_MAXT) {
@@ -340,7 +340,7 @@ int tp_cp_apply_f64(int d, const int* q, int r_in, const double* F, int n_terms,
 
 int tp_cp_contract_f64(int d, const int* q, int R, const double* F, int nw, const double* W, double* out,
                        void* stream) {
-  if (d < 1 || d > TP_MAXD || R < 1 || nw < 0 || !q || !F || !out || (nw > 0 && !W)) return TP_EINVAL;
+  if (d < 1 || d > TP_MAXD_GEN || R < 1 || nw < 0 || !q || !F || !out || (nw > 0 && !W)) return TP_EINVAL;
   QOff qo;
   qo.v[0] = 0;
   for (int k = 0; k < d; ++k) {

@@ -486,3 +486,26 @@ def test_als_near_singular_gram_trace_rule(als_variant, variant, cluster):
     assert sens_t > 1e-7   # (really ill-conditioned: the reference's own rounding moves the fit)
     assert float(np.max(np.abs(np.array(trace) - np.array(otrace)) / np.array(otrace))) <= 10 * sens_t
     assert metrics.cp_rel_diff(ref, out.to_numpy()) <= 10 * sens_f
+
+
+@pytest.mark.parametrize("d", [10, 16])
+def test_many_modes(d):
+    """More modes than the fused kernels hold (d > 8): ALS through the streamed variant,
+    inner product and operator apply up to 16 modes, against the oracle."""
+    from oracle import operators as oops
+    rng = np.random.default_rng(d)
+    qs = tuple(int(q) for q in rng.integers(5, 9, size=d))
+    R, r = 14, 3
+    V = rand_factors(rng, qs, R, 0.6)
+    init = [v[:, :r].copy() for v in V]
+    assert cp.als_plan(qs, R, r)["kernel"] == "als_generic"
+    out, ref, trace, otrace = _als_case(V, init, 4, 1e-10)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+    S = specs_for(qs)
+    T = cp.CPTensor(S, V)
+    assert abs(cp.inner_product(T, T) - ocp.inner_product(V, V).real) <= 1e-12 * abs(cp.inner_product(T, T))
+    mats = [[rng.standard_normal((q, q)) / q if k == t else None for k, q in enumerate(qs)] for t in range(3)]
+    L = operators.SeparableOperator(S, (0.5, -1.0, 2.0), tuple(tuple(m) for m in mats))
+    got = operators.apply(L, T).to_numpy()
+    exp = oops.apply([0.5, -1.0, 2.0], mats, V)
+    assert metrics.cp_rel_diff(exp, got) <= 1e-13
