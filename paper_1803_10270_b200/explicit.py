@@ -286,5 +286,4 @@ def run(f0: CPTensor, L: SeparableOperator, config: ExplicitConfig, steps: int, 
         raise cp.ConditioningError("normal equations produced non-finite coefficients")
     if bad & 1:
         raise cp.ConditioningError("regularised normal equations are not positive definite")
-    _ = math
     return cur

@@ -443,11 +443,27 @@ def _norms_batch(hs):
 
 
 def inner_product(h1: HTTensor, h2: HTTensor) -> float:
-    """ht.py:264-276 via the polarisation identity on the device norms:
-    <h1, h2> = (|h1 + h2|^2 - |h1 - h2|^2) / 4 (real path)."""
+    """ht.py:264-276: leaves-to-root contraction of the two trees on the device.
+    Leaf Grams U1^T U2; an interior node folds its children's Grams into its
+    transfers, M_t = sum B1[a,b,i] M_l[a,c] M_r[b,d] B2[c,d,j] (two GEMMs and a
+    batched one); the root's 1x1 Gram is the inner product (real path)."""
     _check_compatible(h1, h2)
-    n = _norms_batch([add(h1, h2), add(h1, scale(h2, -1.0))])
-    return float((n[0] ** 2 - n[1] ** 2) / 4.0)
+    nodes = h1.tree.nodes
+    grams = [None] * len(nodes)
+    for i in reversed(range(len(nodes))):
+        node = nodes[i]
+        if node.is_leaf:
+            grams[i] = h1.frames[i].T @ h2.frames[i]
+            continue
+        b1, b2 = h1.transfers[i], h2.transfers[i]
+        ml, mr = grams[node.left], grams[node.right]
+        ka, kb, ki = b1.shape
+        kc, kd = ml.shape[1], mr.shape[1]
+        t = (ml.T @ b1.reshape(ka, kb * ki)).reshape(kc, kb, ki)          # [c, b, i]
+        t = (mr.T @ t.permute(1, 0, 2).reshape(kb, kc * ki))               # [d, (c, i)]
+        t = t.reshape(kd, kc, ki).permute(1, 0, 2).reshape(kc * kd, ki)   # [(c, d), i]
+        grams[i] = t.T @ b2.reshape(kc * kd, b2.shape[2])
+    return float(grams[0].reshape(-1)[0].item())
 
 
 def apply_operator(op, h: HTTensor) -> HTTensor:

@@ -2,7 +2,6 @@
 every symbol include/tpde_b200.h declares (no compute calls), and host-side
 validation mirrors the reference's error behaviour."""
 
-import ctypes
 
 import numpy as np
 import pytest
@@ -93,7 +92,6 @@ def test_no_cpu_fallback_without_device():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError, match="CUDA device"):
         _lib.device()
-    _ = ctypes
 
 
 def test_explicit_config_validation():

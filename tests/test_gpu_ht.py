@@ -9,7 +9,6 @@ import numpy as np
 import pytest
 
 from conftest import load_golden, unpack_ht
-from oracle import cp_als as ocp
 from oracle import ht_hsvd as oht
 from oracle import metrics
 
@@ -121,7 +120,25 @@ def test_norm_and_inner_product():
     n1 = oht.norm(o1)
     assert abs(ht.norm(h1) - n1) <= 1e-12 * n1
     ip = oht.inner_product(o1, o2).real
-    assert abs(ht.inner_product(h1, h2) - ip) <= 1e-10 * oht.norm(o1) * oht.norm(o2)
+    assert abs(ht.inner_product(h1, h2) - ip) <= 1e-13 * oht.norm(o1) * oht.norm(o2)
+
+
+def test_inner_product_nearly_orthogonal():
+    """<h1, h2> ~ 1e-9 |h1| |h2|: a direct contraction keeps it to rounding of
+    |h1| |h2| (a polarisation identity on two norms would lose it entirely)."""
+    rng = np.random.default_rng(13)
+    d, q = 4, 9
+    S = specs(d, q)
+    f = [rng.standard_normal((q, 3)) for _ in range(d)]
+    g = [rng.standard_normal((q, 2)) for _ in range(d)]
+    qf, _ = np.linalg.qr(f[0])
+    g[0] = g[0] - qf @ (qf.T @ g[0]) + 1e-9 * f[0][:, :2]
+    of, og = oht.from_cp(f), oht.from_cp(g)
+    ip = oht.inner_product(of, og).real
+    scale_ = oht.norm(of) * oht.norm(og)
+    assert abs(ip) < 1e-7 * scale_
+    got = ht.inner_product(ht.from_cp(cp.CPTensor(S, f)), ht.from_cp(cp.CPTensor(S, g)))
+    assert abs(got - ip) <= 1e-14 * scale_
 
 
 def test_from_cp_add_scale_apply():
@@ -142,7 +159,6 @@ def test_from_cp_add_scale_apply():
     from oracle import operators as oops
     ref_cp = oops.apply([-1.0, -0.5, 0.75], mats, f)
     assert metrics.ht_rel_diff(oht.from_cp(ref_cp), out.to_oracle()) <= 1e-12
-    _ = ocp
 
 
 @pytest.mark.parametrize("form_gemm", [1, 0])

@@ -8,7 +8,6 @@ import math
 
 import numpy as np
 import pytest
-import torch
 
 from oracle import cp_als as ocp
 from oracle import metrics
@@ -84,7 +83,6 @@ def test_sharded_api_single_rank_equals_fused_kernel():
     a = parallel.sharded_cp_approx_als(cp.CPTensor(S, V), init, cfg)
     b = cp.cp_approx_als(cp.CPTensor(S, V), r, cfg, init=init)
     assert metrics.cp_rel_diff(b.to_numpy(), a.to_numpy()) <= 1e-12
-    _ = torch
 
 
 def test_captured_graph_replay_matches_eager():
