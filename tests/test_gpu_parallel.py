@@ -8,6 +8,7 @@ import math
 
 import numpy as np
 import pytest
+import torch
 
 from oracle import cp_als as ocp
 from oracle import metrics
