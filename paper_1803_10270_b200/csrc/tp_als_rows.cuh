@@ -20,6 +20,7 @@ struct RowsArgs {
   double* Hg;                       // [2][P][kpad][pad4(r)] had publish staging (multicast source)
   double* Ag;                       // [2][P][S][gstride] A-block publish staging
   int mc;                           // publishes by TMA multicast from global staging (else st.async)
+  int split;                        // rhs product on warps 0-3 while warps 4-7 form A_j and its inverse
   const double* norm_sq;
   double* trace;
   int* info;

@@ -422,14 +422,16 @@ def test_apply_more_than_64_terms(cplx):
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-12, atol=1e-12)
 
 
-@pytest.mark.parametrize("comm", ["mc", "dsmem"])
+@pytest.mark.parametrize("comm", ["mc", "dsmem", "mc-unsplit"])
 @pytest.mark.parametrize("ns", [6, 0])
 @pytest.mark.parametrize("reg", [None, 1e-10])
 @pytest.mark.parametrize("qs,R,r", [((256,) * 6, 512, 32), ((48, 40, 64, 36), 200, 16), ((20, 33, 17, 40), 64, 8)])
 def test_als_rows_kernel(als_variant, comm, ns, reg, qs, R, r):
     """Cluster-row kernel (variant 8: 16-CTA clusters own R-slabs, one flag exchange per mode
     update): warm-started Newton-Schulz inverse on and off (exact sweep every time), both
-    regulariser rules, ragged modes, config-1 size, with the residual trace."""
+    regulariser rules, ragged modes, config-1 size, with the residual trace; cluster publishes
+    by TMA multicast or st.async; the rhs product beside the inverse (split warps, default)
+    or before it."""
     import ctypes
     from paper_1803_10270_b200 import _lib
     L = _lib.lib()
@@ -438,6 +440,8 @@ def test_als_rows_kernel(als_variant, comm, ns, reg, qs, R, r):
     L.tp_debug_set_als_ns(ns)
     L.tp_debug_set_als_rows_mc.argtypes = [ctypes.c_int]
     L.tp_debug_set_als_rows_mc(0 if comm == "dsmem" else 1)    # cluster publishes: TMA multicast / st.async
+    L.tp_debug_set_als_rows_split.argtypes = [ctypes.c_int]
+    L.tp_debug_set_als_rows_split(0 if comm == "mc-unsplit" else 1)
     try:
         assert cp.als_plan(qs, R, r)["kernel"] == "als_rows"
         rng = np.random.default_rng(R + r + ns)
@@ -455,6 +459,7 @@ def test_als_rows_kernel(als_variant, comm, ns, reg, qs, R, r):
     finally:
         L.tp_debug_set_als_ns(6)
         L.tp_debug_set_als_rows_mc(1)
+        L.tp_debug_set_als_rows_split(1)
 
 
 def test_als_rows_is_config1_default():

@@ -50,8 +50,10 @@ U = I0.data.clone()
 outs = {}
 ref = ocp.als([np.asarray(v) for v in w["V"]], [np.asarray(v) for v in w["init"]], 20, lam=1e-10)
 L.tp_debug_set_als_rows_mc.argtypes = [ctypes.c_int]
-for name, var, cs, pr in [("rows16", 8, 16, 0)]:
+for name, var, cs, pr in [("rows16", 8, 16, 0), ("unsplit", 8, 16, 0)]:
     L.tp_debug_set_als_rows_mc(0 if pr == -2 else 1)
+    L.tp_debug_set_als_rows_split.argtypes = [ctypes.c_int]
+    L.tp_debug_set_als_rows_split(0 if name == "unsplit" else 1)
     pr = max(pr, 0)
     L.tp_debug_set_als_variant(var, cs)
     L.tp_debug_set_als_rows(1 if var == 8 else 0, pr)
