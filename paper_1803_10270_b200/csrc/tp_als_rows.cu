@@ -416,6 +416,9 @@ __device__ __forceinline__ void rw_chains(uint32_t a0, uint32_t arow, const uint
 struct RwCtx {
   int b, c, S, P, w, c0;   // rank in cluster, cluster (slab), sizes, slab width / start
   int oc0, wc;             // owned slab columns [oc0, oc0 + wc)
+  uint32_t in_bytes;       // bytes an exchange delivers into this CTA's inbox (the S - 1 peers' pieces)
+  uint32_t pub_bytes;      // bytes the publishes of an exchange deliver (had rows + A blocks)
+  int gcnt;                // packed Gram entries this CTA owns
 };
 
 #define RW_PROF(i)                                                   \
@@ -456,14 +459,8 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
   const uint32_t cst32 = smem_u32(cst), gst32 = smem_u32(gst);
   const uint32_t us32 = smem_u32(sm.Us), vs32 = smem_u32(sm.Vs + (size_t)a.vrow[k] * a.ldw);
   if (tid == 0) {   // this phase's expected bytes (peers may already be sending: tx count goes negative)
-    uint32_t pub = 0;
-    for (int q = 0; q < S; ++q) {
-      if (hmode < 0) break;
-      if (a.mc) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * rh + gs) * 8);   // every owner, self incl.
-      else if (q != x.b) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * r + gs) * 8);
-    }
-    mbar_arrive_expect_tx(sm.bar + 1, (uint32_t)((S - 1) * (x.wc * rs2 + gs) * 8));
-    mbar_arrive_expect_tx(sm.bar + 2, pub);
+    mbar_arrive_expect_tx(sm.bar + 1, x.in_bytes);
+    mbar_arrive_expect_tx(sm.bar + 2, hmode >= 0 ? x.pub_bytes : 0u);
   }
   // ---- 1. partials into local staging
   for (int it = warp; it < nitems; it += RW_NW) {
@@ -507,6 +504,7 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
     }
   }
   __syncthreads();
+  RW_PROF(14);
   // ---- 2. pushes: owner q <- (C^T rows [oc0(q), oc1(q)), Gram block q) into its slot b
   {
     const uint32_t slot = smem_u32(sm.inbox) + 8u * (uint32_t)(x.b * piece);
@@ -567,7 +565,7 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
   // multicast staging of this exchange (double-buffered by exchange parity)
   double* Hgc = a.mc ? a.Hg + ((size_t)ph_pub * x.P + x.c) * (size_t)a.kpad * rh : nullptr;
   double* Agc = a.mc ? a.Ag + ((size_t)ph_pub * x.P + x.c) * (size_t)S * gs : nullptr;
-  const int gcnt = (ng * (x.b + 1)) / S - (ng * x.b) / S;
+  const int gcnt = x.gcnt;
   for (int e = tid; e < gs; e += RW_NT) sm.Gown[(size_t)k * gs + e] = sm.gpub[e];
   if (want_ovl) {
     double ovl = 0.0, self = 0.0;
@@ -609,6 +607,7 @@ __device__ void rw_exchange(const RowsArgs& a, const RwSmem& sm, const RwCtx& x,
       Ab[e] = v;
       if (a.mc) Agc[(size_t)x.b * gs + e] = v;
     }
+    RW_PROF(15);
     for (int e = tid; e < ncr; e += RW_NT) {
       const int dv = sm.divT[e], cc = dv & 0xffff, l = dv >> 16;
       double f[TP_MAXD];
@@ -751,6 +750,18 @@ __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ Row
     }
   }
   __syncthreads();
+  {
+    const int gs = a.gstride;
+    uint32_t pub = 0;
+    for (int q = 0; q < a.S; ++q) {
+      if (a.mc) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * rh + gs) * 8);   // every owner, self incl.
+      else if (q != x.b) pub += (uint32_t)(((sm.ocT[q + 1] - sm.ocT[q]) * r + gs) * 8);
+    }
+    x.pub_bytes = pub;
+    x.in_bytes = (uint32_t)((a.S - 1) * (x.wc * a.rs2 + gs) * 8);
+    const int ng = r * (r + 1) / 2;
+    x.gcnt = (ng * (x.b + 1)) / a.S - (ng * x.b) / a.S;
+  }
   for (int k = 0; k < d; ++k) {
     const int qb0 = sm.qb0T[k], nb = sm.nbT[k];
     const double* Vk = a.V + a.offV[k] + (size_t)qb0 * a.R + x.c0;

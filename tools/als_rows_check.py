@@ -84,9 +84,9 @@ for name, var, cs, pr in [("rows16", 8, 16, 0), ("unsplit", 8, 16, 0)]:
         L.tp_debug_set_als_profile(None)
         p = prof.cpu().numpy() / 120.0
         lab = {7: "Y dmma", 8: "slot store", 1: "signal", 2: "inverse", 3: "wait", 4: "gather", 5: "solve",
-               9: "xch dmma+push", 10: "B1", 11: "reduce+publish", 6: "B2", 0: "loop", 12: "owner sums", 13: "A/H blocks"}
+               9: "xch dmma+push", 10: "B1", 11: "reduce+publish", 6: "B2", 0: "loop", 12: "owner sums", 13: "H blocks", 14: "xch dmma", 15: "A blk"}
         print("   cycles per mode update: " + " | ".join("%s %.0f" % (lab[i], p[i]) for i in
-                                                          (7, 8, 1, 2, 3, 4, 5, 9, 10, 12, 13, 11, 6, 0)), flush=True)
+                                                          (7, 8, 1, 2, 3, 4, 5, 14, 9, 10, 12, 15, 13, 11, 6, 0)), flush=True)
     if var == 8:
         L.tp_debug_set_als_ns.argtypes = [ctypes.c_int]
         L.tp_debug_set_als_ns(0)
