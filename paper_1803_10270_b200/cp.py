@@ -303,7 +303,7 @@ def als_plan(qs, R: int, r: int, grid: int = 0) -> dict:
     st = _lib.lib().tp_cp_als_plan(len(qs), _lib.int_array(qs), R, r, grid, out)
     _lib.check(st, "als_plan")
     variant = {0: "als_persistent", 1: "als_cluster", 2: "als_small", 3: "als_persistent_cluster",
-               5: "als_tiny8", 7: "als_generic", 8: "als_rows"}[out[0]]
+               5: "als_tiny8", 7: "als_generic", 8: "als_rows", 9: "als_w"}[out[0]]
     return {"kernel": variant, "ctas": out[1], "cluster": out[2], "smem_bytes": out[3]}
 
 

@@ -23,6 +23,7 @@
 // reproducible for a fixed grid size.
 #include "tp_common.cuh"
 #include "tp_als_rows.cuh"
+#include "tp_als_w.cuh"
 #include <cooperative_groups.h>
 #include <cstring>
 #include <cstdlib>
@@ -2460,6 +2461,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_xg(const __grid_constant__ AlsA
 struct AlsPlan {
   AlsArgs a;
   RowsPlan rows;            // variant 8: cluster-row kernel (tp_als_rows.cu)
+  WPlan w;                  // variant 9: Gram-space kernel (tp_als_w.cu) with the cluster-row kernel as its fallback
   int P, rm, variant, Pr;   // variant 0: als_persistent, 1: als_cluster (P = Pr * a.Pq), 2: als_small,
                             // 3: als_persistent as one cluster of P CTAs, 5: als_tiny8 (r <= 8, one CTA)
   size_t smem, ws_inner, ws_total, ydoubles;
@@ -2703,15 +2705,23 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
   }
   // large truncations: the cluster-row kernel (one flag exchange + two cluster barriers per
   // mode update instead of two grid barriers)
-  if (g_variant == 8 || (g_variant == 0 && grid <= 0 && P >= 64 && g_rows)) {
+  if (g_variant == 8 || g_variant == 9 || (g_variant == 0 && grid <= 0 && P >= 64 && g_rows)) {
     AlsPlan cp = pl;
     if (als_rows_plan(d, q, R, r, g_cluster > 0 ? g_cluster : 0, g_rows_p, cp.rows) == TP_OK) {
       cp.variant = 8; cp.P = cp.rows.a.S * cp.rows.a.P; cp.Pr = cp.rows.a.P; cp.smem = cp.rows.smem;
       cp.ws_total = cp.rows.ws;
+      // well-conditioned large truncations: the sweeps in Gram space (no reduction over the factor
+      // rows), the cluster-row kernel launched behind it as the conditioning fallback
+      if ((g_variant == 0 || g_variant == 9) && als_w_plan(d, q, R, r, cp.w) == TP_OK) {
+        cp.variant = 9; cp.P = cp.w.a.P; cp.Pr = cp.w.a.P; cp.smem = cp.w.smem;
+        cp.ws_total = align_up(cp.w.ws) + cp.rows.ws;
+      } else if (g_variant == 9) {
+        return TP_EUNSUPPORTED;
+      }
       pl = cp;
       return TP_OK;
     }
-    if (g_variant == 8) return TP_EUNSUPPORTED;
+    if (g_variant == 8 || g_variant == 9) return TP_EUNSUPPORTED;
   }
   // large truncations: the cluster variant (fewer bytes per CTA per mode update)
   const bool want = g_variant == 2 || (g_variant == 0 && grid <= 0 && P >= 64 && g_cluster >= 0);
@@ -2807,6 +2817,15 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
   if (st != TP_OK) return st;
   if (!ws || ws_bytes < pl.ws_total) return TP_EWORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
+  if (pl.variant == 9) {
+    const int* redo = nullptr;
+    const int pc = g_prof_cta < 0 ? pl.P + g_prof_cta : g_prof_cta;
+    st = als_w_run(pl.w, V, U, sweeps, reg, reg_mode, tol, stall, trace, info, ws, align_up(pl.w.ws), s, g_prof, pc, &redo);
+    if (st != TP_OK || sweeps == 0) return st;
+    return als_rows_run(pl.rows, V, U, sweeps, reg, reg_mode, tol, stall, trace, info,
+                        static_cast<char*>(ws) + align_up(pl.w.ws), ws_bytes - align_up(pl.w.ws), s, nullptr, 0,
+                        g_ns_max > 0, redo);
+  }
   if (pl.variant == 8)
     return als_rows_run(pl.rows, V, U, sweeps, reg, reg_mode, tol, stall, trace, info, ws, ws_bytes, s, g_prof,
                         g_prof_cta < 0 ? pl.P + g_prof_cta : g_prof_cta, g_ns_max > 0);

@@ -703,6 +703,7 @@ template <int RM>
 __global__ void __launch_bounds__(RW_NT, 1) als_rows(const __grid_constant__ RowsArgs a) {
   extern __shared__ __align__(16) double smem[];
   constexpr int NT = RM / 8;
+  if (a.run_if && *a.run_if == 0) return;   // (uniform: the fallback launch behind the Gram-space kernel)
   const RwSmem sm = rw_carve(smem, a, RM);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   long long prof_t = clock64(), prof_acc[16] = {};
@@ -1183,7 +1184,7 @@ int als_rows_plan(int d, const int* q, int R, int r, int S_force, int P_force, R
 
 int als_rows_run(const RowsPlan& plan, const double* V, double* U, int sweeps, double reg, int reg_mode, double tol,
                  double stall, double* trace, int* info, void* ws, size_t ws_bytes, cudaStream_t st, long long* prof,
-                 int prof_cta, int ns) {
+                 int prof_cta, int ns, const int* run_if) {
   if (!ws || ws_bytes < plan.ws) return TP_EWORKSPACE;
   RowsArgs a = plan.a;
   Carver cv(ws, ws_bytes);
@@ -1201,7 +1202,8 @@ int als_rows_run(const RowsPlan& plan, const double* V, double* U, int sweeps, d
   a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = tol; a.stall = stall;
   a.need_resid = (trace != nullptr) || (tol > 0.0) || (stall > -INFINITY);
   a.prof = prof; a.prof_cta = prof_cta;
-  cudaError_t e = cudaMemsetAsync(info, 0, 2 * sizeof(int), st);
+  a.run_if = run_if;
+  cudaError_t e = run_if ? cudaSuccess : cudaMemsetAsync(info, 0, 2 * sizeof(int), st);   // (the first kernel owns info)
   if (e != cudaSuccess) return cuda_status(e);
   e = cudaMemsetAsync(a.flags, 0, sizeof(unsigned int) * 2 * (size_t)a.S * a.P, st);
   if (e != cudaSuccess) return cuda_status(e);

@@ -30,6 +30,7 @@ struct RowsArgs {
   int need_resid;
   long long* prof;
   int prof_cta;
+  const int* run_if;                // optional device flag: the launch returns at once unless *run_if != 0
 };
 
 struct RowsPlan {
@@ -41,6 +42,6 @@ struct RowsPlan {
 int als_rows_plan(int d, const int* q, int R, int r, int S_force, int P_force, RowsPlan& pl);
 int als_rows_run(const RowsPlan& plan, const double* V, double* U, int sweeps, double reg, int reg_mode, double tol,
                  double stall, double* trace, int* info, void* ws, size_t ws_bytes, cudaStream_t st, long long* prof,
-                 int prof_cta, int ns);
+                 int prof_cta, int ns, const int* run_if = nullptr);
 
 }  // namespace tp
