@@ -609,10 +609,14 @@ def run_fused(args, world, rank, local, dev):
                 "statistic": "median of 3 timed repetitions of the K steps"},
         "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
-                     "kernel": f"tp::{plan['kernel']}<32> (one launch per step; {plan['ctas']} CTAs, "
+                     "kernel": (f"tp::als_w ({plan['ctas']} CTAs, {plan['smem_bytes']} B smem; a step = one batched bgemm "
+                                "launch (W_k = V_k^T V_k) + als_w + the als_rows fallback "
+                                "launch that returns at once; achieved = reference-algorithm flops / whole step)")
+                               if plan["kernel"] == "als_w" else
+                               f"tp::{plan['kernel']}<32> (one launch per step; {plan['ctas']} CTAs, "
                                f"cluster {plan['cluster']}, {plan['smem_bytes']} B smem)",
                      "flops_per_launch": FLOPS_PER_STEP, "peak_source": PEAK_SOURCE},
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * (3 if plan["kernel"] == "als_w" else 1),
         "clocks": clk.summary(),
         "wall_s_timed_region": t_wall,
         "steady_state_sweeps_per_s": steady,

@@ -2619,7 +2619,7 @@ static int plan_als(int d, const int* q, int R, int r, int grid, AlsPlan& pl) {
   PlanKey key;
   memset(&key, 0, sizeof(key));
   if (cudaGetDevice(&key.dev) != cudaSuccess) { cudaGetLastError(); key.dev = -1; }
-  key.d = d; key.R = R; key.r = r; key.grid = grid; key.variant = g_variant * 2 + g_early_inv + 1000 * g_rows + 100000 * g_rows_p; key.cluster = g_cluster;
+  key.d = d; key.R = R; key.r = r; key.grid = grid; key.variant = g_variant * 2 + g_early_inv + 1000 * g_rows + 100000 * g_rows_p + 4000000 * als_w_enabled(); key.cluster = g_cluster;
   for (int k = 0; k < d; ++k) key.q[k] = q[k];
   {
     std::lock_guard<std::mutex> lk(mu);

@@ -340,14 +340,65 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
   // ---- setup: zero, initial crosses / Grams of the guess, had_0, first piece
   for (size_t e = tid; e < wk_smem_doubles(d); e += WK_NT) smem[e] = 0.0;
   __syncthreads();
+  // initial crosses C_k[:, own] = U_k^T V_k[:, own]: the rows of the mode split over the 8 warps
   for (int k = 0; k < d; ++k) {
-    {
-      const int i = tid >> 3, cc = tid & 7;
-      if (i < r && cc < wv) sm.Cs[k * W_HAD + tid] = __ldg(a.C0 + ((size_t)k * r + i) * R + col0 + cc);
+    const int qk = a.q[k], r0 = (qk * warp) / 8, r1 = (qk * (warp + 1)) / 8;
+    const double* Uk = a.U + a.offU[k];
+    const double* Vk = a.V + a.offV[k] + col0;
+    double acc[4][2] = {};
+    for (int row = r0; row < r1; row += 4) {
+      const int rr = row + t;
+      const bool rv = rr < r1;
+      const double fb = (rv && g < wv) ? __ldg(Vk + (size_t)rr * R + g) : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int m = 8 * mt + g;
+        const double fa = (rv && m < r) ? __ldcg(Uk + (size_t)rr * r + m) : 0.0;
+        dmma_8x8x4(acc[mt][0], acc[mt][1], fa, fb);
+      }
     }
-    for (int e = tid; e < r * r; e += WK_NT) {
-      const int i = e / r, cc = e - i * r;
-      sm.Gs[(size_t)k * WK_MAT + i * WK_RH + cc] = __ldg(a.G0 + (size_t)k * r * r + e);
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+      *reinterpret_cast<double2*>(sm.Yp + warp * W_HAD + (8 * mt + g) * 8 + 2 * t) = make_double2(acc[mt][0], acc[mt][1]);
+    __syncthreads();
+    {
+      double v = 0.0;
+      for (int w = 0; w < 8; ++w) v += sm.Yp[w * W_HAD + tid];
+      sm.Cs[k * W_HAD + tid] = v;
+    }
+    __syncthreads();
+  }
+  // initial Grams G_k = U_k^T U_k: the 16 d tiles dealt to the CTAs, gathered through the armed buffer
+  for (int it = c; it < 16 * d; it += P) {
+    const int k = it >> 4, mt = (it >> 2) & 3, nt = it & 3;
+    const int qk = a.q[k], r0 = (qk * warp) / 8, r1 = (qk * (warp + 1)) / 8;
+    const double* Uk = a.U + a.offU[k];
+    double g0 = 0.0, g1 = 0.0;
+    for (int row = r0; row < r1; row += 4) {
+      const int rr = row + t;
+      const bool rv = rr < r1;
+      const int m = 8 * mt + g, n = 8 * nt + g;
+      const double fa = (rv && m < r) ? __ldcg(Uk + (size_t)rr * r + m) : 0.0;
+      const double fb = (rv && n < r) ? __ldcg(Uk + (size_t)rr * r + n) : 0.0;
+      dmma_8x8x4(g0, g1, fa, fb);
+    }
+    *reinterpret_cast<double2*>(sm.Yp + warp * 64 + g * 8 + 2 * t) = make_double2(g0, g1);
+    __syncthreads();
+    if (tid < 64) {
+      double v = 0.0;
+      for (int w = 0; w < 8; ++w) v += sm.Yp[w * 64 + tid];
+      a.g0buf[(size_t)k * MSZ + (8 * mt + (tid >> 3)) * W_RM + 8 * nt + (tid & 7)] = v;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < d * (int)MSZ; e += 8 * WK_NT) {
+    double v[8];
+    const int n = min(8, (d * (int)MSZ - e + WK_NT - 1) / WK_NT);
+    wk_ldn<8>(a.g0buf + e, WK_NT, n, dead, v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int ee = e + q * WK_NT;
+      if (q < n) sm.Gs[(size_t)(ee >> 10) * WK_MAT + ((ee >> 5) & 31) * WK_RH + (ee & 31)] = v[q];
     }
   }
   __syncthreads();
@@ -705,6 +756,8 @@ static int g_w_on = 1;            // debug hook: 0 = never plan the Gram-space k
 static int g_w_dbg = 0;           // debug hook: timing experiments (results may be wrong)
 static double g_w_cond = 1e3;     // debug hook: pivot-ratio bound above which the direct kernel reruns
 
+int als_w_enabled() { return g_w_on; }
+
 int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
   if (!g_w_on || d < 2 || d > TP_MAXD || r < 1 || r > W_RM || R < 1) return TP_EUNSUPPORTED;
   const int P = (R + W_SLAB - 1) / W_SLAB;
@@ -733,9 +786,8 @@ int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
   pl.smem = wk_smem_doubles(d) * sizeof(double);
   if (pl.smem > (size_t)smem_optin) return TP_EUNSUPPORTED;
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
-  pl.ws = align_up(sizeof(double) * (size_t)d * R * R) + align_up(sizeof(double) * (size_t)d * r * R) +
-          align_up(sizeof(double) * (size_t)d * r * r) + align_up(sizeof(double) * 2 * (size_t)d * P * W_PIECE) +
-          align_up(sizeof(double) * 2 * (size_t)d * W_RM * W_RM) + align_up(sizeof(int)) + align_up(sizeof(double)) +
+  pl.ws = align_up(sizeof(double) * (size_t)d * R * R) + align_up(sizeof(double) * 2 * (size_t)d * P * W_PIECE) +
+          align_up(sizeof(double) * 3 * (size_t)d * W_RM * W_RM) + 512 + align_up(sizeof(int)) + align_up(sizeof(double)) +
           pl.ws_inner + 256;
   return TP_OK;
 }
@@ -745,17 +797,16 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
               int prof_cta, const int** redo_out) {
   if (!ws || ws_bytes < plan.ws) return TP_EWORKSPACE;
   WArgs a = plan.a;
-  const int d = a.d, R = a.R, r = a.r, P = a.P;
+  const int d = a.d, R = a.R, P = a.P;
   Carver cv(ws, ws_bytes);
   double* W = cv.take<double>((size_t)d * R * R);
-  double* C0 = cv.take<double>((size_t)d * r * R);
-  double* G0 = cv.take<double>((size_t)d * r * r);
   a.pieces = cv.take<double>(2 * (size_t)d * P * W_PIECE);   // pieces, msum: one memset to the sentinel
   a.msum = cv.take<double>(2 * (size_t)d * W_RM * W_RM);
+  a.g0buf = cv.take<double>((size_t)d * W_RM * W_RM);
   a.redo = cv.take<int>(1);
   double* nsq = cv.take<double>(1);
   double* part = cv.take<double>(plan.ws_inner / sizeof(double));
-  a.W = W; a.C0 = C0; a.G0 = G0;
+  a.W = W;
   a.V = V; a.U = U; a.trace = trace; a.info = info; a.norm_sq = nsq;
   a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = tol; a.stall = stall;
   a.need_resid = (trace != nullptr) || (tol > 0.0) || (stall > -INFINITY);
@@ -776,26 +827,17 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
     const int s = launch_inner(d, a.q, R, V, R, V, 1, nsq, part, st);   // ||V||^2 (cp.py:186-188)
     if (s != TP_OK) return s;
   }
-  // W_k = V_k^T V_k, C0_k = U_k^T V_k, G0_k = U_k^T U_k (batched over the modes when the grids agree)
+  // W_k = V_k^T V_k (batched over the modes when the grids agree)
   const int nbat = plan.uniform_q ? 1 : d;
   for (int b = 0; b < nbat; ++b) {
     const int qk = a.q[b];
     const double* Vk = V + a.offV[b];
-    const double* Uk = U + a.offU[b];
     BGemm gw = bgemm_desc(R, R, qk, Vk, 1, R, Vk, R, 1, W + (size_t)b * R * R, R, 1);
-    BGemm gc = bgemm_desc(r, R, qk, Uk, 1, r, Vk, R, 1, C0 + (size_t)b * r * R, R, 1);
-    BGemm gg = bgemm_desc(r, r, qk, Uk, 1, r, Uk, r, 1, G0 + (size_t)b * r * r, r, 1);
     if (plan.uniform_q) {
-      gw.nb1 = gc.nb1 = gg.nb1 = d;
+      gw.nb1 = d;
       gw.sA1 = gw.sB1 = (long long)qk * R; gw.sC1 = (long long)R * R;
-      gc.sA1 = (long long)qk * r; gc.sB1 = (long long)qk * R; gc.sC1 = (long long)r * R;
-      gg.sA1 = gg.sB1 = (long long)qk * r; gg.sC1 = (long long)r * r;
     }
     e = bgemm_launch(gw, st);
-    if (e != cudaSuccess) return cuda_status(e);
-    e = bgemm_launch(gc, st);
-    if (e != cudaSuccess) return cuda_status(e);
-    e = bgemm_launch(gg, st);
     if (e != cudaSuccess) return cuda_status(e);
   }
   e = cudaFuncSetAttribute(als_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);

@@ -17,8 +17,7 @@ struct WArgs {
   const double* V;
   double* U;
   const double* W;                  // [d][R][R]   W_k = V_k^T V_k
-  const double* C0;                 // [d][r][R]   crosses of the initial guess U_k^T V_k
-  const double* G0;                 // [d][r][r]   Grams of the initial guess
+  double* g0buf;                    // [d][W_RM * W_RM] Grams of the initial guess (tiles dealt to the CTAs)
   double* pieces;                   // [2][d][P][W_PIECE] (sweep parity, mode, producer); all-ones words = not written yet
   double* msum;                     // [2][d][W_RM * W_RM] reduced M of the round (sweep parity, mode)
   int* redo;                        // set to 1: ill-conditioned -> the direct kernel reruns the truncation
@@ -42,6 +41,7 @@ struct WPlan {
 };
 
 int als_w_plan(int d, const int* q, int R, int r, WPlan& pl);
+int als_w_enabled();   // debug hook state (part of the planner's cache key)
 // launches the setup GEMMs and the kernel; *redo_out = device flag the fallback launch reads
 int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double reg, int reg_mode, double tol,
               double stall, double* trace, int* info, void* ws, size_t ws_bytes, cudaStream_t st, long long* prof,

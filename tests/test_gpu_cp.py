@@ -462,8 +462,95 @@ def test_als_rows_kernel(als_variant, comm, ns, reg, qs, R, r):
         L.tp_debug_set_als_rows_split(1)
 
 
-def test_als_rows_is_config1_default():
-    assert cp.als_plan((256,) * 6, 512, 32)["kernel"] == "als_rows"
+def test_als_w_is_config1_default(als_variant):
+    """Config 1 runs the Gram-space kernel (variant 9); with it disabled (debug hook) the
+    cluster-row kernel is the plan again."""
+    import ctypes
+    from paper_1803_10270_b200 import _lib
+    L = _lib.lib()
+    L.tp_debug_set_als_w.argtypes = [ctypes.c_int, ctypes.c_double]
+    assert cp.als_plan((256,) * 6, 512, 32)["kernel"] == "als_w"
+    L.tp_debug_set_als_w(0, 0.0)
+    try:
+        assert cp.als_plan((256,) * 6, 512, 32)["kernel"] == "als_rows"
+    finally:
+        L.tp_debug_set_als_w(1, 0.0)
+
+
+@pytest.mark.parametrize("reg", [None, 1e-10])
+@pytest.mark.parametrize("qs,R,r", [((256,) * 6, 512, 32), ((300, 280), 1000, 32), ((200, 180, 220, 190), 515, 20),
+                                    ((128, 160, 144), 259, 7), ((96,) * 6, 300, 32)])
+def test_als_w_kernel(als_variant, reg, qs, R, r):
+    """Gram-space kernel (variant 9): the sweeps run on the crosses / Grams with W_k = V_k^T V_k,
+    U_k formed after the last sweep.  Config-1 size, ragged modes, R not a multiple of the
+    8-term slab, ranks that are not tile multiples, both regulariser rules, with the residual
+    trace (Gram identity, cp.py:321-326) -- against the oracle."""
+    als_variant(9, 0)
+    assert cp.als_plan(qs, R, r)["kernel"] == "als_w"
+    rng = np.random.default_rng(R + r)
+    V = [rng.standard_normal((q, R)) / np.sqrt(q) for q in qs]
+    init = [v[:, :r].copy() for v in V]
+    S = specs_for(qs)
+    trace, otrace = [], []
+    out = cp.cp_approx_als(cp.CPTensor(S, V), r, cp.ALSApproxConfig(max_sweeps=5, stall=-np.inf, reg=reg),
+                           init=cp.CPTensor(S, init), trace=trace)
+    ref = ocp.als(V, init, 5, lam=reg, trace=otrace)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+    tnorm = float(np.sqrt(ocp.inner_product(V, V).real))
+    np.testing.assert_allclose(trace, otrace, rtol=1e-7, atol=1e-8 * max(1.0, tnorm))
+    # bitwise reproducible (fixed summation orders, data-carried synchronisation)
+    again = cp.cp_approx_als(cp.CPTensor(S, V), r, cp.ALSApproxConfig(max_sweeps=5, stall=-np.inf, reg=reg),
+                             init=cp.CPTensor(S, init))
+    assert torch.equal(out.data, again.data)
+
+
+def test_als_w_stopping_rules(als_variant):
+    """tol / stall decided on the device after each sweep (cp.py:329-332): same sweep count as the
+    oracle and as the cluster-row kernel, same fit."""
+    qs, R, r = (128,) * 4, 256, 8
+    rng = np.random.default_rng(17)
+    V = [rng.standard_normal((q, R)) / np.sqrt(q) for q in qs]
+    init = [v[:, :r].copy() for v in V]
+    S = specs_for(qs)
+    cfg = cp.ALSApproxConfig(max_sweeps=60, stall=1e-7, reg=1e-10)
+    traces = {}
+    outs = {}
+    for variant in (8, 9):
+        als_variant(variant, 0)
+        assert cp.als_plan(qs, R, r)["kernel"] == {8: "als_rows", 9: "als_w"}[variant]
+        traces[variant] = []
+        outs[variant] = cp.cp_approx_als(cp.CPTensor(S, V), r, cfg, init=cp.CPTensor(S, init), trace=traces[variant])
+    assert len(traces[8]) == len(traces[9]) < 60
+    np.testing.assert_allclose(traces[9], traces[8], rtol=1e-9)
+    assert metrics.cp_rel_diff(outs[8].to_numpy(), outs[9].to_numpy()) <= TOL_TRUNC
+
+
+def test_als_w_ill_conditioned_falls_back(als_variant):
+    """The Gram-space form loses ~eps cond(A_j): above the pivot-ratio bound the kernel writes
+    nothing and the cluster-row kernel launched behind it reruns the truncation -- the result is
+    bitwise the cluster-row kernel's own, and matches the oracle within the problem's sensitivity."""
+    qs, R, r = (128,) * 4, 512, 8
+    rng = np.random.default_rng(23)
+    V = [rng.standard_normal((q, R)) / np.sqrt(q) for q in qs]
+    init = [v[:, :r].copy() for v in V]
+    for f in init:
+        f[:, 1] = f[:, 0] * (1.0 + 1e-7)
+    S = specs_for(qs)
+    cfg = cp.ALSApproxConfig(max_sweeps=4, stall=-np.inf, reg=1e-10)
+    als_variant(9, 0)
+    assert cp.als_plan(qs, R, r)["kernel"] == "als_w"
+    tw = []
+    a = cp.cp_approx_als(cp.CPTensor(S, V), r, cfg, init=cp.CPTensor(S, init), trace=tw)
+    als_variant(8, 0)
+    tr = []
+    b = cp.cp_approx_als(cp.CPTensor(S, V), r, cfg, init=cp.CPTensor(S, init), trace=tr)
+    assert torch.equal(a.data, b.data) and tw == tr
+    assert np.all(np.isfinite(a.data.cpu().numpy()))
+    # an all-zero target (zero pivots) takes the same route: zeros, not an error (cp.py:176-177)
+    als_variant(9, 0)
+    Z = cp.CPTensor(S, [np.zeros((q, R)) for q in qs])
+    z = cp.cp_approx_als(Z, r, cfg, init=cp.CPTensor(S, init))
+    assert torch.count_nonzero(z.data).item() == 0
 
 
 @pytest.mark.parametrize("variant,cluster", [(0, 0), (1, 0), (8, 0)])

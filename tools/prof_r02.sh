@@ -1,4 +1,4 @@
-# Round-2 evidence for the bench's dominant kernel (config 1, als_rows): plain bench line,
+# Round-2 evidence for the bench dominant kernel (config 1, als_w): plain bench line,
 # the launch list of the same bench command, one full ncu capture of the ALS kernel.
 set -x
 python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err
