@@ -127,25 +127,26 @@ __device__ double wk_gemm32(const double* A, const double* B, double* out, int r
 }
 
 // A^-1 (A = sm.Am, symmetric positive definite) -> out by the symmetric sweep operator
-// (Gauss-Jordan, one pivot per barrier; thread t owns row t / 8, columns t % 8 + 8 u).  All
-// 256 threads.  *ratio = max diagonal / min pivot (a lower bound of cond A; inf when a pivot
-// is <= 0 or not finite).
+// (Gauss-Jordan, one pivot per named barrier) on the 128 threads of warps 4-7 -- the other warps
+// keep working on the T product: thread t owns row t / 4, columns t % 4 + 4 u.  *ratio = max
+// diagonal / min pivot (a lower bound of cond A; inf when a pivot is <= 0 or not finite);
+// identical in every thread and every CTA.
 __device__ void wk_inverse(const WSmem& sm, int r, double* out, double* ratio) {
-  constexpr int EPT = W_RM / 8;
-  const int t = threadIdx.x, i = t >> 3, c0 = t & 7;
+  constexpr int EPT = W_RM / 4;
+  const int t = threadIdx.x - 128, i = t >> 2, c0 = t & 3;
   double* pub = sm.pub;
   double v[EPT];
 #pragma unroll
   for (int u = 0; u < EPT; ++u) {
-    const int c = c0 + 8 * u;
+    const int c = c0 + 4 * u;
     v[u] = (i < r && c < r) ? sm.Am[i * WK_RH + c] : 0.0;
   }
   double dmax = 0.0, dmin = INFINITY;
   for (int k = 0; k < r; ++k) dmax = fmax(dmax, sm.Am[k * WK_RH + k]);
   if (i == 0)
 #pragma unroll
-    for (int u = 0; u < EPT; ++u) pub[c0 + 8 * u] = v[u];
-  __syncthreads();
+    for (int u = 0; u < EPT; ++u) pub[c0 + 4 * u] = v[u];
+  wk_bar(1, 128);
   for (int k = 0; k < r; ++k) {
     const double* rk = pub + (k & 1) * 36;
     double* rn = pub + ((k + 1) & 1) * 36;
@@ -155,7 +156,7 @@ __device__ void wk_inverse(const WSmem& sm, int r, double* out, double* ratio) {
     const double f = (i < r ? rk[i] : 0.0) * id;
 #pragma unroll
     for (int u = 0; u < EPT; ++u) {
-      const int c = c0 + 8 * u;
+      const int c = c0 + 4 * u;
       const double akc = rk[c];
       double nv = fma(-f, akc, v[u]);
       nv = (c == k) ? f : nv;
@@ -164,16 +165,16 @@ __device__ void wk_inverse(const WSmem& sm, int r, double* out, double* ratio) {
     }
     if (i == k + 1)
 #pragma unroll
-      for (int u = 0; u < EPT; ++u) rn[c0 + 8 * u] = v[u];
-    __syncthreads();
+      for (int u = 0; u < EPT; ++u) rn[c0 + 4 * u] = v[u];
+    wk_bar(1, 128);
   }
 #pragma unroll
   for (int u = 0; u < EPT; ++u) {
-    const int c = c0 + 8 * u;
+    const int c = c0 + 4 * u;
     out[i * WK_RH + c] = (i < r && c < r) ? -v[u] : 0.0;
   }
   *ratio = (dmin > 0.0) ? dmax / dmin : INFINITY;
-  __syncthreads();
+  wk_bar(1, 128);
 }
 
 // deterministic block sum (all threads call; result valid in all threads)
@@ -298,6 +299,18 @@ __device__ __forceinline__ void wk_ldn(const double* src, size_t stride, int n, 
     if (!bad || *dead) break;
     if (clock64() - t0 > WK_SPIN) { *dead = 1; break; }
   }
+}
+
+// one 8 x 8 tile of a (32 x 32) x (32 x 8) product, K = 32 as two interleaved chains of four steps:
+// A rows at a32 (+32 bytes per step), B rows at b32 (+256 bytes per step)
+__device__ __forceinline__ double2 wk_tile_k32(uint32_t a32, uint32_t b32) {
+  double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 8; ks += 2) {
+    dmma_8x8x4(p0, p1, lds64(a32 + 32u * (uint32_t)ks), lds64(b32 + 256u * (uint32_t)ks));
+    dmma_8x8x4(q0, q1, lds64(a32 + 32u * (uint32_t)(ks + 1)), lds64(b32 + 256u * (uint32_t)(ks + 1)));
+  }
+  return make_double2(p0 + q0, p1 + q1);
 }
 
 #define WK_PROFT(i, T)                                                                    \
@@ -547,6 +560,13 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
           em = fmax(fmax(sm.part[0], sm.part[1]), fmax(sm.part[2], sm.part[3]));
           ok = em <= 1e-8;   // (NaN fails); one step squares the error: |I - A X1| <= (r 1e-8)^2
         }
+        // no warm start / rejected: the exact inverse on these four warps, still beside the T product
+        // (flag 1: Newton-Schulz accepted, 2: exact X_j in place, 3: ill-conditioned -> fallback)
+        if (!ok) {
+          double ratio;
+          wk_inverse(sm, r, sm.Xs + (size_t)j * WK_MAT, &ratio);
+          ok = (ratio <= a.cond_max) ? 2 : 3;
+        }
         if (tid == 128) sm.flag[0] = ok;
         WK_PROFT(4, PT);
       } else {
@@ -584,12 +604,8 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
       WK_PROFT(10, 0);
       WK_PROFT(5, PT);
       double* Xj = sm.Xs + (size_t)j * WK_MAT;
-      const int ok = sm.flag[0];
-      if (!ok) {
-        double ratio;
-        wk_inverse(sm, r, Xj, &ratio);
-        if (!(ratio <= a.cond_max)) { abort_ = 1; stop = true; break; }
-      }
+      if (sm.flag[0] == 3) { abort_ = 1; stop = true; break; }
+      const int ok = sm.flag[0] == 1;
       WK_PROFT(6, PT);
       // ---- C_j[:, own] = X_j T_j (cp.py:316-320 in Gram space).  Warm: X_j = X0 Tn is applied
       // as X0 (Tn T_j) on warps 0-3 while warps 4-7 form the matrix X0 Tn for the next sweep
@@ -597,19 +613,13 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
         const int mt = warp;
         const uint32_t tb = smem_u32(ok ? sm.Yp : sm.Ts) + 8u * (uint32_t)(t * 8 + g);
         if (ok) {
-          double z0 = 0.0, z1 = 0.0;
           const uint32_t na = smem_u32(Tcur) + 8u * (uint32_t)((8 * mt + g) * WK_RH + t);
           const uint32_t sb = smem_u32(sm.Ts) + 8u * (uint32_t)(t * 8 + g);
-#pragma unroll
-          for (int ks = 0; ks < 8; ++ks) dmma_8x8x4(z0, z1, lds64(na + 32u * (uint32_t)ks), lds64(sb + 256u * (uint32_t)ks));
-          *reinterpret_cast<double2*>(sm.Yp + (8 * mt + g) * 8 + 2 * t) = make_double2(z0, z1);
+          *reinterpret_cast<double2*>(sm.Yp + (8 * mt + g) * 8 + 2 * t) = wk_tile_k32(na, sb);
           wk_bar(2, 128);
         }
-        double c0 = 0.0, c1 = 0.0;
         const uint32_t xa = smem_u32(Xj) + 8u * (uint32_t)((8 * mt + g) * WK_RH + t);
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) dmma_8x8x4(c0, c1, lds64(xa + 32u * (uint32_t)ks), lds64(tb + 256u * (uint32_t)ks));
-        *reinterpret_cast<double2*>(sm.Cs + j * W_HAD + (8 * mt + g) * 8 + 2 * t) = make_double2(c0, c1);
+        *reinterpret_cast<double2*>(sm.Cs + j * W_HAD + (8 * mt + g) * 8 + 2 * t) = wk_tile_k32(xa, tb);
       } else {
         // warps 4-7: Y = X_j had_j[:, own] (the partial Gram of this CTA is C_j[:, own] Y^T: the
         // producers publish partials of G_j = C_j had_j^T X_j itself, no product after the reduction)
@@ -617,19 +627,13 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
         const double* hj = sm.hads + hb * W_HAD;
         const uint32_t hb32 = smem_u32(ok ? sm.Yp + W_HAD : hj) + 8u * (uint32_t)(t * 8 + g);
         if (ok) {
-          double z0 = 0.0, z1 = 0.0;
           const uint32_t na = smem_u32(Tcur) + 8u * (uint32_t)((8 * mt + g) * WK_RH + t);
           const uint32_t sb = smem_u32(hj) + 8u * (uint32_t)(t * 8 + g);
-#pragma unroll
-          for (int ks = 0; ks < 8; ++ks) dmma_8x8x4(z0, z1, lds64(na + 32u * (uint32_t)ks), lds64(sb + 256u * (uint32_t)ks));
-          *reinterpret_cast<double2*>(sm.Yp + W_HAD + (8 * mt + g) * 8 + 2 * t) = make_double2(z0, z1);
+          *reinterpret_cast<double2*>(sm.Yp + W_HAD + (8 * mt + g) * 8 + 2 * t) = wk_tile_k32(na, sb);
           wk_bar(1, 128);
         }
-        double y0 = 0.0, y1 = 0.0;
         const uint32_t xa = smem_u32(Xj) + 8u * (uint32_t)((8 * mt + g) * WK_RH + t);
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) dmma_8x8x4(y0, y1, lds64(xa + 32u * (uint32_t)ks), lds64(hb32 + 256u * (uint32_t)ks));
-        *reinterpret_cast<double2*>(sm.Yp + 2 * W_HAD + (8 * mt + g) * 8 + 2 * t) = make_double2(y0, y1);
+        *reinterpret_cast<double2*>(sm.Yp + 2 * W_HAD + (8 * mt + g) * 8 + 2 * t) = wk_tile_k32(xa, hb32);
         if (xp >= 0) {
           double* Xp = sm.Xs + (size_t)xp * WK_MAT;
           for (int e = tid - 128; e < WK_MAT; e += 128) Xp[e] = sm.X1[e];
@@ -672,7 +676,9 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
           for (int e = tid; e < W_PIECE; e += WK_NT) po[e] = wk_sentinel();
         }
         hb ^= 1;
-        __syncthreads();
+        // (every shared buffer written before the next join is disjoint from what slower warps
+        // still read here, except the block-sum scratch of the residual rounds)
+        if (a.need_resid) __syncthreads();
       }
       WK_PROFT(7, PT);
       WK_PROFT(11, 0);
