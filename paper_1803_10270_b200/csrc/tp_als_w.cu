@@ -7,7 +7,7 @@
 // only ever uses U_j through its cross C_j (r x R) and Gram G_j (r x r).  With the
 // target Grams W_j = V_j^T V_j (R x R, one batched GEMM before the sweeps) the same
 // update is, in exact arithmetic,
-//     T_j = had_j W_j,   C_j = X_j T_j,   G_j = (C_j had_j^T) X_j,   X_j = A_j^-1,
+//     T_j = had_j W_j,   C_j = X_j T_j,   G_j = sym(C_j had_j^T X_j),   X_j = A_j^-1,
 // i.e. the sweeps never touch the Q dimension: no reduction over the rows of the
 // factor, one all-gather of had_j (r x R) per mode update instead of a reduce-scatter
 // plus an all-gather, and U_j = V_j had_j^T X_j is formed once after the last sweep.
@@ -15,17 +15,24 @@
 // Grid: P = ceil(R / 8) CTAs; CTA c owns target terms (columns of every C_k) [8c, 8c+8).
 // A round (sweep s, mode j), 256 threads:
 //   warps 0-3  T_j[:, own] = had_j W_j[:, own]: the K range (all R terms) split over the
-//              warps; had_j comes piecewise from the producers' global "pieces" (flag per
-//              piece, ld.acquire), fragments straight from L2 into registers, DMMA;
-//   warps 4-7  meanwhile: warp 4 sums this CTA's share of the partial M = C had^T of the
-//              previous update over all producers (fixed order) and publishes it (second
-//              flag); then G_{j-1} = sym(M X_{j-1}), A_j, and the inverse X_j by one
-//              warm-started Newton-Schulz step (previous sweep's X_j; |I - A X| <= 1e-8
-//              required, else the exact sweep-operator inverse on all threads);
-//   all        C_j[:, own] = X_j T_j, the partial M, the own columns of had_{j+1}, written
-//              as this CTA's piece of the next round; release flag.
-// Everything every CTA computes redundantly (G, A, X) is bitwise identical across CTAs
-// (fixed summation orders), so stopping and fallback decisions are uniform.
+//              warps; had_j comes piecewise from the producers' global "pieces", fragments
+//              straight from L2 into registers (16-byte loads, double-buffered chunks of
+//              four pieces), DMMA; then the matrix Newton-Schulz update of the previous
+//              round (X1 = X0 Tn) while they wait at the join;
+//   warps 4-7  meanwhile: sum this CTA's share of the partial Grams C had^T X of the
+//              previous update over all producers (fixed order) and publish it; gather the
+//              sum, G_{j-1} = sym(.), A_j, and the Newton-Schulz residual of the previous
+//              sweep's X_j (Tn = 2I - A_j X_j, accepted when |I - A_j X_j| <= 1e-8; else,
+//              and in the first sweep, the exact sweep-operator inverse on these warps);
+//   all        C_j[:, own] = X_j T_j applied as X0 (Tn T_j), Y = X_j had_j[:, own], the
+//              partial Gram C_j[:, own] Y^T and the own columns of had_{j+1}, written as
+//              this CTA's piece of the next round.
+// Synchronisation is carried by the data: exchange buffers are armed with all-ones words
+// (a NaN no arithmetic produces), readers spin on the words they need, writers re-arm
+// their words one sweep before the next use -- no flags, no fences, one L2 hop per
+// exchange.  Everything every CTA computes redundantly (G, A, X) is bitwise identical
+// across CTAs (fixed summation orders), so stopping and fallback decisions are uniform,
+// and results are bitwise reproducible.
 //
 // Accuracy: C_j = X (had W) carries an error ~ eps cond(A_j) relative to the direct
 // form; the kernel therefore estimates cond(A_j) from the pivots of every exact inverse
@@ -451,7 +458,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
       const double* Tprev = sm.Tn + (size_t)((uround & 1) ^ 1) * WK_MAT;
       if (last_half && !a.need_resid) { stop = true; break; }
       WK_PROFT(0, PT);
-      // ---- A group, part 1: reduce the partial M of update jp, G_jp = sym(M X_jp)
+      // ---- A group, part 1: reduce the partial Grams of update jp, G_jp = sym(sum)
       if (warp >= 4 && !first) {
         const int t2 = tid - 128;
         double* ms = a.msum + (size_t)slot * MSZ;
@@ -641,7 +648,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
       }
       __syncthreads();
       xpend = ok ? j : -1;   // the matrix X_j = X0 Tn is formed during the next round
-      // ---- this CTA's piece of the next round: partial M = C_j had_j^T, own columns of had_{j+1}
+      // ---- this CTA's piece of the next round: partial Gram C_j[:, own] Y^T, own columns of had_{j+1}
       const int jn = (j + 1) % d;
       const int nsweep = sweep + (jn == 0 ? 1 : 0);
       const bool publish = a.need_resid || nsweep < a.sweeps;

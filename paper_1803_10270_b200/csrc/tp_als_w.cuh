@@ -7,7 +7,7 @@ namespace tp {
 constexpr int W_RM = 32;                          // padded fitted rank
 constexpr int W_SLAB = 8;                         // target terms (columns of C_k) per CTA
 constexpr int W_HAD = W_RM * W_SLAB;              // doubles of one had / C slab
-constexpr int W_PIECE = W_HAD + W_RM * W_RM + 8;  // had slab | partial M | overlap partial (+ pad)
+constexpr int W_PIECE = W_HAD + W_RM * W_RM + 8;  // had slab | partial Gram | overlap partial (+ pad)
 
 struct WArgs {
   int d, R, r, sweeps, P;           // P CTAs; CTA c owns target terms [8 c, 8 c + 8)
@@ -19,7 +19,7 @@ struct WArgs {
   const double* W;                  // [d][R][R]   W_k = V_k^T V_k
   double* g0buf;                    // [d][W_RM * W_RM] Grams of the initial guess (tiles dealt to the CTAs)
   double* pieces;                   // [2][d][P][W_PIECE] (sweep parity, mode, producer); all-ones words = not written yet
-  double* msum;                     // [2][d][W_RM * W_RM] reduced M of the round (sweep parity, mode)
+  double* msum;                     // [2][d][W_RM * W_RM] summed partial Grams of the round (sweep parity, mode)
   int* redo;                        // set to 1: ill-conditioned -> the direct kernel reruns the truncation
   const double* norm_sq;
   double* trace;
