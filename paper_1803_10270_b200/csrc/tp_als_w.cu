@@ -208,7 +208,8 @@ __device__ __forceinline__ double wk_ldv(const double* p) {
   asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
   return v;
 }
-__device__ __forceinline__ bool wk_unset(double v) { return __double_as_longlong(v) == -1LL; }
+// (the high word alone identifies the sentinel: no stored double has an all-ones high word)
+__device__ __forceinline__ bool wk_unset(double v) { return __double2hiint(v) == -1; }
 __device__ __forceinline__ double wk_sentinel() { return __longlong_as_double(-1LL); }
 constexpr long long WK_SPIN = 4000000000LL;   // ~2 s: a missing peer -> info bit 4 instead of a hang
 
