@@ -504,6 +504,58 @@ def test_als_w_kernel(als_variant, reg, qs, R, r):
     assert torch.equal(out.data, again.data)
 
 
+@pytest.mark.parametrize("qs,R,r,sweeps", [((160, 144), 512, 32, 4),            # two modes (slot reuse every round)
+                                           ((72,) * 7, 264, 12, 3),           # seven modes (shared memory near the limit)
+                                           ((80, 96, 72), 257, 1, 3),         # rank 1, last slab one column wide
+                                           ((128, 96, 112), 384, 9, 1),       # one sweep: exact inverses only
+                                           ((128, 96, 112), 384, 31, 2),      # r = 31 (padded to 32)
+                                           ((300, 320, 310), 1184, 16, 2)])   # one CTA per SM (148 slabs)
+def test_als_w_edge_shapes(als_variant, qs, R, r, sweeps):
+    """Corner shapes of the Gram-space kernel against the oracle, with the residual trace."""
+    als_variant(9, 0)
+    assert cp.als_plan(qs, R, r)["kernel"] == "als_w"
+    rng = np.random.default_rng(7 * R + r)
+    V = [rng.standard_normal((q, R)) / np.sqrt(q) for q in qs]
+    init = [v[:, :r].copy() for v in V]
+    S = specs_for(qs)
+    trace, otrace = [], []
+    out = cp.cp_approx_als(cp.CPTensor(S, V), r, cp.ALSApproxConfig(max_sweeps=sweeps, stall=-np.inf, reg=1e-10),
+                           init=cp.CPTensor(S, init), trace=trace)
+    ref = ocp.als(V, init, sweeps, lam=1e-10, trace=otrace)
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+    tnorm = float(np.sqrt(ocp.inner_product(V, V).real))
+    np.testing.assert_allclose(trace, otrace, rtol=1e-7, atol=1e-8 * max(1.0, tnorm))
+    # without the trace (no residual rounds, no trailing barriers): the same fit bitwise
+    out2 = cp.cp_approx_als(cp.CPTensor(S, V), r, cp.ALSApproxConfig(max_sweeps=sweeps, stall=-np.inf, reg=1e-10),
+                            init=cp.CPTensor(S, init))
+    assert torch.equal(out.data, out2.data)
+
+
+def test_als_w_unsupported_shapes_fall_through(als_variant):
+    """Shapes outside the Gram-space kernel's plan (eight modes: shared memory; R > 4 min Q: more work
+    than the direct form; fewer than 32 slabs) keep their direct kernels in the automatic plan."""
+    assert cp.als_plan((128,) * 8, 512, 32)["kernel"] != "als_w"
+    assert cp.als_plan((64,) * 6, 588, 12)["kernel"] != "als_w"
+    assert cp.als_plan((256,) * 4, 200, 32)["kernel"] != "als_w"
+
+
+def test_als_w_tol_stop(als_variant):
+    """tol rule (cp.py:329): stop after the first sweep whose residual is <= tol ||V||."""
+    als_variant(9, 0)
+    qs, R, r = (128,) * 4, 256, 16
+    rng = np.random.default_rng(41)
+    V = [rng.standard_normal((q, R)) / np.sqrt(q) for q in qs]
+    init = [v[:, :r].copy() for v in V]
+    S = specs_for(qs)
+    trace, otrace = [], []
+    out = cp.cp_approx_als(cp.CPTensor(S, V), r, cp.ALSApproxConfig(max_sweeps=20, tol=0.999, stall=-np.inf, reg=1e-10),
+                           init=cp.CPTensor(S, init), trace=trace)
+    ref = ocp.als(V, init, len(trace), lam=1e-10, trace=otrace)
+    tnorm = float(np.sqrt(ocp.inner_product(V, V).real))
+    assert 1 <= len(trace) < 20 and trace[-1] <= 0.999 * tnorm and all(t > 0.999 * tnorm for t in trace[:-1])
+    assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+
+
 def test_als_w_stopping_rules(als_variant):
     """tol / stall decided on the device after each sweep (cp.py:329-332): same sweep count as the
     oracle and as the cluster-row kernel, same fit."""
