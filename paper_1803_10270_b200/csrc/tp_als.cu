@@ -2713,7 +2713,7 @@ static int plan_als_uncached(int d, const int* q, int R, int r, int grid, AlsPla
       // well-conditioned large truncations: the sweeps in Gram space (no reduction over the factor
       // rows), the cluster-row kernel launched behind it as the conditioning fallback
       if ((g_variant == 0 || g_variant == 9) && als_w_plan(d, q, R, r, cp.w) == TP_OK) {
-        cp.variant = 9; cp.P = cp.w.a.P; cp.Pr = cp.w.a.P; cp.smem = cp.w.smem;
+        cp.variant = 9; cp.P = cp.w.a.P << cp.w.a.pair; cp.Pr = cp.w.a.P; cp.smem = cp.w.smem;
         cp.ws_total = align_up(cp.w.ws) + cp.rows.ws;
       } else if (g_variant == 9) {
         return TP_EUNSUPPORTED;
@@ -2792,7 +2792,7 @@ int tp_cp_als_plan(int d, const int* q, int R, int r, int grid, int* out) {
   }
   if (st != TP_OK) return st;
   out[0] = pl.variant; out[1] = pl.P;
-  out[2] = (pl.variant == 1 || pl.variant == 3) ? pl.a.Pq : (pl.variant == 8 ? pl.rows.a.S : 1);
+  out[2] = (pl.variant == 1 || pl.variant == 3) ? pl.a.Pq : (pl.variant == 8 ? pl.rows.a.S : (pl.variant == 9 ? 1 + pl.w.a.pair : 1));
   out[3] = (int)pl.smem;
   return TP_OK;
 }

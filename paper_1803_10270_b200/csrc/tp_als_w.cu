@@ -56,13 +56,14 @@ constexpr int WK_RH = 36;                 // row stride of the r x r matrices (=
 constexpr int WK_MAT = W_RM * WK_RH;
 
 struct WSmem {
-  double *Cs, *hads, *Tp, *Ts, *Gs, *Xs, *Am, *Tn, *X1, *Ms, *Yp, *Ys, *part, *pub, *red;
+  double *Cs, *hads, *Tp, *Ts, *Tl, *Tx, *Gs, *Xs, *Am, *Tn, *X1, *Ms, *Yp, *Ys, *part, *pub, *red;
+  uint64_t* bar;   // [2] pair exchange (round parity)
   int* flag;   // [0]: Newton-Schulz accepted, [1]: a poll timed out
 };
 
 __host__ __device__ inline size_t wk_smem_doubles(int d) {
   return (size_t)d * W_HAD + 2 * W_HAD + 4 * W_HAD + W_HAD + 2 * (size_t)d * WK_MAT + 5 * (size_t)WK_MAT + 8 * W_HAD +
-         8 * WK_RH + 8 + 80 + WK_NT + 8;
+         8 * WK_RH + 8 + 80 + WK_NT + 8 + 3 * W_HAD + 4;
 }
 
 __device__ inline WSmem wk_carve(double* b, int d) {
@@ -71,6 +72,8 @@ __device__ inline WSmem wk_carve(double* b, int d) {
   s.hads = b; b += 2 * W_HAD;
   s.Tp = b; b += 4 * W_HAD;
   s.Ts = b; b += W_HAD;
+  s.Tl = b; b += W_HAD;
+  s.Tx = b; b += 2 * W_HAD;
   s.Gs = b; b += (size_t)d * WK_MAT;
   s.Xs = b; b += (size_t)d * WK_MAT;
   s.Am = b; b += WK_MAT;
@@ -82,7 +85,8 @@ __device__ inline WSmem wk_carve(double* b, int d) {
   s.part = b; b += 8;
   s.pub = b; b += 80;
   s.red = b; b += WK_NT;
-  s.flag = reinterpret_cast<int*>(b);
+  s.flag = reinterpret_cast<int*>(b); b += 2;
+  s.bar = reinterpret_cast<uint64_t*>(b);
   return s;
 }
 
@@ -196,6 +200,16 @@ __device__ inline double wk_block_sum(double v, double* red) {
   const double out = red[0];
   __syncthreads();
   return out;
+}
+
+// remote store into the peer CTA of the pair, completing bytes on the peer's mbarrier
+__device__ __forceinline__ void wk_st_async_v2(uint32_t addr, double x, double y, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
+               "d"(x), "d"(y), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void wk_cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 // ---- data-carried synchronisation ------------------------------------------------------
@@ -351,7 +365,9 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
   const int d = a.d, R = a.R, r = a.r, P = a.P;
   const WSmem sm = wk_carve(smem, d);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int c = blockIdx.x, col0 = W_SLAB * c;
+  // pair mode: the two CTAs of a cluster share a column slab and split the K range of its T product
+  const int pr = a.pair, cid = blockIdx.x, NC = gridDim.x;
+  const int c = cid >> pr, h = cid & pr, col0 = W_SLAB * c;
   const int wv = min(W_SLAB, R - col0);
   volatile int* dead = sm.flag + 1;
   long long prof_t = clock64(), prof_acc[16] = {};
@@ -390,7 +406,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
     __syncthreads();
   }
   // initial Grams G_k = U_k^T U_k: the 16 d tiles dealt to the CTAs, gathered through the armed buffer
-  for (int it = c; it < 16 * d; it += P) {
+  for (int it = cid; it < 16 * d; it += NC) {
     const int k = it >> 4, mt = (it >> 2) & 3, nt = it & 3;
     const int qk = a.q[k], r0 = (qk * warp) / 8, r1 = (qk * (warp + 1)) / 8;
     const double* Uk = a.U + a.offU[k];
@@ -427,7 +443,16 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
     double v = 1.0;
     for (int k = 1; k < d; ++k) v *= sm.Cs[k * W_HAD + tid];
     sm.hads[tid] = v;
-    a.pieces[((size_t)0 * P + c) * W_PIECE + tid] = v;
+    if (h == 0) a.pieces[((size_t)0 * P + c) * W_PIECE + tid] = v;
+  }
+  if (pr) {
+    if (tid == 0) {
+      mbar_init(sm.bar, 1);
+      mbar_init(sm.bar + 1, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    wk_cluster_barrier();   // the peer is running and its barriers exist before any remote store
   }
   __syncthreads();
 
@@ -436,8 +461,9 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
   double prev = INFINITY;
   int done = 0, abort_ = 0, hb = 0, uround = 0, xpend = -1;   // hb: which hads buffer holds had_j of the current round
   // K range of the GEMM warps (pieces) and this CTA's share of the M entries
-  const int npw = (P + 3) / 4;
-  const int e0 = (int)((MSZ * c) / P), ne = (int)((MSZ * (c + 1)) / P) - e0;
+  const int kb0 = pr ? h * ((P + 1) / 2) : 0, kb1 = pr ? min(P, kb0 + (P + 1) / 2) : P;   // this CTA's pieces
+  const int npw = (kb1 - kb0 + 3) / 4;
+  const int e0 = (int)((MSZ * cid) / NC), ne = (int)((MSZ * (cid + 1)) / NC) - e0;
   int nev = 1;
   while (nev < ne) nev <<= 1;
   const int ngr = 128 / nev;                 // producer groups of the Gram reduction (A group, 128 threads)
@@ -526,7 +552,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
         }
         const double self = wk_block_sum(sv, sm.red);
         const double resid = sqrt(fmax(norm_sq - 2.0 * ov + self, 0.0));
-        if (c == 0 && tid == 0 && a.trace) a.trace[sweep - 1] = resid;
+        if (cid == 0 && tid == 0 && a.trace) a.trace[sweep - 1] = resid;
         if (resid <= a.tol * t_norm) stop = true;
         if (prev - resid < a.stall * fmax(t_norm, 1.0)) stop = true;
         prev = resid;
@@ -579,7 +605,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
         WK_PROFT(4, PT);
       } else {
         // ---- GEMM group: T_j[:, own] = had_j W_j[:, own], K split over the four warps
-        const int p0 = warp * npw, p1 = min(P, p0 + npw);
+        const int p0 = kb0 + warp * npw, p1 = min(kb1, p0 + npw);
         const int nch = (max(p1 - p0, 0) + 3) / 4;
         const bool wvalid = g < wv;
         const double* wrow = a.W + (size_t)j * R * R + (size_t)(col0 + (wvalid ? g : 0)) * R;
@@ -603,8 +629,22 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
         for (int mt = 0; mt < 4; ++mt)
           *reinterpret_cast<double2*>(tp + (8 * mt + g) * 8 + 2 * t) = make_double2(acc[mt][0], acc[mt][1]);
         wk_bar(2, 128);
+        double* tsum = pr ? sm.Tl : sm.Ts;
         for (int e = tid; e < W_HAD; e += 128)
-          sm.Ts[e] = (sm.Tp[e] + sm.Tp[W_HAD + e]) + (sm.Tp[2 * W_HAD + e] + sm.Tp[3 * W_HAD + e]);
+          tsum[e] = (sm.Tp[e] + sm.Tp[W_HAD + e]) + (sm.Tp[2 * W_HAD + e] + sm.Tp[3 * W_HAD + e]);
+        if (pr) {
+          // the other half of the K range comes from the peer: each CTA pushes its partial into the
+          // peer's buffer (st.async onto the peer's mbarrier) and adds in rank order
+          const int par = uround & 1;
+          wk_bar(2, 128);
+          if (tid == 0) mbar_arrive_expect_tx(sm.bar + par, (uint32_t)(W_HAD * sizeof(double)));
+          const uint32_t dst = mapa_u32(smem_u32(sm.Tx + par * W_HAD), (uint32_t)(h ^ 1));
+          const uint32_t rbar = mapa_u32(smem_u32(sm.bar + par), (uint32_t)(h ^ 1));
+          wk_st_async_v2(dst + 16u * (uint32_t)tid, sm.Tl[2 * tid], sm.Tl[2 * tid + 1], rbar);
+          mbar_wait(sm.bar + par, (uint32_t)((uround >> 1) & 1));
+          const double* tx = sm.Tx + par * W_HAD;
+          for (int e = tid; e < W_HAD; e += 128) sm.Ts[e] = h == 0 ? sm.Tl[e] + tx[e] : tx[e] + sm.Tl[e];
+        }
         if (xp >= 0) wk_gemm32(sm.Xs + (size_t)xp * WK_MAT, Tprev, sm.X1, r, 1, 0);   // X1 = X0 (2I - A X0)
       }
       WK_PROFT(9, 0);
@@ -661,7 +701,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
           for (int k = 0; k < d; ++k)
             if (k != jn) v *= sm.Cs[k * W_HAD + tid];
           sm.hads[(hb ^ 1) * W_HAD + tid] = v;
-          pn[tid] = v;
+          if (h == 0) pn[tid] = v;
         }
         for (int tile = warp; tile < 16; tile += 8) {
           const int mt = tile >> 2, nt = tile & 3;
@@ -669,17 +709,17 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks)
             dmma_8x8x4(m0, m1, sm.Cs[j * W_HAD + (8 * mt + g) * 8 + 4 * ks + t], yj[(8 * nt + g) * 8 + 4 * ks + t]);
-          *reinterpret_cast<double2*>(pn + W_HAD + (8 * mt + g) * W_RM + 8 * nt + 2 * t) = make_double2(m0, m1);
+          if (h == 0) *reinterpret_cast<double2*>(pn + W_HAD + (8 * mt + g) * W_RM + 8 * nt + 2 * t) = make_double2(m0, m1);
         }
         if (a.need_resid && j == d - 1) {
           double v = 1.0;
           for (int k = 0; k < d; ++k) v *= sm.Cs[k * W_HAD + tid];
           const double ov = wk_block_sum(v, sm.red);
-          if (tid == 0) pn[W_HAD + MSZ] = ov;
+          if (tid == 0 && h == 0) pn[W_HAD + MSZ] = ov;
         }
         // re-arm this CTA's piece of mode j, previous sweep (every reader finished it a sweep ago;
         // its next use is the sweep after this one)
-        if (sweep >= 1) {
+        if (sweep >= 1 && h == 0) {
           double* po = a.pieces + ((size_t)(((sweep - 1) & 1) * d + j) * P + c) * W_PIECE;
           for (int e = tid; e < W_PIECE; e += WK_NT) po[e] = wk_sentinel();
         }
@@ -707,7 +747,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
     }
     const int ls = done - 1;
     int nf = 0;
-    for (int it = c; it < a.tile0[d]; it += P) {
+    for (int it = cid; it < a.tile0[d]; it += NC) {
       int j = 0;
       while (it >= a.tile0[j + 1]) ++j;
       const int row0 = 8 * (it - a.tile0[j]), qj = a.q[j];
@@ -757,20 +797,25 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
   }
   if (tid == 0) {
     if (*dead) atomicOr(a.info, 4);
-    if (c == 0) {
+    if (cid == 0) {
       if (abort_) *a.redo = 1;
       else a.info[1] = done;
     }
   }
   if (a.prof && (int)blockIdx.x == a.prof_cta && (tid == PT || tid == 0))
     for (int q = (tid == 0 ? 8 : 0); q < (tid == 0 ? 16 : 8); ++q) a.prof[q] += prof_acc[q];
+  if (pr) {
+    __syncthreads();
+    wk_cluster_barrier();   // no CTA exits while its peer may still store into its shared memory
+  }
 }
 
+static int g_w_pair = 1;          // debug hook: 0 = one CTA per column slab (no K split over a CTA pair)
 static int g_w_on = 1;            // debug hook: 0 = never plan the Gram-space kernel
 static int g_w_dbg = 0;           // debug hook: timing experiments (results may be wrong)
 static double g_w_cond = 1e3;     // debug hook: pivot-ratio bound above which the direct kernel reruns
 
-int als_w_enabled() { return g_w_on; }
+int als_w_enabled() { return g_w_on + 2 * g_w_pair; }
 
 int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
   if (!g_w_on || d < 2 || d > TP_MAXD || r < 1 || r > W_RM || R < 1) return TP_EUNSUPPORTED;
@@ -789,6 +834,7 @@ int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
   WArgs& a = pl.a;
   memset(&a, 0, sizeof(a));
   a.d = d; a.R = R; a.r = r; a.P = P;
+  a.pair = (g_w_pair && 2 * P <= nsm) ? 1 : 0;
   long long ov = 0, ou = 0;
   int tiles = 0;
   for (int k = 0; k < d; ++k) {
@@ -799,6 +845,19 @@ int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
   pl.uniform_q = qmin == qmax;
   pl.smem = wk_smem_doubles(d) * sizeof(double);
   if (pl.smem > (size_t)smem_optin) return TP_EUNSUPPORTED;
+  if (a.pair) {   // P co-resident 2-CTA clusters?
+    cudaFuncSetAttribute(als_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(2 * P); cfg.blockDim = dim3(WK_NT); cfg.dynamicSmemBytes = pl.smem;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int nclu = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclu, (const void*)als_w, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
+    if (nclu < P) a.pair = 0;
+  }
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
   pl.ws = align_up(sizeof(double) * (size_t)d * R * R) + align_up(sizeof(double) * 2 * (size_t)d * P * W_PIECE) +
           align_up(sizeof(double) * 3 * (size_t)d * W_RM * W_RM) + 512 + align_up(sizeof(int)) + align_up(sizeof(double)) +
@@ -857,13 +916,15 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
   e = cudaFuncSetAttribute(als_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
   if (e != cudaSuccess) return cuda_status(e);
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.gridDim = dim3(P); cfg.blockDim = dim3(WK_NT); cfg.dynamicSmemBytes = plan.smem; cfg.stream = st;
-  cfg.attrs = at; cfg.numAttrs = 1;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = a.pair ? 2 : 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.gridDim = dim3(P << a.pair); cfg.blockDim = dim3(WK_NT); cfg.dynamicSmemBytes = plan.smem; cfg.stream = st;
+  cfg.attrs = at; cfg.numAttrs = 2;
   static const bool noncoop = getenv("TP_ALS_NONCOOP") && getenv("TP_ALS_NONCOOP")[0] == '1';
-  if (noncoop) cfg.numAttrs = 0;
+  if (noncoop) cfg.numAttrs = 1;
   void* args[] = {&a};
   return cuda_status(cudaLaunchKernelExC(&cfg, (const void*)als_w, args));
 }
@@ -871,6 +932,7 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
 }  // namespace tp
 
 extern "C" void tp_debug_set_als_w_dbg(int m) { tp::g_w_dbg = m; }
+extern "C" void tp_debug_set_als_w_pair(int on) { tp::g_w_pair = on; }
 extern "C" void tp_debug_set_als_w(int on, double cond_max) {
   tp::g_w_on = on;
   if (cond_max > 0.0) tp::g_w_cond = cond_max;

@@ -10,7 +10,8 @@ constexpr int W_HAD = W_RM * W_SLAB;              // doubles of one had / C slab
 constexpr int W_PIECE = W_HAD + W_RM * W_RM + 8;  // had slab | partial Gram | overlap partial (+ pad)
 
 struct WArgs {
-  int d, R, r, sweeps, P;           // P CTAs; CTA c owns target terms [8 c, 8 c + 8)
+  int d, R, r, sweeps, P;           // P column slabs: slab c = target terms [8 c, 8 c + 8)
+  int pair;                         // 1: two CTAs (one cluster) per slab, each half of the K range of its T product
   int q[TP_MAXD];
   long long offV[TP_MAXD], offU[TP_MAXD];
   int tile0[TP_MAXD + 1];           // first 8-row tile of mode k in the final-phase item list

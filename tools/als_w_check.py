@@ -64,6 +64,13 @@ print(f"cfg1 traced 6 sweeps ({k}): rel {metrics.cp_rel_diff(ref6, out.to_numpy(
       f"{np.max(np.abs(np.array(tr) - np.array(otr))):.3e} of {otr[-1]:.3e}", flush=True)
 for variant in (8, 9):
     print(f"cfg1 variant {variant}: {timeit(V, init, 20, 1e-10, variant):.1f} us per truncation", flush=True)
+L.tp_debug_set_als_w_pair.argtypes = [ctypes.c_int]
+L.tp_debug_set_als_w_pair(0)
+out, k = run(V, init, 20, 1e-10, 9)
+print(f"cfg1 variant 9 without CTA pairs ({cp.als_plan([v.shape[0] for v in V], 512, 32)}): rel vs oracle "
+      f"{metrics.cp_rel_diff(ref, out.to_numpy()):.3e}, {timeit(V, init, 20, 1e-10, 9):.1f} us per truncation", flush=True)
+L.tp_debug_set_als_w_pair(1)
+print(f"plan with pairs: {cp.als_plan([v.shape[0] for v in V], 512, 32)}", flush=True)
 L.tp_debug_set_als_profile.argtypes = [ctypes.c_void_p]
 names = ["top", "reduce M (wait + sum)", "reduced M wait + load", "G step", "A + Newton-Schulz residual", "join wait",
          "exact inverse", "C / X1 / M / publish", "gemm (wait+load+mma)", "T reduce", "join wait (gemm)", "(gemm) rest of round"]
