@@ -531,6 +531,35 @@ def test_als_w_edge_shapes(als_variant, qs, R, r, sweeps):
     assert torch.equal(out.data, out2.data)
 
 
+@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("qs,R,r", [((256,) * 6, 512, 32), ((200, 180, 220, 190), 515, 20), ((128, 160, 144), 259, 7)])
+def test_als_w_cta_pairs(als_variant, pair, qs, R, r):
+    """The K range of a column slab's T product split over a CTA pair (2-CTA clusters, partials exchanged
+    through distributed shared memory) or kept in one CTA: both against the oracle, odd slab counts included."""
+    import ctypes
+    from paper_1803_10270_b200 import _lib
+    L = _lib.lib()
+    L.tp_debug_set_als_w_pair.argtypes = [ctypes.c_int]
+    als_variant(9, 0)
+    L.tp_debug_set_als_w_pair(pair)
+    try:
+        plan = cp.als_plan(qs, R, r)
+        assert plan["kernel"] == "als_w" and plan["cluster"] == 1 + pair and plan["ctas"] == ((R + 7) // 8) * (1 + pair)
+        rng = np.random.default_rng(R + r + pair)
+        V = [rng.standard_normal((q, R)) / np.sqrt(q) for q in qs]
+        init = [v[:, :r].copy() for v in V]
+        S = specs_for(qs)
+        trace, otrace = [], []
+        out = cp.cp_approx_als(cp.CPTensor(S, V), r, cp.ALSApproxConfig(max_sweeps=4, stall=-np.inf, reg=1e-10),
+                               init=cp.CPTensor(S, init), trace=trace)
+        ref = ocp.als(V, init, 4, lam=1e-10, trace=otrace)
+        assert metrics.cp_rel_diff(ref, out.to_numpy()) <= TOL_TRUNC
+        tnorm = float(np.sqrt(ocp.inner_product(V, V).real))
+        np.testing.assert_allclose(trace, otrace, rtol=1e-7, atol=1e-8 * max(1.0, tnorm))
+    finally:
+        L.tp_debug_set_als_w_pair(1)
+
+
 def test_als_w_unsupported_shapes_fall_through(als_variant):
     """Shapes outside the Gram-space kernel's plan (eight modes: shared memory; R > 4 min Q: more work
     than the direct form; fewer than 32 slabs) keep their direct kernels in the automatic plan."""
