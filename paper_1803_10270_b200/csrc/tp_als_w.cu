@@ -611,16 +611,16 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
         const double* wrow = a.W + (size_t)j * R * R + (size_t)(col0 + (wvalid ? g : 0)) * R;
         double acc[4][2] = {};
         double fa0[32], fb0[8], fa1[32], fb1[8];
-        if (!(a.dbg & 4)) wk_wait_pieces(pc, p0, p1, dead);
-        if (nch > 0 && !(a.dbg & 4)) wk_issue_chunk(pc, wrow, wvalid, R, p0, p1, fa0, fb0);
-        for (int ch = 0; ch < nch && !(a.dbg & 4); ch += 2) {
+        wk_wait_pieces(pc, p0, p1, dead);
+        if (nch > 0) wk_issue_chunk(pc, wrow, wvalid, R, p0, p1, fa0, fb0);
+        for (int ch = 0; ch < nch; ch += 2) {
           if (ch + 1 < nch) wk_issue_chunk(pc, wrow, wvalid, R, p0 + 4 * (ch + 1), p1, fa1, fb1);
           wk_verify_chunk(pc, p0 + 4 * ch, p1, dead, fa0);
-          if (!(a.dbg & 2)) wk_mma_chunk(fa0, fb0, acc);
+          wk_mma_chunk(fa0, fb0, acc);
           if (ch + 2 < nch) wk_issue_chunk(pc, wrow, wvalid, R, p0 + 4 * (ch + 2), p1, fa0, fb0);
           if (ch + 1 < nch) {
             wk_verify_chunk(pc, p0 + 4 * (ch + 1), p1, dead, fa1);
-            if (!(a.dbg & 2)) wk_mma_chunk(fa1, fb1, acc);
+            wk_mma_chunk(fa1, fb1, acc);
           }
         }
         WK_PROFT(8, 0);
@@ -812,7 +812,6 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
 
 static int g_w_pair = 1;          // debug hook: 0 = one CTA per column slab (no K split over a CTA pair)
 static int g_w_on = 1;            // debug hook: 0 = never plan the Gram-space kernel
-static int g_w_dbg = 0;           // debug hook: timing experiments (results may be wrong)
 static double g_w_cond = 1e3;     // debug hook: pivot-ratio bound above which the direct kernel reruns
 
 int als_w_enabled() { return g_w_on + 2 * g_w_pair; }
@@ -884,7 +883,6 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
   a.sweeps = sweeps; a.reg = reg; a.reg_mode = reg_mode; a.tol = tol; a.stall = stall;
   a.need_resid = (trace != nullptr) || (tol > 0.0) || (stall > -INFINITY);
   a.cond_max = g_w_cond;
-  a.dbg = g_w_dbg;
   a.prof = prof; a.prof_cta = prof_cta;
   *redo_out = a.redo;
   cudaError_t e = cudaMemsetAsync(info, 0, 2 * sizeof(int), st);
@@ -931,7 +929,6 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
 
 }  // namespace tp
 
-extern "C" void tp_debug_set_als_w_dbg(int m) { tp::g_w_dbg = m; }
 extern "C" void tp_debug_set_als_w_pair(int on) { tp::g_w_pair = on; }
 extern "C" void tp_debug_set_als_w(int on, double cond_max) {
   tp::g_w_on = on;

@@ -30,7 +30,6 @@ struct WArgs {
   double tol, stall;
   int need_resid;
   double cond_max;
-  int dbg;
   long long* prof;
   int prof_cta;
 };

@@ -74,21 +74,19 @@ print(f"plan with pairs: {cp.als_plan([v.shape[0] for v in V], 512, 32)}", flush
 L.tp_debug_set_als_profile.argtypes = [ctypes.c_void_p]
 names = ["top", "reduce M (wait + sum)", "reduced M wait + load", "G step", "A + Newton-Schulz residual", "join wait",
          "exact inverse", "C / X1 / M / publish", "gemm (wait+load+mma)", "T reduce", "join wait (gemm)", "(gemm) rest of round"]
-for dbg in [int(x) for x in os.environ.get("W_DBG", "0").split(",")]:
-    L.tp_debug_set_als_w_dbg(dbg)
+if True:
     prof = torch.zeros(48, dtype=torch.int64, device="cuda")
     L.tp_debug_set_als_profile(prof.data_ptr())
     run(V, init, 20, 1e-10, 9)
     L.tp_debug_set_als_profile(None)
     p = prof.cpu().numpy() / 120.0
-    print(f"dbg {dbg}: cycles per mode update (CTA 0; A group thread 128 | GEMM group thread 0), {timeit(V, init, 20, 1e-10, 9):.1f} us per truncation:")
+    print(f"cycles per mode update (CTA 0; A group thread 128 | GEMM group thread 0), {timeit(V, init, 20, 1e-10, 9):.1f} us per truncation:")
     for n_, v in zip(names, p):
         print(f"  {n_:28s} {v:9.0f}")
     ab = prof.cpu().numpy()[16:48]
     t0 = ab[ab > 0].min()
     ev = sorted((int(v - t0), f"r{61 + i // 16} {names[i % 16] if i % 16 < len(names) else i % 16}") for i, v in enumerate(ab) if v > 0)
     print("  timeline (rounds 61-62): " + " | ".join(f"{t}: {n}" for t, n in ev))
-L.tp_debug_set_als_w_dbg(0)
 if len(sys.argv) > 1:
     sys.exit(0)
 rng = np.random.default_rng(3)
