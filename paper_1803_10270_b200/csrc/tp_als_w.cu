@@ -337,7 +337,7 @@ __device__ __forceinline__ double2 wk_tile_k32(uint32_t a32, uint32_t b32) {
 
 #define WK_PROFT(i, T)                                                                    \
   do {                                                                                    \
-    if (a.prof && (int)blockIdx.x == a.prof_cta && threadIdx.x == (T)) {                  \
+    if (PROF && a.prof && (int)blockIdx.x == a.prof_cta && threadIdx.x == (T)) {          \
       const long long t_ = clock64();                                                     \
       prof_acc[i] += t_ - prof_t;                                                         \
       prof_t = t_;                                                                        \
@@ -360,6 +360,9 @@ __device__ __forceinline__ void wk_gprod8(const WSmem& sm, int d, int skip, int 
   }
 }
 
+// PROF: clock64 phase probes compiled in (debug hook; the probe code alone shifts the kernel's timing by
+// several per cent through its size, so the product instantiation carries none)
+template <bool PROF>
 __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int d = a.d, R = a.R, r = a.r, P = a.P;
@@ -802,7 +805,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
       else a.info[1] = done;
     }
   }
-  if (a.prof && (int)blockIdx.x == a.prof_cta && (tid == PT || tid == 0))
+  if (PROF && a.prof && (int)blockIdx.x == a.prof_cta && (tid == PT || tid == 0))
     for (int q = (tid == 0 ? 8 : 0); q < (tid == 0 ? 16 : 8); ++q) a.prof[q] += prof_acc[q];
   if (pr) {
     __syncthreads();
@@ -845,7 +848,7 @@ int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
   pl.smem = wk_smem_doubles(d) * sizeof(double);
   if (pl.smem > (size_t)smem_optin) return TP_EUNSUPPORTED;
   if (a.pair) {   // P co-resident 2-CTA clusters?
-    cudaFuncSetAttribute(als_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    cudaFuncSetAttribute(als_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     cudaGetLastError();
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
@@ -854,7 +857,7 @@ int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
     cfg.gridDim = dim3(2 * P); cfg.blockDim = dim3(WK_NT); cfg.dynamicSmemBytes = pl.smem;
     cfg.attrs = at; cfg.numAttrs = 1;
     int nclu = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclu, (const void*)als_w, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
+    if (cudaOccupancyMaxActiveClusters(&nclu, (const void*)als_w<false>, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
     if (nclu < P) a.pair = 0;
   }
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
@@ -911,7 +914,8 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
     e = bgemm_launch(gw, st);
     if (e != cudaSuccess) return cuda_status(e);
   }
-  e = cudaFuncSetAttribute(als_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+  const void* fn = prof ? (const void*)als_w<true> : (const void*)als_w<false>;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
   if (e != cudaSuccess) return cuda_status(e);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[2];
@@ -924,7 +928,7 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
   static const bool noncoop = getenv("TP_ALS_NONCOOP") && getenv("TP_ALS_NONCOOP")[0] == '1';
   if (noncoop) cfg.numAttrs = 1;
   void* args[] = {&a};
-  return cuda_status(cudaLaunchKernelExC(&cfg, (const void*)als_w, args));
+  return cuda_status(cudaLaunchKernelExC(&cfg, fn, args));
 }
 
 }  // namespace tp
