@@ -22,6 +22,8 @@ INCLUDE = PKG.parent / "include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS_OBJ = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
              "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+if os.environ.get("TPDE_PROBES") == "1":   # clock64 phase probes of the fused ALS kernels (tools/als_phases.py ...)
+    FLAGS_OBJ.append("-DTP_ALS_PROBES=1")
 OBJ = PKG.parent / "build"
 
 

@@ -21,6 +21,11 @@
 // in every CTA, so the stopping decision is uniform without host round trips.
 // All cross-CTA reductions use a fixed order: results are bitwise
 // reproducible for a fixed grid size.
+// clock64 phase probes of the fused kernels (debug hook tp_debug_set_als_profile): compiled in only with
+// -DTP_ALS_PROBES=1 (TPDE_PROBES=1 python -m paper_1803_10270_b200.build) -- the product library carries none
+#ifndef TP_ALS_PROBES
+#define TP_ALS_PROBES 0
+#endif
 #include "tp_common.cuh"
 #include "tp_als_rows.cuh"
 #include "tp_als_w.cuh"
@@ -808,7 +813,7 @@ __device__ int gram_inverse_w4(const AlsArgs& a, const Smem& sm, int j, double* 
 // debug phase timers: barrier-synchronised so the attribution is exact
 #define PROF(ph)                                                        \
   do {                                                                  \
-    if (a.prof) {                                                       \
+    if (TP_ALS_PROBES && a.prof) {                                                       \
       __syncthreads();                                                  \
       /* BAR.SYNC defers blocking to the next dependent instruction:  */ \
       /* force it with a shared load before sampling the clock        */ \
@@ -1214,7 +1219,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
   }
   if (status && tid == 0 && p == 0) atomicOr(a.info, 1);
   if (p == 0 && tid == 0) a.info[1] = done;
-  if (a.prof && p == a.prof_cta && tid == 0) {
+  if (TP_ALS_PROBES && a.prof && p == a.prof_cta && tid == 0) {
     for (int q = 0; q < 12; ++q) a.prof[q] += prof_acc[q];
     if (prof_sink == 12345.0) a.prof[11] += 1;
   }
@@ -1365,7 +1370,7 @@ __global__ void __launch_bounds__(NT, 1) als_small(const __grid_constant__ AlsAr
   long long prof_acc[6] = {}, prof_t = clock64();
   double prof_sink = 0.0;
   auto mark = [&](int ph) {   // debug phase timers (a.prof): clock64 after each block barrier
-    if (a.prof) {
+    if (TP_ALS_PROBES && a.prof) {
       prof_sink += *(volatile double*)sm.scal;
       const long long now = clock64();
       prof_acc[ph] += now - prof_t;
@@ -1467,7 +1472,7 @@ __global__ void __launch_bounds__(NT, 1) als_small(const __grid_constant__ AlsAr
   for (int e = tid; e < sumq * r; e += NT) a.U[e] = Us[e];
   if (status && tid == 0) atomicOr(a.info, 1);
   if (tid == 0) a.info[1] = done;
-  if (a.prof && tid == 0) {
+  if (TP_ALS_PROBES && a.prof && tid == 0) {
     for (int q = 0; q < 6; ++q) a.prof[q] += prof_acc[q];
     if (prof_sink == 12345.0) a.prof[11] += 1;
   }
@@ -1576,7 +1581,7 @@ __global__ void __launch_bounds__(TINY_NT, 1) als_tiny8(const __grid_constant__ 
   long long prof_acc[6] = {}, prof_t = clock64();
   double prof_sink = 0.0;
   auto mark = [&](int ph) {   // debug phase timers (a.prof): clock64 after each block barrier
-    if (a.prof) {
+    if (TP_ALS_PROBES && a.prof) {
       prof_sink += *(volatile double*)scal;
       const long long now = clock64();
       prof_acc[ph] += now - prof_t;
@@ -1660,7 +1665,7 @@ __global__ void __launch_bounds__(TINY_NT, 1) als_tiny8(const __grid_constant__ 
         refresh_item(j, ntc);   // G_j
         __syncwarp();
         if (more) status |= warp_sweep_inverse8(a, Gsm, jn, Ai, 8);
-        if (a.prof) prof_acc[4] += clock64() - prof_t;   // warp-0 path (debug)
+        if (TP_ALS_PROBES && a.prof) prof_acc[4] += clock64() - prof_t;   // warp-0 path (debug)
       } else if (worker) {
         for (int it = wk; it < ntc; it += NWK) refresh_item(j, it);   // C_j
         asm volatile("bar.sync 1, %0;" ::"r"(NTK) : "memory");
@@ -1702,7 +1707,7 @@ __global__ void __launch_bounds__(TINY_NT, 1) als_tiny8(const __grid_constant__ 
   }
   if (status && tid == 0) atomicOr(a.info, 1);
   if (tid == 0) a.info[1] = done;
-  if (a.prof && tid == 0) {
+  if (TP_ALS_PROBES && a.prof && tid == 0) {
     for (int q = 0; q < 6; ++q) a.prof[q] += prof_acc[q];
     if (prof_sink == 12345.0) a.prof[11] += 1;
   }
@@ -2196,7 +2201,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_cluster(const __grid_constant__
   }
   if (status && tid == 0 && p == 0) atomicOr(a.info, 1);
   if (p == 0 && tid == 0) a.info[1] = done;
-  if (a.prof && p == a.prof_cta && tid == 0) {
+  if (TP_ALS_PROBES && a.prof && p == a.prof_cta && tid == 0) {
     for (int q = 0; q < 16; ++q) a.prof[q] += prof_acc[q];
     if (prof_sink == 12345.0) a.prof[11] += 1;
   }
