@@ -21,11 +21,6 @@
 // in every CTA, so the stopping decision is uniform without host round trips.
 // All cross-CTA reductions use a fixed order: results are bitwise
 // reproducible for a fixed grid size.
-// clock64 phase probes of the fused kernels (debug hook tp_debug_set_als_profile): compiled in only with
-// -DTP_ALS_PROBES=1 (TPDE_PROBES=1 python -m paper_1803_10270_b200.build) -- the product library carries none
-#ifndef TP_ALS_PROBES
-#define TP_ALS_PROBES 0
-#endif
 #include "tp_common.cuh"
 #include "tp_als_rows.cuh"
 #include "tp_als_w.cuh"
@@ -1017,12 +1012,12 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       // ---------------- phase A
       PROF(0);
       if (pending >= 0) {
-        if (!(a.dbg_skip & 2) && !staged) stage_u(a, sm, pending, bphase);
+        if (!(TP_ALS_PROBES && a.dbg_skip & 2) && !staged) stage_u(a, sm, pending, bphase);
         staged = false;
         PROF(10);
-        if (!(a.dbg_skip & 4)) cross_slab<RM>(a, sm, pending, w);
+        if (!(TP_ALS_PROBES && a.dbg_skip & 4)) cross_slab<RM>(a, sm, pending, w);
         PROF(11);
-        if (!(a.dbg_skip & 8)) gram_share(a, sm, pending, a.local_gram != 0);
+        if (!(TP_ALS_PROBES && a.dbg_skip & 8)) gram_share(a, sm, pending, a.local_gram != 0);
       }
       if (rows_mode >= 0) {   // warm-start rows of the previous NS solve
         ns_rows<RM>(a, sm, rows_mode, rows_sweep);
@@ -1047,7 +1042,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         sm.hadT[c * rh + l] = v;
       }
       __syncthreads();
-      if (!(a.dbg_skip & 16)) {
+      if (!(TP_ALS_PROBES && a.dbg_skip & 16)) {
         // Y_p[s][l] = sum_c V_j[s][c0+c] had[l][c]: M = s, N = l, K = c (DMMA),
         // all RM/8 N tiles of an M tile as independent chains.  Stored
         // consumer-major: row s goes to the CTA pc that owns column s in phase
@@ -1109,7 +1104,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       } else if (bulk) {
         if (tid == 0) {
           const uint32_t gbytes = (pending >= 0 && !a.local_gram) ? (uint32_t)rr * 8u : 0u;
-          const uint32_t ybytes = (E > 0 && !(a.dbg_skip & 32)) ? (uint32_t)(P * nb) * 8u : 0u;
+          const uint32_t ybytes = (E > 0 && !(TP_ALS_PROBES && a.dbg_skip & 32)) ? (uint32_t)(P * nb) * 8u : 0u;
           fence_proxy_async();
           mbar_arrive_expect_tx(sm.bar + 1, gbytes);
           if (gbytes) bulk_g2s(sm.Gs + (size_t)pending * rr, a.G + (size_t)pending * rr, gbytes, sm.bar + 1);
@@ -1124,7 +1119,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
         mbar_wait(sm.bar, bphase);
         bphase ^= 1u;
         PROF(5);
-        for (int o = tid; o < ((a.dbg_skip & 64) ? 0 : E); o += ALS_NT) {
+        for (int o = tid; o < ((TP_ALS_PROBES && a.dbg_skip & 64) ? 0 : E); o += ALS_NT) {
           double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
           int q = 0;
           for (; q + 4 <= P; q += 4) {
@@ -1152,7 +1147,7 @@ __global__ void __launch_bounds__(ALS_NT, 1) als_persistent(const __grid_constan
       }
       __syncthreads();
       PROF(4);
-      if (!(a.dbg_skip & 1) && solve_mode<RM>(a, sm, j, sweep, E, status, ns_fail)) { rows_mode = j; rows_sweep = sweep; }
+      if (!(TP_ALS_PROBES && a.dbg_skip & 1) && solve_mode<RM>(a, sm, j, sweep, E, status, ns_fail)) { rows_mode = j; rows_sweep = sweep; }
       PROF(9);
       if (E > 0) {
         const double* ub = sm.vb + 2 * a.ncolmax * r;

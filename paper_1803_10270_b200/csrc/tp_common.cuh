@@ -9,6 +9,13 @@
 #include <vector>
 #include "../../include/tpde_b200.h"
 
+// clock64 phase probes / phase-skipping timing hooks of the fused kernels (tp_debug_set_als_profile,
+// tp_debug_set_als_skip, tp_debug_set_circ_prof): compiled in only with -DTP_ALS_PROBES=1 (TPDE_PROBES=1 build);
+// the product library carries none (their code alone costs 2-3 % on the latency-bound kernels)
+#ifndef TP_ALS_PROBES
+#define TP_ALS_PROBES 0
+#endif
+
 #define TP_MAXD 8          // max modes of a CP tensor handled by the fused ALS kernels
 #define TP_MAXD_GEN 16     // max modes of the streamed ALS, inner product, apply and contraction kernels
 #define TP_RMAX 32         // max fitted rank in the warp-register Cholesky

@@ -775,7 +775,7 @@ struct CircGsArgs {
 };
 
 #define CG_PROF(i)                                                               \
-  if (a.prof && blockIdx.x == 0 && tid == 0) {                                   \
+  if (TP_ALS_PROBES && a.prof && blockIdx.x == 0 && tid == 0) {                                   \
     const long long now = clock64();                                             \
     a.prof[i] += now - t_prev;                                                   \
     t_prev = now;                                                                \
@@ -868,7 +868,7 @@ __device__ void cg_entries(const CircGsArgs& a, const CgTabs& tb, double* gc, in
   }
   if (qn < 0) return;
   __syncthreads();
-  if (a.prof && blockIdx.x == 0 && tid == 0) {
+  if (TP_ALS_PROBES && a.prof && blockIdx.x == 0 && tid == 0) {
     const long long now = clock64();
     a.prof[9] += now - t_prev;
     t_prev = now;
