@@ -362,8 +362,10 @@ __device__ __forceinline__ void wk_gprod8(const WSmem& sm, int d, int skip, int 
 
 // PROF: clock64 phase probes compiled in (debug hook; the probe code alone shifts the kernel's timing by
 // several per cent through its size, so the product instantiation carries none)
-template <bool PROF>
+// RESID: residual rounds (trace / stopping rules) compiled in.
+template <bool PROF, bool RESID>
 __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs a) {
+  const bool need_resid = RESID;   // (== need_resid: the host picks the instantiation)
   extern __shared__ __align__(16) double smem[];
   const int d = a.d, R = a.R, r = a.r, P = a.P;
   const WSmem sm = wk_carve(smem, d);
@@ -459,7 +461,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
   }
   __syncthreads();
 
-  const double norm_sq = a.need_resid ? fmax(*a.norm_sq, 0.0) : 0.0;
+  const double norm_sq = need_resid ? fmax(*a.norm_sq, 0.0) : 0.0;
   const double t_norm = sqrt(norm_sq);
   double prev = INFINITY;
   int done = 0, abort_ = 0, hb = 0, uround = 0, xpend = -1;   // hb: which hads buffer holds had_j of the current round
@@ -480,13 +482,13 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
       const double* pc = a.pieces + (size_t)slot * P * W_PIECE;
       const int jp = (j + d - 1) % d;
       const bool last_half = sweep == a.sweeps;   // only the residual of the last sweep is still due
-      const bool resid_round = a.need_resid && j == 0 && sweep > 0;
+      const bool resid_round = need_resid && j == 0 && sweep > 0;
       // the previous round's Newton-Schulz update X_xp = X0 Tn_prev is still pending: the reducers
       // apply it as two vector products, warps 0-3 form the matrix while they wait at the join
       const int xp = xpend;
       double* Tcur = sm.Tn + (size_t)(uround & 1) * WK_MAT;
       const double* Tprev = sm.Tn + (size_t)((uround & 1) ^ 1) * WK_MAT;
-      if (last_half && !a.need_resid) { stop = true; break; }
+      if (last_half && !need_resid) { stop = true; break; }
       WK_PROFT(0, PT);
       // ---- A group, part 1: reduce the partial Grams of update jp, G_jp = sym(sum)
       if (warp >= 4 && !first) {
@@ -695,7 +697,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
       // ---- this CTA's piece of the next round: partial Gram C_j[:, own] Y^T, own columns of had_{j+1}
       const int jn = (j + 1) % d;
       const int nsweep = sweep + (jn == 0 ? 1 : 0);
-      const bool publish = a.need_resid || nsweep < a.sweeps;
+      const bool publish = need_resid || nsweep < a.sweeps;
       if (publish) {
         double* pn = a.pieces + ((size_t)((nsweep & 1) * d + jn) * P + c) * W_PIECE;
         const double* yj = sm.Yp + 2 * W_HAD;
@@ -714,7 +716,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
             dmma_8x8x4(m0, m1, sm.Cs[j * W_HAD + (8 * mt + g) * 8 + 4 * ks + t], yj[(8 * nt + g) * 8 + 4 * ks + t]);
           if (h == 0) *reinterpret_cast<double2*>(pn + W_HAD + (8 * mt + g) * W_RM + 8 * nt + 2 * t) = make_double2(m0, m1);
         }
-        if (a.need_resid && j == d - 1) {
+        if (need_resid && j == d - 1) {
           double v = 1.0;
           for (int k = 0; k < d; ++k) v *= sm.Cs[k * W_HAD + tid];
           const double ov = wk_block_sum(v, sm.red);
@@ -729,7 +731,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
         hb ^= 1;
         // (every shared buffer written before the next join is disjoint from what slower warps
         // still read here, except the block-sum scratch of the residual rounds)
-        if (a.need_resid) __syncthreads();
+        if (need_resid) __syncthreads();
       }
       WK_PROFT(7, PT);
       WK_PROFT(11, 0);
@@ -848,7 +850,7 @@ int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
   pl.smem = wk_smem_doubles(d) * sizeof(double);
   if (pl.smem > (size_t)smem_optin) return TP_EUNSUPPORTED;
   if (a.pair) {   // P co-resident 2-CTA clusters?
-    cudaFuncSetAttribute(als_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    cudaFuncSetAttribute(als_w<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     cudaGetLastError();
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
@@ -857,7 +859,7 @@ int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
     cfg.gridDim = dim3(2 * P); cfg.blockDim = dim3(WK_NT); cfg.dynamicSmemBytes = pl.smem;
     cfg.attrs = at; cfg.numAttrs = 1;
     int nclu = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclu, (const void*)als_w<false>, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
+    if (cudaOccupancyMaxActiveClusters(&nclu, (const void*)als_w<false, false>, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
     if (nclu < P) a.pair = 0;
   }
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
@@ -914,7 +916,8 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
     e = bgemm_launch(gw, st);
     if (e != cudaSuccess) return cuda_status(e);
   }
-  const void* fn = prof ? (const void*)als_w<true> : (const void*)als_w<false>;
+  const void* fn = prof ? (a.need_resid ? (const void*)als_w<true, true> : (const void*)als_w<true, false>)
+                        : (a.need_resid ? (const void*)als_w<false, true> : (const void*)als_w<false, false>);
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
   if (e != cudaSuccess) return cuda_status(e);
   cudaLaunchConfig_t cfg = {};
