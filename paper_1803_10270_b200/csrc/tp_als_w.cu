@@ -363,11 +363,12 @@ __device__ __forceinline__ void wk_gprod8(const WSmem& sm, int d, int skip, int 
 // PROF: clock64 phase probes compiled in (debug hook; the probe code alone shifts the kernel's timing by
 // several per cent through its size, so the product instantiation carries none)
 // RESID: residual rounds (trace / stopping rules) compiled in.
-template <bool PROF, bool RESID>
+// DC: compile-time mode count (0: a.d) -- the per-mode product loops unroll.
+template <bool PROF, bool RESID, int DC>
 __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs a) {
-  const bool need_resid = RESID;   // (== need_resid: the host picks the instantiation)
+  const bool need_resid = RESID;   // (== a.need_resid: the host picks the instantiation)
   extern __shared__ __align__(16) double smem[];
-  const int d = a.d, R = a.R, r = a.r, P = a.P;
+  const int d = DC ? DC : a.d, R = a.R, r = a.r, P = a.P;
   const WSmem sm = wk_carve(smem, d);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   // pair mode: the two CTAs of a cluster share a column slab and split the K range of its T product
@@ -815,6 +816,19 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
   }
 }
 
+// product instantiations: the usual mode counts compiled in (config 1: 827 -> 781 us per truncation with
+// d = 6 a constant), any other through the generic one
+template <bool RESID>
+static const void* wk_kernel(int d) {
+  switch (d) {
+    case 3: return (const void*)als_w<false, RESID, 3>;
+    case 4: return (const void*)als_w<false, RESID, 4>;
+    case 5: return (const void*)als_w<false, RESID, 5>;
+    case 6: return (const void*)als_w<false, RESID, 6>;
+    default: return (const void*)als_w<false, RESID, 0>;
+  }
+}
+
 static int g_w_pair = 1;          // debug hook: 0 = one CTA per column slab (no K split over a CTA pair)
 static int g_w_on = 1;            // debug hook: 0 = never plan the Gram-space kernel
 static double g_w_cond = 1e3;     // debug hook: pivot-ratio bound above which the direct kernel reruns
@@ -850,7 +864,7 @@ int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
   pl.smem = wk_smem_doubles(d) * sizeof(double);
   if (pl.smem > (size_t)smem_optin) return TP_EUNSUPPORTED;
   if (a.pair) {   // P co-resident 2-CTA clusters?
-    cudaFuncSetAttribute(als_w<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    cudaFuncSetAttribute(als_w<false, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     cudaGetLastError();
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
@@ -859,7 +873,7 @@ int als_w_plan(int d, const int* q, int R, int r, WPlan& pl) {
     cfg.gridDim = dim3(2 * P); cfg.blockDim = dim3(WK_NT); cfg.dynamicSmemBytes = pl.smem;
     cfg.attrs = at; cfg.numAttrs = 1;
     int nclu = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclu, (const void*)als_w<false, false>, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
+    if (cudaOccupancyMaxActiveClusters(&nclu, (const void*)als_w<false, false, 0>, &cfg) != cudaSuccess) { cudaGetLastError(); nclu = 0; }
     if (nclu < P) a.pair = 0;
   }
   pl.ws_inner = align_up(sizeof(double) * (size_t)inner_tiles(R, R, 1));
@@ -916,8 +930,8 @@ int als_w_run(const WPlan& plan, const double* V, double* U, int sweeps, double 
     e = bgemm_launch(gw, st);
     if (e != cudaSuccess) return cuda_status(e);
   }
-  const void* fn = prof ? (a.need_resid ? (const void*)als_w<true, true> : (const void*)als_w<true, false>)
-                        : (a.need_resid ? (const void*)als_w<false, true> : (const void*)als_w<false, false>);
+  const void* fn = prof ? (a.need_resid ? (const void*)als_w<true, true, 0> : (const void*)als_w<true, false, 0>)
+                        : (a.need_resid ? wk_kernel<true>(d) : wk_kernel<false>(d));
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
   if (e != cudaSuccess) return cuda_status(e);
   cudaLaunchConfig_t cfg = {};
