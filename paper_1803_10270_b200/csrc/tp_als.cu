@@ -1510,10 +1510,12 @@ __host__ __device__ inline size_t tiny_smem_doubles(int d, int r, const TinyDims
          (size_t)t.R8 * 8 + (size_t)TINY_KSMAX * t.qmaxp * TINY_PLD + 64 + ALS_PART + 8;
 }
 
+// DC: compile-time mode count (0: a.d) -- the per-mode loops unroll.
+template <int DC>
 __global__ void __launch_bounds__(TINY_NT, 1) als_tiny8(const __grid_constant__ AlsArgs a) {
   extern __shared__ double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
-  const int d = a.d, r = a.r, R = a.R, rr = r * r;
+  const int d = DC ? DC : a.d, r = a.r, R = a.R, rr = r * r;
   TinyDims td;
   tiny_dims(a.q, d, R, td);
   const int Rs = td.Rs, R8 = td.R8;
@@ -2477,8 +2479,10 @@ static int g_rows_p = 0;    // debug hook: cluster count of the cluster-row kern
 
 static int choose_rm(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : 0)); }
 
-static const void* kernel_ptr(int rm, int variant) {
-  if (variant == 5) return (const void*)als_tiny8;
+static const void* tiny8_ptr(int d) { return d == 6 ? (const void*)als_tiny8<6> : (const void*)als_tiny8<0>; }
+
+static const void* kernel_ptr(int rm, int variant, int d = 0) {
+  if (variant == 5) return tiny8_ptr(d);
   if (variant == 3) variant = 0;   // als_persistent launched as one cluster
   if (variant == 2) {
     switch (rm) {
@@ -2859,7 +2863,7 @@ int tp_cp_als_f64(int d, const int* q, int R, const double* V, int r, double* U,
     st = launch_inner(d, q, R, V, R, V, 1, nsq, part, s);   // ||V||^2 (cp.py:186-188)
     if (st != TP_OK) return st;
   }
-  const void* fn = kernel_ptr(pl.rm, pl.variant);
+  const void* fn = kernel_ptr(pl.rm, pl.variant, d);
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return cuda_status(e);
   if (pl.variant == 1 || pl.variant == 3) {
@@ -2953,10 +2957,10 @@ int tp_cp_als_recipe_f64(int d, const int* q, int r, const double* A, int ra, co
   a.rcp_w0 = dw; a.rcp_moff = dm; a.rcp_mats = mats;
   cudaError_t e = cudaMemsetAsync(info, 0, 2 * sizeof(int), s);
   if (e != cudaSuccess) return cuda_status(e);
-  e = cudaFuncSetAttribute((const void*)als_tiny8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  e = cudaFuncSetAttribute(tiny8_ptr(d), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return cuda_status(e);
   void* args[] = {&a};
-  return cuda_status(cudaLaunchKernel((const void*)als_tiny8, dim3(1), dim3(TINY_NT), args, pl.smem, s));
+  return cuda_status(cudaLaunchKernel(tiny8_ptr(d), dim3(1), dim3(TINY_NT), args, pl.smem, s));
 }
 
 }  // extern "C"
