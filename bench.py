@@ -586,12 +586,13 @@ def run_fused(args, world, rank, local, dev):
         e2e_samples.append(e0.elapsed_time(e1))
     e2e_ms = _max_over_ranks(sorted(e2e_samples)[1], world, dev)
     e2e_val = world * args.steps * SWEEPS / (e2e_ms / 1e3)
-    traffic = None
+    traffic, traffic_src = None, None
     for name in ("r02_als_ncu.json", "r01_als_ncu.json"):
         prof_json = ROOT / "profiles" / name
         if prof_json.exists():
             try:
-                traffic = json.loads(prof_json.read_text()).get("dram_bytes_per_launch")
+                pj = json.loads(prof_json.read_text())
+                traffic, traffic_src = pj.get("dram_bytes_per_launch"), pj.get("source")
                 break
             except Exception:
                 traffic = None
@@ -608,7 +609,7 @@ def run_fused(args, world, rank, local, dev):
                 "samples_sweeps_per_s": [world * args.steps * SWEEPS / (m / 1e3) for m in e2e_samples],
                 "statistic": "median of 3 timed repetitions of the K steps"},
         "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": (f"tp::als_w ({plan['ctas']} CTAs, {plan['smem_bytes']} B smem; a step = one batched bgemm "
                                 "launch (W_k = V_k^T V_k) + als_w + the als_rows fallback "
                                 "launch that returns at once; achieved = reference-algorithm flops / whole step)")
