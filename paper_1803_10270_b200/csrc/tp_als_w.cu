@@ -462,10 +462,12 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
   }
   __syncthreads();
 
+  int uround = 0;
+  WK_PROFT(12, 0);   // setup (crosses / Grams of the guess, first piece)
   const double norm_sq = need_resid ? fmax(*a.norm_sq, 0.0) : 0.0;
   const double t_norm = sqrt(norm_sq);
   double prev = INFINITY;
-  int done = 0, abort_ = 0, hb = 0, uround = 0, xpend = -1;   // hb: which hads buffer holds had_j of the current round
+  int done = 0, abort_ = 0, hb = 0, xpend = -1;   // hb: which hads buffer holds had_j of the current round
   // K range of the GEMM warps (pieces) and this CTA's share of the M entries
   const int kb0 = pr ? h * ((P + 1) / 2) : 0, kb1 = pr ? min(P, kb0 + (P + 1) / 2) : P;   // this CTA's pieces
   const int npw = (kb1 - kb0 + 3) / 4;
@@ -741,6 +743,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
     if (stop) { done = sweep; break; }
   }
 
+  WK_PROFT(13, 0);   // (tail of the last round)
   // ---- after the last sweep: U_j = V_j had_j^T X_j (had_j of the last update of mode j)
   if (!abort_ && done > 0) {
     __syncthreads();
@@ -801,6 +804,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
     }
     if (nf) atomicOr(a.info, 2);
   }
+  WK_PROFT(14, 0);   // final phase
   if (tid == 0) {
     if (*dead) atomicOr(a.info, 4);
     if (cid == 0) {

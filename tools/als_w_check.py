@@ -73,7 +73,8 @@ L.tp_debug_set_als_w_pair(1)
 print(f"plan with pairs: {cp.als_plan([v.shape[0] for v in V], 512, 32)}", flush=True)
 L.tp_debug_set_als_profile.argtypes = [ctypes.c_void_p]
 names = ["top", "reduce M (wait + sum)", "reduced M wait + load", "G step", "A + Newton-Schulz residual", "join wait",
-         "exact inverse", "C / X1 / M / publish", "gemm (wait+load+mma)", "T reduce", "join wait (gemm)", "(gemm) rest of round"]
+         "exact inverse", "C / X1 / M / publish", "gemm (wait+load+mma)", "T reduce", "join wait (gemm)", "(gemm) rest of round",
+         "setup (x120: one-off)", "tail (x120)", "final phase (x120: one-off)"]
 if True:
     prof = torch.zeros(48, dtype=torch.int64, device="cuda")
     L.tp_debug_set_als_profile(prof.data_ptr())
