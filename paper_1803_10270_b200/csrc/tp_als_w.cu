@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
     const double* Uk = a.U + a.offU[k];
     const double* Vk = a.V + a.offV[k] + col0;
     double acc[4][2] = {};
+#pragma unroll 8
     for (int row = r0; row < r1; row += 4) {
       const int rr = row + t;
       const bool rv = rr < r1;
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(WK_NT, 1) als_w(const __grid_constant__ WArgs 
     const int qk = a.q[k], r0 = (qk * warp) / 8, r1 = (qk * (warp + 1)) / 8;
     const double* Uk = a.U + a.offU[k];
     double g0 = 0.0, g1 = 0.0;
+#pragma unroll 8
     for (int row = r0; row < r1; row += 4) {
       const int rr = row + t;
       const bool rv = rr < r1;
