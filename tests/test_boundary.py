@@ -136,3 +136,84 @@ def test_implicit_rejects_complex_galerkin_tables():
     Lc = operators.SeparableOperator(Sc, (1.0,), ((Dc, None, None),))
     with pytest.raises(ValueError, match="complex factor matrices"):
         implicit.build_tables(operators.implicit_euler_pair(Lc, 0.1))
+
+
+@pytest.mark.gpu
+def test_integration_binding_runs():
+    """The reference-side ctypes binding printed in INTEGRATION.md, executed as written against a
+    stand-in `tensorpde.cp` (the reference's dataclasses by field name: cp.py:38-76, 150-164; the
+    reference itself does not travel to the GPU box) and checked against the oracle under the
+    reference's trace-scaled regulariser (cp.py:171-173)."""
+    import dataclasses
+    import re
+    import sys
+    import types
+    from pathlib import Path
+
+    import numpy as np
+
+    from oracle import cp_als as ocp, metrics
+
+    text = (Path(__file__).resolve().parents[1] / "INTEGRATION.md").read_text()
+    code = re.search(r"```python\n(# tensorpde/_b200\.py.*?)```", text, re.S).group(1)
+
+    @dataclasses.dataclass(frozen=True)
+    class Spec:
+        Q: int
+
+    @dataclasses.dataclass
+    class CPTensor:
+        specs: tuple
+        factors: list
+
+        @property
+        def ndim(self):
+            return len(self.factors)
+
+        @property
+        def rank(self):
+            return self.factors[0].shape[1]
+
+    @dataclasses.dataclass(frozen=True)
+    class ALSApproxConfig:
+        max_sweeps: int = 200
+        tol: float = 0.0
+        stall: float = 1e-13
+        seed: int = 0
+        quad_points: int = 0
+
+    class ConditioningError(RuntimeError):
+        pass
+
+    def random_cp(specs, r, rng):
+        return CPTensor(specs, [rng.standard_normal((s.Q, r)).astype(complex) for s in specs])
+
+    ref_cp = types.ModuleType("tensorpde.cp")
+    ref_cp.CPTensor, ref_cp.ALSApproxConfig = CPTensor, ALSApproxConfig
+    ref_cp.ConditioningError, ref_cp.random_cp = ConditioningError, random_cp
+    pkg = types.ModuleType("tensorpde")
+    pkg.cp = ref_cp
+    saved = {k: sys.modules.get(k) for k in ("tensorpde", "tensorpde.cp")}
+    sys.modules["tensorpde"], sys.modules["tensorpde.cp"] = pkg, ref_cp
+    try:
+        ns = {}
+        exec(compile(code, "INTEGRATION.md", "exec"), ns)
+        rng = np.random.default_rng(3)
+        qs, R, r = (14, 11, 12), 9, 3
+        specs = tuple(Spec(q) for q in qs)
+        V = [rng.standard_normal((q, R)) for q in qs]
+        init = [v[:, :r].copy() for v in V]
+        trace = []
+        out = ns["cp_approx_als"](CPTensor(specs, [v.astype(complex) for v in V]), r,
+                                  ALSApproxConfig(max_sweeps=7, stall=-np.inf),
+                                  init=CPTensor(specs, [u.astype(complex) for u in init]), trace=trace)
+        otrace = []
+        ref = ocp.als(V, init, 7, lam=None, trace=otrace)
+        assert metrics.cp_rel_diff(ref, [f.real for f in out.factors]) <= 1e-9
+        np.testing.assert_allclose(trace, otrace, rtol=1e-8, atol=1e-12)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                sys.modules.pop(k, None)
+            else:
+                sys.modules[k] = v
